@@ -1,0 +1,171 @@
+/* fastmusic_b200 — C ABI of the B200-native Fast-MUSIC hot path (arXiv 1911.07434).
+ *
+ * Plain pointers and sizes only. Every entry point replaces a reference C++ function
+ * (R/ = reference proj/ tree); the reference has no FFI of its own, so these are the
+ * symbols a maintainer binds (ctypes / cgo / JNI stubs in INTEGRATION.md) and the
+ * C++ facade (include/fastmusic_b200/fastmusic.hpp) re-exposes them under the
+ * reference names with the reference's exceptions.
+ *
+ * Matrices crossing the single-matrix ("_z", complex128) entry points are column-major
+ * interleaved (re, im) doubles exactly like Eigen::MatrixXcd::data() in the reference.
+ * Batched entry points take DEVICE pointers and a cudaStream_t passed as void*.
+ */
+#ifndef FASTMUSIC_B200_H
+#define FASTMUSIC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; the facade maps them onto the reference exceptions
+ * (R/include/fastmusic/types.hpp:17-43): EINVAL -> std::invalid_argument,
+ * ERANK -> RankDeficiencyError, ENOCONV -> NonConvergenceError,
+ * ESINGULAR -> SingularMatrixError. */
+typedef int32_t fm_status;
+#define FM_OK 0
+#define FM_EINVAL 1
+#define FM_ERANK 2
+#define FM_ENOCONV 3
+#define FM_ESINGULAR 4
+#define FM_ECUDA 5
+#define FM_ENOTSUP 6
+
+/* Per-frame status bits written by the batched kernels. */
+#define FM_FRAME_OK 0
+#define FM_FRAME_RANK 1
+#define FM_FRAME_NOCONV 2
+#define FM_FRAME_RANGE 4
+#define FM_FRAME_NONFINITE 8
+
+/* Method enum values follow R/include/fastmusic/types.hpp:46-54 for the three hot-path methods. */
+#define FM_METHOD_EXACT 0
+#define FM_METHOD_FAST1 1
+#define FM_METHOD_FAST2 2
+
+int32_t fm_abi_version(void);
+const char* fm_status_string(fm_status s);
+/* Message of the last failure on the calling thread (never NULL). */
+const char* fm_last_error(void);
+/* Device name and SM count; FM_ECUDA if no device. */
+fm_status fm_device_info(int32_t device, char* name, int32_t name_len, int32_t* sm_count);
+
+/* ------------------------------------------------------------------ host random streams
+ * Bit-exact restatements of the reference generators (run on the host; the draws are
+ * copied to the device, as the BASELINE contract requires). */
+/* Rng::derive, R/src/linalg.cpp:70-75 */
+uint64_t fm_rng_derive(uint64_t seed, uint64_t tag);
+/* first n outputs of Rng(seed).normal(), R/include/fastmusic/rng.hpp:28-39 */
+fm_status fm_rng_normals(uint64_t seed, int64_t n, double* out);
+/* Rng(seed).sample_without_replacement(m, p), R/src/linalg.cpp:54-68 */
+fm_status fm_sample_without_replacement(uint64_t seed, int64_t m, int64_t p, int64_t* out);
+/* gaussian_matrix_real(m, p, seed) row-major, R/src/linalg.cpp:180-192 */
+fm_status fm_gaussian_matrix_real(int64_t m, int64_t p, uint64_t seed, double* out);
+/* Batched per-frame draws (threaded): omega (frames x m x p float, row-major per frame)
+ * from seeds[f] (fast2), or indices (frames x p int32) from seeds[f] (fast1). */
+fm_status fm_draw_omega_batch(int64_t frames, const uint64_t* seeds, int64_t m, int64_t p, float* omega);
+fm_status fm_draw_indices_batch(int64_t frames, const uint64_t* seeds, int64_t m, int64_t p, int32_t* indices);
+
+/* Synthetic BASELINE frames: frame f of a batch uses seed derive(base_seed, f0 + f).
+ * x: frames x m x n complex64 interleaved row-major. angles (frames x k rad) / snr (frames)
+ * may be NULL. fixed_angles (k rad) may be NULL. Threaded over frames. */
+typedef struct fm_scene_desc {
+    int64_t m, n, k;
+    double theta_lo, theta_hi, min_sep; /* radians */
+    double snr_lo_db, snr_hi_db;
+    const double* fixed_angles; /* k entries or NULL */
+    double d, lambda;
+} fm_scene_desc;
+fm_status fm_generate_frames(const fm_scene_desc* scene, uint64_t base_seed, int64_t f0, int64_t frames, float* x,
+                             double* angles, double* snr_db, int32_t threads);
+
+/* ------------------------------------------------------------------ batched plan (device) */
+typedef struct fm_plan_desc {
+    int64_t m;              /* antennas M */
+    int64_t n;              /* snapshots N (even) */
+    int64_t k;              /* sources K, 1 <= K < M, K <= 64 */
+    int32_t method;         /* FM_METHOD_* */
+    int64_t p;              /* sketch width (fast1/fast2), K <= p <= min(M, 64) */
+    int32_t t;              /* power iterations (fast2), 1..20 */
+    int64_t grid_size;      /* L >= 2 */
+    double theta0, theta1;  /* grid span, theta_l = theta0 + ((theta1-theta0) * l) / (L-1) */
+    double d, lambda;       /* ULA spacing and wavelength */
+    int64_t min_sep_cells;  /* peak separation (R/include/fastmusic/bench.hpp:71 default 3) */
+    int64_t max_frames;     /* workspace capacity */
+} fm_plan_desc;
+typedef struct fm_plan_s* fm_plan;
+
+/* Validates like the reference (R/src/estimators.cpp:74-76,88-92,105-112) and allocates
+ * device workspace + the shared grid table on `device`. */
+fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm_plan* out);
+fm_status fm_plan_destroy(fm_plan plan);
+fm_status fm_plan_workspace_bytes(fm_plan plan, int64_t* bytes);
+
+typedef struct fm_batch_io {
+    const float* x;          /* frames x M x N complex64, row-major (FMCX order) */
+    const float* omega;      /* fast2: frames x M x p, row-major; else NULL */
+    const int32_t* indices;  /* fast1: frames x p sorted column indices; else NULL */
+    float* spectrum;         /* frames x L fp32 pseudo-spectrum, or NULL */
+    int32_t* peak_cells;     /* frames x K grid cells ascending (-1 past count) */
+    double* peak_heights;    /* frames x K */
+    double* baseline;        /* frames */
+    int32_t* peak_count;     /* frames (shortfall <=> count < K) */
+    int32_t* status;         /* frames FM_FRAME_* bits (zeroed by the call) */
+    double* basis;           /* frames x K x M complex128 column-major, or NULL */
+    double* eigenvalues;     /* frames x K, or NULL */
+    float* covariance;       /* frames x M x M complex64 export of R, or NULL */
+} fm_batch_io;
+
+/* Device-resident batched pipeline: covariance -> subspace -> spectrum -> peaks, enqueued
+ * on `stream` (cudaStream_t, may be NULL). Asynchronous; per-frame status in io->status. */
+fm_status fm_run_batch(fm_plan plan, int64_t frames, const fm_batch_io* io, void* stream);
+/* Re-run subspace+spectrum for the listed frames (device int32 list) on the covariance kept
+ * from the last fm_run_batch (fast2 redraws with derive(seed, 0xF257 + attempt)). */
+fm_status fm_rerun_frames(fm_plan plan, int64_t count, const int32_t* d_frames, const fm_batch_io* io, void* stream);
+/* Number of kernel launches one fm_run_batch enqueues. */
+int32_t fm_plan_launches_per_batch(fm_plan plan);
+
+/* End-to-end, host buffers (the reference-facing call): H2D of x and of the per-frame draws
+ * (generated here from draw_seeds[f], exactly as the reference draws them), pipeline, fast2
+ * redraws (<= 4 attempts, R/src/estimators.cpp:114-137), D2H of peaks/spectrum/status.
+ * Host outputs may be NULL except peak_cells/peak_count/status. Synchronous. */
+typedef struct fm_host_out {
+    float* spectrum;         /* frames x L or NULL */
+    int32_t* peak_cells;     /* frames x K */
+    double* peak_heights;    /* frames x K or NULL */
+    double* baseline;        /* frames or NULL */
+    int32_t* peak_count;     /* frames */
+    int32_t* status;         /* frames */
+    int32_t* attempts;       /* frames (fast2 draws used) or NULL */
+} fm_host_out;
+fm_status fm_estimate_batch_host(fm_plan plan, int64_t frames, const float* h_x, const uint64_t* draw_seeds,
+                                 fm_host_out* out, void* stream);
+
+/* ------------------------------------------------------------------ reference single-matrix API
+ * complex128, column-major; computed on the GPU in fp64 (facade path of
+ * include/fastmusic_b200/fastmusic.hpp). cost_seconds = CUDA-event time of the subspace
+ * kernels (R/src/estimators.cpp:19-23 semantics). */
+/* spatial_covariance, R/src/scene.cpp:157-159 (+ HermitianMatrix symmetrisation) */
+fm_status fm_z_spatial_covariance(int64_t m, int64_t n, const double* y, double* s_out);
+/* exact_signal_subspace, R/src/estimators.cpp:73-85 */
+fm_status fm_z_exact_signal_subspace(int64_t m, const double* s, int64_t k, double* basis, double* eigenvalues,
+                                     double* cost_seconds);
+/* fast_music_1, R/src/estimators.cpp:87-102 */
+fm_status fm_z_fast_music_1(int64_t m, const double* s, int64_t k, int64_t p, uint64_t seed, double* basis,
+                            double* eigenvalues, double* cost_seconds);
+/* fast_music_2, R/src/estimators.cpp:104-139; *deficient_column set on FM_ERANK */
+fm_status fm_z_fast_music_2(int64_t m, const double* s, int64_t k, int64_t p, int32_t t, uint64_t seed,
+                            double* basis, double* eigenvalues, double* cost_seconds, int64_t* deficient_column);
+/* music_spectrum, R/src/spectrum.cpp:50-68 on theta_l = theta0 + ((theta1-theta0)*l)/(L-1) */
+fm_status fm_z_music_spectrum(int64_t m, int64_t kb, const double* basis, int64_t grid_size, double theta0,
+                              double theta1, double d, double lambda, double* values);
+/* extract_peaks, R/src/spectrum.cpp:182-188; cells ascending */
+fm_status fm_z_extract_peaks(const double* values, int64_t grid_size, int64_t k, int64_t min_sep, int64_t* cells,
+                             double* heights, int64_t* count, double* baseline, int32_t* shortfall);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASTMUSIC_B200_H */

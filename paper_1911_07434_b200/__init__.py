@@ -1,0 +1,14 @@
+"""fastmusic_b200 — B200-native (sm_100a) Fast-MUSIC hot path (arXiv 1911.07434).
+
+The compute lives in ``libfastmusic_b200.so`` (hand-written CUDA kernels behind the
+C ABI in ``include/fastmusic_b200.h``); this package is the Python mirror of the
+reference estimator API over that ABI. Importing fails loudly if the library is absent.
+"""
+from .api import (AngleGrid, BatchPlan, CudaError, Fast1Params, Fast2Params, NonConvergenceError, PeakSet,  # noqa: F401
+                  PseudoSpectrum, RankDeficiencyError, SingularMatrixError, SubspaceEstimate, baseline_grid, derive,
+                  draw_indices_batch, draw_omega_batch, exact_signal_subspace, extract_peaks, fast_music_1,
+                  fast_music_2, gaussian_matrix_real, generate_frames, hermitian, music_spectrum, normals,
+                  sample_without_replacement, spatial_covariance, steering_vector)
+from ._capi import LIB_PATH  # noqa: F401
+
+__all__ = [n for n in dir() if not n.startswith("_")]

@@ -1,0 +1,373 @@
+"""Python mirror of the reference estimator API, executed on the B200 through the C ABI.
+
+Names, argument meaning and error behaviour follow R/include/fastmusic/{estimators,
+spectrum,scene,types}.hpp so the parity tests read like the reference's own tests:
+``fast_music_2(S, K, Fast2Params(p, t, seed))`` -> ``SubspaceEstimate``; parameter
+violations raise ``ValueError`` (std::invalid_argument), rank-deficient sketches raise
+``RankDeficiencyError`` after the reference's redraw policy, solver failures raise
+``NonConvergenceError``.  ``BatchPlan`` drives the batched complex64 pipeline on
+device tensors (torch is used only for device memory and streams).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._capi import LIB, ptr
+
+KPI = 3.14159265358979323846
+
+
+class NonConvergenceError(RuntimeError):
+    def __init__(self, what, residual=float("nan")):
+        super().__init__(what)
+        self.residual = residual
+
+
+class RankDeficiencyError(RuntimeError):
+    def __init__(self, what, column=-1):
+        super().__init__(what)
+        self.column = column
+
+
+class SingularMatrixError(RuntimeError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _check(st: int, column: int = -1):
+    if st == _capi.FM_OK:
+        return
+    msg = _capi.last_error()
+    if st == _capi.FM_EINVAL:
+        raise ValueError(msg)
+    if st == _capi.FM_ERANK:
+        raise RankDeficiencyError(msg, column)
+    if st == _capi.FM_ENOCONV:
+        raise NonConvergenceError(msg)
+    if st == _capi.FM_ESINGULAR:
+        raise SingularMatrixError(msg)
+    if st == _capi.FM_ENOTSUP:
+        raise NotImplementedError(msg)
+    raise CudaError(msg)
+
+
+# ------------------------------------------------------------------ types
+@dataclass
+class Fast1Params:
+    """R/include/fastmusic/estimators.hpp:20-23."""
+    p: int = 0
+    seed: int = 0
+
+
+@dataclass
+class Fast2Params:
+    """R/include/fastmusic/estimators.hpp:25-29."""
+    p: int = 0
+    iterations: int = 1
+    seed: int = 0
+
+
+@dataclass
+class SubspaceEstimate:
+    """R/include/fastmusic/estimators.hpp:13-18."""
+    basis: np.ndarray
+    eigenvalues: np.ndarray
+    method: str = "exact"
+    cost_seconds: float = 0.0
+
+
+@dataclass(frozen=True)
+class AngleGrid:
+    """R/include/fastmusic/spectrum.hpp:12-25, generalised to [theta0, theta1]."""
+    size: int
+    theta0: float = 0.0
+    theta1: float = KPI
+
+    def __post_init__(self):
+        if self.size < 2:
+            raise ValueError("AngleGrid: L >= 2 required")
+
+    def spacing(self) -> float:
+        return (self.theta1 - self.theta0) / float(self.size - 1)
+
+    def theta(self, i) -> float:
+        return self.theta0 + ((self.theta1 - self.theta0) * float(i)) / float(self.size - 1)
+
+    def thetas(self) -> np.ndarray:
+        return self.theta0 + ((self.theta1 - self.theta0) * np.arange(self.size, dtype=np.float64)) / float(self.size - 1)
+
+    def nearest(self, theta: float) -> int:
+        i = int(np.rint((theta - self.theta0) / self.spacing()))
+        return min(max(i, 0), self.size - 1)
+
+
+def baseline_grid(l: int) -> AngleGrid:
+    return AngleGrid(l, -KPI / 2.0, KPI / 2.0)
+
+
+@dataclass
+class PseudoSpectrum:
+    grid: AngleGrid
+    values: np.ndarray
+    method: str = "exact"
+    degenerate: bool = False
+
+
+@dataclass
+class PeakSet:
+    angles: list
+    heights: list
+    baseline: float = 0.0
+    shortfall: bool = False
+    cells: list = field(default_factory=list)
+
+
+# ------------------------------------------------------------------ helpers
+def _cmat(a) -> np.ndarray:
+    """complex128, column-major (Eigen::MatrixXcd storage)."""
+    return np.asfortranarray(np.asarray(a, dtype=np.complex128))
+
+
+def hermitian(a) -> np.ndarray:
+    """HermitianMatrix ctor (R/src/linalg.cpp:46-52): square, finite, 0.5 (A + A^H)."""
+    a = np.asarray(a, dtype=np.complex128)
+    if a.ndim != 2 or a.shape[0] != a.shape[1] or a.shape[0] < 1:
+        raise ValueError("HermitianMatrix: input must be square and non-empty")
+    if not np.all(np.isfinite(a)):
+        raise ValueError("HermitianMatrix: non-finite entries")
+    return _cmat(0.5 * (a + a.conj().T))
+
+
+# ------------------------------------------------------------------ RNG (host, bit-exact)
+def derive(seed: int, tag: int) -> int:
+    return int(LIB.fm_rng_derive(seed & (2**64 - 1), tag & (2**64 - 1)))
+
+
+def normals(seed: int, n: int) -> np.ndarray:
+    out = np.empty(n, np.float64)
+    _check(LIB.fm_rng_normals(seed, n, ptr(out)))
+    return out
+
+
+def sample_without_replacement(seed: int, m: int, p: int) -> np.ndarray:
+    out = np.empty(max(p, 1), np.int64)
+    _check(LIB.fm_sample_without_replacement(seed, m, p, ptr(out)))
+    return out[:p]
+
+
+def gaussian_matrix_real(m: int, p: int, seed: int) -> np.ndarray:
+    out = np.empty((m, p), np.float64)
+    _check(LIB.fm_gaussian_matrix_real(m, p, seed, ptr(out)))
+    return out
+
+
+def draw_omega_batch(seeds, m: int, p: int) -> np.ndarray:
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    out = np.empty((seeds.size, m, p), np.float32)
+    _check(LIB.fm_draw_omega_batch(seeds.size, ptr(seeds), m, p, ptr(out)))
+    return out
+
+
+def draw_indices_batch(seeds, m: int, p: int) -> np.ndarray:
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    out = np.empty((seeds.size, p), np.int32)
+    _check(LIB.fm_draw_indices_batch(seeds.size, ptr(seeds), m, p, ptr(out)))
+    return out
+
+
+def generate_frames(m, n, k, base_seed, f0, frames, theta_lo_deg=-60.0, theta_hi_deg=60.0, min_sep_deg=3.0,
+                    snr_lo_db=10.0, snr_hi_db=30.0, fixed_angles_deg=None, d=0.5, lam=1.0, threads=0, out=None):
+    """Synthetic BASELINE frames; returns (x complex64 [frames, m, n], angles, snr)."""
+    x = out if out is not None else np.empty((frames, m, n), np.complex64)
+    ang = np.empty((frames, k), np.float64)
+    snr = np.empty(frames, np.float64)
+    fixed = None
+    if fixed_angles_deg is not None:
+        fixed = np.array([a * KPI / 180.0 for a in fixed_angles_deg], np.float64)
+    sd = _capi.SceneDesc(m, n, k, theta_lo_deg * KPI / 180.0, theta_hi_deg * KPI / 180.0,
+                         min_sep_deg * KPI / 180.0, snr_lo_db, snr_hi_db, ptr(fixed), d, lam)
+    _check(LIB.fm_generate_frames(C.byref(sd), base_seed, f0, frames, ptr(x), ptr(ang), ptr(snr), threads))
+    return x, ang, snr
+
+
+# ------------------------------------------------------------------ reference single-matrix API
+def steering_vector(theta: float, m: int, d: float, lam: float) -> np.ndarray:
+    """R/src/scene.cpp:72-82."""
+    if m < 1 or d <= 0 or lam <= 0:
+        raise ValueError("steering_vector: need M >= 1, d > 0, lambda > 0")
+    step = 2.0 * KPI * d * np.sin(theta) / lam
+    ph = step * np.arange(m, dtype=np.float64)
+    return np.cos(ph) + 1j * np.sin(ph)
+
+
+def spatial_covariance(y) -> np.ndarray:
+    """R/src/scene.cpp:157-159 — on the GPU in fp64."""
+    y = _cmat(y)
+    if y.ndim != 2 or y.shape[0] < 1 or y.shape[1] < 1:
+        raise ValueError("covariance: empty signal matrix")
+    s = np.empty((y.shape[0], y.shape[0]), np.complex128, order="F")
+    _check(LIB.fm_z_spatial_covariance(y.shape[0], y.shape[1], ptr(y), ptr(s)))
+    return s
+
+
+def _est_out(m, k):
+    return np.empty((m, k), np.complex128, order="F"), np.empty(k, np.float64), C.c_double(0.0)
+
+
+def exact_signal_subspace(s, k: int) -> SubspaceEstimate:
+    """R/src/estimators.cpp:73-85 — batched one-sided Jacobi on the GPU (fp64 here)."""
+    s = hermitian(s)
+    m = s.shape[0]
+    if k < 1 or k >= m:
+        raise ValueError("exact_signal_subspace: need 1 <= K < M")
+    b, e, cost = _est_out(m, k)
+    _check(LIB.fm_z_exact_signal_subspace(m, ptr(s), k, ptr(b), ptr(e), C.byref(cost)))
+    return SubspaceEstimate(b, e, "exact", cost.value)
+
+
+def fast_music_1(s, k: int, params: Fast1Params) -> SubspaceEstimate:
+    """R/src/estimators.cpp:87-102."""
+    s = hermitian(s)
+    m = s.shape[0]
+    if k < 1 or k >= m:
+        raise ValueError("fast_music_1: need 1 <= K < M")
+    if params.p < k or params.p > m:
+        raise ValueError("fast_music_1: need K <= p <= M")
+    b, e, cost = _est_out(m, k)
+    _check(LIB.fm_z_fast_music_1(m, ptr(s), k, params.p, params.seed & (2**64 - 1), ptr(b), ptr(e), C.byref(cost)))
+    return SubspaceEstimate(b, e, "fast1", cost.value)
+
+
+def fast_music_2(s, k: int, params: Fast2Params) -> SubspaceEstimate:
+    """R/src/estimators.cpp:104-139 (redraws with derive(seed, 0xF257 + attempt))."""
+    s = hermitian(s)
+    m = s.shape[0]
+    if k < 1 or k >= m:
+        raise ValueError("fast_music_2: need 1 <= K < M")
+    if params.p < k or params.p > m:
+        raise ValueError("fast_music_2: need K <= p <= M")
+    if params.iterations < 1 or params.iterations > 20:
+        raise ValueError("fast_music_2: need 1 <= t <= 20")
+    b, e, cost = _est_out(m, k)
+    col = C.c_int64(-1)
+    st = LIB.fm_z_fast_music_2(m, ptr(s), k, params.p, params.iterations, params.seed & (2**64 - 1), ptr(b), ptr(e),
+                               C.byref(cost), C.byref(col))
+    _check(st, col.value)
+    return SubspaceEstimate(b, e, "fast2", cost.value)
+
+
+def music_spectrum(estimate: SubspaceEstimate, grid: AngleGrid, d: float, lam: float) -> PseudoSpectrum:
+    """R/src/spectrum.cpp:50-68."""
+    u = _cmat(estimate.basis)
+    if u.ndim != 2 or u.shape[0] < 1:
+        raise ValueError("music_spectrum: empty basis")
+    vals = np.empty(grid.size, np.float64)
+    _check(LIB.fm_z_music_spectrum(u.shape[0], u.shape[1], ptr(u) if u.size else None, grid.size, grid.theta0,
+                                   grid.theta1, d, lam, ptr(vals)))
+    return PseudoSpectrum(grid, vals, estimate.method)
+
+
+def extract_peaks(p: PseudoSpectrum, k: int, min_separation_cells: int) -> PeakSet:
+    """R/src/spectrum.cpp:182-188."""
+    if k < 1:
+        raise ValueError("extract_peaks: K >= 1 required")
+    v = np.ascontiguousarray(p.values, np.float64)
+    cells = np.empty(k, np.int64)
+    heights = np.empty(k, np.float64)
+    count, base, short = C.c_int64(0), C.c_double(0.0), C.c_int32(0)
+    _check(LIB.fm_z_extract_peaks(ptr(v), v.size, k, min_separation_cells, ptr(cells), ptr(heights), C.byref(count),
+                                  C.byref(base), C.byref(short)))
+    n = count.value
+    cl = [int(c) for c in cells[:n]]
+    return PeakSet([p.grid.theta(c) for c in cl], [float(h) for h in heights[:n]], base.value, bool(short.value), cl)
+
+
+# ------------------------------------------------------------------ batched plan
+class BatchPlan:
+    """fm_plan over device tensors (torch for allocation / streams only)."""
+
+    def __init__(self, m, n, k, method="fast2", p=0, t=1, grid_size=3601, theta0=-KPI / 2, theta1=KPI / 2, d=0.5,
+                 lam=1.0, min_sep_cells=3, max_frames=1, device=0):
+        self.desc = _capi.PlanDesc(m, n, k, _capi.METHOD[method], p, t, grid_size, theta0, theta1, d, lam,
+                                   min_sep_cells, max_frames)
+        self.method, self.m, self.n, self.k, self.p, self.t, self.L = method, m, n, k, p, t, grid_size
+        self.max_frames, self.device = max_frames, device
+        h = C.c_void_p()
+        _check(LIB.fm_plan_create(C.byref(self.desc), device, C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            LIB.fm_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.close()
+
+    def workspace_bytes(self) -> int:
+        b = C.c_int64(0)
+        _check(LIB.fm_plan_workspace_bytes(self.handle, C.byref(b)))
+        return b.value
+
+    def launches_per_batch(self) -> int:
+        return int(LIB.fm_plan_launches_per_batch(self.handle))
+
+    def outputs(self, frames, spectrum=True, basis=False, covariance=False):
+        import torch
+        dev = torch.device("cuda", self.device)
+        o = {
+            "peak_cells": torch.empty((frames, self.k), dtype=torch.int32, device=dev),
+            "peak_heights": torch.empty((frames, self.k), dtype=torch.float64, device=dev),
+            "baseline": torch.empty((frames,), dtype=torch.float64, device=dev),
+            "peak_count": torch.empty((frames,), dtype=torch.int32, device=dev),
+            "status": torch.empty((frames,), dtype=torch.int32, device=dev),
+        }
+        if spectrum:
+            o["spectrum"] = torch.empty((frames, self.L), dtype=torch.float32, device=dev)
+        if basis:
+            o["basis"] = torch.empty((frames, self.k, self.m, 2), dtype=torch.float64, device=dev)
+            o["eigenvalues"] = torch.empty((frames, self.k), dtype=torch.float64, device=dev)
+        if covariance:
+            o["covariance"] = torch.empty((frames, self.m, self.m, 2), dtype=torch.float32, device=dev)
+        return o
+
+    def _io(self, x, omega, indices, out):
+        return _capi.BatchIO(ptr(x), ptr(omega), ptr(indices), ptr(out.get("spectrum")), ptr(out["peak_cells"]),
+                             ptr(out["peak_heights"]), ptr(out["baseline"]), ptr(out["peak_count"]),
+                             ptr(out["status"]), ptr(out.get("basis")), ptr(out.get("eigenvalues")),
+                             ptr(out.get("covariance")))
+
+    def run(self, frames, x, omega=None, indices=None, out=None, stream=None):
+        """x: device float32 view of complex64 [frames, M, N]; omega float32 [frames, M, p]; indices int32."""
+        io = self._io(x, omega, indices, out)
+        s = None if stream is None else C.c_void_p(stream.cuda_stream)
+        _check(LIB.fm_run_batch(self.handle, frames, C.byref(io), s))
+        return out
+
+    def rerun(self, frames, x, omega=None, indices=None, out=None, stream=None):
+        io = self._io(x, omega, indices, out)
+        s = None if stream is None else C.c_void_p(stream.cuda_stream)
+        _check(LIB.fm_rerun_frames(self.handle, frames, None, C.byref(io), s))
+        return out
+
+    def estimate_host(self, x_host, draw_seeds, spectrum=None, heights=None, baseline=None, stream=None):
+        """End-to-end from host buffers (pinned recommended): returns dict of host arrays."""
+        frames = x_host.shape[0]
+        cells = np.empty((frames, self.k), np.int32)
+        count = np.empty(frames, np.int32)
+        status = np.empty(frames, np.int32)
+        attempts = np.empty(frames, np.int32)
+        seeds = None if draw_seeds is None else np.ascontiguousarray(draw_seeds, np.uint64)
+        ho = _capi.HostOut(ptr(spectrum), ptr(cells), ptr(heights), ptr(baseline), ptr(count), ptr(status),
+                           ptr(attempts))
+        s = None if stream is None else C.c_void_p(stream.cuda_stream)
+        _check(LIB.fm_estimate_batch_host(self.handle, frames, ptr(x_host), ptr(seeds), C.byref(ho), s))
+        return {"peak_cells": cells, "peak_count": count, "status": status, "attempts": attempts,
+                "spectrum": spectrum, "peak_heights": heights, "baseline": baseline}

@@ -1,0 +1,861 @@
+// C ABI of the B200 Fast-MUSIC path (include/fastmusic_b200.h): plans, the batched
+// device pipeline, the host-buffer end-to-end entry, the fp64 single-matrix entry points
+// behind the reference-named C++ facade, host random draws and the synthetic frame
+// generator. No CPU compute fallback: every numeric stage below launches a kernel.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/fastmusic_b200.h"
+#include "fm_common.cuh"
+#include "host_rng.hpp"
+
+// ------------------------------------------------------------------ kernel launchers (other TUs)
+cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, int64_t frames, int64_t m, int64_t n,
+                             cudaStream_t stream);
+template <typename T>
+cudaError_t fm_launch_rmul(const void*, const void*, const void*, void*, const int32_t*, int, int, int, bool,
+                           cudaStream_t);
+template <typename T>
+cudaError_t fm_launch_gather(const void*, const int32_t*, void*, void*, const int32_t*, int, int, int, cudaStream_t);
+template <typename T>
+cudaError_t fm_launch_qr(const void*, void*, void*, void*, int32_t*, int32_t*, const int32_t*, int, int, int, bool,
+                         cudaStream_t);
+template <typename T>
+cudaError_t fm_launch_nystrom(const void*, const void*, const void*, const void*, const void*, void*, double*,
+                              int32_t*, const int32_t*, int, int, int, int, bool, cudaStream_t);
+cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, int k, cudaStream_t s);
+cudaError_t fm_launch_spectrum_peaks(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
+                                     double* spec64, int K, int min_sep, int32_t* cells, double* heights,
+                                     double* baseline, int32_t* count, int32_t* status, cudaStream_t s);
+cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K, int min_sep, int32_t* cells,
+                                 double* heights, double* baseline, int32_t* count, int32_t* overflow,
+                                 cudaStream_t s);
+cudaError_t fm_launch_orthocheck(const void* basis, int frames, int m, int k, double* dev, cudaStream_t s);
+template <typename T>
+cudaError_t fm_launch_jacobi_eig(const void* R, void* work, void* basis, double* eig, int32_t* status, int frames,
+                                 int m, int k, cudaStream_t s);
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+thread_local std::string g_err = "";
+
+fm_status fail(fm_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+}  // namespace
+
+fm_status fm_fail_cuda(cudaError_t e, const char* expr, const char* file, int line) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e), cudaGetErrorString(e),
+                  file, line, expr);
+    g_err = buf;
+    return e == cudaErrorInvalidValue ? FM_EINVAL : FM_ECUDA;
+}
+
+// ------------------------------------------------------------------ small kernels local to the ABI layer
+namespace {
+
+__global__ void k_clear_bits(int32_t* status, int frames, int32_t bits) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f < frames) status[f] &= ~bits;
+}
+
+// fp64 covariance for the single-matrix facade path (R/src/scene.cpp:138-159 +
+// R/src/linalg.cpp:46-52): y column-major M x N; output S column-major, exactly Hermitian.
+__global__ void k_cov_z(const fmk::c64* __restrict__ y, fmk::c64* __restrict__ s, int m, int n) {
+    const int i = blockIdx.y * blockDim.y + threadIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m || j >= m || j > i) return;
+    fmk::c64 acc = fmk::mk(0.0, 0.0);
+    for (int q = 0; q < n; ++q) {
+        const fmk::c64 a = y[static_cast<size_t>(q) * m + i], b = y[static_cast<size_t>(q) * m + j];
+        acc.re += a.re * b.re + a.im * b.im;
+        acc.im += a.im * b.re - a.re * b.im;
+    }
+    const double inv = 1.0 / static_cast<double>(n);
+    acc.re *= inv;
+    acc.im *= inv;
+    if (i == j) acc.im = 0.0;
+    s[static_cast<size_t>(j) * m + i] = acc;              // S(i, j)
+    s[static_cast<size_t>(i) * m + j] = fmk::conj(acc);   // S(j, i)
+}
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaError_t alloc(size_t count) {
+        n = count;
+        return count ? cudaMalloc(&p, sizeof(T) * count) : cudaSuccess;
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+std::vector<double> zgrid_host(int64_t L, double theta0, double theta1, double d, double lambda) {
+    // theta_l = theta0 + (span * l) / (L - 1)  (R/src/spectrum.cpp:26-28 for theta0 = 0, span = pi);
+    // step = 2 pi d sin(theta) / lambda exactly as R/src/scene.cpp:76.
+    std::vector<double> z(static_cast<size_t>(2 * L));
+    const double span = theta1 - theta0;
+    for (int64_t l = 0; l < L; ++l) {
+        const double th = theta0 + (span * static_cast<double>(l)) / static_cast<double>(L - 1);
+        const double step = 2.0 * kPi * d * std::sin(th) / lambda;
+        z[2 * l] = std::cos(step);
+        z[2 * l + 1] = std::sin(step);
+    }
+    return z;
+}
+
+int hw_threads(int32_t req) {
+    if (req > 0) return req;
+    const unsigned h = std::thread::hardware_concurrency();
+    return h ? static_cast<int>(h) : 1;
+}
+
+template <typename F>
+void parallel_for(int64_t count, int threads, F&& fn) {
+    threads = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(threads, count)));
+    if (threads <= 1) {
+        for (int64_t i = 0; i < count; ++i) fn(i);
+        return;
+    }
+    std::atomic<int64_t> next{0};
+    std::vector<std::thread> pool;
+    for (int w = 0; w < threads; ++w)
+        pool.emplace_back([&] {
+            for (;;) {
+                const int64_t i = next.fetch_add(1);
+                if (i >= count) return;
+                fn(i);
+            }
+        });
+    for (auto& th : pool) th.join();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ misc
+extern "C" int32_t fm_abi_version(void) { return 1; }
+
+extern "C" const char* fm_status_string(fm_status s) {
+    switch (s) {
+        case FM_OK: return "ok";
+        case FM_EINVAL: return "invalid argument";
+        case FM_ERANK: return "rank deficiency";
+        case FM_ENOCONV: return "no convergence";
+        case FM_ESINGULAR: return "singular matrix";
+        case FM_ECUDA: return "cuda error";
+        case FM_ENOTSUP: return "not supported";
+    }
+    return "unknown";
+}
+
+extern "C" const char* fm_last_error(void) { return g_err.c_str(); }
+
+extern "C" fm_status fm_device_info(int32_t device, char* name, int32_t name_len, int32_t* sm_count) {
+    cudaDeviceProp prop;
+    FM_CUDA_OK(cudaGetDeviceProperties(&prop, device));
+    if (name && name_len > 0) {
+        std::strncpy(name, prop.name, static_cast<size_t>(name_len - 1));
+        name[name_len - 1] = '\0';
+    }
+    if (sm_count) *sm_count = prop.multiProcessorCount;
+    return FM_OK;
+}
+
+// ------------------------------------------------------------------ host random streams
+extern "C" uint64_t fm_rng_derive(uint64_t seed, uint64_t tag) { return fmhost::Rng::derive(seed, tag); }
+
+extern "C" fm_status fm_rng_normals(uint64_t seed, int64_t n, double* out) {
+    if (n < 0 || (n > 0 && !out)) return fail(FM_EINVAL, "fm_rng_normals: bad arguments");
+    fmhost::Rng r(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = r.normal();
+    return FM_OK;
+}
+
+extern "C" fm_status fm_sample_without_replacement(uint64_t seed, int64_t m, int64_t p, int64_t* out) {
+    if (p < 1 || p > m) return fail(FM_EINVAL, "sample_without_replacement: need 1 <= p <= m");
+    fmhost::Rng r(seed);
+    const auto v = r.sample_without_replacement(m, p);
+    std::copy(v.begin(), v.end(), out);
+    return FM_OK;
+}
+
+extern "C" fm_status fm_gaussian_matrix_real(int64_t m, int64_t p, uint64_t seed, double* out) {
+    if (m < 1 || p < 1) return fail(FM_EINVAL, "gaussian_matrix: need M, p >= 1");
+    fmhost::gaussian_matrix_real(m, p, seed, out);
+    return FM_OK;
+}
+
+extern "C" fm_status fm_draw_omega_batch(int64_t frames, const uint64_t* seeds, int64_t m, int64_t p, float* omega) {
+    if (frames < 0 || m < 1 || p < 1) return fail(FM_EINVAL, "fm_draw_omega_batch: bad arguments");
+    parallel_for(frames, hw_threads(0), [&](int64_t f) {
+        fmhost::gaussian_matrix_real(m, p, seeds[f], omega + static_cast<size_t>(f) * m * p);
+    });
+    return FM_OK;
+}
+
+extern "C" fm_status fm_draw_indices_batch(int64_t frames, const uint64_t* seeds, int64_t m, int64_t p,
+                                           int32_t* indices) {
+    if (frames < 0 || p < 1 || p > m) return fail(FM_EINVAL, "fm_draw_indices_batch: need 1 <= p <= m");
+    parallel_for(frames, hw_threads(0), [&](int64_t f) {
+        fmhost::Rng r(seeds[f]);
+        const auto v = r.sample_without_replacement(m, p);
+        for (int64_t i = 0; i < p; ++i) indices[static_cast<size_t>(f) * p + i] = static_cast<int32_t>(v[i]);
+    });
+    return FM_OK;
+}
+
+// ------------------------------------------------------------------ synthetic frames
+// Model: angles/SNR from Rng(derive(s_f,1)); sources then noise from
+// Rng(derive(s_f,2)); X = sum_k a_k s_k^T + noise in fp64, rounded to complex64.
+extern "C" fm_status fm_generate_frames(const fm_scene_desc* sc, uint64_t base_seed, int64_t f0, int64_t frames,
+                                        float* x, double* angles, double* snr_db, int32_t threads) {
+    if (!sc || !x || sc->m < 1 || sc->n < 1 || sc->k < 1 || frames < 0)
+        return fail(FM_EINVAL, "fm_generate_frames: bad arguments");
+    const int64_t m = sc->m, n = sc->n, k = sc->k;
+    std::atomic<int> bad{0};
+    parallel_for(frames, hw_threads(threads), [&](int64_t fi) {
+        const uint64_t s_f = fmhost::Rng::derive(base_seed, static_cast<uint64_t>(f0 + fi));
+        std::vector<double> ang;
+        fmhost::Rng ra(fmhost::Rng::derive(s_f, 1));
+        if (sc->fixed_angles) {
+            ang.assign(sc->fixed_angles, sc->fixed_angles + k);
+        } else {
+            int attempts = 0;
+            while (static_cast<int64_t>(ang.size()) < k) {
+                if (++attempts > 100000) {
+                    bad = 1;
+                    return;
+                }
+                const double th = sc->theta_lo + ra.uniform01() * (sc->theta_hi - sc->theta_lo);
+                bool ok = true;
+                for (double a : ang)
+                    if (std::abs(th - a) < sc->min_sep) {
+                        ok = false;
+                        break;
+                    }
+                if (ok) ang.push_back(th);
+            }
+        }
+        std::sort(ang.begin(), ang.end());
+        const double snr = sc->snr_lo_db + (sc->snr_hi_db - sc->snr_lo_db) * ra.uniform01();
+        const double sigma2 = static_cast<double>(k) / std::pow(10.0, snr / 10.0);
+        fmhost::Rng rn(fmhost::Rng::derive(s_f, 2));
+        const double inv_sqrt2 = 1.0 / std::sqrt(2.0);
+        std::vector<double> src(static_cast<size_t>(2 * k * n));
+        for (int64_t i = 0; i < k * n; ++i) {
+            const double re = rn.normal();
+            const double im = rn.normal();
+            src[2 * i] = re * inv_sqrt2;
+            src[2 * i + 1] = im * inv_sqrt2;
+        }
+        std::vector<double> st(static_cast<size_t>(2 * k * m));
+        for (int64_t q = 0; q < k; ++q) {
+            const double step = 2.0 * kPi * sc->d * std::sin(ang[q]) / sc->lambda;
+            for (int64_t i = 0; i < m; ++i) {
+                const double ph = step * static_cast<double>(i);
+                st[2 * (q * m + i)] = std::cos(ph);
+                st[2 * (q * m + i) + 1] = std::sin(ph);
+            }
+        }
+        const double scale = std::sqrt(sigma2 / 2.0);
+        float* xf = x + static_cast<size_t>(fi) * 2 * m * n;
+        for (int64_t i = 0; i < m; ++i) {
+            for (int64_t j = 0; j < n; ++j) {
+                double ar_acc = 0.0, ai_acc = 0.0;
+                for (int64_t q = 0; q < k; ++q) {
+                    const double ar = st[2 * (q * m + i)], ai = st[2 * (q * m + i) + 1];
+                    const double sr = src[2 * (q * n + j)], si = src[2 * (q * n + j) + 1];
+                    ar_acc += ar * sr - ai * si;
+                    ai_acc += ar * si + ai * sr;
+                }
+                const double nr = rn.normal();
+                const double ni = rn.normal();
+                ar_acc += scale * nr;
+                ai_acc += scale * ni;
+                xf[2 * (i * n + j)] = static_cast<float>(ar_acc);
+                xf[2 * (i * n + j) + 1] = static_cast<float>(ai_acc);
+            }
+        }
+        if (angles) std::copy(ang.begin(), ang.end(), angles + fi * k);
+        if (snr_db) snr_db[fi] = snr;
+    });
+    if (bad) return fail(FM_EINVAL, "random_scene: cannot place targets at this separation");
+    return FM_OK;
+}
+
+// ------------------------------------------------------------------ plan
+struct fm_plan_s {
+    fm_plan_desc d{};
+    int device = 0;
+    // workspace
+    float* R = nullptr;       // frames x M x M complex64
+    float* C = nullptr;       // frames x p x M complex64
+    float* V = nullptr;       // frames x p x M complex64
+    double* work = nullptr;   // frames x 2 x p x M complex128
+    double* Rt = nullptr;     // frames x p x p complex128
+    double* H = nullptr;      // frames x p x p complex128 (fast1)
+    double* basis = nullptr;  // frames x K x M complex128
+    double* eig = nullptr;    // frames x K
+    double* t = nullptr;      // frames x M complex128
+    double* zgrid = nullptr;  // L complex128
+    int32_t* scratch_status = nullptr;  // frames
+    // host-path staging
+    float* x_dev = nullptr;
+    float* omega_dev = nullptr;
+    int32_t* idx_dev = nullptr;
+    float* spec_dev = nullptr;
+    int32_t* cells_dev = nullptr;
+    double* heights_dev = nullptr;
+    double* base_dev = nullptr;
+    int32_t* count_dev = nullptr;
+    int32_t* status_dev = nullptr;
+    float* omega_pinned = nullptr;
+    int32_t* status_pinned = nullptr;
+    size_t bytes = 0;
+    std::vector<void*> allocs;
+
+    template <typename T>
+    cudaError_t get(T** p, size_t count) {
+        if (count == 0) {
+            *p = nullptr;
+            return cudaSuccess;
+        }
+        void* q = nullptr;
+        cudaError_t e = cudaMalloc(&q, sizeof(T) * count);
+        if (e != cudaSuccess) return e;
+        allocs.push_back(q);
+        bytes += sizeof(T) * count;
+        *p = static_cast<T*>(q);
+        return cudaSuccess;
+    }
+    ~fm_plan_s() {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        for (void* q : allocs) cudaFree(q);
+        if (omega_pinned) cudaFreeHost(omega_pinned);
+        if (status_pinned) cudaFreeHost(status_pinned);
+        cudaSetDevice(prev);
+    }
+};
+
+static fm_status validate_desc(const fm_plan_desc* d) {
+    if (!d) return fail(FM_EINVAL, "fm_plan_create: null descriptor");
+    if (d->m < 2) return fail(FM_EINVAL, "plan: need M >= 2");
+    if (d->n < 2 || (d->n & 1)) return fail(FM_EINVAL, "plan: need even N >= 2 (TMA row stride)");
+    const char* who = d->method == FM_METHOD_FAST2 ? "fast_music_2" : d->method == FM_METHOD_FAST1 ? "fast_music_1"
+                                                                                                 : "exact_signal_subspace";
+    if (d->k < 1 || d->k >= d->m) return fail(FM_EINVAL, std::string(who) + ": need 1 <= K < M");
+    if (d->k > 64) return fail(FM_ENOTSUP, "plan: K <= 64 supported");
+    if (d->method == FM_METHOD_FAST1 || d->method == FM_METHOD_FAST2) {
+        if (d->p < d->k || d->p > d->m) return fail(FM_EINVAL, std::string(who) + ": need K <= p <= M");
+        if (d->p > 64) return fail(FM_ENOTSUP, "plan: p <= 64 supported");
+    } else if (d->method != FM_METHOD_EXACT) {
+        return fail(FM_EINVAL, "plan: unknown method");
+    }
+    if (d->method == FM_METHOD_FAST2 && (d->t < 1 || d->t > 20))
+        return fail(FM_EINVAL, "fast_music_2: need 1 <= t <= 20");
+    if (d->grid_size < 2) return fail(FM_EINVAL, "AngleGrid: L >= 2 required");
+    if (d->d <= 0.0 || d->lambda <= 0.0) return fail(FM_EINVAL, "steering_vector: need M >= 1, d > 0, lambda > 0");
+    if (d->min_sep_cells < 0) return fail(FM_EINVAL, "plan: min_sep_cells >= 0");
+    if (d->max_frames < 1) return fail(FM_EINVAL, "plan: max_frames >= 1");
+    if (d->m > 4096) return fail(FM_ENOTSUP, "plan: M <= 4096 supported");
+    return FM_OK;
+}
+
+extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm_plan* out) {
+    if (!out) return fail(FM_EINVAL, "fm_plan_create: null out");
+    *out = nullptr;
+    fm_status st = validate_desc(desc);
+    if (st != FM_OK) return st;
+    FM_CUDA_OK(cudaSetDevice(device));
+    auto* pl = new fm_plan_s();
+    pl->d = *desc;
+    pl->device = device;
+    const size_t B = static_cast<size_t>(desc->max_frames), M = desc->m, K = desc->k, L = desc->grid_size;
+    const size_t P = desc->method == FM_METHOD_EXACT ? 0 : static_cast<size_t>(desc->p);
+    cudaError_t e = cudaSuccess;
+    auto chk = [&](cudaError_t x) {
+        if (e == cudaSuccess) e = x;
+    };
+    chk(pl->get(&pl->R, B * M * M * 2));
+    chk(pl->get(&pl->C, B * P * M * 2));
+    chk(pl->get(&pl->V, B * P * M * 2));
+    const size_t MP = (M + 15) / 16 * 16;  // Jacobi pads columns to blocks of 16
+    const size_t work_elems = desc->method == FM_METHOD_EXACT ? B * MP * MP * 2 : B * 2 * P * M * 2;
+    chk(pl->get(&pl->work, work_elems));
+    chk(pl->get(&pl->Rt, B * P * P * 2));
+    chk(pl->get(&pl->H, desc->method == FM_METHOD_FAST1 ? B * P * P * 2 : 0));
+    chk(pl->get(&pl->basis, B * K * M * 2));
+    chk(pl->get(&pl->eig, B * K));
+    chk(pl->get(&pl->t, B * M * 2));
+    chk(pl->get(&pl->zgrid, L * 2));
+    chk(pl->get(&pl->scratch_status, B));
+    if (e != cudaSuccess) {
+        delete pl;
+        return fm_fail_cuda(e, "fm_plan_create workspace", __FILE__, __LINE__);
+    }
+    const auto z = zgrid_host(desc->grid_size, desc->theta0, desc->theta1, desc->d, desc->lambda);
+    e = cudaMemcpy(pl->zgrid, z.data(), sizeof(double) * z.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        delete pl;
+        return fm_fail_cuda(e, "fm_plan_create zgrid", __FILE__, __LINE__);
+    }
+    *out = pl;
+    return FM_OK;
+}
+
+extern "C" fm_status fm_plan_destroy(fm_plan plan) {
+    delete plan;
+    return FM_OK;
+}
+
+extern "C" fm_status fm_plan_workspace_bytes(fm_plan plan, int64_t* bytes) {
+    if (!plan || !bytes) return fail(FM_EINVAL, "fm_plan_workspace_bytes: null");
+    *bytes = static_cast<int64_t>(plan->bytes);
+    return FM_OK;
+}
+
+extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
+    if (!plan) return 0;
+    const int t = plan->d.t;
+    int n = 1 /*cov*/ + 1 /*clear*/ + 2 /*autocorr, spectrum+peaks*/;
+    if (plan->d.method == FM_METHOD_FAST2) n += 1 + 2 * t + 1 + 1;  // rmul, t x (qr, rmul), qr final, nystrom
+    else if (plan->d.method == FM_METHOD_FAST1) n += 3;             // gather, qr final, nystrom
+    else n += 1;                                                    // jacobi
+    return n;
+}
+
+static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io, const float* R, cudaStream_t s) {
+    const auto& d = pl->d;
+    const int F = static_cast<int>(frames), M = static_cast<int>(d.m), P = static_cast<int>(d.p),
+              K = static_cast<int>(d.k);
+    double* basis = io->basis ? io->basis : pl->basis;
+    double* eig = io->eigenvalues ? io->eigenvalues : pl->eig;
+    k_clear_bits<<<(F + 255) / 256, 256, 0, s>>>(io->status, F, FM_FRAME_RANK | FM_FRAME_NOCONV);
+    FM_CUDA_OK(cudaGetLastError());
+    if (d.method == FM_METHOD_FAST2) {
+        FM_CUDA_OK(fm_launch_rmul<float>(R, io->omega, nullptr, pl->C, nullptr, F, M, P, true, s));
+        for (int it = 0; it < d.t; ++it) {
+            FM_CUDA_OK(fm_launch_qr<float>(pl->C, pl->work, pl->V, nullptr, io->status, nullptr, nullptr, F, M, P,
+                                           false, s));
+            FM_CUDA_OK(fm_launch_rmul<float>(R, nullptr, pl->V, pl->C, nullptr, F, M, P, false, s));
+        }
+        FM_CUDA_OK(fm_launch_qr<float>(pl->C, pl->work, nullptr, pl->Rt, pl->scratch_status, nullptr, nullptr, F, M,
+                                       P, true, s));
+        FM_CUDA_OK(fm_launch_nystrom<float>(pl->V, pl->C, nullptr, pl->work, pl->Rt, basis, eig, io->status, nullptr,
+                                            F, M, P, K, true, s));
+    } else if (d.method == FM_METHOD_FAST1) {
+        FM_CUDA_OK(fm_launch_gather<float>(R, io->indices, pl->C, pl->H, nullptr, F, M, P, s));
+        FM_CUDA_OK(fm_launch_qr<float>(pl->C, pl->work, nullptr, pl->Rt, pl->scratch_status, nullptr, nullptr, F, M,
+                                       P, true, s));
+        FM_CUDA_OK(fm_launch_nystrom<float>(nullptr, nullptr, pl->H, pl->work, pl->Rt, basis, eig, io->status,
+                                            nullptr, F, M, P, K, false, s));
+    } else {
+        FM_CUDA_OK(fm_launch_jacobi_eig<float>(R, pl->work, basis, eig, io->status, F, M, K, s));
+    }
+    FM_CUDA_OK(fm_launch_autocorr(basis, pl->t, F, M, K, s));
+    FM_CUDA_OK(fm_launch_spectrum_peaks(pl->t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, nullptr,
+                                        K, static_cast<int>(d.min_sep_cells), io->peak_cells, io->peak_heights,
+                                        io->baseline, io->peak_count, io->status, s));
+    return FM_OK;
+}
+
+static fm_status check_io(fm_plan pl, int64_t frames, const fm_batch_io* io) {
+    if (!pl || !io) return fail(FM_EINVAL, "fm_run_batch: null plan/io");
+    if (frames < 1 || frames > pl->d.max_frames) return fail(FM_EINVAL, "fm_run_batch: frames outside [1, max_frames]");
+    if (!io->x || !io->peak_cells || !io->peak_heights || !io->baseline || !io->peak_count || !io->status)
+        return fail(FM_EINVAL, "fm_run_batch: x, peak outputs and status are required");
+    if (pl->d.method == FM_METHOD_FAST2 && !io->omega) return fail(FM_EINVAL, "fm_run_batch: fast2 needs omega");
+    if (pl->d.method == FM_METHOD_FAST1 && !io->indices) return fail(FM_EINVAL, "fm_run_batch: fast1 needs indices");
+    return FM_OK;
+}
+
+extern "C" fm_status fm_run_batch(fm_plan pl, int64_t frames, const fm_batch_io* io, void* stream) {
+    fm_status st = check_io(pl, frames, io);
+    if (st != FM_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    FM_CUDA_OK(cudaSetDevice(pl->device));
+    FM_CUDA_OK(cudaMemsetAsync(io->status, 0, sizeof(int32_t) * frames, s));
+    float* R = io->covariance ? io->covariance : pl->R;
+    FM_CUDA_OK(fm_launch_cov_tc(io->x, R, io->status, frames, pl->d.m, pl->d.n, s));
+    return run_post_cov(pl, frames, io, R, s);
+}
+
+extern "C" fm_status fm_rerun_frames(fm_plan pl, int64_t frames, const int32_t* /*d_frames: all frames rerun*/, const fm_batch_io* io,
+                                     void* stream) {
+    fm_status st = check_io(pl, frames, io);
+    if (st != FM_OK) return st;
+    FM_CUDA_OK(cudaSetDevice(pl->device));
+    const float* R = io->covariance ? io->covariance : pl->R;
+    return run_post_cov(pl, frames, io, R, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const float* h_x, const uint64_t* draw_seeds,
+                                            fm_host_out* out, void* stream) {
+    if (!pl || !h_x || !out || !out->peak_cells || !out->peak_count || !out->status)
+        return fail(FM_EINVAL, "fm_estimate_batch_host: null argument");
+    if (frames < 1 || frames > pl->d.max_frames) return fail(FM_EINVAL, "fm_estimate_batch_host: frames out of range");
+    const auto& d = pl->d;
+    if (d.method != FM_METHOD_EXACT && !draw_seeds) return fail(FM_EINVAL, "fm_estimate_batch_host: seeds required");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    FM_CUDA_OK(cudaSetDevice(pl->device));
+    const size_t B = static_cast<size_t>(d.max_frames), M = d.m, N = d.n, P = d.p, K = d.k, L = d.grid_size;
+    if (!pl->x_dev) {
+        cudaError_t e = cudaSuccess;
+        auto chk = [&](cudaError_t x) {
+            if (e == cudaSuccess) e = x;
+        };
+        chk(pl->get(&pl->x_dev, B * M * N * 2));
+        chk(pl->get(&pl->omega_dev, d.method == FM_METHOD_FAST2 ? B * M * P : 0));
+        chk(pl->get(&pl->idx_dev, d.method == FM_METHOD_FAST1 ? B * P : 0));
+        chk(pl->get(&pl->spec_dev, B * L));
+        chk(pl->get(&pl->cells_dev, B * K));
+        chk(pl->get(&pl->heights_dev, B * K));
+        chk(pl->get(&pl->base_dev, B));
+        chk(pl->get(&pl->count_dev, B));
+        chk(pl->get(&pl->status_dev, B));
+        if (d.method == FM_METHOD_FAST2) chk(cudaMallocHost(&pl->omega_pinned, sizeof(float) * B * M * P));
+        chk(cudaMallocHost(&pl->status_pinned, sizeof(int32_t) * B));
+        if (e != cudaSuccess) return fm_fail_cuda(e, "fm_estimate_batch_host staging", __FILE__, __LINE__);
+    }
+    FM_CUDA_OK(cudaMemcpyAsync(pl->x_dev, h_x, sizeof(float) * frames * M * N * 2, cudaMemcpyHostToDevice, s));
+    std::vector<int32_t> idx_host;
+    if (d.method == FM_METHOD_FAST2) {
+        fm_draw_omega_batch(frames, draw_seeds, d.m, d.p, pl->omega_pinned);
+        FM_CUDA_OK(cudaMemcpyAsync(pl->omega_dev, pl->omega_pinned, sizeof(float) * frames * M * P,
+                                   cudaMemcpyHostToDevice, s));
+    } else if (d.method == FM_METHOD_FAST1) {
+        idx_host.resize(static_cast<size_t>(frames) * P);
+        fm_status st = fm_draw_indices_batch(frames, draw_seeds, d.m, d.p, idx_host.data());
+        if (st != FM_OK) return st;
+        FM_CUDA_OK(cudaMemcpyAsync(pl->idx_dev, idx_host.data(), sizeof(int32_t) * idx_host.size(),
+                                   cudaMemcpyHostToDevice, s));
+    }
+    fm_batch_io io{};
+    io.x = pl->x_dev;
+    io.omega = pl->omega_dev;
+    io.indices = pl->idx_dev;
+    io.spectrum = out->spectrum ? pl->spec_dev : nullptr;
+    io.peak_cells = pl->cells_dev;
+    io.peak_heights = pl->heights_dev;
+    io.baseline = pl->base_dev;
+    io.peak_count = pl->count_dev;
+    io.status = pl->status_dev;
+    fm_status st = fm_run_batch(pl, frames, &io, stream);
+    if (st != FM_OK) return st;
+    std::vector<int32_t> attempts(static_cast<size_t>(frames), 1);
+    if (d.method == FM_METHOD_FAST2) {
+        // R/src/estimators.cpp:114-137: up to 3 sub-seeded redraws per rank-deficient frame.
+        std::vector<uint64_t> seeds(draw_seeds, draw_seeds + frames);
+        for (int attempt = 1; attempt < 4; ++attempt) {
+            FM_CUDA_OK(cudaMemcpyAsync(pl->status_pinned, pl->status_dev, sizeof(int32_t) * frames,
+                                       cudaMemcpyDeviceToHost, s));
+            FM_CUDA_OK(cudaStreamSynchronize(s));
+            bool any = false;
+            for (int64_t f = 0; f < frames; ++f) {
+                if (pl->status_pinned[f] & FM_FRAME_RANK) {
+                    any = true;
+                    attempts[f] = attempt + 1;
+                    const uint64_t ds = fmhost::Rng::derive(draw_seeds[f], 0xF257u + static_cast<uint64_t>(attempt));
+                    fmhost::gaussian_matrix_real(d.m, d.p, ds, pl->omega_pinned + static_cast<size_t>(f) * M * P);
+                    FM_CUDA_OK(cudaMemcpyAsync(pl->omega_dev + static_cast<size_t>(f) * M * P,
+                                               pl->omega_pinned + static_cast<size_t>(f) * M * P,
+                                               sizeof(float) * M * P, cudaMemcpyHostToDevice, s));
+                }
+            }
+            if (!any) break;
+            st = fm_rerun_frames(pl, frames, nullptr, &io, stream);
+            if (st != FM_OK) return st;
+        }
+    }
+    FM_CUDA_OK(cudaMemcpyAsync(out->peak_cells, pl->cells_dev, sizeof(int32_t) * frames * K, cudaMemcpyDeviceToHost, s));
+    FM_CUDA_OK(cudaMemcpyAsync(out->peak_count, pl->count_dev, sizeof(int32_t) * frames, cudaMemcpyDeviceToHost, s));
+    FM_CUDA_OK(cudaMemcpyAsync(out->status, pl->status_dev, sizeof(int32_t) * frames, cudaMemcpyDeviceToHost, s));
+    if (out->peak_heights)
+        FM_CUDA_OK(cudaMemcpyAsync(out->peak_heights, pl->heights_dev, sizeof(double) * frames * K,
+                                   cudaMemcpyDeviceToHost, s));
+    if (out->baseline)
+        FM_CUDA_OK(cudaMemcpyAsync(out->baseline, pl->base_dev, sizeof(double) * frames, cudaMemcpyDeviceToHost, s));
+    if (out->spectrum)
+        FM_CUDA_OK(cudaMemcpyAsync(out->spectrum, pl->spec_dev, sizeof(float) * frames * L, cudaMemcpyDeviceToHost, s));
+    FM_CUDA_OK(cudaStreamSynchronize(s));
+    if (out->attempts) std::copy(attempts.begin(), attempts.end(), out->attempts);
+    return FM_OK;
+}
+
+// ------------------------------------------------------------------ fp64 single-matrix entry points
+namespace {
+
+struct ZCtx {
+    cudaStream_t s = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ZCtx() {
+        cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+    }
+    ~ZCtx() {
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+        if (s) cudaStreamDestroy(s);
+    }
+};
+
+// column-major complex128 Hermitian S -> row-major R (= conj of the column-major buffer)
+std::vector<double> to_rowmajor_hermitian(const double* s, int64_t m) {
+    std::vector<double> r(static_cast<size_t>(2 * m * m));
+    for (int64_t e = 0; e < m * m; ++e) {
+        r[2 * e] = s[2 * e];
+        r[2 * e + 1] = -s[2 * e + 1];
+    }
+    return r;
+}
+
+bool all_finite(const double* a, int64_t n) {
+    for (int64_t i = 0; i < n; ++i)
+        if (!std::isfinite(a[i])) return false;
+    return true;
+}
+
+fm_status check_hermitian_input(const double* s, int64_t m, const char* who) {
+    if (!s || m < 1) return fail(FM_EINVAL, std::string(who) + ": null or empty matrix");
+    if (!all_finite(s, 2 * m * m)) return fail(FM_EINVAL, std::string(who) + ": non-finite entries");
+    return FM_OK;
+}
+
+}  // namespace
+
+extern "C" fm_status fm_z_spatial_covariance(int64_t m, int64_t n, const double* y, double* s_out) {
+    if (m < 1 || n < 1) return fail(FM_EINVAL, "covariance: empty signal matrix");
+    if (!y || !s_out) return fail(FM_EINVAL, "covariance: null pointer");
+    if (!all_finite(y, 2 * m * n)) return fail(FM_EINVAL, "covariance: non-finite entries");
+    ZCtx c;
+    DevBuf<double> dy, ds;
+    FM_CUDA_OK(dy.alloc(2 * m * n));
+    FM_CUDA_OK(ds.alloc(2 * m * m));
+    FM_CUDA_OK(cudaMemcpyAsync(dy.p, y, sizeof(double) * 2 * m * n, cudaMemcpyHostToDevice, c.s));
+    dim3 blk(16, 16), grd(static_cast<unsigned>((m + 15) / 16), static_cast<unsigned>((m + 15) / 16));
+    k_cov_z<<<grd, blk, 0, c.s>>>(reinterpret_cast<const fmk::c64*>(dy.p), reinterpret_cast<fmk::c64*>(ds.p),
+                                  static_cast<int>(m), static_cast<int>(n));
+    FM_CUDA_OK(cudaGetLastError());
+    FM_CUDA_OK(cudaMemcpyAsync(s_out, ds.p, sizeof(double) * 2 * m * m, cudaMemcpyDeviceToHost, c.s));
+    FM_CUDA_OK(cudaStreamSynchronize(c.s));
+    return FM_OK;
+}
+
+static fm_status z_nystrom_common(int64_t m, const double* s, int64_t k, int64_t p, int32_t t, uint64_t seed,
+                                  bool fast2, double* basis, double* eigenvalues, double* cost_seconds,
+                                  int64_t* deficient_column) {
+    ZCtx c;
+    const int M = static_cast<int>(m), P = static_cast<int>(p), K = static_cast<int>(k);
+    const auto rrow = to_rowmajor_hermitian(s, m);
+    DevBuf<double> dR, dOm, dC, dV, dW, dRt, dH, dB, dE;
+    DevBuf<int32_t> dSt, dScr, dDef, dIdx;
+    FM_CUDA_OK(dR.alloc(2 * m * m));
+    FM_CUDA_OK(dOm.alloc(m * p));
+    FM_CUDA_OK(dC.alloc(2 * m * p));
+    FM_CUDA_OK(dV.alloc(2 * m * p));
+    FM_CUDA_OK(dW.alloc(4 * m * p));
+    FM_CUDA_OK(dRt.alloc(2 * p * p));
+    FM_CUDA_OK(dH.alloc(2 * p * p));
+    FM_CUDA_OK(dB.alloc(2 * m * k));
+    FM_CUDA_OK(dE.alloc(k));
+    FM_CUDA_OK(dSt.alloc(1));
+    FM_CUDA_OK(dScr.alloc(1));
+    FM_CUDA_OK(dDef.alloc(1));
+    FM_CUDA_OK(dIdx.alloc(p));
+    FM_CUDA_OK(cudaMemcpyAsync(dR.p, rrow.data(), sizeof(double) * rrow.size(), cudaMemcpyHostToDevice, c.s));
+    FM_CUDA_OK(cudaEventRecord(c.e0, c.s));
+    int32_t st_host = 0, def_host = -1;
+    if (fast2) {
+        std::vector<double> om(static_cast<size_t>(m * p));
+        for (int attempt = 0;; ++attempt) {
+            const uint64_t ds = attempt == 0 ? seed : fmhost::Rng::derive(seed, 0xF257u + static_cast<uint64_t>(attempt));
+            fmhost::gaussian_matrix_real(m, p, ds, om.data());
+            FM_CUDA_OK(cudaMemcpyAsync(dOm.p, om.data(), sizeof(double) * om.size(), cudaMemcpyHostToDevice, c.s));
+            FM_CUDA_OK(cudaMemsetAsync(dSt.p, 0, sizeof(int32_t), c.s));
+            FM_CUDA_OK(cudaMemsetAsync(dDef.p, 0xff, sizeof(int32_t), c.s));
+            FM_CUDA_OK(fm_launch_rmul<double>(dR.p, dOm.p, nullptr, dC.p, nullptr, 1, M, P, true, c.s));
+            for (int it = 0; it < t; ++it) {
+                FM_CUDA_OK(fm_launch_qr<double>(dC.p, dW.p, dV.p, nullptr, dSt.p, dDef.p, nullptr, 1, M, P, false, c.s));
+                FM_CUDA_OK(fm_launch_rmul<double>(dR.p, nullptr, dV.p, dC.p, nullptr, 1, M, P, false, c.s));
+            }
+            FM_CUDA_OK(cudaMemcpyAsync(&st_host, dSt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, c.s));
+            FM_CUDA_OK(cudaMemcpyAsync(&def_host, dDef.p, sizeof(int32_t), cudaMemcpyDeviceToHost, c.s));
+            FM_CUDA_OK(cudaStreamSynchronize(c.s));
+            if (!(st_host & FM_FRAME_RANK)) break;
+            if (attempt + 1 >= 4) {
+                if (deficient_column) *deficient_column = def_host;
+                char msg[160];
+                std::snprintf(msg, sizeof msg, "qr_orthonormal: rank deficient sketch; column %d is dependent",
+                              def_host);
+                return fail(FM_ERANK, msg);
+            }
+        }
+        FM_CUDA_OK(fm_launch_qr<double>(dC.p, dW.p, nullptr, dRt.p, dScr.p, nullptr, nullptr, 1, M, P, true, c.s));
+        FM_CUDA_OK(fm_launch_nystrom<double>(dV.p, dC.p, nullptr, dW.p, dRt.p, dB.p, dE.p, dSt.p, nullptr, 1, M, P, K,
+                                             true, c.s));
+    } else {
+        fmhost::Rng r(seed);
+        const auto idx = r.sample_without_replacement(m, p);
+        std::vector<int32_t> idx32(idx.begin(), idx.end());
+        FM_CUDA_OK(cudaMemcpyAsync(dIdx.p, idx32.data(), sizeof(int32_t) * p, cudaMemcpyHostToDevice, c.s));
+        FM_CUDA_OK(cudaMemsetAsync(dSt.p, 0, sizeof(int32_t), c.s));
+        FM_CUDA_OK(fm_launch_gather<double>(dR.p, dIdx.p, dC.p, dH.p, nullptr, 1, M, P, c.s));
+        FM_CUDA_OK(fm_launch_qr<double>(dC.p, dW.p, nullptr, dRt.p, dScr.p, nullptr, nullptr, 1, M, P, true, c.s));
+        FM_CUDA_OK(fm_launch_nystrom<double>(nullptr, nullptr, dH.p, dW.p, dRt.p, dB.p, dE.p, dSt.p, nullptr, 1, M, P,
+                                             K, false, c.s));
+    }
+    FM_CUDA_OK(cudaEventRecord(c.e1, c.s));
+    FM_CUDA_OK(cudaMemcpyAsync(basis, dB.p, sizeof(double) * 2 * m * k, cudaMemcpyDeviceToHost, c.s));
+    FM_CUDA_OK(cudaMemcpyAsync(eigenvalues, dE.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c.s));
+    FM_CUDA_OK(cudaMemcpyAsync(&st_host, dSt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, c.s));
+    FM_CUDA_OK(cudaStreamSynchronize(c.s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c.e0, c.e1);
+    if (cost_seconds) *cost_seconds = ms * 1e-3;
+    if (st_host & FM_FRAME_NOCONV) return fail(FM_ENOCONV, "thin_svd: Jacobi SVD did not converge");
+    return FM_OK;
+}
+
+extern "C" fm_status fm_z_fast_music_2(int64_t m, const double* s, int64_t k, int64_t p, int32_t t, uint64_t seed,
+                                       double* basis, double* eigenvalues, double* cost_seconds,
+                                       int64_t* deficient_column) {
+    fm_status st = check_hermitian_input(s, m, "fast_music_2");
+    if (st != FM_OK) return st;
+    if (k < 1 || k >= m) return fail(FM_EINVAL, "fast_music_2: need 1 <= K < M");
+    if (p < k || p > m) return fail(FM_EINVAL, "fast_music_2: need K <= p <= M");
+    if (t < 1 || t > 20) return fail(FM_EINVAL, "fast_music_2: need 1 <= t <= 20");
+    if (p > 64) return fail(FM_ENOTSUP, "fast_music_2: p <= 64 supported");
+    if (!basis || !eigenvalues) return fail(FM_EINVAL, "fast_music_2: null output");
+    return z_nystrom_common(m, s, k, p, t, seed, true, basis, eigenvalues, cost_seconds, deficient_column);
+}
+
+extern "C" fm_status fm_z_fast_music_1(int64_t m, const double* s, int64_t k, int64_t p, uint64_t seed, double* basis,
+                                       double* eigenvalues, double* cost_seconds) {
+    fm_status st = check_hermitian_input(s, m, "fast_music_1");
+    if (st != FM_OK) return st;
+    if (k < 1 || k >= m) return fail(FM_EINVAL, "fast_music_1: need 1 <= K < M");
+    if (p < k || p > m) return fail(FM_EINVAL, "fast_music_1: need K <= p <= M");
+    if (p > 64) return fail(FM_ENOTSUP, "fast_music_1: p <= 64 supported");
+    if (!basis || !eigenvalues) return fail(FM_EINVAL, "fast_music_1: null output");
+    return z_nystrom_common(m, s, k, p, 1, seed, false, basis, eigenvalues, cost_seconds, nullptr);
+}
+
+extern "C" fm_status fm_z_exact_signal_subspace(int64_t m, const double* s, int64_t k, double* basis,
+                                                double* eigenvalues, double* cost_seconds) {
+    fm_status st = check_hermitian_input(s, m, "exact_signal_subspace");
+    if (st != FM_OK) return st;
+    if (k < 1 || k >= m) return fail(FM_EINVAL, "exact_signal_subspace: need 1 <= K < M");
+    if (!basis || !eigenvalues) return fail(FM_EINVAL, "exact_signal_subspace: null output");
+    if (m > 384) return fail(FM_ENOTSUP, "exact_signal_subspace: M <= 384 supported (fp64 Jacobi block staging)");
+    const int64_t mp = (m + 15) / 16 * 16;
+    ZCtx c;
+    const auto rrow = to_rowmajor_hermitian(s, m);
+    DevBuf<double> dR, dW, dB, dE;
+    DevBuf<int32_t> dSt;
+    FM_CUDA_OK(dR.alloc(2 * m * m));
+    FM_CUDA_OK(dW.alloc(2 * mp * mp));
+    FM_CUDA_OK(dB.alloc(2 * m * k));
+    FM_CUDA_OK(dE.alloc(k));
+    FM_CUDA_OK(dSt.alloc(1));
+    FM_CUDA_OK(cudaMemcpyAsync(dR.p, rrow.data(), sizeof(double) * rrow.size(), cudaMemcpyHostToDevice, c.s));
+    FM_CUDA_OK(cudaMemsetAsync(dSt.p, 0, sizeof(int32_t), c.s));
+    FM_CUDA_OK(cudaEventRecord(c.e0, c.s));
+    FM_CUDA_OK(fm_launch_jacobi_eig<double>(dR.p, dW.p, dB.p, dE.p, dSt.p, 1, static_cast<int>(m),
+                                            static_cast<int>(k), c.s));
+    FM_CUDA_OK(cudaEventRecord(c.e1, c.s));
+    int32_t st_host = 0;
+    FM_CUDA_OK(cudaMemcpyAsync(basis, dB.p, sizeof(double) * 2 * m * k, cudaMemcpyDeviceToHost, c.s));
+    FM_CUDA_OK(cudaMemcpyAsync(eigenvalues, dE.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c.s));
+    FM_CUDA_OK(cudaMemcpyAsync(&st_host, dSt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, c.s));
+    FM_CUDA_OK(cudaStreamSynchronize(c.s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c.e0, c.e1);
+    if (cost_seconds) *cost_seconds = ms * 1e-3;
+    if (st_host & FM_FRAME_NOCONV) return fail(FM_ENOCONV, "hermitian_eig: eigensolver did not converge");
+    return FM_OK;
+}
+
+extern "C" fm_status fm_z_music_spectrum(int64_t m, int64_t kb, const double* basis, int64_t L, double theta0,
+                                         double theta1, double d, double lambda, double* values) {
+    if (m < 1) return fail(FM_EINVAL, "music_spectrum: empty basis");
+    if (L < 2) return fail(FM_EINVAL, "AngleGrid: L >= 2 required");
+    if (d <= 0.0 || lambda <= 0.0) return fail(FM_EINVAL, "steering_vector: need M >= 1, d > 0, lambda > 0");
+    if (kb < 0 || (kb > 0 && !basis) || !values) return fail(FM_EINVAL, "music_spectrum: bad arguments");
+    ZCtx c;
+    DevBuf<double> dB, dT, dZ, dOut, dDev;
+    FM_CUDA_OK(dB.alloc(std::max<int64_t>(2 * m * kb, 2)));
+    FM_CUDA_OK(dT.alloc(2 * m));
+    FM_CUDA_OK(dZ.alloc(2 * L));
+    FM_CUDA_OK(dOut.alloc(L));
+    FM_CUDA_OK(dDev.alloc(1));
+    if (kb > 0)
+        FM_CUDA_OK(cudaMemcpyAsync(dB.p, basis, sizeof(double) * 2 * m * kb, cudaMemcpyHostToDevice, c.s));
+    const auto z = zgrid_host(L, theta0, theta1, d, lambda);
+    FM_CUDA_OK(cudaMemcpyAsync(dZ.p, z.data(), sizeof(double) * z.size(), cudaMemcpyHostToDevice, c.s));
+    if (kb > 0) {
+        double dev = 0.0;
+        FM_CUDA_OK(fm_launch_orthocheck(dB.p, 1, static_cast<int>(m), static_cast<int>(kb), dDev.p, c.s));
+        FM_CUDA_OK(cudaMemcpyAsync(&dev, dDev.p, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+        FM_CUDA_OK(cudaStreamSynchronize(c.s));
+        if (!(dev <= 1e-6)) return fail(FM_EINVAL, "music_spectrum: basis columns are not orthonormal");
+    }
+    FM_CUDA_OK(fm_launch_autocorr(dB.p, dT.p, 1, static_cast<int>(m), static_cast<int>(kb), c.s));
+    FM_CUDA_OK(fm_launch_spectrum_peaks(dT.p, dZ.p, 1, static_cast<int>(m), static_cast<int>(L), nullptr, dOut.p, 1, 0,
+                                        nullptr, nullptr, nullptr, nullptr, nullptr, c.s));
+    FM_CUDA_OK(cudaMemcpyAsync(values, dOut.p, sizeof(double) * L, cudaMemcpyDeviceToHost, c.s));
+    FM_CUDA_OK(cudaStreamSynchronize(c.s));
+    return FM_OK;
+}
+
+extern "C" fm_status fm_z_extract_peaks(const double* values, int64_t L, int64_t k, int64_t min_sep, int64_t* cells,
+                                        double* heights, int64_t* count, double* baseline, int32_t* shortfall) {
+    if (k < 1) return fail(FM_EINVAL, "extract_peaks: K >= 1 required");
+    if (k > 64) return fail(FM_ENOTSUP, "extract_peaks: K <= 64 supported");
+    if (!values || L < 1 || !cells || !heights || !count || !baseline || !shortfall)
+        return fail(FM_EINVAL, "extract_peaks: bad arguments");
+    ZCtx c;
+    DevBuf<double> dV, dH, dBase;
+    DevBuf<int32_t> dC, dN, dOv;
+    FM_CUDA_OK(dV.alloc(L));
+    FM_CUDA_OK(dH.alloc(k));
+    FM_CUDA_OK(dBase.alloc(1));
+    FM_CUDA_OK(dC.alloc(k));
+    FM_CUDA_OK(dN.alloc(1));
+    FM_CUDA_OK(dOv.alloc(1));
+    FM_CUDA_OK(cudaMemcpyAsync(dV.p, values, sizeof(double) * L, cudaMemcpyHostToDevice, c.s));
+    FM_CUDA_OK(cudaMemsetAsync(dOv.p, 0, sizeof(int32_t), c.s));
+    FM_CUDA_OK(fm_launch_peaks_only(dV.p, 1, static_cast<int>(L), static_cast<int>(k), static_cast<int>(min_sep), dC.p,
+                                    dH.p, dBase.p, dN.p, dOv.p, c.s));
+    std::vector<int32_t> c32(static_cast<size_t>(k));
+    int32_t n = 0, ov = 0;
+    FM_CUDA_OK(cudaMemcpyAsync(c32.data(), dC.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, c.s));
+    FM_CUDA_OK(cudaMemcpyAsync(heights, dH.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c.s));
+    FM_CUDA_OK(cudaMemcpyAsync(baseline, dBase.p, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+    FM_CUDA_OK(cudaMemcpyAsync(&n, dN.p, sizeof(int32_t), cudaMemcpyDeviceToHost, c.s));
+    FM_CUDA_OK(cudaMemcpyAsync(&ov, dOv.p, sizeof(int32_t), cudaMemcpyDeviceToHost, c.s));
+    FM_CUDA_OK(cudaStreamSynchronize(c.s));
+    if (ov) return fail(FM_ENOTSUP, "extract_peaks: more local maxima than the candidate buffer holds");
+    for (int64_t i = 0; i < k; ++i) cells[i] = c32[static_cast<size_t>(i)];
+    *count = n;
+    *shortfall = n < k ? 1 : 0;
+    return FM_OK;
+}

@@ -1,0 +1,65 @@
+// Shared device helpers for the Fast-MUSIC B200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace fmk {
+
+// Per-frame status bits (written by kernels; mapped to the reference's
+// exceptions by the host layer, R/include/fastmusic/types.hpp:18-43).
+enum FrameStatus : int32_t {
+    kFrameOk = 0,
+    kFrameRank = 1,      // sketch lost column rank  -> RankDeficiencyError (host redraws)
+    kFrameNoConv = 2,    // Jacobi sweep cap hit     -> NonConvergenceError
+    kFrameRange = 4,     // input outside fp16 operand range of the tensor-core covariance
+    kFrameNonFinite = 8  // NaN/Inf in the input frame
+};
+
+template <typename T> struct cplx { T re, im; };
+using c32 = cplx<float>;
+using c64 = cplx<double>;
+
+template <typename T> __host__ __device__ __forceinline__ cplx<T> mk(T r, T i) { return {r, i}; }
+template <typename T> __host__ __device__ __forceinline__ cplx<T> operator+(cplx<T> a, cplx<T> b) { return {a.re + b.re, a.im + b.im}; }
+template <typename T> __host__ __device__ __forceinline__ cplx<T> operator-(cplx<T> a, cplx<T> b) { return {a.re - b.re, a.im - b.im}; }
+template <typename T> __host__ __device__ __forceinline__ cplx<T> operator*(cplx<T> a, cplx<T> b) {
+    return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+template <typename T> __host__ __device__ __forceinline__ cplx<T> operator*(T s, cplx<T> a) { return {s * a.re, s * a.im}; }
+template <typename T> __host__ __device__ __forceinline__ cplx<T> conj(cplx<T> a) { return {a.re, -a.im}; }
+template <typename T> __host__ __device__ __forceinline__ T norm2(cplx<T> a) { return a.re * a.re + a.im * a.im; }
+// acc += conj(a) * b
+template <typename T> __host__ __device__ __forceinline__ void cmac_conj(cplx<T>& acc, cplx<T> a, cplx<T> b) {
+    acc.re = fma(a.re, b.re, fma(a.im, b.im, acc.re));
+    acc.im = fma(a.re, b.im, fma(-a.im, b.re, acc.im));
+}
+// acc += a * b
+template <typename T> __host__ __device__ __forceinline__ void cmac(cplx<T>& acc, cplx<T> a, cplx<T> b) {
+    acc.re = fma(a.re, b.re, fma(-a.im, b.im, acc.re));
+    acc.im = fma(a.re, b.im, fma(a.im, b.re, acc.im));
+}
+template <typename T> __device__ __forceinline__ cplx<double> to64(cplx<T> a) { return {double(a.re), double(a.im)}; }
+
+template <typename T> struct eps_of;
+template <> struct eps_of<float> { static constexpr double value = 1.1920928955078125e-07; };
+template <> struct eps_of<double> { static constexpr double value = 2.220446049250313e-16; };
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace fmk
+
+#define FM_CUDA_OK(expr)                                                     \
+    do {                                                                     \
+        cudaError_t _e = (expr);                                             \
+        if (_e != cudaSuccess) return fm_fail_cuda(_e, #expr, __FILE__, __LINE__); \
+    } while (0)

@@ -1,0 +1,361 @@
+// K6 + K7 — MUSIC pseudo-spectrum over the angle grid and peak picking, batched.
+//
+// Reference lines replaced:
+//   music_spectrum / denominator_spectrum   R/src/spectrum.cpp:37-68
+//   steering_vector                         R/src/scene.cpp:72-82
+//   extract_peaks (local_maxima, ranked_maxima, select_separated,
+//                  baseline_outside, to_peak_set)  R/src/spectrum.cpp:97-188
+//
+// Formulation. For an orthonormal basis U (M x K) and a ULA steering vector with
+// a_m = z^m, z = exp(j * 2 pi d sin(theta) / lambda), the reference denominator
+//     d(theta) = M - ||U^H a||^2 = M - a^H (U U^H) a
+// is a trigonometric polynomial in z whose coefficients are the diagonal sums of the
+// signal projector:   t_delta = sum_m (U U^H)_{m, m+delta} = sum_k sum_m U_mk conj(U_{m+delta,k})
+//     d = (M - t_0) - 2 Re( sum_{delta=1}^{M-1} t_delta z^delta ).
+// The t_delta (M complex per frame) are computed once per frame (k_autocorr) and every
+// grid point costs M-1 complex Horner steps in fp64 instead of the K*M complex MACs of
+// U^H a — and fp64 removes the cancellation M - ||U^H a||^2 that makes an fp32/TF32 GEMM
+// of U^H A miss the 0.05 dB gate. The reference floor 1e-12*M is kept.
+//
+// Layout: basis B x K x M complex<double> (column-major per frame); t B x M complex<double>;
+// zgrid L complex<double> (host-computed exp(j*step_l) with the reference's step formula);
+// spectrum out B x L (fp32 and/or fp64); peaks B x K int32 cells + fp64 heights, baseline,
+// count (shortfall = count < K).
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "fm_common.cuh"
+
+namespace fmk {
+namespace spec {
+
+constexpr int kNT = 256;
+constexpr int kNW = kNT / 32;
+
+// t_delta, delta = 0..M-1, for frame blockIdx.y; one thread per delta.
+__global__ void __launch_bounds__(kNT) k_autocorr(const c64* __restrict__ basis, c64* __restrict__ t, int m, int k) {
+    extern __shared__ c64 col[];  // one basis column (M complex)
+    const int f = blockIdx.y;
+    const int delta = blockIdx.x * kNT + threadIdx.x;
+    const c64* Uf = basis + static_cast<size_t>(f) * m * k;
+    c64 acc = mk(0.0, 0.0);
+    for (int kk = 0; kk < k; ++kk) {
+        __syncthreads();
+        for (int r = threadIdx.x; r < m; r += kNT) col[r] = Uf[static_cast<size_t>(kk) * m + r];
+        __syncthreads();
+        if (delta < m) {
+            for (int r = 0; r + delta < m; ++r) {
+                // U_r * conj(U_{r+delta})
+                const c64 a = col[r], b = col[r + delta];
+                acc.re = fma(a.re, b.re, fma(a.im, b.im, acc.re));
+                acc.im = fma(a.im, b.re, fma(-a.re, b.im, acc.im));
+            }
+        }
+    }
+    if (delta < m) t[static_cast<size_t>(f) * m + delta] = acc;
+}
+
+// Block-wide (height desc, cell asc) argmax helper.
+__device__ __forceinline__ bool better(double h1, int c1, double h2, int c2) {
+    return h1 > h2 || (h1 == h2 && c1 < c2);
+}
+
+// R/src/spectrum.cpp:97-188 on values v[0..L) held in shared memory.
+// Outputs: cells (ascending), heights, baseline, count. Returns the candidate overflow flag.
+__device__ void block_peaks(const double* v, int L, int K, int min_sep, int* cand_cell, double* cand_h, int cap,
+                            int* out_cells, double* out_h, double* out_base, int* out_count, bool& overflow) {
+    __shared__ int s_nc;
+    __shared__ int s_sel[64];
+    __shared__ double s_selh[64];
+    __shared__ int s_nsel;
+    __shared__ double s_wh[kNW];
+    __shared__ int s_wc[kNW];
+    __shared__ int s_wi[kNW];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        s_nc = 0;
+        s_nsel = 0;
+    }
+    __syncthreads();
+    // 1. strict local maxima; plateau -> leftmost index (run start with a rising edge)
+    for (int l = 1 + threadIdx.x; l + 1 < L; l += kNT) {
+        const double x = v[l];
+        if (x > v[l - 1]) {
+            int r = l;
+            while (r + 1 < L && v[r + 1] == x) ++r;
+            if (r + 1 < L && v[r + 1] < x) {
+                const int slot = atomicAdd(&s_nc, 1);
+                if (slot < cap) {
+                    cand_cell[slot] = l;
+                    cand_h[slot] = x;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const int nc = min(s_nc, cap);
+    overflow = s_nc > cap;
+    // 2. greedy selection in (height desc, cell asc) order with |dc| >= min_sep:
+    //    repeatedly take the best candidate not clashing with the current selection.
+    for (int it = 0; it < K; ++it) {
+        double bh = -1.0;
+        int bc = 0x7fffffff, bi = -1;
+        const int nsel = s_nsel;
+        for (int i = threadIdx.x; i < nc; i += kNT) {
+            const int c = cand_cell[i];
+            bool clash = false;
+            for (int s = 0; s < nsel; ++s)
+                if (abs(c - s_sel[s]) < min_sep) {
+                    clash = true;
+                    break;
+                }
+            if (clash) continue;
+            const double h = cand_h[i];
+            if (bi < 0 || better(h, c, bh, bc)) {
+                bh = h;
+                bc = c;
+                bi = i;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double oh = __shfl_xor_sync(0xffffffffu, bh, o);
+            const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (oi >= 0 && (bi < 0 || better(oh, oc, bh, bc))) {
+                bh = oh;
+                bc = oc;
+                bi = oi;
+            }
+        }
+        if (lane == 0) {
+            s_wh[warp] = bh;
+            s_wc[warp] = bc;
+            s_wi[warp] = bi;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int wi = -1;
+            double wh = -1.0;
+            int wc = 0x7fffffff;
+            for (int w = 0; w < kNW; ++w)
+                if (s_wi[w] >= 0 && (wi < 0 || better(s_wh[w], s_wc[w], wh, wc))) {
+                    wi = s_wi[w];
+                    wh = s_wh[w];
+                    wc = s_wc[w];
+                }
+            if (wi >= 0) {
+                s_sel[s_nsel] = wc;
+                s_selh[s_nsel] = wh;
+                s_nsel = s_nsel + 1;
+            }
+        }
+        __syncthreads();
+        if (s_nsel == nsel) break;  // exhausted: shortfall
+    }
+    const int nsel = s_nsel;
+    // 3. baseline: max over cells farther than min_sep from every selected peak (init 0)
+    double p0 = 0.0;
+    for (int l = threadIdx.x; l < L; l += kNT) {
+        bool near = false;
+        for (int s = 0; s < nsel; ++s)
+            if (abs(l - s_sel[s]) <= min_sep) {
+                near = true;
+                break;
+            }
+        if (!near) p0 = fmax(p0, v[l]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) p0 = fmax(p0, __shfl_xor_sync(0xffffffffu, p0, o));
+    if (lane == 0) s_wh[warp] = p0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int w = 0; w < kNW; ++w) b = fmax(b, s_wh[w]);
+        // 4. ascending cell order (to_peak_set)
+        for (int x = 0; x < nsel; ++x) {
+            int best = x;
+            for (int y = x + 1; y < nsel; ++y)
+                if (s_sel[y] < s_sel[best]) best = y;
+            const int tc = s_sel[x];
+            s_sel[x] = s_sel[best];
+            s_sel[best] = tc;
+            const double th = s_selh[x];
+            s_selh[x] = s_selh[best];
+            s_selh[best] = th;
+        }
+        for (int x = 0; x < K; ++x) {
+            out_cells[x] = x < nsel ? s_sel[x] : -1;
+            out_h[x] = x < nsel ? s_selh[x] : 0.0;
+        }
+        *out_base = b;
+        *out_count = nsel;
+    }
+    __syncthreads();
+}
+
+struct PeakOut {
+    int32_t* cells;     // B x K
+    double* heights;    // B x K
+    double* baseline;   // B
+    int32_t* count;     // B
+};
+
+// Candidate capacity: a degree-(M-1) trigonometric denominator has < M interior minima,
+// so 2M + 64 slots cover any MUSIC spectrum; bounded by the shared-memory budget.
+__host__ __device__ __forceinline__ int cand_cap(int L, int m) {
+    const int budget = (200 * 1024 - 8 * L - 16 * m) / 12;
+    const int want = L / 2 + 1 < 2 * m + 64 ? L / 2 + 1 : 2 * m + 64;
+    return want < budget ? want : budget;
+}
+__host__ __device__ __forceinline__ int cand_cap_values(int L) {
+    const int budget = (200 * 1024 - 8 * L) / 12;
+    return L / 2 + 1 < budget ? L / 2 + 1 : budget;
+}
+
+// Spectrum (fp64 Horner over z) + peaks, one CTA per frame.
+__global__ void __launch_bounds__(kNT) k_spectrum_peaks(const c64* __restrict__ t, const c64* __restrict__ zgrid,
+                                                        int m, int L, float* __restrict__ spec32,
+                                                        double* __restrict__ spec64, int K, int min_sep,
+                                                        PeakOut out, int32_t* __restrict__ status) {
+    extern __shared__ uint8_t dsm[];
+    double* sP = reinterpret_cast<double*>(dsm);
+    c64* st = reinterpret_cast<c64*>(sP + L);
+    const int cap = cand_cap(L, m);
+    int* ccell = reinterpret_cast<int*>(st + m);
+    double* ch = reinterpret_cast<double*>(ccell + ((cap + 1) & ~1));
+    const int f = blockIdx.x;
+    for (int r = threadIdx.x; r < m; r += kNT) st[r] = t[static_cast<size_t>(f) * m + r];
+    __syncthreads();
+    const double c0 = static_cast<double>(m) - st[0].re;
+    const double floor_v = 1e-12 * static_cast<double>(m);
+    for (int l = threadIdx.x; l < L; l += kNT) {
+        const c64 z = zgrid[l];
+        double pr = 0.0, pi = 0.0;
+        if (m > 1) {
+            pr = st[m - 1].re;
+            pi = st[m - 1].im;
+            for (int dlt = m - 2; dlt >= 1; --dlt) {
+                const double nr = fma(pr, z.re, fma(-pi, z.im, st[dlt].re));
+                const double ni = fma(pr, z.im, fma(pi, z.re, st[dlt].im));
+                pr = nr;
+                pi = ni;
+            }
+            const double sr = pr * z.re - pi * z.im;  // Re(p * z)
+            pr = sr;
+        }
+        const double d = c0 - 2.0 * pr;
+        const double P = 1.0 / fmax(d, floor_v);
+        sP[l] = P;
+        if (spec32) spec32[static_cast<size_t>(f) * L + l] = static_cast<float>(P);
+        if (spec64) spec64[static_cast<size_t>(f) * L + l] = P;
+    }
+    __syncthreads();
+    if (out.cells) {
+        bool overflow = false;
+        block_peaks(sP, L, K, min_sep, ccell, ch, cap, out.cells + static_cast<size_t>(f) * K,
+                    out.heights + static_cast<size_t>(f) * K, out.baseline + f, out.count + f, overflow);
+        if (overflow && threadIdx.x == 0 && status) atomicOr(&status[f], kFrameNoConv);
+    }
+}
+
+// Peaks only, on caller-provided fp64 values (facade extract_peaks).
+__global__ void __launch_bounds__(kNT) k_peaks_only(const double* __restrict__ values, int L, int K, int min_sep,
+                                                    PeakOut out, int32_t* __restrict__ overflow_flag) {
+    extern __shared__ uint8_t dsm[];
+    double* sv = reinterpret_cast<double*>(dsm);
+    const int cap = cand_cap_values(L);
+    int* ccell = reinterpret_cast<int*>(sv + L);
+    double* ch = reinterpret_cast<double*>(ccell + ((cap + 1) & ~1));
+    const int f = blockIdx.x;
+    for (int l = threadIdx.x; l < L; l += kNT) sv[l] = values[static_cast<size_t>(f) * L + l];
+    __syncthreads();
+    bool overflow = false;
+    block_peaks(sv, L, K, min_sep, ccell, ch, cap, out.cells + static_cast<size_t>(f) * K,
+                out.heights + static_cast<size_t>(f) * K, out.baseline + f, out.count + f, overflow);
+    if (overflow && threadIdx.x == 0 && overflow_flag) atomicOr(overflow_flag, 1);
+}
+
+// max |U^H U - I| per frame (music_spectrum precondition, R/src/spectrum.cpp:55-61).
+__global__ void __launch_bounds__(kNT) k_orthocheck(const c64* __restrict__ basis, int m, int k,
+                                                    double* __restrict__ dev) {
+    __shared__ double s_w[kNW];
+    const int f = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const c64* Uf = basis + static_cast<size_t>(f) * m * k;
+    double mx = 0.0;
+    for (int e = warp; e < k * k; e += kNW) {
+        const int i = e % k, j = e / k;
+        c64 s = mk(0.0, 0.0);
+        for (int r = lane; r < m; r += 32) cmac_conj(s, Uf[static_cast<size_t>(i) * m + r], Uf[static_cast<size_t>(j) * m + r]);
+        s.re = warp_sum(s.re);
+        s.im = warp_sum(s.im);
+        if (i == j) s.re -= 1.0;
+        mx = fmax(mx, sqrt(norm2(s)));
+    }
+    if (lane == 0) s_w[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int w = 0; w < kNW; ++w) b = fmax(b, s_w[w]);
+        dev[f] = b;
+    }
+}
+
+}  // namespace spec
+}  // namespace fmk
+
+using namespace fmk;
+
+cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, int k, cudaStream_t s) {
+    const size_t smem = sizeof(c64) * m;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(spec::k_autocorr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+    }
+    dim3 grid((m + spec::kNT - 1) / spec::kNT, frames);
+    spec::k_autocorr<<<grid, spec::kNT, smem, s>>>(static_cast<const c64*>(basis), static_cast<c64*>(t), m, k);
+    return cudaGetLastError();
+}
+
+static size_t spectrum_smem(int m, int L) {
+    const int cap = spec::cand_cap(L, m);
+    if (cap < 16) return ~size_t(0);
+    return sizeof(double) * L + sizeof(c64) * m + sizeof(int) * ((cap + 1) & ~1) + sizeof(double) * cap + 16;
+}
+
+cudaError_t fm_launch_spectrum_peaks(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
+                                     double* spec64, int K, int min_sep, int32_t* cells, double* heights,
+                                     double* baseline, int32_t* count, int32_t* status, cudaStream_t s) {
+    const size_t smem = spectrum_smem(m, L);
+    if (smem > 227 * 1024 || K > 64) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(spec::k_spectrum_peaks, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    spec::PeakOut out{cells, heights, baseline, count};
+    spec::k_spectrum_peaks<<<frames, spec::kNT, smem, s>>>(static_cast<const c64*>(t), static_cast<const c64*>(zgrid),
+                                                           m, L, spec32, spec64, K, min_sep, out, status);
+    return cudaGetLastError();
+}
+
+cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K, int min_sep, int32_t* cells,
+                                 double* heights, double* baseline, int32_t* count, int32_t* overflow,
+                                 cudaStream_t s) {
+    const int cap = spec::cand_cap_values(L);
+    const size_t smem = sizeof(double) * L + sizeof(int) * ((cap + 1) & ~1) + sizeof(double) * cap + 16;
+    if (cap < 16 || smem > 227 * 1024 || K > 64) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(spec::k_peaks_only, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    spec::PeakOut out{cells, heights, baseline, count};
+    spec::k_peaks_only<<<frames, spec::kNT, smem, s>>>(values, L, K, min_sep, out, overflow);
+    return cudaGetLastError();
+}
+
+cudaError_t fm_launch_orthocheck(const void* basis, int frames, int m, int k, double* dev, cudaStream_t s) {
+    spec::k_orthocheck<<<frames, spec::kNT, 0, s>>>(static_cast<const c64*>(basis), m, k, dev);
+    return cudaGetLastError();
+}

@@ -1,0 +1,567 @@
+// K2/K3/K4 — randomized range finder, orthonormalisation and Nystrom rank restriction,
+// batched over frames (one CTA per frame for the small-matrix stages).
+//
+// Reference lines replaced:
+//   fast_music_2            R/src/estimators.cpp:104-139  (C = S Omega, t x {V = orth(C); C = S V},
+//                                                          W = pinv(V^H C), rank-restricted recovery)
+//   fast_music_1            R/src/estimators.cpp:87-102   (C = S(:,I), W = pinv(S(I,I)))
+//   rank_restricted_subspace R/src/estimators.cpp:37-50   (+ clamp_nonnegative :25-31)
+//   qr_orthonormal          R/src/linalg.cpp:127-141      (column-pivoted Householder, Eigen rank rule)
+//   pseudo_inverse          R/src/linalg.cpp:143-163      (SVD, cutoff max(r,c)*eps*sigma1)
+//   thin_svd / JacobiSVD    R/src/linalg.cpp:93-125
+//
+// Layouts (HBM / L2): R  B x M x M complex<T> row-major (K1 output, Hermitian);
+//   Omega B x M x p real<T> row-major (the reference fill order, R/src/linalg.cpp:186-190);
+//   C, V  B x p x M complex<T> column-major (column c contiguous);
+//   work  B x 2 x p x M complex<double> (Householder vectors | explicit Q);
+//   Rt    B x p x p complex<double> (R factor with the column pivoting undone).
+// Arithmetic: products C = R V in T (fp32 for the batched c64 path, fp64 for the
+// reference-facade path); every small-matrix step (Householder QR, Gram H, Jacobi SVD,
+// pinv, B' = Rt W Rt^H, basis U = Q Z_K) in fp64. Rank / pinv cutoffs
+// use the reference formulas with the machine epsilon of the data type T.
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "fm_common.cuh"
+
+namespace fmk {
+namespace sub {
+
+constexpr int kNT = 256;  // threads per block
+constexpr int kNW = kNT / 32;
+
+__device__ __forceinline__ int frame_of(const int32_t* map) { return map ? map[blockIdx.y] : blockIdx.y; }
+__device__ __forceinline__ int frame_of_x(const int32_t* map) { return map ? map[blockIdx.x] : blockIdx.x; }
+
+// ------------------------------------------------------------------ C = R * rhs
+// C[c][m] = sum_j R[m][j] rhs[j][c] = sum_j conj(R[j][m]) rhs[j][c]  (R Hermitian; the
+// conj-transpose read makes the R loads coalesced across threads m).
+// rhs: REAL -> Omega row-major M x p (real); else V column-major p x M (complex).
+template <typename T, int PC, bool REAL>
+__global__ void __launch_bounds__(kNT) k_rmul(const cplx<T>* __restrict__ R, const T* __restrict__ omega,
+                                               const cplx<T>* __restrict__ V, cplx<T>* __restrict__ C,
+                                               const int32_t* __restrict__ fmap, int m, int p) {
+    constexpr int JC = 32;
+    __shared__ cplx<T> rhs_s[JC][PC];
+    const int f = frame_of(fmap);
+    const int row = blockIdx.x * kNT + threadIdx.x;
+    const int c0 = blockIdx.z * PC;  // column slice (p > PC)
+    const cplx<T>* Rf = R + static_cast<size_t>(f) * m * m;
+    cplx<T> acc[PC];
+#pragma unroll
+    for (int c = 0; c < PC; ++c) acc[c] = mk<T>(0, 0);
+    for (int j0 = 0; j0 < m; j0 += JC) {
+        const int jn = min(JC, m - j0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < JC * PC; e += kNT) {
+            const int jj = e / PC, c = e % PC;
+            cplx<T> v = mk<T>(0, 0);
+            if (jj < jn && c0 + c < p) {
+                if (REAL) {
+                    v.re = omega[static_cast<size_t>(f) * m * p + static_cast<size_t>(j0 + jj) * p + c0 + c];
+                } else {
+                    v = V[static_cast<size_t>(f) * m * p + static_cast<size_t>(c0 + c) * m + j0 + jj];
+                }
+            }
+            rhs_s[jj][c] = v;
+        }
+        __syncthreads();
+        if (row < m) {
+            const cplx<T>* col = Rf + static_cast<size_t>(j0) * m + row;
+#pragma unroll 4
+            for (int jj = 0; jj < jn; ++jj) {
+                const cplx<T> r = col[static_cast<size_t>(jj) * m];  // R[j][row] -> conj gives R[row][j]
+#pragma unroll
+                for (int c = 0; c < PC; ++c) {
+                    if (REAL) {
+                        acc[c].re = fma(r.re, rhs_s[jj][c].re, acc[c].re);
+                        acc[c].im = fma(-r.im, rhs_s[jj][c].re, acc[c].im);
+                    } else {
+                        cmac_conj(acc[c], r, rhs_s[jj][c]);
+                    }
+                }
+            }
+        }
+    }
+    if (row < m) {
+        cplx<T>* Cf = C + static_cast<size_t>(f) * m * p;
+#pragma unroll
+        for (int c = 0; c < PC; ++c)
+            if (c0 + c < p) Cf[static_cast<size_t>(c0 + c) * m + row] = acc[c];
+    }
+}
+
+// ------------------------------------------------------------------ fast1 gather
+// C = R(:, I) (column-major p x M), H = R(I, I) (p x p, fp64).
+template <typename T>
+__global__ void __launch_bounds__(kNT) k_gather(const cplx<T>* __restrict__ R, const int32_t* __restrict__ idx,
+                                                 cplx<T>* __restrict__ C, c64* __restrict__ H,
+                                                 const int32_t* __restrict__ fmap, int m, int p) {
+    const int f = frame_of_x(fmap);
+    const cplx<T>* Rf = R + static_cast<size_t>(f) * m * m;
+    const int32_t* ix = idx + static_cast<size_t>(f) * p;
+    cplx<T>* Cf = C + static_cast<size_t>(f) * m * p;
+    for (int e = threadIdx.x; e < m * p; e += kNT) {
+        const int c = e / m, row = e % m;
+        // column I_c of R: R[row][I_c] = conj(R[I_c][row]) -> coalesced read of row I_c
+        Cf[static_cast<size_t>(c) * m + row] = conj(Rf[static_cast<size_t>(ix[c]) * m + row]);
+    }
+    c64* Hf = H + static_cast<size_t>(f) * p * p;
+    for (int e = threadIdx.x; e < p * p; e += kNT) {
+        const int i = e % p, j = e / p;  // column-major H[j][i] = H(i, j)
+        Hf[static_cast<size_t>(j) * p + i] = to64(Rf[static_cast<size_t>(ix[i]) * m + ix[j]]);
+    }
+}
+
+// ------------------------------------------------------------------ block helpers
+__device__ __forceinline__ c64 warp_sum_c(c64 v) {
+    v.re = warp_sum(v.re);
+    v.im = warp_sum(v.im);
+    return v;
+}
+
+// ------------------------------------------------------------------ pivoted Householder QR
+// R/src/linalg.cpp:127-141 (ColPivHouseholderQR + rank()). One CTA per frame, fp64.
+// Column-major A = work[f][0] (p x M), explicit Q = work[f][1]. Warp w owns columns
+// j == w (mod 8) for the reductions and the trailing updates.
+// OUT: MODE 0 -> V (T, column-major) for the power iteration;
+//      MODE 1 -> Q (fp64, in work[f][1]) and Rt (p x p, pivoting undone) for the Nystrom tail.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kNT) k_qr(const cplx<T>* __restrict__ Cin, c64* __restrict__ work,
+                                             cplx<T>* __restrict__ Vout, c64* __restrict__ Rt,
+                                             int32_t* __restrict__ status, int32_t* __restrict__ defcol,
+                                             const int32_t* __restrict__ fmap, int m, int p) {
+    __shared__ double nrm2[64];
+    __shared__ c64 rdiag[64];
+    __shared__ double tau[64];
+    __shared__ int perm[64];
+    __shared__ int s_pivot;
+    __shared__ double s_maxcol;
+    const int f = frame_of_x(fmap);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    c64* A = work + static_cast<size_t>(f) * 2 * p * m;
+    c64* Q = A + static_cast<size_t>(p) * m;
+    const cplx<T>* Cf = Cin + static_cast<size_t>(f) * m * p;
+    const double eps = eps_of<T>::value;
+
+    // load + initial column norms
+    for (int j = warp; j < p; j += kNW) {
+        double s = 0.0;
+        for (int r = lane; r < m; r += 32) {
+            const c64 v = to64(Cf[static_cast<size_t>(j) * m + r]);
+            A[static_cast<size_t>(j) * m + r] = v;
+            s += norm2(v);
+        }
+        s = warp_sum(s);
+        if (lane == 0) nrm2[j] = s;
+    }
+    if (threadIdx.x < p) perm[threadIdx.x] = threadIdx.x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mx = 0.0;
+        for (int j = 0; j < p; ++j) mx = fmax(mx, nrm2[j]);
+        s_maxcol = sqrt(mx);
+    }
+    __syncthreads();
+    const double thr_helper = (s_maxcol * eps) * (s_maxcol * eps) / static_cast<double>(m);
+    int nonzero = p;  // tracked by thread 0 only
+
+    for (int k = 0; k < p; ++k) {
+        if (threadIdx.x == 0) {
+            int piv = k;
+            double best = nrm2[k];
+            for (int j = k + 1; j < p; ++j)
+                if (nrm2[j] > best) {
+                    best = nrm2[j];
+                    piv = j;
+                }
+            if (nonzero == p && best < thr_helper * static_cast<double>(m - k)) nonzero = k;
+            s_pivot = piv;
+            const int tp = perm[k];
+            perm[k] = perm[piv];
+            perm[piv] = tp;
+            nrm2[piv] = nrm2[k];
+            nrm2[k] = best;
+        }
+        __syncthreads();
+        const int piv = s_pivot;
+        if (piv != k) {
+            for (int r = threadIdx.x; r < m; r += kNT) {
+                const c64 a = A[static_cast<size_t>(k) * m + r];
+                A[static_cast<size_t>(k) * m + r] = A[static_cast<size_t>(piv) * m + r];
+                A[static_cast<size_t>(piv) * m + r] = a;
+            }
+        }
+        __syncthreads();
+        // Householder for x = A[k:, k]; H x = alpha e_k, alpha = -phase(x0) ||x||.
+        if (threadIdx.x == 0) {
+            const double xn = sqrt(fmax(nrm2[k], 0.0));
+            const c64 x0 = A[static_cast<size_t>(k) * m + k];
+            const double ax0 = sqrt(norm2(x0));
+            if (xn == 0.0) {
+                rdiag[k] = mk(0.0, 0.0);
+                tau[k] = 0.0;
+            } else {
+                const c64 ph = ax0 > 0.0 ? mk(x0.re / ax0, x0.im / ax0) : mk(1.0, 0.0);
+                rdiag[k] = mk(-ph.re * xn, -ph.im * xn);
+                A[static_cast<size_t>(k) * m + k] = mk(x0.re + ph.re * xn, x0.im + ph.im * xn);  // v_k
+                tau[k] = 1.0 / (xn * (xn + ax0));  // 2 / (v^H v)
+            }
+        }
+        __syncthreads();
+        const double tk = tau[k];
+        const c64* v = A + static_cast<size_t>(k) * m;
+        for (int j = k + 1 + warp; j < p; j += kNW) {
+            c64* a = A + static_cast<size_t>(j) * m;
+            c64 w = mk(0.0, 0.0);
+            for (int r = k + lane; r < m; r += 32) cmac_conj(w, v[r], a[r]);
+            w = warp_sum_c(w);
+            double s = 0.0;
+            const c64 tw = mk(tk * w.re, tk * w.im);
+            for (int r = k + lane; r < m; r += 32) {
+                const c64 vr = v[r];
+                c64 ar = a[r];
+                ar.re -= vr.re * tw.re - vr.im * tw.im;
+                ar.im -= vr.re * tw.im + vr.im * tw.re;
+                a[r] = ar;
+                if (r > k) s += norm2(ar);
+            }
+            s = warp_sum(s);
+            if (lane == 0) nrm2[j] = s;
+        }
+        __syncthreads();
+    }
+
+    // rank (Eigen ColPivHouseholderQR::rank) with the data-type epsilon
+    if (threadIdx.x == 0) {
+        double maxpivot = 0.0;
+        for (int k = 0; k < p; ++k) maxpivot = fmax(maxpivot, sqrt(norm2(rdiag[k])));
+        const double thr = maxpivot * eps * static_cast<double>(p);
+        int rank = 0;
+        for (int k = 0; k < nonzero; ++k) rank += sqrt(norm2(rdiag[k])) > thr ? 1 : 0;
+        if (rank < p) {
+            atomicOr(&status[f], kFrameRank);
+            if (defcol) defcol[f] = perm[rank];
+        }
+    }
+
+    // explicit Q: column j = H_0 H_1 ... H_j e_j  (columns independent: one warp each)
+    for (int j = warp; j < p; j += kNW) {
+        c64* q = Q + static_cast<size_t>(j) * m;
+        for (int r = lane; r < m; r += 32) q[r] = mk(r == j ? 1.0 : 0.0, 0.0);
+        __syncwarp();
+        for (int k = j; k >= 0; --k) {
+            const c64* v = A + static_cast<size_t>(k) * m;
+            c64 w = mk(0.0, 0.0);
+            for (int r = k + lane; r < m; r += 32) cmac_conj(w, v[r], q[r]);
+            w = warp_sum_c(w);
+            const c64 tw = mk(tau[k] * w.re, tau[k] * w.im);
+            for (int r = k + lane; r < m; r += 32) {
+                const c64 vr = v[r];
+                q[r].re -= vr.re * tw.re - vr.im * tw.im;
+                q[r].im -= vr.re * tw.im + vr.im * tw.re;
+            }
+            __syncwarp();
+        }
+        if (MODE == 0) {
+            cplx<T>* vo = Vout + static_cast<size_t>(f) * m * p + static_cast<size_t>(j) * m;
+            for (int r = lane; r < m; r += 32) vo[r] = mk<T>(static_cast<T>(q[r].re), static_cast<T>(q[r].im));
+        }
+    }
+    if (MODE == 1) {
+        // Rt[:, perm[j]] = R[:, j]  (C = Q R P^T), column-major p x p
+        c64* Rf = Rt + static_cast<size_t>(f) * p * p;
+        for (int e = threadIdx.x; e < p * p; e += kNT) {
+            const int i = e % p, j = e / p;
+            c64 val = mk(0.0, 0.0);
+            if (i == j) val = rdiag[i];
+            else if (j > i) val = A[static_cast<size_t>(j) * m + i];
+            Rf[static_cast<size_t>(perm[j]) * p + i] = val;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ one-sided Jacobi SVD
+// n x n complex fp64, column-major in smem (a[c*n + r]); v accumulates right rotations.
+// Round-robin (circle) ordering, one warp per column pair. Returns false on sweep cap.
+__device__ bool block_jacobi_svd(c64* a, c64* v, int n, double* sig, int* order) {
+    __shared__ int s_rot;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) v[e] = mk((e % n) == (e / n) ? 1.0 : 0.0, 0.0);
+    const int np = (n + 1) & ~1;
+    bool converged = false;
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        if (threadIdx.x == 0) s_rot = 0;
+        __syncthreads();
+        for (int rnd = 0; rnd < np - 1; ++rnd) {
+            for (int idx = warp; idx < np / 2; idx += blockDim.x / 32) {
+                int i, j;
+                if (idx == 0) {
+                    i = rnd;
+                    j = np - 1;
+                } else {
+                    i = (rnd + idx) % (np - 1);
+                    j = (rnd - idx + (np - 1)) % (np - 1);
+                }
+                if (i > j) {
+                    const int t = i;
+                    i = j;
+                    j = t;
+                }
+                if (j >= n) continue;
+                c64* ai = a + i * n;
+                c64* aj = a + j * n;
+                double al = 0.0, be = 0.0;
+                c64 ga = mk(0.0, 0.0);
+                for (int r = lane; r < n; r += 32) {
+                    al += norm2(ai[r]);
+                    be += norm2(aj[r]);
+                    cmac_conj(ga, ai[r], aj[r]);
+                }
+                al = warp_sum(al);
+                be = warp_sum(be);
+                ga = warp_sum_c(ga);
+                const double g = sqrt(norm2(ga));
+                if (g == 0.0 || g <= 1e-15 * sqrt(al * be)) continue;
+                const double zeta = (be - al) / (2.0 * g);
+                const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double c = 1.0 / sqrt(1.0 + t * t);
+                const double s = c * t;
+                const c64 e = mk(ga.re / g, ga.im / g);  // e^{i phi}
+                // a_i' = c a_i - s e^{-i phi} a_j ;  a_j' = s e^{i phi} a_i + c a_j
+                for (int r = lane; r < n; r += 32) {
+                    const c64 x = ai[r], y = aj[r];
+                    const c64 ey = mk(e.re * y.re + e.im * y.im, e.re * y.im - e.im * y.re);  // conj(e) y
+                    const c64 ex = mk(e.re * x.re - e.im * x.im, e.re * x.im + e.im * x.re);  // e x
+                    ai[r] = mk(c * x.re - s * ey.re, c * x.im - s * ey.im);
+                    aj[r] = mk(s * ex.re + c * y.re, s * ex.im + c * y.im);
+                }
+                c64* vi = v + i * n;
+                c64* vj = v + j * n;
+                for (int r = lane; r < n; r += 32) {
+                    const c64 x = vi[r], y = vj[r];
+                    const c64 ey = mk(e.re * y.re + e.im * y.im, e.re * y.im - e.im * y.re);
+                    const c64 ex = mk(e.re * x.re - e.im * x.im, e.re * x.im + e.im * x.re);
+                    vi[r] = mk(c * x.re - s * ey.re, c * x.im - s * ey.im);
+                    vj[r] = mk(s * ex.re + c * y.re, s * ex.im + c * y.im);
+                }
+                if (lane == 0) s_rot = 1;
+            }
+            __syncthreads();
+        }
+        if (s_rot == 0) {
+            converged = true;
+            break;
+        }
+    }
+    // singular values and descending order (stable: ties keep the lower index)
+    for (int c = warp; c < n; c += blockDim.x / 32) {
+        double s = 0.0;
+        for (int r = lane; r < n; r += 32) s += norm2(a[c * n + r]);
+        s = warp_sum(s);
+        if (lane == 0) sig[c] = sqrt(s);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int c = 0; c < n; ++c) order[c] = c;
+        for (int x = 0; x < n; ++x) {
+            int best = x;
+            for (int y = x + 1; y < n; ++y)
+                if (sig[order[y]] > sig[order[best]]) best = y;
+            const int t = order[x];
+            order[x] = order[best];
+            order[best] = t;
+        }
+    }
+    __syncthreads();
+    return converged;
+}
+
+// ------------------------------------------------------------------ Nystrom tail
+// MODE_FAST2: H = V^H C (V, C: the last power-iteration sketch); MODE_FAST1: H from k_gather.
+// W = pinv(H)  (cutoff p*eps_T*sigma1)            R/src/linalg.cpp:143-163
+// B' = Rt W Rt^H; SVD(B') = Ub Sb ..;  U = Q Ub(:,1:K); lambda = clamp(Sb(1:K))
+//                                                  R/src/estimators.cpp:37-50, :25-31
+// Output basis column-major K x M fp64, eigenvalues K fp64.
+template <typename T, bool FAST2>
+__global__ void __launch_bounds__(kNT) k_nystrom(const cplx<T>* __restrict__ V, const cplx<T>* __restrict__ C,
+                                                  const c64* __restrict__ Hin, const c64* __restrict__ work,
+                                                  const c64* __restrict__ Rt, c64* __restrict__ basis,
+                                                  double* __restrict__ eig, int32_t* __restrict__ status,
+                                                  const int32_t* __restrict__ fmap, int m, int p, int k) {
+    extern __shared__ uint8_t dsm[];
+    c64* sa = reinterpret_cast<c64*>(dsm);  // p x p
+    c64* sv = sa + p * p;                   // p x p
+    c64* sw = sv + p * p;                   // p x p (W)
+    c64* st = sv;                           // p x p temp (aliases sv once W is formed)
+    double* sig = reinterpret_cast<double*>(sw + p * p);
+    int* order = reinterpret_cast<int*>(sig + p);
+    const int f = frame_of_x(fmap);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double eps = eps_of<T>::value;
+
+    // H (column-major)
+    if (FAST2) {
+        const cplx<T>* Vf = V + static_cast<size_t>(f) * m * p;
+        const cplx<T>* Cf = C + static_cast<size_t>(f) * m * p;
+        for (int e = warp; e < p * p; e += kNW) {
+            const int i = e % p, j = e / p;
+            c64 s = mk(0.0, 0.0);
+            for (int r = lane; r < m; r += 32)
+                cmac_conj(s, to64(Vf[static_cast<size_t>(i) * m + r]), to64(Cf[static_cast<size_t>(j) * m + r]));
+            s = warp_sum_c(s);
+            if (lane == 0) sa[j * p + i] = s;
+        }
+    } else {
+        const c64* Hf = Hin + static_cast<size_t>(f) * p * p;
+        for (int e = threadIdx.x; e < p * p; e += kNT) sa[e] = Hf[e];
+    }
+    __syncthreads();
+    bool ok = block_jacobi_svd(sa, sv, p, sig, order);
+    // W = V diag(1/s) U^H, U_c = a_c / s_c
+    const double s1 = sig[order[0]];
+    const double cutoff = static_cast<double>(p) * eps * s1;
+    for (int e = threadIdx.x; e < p * p; e += kNT) {
+        const int i = e % p, j = e / p;  // W(i, j)
+        c64 acc = mk(0.0, 0.0);
+        if (s1 > 0.0) {
+            for (int c = 0; c < p; ++c) {
+                const double s = sig[c];
+                if (s > cutoff) {
+                    // v(i,c) * conj(a(j,c)) / s^2   (u = a / s)
+                    const c64 vi = sv[c * p + i];
+                    const c64 aj = sa[c * p + j];
+                    const double w = 1.0 / (s * s);
+                    acc.re += w * (vi.re * aj.re + vi.im * aj.im);
+                    acc.im += w * (vi.im * aj.re - vi.re * aj.im);
+                }
+            }
+        }
+        sw[j * p + i] = acc;
+    }
+    __syncthreads();
+    // T = Rt W ; B' = T Rt^H
+    const c64* Rf = Rt + static_cast<size_t>(f) * p * p;
+    for (int e = threadIdx.x; e < p * p; e += kNT) {
+        const int i = e % p, j = e / p;
+        c64 acc = mk(0.0, 0.0);
+        for (int c = 0; c < p; ++c) cmac(acc, Rf[c * p + i], sw[j * p + c]);
+        st[j * p + i] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < p * p; e += kNT) {
+        const int i = e % p, j = e / p;
+        c64 acc = mk(0.0, 0.0);
+        for (int c = 0; c < p; ++c) cmac(acc, st[c * p + i], conj(Rf[c * p + j]));
+        sa[j * p + i] = acc;
+    }
+    __syncthreads();
+    ok = block_jacobi_svd(sa, sv, p, sig, order) && ok;
+    // basis U[:, kk] = Q * (a[:, order[kk]] / sig)
+    const c64* Qf = work + static_cast<size_t>(f) * 2 * p * m + static_cast<size_t>(p) * m;
+    c64* Bf = basis + static_cast<size_t>(f) * m * k;
+    for (int e = threadIdx.x; e < m * k; e += kNT) {
+        const int kk = e / m, r = e % m;
+        const int c = order[kk];
+        const double s = sig[c];
+        const double inv = s > 0.0 ? 1.0 / s : 0.0;
+        c64 acc = mk(0.0, 0.0);
+        for (int q = 0; q < p; ++q) cmac(acc, Qf[static_cast<size_t>(q) * m + r], sa[c * p + q]);
+        Bf[static_cast<size_t>(kk) * m + r] = mk(acc.re * inv, acc.im * inv);
+    }
+    if (threadIdx.x < k) {
+        double lam = sig[order[threadIdx.x]];
+        if (lam < 0.0 && lam >= -1e-10) lam = 0.0;
+        eig[static_cast<size_t>(f) * k + threadIdx.x] = lam;
+    }
+    if (threadIdx.x == 0 && !ok) atomicOr(&status[f], kFrameNoConv);
+}
+
+}  // namespace sub
+}  // namespace fmk
+
+// ------------------------------------------------------------------ launchers (host)
+using namespace fmk;
+
+template <typename T>
+cudaError_t fm_launch_rmul(const void* R, const void* omega, const void* V, void* C, const int32_t* fmap, int frames,
+                           int m, int p, bool real_rhs, cudaStream_t s) {
+    constexpr int kMaxPC = sizeof(T) == 4 ? 64 : 32;
+    const int slices = (p + kMaxPC - 1) / kMaxPC;
+    dim3 grid((m + sub::kNT - 1) / sub::kNT, frames, slices);
+    auto Rp = static_cast<const cplx<T>*>(R);
+    auto Op = static_cast<const T*>(omega);
+    auto Vp = static_cast<const cplx<T>*>(V);
+    auto Cp = static_cast<cplx<T>*>(C);
+#define FM_RMUL(PC)                                                                                   \
+    if (p <= PC || (PC == kMaxPC)) {                                                                  \
+        if (real_rhs) sub::k_rmul<T, PC, true><<<grid, sub::kNT, 0, s>>>(Rp, Op, Vp, Cp, fmap, m, p);  \
+        else sub::k_rmul<T, PC, false><<<grid, sub::kNT, 0, s>>>(Rp, Op, Vp, Cp, fmap, m, p);         \
+        return cudaGetLastError();                                                                    \
+    }
+    FM_RMUL(8)
+    FM_RMUL(16)
+    FM_RMUL(32)
+    if constexpr (kMaxPC == 64) { FM_RMUL(64) }
+#undef FM_RMUL
+    return cudaErrorInvalidValue;
+}
+
+template <typename T>
+cudaError_t fm_launch_gather(const void* R, const int32_t* idx, void* C, void* H, const int32_t* fmap, int frames,
+                             int m, int p, cudaStream_t s) {
+    sub::k_gather<T><<<frames, sub::kNT, 0, s>>>(static_cast<const cplx<T>*>(R), idx, static_cast<cplx<T>*>(C),
+                                                 static_cast<c64*>(H), fmap, m, p);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t fm_launch_qr(const void* C, void* work, void* Vout, void* Rt, int32_t* status, int32_t* defcol,
+                         const int32_t* fmap, int frames, int m, int p, bool final_mode, cudaStream_t s) {
+    if (p > 64 || p < 1 || m < p) return cudaErrorInvalidValue;
+    if (final_mode)
+        sub::k_qr<T, 1><<<frames, sub::kNT, 0, s>>>(static_cast<const cplx<T>*>(C), static_cast<c64*>(work), nullptr,
+                                                    static_cast<c64*>(Rt), status, defcol, fmap, m, p);
+    else
+        sub::k_qr<T, 0><<<frames, sub::kNT, 0, s>>>(static_cast<const cplx<T>*>(C), static_cast<c64*>(work),
+                                                    static_cast<cplx<T>*>(Vout), nullptr, status, defcol, fmap, m, p);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t fm_launch_nystrom(const void* V, const void* C, const void* H, const void* work, const void* Rt,
+                              void* basis, double* eig, int32_t* status, const int32_t* fmap, int frames, int m,
+                              int p, int k, bool fast2, cudaStream_t s) {
+    const size_t smem = 3 * sizeof(c64) * p * p + sizeof(double) * p + sizeof(int) * p;
+    auto kern = fast2 ? sub::k_nystrom<T, true> : sub::k_nystrom<T, false>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<frames, sub::kNT, smem, s>>>(static_cast<const cplx<T>*>(V), static_cast<const cplx<T>*>(C),
+                                        static_cast<const c64*>(H), static_cast<const c64*>(work),
+                                        static_cast<const c64*>(Rt), static_cast<c64*>(basis), eig, status, fmap, m,
+                                        p, k);
+    return cudaGetLastError();
+}
+
+template cudaError_t fm_launch_rmul<float>(const void*, const void*, const void*, void*, const int32_t*, int, int, int,
+                                           bool, cudaStream_t);
+template cudaError_t fm_launch_rmul<double>(const void*, const void*, const void*, void*, const int32_t*, int, int,
+                                            int, bool, cudaStream_t);
+template cudaError_t fm_launch_gather<float>(const void*, const int32_t*, void*, void*, const int32_t*, int, int, int,
+                                             cudaStream_t);
+template cudaError_t fm_launch_gather<double>(const void*, const int32_t*, void*, void*, const int32_t*, int, int, int,
+                                              cudaStream_t);
+template cudaError_t fm_launch_qr<float>(const void*, void*, void*, void*, int32_t*, int32_t*, const int32_t*, int, int,
+                                         int, bool, cudaStream_t);
+template cudaError_t fm_launch_qr<double>(const void*, void*, void*, void*, int32_t*, int32_t*, const int32_t*, int,
+                                          int, int, bool, cudaStream_t);
+template cudaError_t fm_launch_nystrom<float>(const void*, const void*, const void*, const void*, const void*, void*,
+                                              double*, int32_t*, const int32_t*, int, int, int, int, bool,
+                                              cudaStream_t);
+template cudaError_t fm_launch_nystrom<double>(const void*, const void*, const void*, const void*, const void*, void*,
+                                               double*, int32_t*, const int32_t*, int, int, int, int, bool,
+                                               cudaStream_t);

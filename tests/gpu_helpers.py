@@ -1,0 +1,54 @@
+"""Shared helpers for the GPU parity tests (oracle = checker only)."""
+import numpy as np
+
+
+def plan_for(fm, cfg, frames):
+    sp = cfg.spec
+    return fm.BatchPlan(sp.m, sp.n, sp.k, cfg.method, p=cfg.p, t=cfg.t, grid_size=cfg.grid_size,
+                        min_sep_cells=cfg.min_sep_cells, max_frames=frames)
+
+
+def draws(fm, oracle, cfg, frames):
+    fseeds = [oracle.frame_seed(cfg.base_seed, f) for f in frames]
+    if cfg.method == "fast2":
+        return fm.draw_omega_batch([fm.derive(s, 4) for s in fseeds], cfg.spec.m, cfg.p), None
+    if cfg.method == "fast1":
+        return None, fm.draw_indices_batch([fm.derive(s, 3) for s in fseeds], cfg.spec.m, cfg.p)
+    return None, None
+
+
+def run_gpu(fm, oracle, cfg, x, frames, basis=True, covariance=False):
+    import torch
+    nf = len(frames)
+    plan = plan_for(fm, cfg, nf)
+    om, ix = draws(fm, oracle, cfg, frames)
+    xd = torch.from_numpy(np.ascontiguousarray(x).view(np.float32)).cuda()
+    omd = torch.from_numpy(om).cuda() if om is not None else None
+    ixd = torch.from_numpy(ix).cuda() if ix is not None else None
+    out = plan.outputs(nf, spectrum=True, basis=basis, covariance=covariance)
+    plan.run(nf, xd, omd, ixd, out)
+    torch.cuda.synchronize()
+    res = {k: v.cpu().numpy() for k, v in out.items()}
+    if basis:
+        b = res["basis"]
+        res["basis_c"] = (b[..., 0] + 1j * b[..., 1]).transpose(0, 2, 1)  # [f, M, K]
+    if covariance:
+        c = res["covariance"]
+        res["cov_c"] = c[..., 0] + 1j * c[..., 1]
+    plan.close()
+    return res
+
+
+def compare_frames(oracle, cfg, x, frames, res, grid=None, a_mat=None, db_tol=0.05):
+    grid = grid or oracle.baseline_grid(cfg.grid_size)
+    worst = 0.0
+    mismatched = []
+    for i, f in enumerate(frames):
+        est, p_ref, pk = oracle.run_frame(cfg, x[i], f, grid, a_mat)
+        p_gpu = res["spectrum"][i].astype(np.float64)
+        worst = max(worst, oracle.spectrum_db_error(p_gpu, p_ref))
+        n = int(res["peak_count"][i])
+        cells = [int(c) for c in res["peak_cells"][i][:n]]
+        if cells != pk.cells:
+            mismatched.append((f, cells, pk.cells))
+    return worst, mismatched

@@ -1,0 +1,79 @@
+"""GPU parity of the batched complex64 pipeline against the fp64 oracle.
+
+Gate (BASELINE.json north_star): identical peak grid indices, and pseudo-spectra within
+0.05 dB wherever the oracle spectrum is within 40 dB of its maximum. Covariance parity
+(tensor-core fp16 operands, fp32 accumulation) is checked entrywise against fp64.
+"""
+import numpy as np
+import pytest
+
+from tests.gpu_helpers import compare_frames, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+DB_TOL = 0.05
+
+
+@pytest.fixture(scope="module")
+def cfgs(oracle):
+    return oracle.baseline_configs()
+
+
+def _data(oracle, cfg, frames):
+    x, ang, snr = oracle.generate_batch(cfg.base_seed, frames, cfg.spec)
+    return x
+
+
+@pytest.mark.parametrize("name,frames", [("c1", [0]), ("c2", [0, 1, 2]), ("c4", [0])])
+def test_covariance_tc_vs_fp64(fm, oracle, cfgs, name, frames):
+    cfg = cfgs[name]
+    x = _data(oracle, cfg, frames)
+    res = run_gpu(fm, oracle, cfg, x, frames, basis=False, covariance=True)
+    for i in range(len(frames)):
+        ref = oracle.spatial_covariance(x[i])
+        got = res["cov_c"][i]
+        rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        assert rel < 2e-4, (name, i, rel)
+        assert np.all(np.diag(got).imag == 0.0)
+        assert np.max(np.abs(got - got.conj().T)) <= 1e-6 * np.max(np.abs(ref))
+    assert np.all(res["status"] == 0)
+
+
+@pytest.mark.parametrize("name,frames", [
+    ("c1", [0]),
+    ("c2", list(range(12))),
+    ("c3", list(range(8))),
+    ("c5", list(range(3))),
+])
+def test_pipeline_parity(fm, oracle, cfgs, name, frames):
+    cfg = cfgs[name]
+    x = _data(oracle, cfg, frames)
+    res = run_gpu(fm, oracle, cfg, x, frames)
+    assert np.all(res["status"] == 0), res["status"]
+    worst, mism = compare_frames(oracle, cfg, x, frames, res)
+    assert not mism, mism
+    assert worst <= DB_TOL, worst
+
+
+def test_c4_parity(fm, oracle, cfgs):
+    cfg = cfgs["c4"]
+    frames = [0]
+    x = _data(oracle, cfg, frames)
+    res = run_gpu(fm, oracle, cfg, x, frames)
+    assert np.all(res["status"] == 0), res["status"]
+    worst, mism = compare_frames(oracle, cfg, x, frames, res)
+    assert not mism, mism
+    assert worst <= DB_TOL, worst
+
+
+def test_subspace_close_to_oracle(fm, oracle, cfgs):
+    cfg = cfgs["c2"]
+    frames = [3, 4]
+    x = _data(oracle, cfg, frames)
+    res = run_gpu(fm, oracle, cfg, x, frames)
+    for i, f in enumerate(frames):
+        est, _, _ = oracle.run_frame(cfg, x[i], f)
+        u = res["basis_c"][i]
+        assert np.max(np.abs(u.conj().T @ u - np.eye(cfg.spec.k))) < 1e-12
+        assert oracle.projector_error(u, est.basis) < 1e-4
+        assert np.allclose(res["eigenvalues"][i], est.eigenvalues, rtol=1e-4)
