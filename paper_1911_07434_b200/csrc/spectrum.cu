@@ -24,6 +24,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "fm_common.cuh"
@@ -107,7 +108,7 @@ __device__ void block_peaks(const double* v, int L, int K, int min_sep, int* can
             const int c = cand_cell[i];
             bool clash = false;
             for (int s = 0; s < nsel; ++s)
-                if (abs(c - s_sel[s]) < min_sep) {
+                if (abs(c - s_sel[s]) < min_sep || c == s_sel[s]) {  // each candidate considered once
                     clash = true;
                     break;
                 }
@@ -323,7 +324,7 @@ cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, in
 
 static size_t spectrum_smem(int m, int L) {
     const int cap = spec::cand_cap(L, m);
-    if (cap < 16) return ~size_t(0);
+    if (cap < std::min(L / 2 + 1, 16)) return ~size_t(0);
     return sizeof(double) * L + sizeof(c64) * m + sizeof(int) * ((cap + 1) & ~1) + sizeof(double) * cap + 16;
 }
 
@@ -346,7 +347,7 @@ cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K,
                                  cudaStream_t s) {
     const int cap = spec::cand_cap_values(L);
     const size_t smem = sizeof(double) * L + sizeof(int) * ((cap + 1) & ~1) + sizeof(double) * cap + 16;
-    if (cap < 16 || smem > 227 * 1024 || K > 64) return cudaErrorInvalidValue;
+    if (cap < std::min(L / 2 + 1, 16) || smem > 227 * 1024 || K > 64) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(spec::k_peaks_only, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
