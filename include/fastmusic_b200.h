@@ -123,6 +123,12 @@ fm_status fm_run_batch(fm_plan plan, int64_t frames, const fm_batch_io* io, void
 /* Re-run subspace+spectrum for the listed frames (device int32 list) on the covariance kept
  * from the last fm_run_batch (fast2 redraws with derive(seed, 0xF257 + attempt)). */
 fm_status fm_rerun_frames(fm_plan plan, int64_t count, const int32_t* d_frames, const fm_batch_io* io, void* stream);
+/* Stage timing: when enabled, every fm_run_batch records CUDA events on its stream between
+ * its stages; once the stream is synchronised, fm_plan_stage_times returns the summed
+ * {covariance, subspace, autocorrelation, spectrum+peaks} ms over the batches recorded since
+ * profiling was enabled (or last read), their count in *runs, and restarts the count. */
+fm_status fm_plan_set_profiling(fm_plan plan, int32_t on);
+fm_status fm_plan_stage_times(fm_plan plan, float* ms4, int32_t* runs);
 /* Number of kernel launches one fm_run_batch enqueues. */
 int32_t fm_plan_launches_per_batch(fm_plan plan);
 

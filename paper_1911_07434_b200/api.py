@@ -316,6 +316,17 @@ class BatchPlan:
         _check(LIB.fm_plan_workspace_bytes(self.handle, C.byref(b)))
         return b.value
 
+    def set_profiling(self, on: bool = True):
+        _check(LIB.fm_plan_set_profiling(self.handle, 1 if on else 0))
+
+    def stage_times_ms(self):
+        """Summed {covariance, subspace, autocorr, spectrum_peaks} ms and the number of batches
+        recorded since profiling was enabled / last read (call after synchronising)."""
+        ms = np.zeros(4, np.float32)
+        runs = C.c_int32(0)
+        _check(LIB.fm_plan_stage_times(self.handle, ptr(ms), C.byref(runs)))
+        return dict(zip(("covariance", "subspace", "autocorr", "spectrum_peaks"), ms.astype(float))), runs.value
+
     def launches_per_batch(self) -> int:
         return int(LIB.fm_plan_launches_per_batch(self.handle))
 

@@ -328,6 +328,13 @@ struct fm_plan_s {
     float* omega_pinned = nullptr;
     int32_t* status_pinned = nullptr;
     size_t bytes = 0;
+    // optional per-stage CUDA events (covariance | subspace | autocorr | spectrum+peaks),
+    // one set of 5 per recorded batch (ring of kMaxProf batches), summed by fm_plan_stage_times
+    static constexpr int kMaxProf = 4096;
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev;
+    int prof_runs = 0;
+    int cur = 0;
     std::vector<void*> allocs;
 
     template <typename T>
@@ -349,6 +356,8 @@ struct fm_plan_s {
         cudaGetDevice(&prev);
         cudaSetDevice(device);
         for (void* q : allocs) cudaFree(q);
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
         if (omega_pinned) cudaFreeHost(omega_pinned);
         if (status_pinned) cudaFreeHost(status_pinned);
         cudaSetDevice(prev);
@@ -432,6 +441,31 @@ extern "C" fm_status fm_plan_workspace_bytes(fm_plan plan, int64_t* bytes) {
     return FM_OK;
 }
 
+extern "C" fm_status fm_plan_set_profiling(fm_plan plan, int32_t on) {
+    if (!plan) return fail(FM_EINVAL, "fm_plan_set_profiling: null plan");
+    FM_CUDA_OK(cudaSetDevice(plan->device));
+    plan->profiling = on != 0;
+    plan->prof_runs = 0;
+    return FM_OK;
+}
+
+// Sum over the batches recorded since profiling was (re)enabled; *runs gets their count.
+extern "C" fm_status fm_plan_stage_times(fm_plan plan, float* ms, int32_t* runs) {
+    if (!plan || !ms) return fail(FM_EINVAL, "fm_plan_stage_times: null argument");
+    const int n = std::min(plan->prof_runs, fm_plan_s::kMaxProf);
+    for (int i = 0; i < 4; ++i) ms[i] = 0.f;
+    for (int r = 0; r < n; ++r)
+        for (int i = 0; i < 4; ++i) {
+            float t = 0.f;
+            FM_CUDA_OK(cudaEventElapsedTime(&t, plan->ev[static_cast<size_t>(r) * 5 + i],
+                                            plan->ev[static_cast<size_t>(r) * 5 + i + 1]));
+            ms[i] += t;
+        }
+    if (runs) *runs = n;
+    plan->prof_runs = 0;
+    return FM_OK;
+}
+
 extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
     if (!plan) return 0;
     const int t = plan->d.t;
@@ -440,6 +474,21 @@ extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
     else if (plan->d.method == FM_METHOD_FAST1) n += 3;             // gather, qr final, nystrom
     else n += 1;                                                    // jacobi
     return n;
+}
+
+static void mark(fm_plan pl, int i, cudaStream_t s) {
+    if (!pl->profiling) return;
+    if (i == 0) {
+        pl->cur = pl->prof_runs % fm_plan_s::kMaxProf;
+        const size_t need = static_cast<size_t>(pl->cur + 1) * 5;
+        while (pl->ev.size() < need) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            pl->ev.push_back(e);
+        }
+        pl->prof_runs++;
+    }
+    cudaEventRecord(pl->ev[static_cast<size_t>(pl->cur) * 5 + i], s);
 }
 
 static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io, const float* R, cudaStream_t s) {
@@ -470,10 +519,13 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     } else {
         FM_CUDA_OK(fm_launch_jacobi_eig<float>(R, pl->work, basis, eig, io->status, F, M, K, s));
     }
+    mark(pl, 2, s);
     FM_CUDA_OK(fm_launch_autocorr(basis, pl->t, F, M, K, s));
+    mark(pl, 3, s);
     FM_CUDA_OK(fm_launch_spectrum_peaks(pl->t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, nullptr,
                                         K, static_cast<int>(d.min_sep_cells), io->peak_cells, io->peak_heights,
                                         io->baseline, io->peak_count, io->status, s));
+    mark(pl, 4, s);
     return FM_OK;
 }
 
@@ -494,7 +546,9 @@ extern "C" fm_status fm_run_batch(fm_plan pl, int64_t frames, const fm_batch_io*
     FM_CUDA_OK(cudaSetDevice(pl->device));
     FM_CUDA_OK(cudaMemsetAsync(io->status, 0, sizeof(int32_t) * frames, s));
     float* R = io->covariance ? io->covariance : pl->R;
+    mark(pl, 0, s);
     FM_CUDA_OK(fm_launch_cov_tc(io->x, R, io->status, frames, pl->d.m, pl->d.n, s));
+    mark(pl, 1, s);
     return run_post_cov(pl, frames, io, R, s);
 }
 
