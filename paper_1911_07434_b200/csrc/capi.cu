@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -476,6 +477,20 @@ extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
     return n;
 }
 
+// FM_DEBUG_SYNC=1: synchronise after every launch so a fault is attributed to its kernel.
+static bool debug_sync() {
+    static const bool on = [] {
+        const char* e = std::getenv("FM_DEBUG_SYNC");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+#define FM_LAUNCH(expr)                                                  \
+    do {                                                                 \
+        FM_CUDA_OK(expr);                                                \
+        if (debug_sync()) FM_CUDA_OK(cudaStreamSynchronize(s));          \
+    } while (0)
+
 static void mark(fm_plan pl, int i, cudaStream_t s) {
     if (!pl->profiling) return;
     if (i == 0) {
@@ -500,29 +515,29 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     k_clear_bits<<<(F + 255) / 256, 256, 0, s>>>(io->status, F, FM_FRAME_RANK | FM_FRAME_NOCONV);
     FM_CUDA_OK(cudaGetLastError());
     if (d.method == FM_METHOD_FAST2) {
-        FM_CUDA_OK(fm_launch_rmul<float>(R, io->omega, nullptr, pl->C, nullptr, F, M, P, true, s));
+        FM_LAUNCH(fm_launch_rmul<float>(R, io->omega, nullptr, pl->C, nullptr, F, M, P, true, s));
         for (int it = 0; it < d.t; ++it) {
-            FM_CUDA_OK(fm_launch_qr<float>(pl->C, pl->work, pl->V, nullptr, io->status, nullptr, nullptr, F, M, P,
+            FM_LAUNCH(fm_launch_qr<float>(pl->C, pl->work, pl->V, nullptr, io->status, nullptr, nullptr, F, M, P,
                                            false, s));
-            FM_CUDA_OK(fm_launch_rmul<float>(R, nullptr, pl->V, pl->C, nullptr, F, M, P, false, s));
+            FM_LAUNCH(fm_launch_rmul<float>(R, nullptr, pl->V, pl->C, nullptr, F, M, P, false, s));
         }
-        FM_CUDA_OK(fm_launch_qr<float>(pl->C, pl->work, nullptr, pl->Rt, pl->scratch_status, nullptr, nullptr, F, M,
+        FM_LAUNCH(fm_launch_qr<float>(pl->C, pl->work, nullptr, pl->Rt, pl->scratch_status, nullptr, nullptr, F, M,
                                        P, true, s));
-        FM_CUDA_OK(fm_launch_nystrom<float>(pl->V, pl->C, nullptr, pl->work, pl->Rt, basis, eig, io->status, nullptr,
+        FM_LAUNCH(fm_launch_nystrom<float>(pl->V, pl->C, nullptr, pl->work, pl->Rt, basis, eig, io->status, nullptr,
                                             F, M, P, K, true, s));
     } else if (d.method == FM_METHOD_FAST1) {
-        FM_CUDA_OK(fm_launch_gather<float>(R, io->indices, pl->C, pl->H, nullptr, F, M, P, s));
-        FM_CUDA_OK(fm_launch_qr<float>(pl->C, pl->work, nullptr, pl->Rt, pl->scratch_status, nullptr, nullptr, F, M,
+        FM_LAUNCH(fm_launch_gather<float>(R, io->indices, pl->C, pl->H, nullptr, F, M, P, s));
+        FM_LAUNCH(fm_launch_qr<float>(pl->C, pl->work, nullptr, pl->Rt, pl->scratch_status, nullptr, nullptr, F, M,
                                        P, true, s));
-        FM_CUDA_OK(fm_launch_nystrom<float>(nullptr, nullptr, pl->H, pl->work, pl->Rt, basis, eig, io->status,
+        FM_LAUNCH(fm_launch_nystrom<float>(nullptr, nullptr, pl->H, pl->work, pl->Rt, basis, eig, io->status,
                                             nullptr, F, M, P, K, false, s));
     } else {
-        FM_CUDA_OK(fm_launch_jacobi_eig<float>(R, pl->work, basis, eig, io->status, F, M, K, s));
+        FM_LAUNCH(fm_launch_jacobi_eig<float>(R, pl->work, basis, eig, io->status, F, M, K, s));
     }
     mark(pl, 2, s);
-    FM_CUDA_OK(fm_launch_autocorr(basis, pl->t, F, M, K, s));
+    FM_LAUNCH(fm_launch_autocorr(basis, pl->t, F, M, K, s));
     mark(pl, 3, s);
-    FM_CUDA_OK(fm_launch_spectrum_peaks(pl->t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, nullptr,
+    FM_LAUNCH(fm_launch_spectrum_peaks(pl->t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, nullptr,
                                         K, static_cast<int>(d.min_sep_cells), io->peak_cells, io->peak_heights,
                                         io->baseline, io->peak_count, io->status, s));
     mark(pl, 4, s);
@@ -547,7 +562,7 @@ extern "C" fm_status fm_run_batch(fm_plan pl, int64_t frames, const fm_batch_io*
     FM_CUDA_OK(cudaMemsetAsync(io->status, 0, sizeof(int32_t) * frames, s));
     float* R = io->covariance ? io->covariance : pl->R;
     mark(pl, 0, s);
-    FM_CUDA_OK(fm_launch_cov_tc(io->x, R, io->status, frames, pl->d.m, pl->d.n, s));
+    FM_LAUNCH(fm_launch_cov_tc(io->x, R, io->status, frames, pl->d.m, pl->d.n, s));
     mark(pl, 1, s);
     return run_post_cov(pl, frames, io, R, s);
 }

@@ -351,7 +351,9 @@ __device__ bool block_jacobi_svd(c64* a, c64* v, int n, double* sig, int* order)
             }
             __syncthreads();
         }
-        if (s_rot == 0) {
+        const bool done = (s_rot == 0);
+        __syncthreads();  // every warp has read s_rot before thread 0 resets it next sweep
+        if (done) {
             converged = true;
             break;
         }
