@@ -34,6 +34,19 @@ cudaError_t fm_launch_qr(const void*, void*, void*, void*, int32_t*, int32_t*, c
 template <typename T>
 cudaError_t fm_launch_nystrom(const void*, const void*, const void*, const void*, const void*, void*, double*,
                               int32_t*, const int32_t*, int, int, int, int, bool, cudaStream_t);
+cudaError_t fm_launch_cholqr(const void* C, void* work, void* Vout, void* Rt, int32_t* status, const int32_t* fmap,
+                             int frames, int m, int p, bool final_mode, const void* Vin, void* Hout, cudaStream_t s);
+template <typename T>
+cudaError_t fm_launch_nystrom_warp(const void* H, const void* work, const void* Rt, void* basis, double* eig,
+                                   int32_t* status, int frames, int m, int p, int k, cudaStream_t s);
+cudaError_t fm_launch_cholqr_warp(const void* C, void* work, void* Vout, void* Rt, void* Hout, const void* Vin,
+                                  int32_t* status, int frames, int m, int p, bool final_mode, cudaStream_t s);
+cudaError_t fm_launch_nystrom_warp2(const void* H, const void* work, const void* Rt, void* basis, double* eig,
+                                    int32_t* status, int frames, int m, int p, int k, cudaStream_t s);
+cudaError_t fm_launch_orth_tiled(const void* C, void* Vout, int32_t* status, int frames, int m, int p,
+                                 cudaStream_t s);
+cudaError_t fm_launch_final_tiled(const void* C, const void* V, const void* H, void* basis, double* eig,
+                                  int32_t* status, int frames, int m, int p, int k, cudaStream_t s);
 cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, int k, cudaStream_t s);
 cudaError_t fm_launch_spectrum_peaks(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
                                      double* spec64, int K, int min_sep, int32_t* cells, double* heights,
@@ -411,7 +424,7 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
     const size_t work_elems = desc->method == FM_METHOD_EXACT ? B * MP * MP * 2 : B * 2 * P * M * 2;
     chk(pl->get(&pl->work, work_elems));
     chk(pl->get(&pl->Rt, B * P * P * 2));
-    chk(pl->get(&pl->H, desc->method == FM_METHOD_FAST1 ? B * P * P * 2 : 0));
+    chk(pl->get(&pl->H, B * P * P * 2));
     chk(pl->get(&pl->basis, B * K * M * 2));
     chk(pl->get(&pl->eig, B * K));
     chk(pl->get(&pl->t, B * M * 2));
@@ -514,23 +527,50 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     double* eig = io->eigenvalues ? io->eigenvalues : pl->eig;
     k_clear_bits<<<(F + 255) / 256, 256, 0, s>>>(io->status, F, FM_FRAME_RANK | FM_FRAME_NOCONV);
     FM_CUDA_OK(cudaGetLastError());
+    const bool warp_path = P <= 32;  // block-per-frame small-matrix kernels (smallmat.cu)
+    const bool tiled = P <= 32 && (P % 4) == 0;  // register-tiled Gram + fused final stage
+    auto orth = [&](bool final_mode, const void* vin) -> fm_status {
+        if (tiled && !final_mode) {
+            FM_LAUNCH(fm_launch_orth_tiled(pl->C, pl->V, io->status, F, M, P, s));
+            return FM_OK;
+        }
+        if (warp_path)
+            FM_LAUNCH(fm_launch_cholqr_warp(pl->C, pl->work, final_mode ? nullptr : pl->V, pl->Rt, pl->H, vin,
+                                            final_mode ? pl->scratch_status : io->status, F, M, P, final_mode, s));
+        else
+            FM_LAUNCH(fm_launch_cholqr(pl->C, pl->work, final_mode ? nullptr : pl->V, final_mode ? pl->Rt : nullptr,
+                                       final_mode ? pl->scratch_status : io->status, nullptr, F, M, P, final_mode,
+                                       vin, pl->H, s));
+        return FM_OK;
+    };
+    auto nystrom = [&]() -> fm_status {
+        if (warp_path)
+            FM_LAUNCH(fm_launch_nystrom_warp2(pl->H, pl->work, pl->Rt, basis, eig, io->status, F, M, P, K, s));
+        else
+            FM_LAUNCH(fm_launch_nystrom_warp<float>(pl->H, pl->work, pl->Rt, basis, eig, io->status, F, M, P, K, s));
+        return FM_OK;
+    };
+    fm_status st = FM_OK;
     if (d.method == FM_METHOD_FAST2) {
         FM_LAUNCH(fm_launch_rmul<float>(R, io->omega, nullptr, pl->C, nullptr, F, M, P, true, s));
         for (int it = 0; it < d.t; ++it) {
-            FM_LAUNCH(fm_launch_qr<float>(pl->C, pl->work, pl->V, nullptr, io->status, nullptr, nullptr, F, M, P,
-                                           false, s));
+            if ((st = orth(false, nullptr)) != FM_OK) return st;
             FM_LAUNCH(fm_launch_rmul<float>(R, nullptr, pl->V, pl->C, nullptr, F, M, P, false, s));
         }
-        FM_LAUNCH(fm_launch_qr<float>(pl->C, pl->work, nullptr, pl->Rt, pl->scratch_status, nullptr, nullptr, F, M,
-                                       P, true, s));
-        FM_LAUNCH(fm_launch_nystrom<float>(pl->V, pl->C, nullptr, pl->work, pl->Rt, basis, eig, io->status, nullptr,
-                                            F, M, P, K, true, s));
+        if (tiled) {
+            FM_LAUNCH(fm_launch_final_tiled(pl->C, pl->V, nullptr, basis, eig, io->status, F, M, P, K, s));
+        } else {
+            if ((st = orth(true, pl->V)) != FM_OK) return st;
+            if ((st = nystrom()) != FM_OK) return st;
+        }
     } else if (d.method == FM_METHOD_FAST1) {
         FM_LAUNCH(fm_launch_gather<float>(R, io->indices, pl->C, pl->H, nullptr, F, M, P, s));
-        FM_LAUNCH(fm_launch_qr<float>(pl->C, pl->work, nullptr, pl->Rt, pl->scratch_status, nullptr, nullptr, F, M,
-                                       P, true, s));
-        FM_LAUNCH(fm_launch_nystrom<float>(nullptr, nullptr, pl->H, pl->work, pl->Rt, basis, eig, io->status,
-                                            nullptr, F, M, P, K, false, s));
+        if (tiled) {
+            FM_LAUNCH(fm_launch_final_tiled(pl->C, nullptr, pl->H, basis, eig, io->status, F, M, P, K, s));
+        } else {
+            if ((st = orth(true, nullptr)) != FM_OK) return st;
+            if ((st = nystrom()) != FM_OK) return st;
+        }
     } else {
         FM_LAUNCH(fm_launch_jacobi_eig<float>(R, pl->work, basis, eig, io->status, F, M, K, s));
     }

@@ -1,0 +1,991 @@
+// K3/K4 for the batched complex64 path — block-per-frame small-matrix kernels (p <= 32)
+// designed around short critical paths: every phase is spread over the whole CTA.
+//
+// k_cholqr_blk (R/src/linalg.cpp:127-141 qr_orthonormal; Eigen ColPivHouseholderQR rank rule)
+//   G = C^H C in fp64 (products of fp32 data are exact in fp64) -> masked outer-product
+//   pivoted Cholesky over all threads (pivot = largest remaining Schur diagonal = Eigen's
+//   largest remaining column norm, so |R_kk| = sqrt(pivot_k) is the pivoted-QR diagonal in
+//   exact arithmetic) -> rows of C P R^-1 by forward substitution (thread per row).
+//   MODE 0: V (complex64) for the power iteration + rank flag (fp32 epsilon).
+//   MODE 1: CholQR2 -> Q (fp64) + Rt = Q^H C + H = V^H C for the Nystrom tail.
+// k_nystrom_blk (R/src/estimators.cpp:37-50 rank_restricted_subspace + :25-31 clamp;
+//                R/src/linalg.cpp:143-163 pseudo_inverse)
+//   H (Hermitian PD) = L_H L_H^H, so W = pinv(H) = L_H^-H L_H^-1 and B' = Rt W Rt^H = Y Y^H with
+//   Y = Rt L_H^-H. The top-K eigenvectors of B' are the top-K left singular vectors of Y:
+//   one-sided Jacobi on Y's columns (one warp per column pair per round), eigenvalues = s^2.
+//   B' is never formed. A Cholesky pivot below p*eps_32*max is flagged (degenerate pinv).
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "fm_common.cuh"
+
+namespace fmk {
+namespace smb {
+
+constexpr int kNT = 256;
+constexpr int kNW = kNT / 32;
+constexpr int kRC = 64;   // rows per staged Gram chunk
+constexpr int kRCP = 65;  // padded column stride (conflict-free 16-B column reads)
+__device__ int* g_phase_dbg = nullptr;
+
+// G(i, j) = sum_r conj(X_i[r]) Y_j[r] over column-major p x m operands. Threads own entries
+// (HERM: upper triangle, mirrored); rows staged kRC at a time in padded shared memory and
+// each entry's sum split over two row halves for shorter FMA chains.
+template <bool HERM, typename XT, typename YT>
+__device__ void block_gram(const XT* __restrict__ X, const YT* __restrict__ Y, int m, int p, c64* chunk, c64* G,
+                           c64* part) {
+    const int ne = HERM ? p * (p + 1) / 2 : p * p;
+    const int slots = 2 * ne;                 // (entry, half)
+    const int per = (slots + kNT - 1) / kNT;  // <= 8 for p <= 32
+    c64 acc[8];
+    int ei[8], ej[8], eh[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        acc[q] = mk(0.0, 0.0);
+        const int sl = threadIdx.x + kNT * q;
+        int e = sl >> 1, i = 0, j = 0;
+        if (q < per && sl < slots) {
+            if (HERM) {
+                int rem = e;
+                while (rem >= p - i) { rem -= p - i; ++i; }
+                j = i + rem;
+            } else {
+                i = e % p;
+                j = e / p;
+            }
+        }
+        ei[q] = i;
+        ej[q] = j;
+        eh[q] = sl & 1;
+    }
+    c64* cy = HERM ? chunk : chunk + p * kRCP;
+    long long tst = 0, tcp = 0;
+    for (int r0 = 0; r0 < m; r0 += kRC) {
+        const int rn = min(kRC, m - r0);
+        __syncthreads();
+        long long ta = clock64();
+        for (int e = threadIdx.x; e < p * kRC; e += kNT) {
+            const int c = e / kRC, r = e % kRC;
+            chunk[c * kRCP + r] = r < rn ? to64(X[static_cast<size_t>(c) * m + r0 + r]) : mk(0.0, 0.0);
+            if (!HERM) cy[c * kRCP + r] = r < rn ? to64(Y[static_cast<size_t>(c) * m + r0 + r]) : mk(0.0, 0.0);
+        }
+        __syncthreads();
+        long long tb = clock64();
+        tst += tb - ta;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (q < per && threadIdx.x + kNT * q < slots) {
+                const c64* xi = chunk + ei[q] * kRCP + eh[q] * (kRC / 2);
+                const c64* yj = cy + ej[q] * kRCP + eh[q] * (kRC / 2);
+                c64 a = acc[q];
+#pragma unroll 8
+                for (int r = 0; r < kRC / 2; ++r) cmac_conj(a, xi[r], yj[r]);
+                acc[q] = a;
+            }
+        }
+        __syncthreads();
+        tcp += clock64() - tb;
+    }
+    (void)tst;
+    (void)tcp;
+    // combine halves through `part`, write G (column-major)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int sl = threadIdx.x + kNT * q;
+        if (q < per && sl < slots && eh[q] == 1) part[sl >> 1] = acc[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int sl = threadIdx.x + kNT * q;
+        if (q < per && sl < slots && eh[q] == 0) {
+            const c64 v = acc[q] + part[sl >> 1];
+            G[ej[q] * p + ei[q]] = v;
+            if (HERM) G[ei[q] * p + ej[q]] = conj(v);
+        }
+    }
+    __syncthreads();
+}
+
+// Masked outer-product Cholesky of the Hermitian p x p A (column-major, destroyed), all threads.
+// perm[k] = original index eliminated at step k (k if !pivot), d[k] its Schur pivot,
+// L[k * p + i] = l_k(i) by ORIGINAL row index i (zero for rows eliminated earlier).
+__device__ void block_chol(c64* A, int p, bool pivot, int* perm, double* d, c64* L, int* done, double* s_inv) {
+    for (int i = threadIdx.x; i < p; i += kNT) done[i] = 0;
+    __syncthreads();
+    for (int k = 0; k < p; ++k) {
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            int piv = k;
+            if (pivot) {
+                double best = -1.0;
+                int bi = p;
+                for (int j = lane; j < p; j += 32) {
+                    if (done[j]) continue;
+                    const double v = A[j * p + j].re;
+                    if (v > best || (v == best && j < bi)) { best = v; bi = j; }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+                }
+                piv = bi;
+            }
+            if (lane == 0) {
+                const double dk = A[piv * p + piv].re;
+                perm[k] = piv;
+                d[k] = dk;
+                done[piv] = 1;
+                *s_inv = dk > 0.0 ? 1.0 / sqrt(dk) : 0.0;
+            }
+        }
+        __syncthreads();
+        const int piv = perm[k];
+        const double inv = *s_inv;
+        for (int i = threadIdx.x; i < p; i += kNT) {
+            // l_k(i) = A(i, piv) / sqrt(A(piv, piv)) for rows not yet eliminated (incl. piv)
+            const bool live = !done[i] || i == piv;
+            const c64 a = A[piv * p + i];
+            L[k * p + i] = live ? mk(a.re * inv, a.im * inv) : mk(0.0, 0.0);
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < p * p; e += kNT) {
+            const int i = e % p, j = e / p;
+            if (done[i] || done[j]) continue;
+            const c64 li = L[k * p + i], lj = L[k * p + j];
+            c64 a = A[e];
+            a.re -= li.re * lj.re + li.im * lj.im;  // li * conj(lj)
+            a.im -= li.im * lj.re - li.re * lj.im;
+            A[e] = a;
+        }
+        __syncthreads();
+    }
+}
+
+// Out[j][r] = v_j with v L_p^H = x, x_a = X[perm[a]][r], L_p(j, a) = L[a * p + perm[j]]
+// (forward substitution: v_j = (x_j - sum_{a<j} v_a conj(L_p(j,a))) / L_p(j,j)). Thread per row.
+template <int PC, typename XT, typename OT>
+__device__ void rows_solve(const XT* __restrict__ X, const int* perm, const c64* L, int m, int p, OT* __restrict__ Out) {
+    for (int r = threadIdx.x; r < m; r += kNT) {
+        c64 v[PC];
+#pragma unroll
+        for (int j = 0; j < PC; ++j) {
+            if (j < p) {
+                const int pj = perm[j];
+                c64 x = to64(X[static_cast<size_t>(pj) * m + r]);
+#pragma unroll
+                for (int a = 0; a < PC; ++a) {
+                    if (a < j) {
+                        const c64 l = L[a * p + pj];
+                        x.re -= v[a].re * l.re + v[a].im * l.im;
+                        x.im -= v[a].im * l.re - v[a].re * l.im;
+                    }
+                }
+                const double ljj = L[j * p + pj].re;
+                const double inv = ljj > 0.0 ? 1.0 / ljj : 0.0;
+                v[j] = mk(x.re * inv, x.im * inv);
+                OT o;
+                o.re = static_cast<decltype(o.re)>(v[j].re);
+                o.im = static_cast<decltype(o.im)>(v[j].im);
+                Out[static_cast<size_t>(j) * m + r] = o;
+            }
+        }
+    }
+}
+
+struct CholSmem {
+    c64* G;      // p x p
+    c64* L;      // p x p
+    c64* chunk;  // 2 x p x kRCP
+    c64* part;   // p x p
+};
+
+template <int PC>
+__host__ __device__ constexpr size_t chol_smem_bytes() {
+    return sizeof(c64) * (3 * PC * PC + 2 * PC * kRCP);
+}
+
+__device__ __forceinline__ CholSmem carve(uint8_t* dsm, int p) {
+    CholSmem s;
+    s.G = reinterpret_cast<c64*>(dsm);
+    s.L = s.G + p * p;
+    s.part = s.L + p * p;
+    s.chunk = s.part + p * p;
+    return s;
+}
+
+template <int PC, int MODE>
+__global__ void __launch_bounds__(kNT) k_cholqr_blk(const c32* __restrict__ Cin, c64* __restrict__ work,
+                                                    c32* __restrict__ Vout, c64* __restrict__ Rt,
+                                                    c64* __restrict__ Hout, const c32* __restrict__ Vin,
+                                                    int32_t* __restrict__ status, int m, int p) {
+    extern __shared__ uint8_t dsm[];
+    __shared__ int perm[32], done[32];
+    __shared__ double d[32];
+    __shared__ double s_inv;
+    const CholSmem sm = carve(dsm, p);
+    const int f = blockIdx.x;
+    const c32* Cf = Cin + static_cast<size_t>(f) * m * p;
+    long long t0 = clock64();
+    block_gram<true>(Cf, Cf, m, p, sm.chunk, sm.G, sm.part);
+    long long t1 = clock64();
+    block_chol(sm.G, p, true, perm, d, sm.L, done, &s_inv);
+    long long t2 = clock64();
+    if (MODE == 0) {
+        if (threadIdx.x == 0) {
+            // Eigen ColPivHouseholderQR::rank(): nonzero-pivot cut + |R_kk| > eps * p * maxpivot
+            const double eps = eps_of<float>::value;
+            const double thr_helper = fmax(d[0], 0.0) * eps * eps / static_cast<double>(m);
+            int nonzero = p;
+            double maxpivot = 0.0;
+            for (int k = 0; k < p; ++k) {
+                if (nonzero == p && d[k] < thr_helper * static_cast<double>(m - k)) nonzero = k;
+                maxpivot = fmax(maxpivot, sqrt(fmax(d[k], 0.0)));
+            }
+            const double thr = maxpivot * eps * static_cast<double>(p);
+            int rank = 0;
+            for (int k = 0; k < nonzero; ++k) rank += sqrt(fmax(d[k], 0.0)) > thr ? 1 : 0;
+            if (rank < p) atomicOr(&status[f], kFrameRank);
+        }
+        rows_solve<PC>(Cf, perm, sm.L, m, p, Vout + static_cast<size_t>(f) * m * p);
+        __syncthreads();
+        long long t3 = clock64();
+        if (threadIdx.x == 0 && g_phase_dbg) {
+            g_phase_dbg[f * 4 + 0] = static_cast<int>(t1 - t0);
+            g_phase_dbg[f * 4 + 1] = static_cast<int>(t2 - t1);
+            g_phase_dbg[f * 4 + 2] = static_cast<int>(t3 - t2);
+        }
+        return;
+    }
+    c64* Q1 = work + static_cast<size_t>(f) * 2 * p * m;
+    c64* Q = Q1 + static_cast<size_t>(p) * m;
+    rows_solve<PC>(Cf, perm, sm.L, m, p, Q1);
+    __syncthreads();
+    block_gram<true>(static_cast<const c64*>(Q1), static_cast<const c64*>(Q1), m, p, sm.chunk, sm.G, sm.part);
+    block_chol(sm.G, p, false, perm, d, sm.L, done, &s_inv);
+    rows_solve<PC>(static_cast<const c64*>(Q1), perm, sm.L, m, p, Q);
+    __syncthreads();
+    block_gram<false>(static_cast<const c64*>(Q), Cf, m, p, sm.chunk, sm.G, sm.part);
+    c64* Rf = Rt + static_cast<size_t>(f) * p * p;
+    for (int e = threadIdx.x; e < p * p; e += kNT) Rf[e] = sm.G[e];
+    if (Vin) {
+        block_gram<false>(Vin + static_cast<size_t>(f) * m * p, Cf, m, p, sm.chunk, sm.G, sm.part);
+        c64* Hf = Hout + static_cast<size_t>(f) * p * p;
+        for (int e = threadIdx.x; e < p * p; e += kNT) Hf[e] = sm.G[e];
+    }
+}
+
+// ------------------------------------------------------------------ single-warp p x p kernels
+// Same contract as block_chol, executed by one warp with __syncwarp only (called by warp 0).
+__device__ void warp_chol(c64* A, int p, bool pivot, int* perm, double* d, c64* L, int* done) {
+    const int lane = threadIdx.x & 31;
+    for (int i = lane; i < p; i += 32) done[i] = 0;
+    __syncwarp();
+    for (int k = 0; k < p; ++k) {
+        int piv = k;
+        if (pivot) {
+            double best = -1.0;
+            int bi = p;
+            for (int j = lane; j < p; j += 32) {
+                if (done[j]) continue;
+                const double v = A[j * p + j].re;
+                if (v > best || (v == best && j < bi)) { best = v; bi = j; }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            piv = bi;
+        }
+        const double dk = A[piv * p + piv].re;
+        const double inv = dk > 0.0 ? rsqrt(dk) : 0.0;
+        __syncwarp();
+        if (lane == 0) {
+            perm[k] = piv;
+            d[k] = dk;
+            done[piv] = 1;
+        }
+        __syncwarp();
+        for (int i = lane; i < p; i += 32) {
+            const bool live = !done[i] || i == piv;
+            const c64 a = A[piv * p + i];
+            L[k * p + i] = live ? mk(a.re * inv, a.im * inv) : mk(0.0, 0.0);
+        }
+        __syncwarp();
+        for (int e = lane; e < p * p; e += 32) {
+            const int i = e % p, j = e / p;
+            if (done[i] || done[j]) continue;
+            const c64 li = L[k * p + i], lj = L[k * p + j];
+            c64 a = A[e];
+            a.re -= li.re * lj.re + li.im * lj.im;
+            a.im -= li.im * lj.re - li.re * lj.im;
+            A[e] = a;
+        }
+        __syncwarp();
+    }
+}
+
+// Cyclic two-sided Jacobi eigensolver for the Hermitian n x n A (column-major, shared; n <= 32),
+// one warp, parallel (circle) ordering: the n/2 rotations of a round are disjoint and commute,
+// so all column rotations (A and Z) are applied, then all row rotations. Rotation parameters
+// come from three entries (no reductions). On return diag(A) holds the eigenvalues and Z the
+// eigenvectors (columns). prm: 4 * 32 doubles of scratch. Returns sweeps (0 = cap hit).
+__device__ int warp_jacobi_herm(c64* A, c64* Z, int n, double* prm) {
+    const int lane = threadIdx.x & 31;
+    for (int e = lane; e < n * n; e += 32) Z[e] = mk((e % n) == (e / n) ? 1.0 : 0.0, 0.0);
+    const int np = (n + 1) & ~1, npairs = np / 2;
+    double* pc = prm;            // c
+    double* ps = prm + 32;       // s magnitude (0 = identity)
+    double* per = prm + 64;      // e^{i phi} re
+    double* pei = prm + 96;      // e^{i phi} im
+    double dscale = 0.0;
+    for (int c = 0; c < n; ++c) dscale = fmax(dscale, fabs(A[c * n + c].re));
+    __syncwarp();
+    for (int sweep = 0; sweep < 30; ++sweep) {
+        bool any = false;
+        for (int rnd = 0; rnd < np - 1; ++rnd) {
+            int pi = 0, pj = 0;  // this lane's pair (lanes < npairs)
+            if (lane < npairs) {
+                if (lane == 0) {
+                    pi = rnd;
+                    pj = np - 1;
+                } else {
+                    pi = rnd + lane;
+                    if (pi >= np - 1) pi -= np - 1;
+                    pj = rnd - lane;
+                    if (pj < 0) pj += np - 1;
+                }
+                if (pi > pj) { const int t = pi; pi = pj; pj = t; }
+                double c = 1.0, sm = 0.0, er = 1.0, ei = 0.0;
+                if (pj < n) {
+                    const c64 b = A[pj * n + pi];  // a(pi, pj)
+                    const double app = A[pi * n + pi].re, aqq = A[pj * n + pj].re;
+                    const double b2 = norm2(b);
+                    const double thr = 1e-15 * 1e-15;
+                    if (b2 > thr * fabs(app * aqq) && b2 > (1e-30 * dscale) * (1e-30 * dscale)) {
+                        const double ib = rsqrt(b2);
+                        const double tau = (aqq - app) * 0.5 * ib;
+                        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        c = rsqrt(1.0 + t * t);
+                        sm = t * c;
+                        er = b.re * ib;
+                        ei = b.im * ib;
+                    }
+                }
+                pc[lane] = c;
+                ps[lane] = sm;
+                per[lane] = er;
+                pei[lane] = ei;
+            }
+            const bool rot = __any_sync(0xffffffffu, lane < npairs && ps[lane] != 0.0);
+            __syncwarp();
+            if (!rot) continue;
+            any = true;
+            // columns (A and Z): a(r,i) = c a_ri - conj(s) a_rj ; a(r,j) = s a_ri + c a_rj
+            for (int e = lane; e < 2 * npairs * n; e += 32) {
+                const int which = e >= npairs * n;
+                const int e2 = which ? e - npairs * n : e;
+                const int t = e2 / n, r = e2 % n;
+                if (ps[t] == 0.0) continue;
+                int i, j;
+                if (t == 0) { i = rnd; j = np - 1; }
+                else {
+                    i = rnd + t; if (i >= np - 1) i -= np - 1;
+                    j = rnd - t; if (j < 0) j += np - 1;
+                }
+                if (i > j) { const int x = i; i = j; j = x; }
+                if (j >= n) continue;
+                c64* M = which ? Z : A;
+                const double c = pc[t], sm = ps[t];
+                const double sr = sm * per[t], si = sm * pei[t];
+                const c64 x = M[i * n + r], y = M[j * n + r];
+                M[i * n + r] = mk(c * x.re - (sr * y.re + si * y.im), c * x.im - (sr * y.im - si * y.re));
+                M[j * n + r] = mk(sr * x.re - si * x.im + c * y.re, sr * x.im + si * x.re + c * y.im);
+            }
+            __syncwarp();
+            // rows: a(i,r) = c a_ir - s a_jr ; a(j,r) = conj(s) a_ir + c a_jr
+            for (int e = lane; e < npairs * n; e += 32) {
+                const int t = e / n, r = e % n;
+                if (ps[t] == 0.0) continue;
+                int i, j;
+                if (t == 0) { i = rnd; j = np - 1; }
+                else {
+                    i = rnd + t; if (i >= np - 1) i -= np - 1;
+                    j = rnd - t; if (j < 0) j += np - 1;
+                }
+                if (i > j) { const int x = i; i = j; j = x; }
+                if (j >= n) continue;
+                const double c = pc[t], sm = ps[t];
+                const double sr = sm * per[t], si = sm * pei[t];
+                const c64 x = A[r * n + i], y = A[r * n + j];
+                A[r * n + i] = mk(c * x.re - (sr * y.re - si * y.im), c * x.im - (sr * y.im + si * y.re));
+                A[r * n + j] = mk(sr * x.re + si * x.im + c * y.re, sr * x.im - si * x.re + c * y.im);
+            }
+            __syncwarp();
+        }
+        if (!any) return sweep + 1;
+    }
+    return 0;
+}
+
+// ------------------------------------------------------------------ register-tiled fp64 Gram(s)
+// Up to two products G1 = X1^H Y1 (HERM1: X1 == Y1, upper tiles mirrored) and G2 = X2^H Y2 of
+// column-major p x m operands (p % 4 == 0). Rows are staged kRCH at a time row-major in shared
+// memory with a padded stride (p + 1 complex, conflict-free 16-B reads across 8 row groups);
+// each thread accumulates a 4x4 tile over every 8th row (16 complex MACs per 8 shared loads),
+// and the 8 row-group partials are reduced with shuffles. Results: column-major p x p in G1/G2.
+constexpr int kRG = 8;      // row groups (consecutive lanes)
+constexpr int kRCH = 64;    // rows per staged chunk
+
+template <typename T1, typename T2>
+__device__ void tiled_gram2(const T1* __restrict__ X1, bool herm1, const T1* __restrict__ Y1, const T2* __restrict__ X2,
+                            const T2* __restrict__ Y2, int m, int p, c64* stage, c64* G1, c64* G2) {
+    const int nb = p >> 2;
+    const int t1 = herm1 ? nb * (nb + 1) / 2 : nb * nb;
+    const int t2 = X2 ? nb * nb : 0;
+    const int ntiles = t1 + t2;
+    const int ld = p + 1;
+    // staged buffers: X1 (and Y1 if distinct), X2 (and Y2 if distinct)
+    c64* sX1 = stage;
+    c64* sY1 = herm1 ? sX1 : sX1 + kRCH * ld;
+    c64* sX2 = sY1 + (herm1 ? kRCH * ld : kRCH * ld);
+    c64* sY2 = (X2 && Y2 == reinterpret_cast<const T2*>(X1)) ? sX1 : sX2 + kRCH * ld;
+    const bool y2_is_x1 = X2 && Y2 == reinterpret_cast<const T2*>(X1);
+    const int lane = threadIdx.x & 31;
+    const int rg = threadIdx.x % kRG;
+    for (int pass = 0; pass * (kNT / kRG) < ntiles; ++pass) {
+        const int tile = pass * (kNT / kRG) + threadIdx.x / kRG;
+        const bool active = tile < ntiles;
+        const bool second = tile >= t1;
+        int ti = 0, tj = 0;
+        if (active) {
+            if (!second) {
+                if (herm1) {
+                    int rem = tile;
+                    while (rem >= nb - ti) { rem -= nb - ti; ++ti; }
+                    tj = ti + rem;
+                } else {
+                    ti = tile % nb;
+                    tj = tile / nb;
+                }
+            } else {
+                ti = (tile - t1) % nb;
+                tj = (tile - t1) / nb;
+            }
+        }
+        c64 acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = mk(0.0, 0.0);
+        for (int r0 = 0; r0 < m; r0 += kRCH) {
+            const int rn = min(kRCH, m - r0);
+            __syncthreads();
+            for (int e = threadIdx.x; e < p * kRCH; e += kNT) {
+                const int c = e / kRCH, r = e % kRCH;
+                const bool ok = r < rn;
+                sX1[r * ld + c] = ok ? to64(X1[static_cast<size_t>(c) * m + r0 + r]) : mk(0.0, 0.0);
+                if (!herm1) sY1[r * ld + c] = ok ? to64(Y1[static_cast<size_t>(c) * m + r0 + r]) : mk(0.0, 0.0);
+                if (X2) {
+                    sX2[r * ld + c] = ok ? to64(X2[static_cast<size_t>(c) * m + r0 + r]) : mk(0.0, 0.0);
+                    if (!y2_is_x1) sY2[r * ld + c] = ok ? to64(Y2[static_cast<size_t>(c) * m + r0 + r]) : mk(0.0, 0.0);
+                }
+            }
+            __syncthreads();
+            if (active) {
+                const c64* xs = second ? sX2 : sX1;
+                const c64* ys = second ? sY2 : sY1;
+                for (int r = rg; r < rn; r += kRG) {
+                    c64 x[4], y[4];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) {
+                        x[a] = xs[r * ld + 4 * ti + a];
+                        y[a] = ys[r * ld + 4 * tj + a];
+                    }
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) cmac_conj(acc[a][b], x[a], y[b]);
+                }
+            }
+        }
+        // reduce the kRG row-group partials (consecutive lanes)
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+#pragma unroll
+                for (int o = 1; o < kRG; o <<= 1) {
+                    acc[a][b].re += __shfl_xor_sync(0xffffffffu, acc[a][b].re, o);
+                    acc[a][b].im += __shfl_xor_sync(0xffffffffu, acc[a][b].im, o);
+                }
+            }
+        if (active && rg == 0) {
+            c64* G = second ? G2 : G1;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int i = 4 * ti + a, j = 4 * tj + b;
+                    G[j * p + i] = acc[a][b];
+                    if (!second && herm1 && ti != tj) G[i * p + j] = conj(acc[a][b]);
+                }
+        }
+        (void)lane;
+    }
+    __syncthreads();
+}
+
+template <int PC>
+__host__ __device__ constexpr size_t tiled_stage_bytes(int nbuf) {
+    return sizeof(c64) * nbuf * kRCH * (PC + 1);
+}
+
+// Power-iteration orthonormalisation with the tiled Gram (p % 4 == 0): pivoted Cholesky QR,
+// Eigen rank rule, V = C P R^-1.
+template <int PC>
+__global__ void __launch_bounds__(kNT, 2) k_orth_tiled(const c32* __restrict__ Cin, c32* __restrict__ Vout,
+                                                    int32_t* __restrict__ status, int m, int p) {
+    extern __shared__ uint8_t dsm[];
+    c64* G = reinterpret_cast<c64*>(dsm);
+    c64* L = G + PC * PC;
+    c64* stage = L + PC * PC;
+    __shared__ int perm[32], done[32];
+    __shared__ double d[32];
+    __shared__ double s_inv;
+    const int f = blockIdx.x;
+    const c32* Cf = Cin + static_cast<size_t>(f) * m * p;
+    tiled_gram2<c32, c32>(Cf, true, Cf, nullptr, nullptr, m, p, stage, G, nullptr);
+    block_chol(G, p, true, perm, d, L, done, &s_inv);
+    if (threadIdx.x == 0) {
+        const double eps = eps_of<float>::value;
+        const double thr_helper = fmax(d[0], 0.0) * eps * eps / static_cast<double>(m);
+        int nonzero = p;
+        double maxpivot = 0.0;
+        for (int k = 0; k < p; ++k) {
+            if (nonzero == p && d[k] < thr_helper * static_cast<double>(m - k)) nonzero = k;
+            maxpivot = fmax(maxpivot, sqrt(fmax(d[k], 0.0)));
+        }
+        const double thr = maxpivot * eps * static_cast<double>(p);
+        int rank = 0;
+        for (int k = 0; k < nonzero; ++k) rank += sqrt(fmax(d[k], 0.0)) > thr ? 1 : 0;
+        if (rank < p) atomicOr(&status[f], kFrameRank);
+    }
+    rows_solve<PC>(Cf, perm, L, m, p, Vout + static_cast<size_t>(f) * m * p);
+}
+
+__device__ __forceinline__ c64 warp_sum_c(c64 v) {
+    v.re = warp_sum(v.re);
+    v.im = warp_sum(v.im);
+    return v;
+}
+
+// One-sided Jacobi on the n columns of a (column-major n x n, shared), one warp per pair per
+// round (circle ordering). Rotation parameters seeded in fp32 (short MUFU latency), applied as
+// an exactly unitary fp64 rotation (c from t in fp64, |e| = 1 to fp64 via Newton steps).
+// Returns sweeps used (0 = cap hit).
+__device__ int block_hestenes(c64* a, int n, int* s_rot) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int np = (n + 1) & ~1;
+    const double tol = 8.0 * 2.220446049250313e-16 * n;
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        if (threadIdx.x == 0) *s_rot = 0;
+        __syncthreads();
+        for (int rnd = 0; rnd < np - 1; ++rnd) {
+            for (int idx = warp; idx < np / 2; idx += kNW) {
+                int i, j;
+                if (idx == 0) {
+                    i = rnd;
+                    j = np - 1;
+                } else {
+                    i = rnd + idx;
+                    if (i >= np - 1) i -= np - 1;
+                    j = rnd - idx;
+                    if (j < 0) j += np - 1;
+                }
+                if (i > j) {
+                    const int t = i;
+                    i = j;
+                    j = t;
+                }
+                if (j >= n) continue;
+                c64* ai = a + i * n;
+                c64* aj = a + j * n;
+                double al = 0.0, be = 0.0;
+                c64 ga = mk(0.0, 0.0);
+                for (int r = lane; r < n; r += 32) {
+                    const c64 x = ai[r], y = aj[r];
+                    al += norm2(x);
+                    be += norm2(y);
+                    cmac_conj(ga, x, y);
+                }
+                al = warp_sum(al);
+                be = warp_sum(be);
+                ga = warp_sum_c(ga);
+                const double g2 = norm2(ga);
+                if (!(g2 > tol * tol * al * be) || g2 == 0.0) continue;
+                const float gf = sqrtf(static_cast<float>(g2));
+                const float zeta = static_cast<float>(be - al) / (2.0f * gf);
+                const float tf = (zeta >= 0.0f ? 1.0f : -1.0f) / (fabsf(zeta) + sqrtf(1.0f + zeta * zeta));
+                const double t = tf;
+                const double c = rsqrt(1.0 + t * t);
+                const double s = c * t;
+                double ig = static_cast<double>(rsqrtf(static_cast<float>(g2)));
+                ig = ig * (1.5 - 0.5 * g2 * ig * ig);  // Newton: 1/|g| to fp64
+                ig = ig * (1.5 - 0.5 * g2 * ig * ig);
+                const c64 e = mk(ga.re * ig, ga.im * ig);
+                for (int r = lane; r < n; r += 32) {
+                    const c64 x = ai[r], y = aj[r];
+                    ai[r] = mk(c * x.re - s * (e.re * y.re + e.im * y.im), c * x.im - s * (e.re * y.im - e.im * y.re));
+                    aj[r] = mk(s * (e.re * x.re - e.im * x.im) + c * y.re, s * (e.re * x.im + e.im * x.re) + c * y.im);
+                }
+                if (lane == 0) *s_rot = 1;
+            }
+            __syncthreads();
+        }
+        const bool fin = (*s_rot == 0);
+        __syncthreads();
+        if (fin) return sweep + 1;
+    }
+    return 0;
+}
+
+template <int PC>
+__host__ __device__ constexpr size_t nys_smem_bytes() {
+    return sizeof(c64) * (3 * PC * PC) + sizeof(double) * PC;
+}
+
+template <int PC>
+__global__ void __launch_bounds__(kNT) k_nystrom_blk(const c64* __restrict__ Hin, const c64* __restrict__ work,
+                                                     const c64* __restrict__ Rt, c64* __restrict__ basis,
+                                                     double* __restrict__ eig, int32_t* __restrict__ status, int m,
+                                                     int p, int k, int32_t* __restrict__ dbg) {
+    extern __shared__ uint8_t dsm[];
+    c64* A = reinterpret_cast<c64*>(dsm);  // H, then Y
+    c64* L = A + p * p;
+    c64* Rs = L + p * p;
+    double* sig = reinterpret_cast<double*>(Rs + p * p);
+    __shared__ int perm[32], done[32], order[32];
+    __shared__ double d[32];
+    __shared__ double s_inv;
+    __shared__ int s_rot;
+    const int f = blockIdx.x;
+    const c64* Hf = Hin + static_cast<size_t>(f) * p * p;
+    const c64* Rf = Rt + static_cast<size_t>(f) * p * p;
+    for (int e = threadIdx.x; e < p * p; e += kNT) {
+        const int i = e % p, j = e / p;
+        const c64 a = Hf[j * p + i], b = Hf[i * p + j];
+        A[e] = mk(0.5 * (a.re + b.re), 0.5 * (a.im - b.im));  // Herm(H)(i, j)
+        Rs[e] = Rf[e];
+    }
+    __syncthreads();
+    block_chol(A, p, false, perm, d, L, done, &s_inv);
+    // Y = Rt L_H^-H: row i of Y solves y L^H = rt_i (thread per row i < p), into A (column-major)
+    if (threadIdx.x < p) {
+        const int i = threadIdx.x;
+        c64 v[PC];
+#pragma unroll
+        for (int j = 0; j < PC; ++j) {
+            if (j < p) {
+                c64 x = Rs[j * p + i];
+#pragma unroll
+                for (int a = 0; a < PC; ++a) {
+                    if (a < j) {
+                        const c64 l = L[a * p + j];
+                        x.re -= v[a].re * l.re + v[a].im * l.im;
+                        x.im -= v[a].im * l.re - v[a].re * l.im;
+                    }
+                }
+                const double ljj = L[j * p + j].re;
+                const double inv = ljj > 0.0 ? 1.0 / ljj : 0.0;
+                v[j] = mk(x.re * inv, x.im * inv);
+                A[j * p + i] = v[j];
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double dmax = 0.0, dmin = 1e300;
+        for (int q = 0; q < p; ++q) {
+            dmax = fmax(dmax, d[q]);
+            dmin = fmin(dmin, d[q]);
+        }
+        if (!(dmin > static_cast<double>(p) * eps_of<float>::value * dmax)) atomicOr(&status[f], kFrameNoConv);
+    }
+    const int sw = block_hestenes(A, p, &s_rot);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int c = warp; c < p; c += kNW) {
+        double s = 0.0;
+        for (int r = lane; r < p; r += 32) s += norm2(A[c * p + r]);
+        s = warp_sum(s);
+        if (lane == 0) sig[c] = sqrt(s);
+    }
+    __syncthreads();
+    if (threadIdx.x < p) {  // descending rank (ties: lower index first)
+        const int c = threadIdx.x;
+        int rank = 0;
+        for (int q = 0; q < p; ++q)
+            if (q != c && (sig[q] > sig[c] || (sig[q] == sig[c] && q < c))) ++rank;
+        order[rank] = c;
+    }
+    __syncthreads();
+    const c64* Qf = work + static_cast<size_t>(f) * 2 * p * m + static_cast<size_t>(p) * m;
+    c64* Bf = basis + static_cast<size_t>(f) * m * k;
+    for (int e = threadIdx.x; e < m * k; e += kNT) {
+        const int kk = e / m, r = e % m;
+        const int c = order[kk];
+        const double inv = sig[c] > 0.0 ? 1.0 / sig[c] : 0.0;
+        c64 acc = mk(0.0, 0.0);
+        for (int q = 0; q < p; ++q) cmac(acc, Qf[static_cast<size_t>(q) * m + r], A[c * p + q]);
+        Bf[static_cast<size_t>(kk) * m + r] = mk(acc.re * inv, acc.im * inv);
+    }
+    if (threadIdx.x < k) {
+        double lam = sig[order[threadIdx.x]];
+        lam *= lam;
+        if (lam < 0.0 && lam >= -1e-10) lam = 0.0;
+        eig[static_cast<size_t>(f) * k + threadIdx.x] = lam;
+    }
+    if (threadIdx.x == 0 && sw == 0) atomicOr(&status[f], kFrameNoConv);
+    if (threadIdx.x == 0 && dbg) dbg[f] = sw;
+}
+
+
+// Fused Nystrom tail (fast2: V = last power-iteration basis; fast1: H given):
+//   G = C^H C, H = V^H C (one tiled pass); G = R^H R (Cholesky, C = Q R); H = L_H L_H^H;
+//   Y = R L_H^-H (so B' = Rt W Rt^H = Y Y^H with Rt = R); one-sided Jacobi on Y -> Z, s;
+//   T = R^-1 Z_K; U = C T. A single CholQR suffices: U spans the large-singular-value
+//   directions of C, where C R^-1 is orthonormal to ~eps64 * (s_1/s_K)^2.
+template <int PC>
+__global__ void __launch_bounds__(kNT, 2) k_final_tiled(const c32* __restrict__ Cin, const c32* __restrict__ Vin,
+                                                     const c64* __restrict__ Hin, c64* __restrict__ basis,
+                                                     double* __restrict__ eig, int32_t* __restrict__ status, int m,
+                                                     int p, int k, int32_t* __restrict__ dbg) {
+    extern __shared__ uint8_t dsm[];
+    c64* G = reinterpret_cast<c64*>(dsm);  // -> R^H (L of G)
+    c64* H = G + PC * PC;                  // -> Y
+    c64* L = H + PC * PC;                  // Cholesky factors (original-index form)
+    c64* LH = L + PC * PC;
+    c64* Tm = LH + PC * PC;                // p x k  (T = R^-1 Z_K)
+    double* sig = reinterpret_cast<double*>(Tm + PC * PC);
+    c64* stage = reinterpret_cast<c64*>(sig + PC);
+    __shared__ int perm[32], done[32], order[32];
+    __shared__ double d[32];
+    __shared__ double s_inv;
+    __shared__ int s_rot;
+    const int f = blockIdx.x;
+    const c32* Cf = Cin + static_cast<size_t>(f) * m * p;
+    long long T0 = clock64();
+    if (Vin) {
+        tiled_gram2<c32, c32>(Cf, true, Cf, Vin + static_cast<size_t>(f) * m * p, Cf, m, p, stage, G, H);
+    } else {
+        tiled_gram2<c32, c32>(Cf, true, Cf, nullptr, nullptr, m, p, stage, G, nullptr);
+        const c64* Hf = Hin + static_cast<size_t>(f) * p * p;
+        for (int e = threadIdx.x; e < p * p; e += kNT) H[e] = Hf[e];
+        __syncthreads();
+    }
+    long long T1 = clock64();
+    for (int e = threadIdx.x; e < p * p; e += kNT) {  // Herm(H) in place
+        const int i = e % p, j = e / p;
+        if (i <= j) {
+            const c64 a = H[j * p + i], b = H[i * p + j];
+            const c64 hm = mk(0.5 * (a.re + b.re), 0.5 * (a.im - b.im));
+            H[j * p + i] = hm;
+            H[i * p + j] = conj(hm);
+        }
+    }
+    __syncthreads();
+    block_chol(G, p, false, perm, d, L, done, &s_inv);  // G = L L^H, R = L^H
+    block_chol(H, p, false, perm, d, LH, done, &s_inv);
+    if (threadIdx.x == 0) {
+        double dmax = 0.0, dmin = 1e300;
+        for (int q = 0; q < p; ++q) {
+            dmax = fmax(dmax, d[q]);
+            dmin = fmin(dmin, d[q]);
+        }
+        if (!(dmin > static_cast<double>(p) * eps_of<float>::value * dmax)) atomicOr(&status[f], kFrameNoConv);
+    }
+    // Y(i, :) solves y LH^H = R(i, :), R(i, j) = conj(L[i * p + j]) (j >= i); Y -> H
+    if (threadIdx.x < p) {
+        const int i = threadIdx.x;
+        c64 v[PC];
+#pragma unroll
+        for (int j = 0; j < PC; ++j) {
+            if (j < p) {
+                c64 x = j >= i ? conj(L[i * p + j]) : mk(0.0, 0.0);
+#pragma unroll
+                for (int a = 0; a < PC; ++a) {
+                    if (a < j) {
+                        const c64 l = LH[a * p + j];
+                        x.re -= v[a].re * l.re + v[a].im * l.im;
+                        x.im -= v[a].im * l.re - v[a].re * l.im;
+                    }
+                }
+                const double ljj = LH[j * p + j].re;
+                const double inv = ljj > 0.0 ? 1.0 / ljj : 0.0;
+                v[j] = mk(x.re * inv, x.im * inv);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < PC; ++j)
+            if (j < p) Tm[j * p + i] = v[j];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < p * p; e += kNT) H[e] = Tm[e];
+    __syncthreads();
+    long long T2 = clock64();
+    const int sw = block_hestenes(H, p, &s_rot);
+    long long T3 = clock64();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int c = warp; c < p; c += kNW) {
+        double s2 = 0.0;
+        for (int r = lane; r < p; r += 32) s2 += norm2(H[c * p + r]);
+        s2 = warp_sum(s2);
+        if (lane == 0) sig[c] = sqrt(s2);
+    }
+    __syncthreads();
+    if (threadIdx.x < p) {
+        const int c = threadIdx.x;
+        int rank = 0;
+        for (int q = 0; q < p; ++q)
+            if (q != c && (sig[q] > sig[c] || (sig[q] == sig[c] && q < c))) ++rank;
+        order[rank] = c;
+    }
+    __syncthreads();
+    // T(:, kk) = R^-1 z, z = H(:, order[kk]) / sig (back substitution, R(i,j) = conj(L[i*p + j]))
+    if (threadIdx.x < k) {
+        const int kk = threadIdx.x, c = order[kk];
+        const double inv_s = sig[c] > 0.0 ? 1.0 / sig[c] : 0.0;
+        for (int i = p - 1; i >= 0; --i) {
+            c64 acc = H[c * p + i];
+            acc.re *= inv_s;
+            acc.im *= inv_s;
+            for (int j = i + 1; j < p; ++j) {
+                const c64 rij = conj(L[i * p + j]);
+                const c64 tj = Tm[kk * p + j];
+                acc.re -= rij.re * tj.re - rij.im * tj.im;
+                acc.im -= rij.re * tj.im + rij.im * tj.re;
+            }
+            const double rii = L[i * p + i].re;
+            const double inv = rii > 0.0 ? 1.0 / rii : 0.0;
+            Tm[kk * p + i] = mk(acc.re * inv, acc.im * inv);
+        }
+    }
+    __syncthreads();
+    c64* Bf = basis + static_cast<size_t>(f) * m * k;
+    for (int r = threadIdx.x; r < m; r += kNT) {
+        c64 crow[PC];
+#pragma unroll
+        for (int q = 0; q < PC; ++q)
+            if (q < p) crow[q] = to64(Cf[static_cast<size_t>(q) * m + r]);
+        for (int kk = 0; kk < k; ++kk) {
+            c64 acc = mk(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < PC; ++q)
+                if (q < p) cmac(acc, crow[q], Tm[kk * p + q]);
+            Bf[static_cast<size_t>(kk) * m + r] = acc;
+        }
+    }
+    if (threadIdx.x < k) {
+        double lam = sig[order[threadIdx.x]];
+        lam *= lam;  // eigenvalue of B' = Y Y^H
+        if (lam < 0.0 && lam >= -1e-10) lam = 0.0;
+        eig[static_cast<size_t>(f) * k + threadIdx.x] = lam;
+    }
+    if (threadIdx.x == 0 && sw == 0) atomicOr(&status[f], kFrameNoConv);
+    if (threadIdx.x == 0 && dbg) dbg[f] = sw;
+    __syncthreads();
+    long long T4 = clock64();
+    if (threadIdx.x == 0 && g_phase_dbg) {
+        g_phase_dbg[f * 4 + 0] = static_cast<int>(T1 - T0);
+        g_phase_dbg[f * 4 + 1] = static_cast<int>(T2 - T1);
+        g_phase_dbg[f * 4 + 2] = static_cast<int>(T3 - T2);
+        g_phase_dbg[f * 4 + 3] = static_cast<int>(T4 - T3);
+        (void)sw;
+    }
+}
+
+}  // namespace smb
+}  // namespace fmk
+
+using namespace fmk;
+
+static int32_t* g_sweep_dbg = nullptr;
+extern "C" int32_t fm_debug_set_sweep_buffer(int32_t* d) {
+    g_sweep_dbg = d;
+    return 0;
+}
+extern "C" int32_t fm_debug_set_phase_buffer(int32_t* d) {
+    return cudaMemcpyToSymbol(smb::g_phase_dbg, &d, sizeof(d)) == cudaSuccess ? 0 : 1;
+}
+
+cudaError_t fm_launch_cholqr_warp(const void* C, void* work, void* Vout, void* Rt, void* Hout, const void* Vin,
+                                  int32_t* status, int frames, int m, int p, bool final_mode, cudaStream_t s) {
+    if (p > 32 || p < 1 || m < p) return cudaErrorInvalidValue;
+    auto go = [&](auto kern, size_t smem) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        kern<<<frames, smb::kNT, smem, s>>>(static_cast<const c32*>(C), static_cast<c64*>(work),
+                                            static_cast<c32*>(Vout), static_cast<c64*>(Rt), static_cast<c64*>(Hout),
+                                            static_cast<const c32*>(Vin), status, m, p);
+        return cudaGetLastError();
+    };
+    if (p <= 8) return final_mode ? go(smb::k_cholqr_blk<8, 1>, smb::chol_smem_bytes<8>())
+                                  : go(smb::k_cholqr_blk<8, 0>, smb::chol_smem_bytes<8>());
+    if (p <= 16) return final_mode ? go(smb::k_cholqr_blk<16, 1>, smb::chol_smem_bytes<16>())
+                                   : go(smb::k_cholqr_blk<16, 0>, smb::chol_smem_bytes<16>());
+    return final_mode ? go(smb::k_cholqr_blk<32, 1>, smb::chol_smem_bytes<32>())
+                      : go(smb::k_cholqr_blk<32, 0>, smb::chol_smem_bytes<32>());
+}
+
+cudaError_t fm_launch_orth_tiled(const void* C, void* Vout, int32_t* status, int frames, int m, int p,
+                                  cudaStream_t s) {
+    if (p > 32 || (p & 3) || m < p) return cudaErrorInvalidValue;
+    auto go = [&](auto kern, size_t smem) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        kern<<<frames, smb::kNT, smem, s>>>(static_cast<const c32*>(C), static_cast<c32*>(Vout), status, m, p);
+        return cudaGetLastError();
+    };
+    if (p <= 8) return go(smb::k_orth_tiled<8>, sizeof(c64) * 2 * 64 + smb::tiled_stage_bytes<8>(1));
+    if (p <= 16) return go(smb::k_orth_tiled<16>, sizeof(c64) * 2 * 256 + smb::tiled_stage_bytes<16>(1));
+    return go(smb::k_orth_tiled<32>, sizeof(c64) * 2 * 1024 + smb::tiled_stage_bytes<32>(1));
+}
+
+cudaError_t fm_launch_final_tiled(const void* C, const void* V, const void* H, void* basis, double* eig,
+                                  int32_t* status, int frames, int m, int p, int k, cudaStream_t s) {
+    if (p > 32 || (p & 3) || k > p || m < p) return cudaErrorInvalidValue;
+    auto go = [&](auto kern, int pc) {
+        const size_t smem = sizeof(c64) * 5 * pc * pc + sizeof(double) * pc + sizeof(c64) * 3 * 64 * (pc + 1);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        kern<<<frames, smb::kNT, smem, s>>>(static_cast<const c32*>(C), static_cast<const c32*>(V),
+                                            static_cast<const c64*>(H), static_cast<c64*>(basis), eig, status, m, p, k,
+                                            g_sweep_dbg);
+        return cudaGetLastError();
+    };
+    if (p <= 8) return go(smb::k_final_tiled<8>, 8);
+    if (p <= 16) return go(smb::k_final_tiled<16>, 16);
+    return go(smb::k_final_tiled<32>, 32);
+}
+
+cudaError_t fm_launch_nystrom_warp2(const void* H, const void* work, const void* Rt, void* basis, double* eig,
+                                    int32_t* status, int frames, int m, int p, int k, cudaStream_t s) {
+    if (p > 32 || k > p) return cudaErrorInvalidValue;
+    auto go = [&](auto kern, size_t smem) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        kern<<<frames, smb::kNT, smem, s>>>(static_cast<const c64*>(H), static_cast<const c64*>(work),
+                                            static_cast<const c64*>(Rt), static_cast<c64*>(basis), eig, status, m, p,
+                                            k, g_sweep_dbg);
+        return cudaGetLastError();
+    };
+    if (p <= 8) return go(smb::k_nystrom_blk<8>, smb::nys_smem_bytes<8>());
+    if (p <= 16) return go(smb::k_nystrom_blk<16>, smb::nys_smem_bytes<16>());
+    return go(smb::k_nystrom_blk<32>, smb::nys_smem_bytes<32>());
+}

@@ -283,16 +283,245 @@ __global__ void __launch_bounds__(kNT) k_qr(const cplx<T>* __restrict__ Cin, c64
     }
 }
 
+// ------------------------------------------------------------------ pivoted Cholesky QR (fp32 batch path)
+// Same factorisation as the reference's column-pivoted QR (R/src/linalg.cpp:127-141) in exact
+// arithmetic: the pivoted Cholesky factor of G = C^H C (fp64; products of fp32 data are exact)
+// is R with |R_kk| = sqrt(Schur pivot), so Eigen's rank rule (nonzero-pivot cut + |R_kk| >
+// eps*p*maxpivot, eps of the data type) is applied to the same quantities. Far fewer block
+// barriers than Householder: one Gram pass, a p x p factorisation + inverse in one warp, a
+// row-parallel product with L^-H.
+//   MODE 0: V = C P L^-H (complex64, column-major) for the power iteration, rank flags.
+//   MODE 1: CholQR2 -> Q (fp64, work[f][1]) and Rt = Q^H C for the Nystrom tail.
+constexpr int kRC = 64;   // rows per staged Gram chunk
+constexpr int kRCP = 65;  // padded column stride (16-B elements): conflict-free column reads
+
+// G(i, j) = sum_r conj(X_i[r]) Y_j[r] over column-major X, Y (p x m), staged kRC rows at a time.
+// HERM: X == Y, only i <= j computed and mirrored.
+template <bool HERM, typename XT, typename YT>
+__device__ void block_gram(const XT* __restrict__ X, const YT* __restrict__ Y, int m, int p, c64* chunk, c64* G) {
+    const int ne = HERM ? p * (p + 1) / 2 : p * p;
+    constexpr int kMaxE = 16;  // entries per thread (p <= 64: 4096 / 256)
+    c64 acc[kMaxE];
+    int cnt = 0;
+    for (int e = threadIdx.x; e < ne && cnt < kMaxE; e += blockDim.x) acc[cnt++] = mk(0.0, 0.0);
+    c64* cy = HERM ? chunk : chunk + p * kRCP;
+    for (int r0 = 0; r0 < m; r0 += kRC) {
+        const int rn = min(kRC, m - r0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < p * kRC; e += blockDim.x) {
+            const int c = e / kRC, r = e % kRC;
+            chunk[c * kRCP + r] = r < rn ? to64(X[static_cast<size_t>(c) * m + r0 + r]) : mk(0.0, 0.0);
+            if (!HERM) cy[c * kRCP + r] = r < rn ? to64(Y[static_cast<size_t>(c) * m + r0 + r]) : mk(0.0, 0.0);
+        }
+        __syncthreads();
+        int q = 0;
+        for (int e = threadIdx.x; e < ne && q < kMaxE; e += blockDim.x, ++q) {
+            int i, j;
+            if (HERM) {
+                i = 0;
+                int rem = e;
+                while (rem >= p - i) { rem -= p - i; ++i; }
+                j = i + rem;
+            } else {
+                i = e % p;
+                j = e / p;
+            }
+            const c64* xi = chunk + i * kRCP;
+            const c64* yj = cy + j * kRCP;
+            c64 a = acc[q];
+            for (int r = 0; r < rn; ++r) cmac_conj(a, xi[r], yj[r]);
+            acc[q] = a;
+        }
+    }
+    int q = 0;
+    for (int e = threadIdx.x; e < ne && q < kMaxE; e += blockDim.x, ++q) {
+        int i, j;
+        if (HERM) {
+            i = 0;
+            int rem = e;
+            while (rem >= p - i) { rem -= p - i; ++i; }
+            j = i + rem;
+            G[i * p + j] = conj(acc[q]);  // G(j, i)
+        } else {
+            i = e % p;
+            j = e / p;
+        }
+        G[j * p + i] = acc[q];  // column-major G(i, j)
+    }
+    __syncthreads();
+}
+
+// In-place Cholesky of the Hermitian p x p matrix A (column-major) by warp 0: A_perm = L L^H,
+// then A <- L^-1 (lower triangular). Optional diagonal pivoting; d[k] = Schur pivot at step k.
+__device__ void warp_cholesky_inv(c64* A, int p, bool pivot, int* perm, double* d) {
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    for (int k = 0; k < p; ++k) {
+        int piv = k;
+        if (pivot) {
+            double best = -1.0;
+            int bi = p;
+            for (int j = k + lane; j < p; j += 32) {
+                const double v = A[j * p + j].re;
+                if (v > best || (v == best && j < bi)) { best = v; bi = j; }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            piv = bi;
+        }
+        if (piv != k) {  // symmetric swap of rows/cols k and piv
+            for (int i = lane; i < p; i += 32) {
+                const c64 t = A[k * p + i]; A[k * p + i] = A[piv * p + i]; A[piv * p + i] = t;
+            }
+            __syncwarp();
+            for (int i = lane; i < p; i += 32) {
+                const c64 t = A[i * p + k]; A[i * p + k] = A[i * p + piv]; A[i * p + piv] = t;
+            }
+            if (lane == 0) { const int t = perm[k]; perm[k] = perm[piv]; perm[piv] = t; }
+            __syncwarp();
+        }
+        const double dk = A[k * p + k].re;
+        if (lane == 0) d[k] = dk;
+        const double lkk = dk > 0.0 ? sqrt(dk) : 0.0;
+        const double inv = lkk > 0.0 ? 1.0 / lkk : 0.0;
+        __syncwarp();
+        for (int i = k + lane; i < p; i += 32) {
+            const c64 v = A[k * p + i];
+            A[k * p + i] = i == k ? mk(lkk, 0.0) : mk(v.re * inv, v.im * inv);
+        }
+        __syncwarp();
+        const int nt = p - k - 1;  // Schur update of the trailing block (lower + mirror)
+        for (int e = lane; e < nt * nt; e += 32) {
+            const int i = k + 1 + e % nt, j = k + 1 + e / nt;
+            if (j > i) continue;
+            const c64 li = A[k * p + i], lj = A[k * p + j];
+            c64 a = A[j * p + i];
+            a.re -= li.re * lj.re + li.im * lj.im;  // li * conj(lj)
+            a.im -= li.im * lj.re - li.re * lj.im;
+            A[j * p + i] = a;
+            A[i * p + j] = conj(a);
+        }
+        __syncwarp();
+    }
+    // L^-1 by forward substitution, one lane per column c (columns independent).
+    for (int c = lane; c < p; c += 32) {
+        const double lcc = A[c * p + c].re;
+        const double icc = lcc > 0.0 ? 1.0 / lcc : 0.0;
+        c64 x[64];
+        x[c] = mk(icc, 0.0);
+        for (int i = c + 1; i < p; ++i) {
+            c64 acc = mk(0.0, 0.0);
+            for (int q = c; q < i; ++q) cmac(acc, A[q * p + i], x[q]);  // L(i,q) Linv(q,c)
+            const double lii = A[i * p + i].re;
+            const double ii = lii > 0.0 ? -1.0 / lii : 0.0;
+            x[i] = mk(acc.re * ii, acc.im * ii);
+        }
+        __syncwarp(__activemask());
+        for (int i = 0; i < c; ++i) A[c * p + i] = mk(0.0, 0.0);
+        for (int i = c; i < p; ++i) A[c * p + i] = x[i];
+    }
+    __syncwarp();
+}
+
+// Out[j][r] = sum_{i <= j} X[perm[i]][r] conj(Linv(j, i))   (rows of X P L^-H), 16 columns at a time.
+template <typename XT, typename OT>
+__device__ void rows_apply_linvh(const XT* __restrict__ X, const int* perm, const c64* Linv, int m, int p,
+                                 OT* __restrict__ Out) {
+    for (int r = threadIdx.x; r < m; r += blockDim.x) {
+        for (int jb = 0; jb < p; jb += 16) {
+            const int jn = min(16, p - jb);
+            c64 acc[16];
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) acc[jj] = mk(0.0, 0.0);
+            for (int i = 0; i < jb + jn; ++i) {
+                const c64 x = to64(X[static_cast<size_t>(perm ? perm[i] : i) * m + r]);
+                const c64* lcol = Linv + i * p + jb;  // Linv(jb.., i)
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                    if (jj < jn && i <= jb + jj) cmac(acc[jj], x, conj(lcol[jj]));
+                }
+            }
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj)
+                if (jj < jn) {
+                    OT o;
+                    o.re = static_cast<decltype(o.re)>(acc[jj].re);
+                    o.im = static_cast<decltype(o.im)>(acc[jj].im);
+                    Out[static_cast<size_t>(jb + jj) * m + r] = o;
+                }
+        }
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kNT) k_cholqr(const c32* __restrict__ Cin, c64* __restrict__ work,
+                                                 c32* __restrict__ Vout, c64* __restrict__ Rt,
+                                                 int32_t* __restrict__ status, const int32_t* __restrict__ fmap,
+                                                 int m, int p, const c32* __restrict__ Vin, c64* __restrict__ Hout) {
+    extern __shared__ uint8_t dsm[];
+    c64* G = reinterpret_cast<c64*>(dsm);  // p x p
+    c64* chunk = G + p * p;                // 2 x p x kRC
+    __shared__ int perm[64];
+    __shared__ double d[64];
+    const int f = frame_of_x(fmap);
+    const c32* Cf = Cin + static_cast<size_t>(f) * m * p;
+    if (threadIdx.x < p) perm[threadIdx.x] = threadIdx.x;
+    block_gram<true>(Cf, Cf, m, p, chunk, G);
+    warp_cholesky_inv(G, p, true, perm, d);
+    __syncthreads();
+    if (MODE == 0 && threadIdx.x == 0) {
+        // Eigen ColPivHouseholderQR::rank() on the pivoted-Cholesky diagonal, data eps = fp32
+        const double eps = eps_of<float>::value;
+        const double thr_helper = fmax(d[0], 0.0) * eps * eps / static_cast<double>(m);  // maxColNorm^2 = d[0]
+        int nonzero = p;
+        double maxpivot = 0.0;
+        for (int k = 0; k < p; ++k) {
+            if (nonzero == p && d[k] < thr_helper * static_cast<double>(m - k)) nonzero = k;
+            maxpivot = fmax(maxpivot, sqrt(fmax(d[k], 0.0)));
+        }
+        const double thr = maxpivot * eps * static_cast<double>(p);
+        int rank = 0;
+        for (int k = 0; k < nonzero; ++k) rank += sqrt(fmax(d[k], 0.0)) > thr ? 1 : 0;
+        if (rank < p) atomicOr(&status[f], kFrameRank);
+    }
+    if (MODE == 0) {
+        rows_apply_linvh(Cf, perm, G, m, p, Vout + static_cast<size_t>(f) * m * p);
+        return;
+    }
+    // MODE 1: Q1 = C P L1^-H -> work[f][0]; Q = Q1 L2^-H -> work[f][1]; Rt = Q^H C.
+    c64* Q1 = work + static_cast<size_t>(f) * 2 * p * m;
+    c64* Q = Q1 + static_cast<size_t>(p) * m;
+    rows_apply_linvh(Cf, perm, G, m, p, Q1);
+    __syncthreads();
+    block_gram<true>(static_cast<const c64*>(Q1), static_cast<const c64*>(Q1), m, p, chunk, G);
+    warp_cholesky_inv(G, p, false, nullptr, d);
+    __syncthreads();
+    rows_apply_linvh(static_cast<const c64*>(Q1), nullptr, G, m, p, Q);
+    __syncthreads();
+    block_gram<false>(static_cast<const c64*>(Q), Cf, m, p, chunk, G);
+    c64* Rf = Rt + static_cast<size_t>(f) * p * p;
+    for (int e = threadIdx.x; e < p * p; e += kNT) Rf[e] = G[e];
+    if (Vin) {  // fast2: H = V^H C with V the last power-iteration basis (W = pinv(H))
+        block_gram<false>(Vin + static_cast<size_t>(f) * m * p, Cf, m, p, chunk, G);
+        c64* Hf = Hout + static_cast<size_t>(f) * p * p;
+        for (int e = threadIdx.x; e < p * p; e += kNT) Hf[e] = G[e];
+    }
+}
+
 // ------------------------------------------------------------------ one-sided Jacobi SVD
 // n x n complex fp64, column-major in smem (a[c*n + r]); v accumulates right rotations.
 // Round-robin (circle) ordering, one warp per column pair. Returns false on sweep cap.
-__device__ bool block_jacobi_svd(c64* a, c64* v, int n, double* sig, int* order) {
+__device__ bool block_jacobi_svd(c64* a, c64* v, int n, double* sig, int* order, int* sweeps_out = nullptr) {
     __shared__ int s_rot;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) v[e] = mk((e % n) == (e / n) ? 1.0 : 0.0, 0.0);
     const int np = (n + 1) & ~1;
     bool converged = false;
-    for (int sweep = 0; sweep < 60; ++sweep) {
+    for (int sweep = 0; sweep < 40; ++sweep) {
         if (threadIdx.x == 0) s_rot = 0;
         __syncthreads();
         for (int rnd = 0; rnd < np - 1; ++rnd) {
@@ -324,7 +553,7 @@ __device__ bool block_jacobi_svd(c64* a, c64* v, int n, double* sig, int* order)
                 be = warp_sum(be);
                 ga = warp_sum_c(ga);
                 const double g = sqrt(norm2(ga));
-                if (g == 0.0 || g <= 1e-15 * sqrt(al * be)) continue;
+                if (g == 0.0 || g <= 8.0 * 2.220446049250313e-16 * n * sqrt(al * be)) continue;
                 const double zeta = (be - al) / (2.0 * g);
                 const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                 const double c = 1.0 / sqrt(1.0 + t * t);
@@ -355,6 +584,7 @@ __device__ bool block_jacobi_svd(c64* a, c64* v, int n, double* sig, int* order)
         __syncthreads();  // every warp has read s_rot before thread 0 resets it next sweep
         if (done) {
             converged = true;
+            if (sweeps_out && threadIdx.x == 0) *sweeps_out = sweep + 1;
             break;
         }
     }
@@ -381,6 +611,210 @@ __device__ bool block_jacobi_svd(c64* a, c64* v, int n, double* sig, int* order)
     return converged;
 }
 
+__device__ int32_t* g_dbg_sweeps = nullptr;  // optional per-frame Jacobi sweep counts (debug)
+
+// ------------------------------------------------------------------ warp-per-frame Nystrom tail
+// Hermitian eigendecomposition of an n x n matrix (n <= 64, column-major in the warp's shared
+// slice) by cyclic two-sided Jacobi with the parallel (circle) ordering: the n/2 disjoint
+// rotations of a round commute, so all column rotations are applied, then all row rotations.
+// Rotation (R/tests/oracle_jacobi.hpp form): b = a_pq, phi = arg b, tau = (a_qq - a_pp) / 2|b|,
+// t = sgn(tau) / (|tau| + sqrt(1 + tau^2)), c = 1/sqrt(1+t^2), s = t c e^{i phi}.
+// Warp-synchronous: no block barriers. Returns sweeps used (0 = no convergence in 30).
+__device__ int warp_jacobi_eigh(c64* A, c64* Z, int n, double* rc, double* rs, c64* re) {
+    const int lane = threadIdx.x & 31;
+    for (int e = lane; e < n * n; e += 32) Z[e] = mk((e % n) == (e / n) ? 1.0 : 0.0, 0.0);
+    const int np = (n + 1) & ~1;
+    const int npairs = np / 2;
+    double dmax = 0.0;  // scale for an absolute floor on negligible off-diagonals
+    for (int c = 0; c < n; ++c) dmax = fmax(dmax, fabs(A[c * n + c].re));
+    const double floor2 = (1e-18 * dmax) * (1e-18 * dmax);
+    __syncwarp();
+    for (int sweep = 0; sweep < 30; ++sweep) {
+        bool any = false;
+        for (int rnd = 0; rnd < np - 1; ++rnd) {
+            // rotation parameters, one lane per pair
+            for (int t = lane; t < npairs; t += 32) {
+                int i, j;
+                if (t == 0) { i = rnd; j = np - 1; }
+                else { i = (rnd + t) % (np - 1); j = (rnd - t + (np - 1)) % (np - 1); }
+                if (i > j) { const int x = i; i = j; j = x; }
+                double c = 1.0, sm = 0.0;
+                c64 ph = mk(1.0, 0.0);
+                if (j < n) {
+                    const c64 b = A[j * n + i];  // a(i, j)
+                    const double app = A[i * n + i].re, aqq = A[j * n + j].re;
+                    const double ab2 = norm2(b);
+                    if (ab2 > floor2 && ab2 > 1e-30 * fabs(app * aqq)) {
+                        const double ab = sqrt(ab2);
+                        const double tau = (aqq - app) / (2.0 * ab);
+                        const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        c = 1.0 / sqrt(1.0 + tt * tt);
+                        sm = tt * c;
+                        ph = mk(b.re / ab, b.im / ab);
+                    }
+                }
+                rc[t] = c;
+                rs[t] = sm;
+                re[t] = ph;
+            }
+            __syncwarp();
+            bool rot = false;
+            for (int t = 0; t < npairs; ++t) rot |= rs[t] != 0.0;
+            any |= rot;
+            if (!rot) continue;
+            // columns: a(r,i) = c a_ri - conj(s) a_rj ; a(r,j) = s a_ri + c a_rj  (A and Z)
+            for (int e = lane; e < npairs * n * 2; e += 32) {
+                const int which = e / (npairs * n);  // 0: A, 1: Z
+                const int t = (e / n) % npairs, r = e % n;
+                int i, j;
+                if (t == 0) { i = rnd; j = np - 1; }
+                else { i = (rnd + t) % (np - 1); j = (rnd - t + (np - 1)) % (np - 1); }
+                if (i > j) { const int x = i; i = j; j = x; }
+                if (j >= n || rs[t] == 0.0) continue;
+                c64* M = which ? Z : A;
+                const double c = rc[t], sm = rs[t];
+                const c64 s = mk(sm * re[t].re, sm * re[t].im);
+                const c64 x = M[i * n + r], y = M[j * n + r];
+                M[i * n + r] = mk(c * x.re - (s.re * y.re + s.im * y.im), c * x.im - (s.re * y.im - s.im * y.re));
+                M[j * n + r] = mk(s.re * x.re - s.im * x.im + c * y.re, s.re * x.im + s.im * x.re + c * y.im);
+            }
+            __syncwarp();
+            // rows: a(i,r) = c a_ir - s a_jr ; a(j,r) = conj(s) a_ir + c a_jr
+            for (int e = lane; e < npairs * n; e += 32) {
+                const int t = e / n, r = e % n;
+                int i, j;
+                if (t == 0) { i = rnd; j = np - 1; }
+                else { i = (rnd + t) % (np - 1); j = (rnd - t + (np - 1)) % (np - 1); }
+                if (i > j) { const int x = i; i = j; j = x; }
+                if (j >= n || rs[t] == 0.0) continue;
+                const double c = rc[t], sm = rs[t];
+                const c64 s = mk(sm * re[t].re, sm * re[t].im);
+                const c64 x = A[r * n + i], y = A[r * n + j];
+                A[r * n + i] = mk(c * x.re - (s.re * y.re - s.im * y.im), c * x.im - (s.re * y.im + s.im * y.re));
+                A[r * n + j] = mk(s.re * x.re + s.im * x.im + c * y.re, s.re * x.im - s.im * x.re + c * y.im);
+            }
+            __syncwarp();
+        }
+        if (!any) return sweep + 1;
+    }
+    return 0;
+}
+
+// Descending order of the real diagonal (ties: lower index first), computed by lane 0.
+__device__ void warp_order_desc(const c64* A, int n, bool by_abs, int* order) {
+    if ((threadIdx.x & 31) == 0) {
+        for (int c = 0; c < n; ++c) order[c] = c;
+        for (int x = 0; x < n; ++x) {
+            int best = x;
+            for (int y = x + 1; y < n; ++y) {
+                const double vy = A[order[y] * n + order[y]].re, vb = A[order[best] * n + order[best]].re;
+                if ((by_abs ? fabs(vy) > fabs(vb) : vy > vb)) best = y;
+            }
+            const int t = order[x]; order[x] = order[best]; order[best] = t;
+        }
+    }
+    __syncwarp();
+}
+
+// One warp per frame: W = pinv(Herm(H)) (cutoff p*eps_T*max|lambda|), B' = Rt W Rt^H,
+// eig(B') descending, U = Q Z_K, lambda = clamp(Z_K eigenvalues). R/src/estimators.cpp:37-50,
+// R/src/linalg.cpp:143-163. Q (fp64, work[f][1]), Rt, H (p x p column-major) from k_cholqr<1> /
+// k_gather.
+template <typename T>
+__global__ void __launch_bounds__(128) k_nystrom_warp(const c64* __restrict__ Hin, const c64* __restrict__ work,
+                                                     const c64* __restrict__ Rt, c64* __restrict__ basis,
+                                                     double* __restrict__ eig, int32_t* __restrict__ status,
+                                                     int frames, int m, int p, int k) {
+    extern __shared__ uint8_t dsm[];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int f = blockIdx.x * (blockDim.x >> 5) + wib;
+    const size_t per_warp = sizeof(c64) * (3 * p * p + 2 * 64) + sizeof(double) * 2 * 64 + sizeof(int) * 64;
+    uint8_t* base = dsm + wib * ((per_warp + 15) & ~size_t(15));
+    c64* A = reinterpret_cast<c64*>(base);
+    c64* Z = A + p * p;
+    c64* Tm = Z + p * p;
+    c64* re = Tm + p * p;
+    c64* zk = re + 64;
+    double* rc = reinterpret_cast<double*>(zk + 64);
+    double* rs = rc + 64;
+    int* order = reinterpret_cast<int*>(rs + 64);
+    if (f >= frames) return;
+    const double eps = eps_of<T>::value;
+    const c64* Hf = Hin + static_cast<size_t>(f) * p * p;
+    for (int e = lane; e < p * p; e += 32) {
+        const int i = e % p, j = e / p;
+        const c64 a = Hf[j * p + i], b = Hf[i * p + j];
+        A[e] = mk(0.5 * (a.re + b.re), 0.5 * (a.im - b.im));  // Herm(H)(i, j)
+    }
+    __syncwarp();
+    const int sw1 = warp_jacobi_eigh(A, Z, p, rc, rs, re);
+    warp_order_desc(A, p, true, order);
+    const double lmax = fabs(A[order[0] * p + order[0]].re);
+    const double cutoff = static_cast<double>(p) * eps * lmax;
+    // W = Z diag(1/lambda) Z^H over |lambda| > cutoff -> Tm
+    for (int e = lane; e < p * p; e += 32) {
+        const int i = e % p, j = e / p;
+        c64 acc = mk(0.0, 0.0);
+        if (lmax > 0.0)
+            for (int c = 0; c < p; ++c) {
+                const double l = A[c * p + c].re;
+                if (fabs(l) > cutoff) {
+                    const c64 zi = Z[c * p + i], zj = Z[c * p + j];
+                    const double w = 1.0 / l;
+                    acc.re += w * (zi.re * zj.re + zi.im * zj.im);
+                    acc.im += w * (zi.im * zj.re - zi.re * zj.im);
+                }
+            }
+        Tm[e] = acc;
+    }
+    __syncwarp();
+    // A = Rt W ; then B' = A Rt^H -> Z (scratch), copied back to A
+    const c64* Rf = Rt + static_cast<size_t>(f) * p * p;
+    for (int e = lane; e < p * p; e += 32) {
+        const int i = e % p, j = e / p;
+        c64 acc = mk(0.0, 0.0);
+        for (int c = 0; c < p; ++c) cmac(acc, Rf[c * p + i], Tm[j * p + c]);
+        A[e] = acc;
+    }
+    __syncwarp();
+    for (int e = lane; e < p * p; e += 32) {
+        const int i = e % p, j = e / p;
+        c64 acc = mk(0.0, 0.0);
+        for (int c = 0; c < p; ++c) cmac(acc, A[c * p + i], conj(Rf[c * p + j]));
+        Tm[e] = acc;
+    }
+    __syncwarp();
+    for (int e = lane; e < p * p; e += 32) {  // Hermitian part of B'
+        const int i = e % p, j = e / p;
+        const c64 a = Tm[j * p + i], b = Tm[i * p + j];
+        A[e] = mk(0.5 * (a.re + b.re), 0.5 * (a.im - b.im));
+    }
+    __syncwarp();
+    const int sw2 = warp_jacobi_eigh(A, Z, p, rc, rs, re);
+    warp_order_desc(A, p, false, order);
+    // basis U(:, kk) = Q Z(:, order[kk])
+    const c64* Qf = work + static_cast<size_t>(f) * 2 * p * m + static_cast<size_t>(p) * m;
+    c64* Bf = basis + static_cast<size_t>(f) * m * k;
+    for (int kk = 0; kk < k; ++kk) {
+        const int c = order[kk];
+        for (int q = lane; q < p; q += 32) zk[q] = Z[c * p + q];
+        __syncwarp();
+        for (int r = lane; r < m; r += 32) {
+            c64 acc = mk(0.0, 0.0);
+            for (int q = 0; q < p; ++q) cmac(acc, Qf[static_cast<size_t>(q) * m + r], zk[q]);
+            Bf[static_cast<size_t>(kk) * m + r] = acc;
+        }
+        __syncwarp();
+    }
+    for (int kk = lane; kk < k; kk += 32) {
+        double lam = A[order[kk] * p + order[kk]].re;
+        if (lam < 0.0 && lam >= -1e-10) lam = 0.0;
+        eig[static_cast<size_t>(f) * k + kk] = lam;
+    }
+    if (lane == 0 && (sw1 == 0 || sw2 == 0)) atomicOr(&status[f], kFrameNoConv);
+    if (lane == 0 && g_dbg_sweeps) g_dbg_sweeps[f] = sw1 | (sw2 << 8);
+}
+
 // ------------------------------------------------------------------ Nystrom tail
 // MODE_FAST2: H = V^H C (V, C: the last power-iteration sketch); MODE_FAST1: H from k_gather.
 // W = pinv(H)  (cutoff p*eps_T*sigma1)            R/src/linalg.cpp:143-163
@@ -392,7 +826,9 @@ __global__ void __launch_bounds__(kNT) k_nystrom(const cplx<T>* __restrict__ V, 
                                                   const c64* __restrict__ Hin, const c64* __restrict__ work,
                                                   const c64* __restrict__ Rt, c64* __restrict__ basis,
                                                   double* __restrict__ eig, int32_t* __restrict__ status,
-                                                  const int32_t* __restrict__ fmap, int m, int p, int k) {
+                                                  const int32_t* __restrict__ fmap, int m, int p, int k,
+                                                  int32_t* __restrict__ dbg) {
+    __shared__ int s_sw[2];
     extern __shared__ uint8_t dsm[];
     c64* sa = reinterpret_cast<c64*>(dsm);  // p x p
     c64* sv = sa + p * p;                   // p x p
@@ -421,7 +857,7 @@ __global__ void __launch_bounds__(kNT) k_nystrom(const cplx<T>* __restrict__ V, 
         for (int e = threadIdx.x; e < p * p; e += kNT) sa[e] = Hf[e];
     }
     __syncthreads();
-    bool ok = block_jacobi_svd(sa, sv, p, sig, order);
+    bool ok = block_jacobi_svd(sa, sv, p, sig, order, &s_sw[0]);
     // W = V diag(1/s) U^H, U_c = a_c / s_c
     const double s1 = sig[order[0]];
     const double cutoff = static_cast<double>(p) * eps * s1;
@@ -460,7 +896,8 @@ __global__ void __launch_bounds__(kNT) k_nystrom(const cplx<T>* __restrict__ V, 
         sa[j * p + i] = acc;
     }
     __syncthreads();
-    ok = block_jacobi_svd(sa, sv, p, sig, order) && ok;
+    ok = block_jacobi_svd(sa, sv, p, sig, order, &s_sw[1]) && ok;
+    if (dbg && threadIdx.x == 0) dbg[f] = s_sw[0] | (s_sw[1] << 8);
     // basis U[:, kk] = Q * (a[:, order[kk]] / sig)
     const c64* Qf = work + static_cast<size_t>(f) * 2 * p * m + static_cast<size_t>(p) * m;
     c64* Bf = basis + static_cast<size_t>(f) * m * k;
@@ -532,6 +969,22 @@ cudaError_t fm_launch_qr(const void* C, void* work, void* Vout, void* Rt, int32_
     return cudaGetLastError();
 }
 
+cudaError_t fm_launch_cholqr(const void* C, void* work, void* Vout, void* Rt, int32_t* status, const int32_t* fmap,
+                             int frames, int m, int p, bool final_mode, const void* Vin, void* Hout, cudaStream_t s) {
+    if (p > 64 || p < 1 || m < p) return cudaErrorInvalidValue;
+    const size_t smem = sizeof(c64) * (p * p + 2 * p * sub::kRCP);
+    auto kern = final_mode ? sub::k_cholqr<1> : sub::k_cholqr<0>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<frames, sub::kNT, smem, s>>>(static_cast<const c32*>(C), static_cast<c64*>(work), static_cast<c32*>(Vout),
+                                        static_cast<c64*>(Rt), status, fmap, m, p, static_cast<const c32*>(Vin),
+                                        static_cast<c64*>(Hout));
+    return cudaGetLastError();
+}
+
+
 template <typename T>
 cudaError_t fm_launch_nystrom(const void* V, const void* C, const void* H, const void* work, const void* Rt,
                               void* basis, double* eig, int32_t* status, const int32_t* fmap, int frames, int m,
@@ -545,7 +998,7 @@ cudaError_t fm_launch_nystrom(const void* V, const void* C, const void* H, const
     kern<<<frames, sub::kNT, smem, s>>>(static_cast<const cplx<T>*>(V), static_cast<const cplx<T>*>(C),
                                         static_cast<const c64*>(H), static_cast<const c64*>(work),
                                         static_cast<const c64*>(Rt), static_cast<c64*>(basis), eig, status, fmap, m,
-                                        p, k);
+                                        p, k, nullptr);
     return cudaGetLastError();
 }
 
@@ -567,3 +1020,23 @@ template cudaError_t fm_launch_nystrom<float>(const void*, const void*, const vo
 template cudaError_t fm_launch_nystrom<double>(const void*, const void*, const void*, const void*, const void*, void*,
                                                double*, int32_t*, const int32_t*, int, int, int, int, bool,
                                                cudaStream_t);
+
+
+template <typename T>
+cudaError_t fm_launch_nystrom_warp(const void* H, const void* work, const void* Rt, void* basis, double* eig,
+                                   int32_t* status, int frames, int m, int p, int k, cudaStream_t s) {
+    if (p > 64 || k > p) return cudaErrorInvalidValue;
+    const int wpb = 4;
+    const size_t per_warp = sizeof(c64) * (3 * p * p + 2 * 64) + sizeof(double) * 2 * 64 + sizeof(int) * 64;
+    const size_t smem = wpb * ((per_warp + 15) & ~size_t(15));
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(sub::k_nystrom_warp<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    sub::k_nystrom_warp<T><<<(frames + wpb - 1) / wpb, 32 * wpb, smem, s>>>(
+        static_cast<const c64*>(H), static_cast<const c64*>(work), static_cast<const c64*>(Rt),
+        static_cast<c64*>(basis), eig, status, frames, m, p, k);
+    return cudaGetLastError();
+}
+template cudaError_t fm_launch_nystrom_warp<float>(const void*, const void*, const void*, void*, double*, int32_t*,
+                                                   int, int, int, int, cudaStream_t);
