@@ -129,7 +129,10 @@ fm_status fm_rerun_frames(fm_plan plan, int64_t count, const int32_t* d_frames, 
  * profiling was enabled (or last read), their count in *runs, and restarts the count. */
 fm_status fm_plan_set_profiling(fm_plan plan, int32_t on);
 fm_status fm_plan_stage_times(fm_plan plan, float* ms4, int32_t* runs);
-/* Number of kernel launches one fm_run_batch enqueues. */
+/* Split each fm_run_batch into `subbatches` frame ranges run concurrently on plan-owned
+ * streams forked from / joined into the caller's stream (0 = automatic: 4 when frames >= 512). */
+fm_status fm_plan_set_concurrency(fm_plan plan, int32_t subbatches);
+/* Number of kernel launches one fm_run_batch enqueues (per sub-batch). */
 int32_t fm_plan_launches_per_batch(fm_plan plan);
 
 /* End-to-end, host buffers (the reference-facing call): H2D of x and of the per-frame draws

@@ -327,6 +327,10 @@ class BatchPlan:
         _check(LIB.fm_plan_stage_times(self.handle, ptr(ms), C.byref(runs)))
         return dict(zip(("covariance", "subspace", "autocorr", "spectrum_peaks"), ms.astype(float))), runs.value
 
+    def set_concurrency(self, subbatches: int):
+        """Run each batch as `subbatches` concurrent frame ranges (0 = automatic)."""
+        _check(LIB.fm_plan_set_concurrency(self.handle, subbatches))
+
     def launches_per_batch(self) -> int:
         return int(LIB.fm_plan_launches_per_batch(self.handle))
 

@@ -349,6 +349,10 @@ struct fm_plan_s {
     std::vector<cudaEvent_t> ev;
     int prof_runs = 0;
     int cur = 0;
+    // concurrent sub-batches: plan-owned streams forked from / joined into the caller's stream
+    int nsub = 0;  // 0 = automatic
+    std::vector<cudaStream_t> sub;
+    std::vector<cudaEvent_t> sub_ev;  // [0] fork, [1..] joins
     std::vector<void*> allocs;
 
     template <typename T>
@@ -372,6 +376,10 @@ struct fm_plan_s {
         for (void* q : allocs) cudaFree(q);
         for (cudaEvent_t e : ev)
             if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : sub_ev)
+            if (e) cudaEventDestroy(e);
+        for (cudaStream_t q : sub)
+            if (q) cudaStreamDestroy(q);
         if (omega_pinned) cudaFreeHost(omega_pinned);
         if (status_pinned) cudaFreeHost(status_pinned);
         cudaSetDevice(prev);
@@ -519,68 +527,119 @@ static void mark(fm_plan pl, int i, cudaStream_t s) {
     cudaEventRecord(pl->ev[static_cast<size_t>(pl->cur) * 5 + i], s);
 }
 
-static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io, const float* R, cudaStream_t s) {
+// Per-sub-batch view of the plan workspace (pointers offset to the sub-batch's first frame).
+struct WorkView {
+    float* C;
+    float* V;
+    double* work;
+    double* Rt;
+    double* H;
+    double* basis;
+    double* eig;
+    double* t;
+    int32_t* scratch;
+};
+
+static WorkView work_view(fm_plan pl, int64_t f0) {
+    const auto& d = pl->d;
+    const size_t M = d.m, P = d.method == FM_METHOD_EXACT ? 0 : d.p, K = d.k;
+    const size_t MP = (M + 15) / 16 * 16;
+    const size_t wsz = d.method == FM_METHOD_EXACT ? MP * MP * 2 : 2 * P * M * 2;
+    WorkView w;
+    w.C = pl->C + f0 * P * M * 2;
+    w.V = pl->V + f0 * P * M * 2;
+    w.work = pl->work + f0 * wsz;
+    w.Rt = pl->Rt + f0 * P * P * 2;
+    w.H = pl->H + f0 * P * P * 2;
+    w.basis = pl->basis + f0 * K * M * 2;
+    w.eig = pl->eig + f0 * K;
+    w.t = pl->t + f0 * M * 2;
+    w.scratch = pl->scratch_status + f0;
+    return w;
+}
+
+static fm_batch_io io_view(fm_plan pl, const fm_batch_io* io, int64_t f0) {
+    const auto& d = pl->d;
+    const size_t M = d.m, N = d.n, P = d.p, K = d.k, L = d.grid_size;
+    fm_batch_io o = *io;
+    o.x = io->x + f0 * M * N * 2;
+    if (io->omega) o.omega = io->omega + f0 * M * P;
+    if (io->indices) o.indices = io->indices + f0 * P;
+    if (io->spectrum) o.spectrum = io->spectrum + f0 * L;
+    o.peak_cells = io->peak_cells + f0 * K;
+    o.peak_heights = io->peak_heights + f0 * K;
+    o.baseline = io->baseline + f0;
+    o.peak_count = io->peak_count + f0;
+    o.status = io->status + f0;
+    if (io->basis) o.basis = io->basis + f0 * K * M * 2;
+    if (io->eigenvalues) o.eigenvalues = io->eigenvalues + f0 * K;
+    if (io->covariance) o.covariance = io->covariance + f0 * M * M * 2;
+    return o;
+}
+
+static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io, const float* R, cudaStream_t s,
+                              const WorkView& w, bool prof) {
     const auto& d = pl->d;
     const int F = static_cast<int>(frames), M = static_cast<int>(d.m), P = static_cast<int>(d.p),
               K = static_cast<int>(d.k);
-    double* basis = io->basis ? io->basis : pl->basis;
-    double* eig = io->eigenvalues ? io->eigenvalues : pl->eig;
+    double* basis = io->basis ? io->basis : w.basis;
+    double* eig = io->eigenvalues ? io->eigenvalues : w.eig;
     k_clear_bits<<<(F + 255) / 256, 256, 0, s>>>(io->status, F, FM_FRAME_RANK | FM_FRAME_NOCONV);
     FM_CUDA_OK(cudaGetLastError());
     const bool warp_path = P <= 32;  // block-per-frame small-matrix kernels (smallmat.cu)
     const bool tiled = P <= 32 && (P % 4) == 0;  // register-tiled Gram + fused final stage
     auto orth = [&](bool final_mode, const void* vin) -> fm_status {
         if (tiled && !final_mode) {
-            FM_LAUNCH(fm_launch_orth_tiled(pl->C, pl->V, io->status, F, M, P, s));
+            FM_LAUNCH(fm_launch_orth_tiled(w.C, w.V, io->status, F, M, P, s));
             return FM_OK;
         }
         if (warp_path)
-            FM_LAUNCH(fm_launch_cholqr_warp(pl->C, pl->work, final_mode ? nullptr : pl->V, pl->Rt, pl->H, vin,
-                                            final_mode ? pl->scratch_status : io->status, F, M, P, final_mode, s));
+            FM_LAUNCH(fm_launch_cholqr_warp(w.C, w.work, final_mode ? nullptr : w.V, w.Rt, w.H, vin,
+                                            final_mode ? w.scratch : io->status, F, M, P, final_mode, s));
         else
-            FM_LAUNCH(fm_launch_cholqr(pl->C, pl->work, final_mode ? nullptr : pl->V, final_mode ? pl->Rt : nullptr,
-                                       final_mode ? pl->scratch_status : io->status, nullptr, F, M, P, final_mode,
-                                       vin, pl->H, s));
+            FM_LAUNCH(fm_launch_cholqr(w.C, w.work, final_mode ? nullptr : w.V, final_mode ? w.Rt : nullptr,
+                                       final_mode ? w.scratch : io->status, nullptr, F, M, P, final_mode,
+                                       vin, w.H, s));
         return FM_OK;
     };
     auto nystrom = [&]() -> fm_status {
         if (warp_path)
-            FM_LAUNCH(fm_launch_nystrom_warp2(pl->H, pl->work, pl->Rt, basis, eig, io->status, F, M, P, K, s));
+            FM_LAUNCH(fm_launch_nystrom_warp2(w.H, w.work, w.Rt, basis, eig, io->status, F, M, P, K, s));
         else
-            FM_LAUNCH(fm_launch_nystrom_warp<float>(pl->H, pl->work, pl->Rt, basis, eig, io->status, F, M, P, K, s));
+            FM_LAUNCH(fm_launch_nystrom_warp<float>(w.H, w.work, w.Rt, basis, eig, io->status, F, M, P, K, s));
         return FM_OK;
     };
     fm_status st = FM_OK;
     if (d.method == FM_METHOD_FAST2) {
-        FM_LAUNCH(fm_launch_rmul<float>(R, io->omega, nullptr, pl->C, nullptr, F, M, P, true, s));
+        FM_LAUNCH(fm_launch_rmul<float>(R, io->omega, nullptr, w.C, nullptr, F, M, P, true, s));
         for (int it = 0; it < d.t; ++it) {
             if ((st = orth(false, nullptr)) != FM_OK) return st;
-            FM_LAUNCH(fm_launch_rmul<float>(R, nullptr, pl->V, pl->C, nullptr, F, M, P, false, s));
+            FM_LAUNCH(fm_launch_rmul<float>(R, nullptr, w.V, w.C, nullptr, F, M, P, false, s));
         }
         if (tiled) {
-            FM_LAUNCH(fm_launch_final_tiled(pl->C, pl->V, nullptr, basis, eig, io->status, F, M, P, K, s));
+            FM_LAUNCH(fm_launch_final_tiled(w.C, w.V, nullptr, basis, eig, io->status, F, M, P, K, s));
         } else {
-            if ((st = orth(true, pl->V)) != FM_OK) return st;
+            if ((st = orth(true, w.V)) != FM_OK) return st;
             if ((st = nystrom()) != FM_OK) return st;
         }
     } else if (d.method == FM_METHOD_FAST1) {
-        FM_LAUNCH(fm_launch_gather<float>(R, io->indices, pl->C, pl->H, nullptr, F, M, P, s));
+        FM_LAUNCH(fm_launch_gather<float>(R, io->indices, w.C, w.H, nullptr, F, M, P, s));
         if (tiled) {
-            FM_LAUNCH(fm_launch_final_tiled(pl->C, nullptr, pl->H, basis, eig, io->status, F, M, P, K, s));
+            FM_LAUNCH(fm_launch_final_tiled(w.C, nullptr, w.H, basis, eig, io->status, F, M, P, K, s));
         } else {
             if ((st = orth(true, nullptr)) != FM_OK) return st;
             if ((st = nystrom()) != FM_OK) return st;
         }
     } else {
-        FM_LAUNCH(fm_launch_jacobi_eig<float>(R, pl->work, basis, eig, io->status, F, M, K, s));
+        FM_LAUNCH(fm_launch_jacobi_eig<float>(R, w.work, basis, eig, io->status, F, M, K, s));
     }
-    mark(pl, 2, s);
-    FM_LAUNCH(fm_launch_autocorr(basis, pl->t, F, M, K, s));
-    mark(pl, 3, s);
-    FM_LAUNCH(fm_launch_spectrum_peaks(pl->t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, nullptr,
+    if (prof) mark(pl, 2, s);
+    FM_LAUNCH(fm_launch_autocorr(basis, w.t, F, M, K, s));
+    if (prof) mark(pl, 3, s);
+    FM_LAUNCH(fm_launch_spectrum_peaks(w.t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, nullptr,
                                         K, static_cast<int>(d.min_sep_cells), io->peak_cells, io->peak_heights,
                                         io->baseline, io->peak_count, io->status, s));
-    mark(pl, 4, s);
+    if (prof) mark(pl, 4, s);
     return FM_OK;
 }
 
@@ -594,17 +653,65 @@ static fm_status check_io(fm_plan pl, int64_t frames, const fm_batch_io* io) {
     return FM_OK;
 }
 
+static int auto_subbatches(fm_plan pl, int64_t frames) {
+    if (pl->nsub > 0) return static_cast<int>(std::min<int64_t>(pl->nsub, frames));
+    if (const char* e = std::getenv("FM_SUBBATCHES")) return std::max(1, std::atoi(e));
+    return frames >= 512 ? 4 : 1;
+}
+
 extern "C" fm_status fm_run_batch(fm_plan pl, int64_t frames, const fm_batch_io* io, void* stream) {
     fm_status st = check_io(pl, frames, io);
     if (st != FM_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     FM_CUDA_OK(cudaSetDevice(pl->device));
     FM_CUDA_OK(cudaMemsetAsync(io->status, 0, sizeof(int32_t) * frames, s));
-    float* R = io->covariance ? io->covariance : pl->R;
-    mark(pl, 0, s);
-    FM_LAUNCH(fm_launch_cov_tc(io->x, R, io->status, frames, pl->d.m, pl->d.n, s));
-    mark(pl, 1, s);
-    return run_post_cov(pl, frames, io, R, s);
+    const int nsub = auto_subbatches(pl, frames);
+    if (nsub <= 1) {
+        float* R = io->covariance ? io->covariance : pl->R;
+        mark(pl, 0, s);
+        FM_LAUNCH(fm_launch_cov_tc(io->x, R, io->status, frames, pl->d.m, pl->d.n, s));
+        mark(pl, 1, s);
+        return run_post_cov(pl, frames, io, R, s, work_view(pl, 0), true);
+    }
+    while (static_cast<int>(pl->sub.size()) < nsub) {
+        cudaStream_t q;
+        FM_CUDA_OK(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
+        pl->sub.push_back(q);
+    }
+    while (static_cast<int>(pl->sub_ev.size()) < nsub + 1) {
+        cudaEvent_t e;
+        FM_CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        pl->sub_ev.push_back(e);
+    }
+    FM_CUDA_OK(cudaEventRecord(pl->sub_ev[0], s));
+    const int64_t chunk = (frames + nsub - 1) / nsub;
+    const size_t MM2 = static_cast<size_t>(pl->d.m) * pl->d.m * 2;
+    for (int i = 0; i < nsub; ++i) {
+        const int64_t f0 = i * chunk;
+        const int64_t nf = std::min<int64_t>(chunk, frames - f0);
+        if (nf <= 0) break;
+        cudaStream_t q = pl->sub[i];
+        FM_CUDA_OK(cudaStreamWaitEvent(q, pl->sub_ev[0], 0));
+        const fm_batch_io o = io_view(pl, io, f0);
+        float* R = io->covariance ? o.covariance : pl->R + f0 * MM2;
+        if (i == 0) mark(pl, 0, q);
+        {
+            cudaStream_t s = q;  // FM_LAUNCH synchronises `s` in debug mode
+            FM_LAUNCH(fm_launch_cov_tc(o.x, R, o.status, nf, pl->d.m, pl->d.n, q));
+        }
+        if (i == 0) mark(pl, 1, q);
+        st = run_post_cov(pl, nf, &o, R, q, work_view(pl, f0), i == 0);
+        if (st != FM_OK) return st;
+        FM_CUDA_OK(cudaEventRecord(pl->sub_ev[1 + i], q));
+        FM_CUDA_OK(cudaStreamWaitEvent(s, pl->sub_ev[1 + i], 0));
+    }
+    return FM_OK;
+}
+
+extern "C" fm_status fm_plan_set_concurrency(fm_plan plan, int32_t subbatches) {
+    if (!plan || subbatches < 0) return fail(FM_EINVAL, "fm_plan_set_concurrency: bad arguments");
+    plan->nsub = subbatches;
+    return FM_OK;
 }
 
 extern "C" fm_status fm_rerun_frames(fm_plan pl, int64_t frames, const int32_t* /*d_frames: all frames rerun*/, const fm_batch_io* io,
@@ -613,7 +720,7 @@ extern "C" fm_status fm_rerun_frames(fm_plan pl, int64_t frames, const int32_t* 
     if (st != FM_OK) return st;
     FM_CUDA_OK(cudaSetDevice(pl->device));
     const float* R = io->covariance ? io->covariance : pl->R;
-    return run_post_cov(pl, frames, io, R, static_cast<cudaStream_t>(stream));
+    return run_post_cov(pl, frames, io, R, static_cast<cudaStream_t>(stream), work_view(pl, 0), false);
 }
 
 extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const float* h_x, const uint64_t* draw_seeds,
