@@ -23,6 +23,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 
@@ -38,11 +39,13 @@ constexpr int kStagesO = 3;         // fp16 operand ring (UMMA source)
 constexpr int kStageBytes = kRows * kChunk * 8;   // 16 KB fp32 per operand side
 constexpr int kPlaneBytes = kRows * kChunk * 2;   // 4 KB fp16 per plane (Re or Im)
 constexpr int kOpBytes = 2 * kPlaneBytes;         // 8 KB per operand side
-constexpr int kThreads = 192;                     // w0 TMA, w1 MMA, w2..w5 convert + epilogue
+constexpr int kThreads = 320;                     // w0 TMA, w1 MMA, w2..w5 convert, w6..w9 epilogue
 constexpr int kSmemStaging = kStagesS * 2 * kStageBytes;
 constexpr int kSmemOperand = kStagesO * 2 * kOpBytes;
 constexpr int kSmemBarriers = 256;
-constexpr int kSmemBytes = 1024 + kSmemStaging + kSmemOperand + kSmemBarriers;
+constexpr int kEpiLd = 33;                                  // padded row (float2) of the transpose tile
+constexpr int kSmemEpilogue = 4 * 32 * kEpiLd * 8;          // 4 epilogue warps x 32x32 complex
+constexpr int kSmemBytes = 1024 + kSmemStaging + kSmemOperand + kSmemBarriers + kSmemEpilogue;
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -65,14 +68,19 @@ __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
-// Arrive on the barrier at the same smem offset in CTA `target` of the cluster.
+// Arrive on the barrier at the same smem offset in CTA `target` of the cluster (default
+// .release.cta semantics, as CUTLASS's ClusterBarrier::arrive(cta_id): a .release.cluster
+// arrive compiles to MEMBAR.ALL.GPU on every pipeline stage).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar, uint32_t target) {
     asm volatile(
         "{\n\t.reg .b32 ra;\n\t"
         "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
-        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(bar),
+        "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(bar),
         "r"(target)
         : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
@@ -199,9 +207,13 @@ __device__ __forceinline__ void convert_tile(const uint8_t* stage, uint8_t* op, 
     }
 }
 
+// Persistent: CTA pair `pair` processes tiles pair, pair + npairs, ... Warp roles:
+//   w0 TMA producer | w1 MMA issuer (leader) + TMEM owner | w2..w5 converters | w6..w9 epilogue.
+// The epilogue of tile i (TMEM -> fp32 R) overlaps the TMA + fp16 conversion of tile i + 1;
+// the MMA of tile i + 1 starts once both CTAs' epilogues have drained TMEM (acc_empty).
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cov_tc_kernel(const __grid_constant__ CUtensorMap xmap, float* __restrict__ r_out, int32_t* __restrict__ status,
-                  int m, int n, int tiles_per_frame) {
+                  int m, int n, int tiles_per_frame, int total_tiles) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* staging = smem;
@@ -212,32 +224,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* op_full = bars + 2 * kStagesS;
     uint64_t* op_empty = bars + 2 * kStagesS + kStagesO;
     uint64_t* acc_full = bars + 2 * kStagesS + 2 * kStagesO;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
-    int* flag_slot = reinterpret_cast<int*>(tmem_slot + 1);
+    uint64_t* acc_empty = acc_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+    float2* epi = reinterpret_cast<float2*>(operand + kSmemOperand + kSmemBarriers);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
-    const int tile = blockIdx.x >> 1;
-    const int frame = tile / tiles_per_frame;
-    int bi, bj;
-    tile_coords(tile % tiles_per_frame, bi, bj);
-    const bool diag = (bi == bj);
+    const int pair = blockIdx.x >> 1;
+    const int npairs = gridDim.x >> 1;
     const int nk = (n + kChunk - 1) / kChunk;
-    const int row_a = 256 * bi + 128 * static_cast<int>(rank);
-    const int row_b = 256 * bj + 128 * static_cast<int>(rank);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStagesS; ++s) {
             mbar_init(smem_u32(&stage_full[s]), 1);
-            mbar_init(smem_u32(&stage_empty[s]), 4);
+            mbar_init(smem_u32(&stage_empty[s]), 1);
         }
         for (int s = 0; s < kStagesO; ++s) {
-            mbar_init(smem_u32(&op_full[s]), 8);  // 4 converter warps x 2 CTAs (leader's copy used)
+            mbar_init(smem_u32(&op_full[s]), 2);  // one arrive per CTA (leader's copy used)
             mbar_init(smem_u32(&op_empty[s]), 1);
         }
         mbar_init(smem_u32(acc_full), 1);
-        *flag_slot = 0;
+        mbar_init(smem_u32(acc_empty), 2);  // one arrive per CTA's epilogue (leader's copy used)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -255,20 +263,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        // ---------------- TMA producer
+        // ---------------- TMA producer (one thread)
         if (lane == 0) {
-            const uint32_t bytes = diag ? kStageBytes : 2 * kStageBytes;
-            const int ya = frame * m + row_a;
-            const int yb = frame * m + row_b;
-            for (int kc = 0; kc < nk; ++kc) {
-                const int s = kc % kStagesS;
-                mbar_wait(smem_u32(&stage_empty[s]), ((kc / kStagesS) & 1) ^ 1);
-                const uint32_t full = smem_u32(&stage_full[s]);
-                mbar_arrive_expect_tx(full, bytes);
-                uint8_t* st = staging + s * 2 * kStageBytes;
-                const int x = 2 * kChunk * kc;
-                tma_load_2d(smem_u32(st), &xmap, full, x, ya);
-                if (!diag) tma_load_2d(smem_u32(st + kStageBytes), &xmap, full, x, yb);
+            int g = 0;
+            for (int tile = pair; tile < total_tiles; tile += npairs) {
+                const int frame = tile / tiles_per_frame;
+                int bi, bj;
+                tile_coords(tile % tiles_per_frame, bi, bj);
+                const bool diag = (bi == bj);
+                const uint32_t bytes = diag ? kStageBytes : 2 * kStageBytes;
+                const int ya = frame * m + 256 * bi + 128 * static_cast<int>(rank);
+                const int yb = frame * m + 256 * bj + 128 * static_cast<int>(rank);
+                for (int kc = 0; kc < nk; ++kc, ++g) {
+                    const int s = g % kStagesS;
+                    mbar_wait(smem_u32(&stage_empty[s]), ((g / kStagesS) & 1) ^ 1);
+                    const uint32_t full = smem_u32(&stage_full[s]);
+                    mbar_arrive_expect_tx(full, bytes);
+                    uint8_t* st = staging + s * 2 * kStageBytes;
+                    const int x = 2 * kChunk * kc;
+                    tma_load_2d(smem_u32(st), &xmap, full, x, ya);
+                    if (!diag) tma_load_2d(smem_u32(st + kStageBytes), &xmap, full, x, yb);
+                }
             }
         }
     } else if (warp == 1) {
@@ -276,84 +291,121 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (rank == 0 && lane == 0) {
             const uint32_t id_pos = umma_idesc(false);
             const uint32_t id_neg = umma_idesc(true);
-            for (int kc = 0; kc < nk; ++kc) {
-                const int o = kc % kStagesO;
-                mbar_wait_cluster(smem_u32(&op_full[o]), (kc / kStagesO) & 1);
+            int g = 0, t = 0;
+            for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
+                int bi, bj;
+                tile_coords(tile % tiles_per_frame, bi, bj);
+                const bool diag = (bi == bj);
+                mbar_wait_cluster(smem_u32(acc_empty), (t & 1) ^ 1);  // both epilogues drained TMEM
                 tc_fence_after();
-                const uint32_t a = smem_u32(operand + o * 2 * kOpBytes);
-                const uint32_t b = diag ? a : a + kOpBytes;
-                const uint64_t ar = umma_desc(a), ai = umma_desc(a + kPlaneBytes);
-                const uint64_t br = umma_desc(b), bim = umma_desc(b + kPlaneBytes);
-                const uint32_t acc = kc > 0 ? 1u : 0u;
-                umma_f16_2sm(tmem + 0, ar, br, id_pos, acc);
-                umma_f16_2sm(tmem + 0, ai, bim, id_pos, 1u);
-                umma_f16_2sm(tmem + 256, ai, br, id_pos, acc);
-                umma_f16_2sm(tmem + 256, ar, bim, id_neg, 1u);
-                umma_commit_mc(smem_u32(&op_empty[o]));
+                for (int kc = 0; kc < nk; ++kc, ++g) {
+                    const int o = g % kStagesO;
+                    mbar_wait_cluster(smem_u32(&op_full[o]), (g / kStagesO) & 1);
+                    tc_fence_after();
+                    const uint32_t a = smem_u32(operand + o * 2 * kOpBytes);
+                    const uint32_t b = diag ? a : a + kOpBytes;
+                    const uint64_t ar = umma_desc(a), ai = umma_desc(a + kPlaneBytes);
+                    const uint64_t br = umma_desc(b), bim = umma_desc(b + kPlaneBytes);
+                    const uint32_t acc = kc > 0 ? 1u : 0u;
+                    umma_f16_2sm(tmem + 0, ar, br, id_pos, acc);
+                    umma_f16_2sm(tmem + 0, ai, bim, id_pos, 1u);
+                    umma_f16_2sm(tmem + 256, ai, br, id_pos, acc);
+                    umma_f16_2sm(tmem + 256, ar, bim, id_neg, 1u);
+                    umma_commit_mc(smem_u32(&op_empty[o]));
+                }
+                umma_commit_mc(smem_u32(acc_full));
             }
-            umma_commit_mc(smem_u32(acc_full));
         }
-    } else {
-        // ---------------- converters (warps 2..5), then epilogue
+    } else if (warp < 6) {
+        // ---------------- converters (warps 2..5)
         const int cw = warp - 2;
-        float amax = 0.f;
-        bool nonfinite = false;
-        for (int kc = 0; kc < nk; ++kc) {
-            const int s = kc % kStagesS;
-            const int o = kc % kStagesO;
-            mbar_wait(smem_u32(&stage_full[s]), (kc / kStagesS) & 1);
-            mbar_wait(smem_u32(&op_empty[o]), ((kc / kStagesO) & 1) ^ 1);
-            const uint8_t* st = staging + s * 2 * kStageBytes;
-            uint8_t* op = operand + o * 2 * kOpBytes;
-            convert_tile(st, op, cw, lane, row_a, m, amax, nonfinite);
-            if (!diag) convert_tile(st + kStageBytes, op + kOpBytes, cw, lane, row_b, m, amax, nonfinite);
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive_local(smem_u32(&stage_empty[s]));
-                mbar_arrive_cluster(smem_u32(&op_full[o]), 0);
-            }
-        }
-        if (amax > 65504.f) atomicOr(flag_slot, kFrameRange);
-        if (nonfinite) atomicOr(flag_slot, kFrameNonFinite);
-
-        // ---------------- epilogue: TMEM -> registers -> fp32 R
-        mbar_wait(smem_u32(acc_full), 0);
-        tc_fence_after();
-        const int quarter = warp & 3;
-        const int row = 32 * quarter + lane;
-        const int gi = row_a + row;
-        const float inv_n = 1.0f / static_cast<float>(n);
-        const size_t fbase = static_cast<size_t>(frame) * m * m;
-        for (int c0 = 0; c0 < 256; c0 += 32) {
-            uint32_t vr[32], vi[32];
-            const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + c0;
-            tmem_ld32(taddr, vr);
-            tmem_ld32(taddr + 256, vi);
-            tmem_wait_ld();
-            if (gi < m) {
-                const int gj0 = 256 * bj + c0;
-                float2* dst = reinterpret_cast<float2*>(r_out + 2 * (fbase + static_cast<size_t>(gi) * m + gj0));
-#pragma unroll
-                for (int jj = 0; jj < 32; ++jj) {
-                    const int gj = gj0 + jj;
-                    if (gj < m) {
-                        float re = __uint_as_float(vr[jj]) * inv_n;
-                        float im = __uint_as_float(vi[jj]) * inv_n;
-                        if (gj == gi) im = 0.f;
-                        dst[jj] = make_float2(re, im);
-                        if (!diag) {
-                            r_out[2 * (fbase + static_cast<size_t>(gj) * m + gi)] = re;
-                            r_out[2 * (fbase + static_cast<size_t>(gj) * m + gi) + 1] = -im;
-                        }
-                    }
+        int g = 0;
+        for (int tile = pair; tile < total_tiles; tile += npairs) {
+            const int frame = tile / tiles_per_frame;
+            int bi, bj;
+            tile_coords(tile % tiles_per_frame, bi, bj);
+            const bool diag = (bi == bj);
+            const int row_a = 256 * bi + 128 * static_cast<int>(rank);
+            const int row_b = 256 * bj + 128 * static_cast<int>(rank);
+            float amax = 0.f;
+            bool nonfinite = false;
+            for (int kc = 0; kc < nk; ++kc, ++g) {
+                const int s = g % kStagesS;
+                const int o = g % kStagesO;
+                mbar_wait(smem_u32(&stage_full[s]), (g / kStagesS) & 1);
+                mbar_wait(smem_u32(&op_empty[o]), ((g / kStagesO) & 1) ^ 1);
+                const uint8_t* st = staging + s * 2 * kStageBytes;
+                uint8_t* op = operand + o * 2 * kOpBytes;
+                convert_tile(st, op, cw, lane, row_a, m, amax, nonfinite);
+                if (!diag) convert_tile(st + kStageBytes, op + kOpBytes, cw, lane, row_b, m, amax, nonfinite);
+                fence_proxy_async();
+                named_bar_sync(1, 128);  // all four converter warps done with this stage
+                if (warp == 2 && lane == 0) {
+                    mbar_arrive_local(smem_u32(&stage_empty[s]));
+                    if (rank == 0) mbar_arrive_local(smem_u32(&op_full[o]));
+                    else mbar_arrive_cluster(smem_u32(&op_full[o]), 0);
                 }
             }
+            int flag = (amax > 65504.f ? kFrameRange : 0) | (nonfinite ? kFrameNonFinite : 0);
+            flag = __reduce_or_sync(0xffffffffu, flag);
+            if (flag && lane == 0 && status != nullptr) atomicOr(&status[frame], flag);
         }
-        tc_fence_before();
+    } else {
+        // ---------------- epilogue (warps 6..9): TMEM -> registers -> fp32 R
+        const int quarter = warp & 3;
+        const int row = 32 * quarter + lane;
+        const float inv_n = 1.0f / static_cast<float>(n);
+        int t = 0;
+        for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
+            const int frame = tile / tiles_per_frame;
+            int bi, bj;
+            tile_coords(tile % tiles_per_frame, bi, bj);
+            const bool diag = (bi == bj);
+            const int gi = 256 * bi + 128 * static_cast<int>(rank) + row;
+            const size_t fbase = static_cast<size_t>(frame) * m * m;
+            mbar_wait(smem_u32(acc_full), t & 1);
+            tc_fence_after();
+            float2* T = epi + (warp - 6) * 32 * kEpiLd;  // this warp's 32 x 32 transpose tile
+            const int gi0 = 256 * bi + 128 * static_cast<int>(rank) + 32 * quarter;
+            for (int c0 = 0; c0 < 256; c0 += 32) {
+                uint32_t vr[32], vi[32];
+                const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + c0;
+                tmem_ld32(taddr, vr);
+                tmem_ld32(taddr + 256, vi);
+                tmem_wait_ld();
+                const int gj0 = 256 * bj + c0;
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) {
+                    const float re = __uint_as_float(vr[jj]) * inv_n;
+                    float im = __uint_as_float(vi[jj]) * inv_n;
+                    if (gj0 + jj == gi) im = 0.f;
+                    T[lane * kEpiLd + jj] = make_float2(re, im);
+                }
+                __syncwarp();
+                // coalesced: lane = column; one 256-byte row of R per store instruction
+                const int gj = gj0 + lane;
+                for (int r = 0; r < 32; ++r) {
+                    const int gr = gi0 + r;
+                    const float2 v = T[r * kEpiLd + lane];
+                    if (gr < m && gj < m) {
+                        reinterpret_cast<float2*>(r_out)[fbase + static_cast<size_t>(gr) * m + gj] = v;
+                        // mirrored block (off-diagonal tiles): R(gj, gr) = conj(R(gr, gj)); lanes -> rows gj:
+                        // strided, but only M >= 512 frames have off-diagonal tiles
+                        if (!diag) reinterpret_cast<float2*>(r_out)[fbase + static_cast<size_t>(gj) * m + gr] =
+                            make_float2(v.x, -v.y);
+                    }
+                }
+                __syncwarp();
+            }
+            tc_fence_before();
+            named_bar_sync(2, 128);  // all four epilogue warps finished reading TMEM
+            if (warp == 6 && lane == 0) {
+                if (rank == 0) mbar_arrive_local(smem_u32(acc_empty));
+                else mbar_arrive_cluster(smem_u32(acc_empty), 0);
+            }
+        }
     }
     __syncthreads();
-    if (threadIdx.x == 0 && *flag_slot != 0 && status != nullptr) atomicOr(&status[frame], *flag_slot);
     cluster_sync_all();
     if (warp == 1) {
         tc_fence_after();
@@ -408,8 +460,15 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
     const int nb = static_cast<int>((m + 255) / 256);
     const int tiles_per_frame = nb * (nb + 1) / 2;
     const int64_t tiles = frames * tiles_per_frame;
-    if (tiles * 2 > 0x7fffffff) return cudaErrorInvalidValue;
-    cov_tc_kernel<<<dim3(static_cast<unsigned>(2 * tiles)), kThreads, kSmemBytes, stream>>>(
-        map, d_r, d_status, static_cast<int>(m), static_cast<int>(n), tiles_per_frame);
+    if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
+    static int sm_count = 0;
+    if (!sm_count) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t pairs = std::min<int64_t>(tiles, std::max(1, sm_count / 2));
+    cov_tc_kernel<<<dim3(static_cast<unsigned>(2 * pairs)), kThreads, kSmemBytes, stream>>>(
+        map, d_r, d_status, static_cast<int>(m), static_cast<int>(n), tiles_per_frame, static_cast<int>(tiles));
     return cudaGetLastError();
 }
