@@ -55,6 +55,8 @@ cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K,
                                  double* heights, double* baseline, int32_t* count, int32_t* overflow,
                                  cudaStream_t s);
 cudaError_t fm_launch_orthocheck(const void* basis, int frames, int m, int k, double* dev, cudaStream_t s);
+cudaError_t fm_launch_spectrum_multi(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
+                                     double* spec64, cudaStream_t s);
 template <typename T>
 cudaError_t fm_launch_jacobi_eig(const void* R, void* work, void* basis, double* eig, int32_t* status, int frames,
                                  int m, int k, cudaStream_t s);
@@ -327,6 +329,7 @@ struct fm_plan_s {
     double* basis = nullptr;  // frames x K x M complex128
     double* eig = nullptr;    // frames x K
     double* t = nullptr;      // frames x M complex128
+    double* spec64 = nullptr; // frames x L (fp64 spectrum for peak picking)
     double* zgrid = nullptr;  // L complex128
     int32_t* scratch_status = nullptr;  // frames
     // host-path staging
@@ -436,6 +439,7 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
     chk(pl->get(&pl->basis, B * K * M * 2));
     chk(pl->get(&pl->eig, B * K));
     chk(pl->get(&pl->t, B * M * 2));
+    chk(pl->get(&pl->spec64, B * L));
     chk(pl->get(&pl->zgrid, L * 2));
     chk(pl->get(&pl->scratch_status, B));
     if (e != cudaSuccess) {
@@ -491,9 +495,9 @@ extern "C" fm_status fm_plan_stage_times(fm_plan plan, float* ms, int32_t* runs)
 extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
     if (!plan) return 0;
     const int t = plan->d.t;
-    int n = 1 /*cov*/ + 1 /*clear*/ + 2 /*autocorr, spectrum+peaks*/;
-    if (plan->d.method == FM_METHOD_FAST2) n += 1 + 2 * t + 1 + 1;  // rmul, t x (qr, rmul), qr final, nystrom
-    else if (plan->d.method == FM_METHOD_FAST1) n += 3;             // gather, qr final, nystrom
+    int n = 1 /*cov*/ + 1 /*clear*/ + 3 /*autocorr, spectrum, peaks*/;
+    if (plan->d.method == FM_METHOD_FAST2) n += 1 + 2 * t + 1;  // rmul, t x (orth, rmul), fused final
+    else if (plan->d.method == FM_METHOD_FAST1) n += 2;             // gather, fused final
     else n += 1;                                                    // jacobi
     return n;
 }
@@ -537,6 +541,7 @@ struct WorkView {
     double* basis;
     double* eig;
     double* t;
+    double* spec64;
     int32_t* scratch;
 };
 
@@ -554,6 +559,7 @@ static WorkView work_view(fm_plan pl, int64_t f0) {
     w.basis = pl->basis + f0 * K * M * 2;
     w.eig = pl->eig + f0 * K;
     w.t = pl->t + f0 * M * 2;
+    w.spec64 = pl->spec64 + f0 * static_cast<size_t>(d.grid_size);
     w.scratch = pl->scratch_status + f0;
     return w;
 }
@@ -636,9 +642,10 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     if (prof) mark(pl, 2, s);
     FM_LAUNCH(fm_launch_autocorr(basis, w.t, F, M, K, s));
     if (prof) mark(pl, 3, s);
-    FM_LAUNCH(fm_launch_spectrum_peaks(w.t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, nullptr,
-                                        K, static_cast<int>(d.min_sep_cells), io->peak_cells, io->peak_heights,
-                                        io->baseline, io->peak_count, io->status, s));
+    FM_LAUNCH(fm_launch_spectrum_multi(w.t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, w.spec64,
+                                       s));
+    FM_LAUNCH(fm_launch_peaks_only(w.spec64, F, static_cast<int>(d.grid_size), K, static_cast<int>(d.min_sep_cells),
+                                   io->peak_cells, io->peak_heights, io->baseline, io->peak_count, w.scratch, s));
     if (prof) mark(pl, 4, s);
     return FM_OK;
 }

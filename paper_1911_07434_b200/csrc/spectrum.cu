@@ -35,27 +35,41 @@ namespace spec {
 constexpr int kNT = 256;
 constexpr int kNW = kNT / 32;
 
-// t_delta, delta = 0..M-1, for frame blockIdx.y; one thread per delta.
+// t_delta, delta = 0..M-1, for frame blockIdx.x. Thread i owns lags i and M-1-i, so every
+// thread performs M+1 products per basis column (the triangle of lags is load-balanced).
 __global__ void __launch_bounds__(kNT) k_autocorr(const c64* __restrict__ basis, c64* __restrict__ t, int m, int k) {
     extern __shared__ c64 col[];  // one basis column (M complex)
-    const int f = blockIdx.y;
-    const int delta = blockIdx.x * kNT + threadIdx.x;
+    const int f = blockIdx.x;
     const c64* Uf = basis + static_cast<size_t>(f) * m * k;
-    c64 acc = mk(0.0, 0.0);
-    for (int kk = 0; kk < k; ++kk) {
-        __syncthreads();
-        for (int r = threadIdx.x; r < m; r += kNT) col[r] = Uf[static_cast<size_t>(kk) * m + r];
-        __syncthreads();
-        if (delta < m) {
-            for (int r = 0; r + delta < m; ++r) {
-                // U_r * conj(U_{r+delta})
-                const c64 a = col[r], b = col[r + delta];
-                acc.re = fma(a.re, b.re, fma(a.im, b.im, acc.re));
-                acc.im = fma(a.im, b.re, fma(-a.re, b.im, acc.im));
+    const int nh = (m + 1) / 2;
+    for (int i0 = 0; i0 < nh; i0 += blockDim.x) {
+        const int i = i0 + threadIdx.x;
+        const int d1 = i, d2 = m - 1 - i;
+        c64 a1 = mk(0.0, 0.0), a2 = mk(0.0, 0.0);
+        for (int kk = 0; kk < k; ++kk) {
+            __syncthreads();
+            for (int r = threadIdx.x; r < m; r += blockDim.x) col[r] = Uf[static_cast<size_t>(kk) * m + r];
+            __syncthreads();
+            if (i < nh) {
+                for (int r = 0; r + d1 < m; ++r) {  // U_r * conj(U_{r+delta})
+                    const c64 a = col[r], b = col[r + d1];
+                    a1.re = fma(a.re, b.re, fma(a.im, b.im, a1.re));
+                    a1.im = fma(a.im, b.re, fma(-a.re, b.im, a1.im));
+                }
+                if (d2 != d1) {
+                    for (int r = 0; r + d2 < m; ++r) {
+                        const c64 a = col[r], b = col[r + d2];
+                        a2.re = fma(a.re, b.re, fma(a.im, b.im, a2.re));
+                        a2.im = fma(a.im, b.re, fma(-a.re, b.im, a2.im));
+                    }
+                }
             }
         }
+        if (i < nh) {
+            t[static_cast<size_t>(f) * m + d1] = a1;
+            if (d2 != d1) t[static_cast<size_t>(f) * m + d2] = a2;
+        }
     }
-    if (delta < m) t[static_cast<size_t>(f) * m + delta] = acc;
 }
 
 // Block-wide (height desc, cell asc) argmax helper.
@@ -262,6 +276,71 @@ __global__ void __launch_bounds__(kNT) k_spectrum_peaks(const c64* __restrict__ 
     }
 }
 
+// Spectrum for kFPB frames at once: thread = grid point l, the block's kFPB frames share one
+// fp64 power sequence z_l^delta (4 DFMA per step) and each frame adds Re(t_delta z^delta)
+// (2 DFMA) from a shared-memory broadcast of its coefficients: ~2.25 DFMA per (frame, point,
+// delta) versus 4 for a per-frame Horner. The z^delta recurrence error (~delta * eps64) is far
+// below the fp64 cancellation budget of d = (M - t_0) - 2 Re sum_delta t_delta z^delta.
+constexpr int kFPB = 16;
+
+__global__ void __launch_bounds__(kNT) k_spectrum_multi(const c64* __restrict__ t, const c64* __restrict__ zgrid,
+                                                        int frames, int m, int L, float* __restrict__ spec32,
+                                                        double* __restrict__ spec64) {
+    extern __shared__ c64 st[];  // kFPB x m coefficients, delta-major: st[delta * kFPB + f]
+    const int f0 = blockIdx.y * kFPB;
+    const int nf = min(kFPB, frames - f0);
+    for (int e = threadIdx.x; e < kFPB * m; e += kNT) {
+        const int f = e / m, dl = e % m;
+        st[dl * kFPB + f] = f < nf ? t[static_cast<size_t>(f0 + f) * m + dl] : mk(0.0, 0.0);
+    }
+    __syncthreads();
+    // two grid points per thread (l0, l0 + half): 2 power sequences share every coefficient load
+    const int half = (L + 1) / 2;
+    const int l0 = blockIdx.x * kNT + threadIdx.x;
+    if (l0 >= half) return;
+    const int l1 = l0 + half;
+    const bool has1 = l1 < L;
+    const c64 za = zgrid[l0];
+    const c64 zb = has1 ? zgrid[l1] : mk(1.0, 0.0);
+    double acc0[kFPB], acc1[kFPB];
+#pragma unroll
+    for (int f = 0; f < kFPB; ++f) acc0[f] = acc1[f] = 0.0;
+    double ar = 1.0, ai = 0.0, br = 1.0, bi = 0.0;
+    for (int dl = 1; dl < m; ++dl) {
+        const double nar = fma(ar, za.re, -ai * za.im);
+        const double nai = fma(ar, za.im, ai * za.re);
+        const double nbr = fma(br, zb.re, -bi * zb.im);
+        const double nbi = fma(br, zb.im, bi * zb.re);
+        ar = nar;
+        ai = nai;
+        br = nbr;
+        bi = nbi;
+        const c64* row = st + dl * kFPB;
+#pragma unroll
+        for (int f = 0; f < kFPB; ++f) {
+            const c64 c = row[f];
+            acc0[f] = fma(c.re, ar, fma(-c.im, ai, acc0[f]));
+            acc1[f] = fma(c.re, br, fma(-c.im, bi, acc1[f]));
+        }
+    }
+    const double floor_v = 1e-12 * static_cast<double>(m);
+#pragma unroll
+    for (int f = 0; f < kFPB; ++f) {
+        if (f < nf) {
+            const double c0 = static_cast<double>(m) - st[f].re;
+            const double P0 = 1.0 / fmax(c0 - 2.0 * acc0[f], floor_v);
+            const size_t o = static_cast<size_t>(f0 + f) * L;
+            if (spec32) spec32[o + l0] = static_cast<float>(P0);
+            spec64[o + l0] = P0;
+            if (has1) {
+                const double P1 = 1.0 / fmax(c0 - 2.0 * acc1[f], floor_v);
+                if (spec32) spec32[o + l1] = static_cast<float>(P1);
+                spec64[o + l1] = P1;
+            }
+        }
+    }
+}
+
 // Peaks only, on caller-provided fp64 values (facade extract_peaks).
 __global__ void __launch_bounds__(kNT) k_peaks_only(const double* __restrict__ values, int L, int K, int min_sep,
                                                     PeakOut out, int32_t* __restrict__ overflow_flag) {
@@ -317,8 +396,8 @@ cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, in
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
     }
-    dim3 grid((m + spec::kNT - 1) / spec::kNT, frames);
-    spec::k_autocorr<<<grid, spec::kNT, smem, s>>>(static_cast<const c64*>(basis), static_cast<c64*>(t), m, k);
+    const int threads = std::min(spec::kNT, std::max(32, ((m + 1) / 2 + 31) / 32 * 32));
+    spec::k_autocorr<<<frames, threads, smem, s>>>(static_cast<const c64*>(basis), static_cast<c64*>(t), m, k);
     return cudaGetLastError();
 }
 
@@ -339,6 +418,19 @@ cudaError_t fm_launch_spectrum_peaks(const void* t, const void* zgrid, int frame
     spec::PeakOut out{cells, heights, baseline, count};
     spec::k_spectrum_peaks<<<frames, spec::kNT, smem, s>>>(static_cast<const c64*>(t), static_cast<const c64*>(zgrid),
                                                            m, L, spec32, spec64, K, min_sep, out, status);
+    return cudaGetLastError();
+}
+
+cudaError_t fm_launch_spectrum_multi(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
+                                     double* spec64, cudaStream_t s) {
+    const size_t smem = sizeof(c64) * spec::kFPB * m;
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(spec::k_spectrum_multi, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    dim3 grid(((L + 1) / 2 + spec::kNT - 1) / spec::kNT, (frames + spec::kFPB - 1) / spec::kFPB);
+    spec::k_spectrum_multi<<<grid, spec::kNT, smem, s>>>(static_cast<const c64*>(t), static_cast<const c64*>(zgrid),
+                                                         frames, m, L, spec32, spec64);
     return cudaGetLastError();
 }
 

@@ -70,16 +70,21 @@ __global__ void __launch_bounds__(kNT) k_rmul(const cplx<T>* __restrict__ R, con
         __syncthreads();
         if (row < m) {
             const cplx<T>* col = Rf + static_cast<size_t>(j0) * m + row;
-#pragma unroll 4
-            for (int jj = 0; jj < jn; ++jj) {
-                const cplx<T> r = col[static_cast<size_t>(jj) * m];  // R[j][row] -> conj gives R[row][j]
+            // batches of 8 independent R loads in flight per thread before the MACs
+            for (int jj = 0; jj < jn; jj += 8) {
+                cplx<T> r[8];
 #pragma unroll
-                for (int c = 0; c < PC; ++c) {
-                    if (REAL) {
-                        acc[c].re = fma(r.re, rhs_s[jj][c].re, acc[c].re);
-                        acc[c].im = fma(-r.im, rhs_s[jj][c].re, acc[c].im);
-                    } else {
-                        cmac_conj(acc[c], r, rhs_s[jj][c]);
+                for (int u = 0; u < 8; ++u) r[u] = jj + u < jn ? col[static_cast<size_t>(jj + u) * m] : mk<T>(0, 0);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+#pragma unroll
+                    for (int c = 0; c < PC; ++c) {
+                        if (REAL) {
+                            acc[c].re = fma(r[u].re, rhs_s[jj + u][c].re, acc[c].re);
+                            acc[c].im = fma(-r[u].im, rhs_s[jj + u][c].re, acc[c].im);
+                        } else {
+                            cmac_conj(acc[c], r[u], rhs_s[jj + u][c]);
+                        }
                     }
                 }
             }
