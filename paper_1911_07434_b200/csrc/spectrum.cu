@@ -281,8 +281,9 @@ __global__ void __launch_bounds__(kNT) k_spectrum_peaks(const c64* __restrict__ 
 // (2 DFMA) from a shared-memory broadcast of its coefficients: ~2.25 DFMA per (frame, point,
 // delta) versus 4 for a per-frame Horner. The z^delta recurrence error (~delta * eps64) is far
 // below the fp64 cancellation budget of d = (M - t_0) - 2 Re sum_delta t_delta z^delta.
-constexpr int kFPB = 16;
+constexpr int kFPB = 16;  // frames per block (8 when 16 x M coefficients exceed shared memory)
 
+template <int kFPB>
 __global__ void __launch_bounds__(kNT) k_spectrum_multi(const c64* __restrict__ t, const c64* __restrict__ zgrid,
                                                         int frames, int m, int L, float* __restrict__ spec32,
                                                         double* __restrict__ spec64) {
@@ -423,15 +424,19 @@ cudaError_t fm_launch_spectrum_peaks(const void* t, const void* zgrid, int frame
 
 cudaError_t fm_launch_spectrum_multi(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
                                      double* spec64, cudaStream_t s) {
-    const size_t smem = sizeof(c64) * spec::kFPB * m;
-    if (smem > 227 * 1024) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(spec::k_spectrum_multi, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    dim3 grid(((L + 1) / 2 + spec::kNT - 1) / spec::kNT, (frames + spec::kFPB - 1) / spec::kFPB);
-    spec::k_spectrum_multi<<<grid, spec::kNT, smem, s>>>(static_cast<const c64*>(t), static_cast<const c64*>(zgrid),
-                                                         frames, m, L, spec32, spec64);
-    return cudaGetLastError();
+    auto go = [&](auto kern, int fpb) {
+        const size_t smem = sizeof(c64) * fpb * m;
+        if (smem > 200 * 1024) return cudaErrorInvalidValue;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        dim3 grid(((L + 1) / 2 + spec::kNT - 1) / spec::kNT, (frames + fpb - 1) / fpb);
+        kern<<<grid, spec::kNT, smem, s>>>(static_cast<const c64*>(t), static_cast<const c64*>(zgrid), frames, m, L,
+                                           spec32, spec64);
+        return cudaGetLastError();
+    };
+    if (sizeof(c64) * 16 * m <= 200 * 1024) return go(spec::k_spectrum_multi<16>, 16);
+    if (sizeof(c64) * 8 * m <= 200 * 1024) return go(spec::k_spectrum_multi<8>, 8);
+    return go(spec::k_spectrum_multi<4>, 4);
 }
 
 cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K, int min_sep, int32_t* cells,
