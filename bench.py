@@ -215,6 +215,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_1911_07434_b200 as fm
+    from paper_1911_07434_b200.shard import gather_records, pack_records, shard_range
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -229,7 +230,7 @@ def run_ours(args):
     if args.frames:
         B = args.frames
         cfgd = dict(cfgd, frames=B)
-    f0 = rank * B
+    f0, _ = shard_range(rank, world, B)
     # synthetic input for this rank's frames, generated on the host (pinned), staged once
     xh = torch.empty((B, M, N, 2), dtype=torch.float32, pin_memory=True)
     xnp = xh.numpy().view(np.complex64).reshape(B, M, N)
@@ -258,10 +259,8 @@ def run_ours(args):
         plan.run(B, xd, omega, idx, out, stream=stream)
         if world > 1:
             with torch.cuda.stream(stream):
-                rec[:, :K].copy_(out["peak_cells"])
-                rec[:, K].copy_(out["peak_count"])
-                rec[:, K + 1].copy_(out["status"])
-                dist.all_gather_into_tensor(gather.view(-1, K + 2), rec)
+                pack_records(out["peak_cells"], out["peak_count"], out["status"], out=rec)
+                gather_records(rec, world, out=gather)
 
     for _ in range(max(3, args.warmup)):
         step()
