@@ -34,7 +34,7 @@ namespace cov {
 
 constexpr int kRows = 128;          // rows of X per CTA (half of the UMMA M=256 tile)
 constexpr int kChunk = 16;          // complex snapshots per pipeline stage (one UMMA K-slice)
-constexpr int kStagesS = 4;         // fp32 staging ring (TMA destination)
+constexpr int kStagesS = 3;         // fp32 staging ring (TMA destination)
 constexpr int kStagesO = 3;         // fp16 operand ring (UMMA source)
 constexpr int kStageBytes = kRows * kChunk * 8;   // 16 KB fp32 per operand side
 constexpr int kPlaneBytes = kRows * kChunk * 2;   // 4 KB fp16 per plane (Re or Im)
@@ -44,8 +44,11 @@ constexpr int kSmemStaging = kStagesS * 2 * kStageBytes;
 constexpr int kSmemOperand = kStagesO * 2 * kOpBytes;
 constexpr int kSmemBarriers = 256;
 constexpr int kEpiLd = 33;                                  // padded row (float2) of the transpose tile
-constexpr int kSmemEpilogue = 4 * 32 * kEpiLd * 8;          // 4 epilogue warps x 32x32 complex
-constexpr int kSmemBytes = 1024 + kSmemStaging + kSmemOperand + kSmemBarriers + kSmemEpilogue;
+constexpr int kEpiChunk = 4096;                             // 32 rows x 16 complex fp32 (one TMA store box)
+constexpr int kEpiWarpBytes = 4 * kEpiChunk;                // [diag buf0 | diag buf1 | mirror buf0 | mirror buf1]
+constexpr int kSmemEpilogue = 4 * kEpiWarpBytes;            // >= 4 * 32 * kEpiLd * 8 (generic-store fallback)
+static_assert(kSmemEpilogue >= 4 * 32 * kEpiLd * 8, "epilogue region");
+constexpr int kSmemBytes = 1024 + kSmemStaging + kSmemOperand + kSmemEpilogue + kSmemBarriers;
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -106,6 +109,23 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
         : "memory");
 }
+// TMA bulk-tensor store smem -> global (3D map {2M floats, M rows, B frames}; rows / columns
+// outside the frame are clipped by the tensor map, never spill into the next frame).
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int x, int y, int z) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(x), "r"(y), "r"(z)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void sts_v4(uint32_t a, float x, float y, float z, float w) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
+__device__ __forceinline__ void sts_v2(uint32_t a, float x, float y) {
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(x), "f"(y) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -146,6 +166,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
           "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
           "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
           "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
         : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -211,14 +239,17 @@ __device__ __forceinline__ void convert_tile(const uint8_t* stage, uint8_t* op, 
 //   w0 TMA producer | w1 MMA issuer (leader) + TMEM owner | w2..w5 converters | w6..w9 epilogue.
 // The epilogue of tile i (TMEM -> fp32 R) overlaps the TMA + fp16 conversion of tile i + 1;
 // the MMA of tile i + 1 starts once both CTAs' epilogues have drained TMEM (acc_empty).
+template <bool kTmaStore>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    cov_tc_kernel(const __grid_constant__ CUtensorMap xmap, float* __restrict__ r_out, int32_t* __restrict__ status,
+    cov_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap rmap,
+                  const __grid_constant__ CUtensorMap mmap, float* __restrict__ r_out, int32_t* __restrict__ status,
                   int m, int n, int tiles_per_frame, int total_tiles) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* staging = smem;
     uint8_t* operand = smem + kSmemStaging;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(operand + kSmemOperand);
+    uint8_t* epi_bytes = operand + kSmemOperand;  // 1024-aligned (128B-swizzled TMA store boxes)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(epi_bytes + kSmemEpilogue);
     uint64_t* stage_full = bars;
     uint64_t* stage_empty = bars + kStagesS;
     uint64_t* op_full = bars + 2 * kStagesS;
@@ -226,7 +257,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* acc_full = bars + 2 * kStagesS + 2 * kStagesO;
     uint64_t* acc_empty = acc_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
-    float2* epi = reinterpret_cast<float2*>(operand + kSmemOperand + kSmemBarriers);
+    float2* epi = reinterpret_cast<float2*>(epi_bytes);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -255,6 +286,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+        if (kTmaStore) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&rmap)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mmap)) : "memory");
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -350,8 +385,68 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             flag = __reduce_or_sync(0xffffffffu, flag);
             if (flag && lane == 0 && status != nullptr) atomicOr(&status[frame], flag);
         }
+    } else if (kTmaStore) {
+        // ---------------- epilogue (warps 6..9): TMEM -> registers -> swizzled smem -> TMA store.
+        // Per 16-column chunk: two tcgen05.ld (Re, Im), eight conflict-free 16-byte st.shared into a
+        // 128B-swizzled 32 x 16 complex box, one elected cp.async.bulk.tensor store (double-buffered,
+        // bulk groups). TMEM is released as soon as the last chunk is in smem, so the global writes
+        // overlap the next tile's mainloop. Off-diagonal tiles also store the conj-transposed block.
+        const int quarter = warp & 3;
+        const float inv_n = 1.0f / static_cast<float>(n);
+        const uint32_t ebase = smem_u32(epi_bytes) + (warp - 6) * kEpiWarpBytes;
+        int t = 0, gc = 0;
+        for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
+            const int frame = tile / tiles_per_frame;
+            int bi, bj;
+            tile_coords(tile % tiles_per_frame, bi, bj);
+            const bool diag = (bi == bj);
+            const int row0 = 256 * bi + 128 * static_cast<int>(rank) + 32 * quarter;
+            const int gi = row0 + lane;
+            mbar_wait(smem_u32(acc_full), t & 1);
+            tc_fence_after();
+            const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
+            const int nchunks = row0 < m ? min(16, (m - 256 * bj + 15) / 16) : 0;
+            for (int c = 0; c < nchunks; ++c, ++gc) {
+                const int col0 = 256 * bj + 16 * c;
+                uint32_t vr[16], vi[16];
+                tmem_ld16(taddr + 16 * c, vr);
+                tmem_ld16(taddr + 256 + 16 * c, vi);
+                tmem_wait_ld();
+                const int b = gc & 1;
+                if (lane == 0) bulk_wait_read1();  // the store issued from buffer b two chunks ago has read it
+                __syncwarp();
+                const uint32_t dbuf = ebase + b * kEpiChunk;
+                const uint32_t mbuf = ebase + 2 * kEpiChunk + b * kEpiChunk;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float re0 = __uint_as_float(vr[2 * q]) * inv_n;
+                    const float re1 = __uint_as_float(vr[2 * q + 1]) * inv_n;
+                    const float im0 = (col0 + 2 * q == gi) ? 0.f : __uint_as_float(vi[2 * q]) * inv_n;
+                    const float im1 = (col0 + 2 * q + 1 == gi) ? 0.f : __uint_as_float(vi[2 * q + 1]) * inv_n;
+                    sts_v4(dbuf + lane * 128 + ((q ^ (lane & 7)) << 4), re0, im0, re1, im1);
+                    if (!diag) {  // mirrored block row (col0 + 2q (+1)), column gi: conj
+                        sts_v2(mbuf + ((2 * q) * 32 + lane) * 8, re0, -im0);
+                        sts_v2(mbuf + ((2 * q + 1) * 32 + lane) * 8, re1, -im1);
+                    }
+                }
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_3d(&rmap, dbuf, 2 * col0, row0, frame);
+                    if (!diag) tma_store_3d(&mmap, mbuf, 2 * row0, col0, frame);
+                    bulk_commit();
+                }
+            }
+            tc_fence_before();
+            named_bar_sync(2, 128);  // all four epilogue warps finished reading TMEM
+            if (warp == 6 && lane == 0) {
+                if (rank == 0) mbar_arrive_local(smem_u32(acc_empty));
+                else mbar_arrive_cluster(smem_u32(acc_empty), 0);
+            }
+        }
+        if (lane == 0) bulk_wait_all();
     } else {
-        // ---------------- epilogue (warps 6..9): TMEM -> registers -> fp32 R
+        // ---------------- epilogue, generic-store fallback (odd M: row pitch not 16-byte aligned)
         const int quarter = warp & 3;
         const int row = 32 * quarter + lane;
         const float inv_n = 1.0f / static_cast<float>(n);
@@ -442,20 +537,40 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
         return cudaErrorInvalidValue;
     EncodeTiledFn enc = get_encode();
     if (!enc) return cudaErrorNotSupported;
-    CUtensorMap map;
+    CUtensorMap map, rmap, mmap;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * n), static_cast<cuuint64_t>(frames * m)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(8 * n)};
     cuuint32_t box[2] = {32, 128};
-    cuuint32_t estr[2] = {1, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
     CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(d_x), dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(cov_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    const bool tma_store = (m % 2) == 0;  // R row pitch 8M bytes must be a multiple of 16
+    if (tma_store) {
+        cuuint64_t rdims[3] = {static_cast<cuuint64_t>(2 * m), static_cast<cuuint64_t>(m),
+                               static_cast<cuuint64_t>(frames)};
+        cuuint64_t rstr[2] = {static_cast<cuuint64_t>(8 * m), static_cast<cuuint64_t>(8 * m * m)};
+        cuuint32_t rbox[3] = {32, 32, 1};  // 32 rows x 16 complex, 128B-swizzled
+        cuuint32_t mbox[3] = {64, 16, 1};  // 16 rows x 32 complex (mirrored block), plain
+        cr = enc(&rmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d_r, rdims, rstr, rbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+        cr = enc(&mmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d_r, rdims, rstr, mbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    } else {
+        rmap = map;  // unused by the fallback epilogue
+        mmap = map;
+    }
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[tma_store]) {
+        cudaError_t e = tma_store ? cudaFuncSetAttribute(cov_tc_kernel<true>,
+                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes)
+                                  : cudaFuncSetAttribute(cov_tc_kernel<false>,
+                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set[tma_store] = true;
     }
     const int nb = static_cast<int>((m + 255) / 256);
     const int tiles_per_frame = nb * (nb + 1) / 2;
@@ -468,7 +583,14 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
     }
     const int64_t pairs = std::min<int64_t>(tiles, std::max(1, sm_count / 2));
-    cov_tc_kernel<<<dim3(static_cast<unsigned>(2 * pairs)), kThreads, kSmemBytes, stream>>>(
-        map, d_r, d_status, static_cast<int>(m), static_cast<int>(n), tiles_per_frame, static_cast<int>(tiles));
+    const dim3 grid(static_cast<unsigned>(2 * pairs));
+    if (tma_store)
+        cov_tc_kernel<true><<<grid, kThreads, kSmemBytes, stream>>>(map, rmap, mmap, d_r, d_status, static_cast<int>(m),
+                                                                    static_cast<int>(n), tiles_per_frame,
+                                                                    static_cast<int>(tiles));
+    else
+        cov_tc_kernel<false><<<grid, kThreads, kSmemBytes, stream>>>(map, rmap, mmap, d_r, d_status,
+                                                                     static_cast<int>(m), static_cast<int>(n),
+                                                                     tiles_per_frame, static_cast<int>(tiles));
     return cudaGetLastError();
 }
