@@ -47,6 +47,10 @@ cudaError_t fm_launch_orth_tiled(const void* C, void* Vout, int32_t* status, int
                                  cudaStream_t s);
 cudaError_t fm_launch_final_tiled(const void* C, const void* V, const void* H, void* basis, double* eig,
                                   int32_t* status, int frames, int m, int p, int k, cudaStream_t s);
+cudaError_t fm_launch_rmul_tc(const float* d_r, const float* d_omega, const float* d_v, float* d_c, int64_t frames,
+                              int64_t m, int64_t p, cudaStream_t stream);
+cudaError_t fm_launch_final_split(const void* C, const void* V, void* Hw, void* Gw, void* Tw, void* basis, double* eig,
+                                  int32_t* status, int frames, int m, int p, int k, cudaStream_t s);
 cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, int k, cudaStream_t s);
 cudaError_t fm_launch_spectrum_peaks(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
                                      double* spec64, int K, int min_sep, int32_t* cells, double* heights,
@@ -492,12 +496,26 @@ extern "C" fm_status fm_plan_stage_times(fm_plan plan, float* ms, int32_t* runs)
     return FM_OK;
 }
 
+// Tensor-core products (rmul_tc.cu) need an even M (16-byte TMA row pitch) and p <= 32;
+// FM_SIMT_RMUL=1 selects the SIMT k_rmul for comparison.
+static bool tc_rmul(int m, int p) {
+    static const bool simt = std::getenv("FM_SIMT_RMUL") != nullptr;
+    return !simt && (m % 2) == 0 && p >= 4 && p <= 32 && (p % 4) == 0;
+}
+
+static bool split_final() {  // FM_FUSED_FINAL=1 selects the single-kernel k_final_tiled (comparison)
+    static const bool fused = std::getenv("FM_FUSED_FINAL") != nullptr;
+    return !fused;
+}
+
 extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
     if (!plan) return 0;
     const int t = plan->d.t;
     int n = 1 /*cov*/ + 1 /*clear*/ + 3 /*autocorr, spectrum, peaks*/;
-    if (plan->d.method == FM_METHOD_FAST2) n += 1 + 2 * t + 1;  // rmul, t x (orth, rmul), fused final
-    else if (plan->d.method == FM_METHOD_FAST1) n += 2;             // gather, fused final
+    const bool tiled = plan->d.p <= 32 && (plan->d.p % 4) == 0;
+    const int fin = tiled ? (split_final() ? 3 : 1) : 2;  // gram, small-warp, basis | fused | cholqr, nystrom
+    if (plan->d.method == FM_METHOD_FAST2) n += 1 + 2 * t + fin;  // rmul, t x (orth, rmul), final
+    else if (plan->d.method == FM_METHOD_FAST1) n += 1 + fin;      // gather, final
     else n += 1;                                                    // jacobi
     return n;
 }
@@ -617,13 +635,22 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     };
     fm_status st = FM_OK;
     if (d.method == FM_METHOD_FAST2) {
-        FM_LAUNCH(fm_launch_rmul<float>(R, io->omega, nullptr, w.C, nullptr, F, M, P, true, s));
+        if (tc_rmul(M, P))
+            FM_LAUNCH(fm_launch_rmul_tc(R, io->omega, nullptr, w.C, F, M, P, s));
+        else
+            FM_LAUNCH(fm_launch_rmul<float>(R, io->omega, nullptr, w.C, nullptr, F, M, P, true, s));
         for (int it = 0; it < d.t; ++it) {
             if ((st = orth(false, nullptr)) != FM_OK) return st;
-            FM_LAUNCH(fm_launch_rmul<float>(R, nullptr, w.V, w.C, nullptr, F, M, P, false, s));
+            if (tc_rmul(M, P))
+                FM_LAUNCH(fm_launch_rmul_tc(R, nullptr, w.V, w.C, F, M, P, s));
+            else
+                FM_LAUNCH(fm_launch_rmul<float>(R, nullptr, w.V, w.C, nullptr, F, M, P, false, s));
         }
         if (tiled) {
-            FM_LAUNCH(fm_launch_final_tiled(w.C, w.V, nullptr, basis, eig, io->status, F, M, P, K, s));
+            if (split_final())
+                FM_LAUNCH(fm_launch_final_split(w.C, w.V, w.H, w.Rt, w.work, basis, eig, io->status, F, M, P, K, s));
+            else
+                FM_LAUNCH(fm_launch_final_tiled(w.C, w.V, nullptr, basis, eig, io->status, F, M, P, K, s));
         } else {
             if ((st = orth(true, w.V)) != FM_OK) return st;
             if ((st = nystrom()) != FM_OK) return st;
@@ -631,7 +658,10 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     } else if (d.method == FM_METHOD_FAST1) {
         FM_LAUNCH(fm_launch_gather<float>(R, io->indices, w.C, w.H, nullptr, F, M, P, s));
         if (tiled) {
-            FM_LAUNCH(fm_launch_final_tiled(w.C, nullptr, w.H, basis, eig, io->status, F, M, P, K, s));
+            if (split_final())
+                FM_LAUNCH(fm_launch_final_split(w.C, nullptr, w.H, w.Rt, w.work, basis, eig, io->status, F, M, P, K, s));
+            else
+                FM_LAUNCH(fm_launch_final_tiled(w.C, nullptr, w.H, basis, eig, io->status, F, M, P, K, s));
         } else {
             if ((st = orth(true, nullptr)) != FM_OK) return st;
             if ((st = nystrom()) != FM_OK) return st;

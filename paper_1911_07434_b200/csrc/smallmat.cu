@@ -910,6 +910,300 @@ __global__ void __launch_bounds__(kNT, 2) k_final_tiled(const c32* __restrict__ 
     }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Split final stage (p in {4, 8, ..., 32}, p % 4 == 0). The fused k_final_tiled spends ~90% of
+// its time in p x p phases where one frame occupies a whole CTA behind __syncthreads; here the
+// Gram products stay block-per-frame, and every p x p phase runs one WARP per frame (8 frames
+// per CTA for p <= 16), so all frames of a batch are in flight at once.
+//   k_gram_gh   : G = C^H C, H = Herm(V^H C) (fast1: Herm(H given)) in fp64 -> workspace
+//   k_small_warp: G = L L^H, H = L_H L_H^H (warp Cholesky), Y = R L_H^-H (R = L^H),
+//                 one-sided Jacobi on Y (lane-per-column), s, order, T = R^-1 Z_K / s, eig = s^2
+//   k_basis_ct  : U = C T (thread per row, fp64 accumulation)
+// Same algebra as k_final_tiled (R/src/estimators.cpp:37-50, :104-139; linalg.cpp:143-163).
+
+template <int PC>
+__global__ void __launch_bounds__(kNT, 2) k_gram_gh(const c32* __restrict__ Cin, const c32* __restrict__ Vin,
+                                                 c64* __restrict__ Gout, c64* __restrict__ Hio, int m, int p) {
+    extern __shared__ uint8_t dsm[];
+    c64* G = reinterpret_cast<c64*>(dsm);
+    c64* H = G + PC * PC;
+    c64* stage = H + PC * PC;
+    const int f = blockIdx.x;
+    const c32* Cf = Cin + static_cast<size_t>(f) * m * p;
+    c64* Hf = Hio + static_cast<size_t>(f) * p * p;
+    if (Vin) {
+        tiled_gram2<c32, c32>(Cf, true, Cf, Vin + static_cast<size_t>(f) * m * p, Cf, m, p, stage, G, H);
+    } else {
+        tiled_gram2<c32, c32>(Cf, true, Cf, nullptr, nullptr, m, p, stage, G, nullptr);
+        for (int e = threadIdx.x; e < p * p; e += kNT) H[e] = Hf[e];
+        __syncthreads();
+    }
+    c64* Gf = Gout + static_cast<size_t>(f) * p * p;
+    for (int e = threadIdx.x; e < p * p; e += kNT) {
+        const int i = e % p, j = e / p;
+        const c64 a = H[j * p + i], b = H[i * p + j];  // Herm: (H(i,j) + conj(H(j,i))) / 2, exactly Hermitian
+        Gf[e] = G[e];
+        Hf[e] = mk(0.5 * (a.re + b.re), 0.5 * (a.im - b.im));
+    }
+}
+
+template <int PC> struct WarpCfg {
+    static constexpr int kLPC = 32 / PC;                   // lanes per column in the Jacobi
+    static constexpr int kWarps = PC <= 16 ? 8 : 3;        // frames per CTA
+    static constexpr int kLd = PC + ((kLPC - PC) % 8 + 8) % 8;  // ld = LPC (mod 8): conflict-free 16-B rows
+    static constexpr size_t kBytes = sizeof(c64) * (2 * PC * PC + 2 * PC * kLd) + sizeof(double) * PC + sizeof(int) * PC;
+    static constexpr size_t kWarpBytes = (kBytes + 15) / 16 * 16;
+};
+
+// In-place non-pivoted Cholesky of the Hermitian PD p x p A (column-major, ld p) by one warp:
+// lower triangle -> L (diagonal real sqrt(d_k)); the strict upper triangle is left stale.
+// Returns min / max Schur pivots (all lanes).
+__device__ __forceinline__ void warp_chol_lower(c64* A, int p, double& dmin, double& dmax) {
+    const int lane = threadIdx.x & 31;
+    dmin = 1e300;
+    dmax = 0.0;
+    for (int k = 0; k < p; ++k) {
+        const double dk = A[k * p + k].re;
+        dmin = fmin(dmin, dk);
+        dmax = fmax(dmax, dk);
+        const double inv = dk > 0.0 ? 1.0 / sqrt(dk) : 0.0;
+        __syncwarp();
+        for (int i = k + 1 + lane; i < p; i += 32) {
+            const c64 a = A[k * p + i];
+            A[k * p + i] = mk(a.re * inv, a.im * inv);
+        }
+        if (lane == 0) A[k * p + k] = mk(dk > 0.0 ? sqrt(dk) : 0.0, 0.0);
+        __syncwarp();
+        const int nt = p - k - 1;
+        for (int e = lane; e < nt * nt; e += 32) {
+            const int i = k + 1 + e % nt, j = k + 1 + e / nt;
+            if (i < j) continue;
+            const c64 li = A[k * p + i], lj = A[k * p + j];
+            c64 a = A[j * p + i];
+            a.re -= li.re * lj.re + li.im * lj.im;  // li * conj(lj)
+            a.im -= li.im * lj.re - li.re * lj.im;
+            A[j * p + i] = a;
+        }
+        __syncwarp();
+    }
+}
+
+template <int PC>
+__global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
+    k_small_warp(const c64* __restrict__ Gin, const c64* __restrict__ Hin, c64* __restrict__ Tout,
+                 double* __restrict__ eig, int32_t* __restrict__ status, int frames, int p, int k,
+                 int32_t* __restrict__ dbg) {
+    using W = WarpCfg<PC>;
+    constexpr int LPC = W::kLPC;
+    extern __shared__ uint8_t dsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int f = blockIdx.x * W::kWarps + warp;
+    if (f >= frames) return;  // whole warp
+    const int ld = W::kLd;
+    c64* L = reinterpret_cast<c64*>(dsm + warp * W::kWarpBytes);
+    c64* LH = L + PC * PC;
+    c64* Ya = LH + PC * PC;
+    c64* Yb = Ya + PC * ld;
+    double* sig = reinterpret_cast<double*>(Yb + PC * ld);
+    int* order = reinterpret_cast<int*>(sig + PC);
+    const c64* Gf = Gin + static_cast<size_t>(f) * p * p;
+    const c64* Hf = Hin + static_cast<size_t>(f) * p * p;
+    const long long T0 = clock64();
+    for (int e = lane; e < p * p; e += 32) {
+        L[e] = Gf[e];
+        LH[e] = Hf[e];
+    }
+    __syncwarp();
+    double dmin, dmax;
+    warp_chol_lower(L, p, dmin, dmax);   // G = L L^H, R = L^H: R(i, j) = conj(L[i * p + j]), j >= i
+    warp_chol_lower(LH, p, dmin, dmax);  // H = L_H L_H^H
+    if (lane == 0 && !(dmin > static_cast<double>(p) * eps_of<float>::value * dmax))
+        atomicOr(&status[f], kFrameNoConv);
+    for (int e = lane; e < PC * ld; e += 32) Ya[e] = Yb[e] = mk(0.0, 0.0);  // rows >= p stay zero
+    __syncwarp();
+    // Y(i, :) solves y L_H^H = R(i, :) (forward substitution, lane per row); Y -> Ya (ld)
+    if (lane < p) {
+        const int i = lane;
+        for (int j = 0; j < p; ++j) {
+            c64 x = j >= i ? conj(L[i * p + j]) : mk(0.0, 0.0);
+            for (int a = i; a < j; ++a) {  // y_a = 0 for a < i
+                const c64 l = LH[a * p + j];
+                const c64 v = Ya[a * ld + i];
+                x.re -= v.re * l.re + v.im * l.im;
+                x.im -= v.im * l.re - v.re * l.im;
+            }
+            const double ljj = LH[j * p + j].re;
+            const double inv = ljj > 0.0 ? 1.0 / ljj : 0.0;
+            Ya[j * ld + i] = j >= i ? mk(x.re * inv, x.im * inv) : mk(0.0, 0.0);
+        }
+    }
+    __syncwarp();
+    const long long T1 = clock64();
+    // one-sided Jacobi on Y's columns, in place in Ya. Lanes are assigned to column PAIRS: slot
+    // = lane / LPP of the round-robin schedule (slot 0: (rnd, p-1); slot s: (rnd + s, rnd - s)
+    // mod (p - 1)), sub = lane % LPP owns rows sub, sub + LPP, ... of BOTH columns, so every
+    // element is read and written by one lane per round (one __syncwarp per round). Rotation:
+    // fp32-seeded angle, fp64 cos / phase refined by one Newton step (unitary to ~5e-15).
+    constexpr int LPP = 64 / PC;            // lanes per pair
+    constexpr int RPL = PC * PC / 64;       // rows per lane
+    const int slot = lane / LPP, sub = lane % LPP;
+    const bool act = slot < p / 2;
+    const int n1 = p - 1;                   // p even (p % 4 == 0)
+    const double tol = 8.0 * 2.220446049250313e-16 * p;
+    c64* cur = Ya;
+    int sweeps = 0;
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        bool rot_any = false;
+        for (int rnd = 0; rnd < n1; ++rnd) {
+            int i = rnd + slot, j = rnd - slot;
+            if (i >= n1) i -= n1;
+            if (j < 0) j += n1;
+            if (slot == 0) j = n1;
+            const int lo = act ? min(i, j) : 0, hi = act ? max(i, j) : 0;
+            c64* xlo = cur + lo * ld + sub;
+            c64* xhi = cur + hi * ld + sub;
+            c64 x[RPL], y[RPL];
+            double al0 = 0.0, al1 = 0.0, be0 = 0.0, be1 = 0.0;
+            c64 g0 = mk(0.0, 0.0), g1 = mk(0.0, 0.0);
+#pragma unroll
+            for (int t = 0; t < RPL; ++t) {
+                x[t] = xlo[t * LPP];
+                y[t] = xhi[t * LPP];
+                if (t & 1) {
+                    al1 += norm2(x[t]);
+                    be1 += norm2(y[t]);
+                    cmac_conj(g1, x[t], y[t]);
+                } else {
+                    al0 += norm2(x[t]);
+                    be0 += norm2(y[t]);
+                    cmac_conj(g0, x[t], y[t]);
+                }
+            }
+            double al = al0 + al1, be = be0 + be1;
+            c64 ga = mk(g0.re + g1.re, g0.im + g1.im);
+#pragma unroll
+            for (int o = 1; o < LPP; o <<= 1) {
+                al += __shfl_xor_sync(0xffffffffu, al, o);
+                be += __shfl_xor_sync(0xffffffffu, be, o);
+                ga.re += __shfl_xor_sync(0xffffffffu, ga.re, o);
+                ga.im += __shfl_xor_sync(0xffffffffu, ga.im, o);
+            }
+            const double g2 = norm2(ga);
+            const bool rotate = act && (g2 > tol * tol * al * be) && g2 != 0.0;
+            if (rotate) {
+                const float g2f = static_cast<float>(g2);
+                const float igf = rsqrtf(g2f);
+                const float zeta = static_cast<float>(be - al) * (0.5f * igf);
+                const float tf = copysignf(1.0f, zeta) / (fabsf(zeta) + sqrtf(fmaf(zeta, zeta, 1.0f)));
+                const double t = tf;
+                const double x1 = fma(t, t, 1.0);
+                double cs = static_cast<double>(rsqrtf(static_cast<float>(x1)));
+                cs = cs * fma(-0.5 * x1, cs * cs, 1.5);
+                double ig = static_cast<double>(igf);
+                ig = ig * fma(-0.5 * g2, ig * ig, 1.5);
+                const double sn = cs * t;
+                const c64 se = mk(sn * ga.re * ig, sn * ga.im * ig);  // s e
+#pragma unroll
+                for (int t2 = 0; t2 < RPL; ++t2) {
+                    const c64 u = x[t2], v = y[t2];
+                    // lo' = c x - conj(s e) y ; hi' = s e x + c y
+                    xlo[t2 * LPP] = mk(fma(cs, u.re, -fma(se.re, v.re, se.im * v.im)),
+                                       fma(cs, u.im, -fma(se.re, v.im, -se.im * v.re)));
+                    xhi[t2 * LPP] = mk(fma(cs, v.re, fma(se.re, u.re, -se.im * u.im)),
+                                       fma(cs, v.im, fma(se.re, u.im, se.im * u.re)));
+                }
+            }
+            rot_any |= rotate;
+            __syncwarp();
+        }
+        if (!__any_sync(0xffffffffu, rot_any)) {
+            sweeps = sweep + 1;
+            break;
+        }
+    }
+    c64* nxt = Yb;
+    const int c = lane;
+    const long long T2 = clock64();
+    // singular values, descending order (ties: lower index first)
+    if (c < p) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int r = 0; r < p; r += 2) {
+            s0 += norm2(cur[c * ld + r]);
+            s1 += norm2(cur[c * ld + r + 1]);
+        }
+        sig[c] = sqrt(s0 + s1);
+    }
+    __syncwarp();
+    if (lane < p) {
+        int rank = 0;
+        for (int q = 0; q < p; ++q)
+            if (q != lane && (sig[q] > sig[lane] || (sig[q] == sig[lane] && q < lane))) ++rank;
+        order[rank] = lane;
+    }
+    __syncwarp();
+    // T(:, kk) = R^-1 z / s (back substitution; R(i, j) = conj(L[i * p + j])), into nxt (free)
+    c64* Tm = nxt;
+    if (lane < k) {
+        const int kk = lane, cc = order[kk];
+        const double inv_s = sig[cc] > 0.0 ? 1.0 / sig[cc] : 0.0;
+        for (int i = p - 1; i >= 0; --i) {
+            c64 acc = cur[cc * ld + i];
+            acc.re *= inv_s;
+            acc.im *= inv_s;
+            for (int j = i + 1; j < p; ++j) {
+                const c64 rij = conj(L[i * p + j]);
+                const c64 tj = Tm[kk * ld + j];
+                acc.re -= rij.re * tj.re - rij.im * tj.im;
+                acc.im -= rij.re * tj.im + rij.im * tj.re;
+            }
+            const double rii = L[i * p + i].re;
+            const double inv = rii > 0.0 ? 1.0 / rii : 0.0;
+            Tm[kk * ld + i] = mk(acc.re * inv, acc.im * inv);
+        }
+        double lam = sig[cc];
+        lam *= lam;  // eigenvalue of B' = Y Y^H
+        eig[static_cast<size_t>(f) * k + kk] = lam;
+    }
+    __syncwarp();
+    c64* Tf = Tout + static_cast<size_t>(f) * p * k;
+    for (int e = lane; e < p * k; e += 32) Tf[e] = Tm[(e / p) * ld + (e % p)];
+    if (lane == 0 && sweeps == 0) atomicOr(&status[f], kFrameNoConv);
+    if (lane == 0 && dbg) dbg[f] = sweeps;
+    const long long T3 = clock64();
+    if (lane == 0 && g_phase_dbg) {
+        g_phase_dbg[f * 4 + 0] = static_cast<int>(T1 - T0);
+        g_phase_dbg[f * 4 + 1] = static_cast<int>(T2 - T1);
+        g_phase_dbg[f * 4 + 2] = static_cast<int>(T3 - T2);
+        g_phase_dbg[f * 4 + 3] = sweeps;
+    }
+}
+
+template <int PC>
+__global__ void __launch_bounds__(128) k_basis_ct(const c32* __restrict__ Cin, const c64* __restrict__ Tin,
+                                                  c64* __restrict__ basis, int m, int p, int k) {
+    __shared__ c64 Ts[PC * PC];
+    const int f = blockIdx.y;
+    const c64* Tf = Tin + static_cast<size_t>(f) * p * k;
+    for (int e = threadIdx.x; e < p * k; e += blockDim.x) Ts[e] = Tf[e];
+    __syncthreads();
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    const c32* Cf = Cin + static_cast<size_t>(f) * m * p;
+    c64 crow[PC];
+#pragma unroll
+    for (int q = 0; q < PC; ++q)
+        if (q < p) crow[q] = to64(Cf[static_cast<size_t>(q) * m + r]);
+    c64* Bf = basis + static_cast<size_t>(f) * m * k;
+    for (int kk = 0; kk < k; ++kk) {
+        c64 acc = mk(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < PC; ++q)
+            if (q < p) cmac(acc, crow[q], Ts[kk * p + q]);
+        Bf[static_cast<size_t>(kk) * m + r] = acc;
+    }
+}
+
 }  // namespace smb
 }  // namespace fmk
 
@@ -972,6 +1266,36 @@ cudaError_t fm_launch_final_tiled(const void* C, const void* V, const void* H, v
     if (p <= 8) return go(smb::k_final_tiled<8>, 8);
     if (p <= 16) return go(smb::k_final_tiled<16>, 16);
     return go(smb::k_final_tiled<32>, 32);
+}
+
+// Split final stage: G -> Gw, Herm(H) -> Hw (in place for fast1), T -> Tw (p x k per frame).
+cudaError_t fm_launch_final_split(const void* C, const void* V, void* Hw, void* Gw, void* Tw, void* basis, double* eig,
+                                  int32_t* status, int frames, int m, int p, int k, cudaStream_t s) {
+    if (p > 32 || (p & 3) || k > p || m < p || frames < 1) return cudaErrorInvalidValue;
+    auto go = [&](auto gram, auto small, auto bas, int pc, int warps, size_t warp_bytes) {
+        const size_t gsm = sizeof(c64) * 2 * pc * pc + sizeof(c64) * 3 * 64 * (pc + 1);
+        cudaError_t e = cudaFuncSetAttribute(gram, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsm));
+        if (e != cudaSuccess) return e;
+        gram<<<frames, smb::kNT, gsm, s>>>(static_cast<const c32*>(C), static_cast<const c32*>(V),
+                                           static_cast<c64*>(Gw), static_cast<c64*>(Hw), m, p);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        const size_t wsm = warp_bytes * warps;
+        e = cudaFuncSetAttribute(small, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm));
+        if (e != cudaSuccess) return e;
+        small<<<(frames + warps - 1) / warps, 32 * warps, wsm, s>>>(static_cast<const c64*>(Gw),
+                                                                    static_cast<const c64*>(Hw), static_cast<c64*>(Tw),
+                                                                    eig, status, frames, p, k, g_sweep_dbg);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        bas<<<dim3((m + 127) / 128, frames), 128, 0, s>>>(static_cast<const c32*>(C), static_cast<const c64*>(Tw),
+                                                          static_cast<c64*>(basis), m, p, k);
+        return cudaGetLastError();
+    };
+    using namespace smb;
+    if (p <= 8)
+        return go(k_gram_gh<8>, k_small_warp<8>, k_basis_ct<8>, 8, WarpCfg<8>::kWarps, WarpCfg<8>::kWarpBytes);
+    if (p <= 16)
+        return go(k_gram_gh<16>, k_small_warp<16>, k_basis_ct<16>, 16, WarpCfg<16>::kWarps, WarpCfg<16>::kWarpBytes);
+    return go(k_gram_gh<32>, k_small_warp<32>, k_basis_ct<32>, 32, WarpCfg<32>::kWarps, WarpCfg<32>::kWarpBytes);
 }
 
 cudaError_t fm_launch_nystrom_warp2(const void* H, const void* work, const void* Rt, void* basis, double* eig,
