@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "fm_common.cuh"
 
@@ -69,6 +70,156 @@ __global__ void __launch_bounds__(kNT) k_autocorr(const c64* __restrict__ basis,
             t[static_cast<size_t>(f) * m + d1] = a1;
             if (d2 != d1) t[static_cast<size_t>(f) * m + d2] = a2;
         }
+    }
+}
+
+// t_delta by the correlation theorem: with A_k = FFT_N(u_k) (zero-padded, N >= 2M - 1 so the
+// circular correlation has no wrap), sum_r u_k[r] conj(u_k[r + delta]) = (1/N) FFT_N(|A_k|^2)[delta],
+// hence t = (1/N) FFT_N(P), P = sum_k |A_k|^2 (real). O(K N log N) instead of O(K M^2).
+// One CTA per frame; `cnt` columns are transformed in lock-step in shared memory by a self-
+// sorting Stockham FFT: radix-8 passes (8-point DFTs in registers) plus one radix-4/2 pass,
+// twiddles exp(-2 pi i t k / (R p)) = w1(k)^t from per-pass sincospi tables. Shared indices are
+// padded by one slot per 8 (conflict-free stride-8 stores). fp64 throughout.
+__device__ __forceinline__ int fpad(int i) { return i + (i >> 3); }
+__device__ __forceinline__ c64 cmul(c64 a, c64 b) { return mk(a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re); }
+__device__ __forceinline__ c64 cadd(c64 a, c64 b) { return mk(a.re + b.re, a.im + b.im); }
+__device__ __forceinline__ c64 csub(c64 a, c64 b) { return mk(a.re - b.re, a.im - b.im); }
+__device__ __forceinline__ c64 mul_mi(c64 a) { return mk(a.im, -a.re); }  // a * (-i)
+
+template <int R>
+__device__ __forceinline__ void dft_r(c64 (&x)[R]) {
+    if constexpr (R == 2) {
+        const c64 a = x[0], b = x[1];
+        x[0] = cadd(a, b);
+        x[1] = csub(a, b);
+    } else if constexpr (R == 4) {
+        const c64 a0 = cadd(x[0], x[2]), a1 = csub(x[0], x[2]), a2 = cadd(x[1], x[3]), a3 = mul_mi(csub(x[1], x[3]));
+        x[0] = cadd(a0, a2);
+        x[1] = cadd(a1, a3);
+        x[2] = csub(a0, a2);
+        x[3] = csub(a1, a3);
+    } else {
+        constexpr double r2 = 0.70710678118654752440;
+        const c64 a0 = cadd(x[0], x[4]), a1 = csub(x[0], x[4]), a2 = cadd(x[2], x[6]), a3 = mul_mi(csub(x[2], x[6]));
+        const c64 b0 = cadd(x[1], x[5]), b1 = csub(x[1], x[5]), b2 = cadd(x[3], x[7]), b3 = mul_mi(csub(x[3], x[7]));
+        const c64 e0 = cadd(a0, a2), e2 = csub(a0, a2), e1 = cadd(a1, a3), e3 = csub(a1, a3);
+        const c64 o0 = cadd(b0, b2), o2 = csub(b0, b2), o1 = cadd(b1, b3), o3 = csub(b1, b3);
+        const c64 w1 = mk(r2 * (o1.re + o1.im), r2 * (o1.im - o1.re));    // (1 - i)/sqrt2 * o1
+        const c64 w2 = mul_mi(o2);                                        // -i * o2
+        const c64 w3 = mk(r2 * (o3.im - o3.re), -r2 * (o3.re + o3.im));   // (-1 - i)/sqrt2 * o3
+        x[0] = cadd(e0, o0);
+        x[4] = csub(e0, o0);
+        x[1] = cadd(e1, w1);
+        x[5] = csub(e1, w1);
+        x[2] = cadd(e2, w2);
+        x[6] = csub(e2, w2);
+        x[3] = cadd(e3, w3);
+        x[7] = csub(e3, w3);
+    }
+}
+
+// One Stockham pass of radix R with input stride p over cnt transforms (in place: all loads
+// of the pass complete before any store). Each thread holds at most 8 values.
+template <int R>
+__device__ void fft_pass(c64* a, int logn, int cnt, int p, const c64* twp) {
+    constexpr int LR = R == 8 ? 3 : (R == 4 ? 2 : 1);
+    constexpr int GPT = 8 / R;
+    const int nfft = 1 << logn, lt = logn - LR, T = 1 << lt;
+    const int total = cnt << lt;
+    c64 x[GPT][R];
+#pragma unroll
+    for (int g = 0; g < GPT; ++g) {
+        const int e = threadIdx.x + g * blockDim.x;
+        if (e < total) {
+            const int q = e >> lt, i = e & (T - 1);
+#pragma unroll
+            for (int t = 0; t < R; ++t) x[g][t] = a[fpad((q << logn) + i + t * T)];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < GPT; ++g) {
+        const int e = threadIdx.x + g * blockDim.x;
+        if (e < total) {
+            const int q = e >> lt, i = e & (T - 1);
+            const int k = i & (p - 1);
+            const c64 w1 = twp[k];
+            c64 w = w1;
+#pragma unroll
+            for (int t = 1; t < R; ++t) {
+                x[g][t] = cmul(x[g][t], w);
+                if (t + 1 < R) w = cmul(w, w1);
+            }
+            dft_r<R>(x[g]);
+            const int j = ((i - k) << LR) + k;
+#pragma unroll
+            for (int t = 0; t < R; ++t) a[fpad((q << logn) + j + t * p)] = x[g][t];
+        }
+    }
+    __syncthreads();
+}
+
+// Full transform of cnt sequences: radix-8 passes, then a radix-4 or radix-2 pass.
+__device__ void fft_stockham(c64* a, int logn, int cnt, const c64* tw) {
+    int p = 1, off = 0;
+    for (int l = logn; l >= 3; l -= 3) {
+        fft_pass<8>(a, logn, cnt, p, tw + off);
+        off += p;
+        p <<= 3;
+    }
+    const int rem = logn % 3;
+    if (rem == 2) fft_pass<4>(a, logn, cnt, p, tw + off);
+    else if (rem == 1) fft_pass<2>(a, logn, cnt, p, tw + off);
+}
+
+__global__ void __launch_bounds__(kNT, 2) k_autocorr_fft(const c64* __restrict__ basis, c64* __restrict__ t, int m, int k,
+                                                   int logn, int grp) {
+    extern __shared__ c64 fsm[];
+    const int nfft = 1 << logn;
+    c64* tw = fsm;                                         // < nfft entries: per-pass w1 tables
+    double* P = reinterpret_cast<double*>(tw + nfft);      // nfft
+    c64* buf = reinterpret_cast<c64*>(P + nfft);           // fpad(grp * nfft)
+    const int f = blockIdx.x;
+    const c64* Uf = basis + static_cast<size_t>(f) * m * k;
+    {  // twiddle tables: pass with stride p and radix R holds exp(-2 pi i k / (R p)), k < p
+        int p = 1, off = 0;
+        for (int l = logn; l > 0;) {
+            const int lr = l >= 3 ? 3 : l;
+            const int rp = p << lr;
+            for (int kk = threadIdx.x; kk < p; kk += blockDim.x) {
+                double sn, cs;
+                sincospi(-2.0 * static_cast<double>(kk) / static_cast<double>(rp), &sn, &cs);
+                tw[off + kk] = mk(cs, sn);
+            }
+            off += p;
+            p = rp;
+            l -= lr;
+        }
+    }
+    for (int j = threadIdx.x; j < nfft; j += blockDim.x) P[j] = 0.0;
+    for (int k0 = 0; k0 < k; k0 += grp) {
+        const int cnt = min(grp, k - k0);
+        __syncthreads();  // previous group's P accumulation done with buf; tables ready
+        for (int e = threadIdx.x; e < (cnt << logn); e += blockDim.x) {
+            const int q = e >> logn, r = e & (nfft - 1);
+            buf[fpad(e)] = r < m ? Uf[static_cast<size_t>(k0 + q) * m + r] : mk(0.0, 0.0);
+        }
+        __syncthreads();
+        fft_stockham(buf, logn, cnt, tw);
+        for (int j = threadIdx.x; j < nfft; j += blockDim.x) {
+            double acc = P[j];
+            for (int q = 0; q < cnt; ++q) acc += norm2(buf[fpad((q << logn) + j)]);
+            P[j] = acc;
+        }
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < nfft; r += blockDim.x) buf[fpad(r)] = mk(P[r], 0.0);
+    __syncthreads();
+    fft_stockham(buf, logn, 1, tw);
+    const double inv = 1.0 / static_cast<double>(nfft);
+    for (int d = threadIdx.x; d < m; d += blockDim.x) {
+        const c64 v = buf[fpad(d)];
+        t[static_cast<size_t>(f) * m + d] = mk(v.re * inv, v.im * inv);
     }
 }
 
@@ -391,6 +542,27 @@ __global__ void __launch_bounds__(kNT) k_orthocheck(const c64* __restrict__ basi
 using namespace fmk;
 
 cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, int k, cudaStream_t s) {
+    static const bool direct = std::getenv("FM_DIRECT_AUTOCORR") != nullptr;  // comparison switch
+    int logn = 1;
+    while ((1 << logn) < 2 * m - 1) ++logn;
+    if (!direct && logn <= 12) {
+        const int nfft = 1 << logn;
+        const size_t fixed = sizeof(c64) * nfft + sizeof(double) * nfft;
+        const size_t per = sizeof(c64) * (nfft + nfft / 8);  // padded
+        const size_t budget = 96 * 1024;
+        int grp = static_cast<int>(std::max<size_t>(1, budget > fixed ? (budget - fixed) / per : 1));
+        grp = std::min(grp, std::max(1, 8 * spec::kNT / nfft));  // <= 8 values per thread per pass
+        grp = std::max(1, std::min(grp, k));
+        const size_t smem = fixed + per * grp + sizeof(c64);
+        if (smem <= 200 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(spec::k_autocorr_fft, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            spec::k_autocorr_fft<<<frames, spec::kNT, smem, s>>>(static_cast<const c64*>(basis), static_cast<c64*>(t),
+                                                                 m, k, logn, grp);
+            return cudaGetLastError();
+        }
+    }
     const size_t smem = sizeof(c64) * m;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(spec::k_autocorr, cudaFuncAttributeMaxDynamicSharedMemorySize,
