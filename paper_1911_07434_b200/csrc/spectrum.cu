@@ -200,9 +200,19 @@ __global__ void __launch_bounds__(kNT, 2) k_autocorr_fft(const c64* __restrict__
     for (int k0 = 0; k0 < k; k0 += grp) {
         const int cnt = min(grp, k - k0);
         __syncthreads();  // previous group's P accumulation done with buf; tables ready
-        for (int e = threadIdx.x; e < (cnt << logn); e += blockDim.x) {
-            const int q = e >> logn, r = e & (nfft - 1);
-            buf[fpad(e)] = r < m ? Uf[static_cast<size_t>(k0 + q) * m + r] : mk(0.0, 0.0);
+        for (int e0 = 0; e0 < (cnt << logn); e0 += 8 * blockDim.x) {  // 8 loads in flight per thread
+            c64 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + threadIdx.x + u * blockDim.x;
+                const int q = e >> logn, r = e & (nfft - 1);
+                v[u] = (e < (cnt << logn) && r < m) ? Uf[static_cast<size_t>(k0 + q) * m + r] : mk(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + threadIdx.x + u * blockDim.x;
+                if (e < (cnt << logn)) buf[fpad(e)] = v[u];
+            }
         }
         __syncthreads();
         fft_stockham(buf, logn, cnt, tw);
