@@ -60,7 +60,7 @@ cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K,
                                  cudaStream_t s);
 cudaError_t fm_launch_orthocheck(const void* basis, int frames, int m, int k, double* dev, cudaStream_t s);
 cudaError_t fm_launch_spectrum_multi(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
-                                     double* spec64, cudaStream_t s);
+                                     double* spec64, cudaStream_t s, bool symmetric);
 template <typename T>
 cudaError_t fm_launch_jacobi_eig(const void* R, void* work, void* basis, double* eig, int32_t* status, int frames,
                                  int m, int k, cudaStream_t s);
@@ -672,8 +672,12 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     if (prof) mark(pl, 2, s);
     FM_LAUNCH(fm_launch_autocorr(basis, w.t, F, M, K, s));
     if (prof) mark(pl, 3, s);
+    // mirror-symmetric grid (theta0 = -theta1): pairs (theta, -theta) share one evaluation;
+    // FM_NO_SYM_SPECTRUM=1 forces the per-point kernel (comparison)
+    static const bool no_sym = std::getenv("FM_NO_SYM_SPECTRUM") != nullptr;
+    const bool sym = !no_sym && d.theta0 == -d.theta1;
     FM_LAUNCH(fm_launch_spectrum_multi(w.t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, w.spec64,
-                                       s));
+                                       s, sym));
     FM_LAUNCH(fm_launch_peaks_only(w.spec64, F, static_cast<int>(d.grid_size), K, static_cast<int>(d.min_sep_cells),
                                    io->peak_cells, io->peak_heights, io->baseline, io->peak_count, w.scratch, s));
     if (prof) mark(pl, 4, s);

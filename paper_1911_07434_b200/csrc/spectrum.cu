@@ -503,6 +503,80 @@ __global__ void __launch_bounds__(kNT) k_spectrum_multi(const c64* __restrict__ 
     }
 }
 
+// Mirror-symmetric grids (theta0 = -theta1: theta_{L-1-q} = -theta_q, z_{L-1-q} = conj z_q):
+// with A = sum_delta Re t_delta Re z^delta and B = sum_delta Im t_delta Im z^delta,
+//     Re sum t_delta z^delta = A - B   (theta_q),      Re sum t_delta conj(z)^delta = A + B   (-theta_q),
+// so a mirrored pair costs what one point costs in k_spectrum_multi. Thread = two pairs
+// (q0, q0 + qh); the block's kSFPB frames share the two power sequences (fp64 recurrence).
+constexpr int kSFPB = 8;
+
+__global__ void __launch_bounds__(kNT) k_spectrum_sym(const c64* __restrict__ t, const c64* __restrict__ zgrid,
+                                                      int frames, int m, int L, float* __restrict__ spec32,
+                                                      double* __restrict__ spec64) {
+    extern __shared__ c64 st[];  // kSFPB x m coefficients, delta-major
+    const int f0 = blockIdx.y * kSFPB;
+    const int nf = min(kSFPB, frames - f0);
+    for (int e = threadIdx.x; e < kSFPB * m; e += kNT) {
+        const int f = e / m, dl = e % m;
+        st[dl * kSFPB + f] = f < nf ? t[static_cast<size_t>(f0 + f) * m + dl] : mk(0.0, 0.0);
+    }
+    __syncthreads();
+    const int nq = (L + 1) / 2;          // pairs (q, L-1-q); q = L/2 is self-paired when L is odd
+    const int qh = (nq + 1) / 2;
+    const int q0 = blockIdx.x * kNT + threadIdx.x;
+    if (q0 >= qh) return;
+    const int q1 = q0 + qh;
+    const bool has1 = q1 < nq;
+    const c64 za = zgrid[q0];
+    const c64 zb = has1 ? zgrid[q1] : mk(1.0, 0.0);
+    double A0[kSFPB], B0[kSFPB], A1[kSFPB], B1[kSFPB];
+#pragma unroll
+    for (int f = 0; f < kSFPB; ++f) A0[f] = B0[f] = A1[f] = B1[f] = 0.0;
+    double ar = 1.0, ai = 0.0, br = 1.0, bi = 0.0;
+    for (int dl = 1; dl < m; ++dl) {
+        const double nar = fma(ar, za.re, -ai * za.im);
+        const double nai = fma(ar, za.im, ai * za.re);
+        const double nbr = fma(br, zb.re, -bi * zb.im);
+        const double nbi = fma(br, zb.im, bi * zb.re);
+        ar = nar;
+        ai = nai;
+        br = nbr;
+        bi = nbi;
+        const c64* row = st + dl * kSFPB;
+#pragma unroll
+        for (int f = 0; f < kSFPB; ++f) {
+            const c64 c = row[f];
+            A0[f] = fma(c.re, ar, A0[f]);
+            B0[f] = fma(c.im, ai, B0[f]);
+            A1[f] = fma(c.re, br, A1[f]);
+            B1[f] = fma(c.im, bi, B1[f]);
+        }
+    }
+    const double floor_v = 1e-12 * static_cast<double>(m);
+#pragma unroll
+    for (int f = 0; f < kSFPB; ++f) {
+        if (f < nf) {
+            const double c0 = static_cast<double>(m) - st[f].re;
+            const size_t o = static_cast<size_t>(f0 + f) * L;
+            const int qs[2] = {q0, q1};
+            const double As[2] = {A0[f], A1[f]}, Bs[2] = {B0[f], B1[f]};
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                if (u == 1 && !has1) break;
+                const int q = qs[u], qm = L - 1 - q;
+                const double Pp = 1.0 / fmax(c0 - 2.0 * (As[u] - Bs[u]), floor_v);
+                if (spec32) spec32[o + q] = static_cast<float>(Pp);
+                spec64[o + q] = Pp;
+                if (qm != q) {
+                    const double Pm = 1.0 / fmax(c0 - 2.0 * (As[u] + Bs[u]), floor_v);
+                    if (spec32) spec32[o + qm] = static_cast<float>(Pm);
+                    spec64[o + qm] = Pm;
+                }
+            }
+        }
+    }
+}
+
 // Peaks only, on caller-provided fp64 values (facade extract_peaks).
 __global__ void __launch_bounds__(kNT) k_peaks_only(const double* __restrict__ values, int L, int K, int min_sep,
                                                     PeakOut out, int32_t* __restrict__ overflow_flag) {
@@ -605,7 +679,18 @@ cudaError_t fm_launch_spectrum_peaks(const void* t, const void* zgrid, int frame
 }
 
 cudaError_t fm_launch_spectrum_multi(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
-                                     double* spec64, cudaStream_t s) {
+                                     double* spec64, cudaStream_t s, bool symmetric) {
+    if (symmetric && sizeof(c64) * spec::kSFPB * m <= 200 * 1024) {
+        const size_t smem = sizeof(c64) * spec::kSFPB * m;
+        cudaError_t e = cudaFuncSetAttribute(spec::k_spectrum_sym, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        const int qh = ((L + 1) / 2 + 1) / 2;
+        dim3 grid((qh + spec::kNT - 1) / spec::kNT, (frames + spec::kSFPB - 1) / spec::kSFPB);
+        spec::k_spectrum_sym<<<grid, spec::kNT, smem, s>>>(static_cast<const c64*>(t), static_cast<const c64*>(zgrid),
+                                                           frames, m, L, spec32, spec64);
+        return cudaGetLastError();
+    }
     auto go = [&](auto kern, int fpb) {
         const size_t smem = sizeof(c64) * fpb * m;
         if (smem > 200 * 1024) return cudaErrorInvalidValue;
