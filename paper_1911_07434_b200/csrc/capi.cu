@@ -49,6 +49,8 @@ cudaError_t fm_launch_final_tiled(const void* C, const void* V, const void* H, v
                                   int32_t* status, int frames, int m, int p, int k, cudaStream_t s);
 cudaError_t fm_launch_rmul_tc(const float* d_r, const float* d_omega, const float* d_v, float* d_c, int64_t frames,
                               int64_t m, int64_t p, cudaStream_t stream);
+cudaError_t fm_launch_orth_split(const void* C, void* Vout, void* Lw, int32_t* permw, int32_t* status, int frames,
+                                 int m, int p, cudaStream_t s);
 cudaError_t fm_launch_final_split(const void* C, const void* V, void* Hw, void* Gw, void* Tw, void* basis, double* eig,
                                   int32_t* status, int frames, int m, int p, int k, cudaStream_t s);
 cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, int k, cudaStream_t s);
@@ -514,7 +516,8 @@ extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
     int n = 1 /*cov*/ + 1 /*clear*/ + 3 /*autocorr, spectrum, peaks*/;
     const bool tiled = plan->d.p <= 32 && (plan->d.p % 4) == 0;
     const int fin = tiled ? (split_final() ? 3 : 1) : 2;  // gram, small-warp, basis | fused | cholqr, nystrom
-    if (plan->d.method == FM_METHOD_FAST2) n += 1 + 2 * t + fin;  // rmul, t x (orth, rmul), final
+    const int orth = tiled && split_final() ? 3 : 1;  // gram, pivoted chol, rows solve | fused
+    if (plan->d.method == FM_METHOD_FAST2) n += 1 + t * (orth + 1) + fin;  // rmul, t x (orth, rmul), final
     else if (plan->d.method == FM_METHOD_FAST1) n += 1 + fin;      // gather, final
     else n += 1;                                                    // jacobi
     return n;
@@ -614,7 +617,10 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     const bool tiled = P <= 32 && (P % 4) == 0;  // register-tiled Gram + fused final stage
     auto orth = [&](bool final_mode, const void* vin) -> fm_status {
         if (tiled && !final_mode) {
-            FM_LAUNCH(fm_launch_orth_tiled(w.C, w.V, io->status, F, M, P, s));
+            if (split_final())
+                FM_LAUNCH(fm_launch_orth_split(w.C, w.V, w.Rt, reinterpret_cast<int32_t*>(w.H), io->status, F, M, P, s));
+            else
+                FM_LAUNCH(fm_launch_orth_tiled(w.C, w.V, io->status, F, M, P, s));
             return FM_OK;
         }
         if (warp_path)

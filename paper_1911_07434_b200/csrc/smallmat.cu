@@ -17,6 +17,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "fm_common.cuh"
@@ -1204,6 +1205,146 @@ __global__ void __launch_bounds__(128) k_basis_ct(const c32* __restrict__ Cin, c
     }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Split power-iteration orthonormalisation (R/src/linalg.cpp:127-141 qr_orthonormal with the
+// Eigen ColPivHouseholderQR rank rule), same algebra as k_orth_tiled:
+//   k_gram_only : G = C^H C (fp64, block per frame) -> workspace
+//   k_cholpiv_warp: pivoted Cholesky of G by one warp per frame (pivot = largest remaining Schur
+//                 diagonal), rank rule in fp32 epsilon -> L (by original row index) + perm
+//   k_rows_solve: V = C P R^-1 by forward substitution, thread per row (fp64 -> complex64)
+template <int PC>
+__global__ void __launch_bounds__(kNT, 2) k_gram_only(const c32* __restrict__ Cin, c64* __restrict__ Gout, int m,
+                                                   int p) {
+    extern __shared__ uint8_t dsm[];
+    c64* G = reinterpret_cast<c64*>(dsm);
+    c64* stage = G + PC * PC;
+    const int f = blockIdx.x;
+    tiled_gram2<c32, c32>(Cin + static_cast<size_t>(f) * m * p, true, Cin + static_cast<size_t>(f) * m * p, nullptr,
+                          nullptr, m, p, stage, G, nullptr);
+    c64* Gf = Gout + static_cast<size_t>(f) * p * p;
+    for (int e = threadIdx.x; e < p * p; e += kNT) Gf[e] = G[e];
+}
+
+template <int PC> struct PivCfg {
+    static constexpr int kWarps = PC <= 16 ? 8 : 4;
+    static constexpr size_t kWarpBytes = sizeof(c64) * 2 * PC * PC + sizeof(double) * PC;
+};
+
+template <int PC>
+__global__ void __launch_bounds__(32 * PivCfg<PC>::kWarps)
+    k_cholpiv_warp(c64* __restrict__ GL, int32_t* __restrict__ perm_out, int32_t* __restrict__ status, int frames,
+                   int m, int p) {
+    extern __shared__ uint8_t dsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int f = blockIdx.x * PivCfg<PC>::kWarps + warp;
+    if (f >= frames) return;
+    c64* A = reinterpret_cast<c64*>(dsm + warp * PivCfg<PC>::kWarpBytes);
+    c64* L = A + PC * PC;
+    double* d = reinterpret_cast<double*>(L + PC * PC);
+    c64* GLf = GL + static_cast<size_t>(f) * p * p;
+    for (int e = lane; e < p * p; e += 32) {
+        A[e] = GLf[e];
+        L[e] = mk(0.0, 0.0);
+    }
+    __syncwarp();
+    bool done = lane >= p;  // lane i <-> original row / column i
+    int my_step = -1;
+    for (int k = 0; k < p; ++k) {
+        // pivot: largest remaining Schur diagonal, ties -> lower index
+        double best = done ? -1.0 : A[lane * p + lane].re;
+        int bi = done ? p : lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ob > best || (ob == best && oi < bi)) {
+                best = ob;
+                bi = oi;
+            }
+        }
+        const int piv = bi;
+        const double dk = A[piv * p + piv].re;
+        const double inv = dk > 0.0 ? 1.0 / sqrt(dk) : 0.0;
+        if (lane == 0) d[k] = dk;
+        if (lane == piv) {
+            done = true;
+            my_step = k;
+        }
+        // l_k(i) = A(i, piv) / sqrt(d_k) for rows not yet eliminated (incl. piv)
+        c64 li = mk(0.0, 0.0);
+        if (lane < p && (!done || lane == piv)) {
+            const c64 a = A[piv * p + lane];
+            li = mk(a.re * inv, a.im * inv);
+        }
+        if (lane < p) L[k * p + lane] = li;
+        __syncwarp();
+        if (lane < p && !done) {  // A(i, j) -= l_i conj(l_j) over live j
+            for (int j = 0; j < p; ++j) {
+                const c64 lj = L[k * p + j];
+                c64 a = A[j * p + lane];
+                a.re -= li.re * lj.re + li.im * lj.im;
+                a.im -= li.im * lj.re - li.re * lj.im;
+                A[j * p + lane] = a;
+            }
+        }
+        __syncwarp();
+    }
+    if (lane < p) perm_out[static_cast<size_t>(f) * p + my_step] = lane;
+    for (int e = lane; e < p * p; e += 32) GLf[e] = L[e];
+    if (lane == 0) {  // Eigen ColPivHouseholderQR rank rule (fp32 epsilon), as k_orth_tiled
+        const double eps = eps_of<float>::value;
+        const double thr_helper = fmax(d[0], 0.0) * eps * eps / static_cast<double>(m);
+        int nonzero = p;
+        double maxpivot = 0.0;
+        for (int k = 0; k < p; ++k) {
+            if (nonzero == p && d[k] < thr_helper * static_cast<double>(m - k)) nonzero = k;
+            maxpivot = fmax(maxpivot, sqrt(fmax(d[k], 0.0)));
+        }
+        const double thr = maxpivot * eps * static_cast<double>(p);
+        int rank = 0;
+        for (int k = 0; k < nonzero; ++k) rank += sqrt(fmax(d[k], 0.0)) > thr ? 1 : 0;
+        if (rank < p) atomicOr(&status[f], kFrameRank);
+    }
+}
+
+template <int PC>
+__global__ void __launch_bounds__(128) k_rows_solve(const c32* __restrict__ Cin, const c64* __restrict__ Lin,
+                                                    const int32_t* __restrict__ perm_in, c32* __restrict__ Vout, int m,
+                                                    int p) {
+    __shared__ c64 L[PC * PC];
+    __shared__ int perm[PC];
+    const int f = blockIdx.y;
+    for (int e = threadIdx.x; e < p * p; e += blockDim.x) L[e] = Lin[static_cast<size_t>(f) * p * p + e];
+    for (int e = threadIdx.x; e < p; e += blockDim.x) perm[e] = perm_in[static_cast<size_t>(f) * p + e];
+    __syncthreads();
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    const c32* X = Cin + static_cast<size_t>(f) * m * p;
+    c32* Out = Vout + static_cast<size_t>(f) * m * p;
+    c64 v[PC];
+#pragma unroll
+    for (int j = 0; j < PC; ++j) {
+        if (j < p) {
+            const int pj = perm[j];
+            c64 x = to64(X[static_cast<size_t>(pj) * m + r]);
+#pragma unroll
+            for (int a = 0; a < PC; ++a) {
+                if (a < j) {
+                    const c64 l = L[a * p + pj];
+                    x.re -= v[a].re * l.re + v[a].im * l.im;
+                    x.im -= v[a].im * l.re - v[a].re * l.im;
+                }
+            }
+            const double ljj = L[j * p + pj].re;
+            const double inv = ljj > 0.0 ? 1.0 / ljj : 0.0;
+            v[j] = mk(x.re * inv, x.im * inv);
+            Out[static_cast<size_t>(j) * m + r] = mk(static_cast<float>(v[j].re), static_cast<float>(v[j].im));
+        }
+    }
+}
+
+
 }  // namespace smb
 }  // namespace fmk
 
@@ -1266,6 +1407,34 @@ cudaError_t fm_launch_final_tiled(const void* C, const void* V, const void* H, v
     if (p <= 8) return go(smb::k_final_tiled<8>, 8);
     if (p <= 16) return go(smb::k_final_tiled<16>, 16);
     return go(smb::k_final_tiled<32>, 32);
+}
+
+// Split orthonormalisation: G -> Lw (in place), perm -> permw, V = C P R^-1 -> Vout.
+cudaError_t fm_launch_orth_split(const void* C, void* Vout, void* Lw, int32_t* permw, int32_t* status, int frames,
+                                 int m, int p, cudaStream_t s) {
+    if (p > 32 || (p & 3) || m < p || frames < 1) return cudaErrorInvalidValue;
+    auto go = [&](auto gram, auto piv, auto solve, int pc, int pw, size_t pbytes) {
+        const size_t gsm = sizeof(c64) * pc * pc + sizeof(c64) * 3 * 64 * (pc + 1);
+        cudaError_t e = cudaFuncSetAttribute(gram, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsm));
+        if (e != cudaSuccess) return e;
+        gram<<<frames, smb::kNT, gsm, s>>>(static_cast<const c32*>(C), static_cast<c64*>(Lw), m, p);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(piv, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pw * pbytes));
+        if (e != cudaSuccess) return e;
+        piv<<<(frames + pw - 1) / pw, 32 * pw, pw * pbytes, s>>>(static_cast<c64*>(Lw), permw, status, frames, m, p);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        solve<<<dim3((m + 127) / 128, frames), 128, 0, s>>>(static_cast<const c32*>(C), static_cast<const c64*>(Lw),
+                                                            permw, static_cast<c32*>(Vout), m, p);
+        return cudaGetLastError();
+    };
+    using namespace smb;
+    if (p <= 8)
+        return go(k_gram_only<8>, k_cholpiv_warp<8>, k_rows_solve<8>, 8, PivCfg<8>::kWarps, PivCfg<8>::kWarpBytes);
+    if (p <= 16)
+        return go(k_gram_only<16>, k_cholpiv_warp<16>, k_rows_solve<16>, 16, PivCfg<16>::kWarps,
+                  PivCfg<16>::kWarpBytes);
+    return go(k_gram_only<32>, k_cholpiv_warp<32>, k_rows_solve<32>, 32, PivCfg<32>::kWarps, PivCfg<32>::kWarpBytes);
 }
 
 // Split final stage: G -> Gw, Herm(H) -> Hw (in place for fast1), T -> Tw (p x k per frame).
