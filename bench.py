@@ -320,33 +320,35 @@ def run_ours(args):
             dist.destroy_process_group()
         return 0
 
-    # ---------------- roofline (dominant stage) + path roofline
+    # ---------------- roofline of the dominant kernel, timed alone: one sub-batch (the whole
+    # batch in one launch per kernel), CUDA events on the plan's launch stream around each stage
     hbm, bf16, bf16_sus, src = load_peaks()
     alg = algorithmic(cfgd)
-    stage_ms = {k: v / max(runs, 1) for k, v in stage_sum.items()}  # sub-batch 0 (fsub frames)
-    dom = max(stage_ms, key=stage_ms.get)
+    stage_ms = {k: v / max(runs, 1) for k, v in stage_sum.items()}  # sub-batch 0 (fsub frames), in-step
+    plan.set_concurrency(1)
+    plan.set_profiling(True)
+    for _ in range(args.roof_steps):
+        plan.run(B, xd, omega, idx, out, stream=stream)
+    torch.cuda.synchronize()
+    alone_sum, alone_runs = plan.stage_times_ms()
+    plan.set_profiling(False)
+    plan.set_concurrency(nsub)
+    alone_ms = {k: v / max(alone_runs, 1) for k, v in alone_sum.items()}  # all B frames, one launch per kernel
     prof = {}
     try:
         with open(os.path.join(ROOT, "profiles", f"ncu_summary_{args.config}.json")) as f:
             prof = json.load(f)
     except Exception:
         pass
-    if dom == "covariance":
-        bytes_launch = fsub * (8.0 * M * N + 8.0 * M * M)  # X read + R (fp32 complex) written
-        achieved = bytes_launch / (stage_ms[dom] / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": "fmk::cov::cov_tc_kernel", "achieved": achieved, "peak": hbm,
-                "unit": "GB/s", "frac": achieved / hbm, "peak_source": src,
-                "bytes_per_launch": bytes_launch,
-                "traffic": prof.get("cov_tc_kernel", {}).get("dram_bytes")}
-    else:
-        names = {"subspace": "k_rmul/k_qr/k_nystrom", "autocorr": "fmk::spec::k_autocorr",
-                 "spectrum_peaks": "fmk::spec::k_spectrum_peaks"}
-        flops = {"subspace": fsub * alg["w_rf"], "autocorr": fsub * 4.0 * K * M * M,
-                 "spectrum_peaks": fsub * 8.0 * (M - 1) * L}[dom]
-        achieved = flops / (stage_ms[dom] / 1e3) / 1e12
-        roof = {"bound": "fp64", "kernel": names[dom], "achieved": achieved, "peak": 37.0, "unit": "TFLOP/s",
-                "frac": achieved / 37.0, "peak_source": "B200 FP64 nominal (no measured FP64 peak)",
-                "traffic": None}
+    bytes_launch = B * (8.0 * M * N + 8.0 * M * M)  # algorithmic: X read once + R (complex64) written once
+    achieved = bytes_launch / (alone_ms["covariance"] / 1e3) / 1e9
+    cov_prof = prof.get("cov_tc_kernel", {})
+    roof = {"bound": "hbm", "kernel": "fmk::cov::cov_tc_kernel (tcgen05 cta_group::2 + TMA)", "achieved": achieved,
+            "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "peak_source": src,
+            "bytes_per_launch": bytes_launch, "launch_ms": alone_ms["covariance"],
+            "share_of_step": alone_ms["covariance"] / sum(alone_ms.values()),
+            "traffic": (cov_prof["dram_bytes"] * B / cov_prof["frames"]) if "dram_bytes" in cov_prof else None,
+            "traffic_source": cov_prof.get("source")}
     p_tf32 = bf16 / 2.0
     t_roof_ms = max(B * alg["q_frame"] / (hbm * 1e9), B * alg["w_frame"] / (p_tf32 * 1e12)) * 1e3
     line = {
@@ -362,6 +364,8 @@ def run_ours(args):
         "stages_ms_per_step": stage_ms,
         "stages_note": f"CUDA-event durations of sub-batch 0 ({fsub} of {B} frames); {nsub} sub-batches run "
                        f"concurrently on plan-owned streams",
+        "stages_alone_ms": alone_ms,
+        "stages_alone_note": f"all {B} frames in one launch per kernel (concurrency 1), {args.roof_steps} runs",
         "subbatches": nsub,
         "gpu_launches": args.steps * plan.launches_per_batch() * nsub,
         "clocks": clk.summary(),
@@ -398,6 +402,7 @@ def main():
     ap.add_argument("--frames", type=int, default=0, help="override frames per GPU")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--subbatches", type=int, default=0, help="concurrent sub-batches per step (0 = auto)")
+    ap.add_argument("--roof-steps", type=int, default=10, help="runs of the isolated roofline measurement")
     ap.add_argument("--cpu-frames", type=int, default=64)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
