@@ -52,7 +52,8 @@ cudaError_t fm_launch_rmul_tc(const float* d_r, const float* d_omega, const floa
 cudaError_t fm_launch_orth_split(const void* C, void* Vout, void* Lw, int32_t* permw, int32_t* status, int frames,
                                  int m, int p, cudaStream_t s);
 cudaError_t fm_launch_final_split(const void* C, const void* V, void* Hw, void* Gw, void* Tw, void* basis, double* eig,
-                                  int32_t* status, int frames, int m, int p, int k, cudaStream_t s);
+                                  int32_t* status, int frames, int m, int p, int k, cudaStream_t s,
+                                  double* eig_next = nullptr);
 cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, int k, cudaStream_t s);
 cudaError_t fm_launch_spectrum_peaks(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
                                      double* spec64, int K, int min_sep, int32_t* cells, double* heights,
@@ -65,7 +66,7 @@ cudaError_t fm_launch_spectrum_multi(const void* t, const void* zgrid, int frame
                                      double* spec64, cudaStream_t s, bool symmetric);
 template <typename T>
 cudaError_t fm_launch_jacobi_eig(const void* R, void* work, void* basis, double* eig, int32_t* status, int frames,
-                                 int m, int k, cudaStream_t s);
+                                 int m, int k, cudaStream_t s, int only_flagged = 0);
 
 namespace {
 
@@ -94,6 +95,48 @@ __global__ void k_clear_bits(int32_t* status, int frames, int32_t bits) {
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
     if (f < frames) status[f] &= ~bits;
 }
+
+// Exact method, certification of the subspace iteration (run_post_cov): U (complex128, K x M
+// column-major) -> complex64 for the tensor-core product R U.
+__global__ void k_basis_to_c32(const double* __restrict__ basis, float* __restrict__ u32, int64_t n) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) u32[i] = static_cast<float>(basis[i]);
+}
+
+__device__ double* g_exact_ratio = nullptr;  // debug: per-frame residual / gap
+
+// Frame certified iff no flag from the iteration and max_k ||R u_k - lambda_k u_k|| <= tol * gap,
+// gap = lambda_K - lambda_{K+1} (Ritz). Uncertified frames get kFrameRefine (Jacobi reruns them).
+// One warp per frame.
+__global__ void k_exact_certify(const float* __restrict__ ru, const double* __restrict__ basis,
+                                const double* __restrict__ eig, const double* __restrict__ eig_next,
+                                const int32_t* __restrict__ iter_status, int32_t* __restrict__ status, int frames,
+                                int m, int k, double tol) {
+    const int f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (f >= frames) return;
+    const float* rf = ru + static_cast<size_t>(f) * k * m * 2;
+    const double* uf = basis + static_cast<size_t>(f) * k * m * 2;
+    double worst = 0.0;
+    for (int kk = 0; kk < k; ++kk) {
+        const double lam = eig[static_cast<size_t>(f) * k + kk];
+        double s2 = 0.0;
+        for (int r = lane; r < m; r += 32) {
+            const size_t o = (static_cast<size_t>(kk) * m + r) * 2;
+            const double dr = static_cast<double>(rf[o]) - lam * uf[o];
+            const double di = static_cast<double>(rf[o + 1]) - lam * uf[o + 1];
+            s2 += dr * dr + di * di;
+        }
+        worst = fmax(worst, fmk::warp_sum(s2));
+    }
+    if (lane == 0) {
+        const double gap = eig[static_cast<size_t>(f) * k + k - 1] - eig_next[f];
+        const double ratio = gap > 0.0 ? sqrt(worst) / gap : 1e300;
+        if (g_exact_ratio) g_exact_ratio[f] = ratio;
+        if (iter_status[f] != 0 || !(ratio <= tol)) status[f] |= fmk::kFrameRefine;
+    }
+}
+
 
 // fp64 covariance for the single-matrix facade path (R/src/scene.cpp:138-159 +
 // R/src/linalg.cpp:46-52): y column-major M x N; output S column-major, exactly Hermitian.
@@ -338,6 +381,12 @@ struct fm_plan_s {
     double* spec64 = nullptr; // frames x L (fp64 spectrum for peak picking)
     double* zgrid = nullptr;  // L complex128
     int32_t* scratch_status = nullptr;  // frames
+    // exact method via certified subspace iteration (pe > 0): plan-owned Omega, R U product, gap
+    int pe = 0;
+    float* omega_e = nullptr;   // frames x M x pe fp32
+    float* u32 = nullptr;       // frames x K x M complex64 (U for R U)
+    float* ru = nullptr;        // frames x K x M complex64
+    double* eig_next = nullptr; // frames
     // host-path staging
     float* x_dev = nullptr;
     float* omega_dev = nullptr;
@@ -395,6 +444,19 @@ struct fm_plan_s {
     }
 };
 
+// Exact method via certified subspace iteration: p_e = 2K rounded up to a multiple of 4 (>= K + 4),
+// t = kExactIters power steps, Omega from kExactSeed; needs the tensor-core / tiled paths (even M,
+// p_e <= 32, p_e <= M). Otherwise (or FM_EXACT_JACOBI=1) every frame runs the Jacobi solver.
+constexpr uint64_t kExactSeed = 0x4558414354ull;
+constexpr int kExactIters = 3;
+constexpr double kExactTol = 1e-3;  // max_k ||R u_k - lambda_k u_k|| <= tol * (lambda_K - lambda_{K+1})
+static int exact_fast_p(const fm_plan_desc& d) {
+    if (d.method != FM_METHOD_EXACT || std::getenv("FM_EXACT_JACOBI")) return 0;
+    const int pe = std::max<int>(static_cast<int>((2 * d.k + 3) / 4 * 4), static_cast<int>((d.k + 4 + 3) / 4 * 4));
+    if (pe > 32 || pe > d.m || (d.m % 2) || (d.k % 4)) return 0;
+    return pe;
+}
+
 static fm_status validate_desc(const fm_plan_desc* d) {
     if (!d) return fail(FM_EINVAL, "fm_plan_create: null descriptor");
     if (d->m < 2) return fail(FM_EINVAL, "plan: need M >= 2");
@@ -429,7 +491,8 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
     pl->d = *desc;
     pl->device = device;
     const size_t B = static_cast<size_t>(desc->max_frames), M = desc->m, K = desc->k, L = desc->grid_size;
-    const size_t P = desc->method == FM_METHOD_EXACT ? 0 : static_cast<size_t>(desc->p);
+    pl->pe = exact_fast_p(*desc);
+    const size_t P = desc->method == FM_METHOD_EXACT ? static_cast<size_t>(pl->pe) : static_cast<size_t>(desc->p);
     cudaError_t e = cudaSuccess;
     auto chk = [&](cudaError_t x) {
         if (e == cudaSuccess) e = x;
@@ -448,9 +511,27 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
     chk(pl->get(&pl->spec64, B * L));
     chk(pl->get(&pl->zgrid, L * 2));
     chk(pl->get(&pl->scratch_status, B));
+    if (pl->pe > 0) {
+        chk(pl->get(&pl->omega_e, B * M * pl->pe));
+        chk(pl->get(&pl->u32, B * K * M * 2));
+        chk(pl->get(&pl->ru, B * K * M * 2));
+        chk(pl->get(&pl->eig_next, B));
+    }
     if (e != cudaSuccess) {
         delete pl;
         return fm_fail_cuda(e, "fm_plan_create workspace", __FILE__, __LINE__);
+    }
+    if (pl->pe > 0) {  // fixed Gaussian start blocks, one per frame slot
+        std::vector<float> om(B * M * pl->pe);
+        for (size_t f = 0; f < B; ++f)
+            fmhost::gaussian_matrix_real(static_cast<int64_t>(M), pl->pe,
+                                         fmhost::Rng::derive(kExactSeed, static_cast<uint64_t>(f)),
+                                         om.data() + f * M * pl->pe);
+        e = cudaMemcpy(pl->omega_e, om.data(), sizeof(float) * om.size(), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            delete pl;
+            return fm_fail_cuda(e, "fm_plan_create exact omega", __FILE__, __LINE__);
+        }
     }
     const auto z = zgrid_host(desc->grid_size, desc->theta0, desc->theta1, desc->d, desc->lambda);
     e = cudaMemcpy(pl->zgrid, z.data(), sizeof(double) * z.size(), cudaMemcpyHostToDevice);
@@ -519,6 +600,7 @@ extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
     const int orth = tiled && split_final() ? 3 : 1;  // gram, pivoted chol, rows solve | fused
     if (plan->d.method == FM_METHOD_FAST2) n += 1 + t * (orth + 1) + fin;  // rmul, t x (orth, rmul), final
     else if (plan->d.method == FM_METHOD_FAST1) n += 1 + fin;      // gather, final
+    else if (plan->pe > 0) n += 1 + 1 + kExactIters * (3 + 1) + 3 + 1 + 1 + 1 + 1 + 1;  // see run_post_cov
     else n += 1;                                                    // jacobi
     return n;
 }
@@ -564,14 +646,22 @@ struct WorkView {
     double* t;
     double* spec64;
     int32_t* scratch;
+    float* omega_e;
+    float* u32;
+    float* ru;
+    double* eig_next;
 };
 
 static WorkView work_view(fm_plan pl, int64_t f0) {
     const auto& d = pl->d;
-    const size_t M = d.m, P = d.method == FM_METHOD_EXACT ? 0 : d.p, K = d.k;
+    const size_t M = d.m, P = d.method == FM_METHOD_EXACT ? pl->pe : d.p, K = d.k;
     const size_t MP = (M + 15) / 16 * 16;
     const size_t wsz = d.method == FM_METHOD_EXACT ? MP * MP * 2 : 2 * P * M * 2;
     WorkView w;
+    w.omega_e = pl->omega_e ? pl->omega_e + f0 * M * P : nullptr;
+    w.u32 = pl->u32 ? pl->u32 + f0 * K * M * 2 : nullptr;
+    w.ru = pl->ru ? pl->ru + f0 * K * M * 2 : nullptr;
+    w.eig_next = pl->eig_next ? pl->eig_next + f0 : nullptr;
     w.C = pl->C + f0 * P * M * 2;
     w.V = pl->V + f0 * P * M * 2;
     w.work = pl->work + f0 * wsz;
@@ -672,6 +762,30 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
             if ((st = orth(true, nullptr)) != FM_OK) return st;
             if ((st = nystrom()) != FM_OK) return st;
         }
+    } else if (pl->pe > 0) {
+        // exact_signal_subspace as certified subspace iteration: C = R Omega, kExactIters x {V = orth(C),
+        // C = R V}, Nystrom/Rayleigh step -> U, lambda, lambda_{K+1}; then R U and the residual test;
+        // frames not certified (or flagged by the iteration) rerun the Jacobi eigensolver below.
+        const int PE = pl->pe;
+        k_clear_bits<<<(F + 255) / 256, 256, 0, s>>>(w.scratch, F, ~0);
+        FM_CUDA_OK(cudaGetLastError());
+        FM_LAUNCH(fm_launch_rmul_tc(R, w.omega_e, nullptr, w.C, F, M, PE, s));
+        for (int it = 0; it < kExactIters; ++it) {
+            FM_LAUNCH(fm_launch_orth_split(w.C, w.V, w.Rt, reinterpret_cast<int32_t*>(w.H), w.scratch, F, M, PE, s));
+            FM_LAUNCH(fm_launch_rmul_tc(R, nullptr, w.V, w.C, F, M, PE, s));
+        }
+        FM_LAUNCH(fm_launch_final_split(w.C, w.V, w.H, w.Rt, w.work, basis, eig, w.scratch, F, M, PE, K, s,
+                                        w.eig_next));
+        const int64_t nb = static_cast<int64_t>(F) * K * M * 2;
+        k_basis_to_c32<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, s>>>(basis, w.u32, nb);
+        FM_CUDA_OK(cudaGetLastError());
+        FM_LAUNCH(fm_launch_rmul_tc(R, nullptr, w.u32, w.ru, F, M, K, s));
+        k_exact_certify<<<(F + 7) / 8, 256, 0, s>>>(w.ru, basis, eig, w.eig_next, w.scratch, io->status, F, M, K,
+                                                     kExactTol);
+        FM_CUDA_OK(cudaGetLastError());
+        FM_LAUNCH(fm_launch_jacobi_eig<float>(R, w.work, basis, eig, io->status, F, M, K, s, 1));
+        k_clear_bits<<<(F + 255) / 256, 256, 0, s>>>(io->status, F, fmk::kFrameRefine);
+        FM_CUDA_OK(cudaGetLastError());
     } else {
         FM_LAUNCH(fm_launch_jacobi_eig<float>(R, w.work, basis, eig, io->status, F, M, K, s));
     }
@@ -1121,4 +1235,9 @@ extern "C" fm_status fm_z_extract_peaks(const double* values, int64_t L, int64_t
     *count = n;
     *shortfall = n < k ? 1 : 0;
     return FM_OK;
+}
+
+// Debug (not in the public header): per-frame residual / gap of the exact method's certification.
+extern "C" int32_t fm_debug_set_exact_ratio_buffer(double* d) {
+    return cudaMemcpyToSymbol(g_exact_ratio, &d, sizeof(d)) == cudaSuccess ? 0 : 1;
 }

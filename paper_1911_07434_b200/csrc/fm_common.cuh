@@ -13,7 +13,8 @@ enum FrameStatus : int32_t {
     kFrameRank = 1,      // sketch lost column rank  -> RankDeficiencyError (host redraws)
     kFrameNoConv = 2,    // Jacobi sweep cap hit     -> NonConvergenceError
     kFrameRange = 4,     // input outside fp16 operand range of the tensor-core covariance
-    kFrameNonFinite = 8  // NaN/Inf in the input frame
+    kFrameNonFinite = 8, // NaN/Inf in the input frame
+    kFrameRefine = 16    // internal: exact method, subspace iteration not certified -> Jacobi
 };
 
 template <typename T> struct cplx { T re, im; };

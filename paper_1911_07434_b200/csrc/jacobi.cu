@@ -64,7 +64,7 @@ __device__ __forceinline__ bool pair_rotate(cplx<T>* ai, cplx<T>* aj, int mp, in
 template <typename T>
 __global__ void __launch_bounds__(kNT) k_jacobi_eig(const cplx<T>* __restrict__ R, cplx<T>* __restrict__ work,
                                                     c64* __restrict__ basis, double* __restrict__ eig,
-                                                    int32_t* __restrict__ status, int m, int k) {
+                                                    int32_t* __restrict__ status, int m, int k, int only_flagged) {
     extern __shared__ uint8_t dsm[];
     const int mp = (m + kB - 1) / kB * kB;
     const int nb = mp / kB;
@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(kNT) k_jacobi_eig(const cplx<T>* __restrict__ 
     __shared__ int s_rot;
     __shared__ double s_mu;
     const int f = blockIdx.x;
+    if (only_flagged && !(status[f] & kFrameRefine)) return;  // certified by the subspace iteration
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const cplx<T>* Rf = R + static_cast<size_t>(f) * m * m;
     cplx<T>* A = work + static_cast<size_t>(f) * mp * mp;
@@ -200,7 +201,7 @@ using namespace fmk;
 
 template <typename T>
 cudaError_t fm_launch_jacobi_eig(const void* R, void* work, void* basis, double* eig, int32_t* status, int frames,
-                                 int m, int k, cudaStream_t s) {
+                                 int m, int k, cudaStream_t s, int only_flagged) {
     const int mp = (m + jac::kB - 1) / jac::kB * jac::kB;
     const size_t smem = 2 * jac::kB * static_cast<size_t>(mp) * sizeof(cplx<T>);
     if (mp > 1024 || k > 64 || smem > 200 * 1024) return cudaErrorInvalidValue;
@@ -208,11 +209,11 @@ cudaError_t fm_launch_jacobi_eig(const void* R, void* work, void* basis, double*
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     jac::k_jacobi_eig<T><<<frames, jac::kNT, smem, s>>>(static_cast<const cplx<T>*>(R), static_cast<cplx<T>*>(work),
-                                                        static_cast<c64*>(basis), eig, status, m, k);
+                                                        static_cast<c64*>(basis), eig, status, m, k, only_flagged);
     return cudaGetLastError();
 }
 
 template cudaError_t fm_launch_jacobi_eig<float>(const void*, void*, void*, double*, int32_t*, int, int, int,
-                                                 cudaStream_t);
+                                                 cudaStream_t, int);
 template cudaError_t fm_launch_jacobi_eig<double>(const void*, void*, void*, double*, int32_t*, int, int, int,
-                                                  cudaStream_t);
+                                                  cudaStream_t, int);

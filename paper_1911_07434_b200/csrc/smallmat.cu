@@ -994,7 +994,7 @@ template <int PC>
 __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
     k_small_warp(const c64* __restrict__ Gin, const c64* __restrict__ Hin, c64* __restrict__ Tout,
                  double* __restrict__ eig, int32_t* __restrict__ status, int frames, int p, int k,
-                 int32_t* __restrict__ dbg) {
+                 int32_t* __restrict__ dbg, double* __restrict__ eig_next) {
     using W = WarpCfg<PC>;
     constexpr int LPC = W::kLPC;
     extern __shared__ uint8_t dsm[];
@@ -1165,6 +1165,10 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
         double lam = sig[cc];
         lam *= lam;  // eigenvalue of B' = Y Y^H
         eig[static_cast<size_t>(f) * k + kk] = lam;
+    }
+    if (eig_next && lane == 0) {  // (K+1)-th Ritz value (exact method's gap estimate)
+        const double sn = k < p ? sig[order[k]] : 0.0;
+        eig_next[f] = sn * sn;
     }
     __syncwarp();
     c64* Tf = Tout + static_cast<size_t>(f) * p * k;
@@ -1439,7 +1443,8 @@ cudaError_t fm_launch_orth_split(const void* C, void* Vout, void* Lw, int32_t* p
 
 // Split final stage: G -> Gw, Herm(H) -> Hw (in place for fast1), T -> Tw (p x k per frame).
 cudaError_t fm_launch_final_split(const void* C, const void* V, void* Hw, void* Gw, void* Tw, void* basis, double* eig,
-                                  int32_t* status, int frames, int m, int p, int k, cudaStream_t s) {
+                                  int32_t* status, int frames, int m, int p, int k, cudaStream_t s,
+                                  double* eig_next) {
     if (p > 32 || (p & 3) || k > p || m < p || frames < 1) return cudaErrorInvalidValue;
     auto go = [&](auto gram, auto small, auto bas, int pc, int warps, size_t warp_bytes) {
         const size_t gsm = sizeof(c64) * 2 * pc * pc + sizeof(c64) * 3 * 64 * (pc + 1);
@@ -1453,7 +1458,7 @@ cudaError_t fm_launch_final_split(const void* C, const void* V, void* Hw, void* 
         if (e != cudaSuccess) return e;
         small<<<(frames + warps - 1) / warps, 32 * warps, wsm, s>>>(static_cast<const c64*>(Gw),
                                                                     static_cast<const c64*>(Hw), static_cast<c64*>(Tw),
-                                                                    eig, status, frames, p, k, g_sweep_dbg);
+                                                                    eig, status, frames, p, k, g_sweep_dbg, eig_next);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         bas<<<dim3((m + 127) / 128, frames), 128, 0, s>>>(static_cast<const c32*>(C), static_cast<const c64*>(Tw),
                                                           static_cast<c64*>(basis), m, p, k);

@@ -113,3 +113,49 @@ def test_subspace_close_to_oracle(fm, oracle, cfgs):
         assert np.max(np.abs(u.conj().T @ u - np.eye(cfg.spec.k))) < 1e-12
         assert oracle.projector_error(u, est.basis) < 1e-4
         assert np.allclose(res["eigenvalues"][i], est.eigenvalues, rtol=1e-4)
+
+
+def _exact_run(fm, x, m, n, k, env_jacobi):
+    import os
+    import torch
+    old = os.environ.pop("FM_EXACT_JACOBI", None)
+    if env_jacobi:
+        os.environ["FM_EXACT_JACOBI"] = "1"
+    try:
+        plan = fm.BatchPlan(m, n, k, "exact", grid_size=721, max_frames=len(x))
+    finally:
+        os.environ.pop("FM_EXACT_JACOBI", None)
+        if old is not None:
+            os.environ["FM_EXACT_JACOBI"] = old
+    xd = torch.from_numpy(np.ascontiguousarray(x).view(np.float32)).cuda()
+    out = plan.outputs(len(x), spectrum=True, basis=True)
+    plan.run(len(x), xd, None, None, out)
+    torch.cuda.synchronize()
+    res = {kk: v.cpu().numpy() for kk, v in out.items()}
+    plan.close()
+    return res
+
+
+def test_exact_uncertified_frames_fall_back_to_jacobi(fm, oracle):
+    """K = 8 requested but only 5 sources: lambda_K ~ lambda_{K+1} (noise), so the subspace iteration
+    cannot be certified and every frame must come from the Jacobi eigensolver, bitwise."""
+    m, n, k = 64, 128, 8
+    x, _, _ = fm.generate_frames(m, n, 5, 21, 0, 4, snr_lo_db=20.0, snr_hi_db=20.0)
+    a = _exact_run(fm, x, m, n, k, env_jacobi=False)
+    b = _exact_run(fm, x, m, n, k, env_jacobi=True)
+    assert np.array_equal(a["basis"], b["basis"])
+    assert np.array_equal(a["eigenvalues"], b["eigenvalues"])
+    assert np.array_equal(a["spectrum"], b["spectrum"])
+
+
+def test_exact_certified_frames_match_jacobi(fm, oracle):
+    """Well-separated signal subspace: certified subspace-iteration frames agree with the Jacobi
+    solver's peaks and spectra (0.05 dB gate) and eigenvalues (1e-5 relative)."""
+    m, n, k = 128, 256, 8
+    x, _, _ = fm.generate_frames(m, n, k, 22, 0, 6, snr_lo_db=15.0, snr_hi_db=25.0)
+    a = _exact_run(fm, x, m, n, k, env_jacobi=False)
+    b = _exact_run(fm, x, m, n, k, env_jacobi=True)
+    assert np.array_equal(a["peak_cells"], b["peak_cells"])
+    assert np.max(np.abs(a["eigenvalues"] - b["eigenvalues"]) / b["eigenvalues"][:, :1]) < 1e-5
+    for f in range(len(x)):
+        assert oracle.spectrum_db_error(a["spectrum"][f].astype(np.float64), b["spectrum"][f].astype(np.float64)) < DB_TOL
