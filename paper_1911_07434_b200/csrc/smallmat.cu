@@ -970,21 +970,24 @@ __device__ __forceinline__ void warp_chol_lower(c64* A, int p, double& dmin, dou
         dmax = fmax(dmax, dk);
         const double inv = dk > 0.0 ? 1.0 / sqrt(dk) : 0.0;
         __syncwarp();
-        for (int i = k + 1 + lane; i < p; i += 32) {
-            const c64 a = A[k * p + i];
-            A[k * p + i] = mk(a.re * inv, a.im * inv);
+        // lane = row i > k: l_i = A(i, k) / sqrt(d_k), then A(i, j) -= l_i conj(l_j), k < j <= i
+        // (column-major: lanes touch consecutive rows of one column -> conflict-free)
+        c64 li = mk(0.0, 0.0);
+        if (lane > k && lane < p) {
+            const c64 a = A[k * p + lane];
+            li = mk(a.re * inv, a.im * inv);
+            A[k * p + lane] = li;
         }
         if (lane == 0) A[k * p + k] = mk(dk > 0.0 ? sqrt(dk) : 0.0, 0.0);
         __syncwarp();
-        const int nt = p - k - 1;
-        for (int e = lane; e < nt * nt; e += 32) {
-            const int i = k + 1 + e % nt, j = k + 1 + e / nt;
-            if (i < j) continue;
-            const c64 li = A[k * p + i], lj = A[k * p + j];
-            c64 a = A[j * p + i];
-            a.re -= li.re * lj.re + li.im * lj.im;  // li * conj(lj)
-            a.im -= li.im * lj.re - li.re * lj.im;
-            A[j * p + i] = a;
+        if (lane > k && lane < p) {
+            for (int j = k + 1; j <= lane; ++j) {
+                const c64 lj = A[k * p + j];
+                c64 a = A[j * p + lane];
+                a.re -= li.re * lj.re + li.im * lj.im;  // li * conj(lj)
+                a.im -= li.im * lj.re - li.re * lj.im;
+                A[j * p + lane] = a;
+            }
         }
         __syncwarp();
     }
@@ -1023,20 +1026,36 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
         atomicOr(&status[f], kFrameNoConv);
     for (int e = lane; e < PC * ld; e += 32) Ya[e] = Yb[e] = mk(0.0, 0.0);  // rows >= p stay zero
     __syncwarp();
-    // Y(i, :) solves y L_H^H = R(i, :) (forward substitution, lane per row); Y -> Ya (ld)
+    // Y(i, :) solves y L_H^H = R(i, :) (forward substitution, lane per row); Y -> Ya (ld).
+    // Reciprocal pivots first; two partial sums per step for a shorter FMA chain.
+    double* rinv = sig;  // PC doubles, free until the singular values are formed
+    if (lane < p) {
+        const double ljj = LH[lane * p + lane].re;
+        rinv[lane] = ljj > 0.0 ? 1.0 / ljj : 0.0;
+    }
+    __syncwarp();
     if (lane < p) {
         const int i = lane;
         for (int j = 0; j < p; ++j) {
-            c64 x = j >= i ? conj(L[i * p + j]) : mk(0.0, 0.0);
-            for (int a = i; a < j; ++a) {  // y_a = 0 for a < i
-                const c64 l = LH[a * p + j];
-                const c64 v = Ya[a * ld + i];
-                x.re -= v.re * l.re + v.im * l.im;
-                x.im -= v.im * l.re - v.re * l.im;
+            c64 x0 = j >= i ? conj(L[i * p + j]) : mk(0.0, 0.0);
+            c64 x1 = mk(0.0, 0.0);
+            int a = i;
+            for (; a + 1 < j; a += 2) {  // y_a = 0 for a < i
+                const c64 l0 = LH[a * p + j], l1 = LH[(a + 1) * p + j];
+                const c64 v0 = Ya[a * ld + i], v1 = Ya[(a + 1) * ld + i];
+                x0.re -= v0.re * l0.re + v0.im * l0.im;
+                x0.im -= v0.im * l0.re - v0.re * l0.im;
+                x1.re -= v1.re * l1.re + v1.im * l1.im;
+                x1.im -= v1.im * l1.re - v1.re * l1.im;
             }
-            const double ljj = LH[j * p + j].re;
-            const double inv = ljj > 0.0 ? 1.0 / ljj : 0.0;
-            Ya[j * ld + i] = j >= i ? mk(x.re * inv, x.im * inv) : mk(0.0, 0.0);
+            if (a < j) {
+                const c64 l0 = LH[a * p + j];
+                const c64 v0 = Ya[a * ld + i];
+                x0.re -= v0.re * l0.re + v0.im * l0.im;
+                x0.im -= v0.im * l0.re - v0.re * l0.im;
+            }
+            const double inv = rinv[j];
+            Ya[j * ld + i] = j >= i ? mk((x0.re + x1.re) * inv, (x0.im + x1.im) * inv) : mk(0.0, 0.0);
         }
     }
     __syncwarp();
