@@ -60,7 +60,7 @@ cudaError_t fm_launch_spectrum_peaks(const void* t, const void* zgrid, int frame
                                      double* baseline, int32_t* count, int32_t* status, cudaStream_t s);
 cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K, int min_sep, int32_t* cells,
                                  double* heights, double* baseline, int32_t* count, int32_t* overflow,
-                                 cudaStream_t s);
+                                 cudaStream_t s, int cap_hint = 0);
 cudaError_t fm_launch_orthocheck(const void* basis, int frames, int m, int k, double* dev, cudaStream_t s);
 cudaError_t fm_launch_spectrum_multi(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
                                      double* spec64, cudaStream_t s, bool symmetric);
@@ -799,7 +799,8 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     FM_LAUNCH(fm_launch_spectrum_multi(w.t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, w.spec64,
                                        s, sym));
     FM_LAUNCH(fm_launch_peaks_only(w.spec64, F, static_cast<int>(d.grid_size), K, static_cast<int>(d.min_sep_cells),
-                                   io->peak_cells, io->peak_heights, io->baseline, io->peak_count, w.scratch, s));
+                                   io->peak_cells, io->peak_heights, io->baseline, io->peak_count, w.scratch, s,
+                                   2 * M + 64));
     if (prof) mark(pl, 4, s);
     return FM_OK;
 }

@@ -577,15 +577,341 @@ __global__ void __launch_bounds__(kNT) k_spectrum_sym(const c64* __restrict__ t,
     }
 }
 
+// Peaks, one WARP per frame (R/src/spectrum.cpp:97-188, same rules as block_peaks):
+//  1. strict interior maxima with leftmost-plateau rule, found 32 cells at a time (coalesced
+//     loads) and compacted in cell order with ballot/popc; capacity ceil((L-2)/2) is exact
+//     (strict maxima are never adjacent), so there is no overflow;
+//  2. greedy (height desc, cell asc) with |dc| >= min_sep: K warp-argmax rounds, candidates within
+//     min_sep of a pick invalidated (cells are sorted, so they are index neighbours);
+//  3. baseline = max over cells with |l - s| > min_sep for every pick (shared bitmask), init 0;
+//  4. picks in ascending cell order, padded with -1 / 0.
+__device__ __forceinline__ bool better_w(double h1, int c1, double h2, int c2) {
+    return h1 > h2 || (h1 == h2 && c1 < c2);
+}
+
+__global__ void k_peaks_warp(const double* __restrict__ values, int frames, int L, int K, int min_sep, int cap,
+                             PeakOut out) {
+    extern __shared__ uint8_t wsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    const int f = blockIdx.x * nwarps + warp;
+    if (f >= frames) return;
+    const int nmask = (L + 31) / 32;
+    const size_t per = static_cast<size_t>(cap) * 12 + static_cast<size_t>(nmask) * 4 + 64 * 12;
+    uint8_t* base = wsm + static_cast<size_t>(warp) * ((per + 15) / 16 * 16);
+    double* ch = reinterpret_cast<double*>(base);             // cap heights
+    int* cc = reinterpret_cast<int*>(ch + cap);                // cap cells
+    uint32_t* near = reinterpret_cast<uint32_t*>(cc + cap);    // L bits
+    int* sel_c = reinterpret_cast<int*>(near + nmask);         // 64
+    double* sel_h = reinterpret_cast<double*>(((reinterpret_cast<uintptr_t>(sel_c + 64) + 7) & ~uintptr_t(7)));
+    const double* v = values + static_cast<size_t>(f) * L;
+    // 1. candidates in cell order: 4 x 32 cells per batch (coalesced loads in flight), neighbours
+    //    by shuffles; the equal-neighbour (plateau) case scans forward from memory
+    int nc = 0;
+    double prev = v[0];  // value left of the current 32-cell group
+    for (int b0 = 1; b0 < L - 1; b0 += 128) {
+        double xs[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int l = b0 + 32 * u + lane;
+            xs[u] = l < L ? v[l] : 0.0;
+        }
+        const int lr = b0 + 128;
+        const double after = lr < L ? v[lr] : 0.0;  // right neighbour of the last group
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int l = b0 + 32 * u + lane;
+            const double x = xs[u];
+            const double up = __shfl_up_sync(0xffffffffu, x, 1);
+            const double dn = __shfl_down_sync(0xffffffffu, x, 1);
+            const double nxt0 = u < 3 ? __shfl_sync(0xffffffffu, xs[u < 3 ? u + 1 : u], 0) : after;
+            const double xm = lane == 0 ? prev : up;
+            const double xp = lane == 31 ? nxt0 : dn;
+            bool is = false;
+            if (l < L - 1 && x > xm) {
+                if (xp < x) {
+                    is = true;
+                } else if (xp == x) {  // plateau: leftmost cell if the run ends with a drop
+                    int r = l + 1;
+                    while (r + 1 < L && v[r + 1] == x) ++r;
+                    is = (r + 1 < L) && v[r + 1] < x;
+                }
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, is);
+            if (is) {
+                const int pos = nc + __popc(bal & ((1u << lane) - 1u));
+                if (pos < cap) {
+                    ch[pos] = x;
+                    cc[pos] = l;
+                }
+            }
+            nc += __popc(bal);
+            prev = __shfl_sync(0xffffffffu, x, 31);
+        }
+    }
+    if (nc > cap) {  // more maxima than the degree bound allows for (fp noise): CTA kernel reruns it
+        if (lane == 0) out.count[f] = -1;
+        return;
+    }
+    for (int w = lane; w < nmask; w += 32) near[w] = 0u;
+    __syncwarp();
+    // 2. greedy selection
+    int nsel = 0;
+    for (int it = 0; it < K; ++it) {
+        double bh = -1.0;
+        int bc = 0x7fffffff, bi = -1;
+        for (int i = lane; i < nc; i += 32) {
+            const double h = ch[i];
+            if (h >= 0.0 && (bi < 0 || better_w(h, cc[i], bh, bc))) {
+                bh = h;
+                bc = cc[i];
+                bi = i;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double oh = __shfl_xor_sync(0xffffffffu, bh, o);
+            const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (oi >= 0 && (bi < 0 || better_w(oh, oc, bh, bc))) {
+                bh = oh;
+                bc = oc;
+                bi = oi;
+            }
+        }
+        if (bi < 0) break;  // exhausted: shortfall
+        if (lane == 0) {
+            sel_c[nsel] = bc;
+            sel_h[nsel] = bh;
+        }
+        // invalidate the pick and its clashing neighbours (|dc| < min_sep; sorted cells)
+        const int lo = max(0, bi - min_sep), hi = min(nc - 1, bi + min_sep);
+        for (int i = lo + lane; i <= hi; i += 32)
+            if (i == bi || abs(cc[i] - bc) < min_sep) ch[i] = -1.0;
+        // exclusion band for the baseline: |l - pick| <= min_sep
+        for (int d = lane - min_sep; d <= min_sep; d += 32) {
+            const int l = bc + d;
+            if (l >= 0 && l < L) atomicOr(&near[l >> 5], 1u << (l & 31));
+        }
+        ++nsel;
+        __syncwarp();
+    }
+    __syncwarp();
+    // 3. baseline
+    double p0 = 0.0;
+#pragma unroll 8
+    for (int l = lane; l < L; l += 32)
+        if (!((near[l >> 5] >> (l & 31)) & 1u)) p0 = fmax(p0, v[l]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) p0 = fmax(p0, __shfl_xor_sync(0xffffffffu, p0, o));
+    // 4. ascending cell order: rank of each pick (cells are distinct)
+    __syncwarp();
+    for (int x = lane; x < K; x += 32) {
+        if (x < nsel) {
+            const int c = sel_c[x];
+            int rank = 0;
+            for (int y = 0; y < nsel; ++y) rank += sel_c[y] < c ? 1 : 0;
+            out.cells[static_cast<size_t>(f) * K + rank] = c;
+            out.heights[static_cast<size_t>(f) * K + rank] = sel_h[x];
+        } else {
+            out.cells[static_cast<size_t>(f) * K + x] = -1;
+            out.heights[static_cast<size_t>(f) * K + x] = 0.0;
+        }
+    }
+    if (lane == 0) {
+        out.baseline[f] = p0;
+        out.count[f] = nsel;
+    }
+}
+
+// Peaks, one CTA per frame, same rules as block_peaks / k_peaks_warp (R/src/spectrum.cpp:97-188):
+// the frame's values are loaded once (coalesced, all threads) into shared memory; candidates are
+// detected from shared memory 32 cells per warp step and compacted in cell order (per-warp
+// ballot counts -> block prefix -> second pass); warp 0 alone runs the greedy selection (warp
+// argmax, neighbour invalidation, no block barriers); all warps compute the baseline.
+__device__ long long* g_peak_dbg = nullptr;  // debug: per-frame phase cycles
+
+// Peaks, one CTA per frame, same rules as block_peaks (R/src/spectrum.cpp:97-188):
+//  1. values -> shared memory (coalesced); strict interior maxima (leftmost-plateau rule) found
+//     32 cells per warp step, compacted in cell order (per-warp ballot counts -> prefix -> pass 2);
+//  2. candidates sorted once by (height desc, cell asc) with a CTA bitonic sort; lane 0 walks the
+//     sorted list accepting picks with |dc| >= min_sep from every accepted pick (= the greedy);
+//  3. baseline = max over cells with |l - pick| > min_sep for every pick (bitmask), init 0;
+//  4. picks in ascending cell order, padded with -1 / 0.
+__global__ void __launch_bounds__(kNT) k_peaks_cta(const double* __restrict__ values, int L, int K, int min_sep,
+                                                   PeakOut out) {
+    const long long T0 = clock64();
+    extern __shared__ uint8_t psm[];
+    const int cap = max(1, (L - 1) / 2);
+    int n2 = 1;
+    while (n2 < cap) n2 <<= 1;
+    const int nmask = (L + 31) / 32;
+    double* sv = reinterpret_cast<double*>(psm);               // L
+    double* ch = sv + L;                                       // n2 (sort keys: height)
+    int* cc = reinterpret_cast<int*>(ch + n2);                 // n2 (cell)
+    uint32_t* near = reinterpret_cast<uint32_t*>(cc + n2);     // nmask
+    __shared__ int s_cnt[kNW];
+    __shared__ int s_sel[64];
+    __shared__ double s_selh[64];
+    __shared__ int s_nsel;
+    __shared__ double s_wmax[kNW];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int f = blockIdx.x;
+    const double* v = values + static_cast<size_t>(f) * L;
+    for (int l = threadIdx.x; l < L; l += kNT) sv[l] = v[l];
+    for (int w = threadIdx.x; w < nmask; w += kNT) near[w] = 0u;
+    __syncthreads();
+    const long long T1 = clock64();
+    auto is_max = [&](int l) -> bool {
+        if (l < 1 || l >= L - 1) return false;
+        const double x = sv[l], xm = sv[l - 1], xp = sv[l + 1];
+        if (!(x > xm)) return false;
+        if (xp < x) return true;
+        if (!(xp == x)) return false;
+        int r = l + 1;  // plateau
+        while (r + 1 < L && sv[r + 1] == x) ++r;
+        return (r + 1 < L) && sv[r + 1] < x;
+    };
+    const int ngroups = (L - 2 + 31) / 32;
+    const int gpw = (ngroups + kNW - 1) / kNW;  // warp w owns groups [w gpw, (w + 1) gpw): cell order
+    const int g0 = warp * gpw, g1 = min(ngroups, g0 + gpw);
+    uint32_t bals[8];
+    int cnt = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int g = g0 + u;
+        bals[u] = __ballot_sync(0xffffffffu, g < g1 && is_max(1 + 32 * g + lane));
+        cnt += __popc(bals[u]);
+    }
+    for (int g = g0 + 8; g < g1; ++g) cnt += __popc(__ballot_sync(0xffffffffu, is_max(1 + 32 * g + lane)));
+    if (lane == 0) s_cnt[warp] = cnt;
+    __syncthreads();
+    int off = 0, nc = 0;
+    for (int w = 0; w < kNW; ++w) {
+        if (w < warp) off += s_cnt[w];
+        nc += s_cnt[w];
+    }
+    for (int g = g0; g < g1; ++g) {
+        const int u = g - g0;
+        const uint32_t bal = u < 8 ? bals[u < 8 ? u : 0] : __ballot_sync(0xffffffffu, is_max(1 + 32 * g + lane));
+        if ((bal >> lane) & 1u) {
+            const int pos = off + __popc(bal & ((1u << lane) - 1u));
+            const int l = 1 + 32 * g + lane;
+            ch[pos] = sv[l];
+            cc[pos] = l;
+        }
+        off += __popc(bal);
+    }
+    // pad to a power of two with sentinels (sorted last)
+    int ns = 1;
+    while (ns < nc) ns <<= 1;
+    for (int i = nc + threadIdx.x; i < ns; i += kNT) {
+        ch[i] = -1.0;
+        cc[i] = 0x7fffffff;
+    }
+    __syncthreads();
+    const long long T2 = clock64();
+    // bitonic sort by (height desc, cell asc)
+    for (int k2 = 2; k2 <= ns; k2 <<= 1) {
+        for (int j = k2 >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < ns; i += kNT) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const double hi_ = ch[i], hj = ch[ixj];
+                    const int ci = cc[i], cj = cc[ixj];
+                    const bool j_first = better_w(hj, cj, hi_, ci);  // element ixj belongs before i
+                    const bool asc = (i & k2) == 0;
+                    if (asc ? j_first : !j_first) {
+                        ch[i] = hj;
+                        ch[ixj] = hi_;
+                        cc[i] = cj;
+                        cc[ixj] = ci;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // greedy walk over the sorted list (lane 0), exclusion bands by warp 0
+    if (warp == 0) {
+        int nsel = 0;
+        if (lane == 0) {
+            for (int i = 0; i < nc && nsel < K; ++i) {
+                const int c = cc[i];
+                bool clash = false;
+                for (int q = 0; q < nsel; ++q)
+                    if (abs(c - s_sel[q]) < min_sep || c == s_sel[q]) {
+                        clash = true;
+                        break;
+                    }
+                if (!clash) {
+                    s_sel[nsel] = c;
+                    s_selh[nsel] = ch[i];
+                    ++nsel;
+                }
+            }
+            s_nsel = nsel;
+        }
+        __syncwarp();
+        nsel = s_nsel;
+        for (int q = 0; q < nsel; ++q) {
+            const int bc = s_sel[q];
+            for (int d = lane - min_sep; d <= min_sep; d += 32) {
+                const int l = bc + d;
+                if (l >= 0 && l < L) atomicOr(&near[l >> 5], 1u << (l & 31));
+            }
+        }
+    }
+    __syncthreads();
+    const long long T3 = clock64();
+    if (threadIdx.x == 0 && g_peak_dbg) {
+        g_peak_dbg[f * 4 + 0] = T1 - T0;
+        g_peak_dbg[f * 4 + 1] = T2 - T1;
+        g_peak_dbg[f * 4 + 2] = T3 - T2;
+        g_peak_dbg[f * 4 + 3] = nc;
+    }
+    // baseline
+    double p0 = 0.0;
+    for (int l = threadIdx.x; l < L; l += kNT)
+        if (!((near[l >> 5] >> (l & 31)) & 1u)) p0 = fmax(p0, sv[l]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) p0 = fmax(p0, __shfl_xor_sync(0xffffffffu, p0, o));
+    if (lane == 0) s_wmax[warp] = p0;
+    __syncthreads();
+    if (warp == 0) {
+        const int nsel = s_nsel;
+        for (int x = lane; x < K; x += 32) {
+            if (x < nsel) {
+                const int c = s_sel[x];
+                int rank = 0;
+                for (int y = 0; y < nsel; ++y) rank += s_sel[y] < c ? 1 : 0;
+                out.cells[static_cast<size_t>(f) * K + rank] = c;
+                out.heights[static_cast<size_t>(f) * K + rank] = s_selh[x];
+            } else {
+                out.cells[static_cast<size_t>(f) * K + x] = -1;
+                out.heights[static_cast<size_t>(f) * K + x] = 0.0;
+            }
+        }
+        if (lane == 0) {
+            double b = 0.0;
+            for (int w = 0; w < kNW; ++w) b = fmax(b, s_wmax[w]);
+            out.baseline[f] = b;
+            out.count[f] = nsel;
+        }
+    }
+}
+
 // Peaks only, on caller-provided fp64 values (facade extract_peaks).
 __global__ void __launch_bounds__(kNT) k_peaks_only(const double* __restrict__ values, int L, int K, int min_sep,
-                                                    PeakOut out, int32_t* __restrict__ overflow_flag) {
+                                                    PeakOut out, int32_t* __restrict__ overflow_flag,
+                                                    int only_flagged) {
     extern __shared__ uint8_t dsm[];
     double* sv = reinterpret_cast<double*>(dsm);
     const int cap = cand_cap_values(L);
     int* ccell = reinterpret_cast<int*>(sv + L);
     double* ch = reinterpret_cast<double*>(ccell + ((cap + 1) & ~1));
     const int f = blockIdx.x;
+    if (only_flagged && out.count[f] != -1) return;
     for (int l = threadIdx.x; l < L; l += kNT) sv[l] = values[static_cast<size_t>(f) * L + l];
     __syncthreads();
     bool overflow = false;
@@ -706,21 +1032,65 @@ cudaError_t fm_launch_spectrum_multi(const void* t, const void* zgrid, int frame
     return go(spec::k_spectrum_multi<4>, 4);
 }
 
+// cap_hint > 0: candidate capacity per frame for the warp kernel (pipeline: 2M + 64, the degree
+// bound of a MUSIC spectrum plus slack); frames exceeding it are redone by the CTA kernel.
 cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K, int min_sep, int32_t* cells,
                                  double* heights, double* baseline, int32_t* count, int32_t* overflow,
-                                 cudaStream_t s) {
-    const int cap = spec::cand_cap_values(L);
-    const size_t smem = sizeof(double) * L + sizeof(int) * ((cap + 1) & ~1) + sizeof(double) * cap + 16;
-    if (cap < std::min(L / 2 + 1, 16) || smem > 227 * 1024 || K > 64) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(spec::k_peaks_only, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
+                                 cudaStream_t s, int cap_hint) {
+    if (K > 64 || L < 2) return cudaErrorInvalidValue;
+    static const bool block_kernel = std::getenv("FM_BLOCK_PEAKS") != nullptr;  // comparison switch
     spec::PeakOut out{cells, heights, baseline, count};
-    spec::k_peaks_only<<<frames, spec::kNT, smem, s>>>(values, L, K, min_sep, out, overflow);
-    return cudaGetLastError();
+    const int cap_b = spec::cand_cap_values(L);
+    const size_t smem_b = sizeof(double) * L + sizeof(int) * ((cap_b + 1) & ~1) + sizeof(double) * cap_b + 16;
+    auto block = [&](int only_flagged) {
+        if (cap_b < std::min(L / 2 + 1, 16) || smem_b > 227 * 1024) return cudaErrorInvalidValue;
+        cudaError_t e = cudaFuncSetAttribute(spec::k_peaks_only, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem_b));
+        if (e != cudaSuccess) return e;
+        spec::k_peaks_only<<<frames, spec::kNT, smem_b, s>>>(values, L, K, min_sep, out, overflow, only_flagged);
+        return cudaGetLastError();
+    };
+    static const bool warp_env = std::getenv("FM_WARP_PEAKS") != nullptr;
+    bool warp_kernel = warp_env;
+    if (const char* ov = std::getenv("FM_PEAKS_CAP")) {  // test hook: warp kernel + capacity fallback path
+        cap_hint = std::atoi(ov);
+        warp_kernel = true;
+    }
+    if (!block_kernel && !warp_kernel) {  // CTA per frame, exact candidate capacity
+        const int capc = std::max(1, (L - 1) / 2);
+        int n2 = 1;
+        while (n2 < capc) n2 <<= 1;
+        const size_t smem = sizeof(double) * L + static_cast<size_t>(n2) * 12 + sizeof(uint32_t) * ((L + 31) / 32) + 16;
+        if (smem <= 200 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(spec::k_peaks_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            spec::k_peaks_cta<<<frames, spec::kNT, smem, s>>>(values, L, K, min_sep, out);
+            return cudaGetLastError();
+        }
+    }
+    if (!block_kernel) {  // warp per frame
+        const int exact = std::max(1, (L - 1) / 2);
+        const int cap = cap_hint > 0 ? std::min(exact, cap_hint) : exact;
+        const size_t per = (static_cast<size_t>(cap) * 12 + static_cast<size_t>((L + 31) / 32) * 4 + 64 * 12 + 15) / 16 * 16;
+        const int nw = static_cast<int>(std::max<size_t>(1, std::min<size_t>(16, (100 * 1024) / per)));
+        if (per <= 200 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(spec::k_peaks_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(per * nw));
+            if (e != cudaSuccess) return e;
+            spec::k_peaks_warp<<<(frames + nw - 1) / nw, 32 * nw, per * nw, s>>>(values, frames, L, K, min_sep, cap, out);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            return cap < exact ? block(1) : cudaSuccess;
+        }
+    }
+    return block(0);
 }
 
 cudaError_t fm_launch_orthocheck(const void* basis, int frames, int m, int k, double* dev, cudaStream_t s) {
     spec::k_orthocheck<<<frames, spec::kNT, 0, s>>>(static_cast<const c64*>(basis), m, k, dev);
     return cudaGetLastError();
+}
+
+extern "C" int32_t fm_debug_set_peak_buffer(long long* d) {
+    return cudaMemcpyToSymbol(fmk::spec::g_peak_dbg, &d, sizeof(d)) == cudaSuccess ? 0 : 1;
 }

@@ -204,3 +204,19 @@ def test_peaks_match_oracle_random(fm, oracle):
         ref = oracle.extract_peaks(v, k, sep)
         assert got.cells == ref.cells and got.heights == ref.heights
         assert got.baseline == ref.baseline and got.shortfall == ref.shortfall
+
+
+@pytest.mark.parametrize("cap", ["4", "1"])
+def test_peaks_candidate_overflow_falls_back(fm, oracle, monkeypatch, cap):
+    """Warp peak kernel with a tiny candidate capacity (the pipeline uses 2M + 64): frames with more
+    maxima than the capacity are redone by the CTA kernel, results unchanged."""
+    monkeypatch.setenv("FM_PEAKS_CAP", cap)
+    rng = np.random.default_rng(11)
+    for _ in range(20):
+        n = int(rng.integers(20, 400))
+        v = rng.random(n)
+        k, sep = int(rng.integers(1, 9)), int(rng.integers(0, 5))
+        got = fm.extract_peaks(fm.PseudoSpectrum(fm.AngleGrid(n), v), k, sep)
+        ref = oracle.extract_peaks(v, k, sep)
+        assert got.cells == ref.cells and got.heights == ref.heights
+        assert got.baseline == ref.baseline and got.shortfall == ref.shortfall
