@@ -86,3 +86,13 @@ def test_facade_argument_validation_without_gpu(fm):
         fm.hermitian(np.ones((2, 3)))
     with pytest.raises(ValueError):
         fm.AngleGrid(1)
+
+
+def test_library_has_no_unresolved_internal_symbols():
+    """A launcher whose declaration drifted from its definition links into the .so as an undefined
+    C++ symbol and only fails at load time on the GPU box; catch it here."""
+    import subprocess
+    from paper_1911_07434_b200 import _capi
+    out = subprocess.run(["nm", "-D", "--undefined-only", _capi.LIB_PATH], capture_output=True, text=True).stdout
+    bad = [ln for ln in out.splitlines() if "fm_" in ln or "fmk" in ln]
+    assert not bad, bad
