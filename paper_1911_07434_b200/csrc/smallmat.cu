@@ -444,22 +444,36 @@ __device__ int warp_jacobi_herm(c64* A, c64* Z, int n, double* prm) {
 constexpr int kRG = 8;      // row groups (consecutive lanes)
 constexpr int kRCH = 64;    // rows per staged chunk
 
-template <typename T1, typename T2>
+template <int PC, typename T1, typename T2>
 __device__ void tiled_gram2(const T1* __restrict__ X1, bool herm1, const T1* __restrict__ Y1, const T2* __restrict__ X2,
                             const T2* __restrict__ Y2, int m, int p, c64* stage, c64* G1, c64* G2) {
+    // Callers: herm1 always true (G = X1^H X1); X2 optional with Y2 == X1 (H = X2^H X1).
+    (void)Y1;
+    (void)Y2;
     const int nb = p >> 2;
-    const int t1 = herm1 ? nb * (nb + 1) / 2 : nb * nb;
+    const int t1 = nb * (nb + 1) / 2;
     const int t2 = X2 ? nb * nb : 0;
     const int ntiles = t1 + t2;
     const int ld = p + 1;
-    // staged buffers: X1 (and Y1 if distinct), X2 (and Y2 if distinct)
     c64* sX1 = stage;
-    c64* sY1 = herm1 ? sX1 : sX1 + kRCH * ld;
-    c64* sX2 = sY1 + (herm1 ? kRCH * ld : kRCH * ld);
-    c64* sY2 = (X2 && Y2 == reinterpret_cast<const T2*>(X1)) ? sX1 : sX2 + kRCH * ld;
-    const bool y2_is_x1 = X2 && Y2 == reinterpret_cast<const T2*>(X1);
-    const int lane = threadIdx.x & 31;
+    c64* sX2 = sX1 + kRCH * ld;
     const int rg = threadIdx.x % kRG;
+    // software pipeline over row chunks: the next chunk's elements are loaded into registers
+    // (all in flight together) while the current chunk is consumed from shared memory
+    constexpr int kEPT = (PC * kRCH + kNT - 1) / kNT;  // elements per thread per chunk per operand
+    const int nel = p * kRCH;
+    c32 n1[kEPT], n2[kEPT];
+    auto fetch = [&](int r0) {
+        const int rn = min(kRCH, m - r0);
+#pragma unroll
+        for (int u = 0; u < kEPT; ++u) {
+            const int e = threadIdx.x + u * kNT;
+            const int c = e / kRCH, r = e % kRCH;
+            const bool ok = e < nel && r < rn;
+            n1[u] = ok ? X1[static_cast<size_t>(c) * m + r0 + r] : c32{0.f, 0.f};
+            if (X2) n2[u] = ok ? X2[static_cast<size_t>(c) * m + r0 + r] : c32{0.f, 0.f};
+        }
+    };
     for (int pass = 0; pass * (kNT / kRG) < ntiles; ++pass) {
         const int tile = pass * (kNT / kRG) + threadIdx.x / kRG;
         const bool active = tile < ntiles;
@@ -467,14 +481,9 @@ __device__ void tiled_gram2(const T1* __restrict__ X1, bool herm1, const T1* __r
         int ti = 0, tj = 0;
         if (active) {
             if (!second) {
-                if (herm1) {
-                    int rem = tile;
-                    while (rem >= nb - ti) { rem -= nb - ti; ++ti; }
-                    tj = ti + rem;
-                } else {
-                    ti = tile % nb;
-                    tj = tile / nb;
-                }
+                int rem = tile;
+                while (rem >= nb - ti) { rem -= nb - ti; ++ti; }
+                tj = ti + rem;
             } else {
                 ti = (tile - t1) % nb;
                 tj = (tile - t1) / nb;
@@ -485,23 +494,24 @@ __device__ void tiled_gram2(const T1* __restrict__ X1, bool herm1, const T1* __r
         for (int a = 0; a < 4; ++a)
 #pragma unroll
             for (int b = 0; b < 4; ++b) acc[a][b] = mk(0.0, 0.0);
+        fetch(0);
         for (int r0 = 0; r0 < m; r0 += kRCH) {
             const int rn = min(kRCH, m - r0);
-            __syncthreads();
-            for (int e = threadIdx.x; e < p * kRCH; e += kNT) {
-                const int c = e / kRCH, r = e % kRCH;
-                const bool ok = r < rn;
-                sX1[r * ld + c] = ok ? to64(X1[static_cast<size_t>(c) * m + r0 + r]) : mk(0.0, 0.0);
-                if (!herm1) sY1[r * ld + c] = ok ? to64(Y1[static_cast<size_t>(c) * m + r0 + r]) : mk(0.0, 0.0);
-                if (X2) {
-                    sX2[r * ld + c] = ok ? to64(X2[static_cast<size_t>(c) * m + r0 + r]) : mk(0.0, 0.0);
-                    if (!y2_is_x1) sY2[r * ld + c] = ok ? to64(Y2[static_cast<size_t>(c) * m + r0 + r]) : mk(0.0, 0.0);
+            __syncthreads();  // previous chunk consumed
+#pragma unroll
+            for (int u = 0; u < kEPT; ++u) {
+                const int e = threadIdx.x + u * kNT;
+                if (e < nel) {
+                    const int c = e / kRCH, r = e % kRCH;
+                    sX1[r * ld + c] = to64(n1[u]);
+                    if (X2) sX2[r * ld + c] = to64(n2[u]);
                 }
             }
             __syncthreads();
+            if (r0 + kRCH < m) fetch(r0 + kRCH);  // overlaps the compute below
             if (active) {
                 const c64* xs = second ? sX2 : sX1;
-                const c64* ys = second ? sY2 : sY1;
+                const c64* ys = sX1;
                 for (int r = rg; r < rn; r += kRG) {
                     c64 x[4], y[4];
 #pragma unroll
@@ -535,10 +545,9 @@ __device__ void tiled_gram2(const T1* __restrict__ X1, bool herm1, const T1* __r
                 for (int b = 0; b < 4; ++b) {
                     const int i = 4 * ti + a, j = 4 * tj + b;
                     G[j * p + i] = acc[a][b];
-                    if (!second && herm1 && ti != tj) G[i * p + j] = conj(acc[a][b]);
+                    if (!second && ti != tj) G[i * p + j] = conj(acc[a][b]);
                 }
         }
-        (void)lane;
     }
     __syncthreads();
 }
@@ -562,7 +571,7 @@ __global__ void __launch_bounds__(kNT, 2) k_orth_tiled(const c32* __restrict__ C
     __shared__ double s_inv;
     const int f = blockIdx.x;
     const c32* Cf = Cin + static_cast<size_t>(f) * m * p;
-    tiled_gram2<c32, c32>(Cf, true, Cf, nullptr, nullptr, m, p, stage, G, nullptr);
+    tiled_gram2<PC, c32, c32>(Cf, true, Cf, nullptr, nullptr, m, p, stage, G, nullptr);
     block_chol(G, p, true, perm, d, L, done, &s_inv);
     if (threadIdx.x == 0) {
         const double eps = eps_of<float>::value;
@@ -783,9 +792,9 @@ __global__ void __launch_bounds__(kNT, 2) k_final_tiled(const c32* __restrict__ 
     const c32* Cf = Cin + static_cast<size_t>(f) * m * p;
     long long T0 = clock64();
     if (Vin) {
-        tiled_gram2<c32, c32>(Cf, true, Cf, Vin + static_cast<size_t>(f) * m * p, Cf, m, p, stage, G, H);
+        tiled_gram2<PC, c32, c32>(Cf, true, Cf, Vin + static_cast<size_t>(f) * m * p, Cf, m, p, stage, G, H);
     } else {
-        tiled_gram2<c32, c32>(Cf, true, Cf, nullptr, nullptr, m, p, stage, G, nullptr);
+        tiled_gram2<PC, c32, c32>(Cf, true, Cf, nullptr, nullptr, m, p, stage, G, nullptr);
         const c64* Hf = Hin + static_cast<size_t>(f) * p * p;
         for (int e = threadIdx.x; e < p * p; e += kNT) H[e] = Hf[e];
         __syncthreads();
@@ -934,9 +943,9 @@ __global__ void __launch_bounds__(kNT, 2) k_gram_gh(const c32* __restrict__ Cin,
     const c32* Cf = Cin + static_cast<size_t>(f) * m * p;
     c64* Hf = Hio + static_cast<size_t>(f) * p * p;
     if (Vin) {
-        tiled_gram2<c32, c32>(Cf, true, Cf, Vin + static_cast<size_t>(f) * m * p, Cf, m, p, stage, G, H);
+        tiled_gram2<PC, c32, c32>(Cf, true, Cf, Vin + static_cast<size_t>(f) * m * p, Cf, m, p, stage, G, H);
     } else {
-        tiled_gram2<c32, c32>(Cf, true, Cf, nullptr, nullptr, m, p, stage, G, nullptr);
+        tiled_gram2<PC, c32, c32>(Cf, true, Cf, nullptr, nullptr, m, p, stage, G, nullptr);
         for (int e = threadIdx.x; e < p * p; e += kNT) H[e] = Hf[e];
         __syncthreads();
     }
@@ -1243,7 +1252,7 @@ __global__ void __launch_bounds__(kNT, 2) k_gram_only(const c32* __restrict__ Ci
     c64* G = reinterpret_cast<c64*>(dsm);
     c64* stage = G + PC * PC;
     const int f = blockIdx.x;
-    tiled_gram2<c32, c32>(Cin + static_cast<size_t>(f) * m * p, true, Cin + static_cast<size_t>(f) * m * p, nullptr,
+    tiled_gram2<PC, c32, c32>(Cin + static_cast<size_t>(f) * m * p, true, Cin + static_cast<size_t>(f) * m * p, nullptr,
                           nullptr, m, p, stage, G, nullptr);
     c64* Gf = Gout + static_cast<size_t>(f) * p * p;
     for (int e = threadIdx.x; e < p * p; e += kNT) Gf[e] = G[e];
