@@ -1344,129 +1344,49 @@ template <int PC>
 __global__ void __launch_bounds__(128) k_rows_solve(const c32* __restrict__ Cin, const c64* __restrict__ Lin,
                                                     const int32_t* __restrict__ perm_in, c32* __restrict__ Vout, int m,
                                                     int p) {
-    __shared__ c64 L[PC * PC];
+    __shared__ c64 Lp[PC * PC];  // Lp[a * PC + j] = conj-free L_p(j, a) = L[a * p + perm[j]], a < j
+    __shared__ double rinv[PC];  // 1 / L_p(j, j)
     __shared__ int perm[PC];
     const int f = blockIdx.y;
-    for (int e = threadIdx.x; e < p * p; e += blockDim.x) L[e] = Lin[static_cast<size_t>(f) * p * p + e];
     for (int e = threadIdx.x; e < p; e += blockDim.x) perm[e] = perm_in[static_cast<size_t>(f) * p + e];
+    __syncthreads();
+    const c64* Lf = Lin + static_cast<size_t>(f) * p * p;
+    for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+        const int a = e / p, j = e % p;
+        Lp[a * PC + j] = Lf[a * p + perm[j]];
+    }
+    for (int j = threadIdx.x; j < p; j += blockDim.x) {
+        const double ljj = Lf[j * p + perm[j]].re;
+        rinv[j] = ljj > 0.0 ? 1.0 / ljj : 0.0;
+    }
     __syncthreads();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= m) return;
     const c32* X = Cin + static_cast<size_t>(f) * m * p;
     c32* Out = Vout + static_cast<size_t>(f) * m * p;
+    c32 xin[PC];  // all inputs in flight before the (serial) substitution
+#pragma unroll
+    for (int j = 0; j < PC; ++j) xin[j] = j < p ? X[static_cast<size_t>(perm[j]) * m + r] : c32{0.f, 0.f};
     c64 v[PC];
 #pragma unroll
     for (int j = 0; j < PC; ++j) {
         if (j < p) {
-            const int pj = perm[j];
-            c64 x = to64(X[static_cast<size_t>(pj) * m + r]);
+            c64 x = to64(xin[j]);
+            c64 x1 = mk(0.0, 0.0);
 #pragma unroll
             for (int a = 0; a < PC; ++a) {
                 if (a < j) {
-                    const c64 l = L[a * p + pj];
-                    x.re -= v[a].re * l.re + v[a].im * l.im;
-                    x.im -= v[a].im * l.re - v[a].re * l.im;
+                    const c64 l = Lp[a * PC + j];
+                    c64& acc = (a & 1) ? x1 : x;
+                    acc.re -= v[a].re * l.re + v[a].im * l.im;
+                    acc.im -= v[a].im * l.re - v[a].re * l.im;
                 }
             }
-            const double ljj = L[j * p + pj].re;
-            const double inv = ljj > 0.0 ? 1.0 / ljj : 0.0;
-            v[j] = mk(x.re * inv, x.im * inv);
+            const double inv = rinv[j];
+            v[j] = mk((x.re + x1.re) * inv, (x.im + x1.im) * inv);
             Out[static_cast<size_t>(j) * m + r] = mk(static_cast<float>(v[j].re), static_cast<float>(v[j].im));
         }
     }
-}
-
-
-}  // namespace smb
-}  // namespace fmk
-
-using namespace fmk;
-
-static int32_t* g_sweep_dbg = nullptr;
-extern "C" int32_t fm_debug_set_sweep_buffer(int32_t* d) {
-    g_sweep_dbg = d;
-    return 0;
-}
-extern "C" int32_t fm_debug_set_phase_buffer(int32_t* d) {
-    return cudaMemcpyToSymbol(smb::g_phase_dbg, &d, sizeof(d)) == cudaSuccess ? 0 : 1;
-}
-
-cudaError_t fm_launch_cholqr_warp(const void* C, void* work, void* Vout, void* Rt, void* Hout, const void* Vin,
-                                  int32_t* status, int frames, int m, int p, bool final_mode, cudaStream_t s) {
-    if (p > 32 || p < 1 || m < p) return cudaErrorInvalidValue;
-    auto go = [&](auto kern, size_t smem) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        kern<<<frames, smb::kNT, smem, s>>>(static_cast<const c32*>(C), static_cast<c64*>(work),
-                                            static_cast<c32*>(Vout), static_cast<c64*>(Rt), static_cast<c64*>(Hout),
-                                            static_cast<const c32*>(Vin), status, m, p);
-        return cudaGetLastError();
-    };
-    if (p <= 8) return final_mode ? go(smb::k_cholqr_blk<8, 1>, smb::chol_smem_bytes<8>())
-                                  : go(smb::k_cholqr_blk<8, 0>, smb::chol_smem_bytes<8>());
-    if (p <= 16) return final_mode ? go(smb::k_cholqr_blk<16, 1>, smb::chol_smem_bytes<16>())
-                                   : go(smb::k_cholqr_blk<16, 0>, smb::chol_smem_bytes<16>());
-    return final_mode ? go(smb::k_cholqr_blk<32, 1>, smb::chol_smem_bytes<32>())
-                      : go(smb::k_cholqr_blk<32, 0>, smb::chol_smem_bytes<32>());
-}
-
-cudaError_t fm_launch_orth_tiled(const void* C, void* Vout, int32_t* status, int frames, int m, int p,
-                                  cudaStream_t s) {
-    if (p > 32 || (p & 3) || m < p) return cudaErrorInvalidValue;
-    auto go = [&](auto kern, size_t smem) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        kern<<<frames, smb::kNT, smem, s>>>(static_cast<const c32*>(C), static_cast<c32*>(Vout), status, m, p);
-        return cudaGetLastError();
-    };
-    if (p <= 8) return go(smb::k_orth_tiled<8>, sizeof(c64) * 2 * 64 + smb::tiled_stage_bytes<8>(1));
-    if (p <= 16) return go(smb::k_orth_tiled<16>, sizeof(c64) * 2 * 256 + smb::tiled_stage_bytes<16>(1));
-    return go(smb::k_orth_tiled<32>, sizeof(c64) * 2 * 1024 + smb::tiled_stage_bytes<32>(1));
-}
-
-cudaError_t fm_launch_final_tiled(const void* C, const void* V, const void* H, void* basis, double* eig,
-                                  int32_t* status, int frames, int m, int p, int k, cudaStream_t s) {
-    if (p > 32 || (p & 3) || k > p || m < p) return cudaErrorInvalidValue;
-    auto go = [&](auto kern, int pc) {
-        const size_t smem = sizeof(c64) * 5 * pc * pc + sizeof(double) * pc + sizeof(c64) * 3 * 64 * (pc + 1);
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        kern<<<frames, smb::kNT, smem, s>>>(static_cast<const c32*>(C), static_cast<const c32*>(V),
-                                            static_cast<const c64*>(H), static_cast<c64*>(basis), eig, status, m, p, k,
-                                            g_sweep_dbg);
-        return cudaGetLastError();
-    };
-    if (p <= 8) return go(smb::k_final_tiled<8>, 8);
-    if (p <= 16) return go(smb::k_final_tiled<16>, 16);
-    return go(smb::k_final_tiled<32>, 32);
-}
-
-// Split orthonormalisation: G -> Lw (in place), perm -> permw, V = C P R^-1 -> Vout.
-cudaError_t fm_launch_orth_split(const void* C, void* Vout, void* Lw, int32_t* permw, int32_t* status, int frames,
-                                 int m, int p, cudaStream_t s) {
-    if (p > 32 || (p & 3) || m < p || frames < 1) return cudaErrorInvalidValue;
-    auto go = [&](auto gram, auto piv, auto solve, int pc, int pw, size_t pbytes) {
-        const size_t gsm = sizeof(c64) * pc * pc + sizeof(c64) * 3 * 64 * (pc + 1);
-        cudaError_t e = cudaFuncSetAttribute(gram, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsm));
-        if (e != cudaSuccess) return e;
-        gram<<<frames, smb::kNT, gsm, s>>>(static_cast<const c32*>(C), static_cast<c64*>(Lw), m, p);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(piv, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pw * pbytes));
-        if (e != cudaSuccess) return e;
-        piv<<<(frames + pw - 1) / pw, 32 * pw, pw * pbytes, s>>>(static_cast<c64*>(Lw), permw, status, frames, m, p);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        solve<<<dim3((m + 127) / 128, frames), 128, 0, s>>>(static_cast<const c32*>(C), static_cast<const c64*>(Lw),
-                                                            permw, static_cast<c32*>(Vout), m, p);
-        return cudaGetLastError();
-    };
-    using namespace smb;
-    if (p <= 8)
-        return go(k_gram_only<8>, k_cholpiv_warp<8>, k_rows_solve<8>, 8, PivCfg<8>::kWarps, PivCfg<8>::kWarpBytes);
-    if (p <= 16)
-        return go(k_gram_only<16>, k_cholpiv_warp<16>, k_rows_solve<16>, 16, PivCfg<16>::kWarps,
-                  PivCfg<16>::kWarpBytes);
-    return go(k_gram_only<32>, k_cholpiv_warp<32>, k_rows_solve<32>, 32, PivCfg<32>::kWarps, PivCfg<32>::kWarpBytes);
 }
 
 // Split final stage: G -> Gw, Herm(H) -> Hw (in place for fast1), T -> Tw (p x k per frame).
