@@ -1389,6 +1389,98 @@ __global__ void __launch_bounds__(128) k_rows_solve(const c32* __restrict__ Cin,
     }
 }
 
+}  // namespace smb
+}  // namespace fmk
+
+using namespace fmk;
+
+static int32_t* g_sweep_dbg = nullptr;
+extern "C" int32_t fm_debug_set_sweep_buffer(int32_t* d) {
+    g_sweep_dbg = d;
+    return 0;
+}
+extern "C" int32_t fm_debug_set_phase_buffer(int32_t* d) {
+    return cudaMemcpyToSymbol(smb::g_phase_dbg, &d, sizeof(d)) == cudaSuccess ? 0 : 1;
+}
+
+cudaError_t fm_launch_cholqr_warp(const void* C, void* work, void* Vout, void* Rt, void* Hout, const void* Vin,
+                                  int32_t* status, int frames, int m, int p, bool final_mode, cudaStream_t s) {
+    if (p > 32 || p < 1 || m < p) return cudaErrorInvalidValue;
+    auto go = [&](auto kern, size_t smem) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        kern<<<frames, smb::kNT, smem, s>>>(static_cast<const c32*>(C), static_cast<c64*>(work),
+                                            static_cast<c32*>(Vout), static_cast<c64*>(Rt), static_cast<c64*>(Hout),
+                                            static_cast<const c32*>(Vin), status, m, p);
+        return cudaGetLastError();
+    };
+    if (p <= 8) return final_mode ? go(smb::k_cholqr_blk<8, 1>, smb::chol_smem_bytes<8>())
+                                  : go(smb::k_cholqr_blk<8, 0>, smb::chol_smem_bytes<8>());
+    if (p <= 16) return final_mode ? go(smb::k_cholqr_blk<16, 1>, smb::chol_smem_bytes<16>())
+                                   : go(smb::k_cholqr_blk<16, 0>, smb::chol_smem_bytes<16>());
+    return final_mode ? go(smb::k_cholqr_blk<32, 1>, smb::chol_smem_bytes<32>())
+                      : go(smb::k_cholqr_blk<32, 0>, smb::chol_smem_bytes<32>());
+}
+
+cudaError_t fm_launch_orth_tiled(const void* C, void* Vout, int32_t* status, int frames, int m, int p,
+                                  cudaStream_t s) {
+    if (p > 32 || (p & 3) || m < p) return cudaErrorInvalidValue;
+    auto go = [&](auto kern, size_t smem) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        kern<<<frames, smb::kNT, smem, s>>>(static_cast<const c32*>(C), static_cast<c32*>(Vout), status, m, p);
+        return cudaGetLastError();
+    };
+    if (p <= 8) return go(smb::k_orth_tiled<8>, sizeof(c64) * 2 * 64 + smb::tiled_stage_bytes<8>(1));
+    if (p <= 16) return go(smb::k_orth_tiled<16>, sizeof(c64) * 2 * 256 + smb::tiled_stage_bytes<16>(1));
+    return go(smb::k_orth_tiled<32>, sizeof(c64) * 2 * 1024 + smb::tiled_stage_bytes<32>(1));
+}
+
+cudaError_t fm_launch_final_tiled(const void* C, const void* V, const void* H, void* basis, double* eig,
+                                  int32_t* status, int frames, int m, int p, int k, cudaStream_t s) {
+    if (p > 32 || (p & 3) || k > p || m < p) return cudaErrorInvalidValue;
+    auto go = [&](auto kern, int pc) {
+        const size_t smem = sizeof(c64) * 5 * pc * pc + sizeof(double) * pc + sizeof(c64) * 3 * 64 * (pc + 1);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        kern<<<frames, smb::kNT, smem, s>>>(static_cast<const c32*>(C), static_cast<const c32*>(V),
+                                            static_cast<const c64*>(H), static_cast<c64*>(basis), eig, status, m, p, k,
+                                            g_sweep_dbg);
+        return cudaGetLastError();
+    };
+    if (p <= 8) return go(smb::k_final_tiled<8>, 8);
+    if (p <= 16) return go(smb::k_final_tiled<16>, 16);
+    return go(smb::k_final_tiled<32>, 32);
+}
+
+// Split orthonormalisation: G -> Lw (in place), perm -> permw, V = C P R^-1 -> Vout.
+cudaError_t fm_launch_orth_split(const void* C, void* Vout, void* Lw, int32_t* permw, int32_t* status, int frames,
+                                 int m, int p, cudaStream_t s) {
+    if (p > 32 || (p & 3) || m < p || frames < 1) return cudaErrorInvalidValue;
+    auto go = [&](auto gram, auto piv, auto solve, int pc, int pw, size_t pbytes) {
+        const size_t gsm = sizeof(c64) * pc * pc + sizeof(c64) * 3 * 64 * (pc + 1);
+        cudaError_t e = cudaFuncSetAttribute(gram, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsm));
+        if (e != cudaSuccess) return e;
+        gram<<<frames, smb::kNT, gsm, s>>>(static_cast<const c32*>(C), static_cast<c64*>(Lw), m, p);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(piv, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pw * pbytes));
+        if (e != cudaSuccess) return e;
+        piv<<<(frames + pw - 1) / pw, 32 * pw, pw * pbytes, s>>>(static_cast<c64*>(Lw), permw, status, frames, m, p);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        solve<<<dim3((m + 127) / 128, frames), 128, 0, s>>>(static_cast<const c32*>(C), static_cast<const c64*>(Lw),
+                                                            permw, static_cast<c32*>(Vout), m, p);
+        return cudaGetLastError();
+    };
+    using namespace smb;
+    if (p <= 8)
+        return go(k_gram_only<8>, k_cholpiv_warp<8>, k_rows_solve<8>, 8, PivCfg<8>::kWarps, PivCfg<8>::kWarpBytes);
+    if (p <= 16)
+        return go(k_gram_only<16>, k_cholpiv_warp<16>, k_rows_solve<16>, 16, PivCfg<16>::kWarps,
+                  PivCfg<16>::kWarpBytes);
+    return go(k_gram_only<32>, k_cholpiv_warp<32>, k_rows_solve<32>, 32, PivCfg<32>::kWarps, PivCfg<32>::kWarpBytes);
+}
+
 // Split final stage: G -> Gw, Herm(H) -> Hw (in place for fast1), T -> Tw (p x k per frame).
 cudaError_t fm_launch_final_split(const void* C, const void* V, void* Hw, void* Gw, void* Tw, void* basis, double* eig,
                                   int32_t* status, int frames, int m, int p, int k, cudaStream_t s,
