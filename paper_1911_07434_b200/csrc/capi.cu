@@ -22,7 +22,8 @@
 
 // ------------------------------------------------------------------ kernel launchers (other TUs)
 cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, int64_t frames, int64_t m, int64_t n,
-                             cudaStream_t stream);
+                             cudaStream_t stream, void* planes_hi = nullptr, void* planes_lo = nullptr,
+                             float* scale = nullptr);
 template <typename T>
 cudaError_t fm_launch_rmul(const void*, const void*, const void*, void*, const int32_t*, int, int, int, bool,
                            cudaStream_t);

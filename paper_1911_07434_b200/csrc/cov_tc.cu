@@ -133,11 +133,15 @@ __device__ __forceinline__ void convert_tile(const uint8_t* stage, uint8_t* op, 
 //   w0 TMA producer | w1 MMA issuer (leader) + TMEM owner | w2..w5 converters | w6..w9 epilogue.
 // The epilogue of tile i (TMEM -> fp32 R) overlaps the TMA + fp16 conversion of tile i + 1;
 // the MMA of tile i + 1 starts once both CTAs' epilogues have drained TMEM (acc_empty).
-template <bool kTmaStore>
+// kEpi: 0 generic-store fallback (odd M), 1 TMA-stored complex64 R, 2 TMA-stored fp16 hi/lo planes of
+// R / s_f (M <= 256: one tile per frame; s_f = smallest power of two >= max_i R_ii, exchanged between the
+// two CTAs of the pair; rmap / mmap are the hi / lo plane maps, rscale[f] = s_f).
+template <int kEpi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cov_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap rmap,
                   const __grid_constant__ CUtensorMap mmap, float* __restrict__ r_out, int32_t* __restrict__ status,
-                  int m, int n, int tiles_per_frame, int total_tiles) {
+                  int m, int n, int tiles_per_frame, int total_tiles, float* __restrict__ rscale) {
+    constexpr bool kTmaStore = kEpi >= 1;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* staging = smem;
@@ -150,7 +154,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* op_empty = bars + 2 * kStagesS + kStagesO;
     uint64_t* acc_full = bars + 2 * kStagesS + 2 * kStagesO;
     uint64_t* acc_empty = acc_full + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+    uint64_t* xch_bar = acc_empty + 1;                             // [2] peer's diagonal max arrived
+    float* xch_val = reinterpret_cast<float*>(xch_bar + 2);         // [2] peer's diagonal max
+    float* s_wmax = xch_val + 2;                                    // [4] per epilogue warp
+    float* s_scale = s_wmax + 4;                                    // [1]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_scale + 1);
     float2* epi = reinterpret_cast<float2*>(epi_bytes);
 
     const int warp = threadIdx.x >> 5;
@@ -171,6 +179,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         mbar_init(smem_u32(acc_full), 1);
         mbar_init(smem_u32(acc_empty), 2);  // one arrive per CTA's epilogue (leader's copy used)
+        mbar_init(smem_u32(&xch_bar[0]), 1);
+        mbar_init(smem_u32(&xch_bar[1]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -279,6 +289,115 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             flag = __reduce_or_sync(0xffffffffu, flag);
             if (flag && lane == 0 && status != nullptr) atomicOr(&status[frame], flag);
         }
+    } else if (kEpi == 2) {
+        // ---------------- epilogue, fp16 hi/lo planes of R / s_f (M <= 256: tile == frame).
+        // 1. s_f: each thread's diagonal element (TMEM column = its row), CTA max, exchanged with the
+        //    peer CTA through DSMEM + an mbarrier (double-buffered by tile parity).
+        // 2. per 32-column chunk: two tcgen05.ld, x = R/s_f -> hi = fp16(x), lo = fp16(x - hi), two
+        //    128B-swizzled 32 x 64-half boxes, two TMA stores (hi plane, lo plane).
+        const int quarter = warp & 3;
+        const float inv_n = 1.0f / static_cast<float>(n);
+        const uint32_t ebase = smem_u32(epi_bytes) + (warp - 6) * kEpiWarpBytes;
+        const uint32_t peer = rank ^ 1u;
+        int t = 0, gc = 0;
+        for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
+            const int frame = tile;
+            const int row0 = 128 * static_cast<int>(rank) + 32 * quarter;
+            const int gi = row0 + lane;
+            mbar_wait(smem_u32(acc_full), t & 1);
+            tc_fence_after();
+            const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
+            {
+                uint32_t dv[32];
+                tmem_ld32(taddr + row0, dv);
+                tmem_wait_ld();
+                float dg = 0.f;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j == lane) dg = __uint_as_float(dv[j]);
+                dg *= inv_n;
+                if (!(dg >= 0.f) || gi >= m) dg = 0.f;  // non-finite frames are flagged by the converters
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) dg = fmaxf(dg, __shfl_xor_sync(0xffffffffu, dg, o));
+                if (lane == 0) s_wmax[quarter] = dg;
+            }
+            named_bar_sync(2, 128);
+            if (warp == 6 && lane == 0) {
+                const float cmax = fmaxf(fmaxf(s_wmax[0], s_wmax[1]), fmaxf(s_wmax[2], s_wmax[3]));
+                const uint32_t slot = smem_u32(&xch_val[t & 1]), bar = smem_u32(&xch_bar[t & 1]);
+                asm volatile(
+                    "{\n\t.reg .b32 ra, rb;\n\t"
+                    "mapa.shared::cluster.u32 ra, %0, %2;\n\t"
+                    "mapa.shared::cluster.u32 rb, %1, %2;\n\t"
+                    "st.shared::cluster.f32 [ra], %3;\n\t"
+                    "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [rb];\n\t}" ::"r"(slot),
+                    "r"(bar), "r"(peer), "f"(cmax)
+                    : "memory");
+                mbar_wait_cluster(bar, (t >> 1) & 1);
+                const float maxd = fmaxf(cmax, xch_val[t & 1]);
+                float sc = 1.f;
+                if (maxd > 0.f && maxd < 3.0e38f) {
+                    int e;
+                    const float fr = frexpf(maxd, &e);  // maxd = fr 2^e, fr in [0.5, 1)
+                    sc = ldexpf(1.f, fr == 0.5f ? e - 1 : e);
+                }
+                *s_scale = sc;
+                if (rank == 0) rscale[frame] = sc;
+            }
+            named_bar_sync(2, 128);
+            const float mul = inv_n / *s_scale;  // power-of-two divisor: exact
+            const int nchunks = row0 < m ? (m + 31) / 32 : 0;
+            for (int c = 0; c < nchunks; ++c, ++gc) {
+                const int col0 = 32 * c;
+                uint32_t vr[32], vi[32];
+                tmem_ld32(taddr + col0, vr);
+                tmem_ld32(taddr + 256 + col0, vi);
+                tmem_wait_ld();
+                const int b = gc & 1;
+                if (lane == 0) bulk_wait_read1();
+                __syncwarp();
+                const uint32_t hbuf = ebase + b * kEpiChunk;
+                const uint32_t lbuf = ebase + 2 * kEpiChunk + b * kEpiChunk;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {  // 16-byte chunk q = complex 4q .. 4q + 3 (8 halves)
+                    uint32_t hw[4], lw[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int j = 4 * q + u;
+                        const float re = __uint_as_float(vr[j]) * mul;
+                        const float im = (col0 + j == gi) ? 0.f : __uint_as_float(vi[j]) * mul;
+                        const __half hre = __float2half_rn(re), him = __float2half_rn(im);
+                        const __half lre = __float2half_rn(re - __half2float(hre));
+                        const __half lim = __float2half_rn(im - __half2float(him));
+                        hw[u] = static_cast<uint32_t>(__half_as_ushort(hre)) |
+                                (static_cast<uint32_t>(__half_as_ushort(him)) << 16);
+                        lw[u] = static_cast<uint32_t>(__half_as_ushort(lre)) |
+                                (static_cast<uint32_t>(__half_as_ushort(lim)) << 16);
+                    }
+                    const uint32_t off = lane * 128 + ((q ^ (lane & 7)) << 4);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(hbuf + off), "r"(hw[0]), "r"(hw[1]),
+                                 "r"(hw[2]), "r"(hw[3])
+                                 : "memory");
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(lbuf + off), "r"(lw[0]), "r"(lw[1]),
+                                 "r"(lw[2]), "r"(lw[3])
+                                 : "memory");
+                }
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_3d(&rmap, hbuf, 2 * col0, row0, frame);
+                    tma_store_3d(&mmap, lbuf, 2 * col0, row0, frame);
+                    bulk_commit();
+                }
+            }
+            tc_fence_before();
+            named_bar_sync(2, 128);  // all four epilogue warps finished reading TMEM
+            if (warp == 6 && lane == 0) {
+                if (rank == 0) mbar_arrive_local(smem_u32(acc_empty));
+                else mbar_arrive_cluster(smem_u32(acc_empty), 0);
+            }
+        }
+        if (lane == 0) bulk_wait_all();
     } else if (kTmaStore) {
         // ---------------- epilogue (warps 6..9): TMEM -> registers -> swizzled smem -> TMA store.
         // Per 16-column chunk: two tcgen05.ld (Re, Im), eight conflict-free 16-byte st.shared into a
@@ -408,11 +527,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 // Launch K1 for `frames` frames. Requirements: n even (TMA 16-byte row stride).
 // Returns a cudaError_t value (cudaErrorInvalidValue for unsupported shapes).
+// planes_hi != nullptr selects the fp16 hi/lo plane output (M <= 256, M even): planes_hi / planes_lo
+// are frames x M x 2M halves (R / s_f interleaved re, im), scale[f] = s_f; d_r is unused then.
 cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, int64_t frames, int64_t m, int64_t n,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, void* planes_hi, void* planes_lo, float* scale) {
     using namespace fmk::cov;
     if (frames < 1 || m < 1 || n < 2 || (n & 1) || frames * m > 0x7fffffff || 2 * n > 0x7fffffff)
         return cudaErrorInvalidValue;
+    const bool planes = planes_hi != nullptr;
+    if (planes && (m > 256 || (m & 1) || !planes_lo || !scale)) return cudaErrorInvalidValue;
     EncodeTiledFn enc = get_encode();
     if (!enc) return cudaErrorNotSupported;
     CUtensorMap map, rmap, mmap;
@@ -424,8 +547,21 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    const bool tma_store = (m % 2) == 0;  // R row pitch 8M bytes must be a multiple of 16
-    if (tma_store) {
+    const int epi = planes ? 2 : ((m % 2) == 0 ? 1 : 0);  // R row pitch 8M bytes must be a multiple of 16
+    if (epi == 2) {
+        cuuint64_t pdims[3] = {static_cast<cuuint64_t>(2 * m), static_cast<cuuint64_t>(m),
+                               static_cast<cuuint64_t>(frames)};
+        cuuint64_t pstr[2] = {static_cast<cuuint64_t>(4 * m), static_cast<cuuint64_t>(4 * m * m)};
+        cuuint32_t pbox[3] = {64, 32, 1};  // 32 rows x 32 complex halves (128 B rows), 128B-swizzled
+        cr = enc(&rmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, planes_hi, pdims, pstr, pbox, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+        cr = enc(&mmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, planes_lo, pdims, pstr, pbox, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    } else if (epi == 1) {
         cuuint64_t rdims[3] = {static_cast<cuuint64_t>(2 * m), static_cast<cuuint64_t>(m),
                                static_cast<cuuint64_t>(frames)};
         cuuint64_t rstr[2] = {static_cast<cuuint64_t>(8 * m), static_cast<cuuint64_t>(8 * m * m)};
@@ -441,14 +577,16 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
         rmap = map;  // unused by the fallback epilogue
         mmap = map;
     }
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[tma_store]) {
-        cudaError_t e = tma_store ? cudaFuncSetAttribute(cov_tc_kernel<true>,
-                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes)
-                                  : cudaFuncSetAttribute(cov_tc_kernel<false>,
-                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    static bool attr_set[3] = {false, false, false};
+    if (!attr_set[epi]) {
+        cudaError_t e = epi == 2 ? cudaFuncSetAttribute(cov_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                        kSmemBytes)
+                        : epi == 1 ? cudaFuncSetAttribute(cov_tc_kernel<1>,
+                                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes)
+                                   : cudaFuncSetAttribute(cov_tc_kernel<0>,
+                                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         if (e != cudaSuccess) return e;
-        attr_set[tma_store] = true;
+        attr_set[epi] = true;
     }
     const int nb = static_cast<int>((m + 255) / 256);
     const int tiles_per_frame = nb * (nb + 1) / 2;
@@ -462,13 +600,13 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
     }
     const int64_t pairs = std::min<int64_t>(tiles, std::max(1, sm_count / 2));
     const dim3 grid(static_cast<unsigned>(2 * pairs));
-    if (tma_store)
-        cov_tc_kernel<true><<<grid, kThreads, kSmemBytes, stream>>>(map, rmap, mmap, d_r, d_status, static_cast<int>(m),
-                                                                    static_cast<int>(n), tiles_per_frame,
-                                                                    static_cast<int>(tiles));
-    else
-        cov_tc_kernel<false><<<grid, kThreads, kSmemBytes, stream>>>(map, rmap, mmap, d_r, d_status,
-                                                                     static_cast<int>(m), static_cast<int>(n),
-                                                                     tiles_per_frame, static_cast<int>(tiles));
+    auto go = [&](auto kern) {
+        kern<<<grid, kThreads, kSmemBytes, stream>>>(map, rmap, mmap, d_r, d_status, static_cast<int>(m),
+                                                     static_cast<int>(n), tiles_per_frame, static_cast<int>(tiles),
+                                                     scale);
+    };
+    if (epi == 2) go(cov_tc_kernel<2>);
+    else if (epi == 1) go(cov_tc_kernel<1>);
+    else go(cov_tc_kernel<0>);
     return cudaGetLastError();
 }
