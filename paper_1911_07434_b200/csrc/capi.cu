@@ -3,6 +3,7 @@
 // behind the reference-named C++ facade, host random draws and the synthetic frame
 // generator. No CPU compute fallback: every numeric stage below launches a kernel.
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -52,6 +53,9 @@ cudaError_t fm_launch_rmul_tc(const float* d_r, const float* d_omega, const floa
                               int64_t m, int64_t p, cudaStream_t stream);
 cudaError_t fm_launch_orth_split(const void* C, void* Vout, void* Lw, int32_t* permw, int32_t* status, int frames,
                                  int m, int p, cudaStream_t s);
+cudaError_t fm_launch_rmul_planes(const void* planes_hi, const void* planes_lo, const float* d_scale,
+                                  const float* d_omega, const float* d_v, float* d_c, int64_t frames, int64_t m,
+                                  int64_t p, cudaStream_t stream);
 cudaError_t fm_launch_final_split(const void* C, const void* V, void* Hw, void* Gw, void* Tw, void* basis, double* eig,
                                   int32_t* status, int frames, int m, int p, int k, cudaStream_t s,
                                   double* eig_next = nullptr);
@@ -382,6 +386,8 @@ struct fm_plan_s {
     double* spec64 = nullptr; // frames x L (fp64 spectrum for peak picking)
     double* zgrid = nullptr;  // L complex128
     int32_t* scratch_status = nullptr;  // frames
+    float* rscale = nullptr;            // frames: s_f of the fp16 hi/lo R planes (plane mode)
+    bool last_planes = false;           // R of the last run is stored as planes (fm_rerun_frames)
     // exact method via certified subspace iteration (pe > 0): plan-owned Omega, R U product, gap
     int pe = 0;
     float* omega_e = nullptr;   // frames x M x pe fp32
@@ -512,6 +518,7 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
     chk(pl->get(&pl->spec64, B * L));
     chk(pl->get(&pl->zgrid, L * 2));
     chk(pl->get(&pl->scratch_status, B));
+    chk(pl->get(&pl->rscale, B));
     if (pl->pe > 0) {
         chk(pl->get(&pl->omega_e, B * M * pl->pe));
         chk(pl->get(&pl->u32, B * K * M * 2));
@@ -585,6 +592,29 @@ extern "C" fm_status fm_plan_stage_times(fm_plan plan, float* ms, int32_t* runs)
 static bool tc_rmul(int m, int p) {
     static const bool simt = std::getenv("FM_SIMT_RMUL") != nullptr;
     return !simt && (m % 2) == 0 && p >= 4 && p <= 32 && (p % 4) == 0;
+}
+
+// R as fp16 hi/lo planes of R / s_f (cov_tc.cu kEpi = 2 -> rmul_planes_kernel): M <= 256 (one tile per
+// frame), tensor-core products; FM_NO_PLANES=1 keeps complex64 R + the tf32 products (comparison).
+static bool plane_mode(const fm_plan_s* pl) {
+    static const bool off = std::getenv("FM_NO_PLANES") != nullptr;
+    // fast2 only: the exact method's Jacobi fallback and fast1's gather read complex64 R
+    return !off && pl->d.method == FM_METHOD_FAST2 && pl->d.m <= 256 &&
+           tc_rmul(static_cast<int>(pl->d.m), static_cast<int>(pl->d.p));
+}
+struct Planes {  // per-sub-batch view; hi == nullptr: complex64 R
+    void* hi = nullptr;
+    void* lo = nullptr;
+    float* scale = nullptr;
+};
+static Planes planes_view(fm_plan pl, int64_t f0) {
+    Planes v;
+    const size_t plane = static_cast<size_t>(pl->d.max_frames) * pl->d.m * 2 * pl->d.m;  // halves per plane
+    __half* base = reinterpret_cast<__half*>(pl->R);
+    v.hi = base + static_cast<size_t>(f0) * pl->d.m * 2 * pl->d.m;
+    v.lo = base + plane + static_cast<size_t>(f0) * pl->d.m * 2 * pl->d.m;
+    v.scale = pl->rscale + f0;
+    return v;
 }
 
 static bool split_final() {  // FM_FUSED_FINAL=1 selects the single-kernel k_final_tiled (comparison)
@@ -696,7 +726,7 @@ static fm_batch_io io_view(fm_plan pl, const fm_batch_io* io, int64_t f0) {
 }
 
 static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io, const float* R, cudaStream_t s,
-                              const WorkView& w, bool prof) {
+                              const WorkView& w, bool prof, const Planes& pv) {
     const auto& d = pl->d;
     const int F = static_cast<int>(frames), M = static_cast<int>(d.m), P = static_cast<int>(d.p),
               K = static_cast<int>(d.k);
@@ -731,17 +761,21 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
         return FM_OK;
     };
     fm_status st = FM_OK;
-    if (d.method == FM_METHOD_FAST2) {
-        if (tc_rmul(M, P))
-            FM_LAUNCH(fm_launch_rmul_tc(R, io->omega, nullptr, w.C, F, M, P, s));
+    // C = R Omega (omega) or C = R V: fp16 planes -> rmul_planes_kernel, complex64 R -> tf32 kernel / SIMT
+    auto rmul = [&](const float* omega, const float* v, float* c, int p) -> fm_status {
+        if (pv.hi)
+            FM_LAUNCH(fm_launch_rmul_planes(pv.hi, pv.lo, pv.scale, omega, v, c, F, M, p, s));
+        else if (tc_rmul(M, p))
+            FM_LAUNCH(fm_launch_rmul_tc(R, omega, v, c, F, M, p, s));
         else
-            FM_LAUNCH(fm_launch_rmul<float>(R, io->omega, nullptr, w.C, nullptr, F, M, P, true, s));
+            FM_LAUNCH(fm_launch_rmul<float>(R, omega, v, c, nullptr, F, M, p, omega != nullptr, s));
+        return FM_OK;
+    };
+    if (d.method == FM_METHOD_FAST2) {
+        if ((st = rmul(io->omega, nullptr, w.C, P)) != FM_OK) return st;
         for (int it = 0; it < d.t; ++it) {
             if ((st = orth(false, nullptr)) != FM_OK) return st;
-            if (tc_rmul(M, P))
-                FM_LAUNCH(fm_launch_rmul_tc(R, nullptr, w.V, w.C, F, M, P, s));
-            else
-                FM_LAUNCH(fm_launch_rmul<float>(R, nullptr, w.V, w.C, nullptr, F, M, P, false, s));
+            if ((st = rmul(nullptr, w.V, w.C, P)) != FM_OK) return st;
         }
         if (tiled) {
             if (split_final())
@@ -770,17 +804,17 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
         const int PE = pl->pe;
         k_clear_bits<<<(F + 255) / 256, 256, 0, s>>>(w.scratch, F, ~0);
         FM_CUDA_OK(cudaGetLastError());
-        FM_LAUNCH(fm_launch_rmul_tc(R, w.omega_e, nullptr, w.C, F, M, PE, s));
+        if ((st = rmul(w.omega_e, nullptr, w.C, PE)) != FM_OK) return st;
         for (int it = 0; it < kExactIters; ++it) {
             FM_LAUNCH(fm_launch_orth_split(w.C, w.V, w.Rt, reinterpret_cast<int32_t*>(w.H), w.scratch, F, M, PE, s));
-            FM_LAUNCH(fm_launch_rmul_tc(R, nullptr, w.V, w.C, F, M, PE, s));
+            if ((st = rmul(nullptr, w.V, w.C, PE)) != FM_OK) return st;
         }
         FM_LAUNCH(fm_launch_final_split(w.C, w.V, w.H, w.Rt, w.work, basis, eig, w.scratch, F, M, PE, K, s,
                                         w.eig_next));
         const int64_t nb = static_cast<int64_t>(F) * K * M * 2;
         k_basis_to_c32<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, s>>>(basis, w.u32, nb);
         FM_CUDA_OK(cudaGetLastError());
-        FM_LAUNCH(fm_launch_rmul_tc(R, nullptr, w.u32, w.ru, F, M, K, s));
+        if ((st = rmul(nullptr, w.u32, w.ru, K)) != FM_OK) return st;
         k_exact_certify<<<(F + 7) / 8, 256, 0, s>>>(w.ru, basis, eig, w.eig_next, w.scratch, io->status, F, M, K,
                                                      kExactTol);
         FM_CUDA_OK(cudaGetLastError());
@@ -829,12 +863,15 @@ extern "C" fm_status fm_run_batch(fm_plan pl, int64_t frames, const fm_batch_io*
     FM_CUDA_OK(cudaSetDevice(pl->device));
     FM_CUDA_OK(cudaMemsetAsync(io->status, 0, sizeof(int32_t) * frames, s));
     const int nsub = auto_subbatches(pl, frames);
+    const bool planes = plane_mode(pl) && !io->covariance;
+    pl->last_planes = planes;
     if (nsub <= 1) {
         float* R = io->covariance ? io->covariance : pl->R;
+        const Planes pv = planes ? planes_view(pl, 0) : Planes{};
         mark(pl, 0, s);
-        FM_LAUNCH(fm_launch_cov_tc(io->x, R, io->status, frames, pl->d.m, pl->d.n, s));
+        FM_LAUNCH(fm_launch_cov_tc(io->x, R, io->status, frames, pl->d.m, pl->d.n, s, pv.hi, pv.lo, pv.scale));
         mark(pl, 1, s);
-        return run_post_cov(pl, frames, io, R, s, work_view(pl, 0), true);
+        return run_post_cov(pl, frames, io, R, s, work_view(pl, 0), true, pv);
     }
     while (static_cast<int>(pl->sub.size()) < nsub) {
         cudaStream_t q;
@@ -857,13 +894,14 @@ extern "C" fm_status fm_run_batch(fm_plan pl, int64_t frames, const fm_batch_io*
         FM_CUDA_OK(cudaStreamWaitEvent(q, pl->sub_ev[0], 0));
         const fm_batch_io o = io_view(pl, io, f0);
         float* R = io->covariance ? o.covariance : pl->R + f0 * MM2;
+        const Planes pv = planes ? planes_view(pl, f0) : Planes{};
         if (i == 0) mark(pl, 0, q);
         {
             cudaStream_t s = q;  // FM_LAUNCH synchronises `s` in debug mode
-            FM_LAUNCH(fm_launch_cov_tc(o.x, R, o.status, nf, pl->d.m, pl->d.n, q));
+            FM_LAUNCH(fm_launch_cov_tc(o.x, R, o.status, nf, pl->d.m, pl->d.n, q, pv.hi, pv.lo, pv.scale));
         }
         if (i == 0) mark(pl, 1, q);
-        st = run_post_cov(pl, nf, &o, R, q, work_view(pl, f0), i == 0);
+        st = run_post_cov(pl, nf, &o, R, q, work_view(pl, f0), i == 0, pv);
         if (st != FM_OK) return st;
         FM_CUDA_OK(cudaEventRecord(pl->sub_ev[1 + i], q));
         FM_CUDA_OK(cudaStreamWaitEvent(s, pl->sub_ev[1 + i], 0));
@@ -883,7 +921,8 @@ extern "C" fm_status fm_rerun_frames(fm_plan pl, int64_t frames, const int32_t* 
     if (st != FM_OK) return st;
     FM_CUDA_OK(cudaSetDevice(pl->device));
     const float* R = io->covariance ? io->covariance : pl->R;
-    return run_post_cov(pl, frames, io, R, static_cast<cudaStream_t>(stream), work_view(pl, 0), false);
+    const Planes pv = pl->last_planes && !io->covariance ? planes_view(pl, 0) : Planes{};
+    return run_post_cov(pl, frames, io, R, static_cast<cudaStream_t>(stream), work_view(pl, 0), false, pv);
 }
 
 extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const float* h_x, const uint64_t* draw_seeds,

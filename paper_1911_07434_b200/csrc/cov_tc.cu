@@ -366,13 +366,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         const int j = 4 * q + u;
                         const float re = __uint_as_float(vr[j]) * mul;
                         const float im = (col0 + j == gi) ? 0.f : __uint_as_float(vi[j]) * mul;
-                        const __half hre = __float2half_rn(re), him = __float2half_rn(im);
-                        const __half lre = __float2half_rn(re - __half2float(hre));
-                        const __half lim = __float2half_rn(im - __half2float(him));
-                        hw[u] = static_cast<uint32_t>(__half_as_ushort(hre)) |
-                                (static_cast<uint32_t>(__half_as_ushort(him)) << 16);
-                        lw[u] = static_cast<uint32_t>(__half_as_ushort(lre)) |
-                                (static_cast<uint32_t>(__half_as_ushort(lim)) << 16);
+                        const __half2 h = __floats2half2_rn(re, im);
+                        const float2 hf = __half22float2(h);
+                        const __half2 l = __floats2half2_rn(re - hf.x, im - hf.y);
+                        hw[u] = *reinterpret_cast<const uint32_t*>(&h);
+                        lw[u] = *reinterpret_cast<const uint32_t*>(&l);
                     }
                     const uint32_t off = lane * 128 + ((q ^ (lane & 7)) << 4);
                     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(hbuf + off), "r"(hw[0]), "r"(hw[1]),

@@ -28,6 +28,7 @@
 // overlaps the next tile. HBM traffic: R once (8 M^2 bytes/frame) + V (8 M p bytes).
 
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -292,6 +293,255 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Plane variant: R arrives as fp16 hi / lo planes of R / s_f (written by the covariance epilogue,
+// cov_tc.cu kEpi = 2), so A needs no conversion pass: per stage of 64 reals (32 complex j) each CTA
+// TMA-loads 128 rows of both planes (16 KB each, 128B-swizzled) and the 32-column chunk of V / Omega;
+// converters only build this CTA's fp16 hi / lo B^T rows; kind::f16 MMAs (K = 16):
+//   MMA1 (N = 4 PH): A_hi x [B_hi(re) B_hi(im) | B_lo(re) B_lo(im)];  MMA2 (N = 2 PH): A_lo x B_hi.
+// Epilogue: C = s_f (D_hi + D_lo). Representation error of R <= 2^-24 s_f (s_f >= max |R_ij|).
+constexpr int kPKc = 64;                     // halves of K per stage
+constexpr int kPStages = 4;
+template <int PH>
+struct PCfg {
+    static constexpr int kN1 = 4 * PH, kN2 = 2 * PH;
+    static constexpr int kOffLo = kABytes;                         // 16 KB planes
+    static constexpr int kOffV = 2 * kABytes;
+    static constexpr int kVBytes = PH * 256;                       // <= PH rows x 32 complex (or 32 x PH floats)
+    static constexpr int kOffB1 = kOffV + kVBytes;
+    static constexpr int kOffB2 = kOffB1 + 2 * PH * 128;
+    static constexpr int kStageBytes = kOffB2 + PH * 128;
+    static constexpr int kTmemCols = kAcc * kN1;
+    static constexpr int kSmem = 1024 + kPStages * kStageBytes + 256;
+    static_assert(kStageBytes % 1024 == 0 && kOffB1 % 1024 == 0 && kOffB2 % 1024 == 0, "SW128 alignment");
+};
+__host__ __device__ constexpr uint32_t idesc_f16(int n) {
+    return (1u << 4) | ((static_cast<uint32_t>(n) >> 3) << 17) | ((256u >> 4) << 24);  // A = B = F16, D = F32
+}
+__device__ __forceinline__ void umma_f16_2sm_(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+    return static_cast<uint32_t>(__half_as_ushort(__float2half_rn(a))) |
+           (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(b))) << 16);
+}
+// hi / lo fp16 split of 8 values -> two 16-byte words
+__device__ __forceinline__ void split8(const float (&x)[8], uint4& hi, uint4& lo) {
+    float h[8], l[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        h[i] = __half2float(__float2half_rn(x[i]));
+        l[i] = x[i] - h[i];
+    }
+    hi = make_uint4(pack_h2(h[0], h[1]), pack_h2(h[2], h[3]), pack_h2(h[4], h[5]), pack_h2(h[6], h[7]));
+    lo = make_uint4(pack_h2(l[0], l[1]), pack_h2(l[2], l[3]), pack_h2(l[4], l[5]), pack_h2(l[6], l[7]));
+}
+
+template <int PH, bool REAL>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    rmul_planes_kernel(const __grid_constant__ CUtensorMap hmap, const __grid_constant__ CUtensorMap lmap,
+                       const __grid_constant__ CUtensorMap vmap, const float* __restrict__ rscale,
+                       float* __restrict__ c_out, int m, int p, int tiles_per_frame, int total_tiles) {
+    using C = PCfg<PH>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024 - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023)) & 1023);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kPStages * C::kStageBytes);
+    uint64_t* full = bars;
+    uint64_t* op_full = bars + kPStages;
+    uint64_t* empty = bars + 2 * kPStages;
+    uint64_t* acc_full = bars + 3 * kPStages;
+    uint64_t* acc_empty = acc_full + kAcc;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + kAcc);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int nk = (2 * m + kPKc - 1) / kPKc;
+    const uint32_t vbytes = REAL ? 32u * p * 4u : static_cast<uint32_t>(p) * 256u;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kPStages; ++s) {
+            mbar_init(smem_u32(&full[s]), 1);
+            mbar_init(smem_u32(&op_full[s]), 2);
+            mbar_init(smem_u32(&empty[s]), 1);
+        }
+        for (int b = 0; b < kAcc; ++b) {
+            mbar_init(smem_u32(&acc_full[b]), 1);
+            mbar_init(smem_u32(&acc_empty[b]), 2);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(C::kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&hmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&lmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vmap)) : "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // TMA producer
+            int g = 0;
+            for (int tile = pair; tile < total_tiles; tile += npairs) {
+                const int frame = tile / tiles_per_frame, rb = tile % tiles_per_frame;
+                const int y = 256 * rb + 128 * static_cast<int>(rank);
+                for (int kc = 0; kc < nk; ++kc, ++g) {
+                    const int s = g % kPStages;
+                    uint8_t* st = smem + s * C::kStageBytes;
+                    mbar_wait(smem_u32(&empty[s]), ((g / kPStages) & 1) ^ 1);
+                    const uint32_t fb = smem_u32(&full[s]);
+                    mbar_arrive_expect_tx(fb, 2 * kABytes + vbytes);
+                    tma_3d(smem_u32(st), &hmap, fb, kPKc * kc, y, frame);
+                    tma_3d(smem_u32(st + C::kOffLo), &lmap, fb, kPKc * kc, y, frame);
+                    if (REAL) tma_3d(smem_u32(st + C::kOffV), &vmap, fb, 0, 32 * kc, frame);
+                    else tma_3d(smem_u32(st + C::kOffV), &vmap, fb, kPKc * kc, 0, frame);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (rank == 0 && lane == 0) {  // MMA issuer
+            constexpr uint32_t id1 = idesc_f16(C::kN1), id2 = idesc_f16(C::kN2);
+            int g = 0, t = 0;
+            for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
+                const int b = t % kAcc;
+                mbar_wait_cluster(smem_u32(&acc_empty[b]), ((t / kAcc) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + static_cast<uint32_t>(b * C::kN1);
+                for (int kc = 0; kc < nk; ++kc, ++g) {
+                    const int s = g % kPStages;
+                    mbar_wait_cluster(smem_u32(&op_full[s]), (g / kPStages) & 1);
+                    tc_fence_after();
+                    const uint32_t st = smem_u32(smem + s * C::kStageBytes);
+#pragma unroll
+                    for (int ks = 0; ks < kPKc / 16; ++ks) {
+                        const uint32_t o = 32u * ks;
+                        umma_f16_2sm_(d, desc_sw128(st + o), desc_sw128(st + C::kOffB1 + o), id1,
+                                      (kc > 0 || ks > 0) ? 1u : 0u);
+                        umma_f16_2sm_(d, desc_sw128(st + C::kOffLo + o), desc_sw128(st + C::kOffB2 + o), id2, 1u);
+                    }
+                    umma_commit_mc(smem_u32(&empty[s]));
+                }
+                umma_commit_mc(smem_u32(&acc_full[b]));
+            }
+        }
+    } else if (warp < 6) {
+        // converters: V / Omega chunk -> fp16 hi / lo B^T rows of this CTA
+        const int ct = threadIdx.x - 64;
+        const int bc = ct >> 3, kq = ct & 7;  // B^T row group and 16-byte chunk (4 complex j)
+        int g = 0;
+        for (int tile = pair; tile < total_tiles; tile += npairs) {
+            for (int kc = 0; kc < nk; ++kc, ++g) {
+                const int s = g % kPStages;
+                uint8_t* st = smem + s * C::kStageBytes;
+                mbar_wait(smem_u32(&full[s]), (g / kPStages) & 1);
+#pragma unroll
+                for (int u = 0; u < PH / 16; ++u) {
+                    const int c = bc + 16 * u;
+                    float re[8], im[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) re[i] = im[i] = 0.f;
+                    if (c < p) {
+                        if (REAL) {  // Omega chunk: 32 rows j x p floats
+                            const float* om = reinterpret_cast<const float*>(st + C::kOffV);
+#pragma unroll
+                            for (int w = 0; w < 4; ++w) {
+                                const float o = om[(4 * kq + w) * p + c];
+                                re[2 * w] = o;
+                                im[2 * w + 1] = o;
+                            }
+                        } else {  // V chunk: p rows c x 32 complex j
+                            const float4* vr = reinterpret_cast<const float4*>(st + C::kOffV + c * 256 + kq * 32);
+                            const float4 a = vr[0], b = vr[1];
+                            const float vv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+                            for (int w = 0; w < 4; ++w) {
+                                re[2 * w] = vv[2 * w];
+                                re[2 * w + 1] = -vv[2 * w + 1];
+                                im[2 * w] = vv[2 * w + 1];
+                                im[2 * w + 1] = vv[2 * w];
+                            }
+                        }
+                    }
+                    uint4 reh, rel, imh, iml;
+                    split8(re, reh, rel);
+                    split8(im, imh, iml);
+                    const int sw = (kq ^ (c & 7)) << 4;  // rows c and PH + c share (c & 7)
+                    uint8_t* b1 = st + C::kOffB1;
+                    uint8_t* b2 = st + C::kOffB2;
+                    if (rank == 0) {
+                        *reinterpret_cast<uint4*>(b1 + c * 128 + sw) = reh;
+                        *reinterpret_cast<uint4*>(b1 + (PH + c) * 128 + sw) = imh;
+                        *reinterpret_cast<uint4*>(b2 + c * 128 + sw) = reh;
+                    } else {
+                        *reinterpret_cast<uint4*>(b1 + c * 128 + sw) = rel;
+                        *reinterpret_cast<uint4*>(b1 + (PH + c) * 128 + sw) = iml;
+                        *reinterpret_cast<uint4*>(b2 + c * 128 + sw) = imh;
+                    }
+                }
+                fence_proxy_async();
+                named_bar_sync(1, 128);
+                if (ct == 0) {
+                    if (rank == 0) mbar_arrive_local(smem_u32(&op_full[s]));
+                    else mbar_arrive_cluster(smem_u32(&op_full[s]), 0);
+                }
+            }
+        }
+    } else {
+        // epilogue: C = s_f (D_hi + D_lo), column-major p x M complex
+        const int quarter = warp & 3;
+        int t = 0;
+        for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
+            const int frame = tile / tiles_per_frame, rb = tile % tiles_per_frame;
+            const int b = t % kAcc;
+            mbar_wait(smem_u32(&acc_full[b]), (t / kAcc) & 1);
+            tc_fence_after();
+            const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + static_cast<uint32_t>(b * C::kN1);
+            uint32_t v[C::kN1];
+#pragma unroll
+            for (int h = 0; h < C::kN1 / 32; ++h) {
+                uint32_t (&vh)[32] = *reinterpret_cast<uint32_t(*)[32]>(v + 32 * h);
+                tmem_ld32(taddr + 32 * h, vh);
+            }
+            tmem_wait_ld();
+            tc_fence_before();
+            named_bar_sync(2, 128);
+            if (warp == 6 && lane == 0) {
+                if (rank == 0) mbar_arrive_local(smem_u32(&acc_empty[b]));
+                else mbar_arrive_cluster(smem_u32(&acc_empty[b]), 0);
+            }
+            const float sf = rscale[frame];
+            const int row = 256 * rb + 128 * static_cast<int>(rank) + 32 * quarter + lane;
+            if (row < m) {
+                float2* cf = reinterpret_cast<float2*>(c_out) + static_cast<size_t>(frame) * m * p;
+#pragma unroll
+                for (int c = 0; c < PH; ++c)
+                    if (c < p)
+                        cf[static_cast<size_t>(c) * m + row] =
+                            make_float2(sf * (__uint_as_float(v[c]) + __uint_as_float(v[2 * PH + c])),
+                                        sf * (__uint_as_float(v[PH + c]) + __uint_as_float(v[3 * PH + c])));
+            }
+        }
+    }
+    __syncthreads();
+    cluster_sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols));
+    }
+}
+
 }  // namespace rmtc
 }  // namespace fmk
 
@@ -363,4 +613,66 @@ extern "C" int32_t fm_debug_rmul_tc(const float* d_r, const float* d_omega, cons
     cudaError_t e = fm_launch_rmul_tc(d_r, d_omega, d_v, d_c, frames, m, p, nullptr);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     return static_cast<int32_t>(e);
+}
+
+// C = R V / C = R Omega from the fp16 hi / lo planes of R / s_f (M <= 256, M even, p % 4 == 0, p <= 32).
+cudaError_t fm_launch_rmul_planes(const void* planes_hi, const void* planes_lo, const float* d_scale,
+                                  const float* d_omega, const float* d_v, float* d_c, int64_t frames, int64_t m,
+                                  int64_t p, cudaStream_t stream) {
+    using namespace fmk::rmtc;
+    if (frames < 1 || m < 2 || (m & 1) || m > 256 || p < 4 || p > 32 || (p & 3) || (!d_omega == !d_v))
+        return cudaErrorInvalidValue;
+    auto enc = fmk::tc::get_encode();
+    if (!enc) return cudaErrorNotSupported;
+    CUtensorMap hmap, lmap, vmap;
+    cuuint32_t estr[3] = {1, 1, 1};
+    {
+        cuuint64_t dims[3] = {static_cast<cuuint64_t>(2 * m), static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(frames)};
+        cuuint64_t strides[2] = {static_cast<cuuint64_t>(4 * m), static_cast<cuuint64_t>(4 * m * m)};
+        cuuint32_t box[3] = {kPKc, kRows, 1};
+        if (enc(&hmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(planes_hi), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+            enc(&lmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(planes_lo), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    if (d_omega) {  // Omega: {p, m, frames}, box {p, 32, 1}
+        cuuint64_t dims[3] = {static_cast<cuuint64_t>(p), static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(frames)};
+        cuuint64_t strides[2] = {static_cast<cuuint64_t>(4 * p), static_cast<cuuint64_t>(4 * p * m)};
+        cuuint32_t box[3] = {static_cast<cuuint32_t>(p), 32, 1};
+        if (enc(&vmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(d_omega), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    } else {  // V: {2m, p, frames}, box {64, p, 1}
+        cuuint64_t dims[3] = {static_cast<cuuint64_t>(2 * m), static_cast<cuuint64_t>(p), static_cast<cuuint64_t>(frames)};
+        cuuint64_t strides[2] = {static_cast<cuuint64_t>(8 * m), static_cast<cuuint64_t>(8 * m * p)};
+        cuuint32_t box[3] = {64, static_cast<cuuint32_t>(p), 1};
+        if (enc(&vmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(d_v), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    const int tiles_per_frame = 1;
+    const int64_t tiles = frames;
+    static int sm_count = 0;
+    if (!sm_count) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t pairs = std::min<int64_t>(tiles, std::max(1, sm_count / 2));
+    const dim3 grid(static_cast<unsigned>(2 * pairs));
+    auto go = [&](auto kern, int smem) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kThreads, smem, stream>>>(hmap, lmap, vmap, d_scale, d_c, static_cast<int>(m), static_cast<int>(p),
+                                               tiles_per_frame, static_cast<int>(tiles));
+        return cudaGetLastError();
+    };
+    if (p <= 16)
+        return d_omega ? go(rmul_planes_kernel<16, true>, PCfg<16>::kSmem) : go(rmul_planes_kernel<16, false>, PCfg<16>::kSmem);
+    return d_omega ? go(rmul_planes_kernel<32, true>, PCfg<32>::kSmem) : go(rmul_planes_kernel<32, false>, PCfg<32>::kSmem);
 }
