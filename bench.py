@@ -245,7 +245,7 @@ def run_ours(args):
         idx = torch.from_numpy(fm.draw_indices_batch(dseeds, M, P)).to(dev)
     xd = xh.to(dev)
     plan = fm.BatchPlan(M, N, K, cfgd["method"], p=P, t=cfgd["t"], grid_size=L, max_frames=B, device=local)
-    nsub = args.subbatches if args.subbatches > 0 else (4 if B >= 512 else 1)
+    nsub = args.subbatches if args.subbatches > 0 else (2 if B >= 512 else 1)
     plan.set_concurrency(nsub)
     fsub = (B + nsub - 1) // nsub  # frames in sub-batch 0 (the one the stage events time)
     out = plan.outputs(B, spectrum=True)
