@@ -35,15 +35,16 @@ namespace cov {
 
 constexpr int kRows = 128;          // rows of X per CTA (half of the UMMA M=256 tile)
 constexpr int kChunk = 16;          // complex snapshots per pipeline stage (one UMMA K-slice)
-constexpr int kStagesS = 3;         // fp32 staging ring (TMA destination)
-constexpr int kStagesO = 3;         // fp16 operand ring (UMMA source)
+constexpr int kStagesS = 3;         // fp32 staging ring (TMA destination), general tiles (A and B sides)
+constexpr int kStagesO = 3;         // fp16 operand ring (UMMA source), general tiles
+constexpr int kMaxStages = 6;       // diagonal-only launches (M <= 256): half-size stages, twice as many
 constexpr int kStageBytes = kRows * kChunk * 8;   // 16 KB fp32 per operand side
 constexpr int kPlaneBytes = kRows * kChunk * 2;   // 4 KB fp16 per plane (Re or Im)
 constexpr int kOpBytes = 2 * kPlaneBytes;         // 8 KB per operand side
 constexpr int kThreads = 320;                     // w0 TMA, w1 MMA, w2..w5 convert, w6..w9 epilogue
 constexpr int kSmemStaging = kStagesS * 2 * kStageBytes;
 constexpr int kSmemOperand = kStagesO * 2 * kOpBytes;
-constexpr int kSmemBarriers = 256;
+constexpr int kSmemBarriers = 512;  // 4 x 6 ring barriers + acc + exchange slots + tmem slot (256 used)
 constexpr int kEpiLd = 33;                                  // padded row (float2) of the transpose tile
 constexpr int kEpiChunk = 4096;                             // 32 rows x 16 complex fp32 (one TMA store box)
 constexpr int kEpiWarpBytes = 4 * kEpiChunk;                // [diag buf0 | diag buf1 | mirror buf0 | mirror buf1]
@@ -149,10 +150,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint8_t* epi_bytes = operand + kSmemOperand;  // 1024-aligned (128B-swizzled TMA store boxes)
     uint64_t* bars = reinterpret_cast<uint64_t*>(epi_bytes + kSmemEpilogue);
     uint64_t* stage_full = bars;
-    uint64_t* stage_empty = bars + kStagesS;
-    uint64_t* op_full = bars + 2 * kStagesS;
-    uint64_t* op_empty = bars + 2 * kStagesS + kStagesO;
-    uint64_t* acc_full = bars + 2 * kStagesS + 2 * kStagesO;
+    uint64_t* stage_empty = bars + kMaxStages;
+    uint64_t* op_full = bars + 2 * kMaxStages;
+    uint64_t* op_empty = bars + 3 * kMaxStages;
+    uint64_t* acc_full = bars + 4 * kMaxStages;
     uint64_t* acc_empty = acc_full + 1;
     uint64_t* xch_bar = acc_empty + 1;                             // [2] peer's diagonal max arrived
     float* xch_val = reinterpret_cast<float*>(xch_bar + 2);         // [2] peer's diagonal max
@@ -167,13 +168,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int pair = blockIdx.x >> 1;
     const int npairs = gridDim.x >> 1;
     const int nk = (n + kChunk - 1) / kChunk;
+    // ring geometry: diagonal-only launches (one tile per frame) use half-size stages, twice as many
+    const bool diag_only = tiles_per_frame == 1;
+    const int nS = diag_only ? kMaxStages : kStagesS, nO = diag_only ? kMaxStages : kStagesO;
+    const int sStride = diag_only ? kStageBytes : 2 * kStageBytes, oStride = diag_only ? kOpBytes : 2 * kOpBytes;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStagesS; ++s) {
+        for (int s = 0; s < kMaxStages; ++s) {
             mbar_init(smem_u32(&stage_full[s]), 1);
             mbar_init(smem_u32(&stage_empty[s]), 1);
         }
-        for (int s = 0; s < kStagesO; ++s) {
+        for (int s = 0; s < kMaxStages; ++s) {
             mbar_init(smem_u32(&op_full[s]), 2);  // one arrive per CTA (leader's copy used)
             mbar_init(smem_u32(&op_empty[s]), 1);
         }
@@ -214,11 +219,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int ya = frame * m + 256 * bi + 128 * static_cast<int>(rank);
                 const int yb = frame * m + 256 * bj + 128 * static_cast<int>(rank);
                 for (int kc = 0; kc < nk; ++kc, ++g) {
-                    const int s = g % kStagesS;
-                    mbar_wait(smem_u32(&stage_empty[s]), ((g / kStagesS) & 1) ^ 1);
+                    const int s = g % nS;
+                    mbar_wait(smem_u32(&stage_empty[s]), ((g / nS) & 1) ^ 1);
                     const uint32_t full = smem_u32(&stage_full[s]);
                     mbar_arrive_expect_tx(full, bytes);
-                    uint8_t* st = staging + s * 2 * kStageBytes;
+                    uint8_t* st = staging + s * sStride;
                     const int x = 2 * kChunk * kc;
                     tma_load_2d(smem_u32(st), &xmap, full, x, ya);
                     if (!diag) tma_load_2d(smem_u32(st + kStageBytes), &xmap, full, x, yb);
@@ -238,10 +243,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 mbar_wait_cluster(smem_u32(acc_empty), (t & 1) ^ 1);  // both epilogues drained TMEM
                 tc_fence_after();
                 for (int kc = 0; kc < nk; ++kc, ++g) {
-                    const int o = g % kStagesO;
-                    mbar_wait_cluster(smem_u32(&op_full[o]), (g / kStagesO) & 1);
+                    const int o = g % nO;
+                    mbar_wait_cluster(smem_u32(&op_full[o]), (g / nO) & 1);
                     tc_fence_after();
-                    const uint32_t a = smem_u32(operand + o * 2 * kOpBytes);
+                    const uint32_t a = smem_u32(operand + o * oStride);
                     const uint32_t b = diag ? a : a + kOpBytes;
                     const uint64_t ar = umma_desc(a), ai = umma_desc(a + kPlaneBytes);
                     const uint64_t br = umma_desc(b), bim = umma_desc(b + kPlaneBytes);
@@ -269,12 +274,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             float amax = 0.f;
             bool nonfinite = false;
             for (int kc = 0; kc < nk; ++kc, ++g) {
-                const int s = g % kStagesS;
-                const int o = g % kStagesO;
-                mbar_wait(smem_u32(&stage_full[s]), (g / kStagesS) & 1);
-                mbar_wait(smem_u32(&op_empty[o]), ((g / kStagesO) & 1) ^ 1);
-                const uint8_t* st = staging + s * 2 * kStageBytes;
-                uint8_t* op = operand + o * 2 * kOpBytes;
+                const int s = g % nS;
+                const int o = g % nO;
+                mbar_wait(smem_u32(&stage_full[s]), (g / nS) & 1);
+                mbar_wait(smem_u32(&op_empty[o]), ((g / nO) & 1) ^ 1);
+                const uint8_t* st = staging + s * sStride;
+                uint8_t* op = operand + o * oStride;
                 convert_tile(st, op, cw, lane, row_a, m, amax, nonfinite);
                 if (!diag) convert_tile(st + kStageBytes, op + kOpBytes, cw, lane, row_b, m, amax, nonfinite);
                 fence_proxy_async();
