@@ -1311,8 +1311,11 @@ __global__ void __launch_bounds__(32 * PivCfg<PC>::kWarps)
         }
         if (lane < p) L[k * p + lane] = li;
         __syncwarp();
-        if (lane < p && !done) {  // A(i, j) -= l_i conj(l_j) over live j
-            for (int j = 0; j < p; ++j) {
+        uint32_t live = __ballot_sync(0xffffffffu, lane < p && !done);
+        if (lane < p && !done) {  // A(i, j) -= l_i conj(l_j) over live columns only
+            while (live) {
+                const int j = __ffs(live) - 1;
+                live &= live - 1;
                 const c64 lj = L[k * p + j];
                 c64 a = A[j * p + lane];
                 a.re -= li.re * lj.re + li.im * lj.im;
