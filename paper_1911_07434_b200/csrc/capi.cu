@@ -24,7 +24,7 @@
 // ------------------------------------------------------------------ kernel launchers (other TUs)
 cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, int64_t frames, int64_t m, int64_t n,
                              cudaStream_t stream, void* planes_hi = nullptr, void* planes_lo = nullptr,
-                             float* scale = nullptr);
+                             float* scale = nullptr, int64_t n_true = 0);
 template <typename T>
 cudaError_t fm_launch_rmul(const void*, const void*, const void*, void*, const int32_t*, int, int, int, bool,
                            cudaStream_t);
@@ -99,6 +99,16 @@ namespace {
 __global__ void k_clear_bits(int32_t* status, int frames, int32_t bits) {
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
     if (f < frames) status[f] &= ~bits;
+}
+
+// Odd N: rows of X (N complex) -> rows of N + 1 complex with a zero last snapshot (the TMA row pitch of
+// the covariance kernel must be a multiple of 16 bytes; a zero snapshot adds nothing to X X^H).
+__global__ void k_pad_rows(const float2* __restrict__ x, float2* __restrict__ xp, int64_t rows, int n) {
+    const int64_t row = blockIdx.x;
+    if (row >= rows) return;
+    const float2* src = x + row * n;
+    float2* dst = xp + row * (n + 1);
+    for (int j = threadIdx.x; j <= n; j += blockDim.x) dst[j] = j < n ? src[j] : make_float2(0.f, 0.f);
 }
 
 // Exact method, certification of the subspace iteration (run_post_cov): U (complex128, K x M
@@ -386,6 +396,7 @@ struct fm_plan_s {
     double* spec64 = nullptr; // frames x L (fp64 spectrum for peak picking)
     double* zgrid = nullptr;  // L complex128
     int32_t* scratch_status = nullptr;  // frames
+    float* x_pad = nullptr;             // odd N: frames x M x (N + 1) complex64
     float* rscale = nullptr;            // frames: s_f of the fp16 hi/lo R planes (plane mode)
     bool last_planes = false;           // R of the last run is stored as planes (fm_rerun_frames)
     // exact method via certified subspace iteration (pe > 0): plan-owned Omega, R U product, gap
@@ -467,7 +478,7 @@ static int exact_fast_p(const fm_plan_desc& d) {
 static fm_status validate_desc(const fm_plan_desc* d) {
     if (!d) return fail(FM_EINVAL, "fm_plan_create: null descriptor");
     if (d->m < 2) return fail(FM_EINVAL, "plan: need M >= 2");
-    if (d->n < 2 || (d->n & 1)) return fail(FM_EINVAL, "plan: need even N >= 2 (TMA row stride)");
+    if (d->n < 1) return fail(FM_EINVAL, "plan: need N >= 1");
     const char* who = d->method == FM_METHOD_FAST2 ? "fast_music_2" : d->method == FM_METHOD_FAST1 ? "fast_music_1"
                                                                                                  : "exact_signal_subspace";
     if (d->k < 1 || d->k >= d->m) return fail(FM_EINVAL, std::string(who) + ": need 1 <= K < M");
@@ -519,6 +530,7 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
     chk(pl->get(&pl->zgrid, L * 2));
     chk(pl->get(&pl->scratch_status, B));
     chk(pl->get(&pl->rscale, B));
+    if (desc->n & 1) chk(pl->get(&pl->x_pad, B * M * (static_cast<size_t>(desc->n) + 1) * 2));
     if (pl->pe > 0) {
         chk(pl->get(&pl->omega_e, B * M * pl->pe));
         chk(pl->get(&pl->u32, B * K * M * 2));
@@ -625,7 +637,7 @@ static bool split_final() {  // FM_FUSED_FINAL=1 selects the single-kernel k_fin
 extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
     if (!plan) return 0;
     const int t = plan->d.t;
-    int n = 1 /*cov*/ + 1 /*clear*/ + 3 /*autocorr, spectrum, peaks*/;
+    int n = 1 /*cov*/ + 1 /*clear*/ + 3 /*autocorr, spectrum, peaks*/ + (plan->x_pad ? 1 : 0) /*odd-N pad*/;
     const bool tiled = plan->d.p <= 32 && (plan->d.p % 4) == 0;
     const int fin = tiled ? (split_final() ? 3 : 1) : 2;  // gram, small-warp, basis | fused | cholqr, nystrom
     const int orth = tiled && split_final() ? 3 : 1;  // gram, pivoted chol, rows solve | fused
@@ -865,11 +877,21 @@ extern "C" fm_status fm_run_batch(fm_plan pl, int64_t frames, const fm_batch_io*
     const int nsub = auto_subbatches(pl, frames);
     const bool planes = plane_mode(pl) && !io->covariance;
     pl->last_planes = planes;
+    const int64_t nx = pl->x_pad ? pl->d.n + 1 : pl->d.n;  // row length fed to the covariance kernel
+    auto xin = [&](const float* x, int64_t f0, int64_t nf, cudaStream_t q) -> const float* {
+        if (!pl->x_pad) return x;
+        float* xp = pl->x_pad + f0 * pl->d.m * nx * 2;
+        k_pad_rows<<<static_cast<unsigned>(nf * pl->d.m), 128, 0, q>>>(reinterpret_cast<const float2*>(x),
+                                                                      reinterpret_cast<float2*>(xp), nf * pl->d.m,
+                                                                      static_cast<int>(pl->d.n));
+        return xp;
+    };
     if (nsub <= 1) {
         float* R = io->covariance ? io->covariance : pl->R;
         const Planes pv = planes ? planes_view(pl, 0) : Planes{};
         mark(pl, 0, s);
-        FM_LAUNCH(fm_launch_cov_tc(io->x, R, io->status, frames, pl->d.m, pl->d.n, s, pv.hi, pv.lo, pv.scale));
+        FM_LAUNCH(fm_launch_cov_tc(xin(io->x, 0, frames, s), R, io->status, frames, pl->d.m, nx, s, pv.hi, pv.lo,
+                                   pv.scale, pl->d.n));
         mark(pl, 1, s);
         return run_post_cov(pl, frames, io, R, s, work_view(pl, 0), true, pv);
     }
@@ -898,7 +920,8 @@ extern "C" fm_status fm_run_batch(fm_plan pl, int64_t frames, const fm_batch_io*
         if (i == 0) mark(pl, 0, q);
         {
             cudaStream_t s = q;  // FM_LAUNCH synchronises `s` in debug mode
-            FM_LAUNCH(fm_launch_cov_tc(o.x, R, o.status, nf, pl->d.m, pl->d.n, q, pv.hi, pv.lo, pv.scale));
+            FM_LAUNCH(fm_launch_cov_tc(xin(o.x, f0, nf, q), R, o.status, nf, pl->d.m, nx, q, pv.hi, pv.lo, pv.scale,
+                                       pl->d.n));
         }
         if (i == 0) mark(pl, 1, q);
         st = run_post_cov(pl, nf, &o, R, q, work_view(pl, f0), i == 0, pv);

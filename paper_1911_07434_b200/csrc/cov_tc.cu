@@ -141,7 +141,8 @@ template <int kEpi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cov_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap rmap,
                   const __grid_constant__ CUtensorMap mmap, float* __restrict__ r_out, int32_t* __restrict__ status,
-                  int m, int n, int tiles_per_frame, int total_tiles, float* __restrict__ rscale) {
+                  int m, int n, int tiles_per_frame, int total_tiles, float* __restrict__ rscale,
+                  float inv_n_true) {
     constexpr bool kTmaStore = kEpi >= 1;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -301,7 +302,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // 2. per 32-column chunk: two tcgen05.ld, x = R/s_f -> hi = fp16(x), lo = fp16(x - hi), two
         //    128B-swizzled 32 x 64-half boxes, two TMA stores (hi plane, lo plane).
         const int quarter = warp & 3;
-        const float inv_n = 1.0f / static_cast<float>(n);
+        const float inv_n = inv_n_true;  // 1 / N of the caller (n may include one zero pad column)
         const uint32_t ebase = smem_u32(epi_bytes) + (warp - 6) * kEpiWarpBytes;
         const uint32_t peer = rank ^ 1u;
         int t = 0, gc = 0;
@@ -408,7 +409,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // bulk groups). TMEM is released as soon as the last chunk is in smem, so the global writes
         // overlap the next tile's mainloop. Off-diagonal tiles also store the conj-transposed block.
         const int quarter = warp & 3;
-        const float inv_n = 1.0f / static_cast<float>(n);
+        const float inv_n = inv_n_true;  // 1 / N of the caller (n may include one zero pad column)
         const uint32_t ebase = smem_u32(epi_bytes) + (warp - 6) * kEpiWarpBytes;
         int t = 0, gc = 0;
         for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
@@ -465,7 +466,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // ---------------- epilogue, generic-store fallback (odd M: row pitch not 16-byte aligned)
         const int quarter = warp & 3;
         const int row = 32 * quarter + lane;
-        const float inv_n = 1.0f / static_cast<float>(n);
+        const float inv_n = inv_n_true;  // 1 / N of the caller (n may include one zero pad column)
         int t = 0;
         for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
             const int frame = tile / tiles_per_frame;
@@ -533,7 +534,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // planes_hi != nullptr selects the fp16 hi/lo plane output (M <= 256, M even): planes_hi / planes_lo
 // are frames x M x 2M halves (R / s_f interleaved re, im), scale[f] = s_f; d_r is unused then.
 cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, int64_t frames, int64_t m, int64_t n,
-                             cudaStream_t stream, void* planes_hi, void* planes_lo, float* scale) {
+                             cudaStream_t stream, void* planes_hi, void* planes_lo, float* scale, int64_t n_true) {
+    if (n_true <= 0) n_true = n;  // n: row length of d_x (even); n_true: snapshots for the 1/N scaling
     using namespace fmk::cov;
     if (frames < 1 || m < 1 || n < 2 || (n & 1) || frames * m > 0x7fffffff || 2 * n > 0x7fffffff)
         return cudaErrorInvalidValue;
@@ -606,7 +608,7 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
     auto go = [&](auto kern) {
         kern<<<grid, kThreads, kSmemBytes, stream>>>(map, rmap, mmap, d_r, d_status, static_cast<int>(m),
                                                      static_cast<int>(n), tiles_per_frame, static_cast<int>(tiles),
-                                                     scale);
+                                                     scale, static_cast<float>(1.0 / static_cast<double>(n_true)));
     };
     if (epi == 2) go(cov_tc_kernel<2>);
     else if (epi == 1) go(cov_tc_kernel<1>);

@@ -46,7 +46,7 @@ def _ragged_cfg(oracle, m, n, k, p=8, t=1, grid=721, seed=11):
 
 # odd M (generic-store epilogue), M % 32 != 0 (clipped TMA store boxes), M > 256 (off-diagonal
 # tiles + mirrored conj-transposed blocks), N < M (rank-deficient R).
-@pytest.mark.parametrize("m,n", [(37, 64), (100, 30), (300, 40), (520, 96), (64, 2)])
+@pytest.mark.parametrize("m,n", [(37, 64), (100, 30), (300, 40), (520, 96), (64, 2), (37, 51), (64, 1), (256, 129)])
 def test_covariance_ragged_shapes(fm, oracle, m, n):
     cfg = _ragged_cfg(oracle, m, n, 2)
     frames = [0, 1, 2]
@@ -63,7 +63,7 @@ def test_covariance_ragged_shapes(fm, oracle, m, n):
         assert np.array_equal(got, got.conj().T) or np.max(np.abs(got - got.conj().T)) <= 1e-6 * np.abs(ref).max()
 
 
-@pytest.mark.parametrize("m,n,k", [(37, 80, 2), (300, 400, 4)])
+@pytest.mark.parametrize("m,n,k", [(37, 80, 2), (300, 400, 4), (64, 101, 3)])
 def test_pipeline_parity_ragged(fm, oracle, m, n, k):
     cfg = _ragged_cfg(oracle, m, n, k)
     frames = [0, 1, 2, 3]
