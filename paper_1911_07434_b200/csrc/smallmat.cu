@@ -452,7 +452,9 @@ __device__ void tiled_gram2(const T1* __restrict__ X1, bool herm1, const T1* __r
     (void)Y2;
     const int nb = p >> 2;
     const int t1 = nb * (nb + 1) / 2;
-    const int t2 = X2 ? nb * nb : 0;
+    // X2^H X1 is only used as H = V^H R V (Hermitian in exact arithmetic, symmetrised by the callers):
+    // both products use the upper-triangle 4x4 tiles and mirror the strictly upper blocks
+    const int t2 = X2 ? nb * (nb + 1) / 2 : 0;
     const int ntiles = t1 + t2;
     const int ld = p + 1;
     c64* sX1 = stage;
@@ -485,8 +487,9 @@ __device__ void tiled_gram2(const T1* __restrict__ X1, bool herm1, const T1* __r
                 while (rem >= nb - ti) { rem -= nb - ti; ++ti; }
                 tj = ti + rem;
             } else {
-                ti = (tile - t1) % nb;
-                tj = (tile - t1) / nb;
+                int rem = tile - t1;
+                while (rem >= nb - ti) { rem -= nb - ti; ++ti; }
+                tj = ti + rem;
             }
         }
         c64 acc[4][4];
@@ -545,7 +548,7 @@ __device__ void tiled_gram2(const T1* __restrict__ X1, bool herm1, const T1* __r
                 for (int b = 0; b < 4; ++b) {
                     const int i = 4 * ti + a, j = 4 * tj + b;
                     G[j * p + i] = acc[a][b];
-                    if (!second && ti != tj) G[i * p + j] = conj(acc[a][b]);
+                    if (ti != tj) G[i * p + j] = conj(acc[a][b]);
                 }
         }
     }
