@@ -1005,6 +1005,42 @@ __device__ __forceinline__ void warp_chol_lower(c64* A, int p, double& dmin, dou
     }
 }
 
+// Two independent in-place Cholesky factorisations (p <= 16) by one warp: lanes 0..15 factor A1,
+// lanes 16..31 factor A2, row = lane & 15 (same schedule as warp_chol_lower). Returns A2's pivot range.
+__device__ __forceinline__ void warp_chol_lower_pair(c64* A1, c64* A2, int p, double& dmin2, double& dmax2) {
+    const int lane = threadIdx.x & 31;
+    c64* A = lane < 16 ? A1 : A2;
+    const int row = lane & 15;
+    double dmin = 1e300, dmax = 0.0;
+    for (int k = 0; k < p; ++k) {
+        const double dk = A[k * p + k].re;
+        dmin = fmin(dmin, dk);
+        dmax = fmax(dmax, dk);
+        const double inv = dk > 0.0 ? 1.0 / sqrt(dk) : 0.0;
+        __syncwarp();
+        c64 li = mk(0.0, 0.0);
+        if (row > k && row < p) {
+            const c64 a = A[k * p + row];
+            li = mk(a.re * inv, a.im * inv);
+            A[k * p + row] = li;
+        }
+        if (row == 0) A[k * p + k] = mk(dk > 0.0 ? sqrt(dk) : 0.0, 0.0);
+        __syncwarp();
+        if (row > k && row < p) {
+            for (int j = k + 1; j <= row; ++j) {
+                const c64 lj = A[k * p + j];
+                c64 a = A[j * p + row];
+                a.re -= li.re * lj.re + li.im * lj.im;
+                a.im -= li.im * lj.re - li.re * lj.im;
+                A[j * p + row] = a;
+            }
+        }
+        __syncwarp();
+    }
+    dmin2 = __shfl_sync(0xffffffffu, dmin, 16);
+    dmax2 = __shfl_sync(0xffffffffu, dmax, 16);
+}
+
 template <int PC>
 __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
     k_small_warp(const c64* __restrict__ Gin, const c64* __restrict__ Hin, c64* __restrict__ Tout,
@@ -1032,8 +1068,12 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
     }
     __syncwarp();
     double dmin, dmax;
-    warp_chol_lower(L, p, dmin, dmax);   // G = L L^H, R = L^H: R(i, j) = conj(L[i * p + j]), j >= i
-    warp_chol_lower(LH, p, dmin, dmax);  // H = L_H L_H^H
+    if (PC <= 16) {
+        warp_chol_lower_pair(L, LH, p, dmin, dmax);  // G = L L^H (R = L^H) and H = L_H L_H^H concurrently
+    } else {
+        warp_chol_lower(L, p, dmin, dmax);   // G = L L^H, R = L^H: R(i, j) = conj(L[i * p + j]), j >= i
+        warp_chol_lower(LH, p, dmin, dmax);  // H = L_H L_H^H
+    }
     if (lane == 0 && !(dmin > static_cast<double>(p) * eps_of<float>::value * dmax))
         atomicOr(&status[f], kFrameNoConv);
     for (int e = lane; e < PC * ld; e += 32) Ya[e] = Yb[e] = mk(0.0, 0.0);  // rows >= p stay zero
