@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(kNT) k_spectrum_multi(const c64* __restrict__ 
 // (q0, q0 + qh); the block's kSFPB frames share the two power sequences (fp64 recurrence).
 constexpr int kSFPB = 8;
 
-__global__ void __launch_bounds__(kNT) k_spectrum_sym(const c64* __restrict__ t, const c64* __restrict__ zgrid,
+__global__ void __launch_bounds__(kNT, 2) k_spectrum_sym(const c64* __restrict__ t, const c64* __restrict__ zgrid,
                                                       int frames, int m, int L, float* __restrict__ spec32,
                                                       double* __restrict__ spec64) {
     extern __shared__ c64 st[];  // kSFPB x m coefficients, delta-major
