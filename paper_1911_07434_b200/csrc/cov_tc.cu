@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 
 #include "fm_common.cuh"
@@ -42,6 +43,7 @@ constexpr int kStageBytes = kRows * kChunk * 8;   // 16 KB fp32 per operand side
 constexpr int kPlaneBytes = kRows * kChunk * 2;   // 4 KB fp16 per plane (Re or Im)
 constexpr int kOpBytes = 2 * kPlaneBytes;         // 8 KB per operand side
 constexpr int kThreads = 320;                     // w0 TMA, w1 MMA, w2..w5 convert, w6..w9 epilogue
+constexpr int kThreadsP = 448;                    // plane epilogue: w6..w13, two warps per TMEM lane quarter
 constexpr int kSmemStaging = kStagesS * 2 * kStageBytes;
 constexpr int kSmemOperand = kStagesO * 2 * kOpBytes;
 constexpr int kSmemBarriers = 512;  // 4 x 6 ring barriers + acc + exchange slots + tmem slot (256 used)
@@ -138,11 +140,11 @@ __device__ __forceinline__ void convert_tile(const uint8_t* stage, uint8_t* op, 
 // R / s_f (M <= 256: one tile per frame; s_f = smallest power of two >= max_i R_ii, exchanged between the
 // two CTAs of the pair; rmap / mmap are the hi / lo plane maps, rscale[f] = s_f).
 template <int kEpi>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEpi == 2 ? kThreadsP : kThreads, 1)
     cov_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap rmap,
                   const __grid_constant__ CUtensorMap mmap, float* __restrict__ r_out, int32_t* __restrict__ status,
                   int m, int n, int tiles_per_frame, int total_tiles, float* __restrict__ rscale,
-                  float inv_n_true) {
+                  float inv_n_true, int dbg) {
     constexpr bool kTmaStore = kEpi >= 1;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -252,10 +254,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const uint64_t ar = umma_desc(a), ai = umma_desc(a + kPlaneBytes);
                     const uint64_t br = umma_desc(b), bim = umma_desc(b + kPlaneBytes);
                     const uint32_t acc = kc > 0 ? 1u : 0u;
-                    umma_f16_2sm(tmem + 0, ar, br, id_pos, acc);
-                    umma_f16_2sm(tmem + 0, ai, bim, id_pos, 1u);
-                    umma_f16_2sm(tmem + 256, ai, br, id_pos, acc);
-                    umma_f16_2sm(tmem + 256, ar, bim, id_neg, 1u);
+                    if (!(dbg & 2)) {
+                        umma_f16_2sm(tmem + 0, ar, br, id_pos, acc);
+                        umma_f16_2sm(tmem + 0, ai, bim, id_pos, 1u);
+                        umma_f16_2sm(tmem + 256, ai, br, id_pos, acc);
+                        umma_f16_2sm(tmem + 256, ar, bim, id_neg, 1u);
+                    }
                     umma_commit_mc(smem_u32(&op_empty[o]));
                 }
                 umma_commit_mc(smem_u32(acc_full));
@@ -296,16 +300,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (flag && lane == 0 && status != nullptr) atomicOr(&status[frame], flag);
         }
     } else if (kEpi == 2) {
-        // ---------------- epilogue, fp16 hi/lo planes of R / s_f (M <= 256: tile == frame).
-        // 1. s_f: each thread's diagonal element (TMEM column = its row), CTA max, exchanged with the
-        //    peer CTA through DSMEM + an mbarrier (double-buffered by tile parity).
+        // ---------------- epilogue, fp16 hi/lo planes of R / s_f (M <= 256: tile == frame). Eight warps:
+        // warp w drains TMEM lane quarter (w & 3), columns [128 h, 128 h + 128), h = (w - 6) >> 2.
+        // 1. s_f: the warps whose column half holds their rows' diagonal read it, CTA max, exchange with
+        //    the peer CTA through DSMEM + an mbarrier (double-buffered by tile parity).
         // 2. per 32-column chunk: two tcgen05.ld, x = R/s_f -> hi = fp16(x), lo = fp16(x - hi), two
-        //    128B-swizzled 32 x 64-half boxes, two TMA stores (hi plane, lo plane).
+        //    128B-swizzled 32 x 64-half boxes (single-buffered per warp), two TMA stores.
         const int quarter = warp & 3;
-        const float inv_n = inv_n_true;  // 1 / N of the caller (n may include one zero pad column)
-        const uint32_t ebase = smem_u32(epi_bytes) + (warp - 6) * kEpiWarpBytes;
+        const int half = (warp - 6) >> 2;
+        const float inv_n = inv_n_true;
+        const uint32_t ebase = smem_u32(epi_bytes) + (warp - 6) * (2 * kEpiChunk);
         const uint32_t peer = rank ^ 1u;
-        int t = 0, gc = 0;
+        int t = 0;
         for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
             const int frame = tile;
             const int row0 = 128 * static_cast<int>(rank) + 32 * quarter;
@@ -313,7 +319,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_wait(smem_u32(acc_full), t & 1);
             tc_fence_after();
             const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
-            {
+            if (half == static_cast<int>(rank)) {
                 uint32_t dv[32];
                 tmem_ld32(taddr + row0, dv);
                 tmem_wait_ld();
@@ -327,8 +333,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int o = 16; o > 0; o >>= 1) dg = fmaxf(dg, __shfl_xor_sync(0xffffffffu, dg, o));
                 if (lane == 0) s_wmax[quarter] = dg;
             }
-            named_bar_sync(2, 128);
-            if (warp == 6 && lane == 0) {
+            named_bar_sync(2, 256);
+            if (half == static_cast<int>(rank) && quarter == 0 && lane == 0) {
                 const float cmax = fmaxf(fmaxf(s_wmax[0], s_wmax[1]), fmaxf(s_wmax[2], s_wmax[3]));
                 const uint32_t slot = smem_u32(&xch_val[t & 1]), bar = smem_u32(&xch_bar[t & 1]);
                 asm volatile(
@@ -350,20 +356,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 *s_scale = sc;
                 if (rank == 0) rscale[frame] = sc;
             }
-            named_bar_sync(2, 128);
+            named_bar_sync(2, 256);
             const float mul = inv_n / *s_scale;  // power-of-two divisor: exact
-            const int nchunks = row0 < m ? (m + 31) / 32 : 0;
-            for (int c = 0; c < nchunks; ++c, ++gc) {
-                const int col0 = 32 * c;
+            const int nchunks = (row0 < m && !(dbg & 4)) ? max(0, min(4, (m - 128 * half + 31) / 32)) : 0;
+            for (int c = 0; c < nchunks; ++c) {
+                const int col0 = 128 * half + 32 * c;
                 uint32_t vr[32], vi[32];
                 tmem_ld32(taddr + col0, vr);
                 tmem_ld32(taddr + 256 + col0, vi);
                 tmem_wait_ld();
-                const int b = gc & 1;
-                if (lane == 0) bulk_wait_read1();
+                if (lane == 0) bulk_wait_read0();  // this warp's previous stores have read the boxes
                 __syncwarp();
-                const uint32_t hbuf = ebase + b * kEpiChunk;
-                const uint32_t lbuf = ebase + 2 * kEpiChunk + b * kEpiChunk;
+                const uint32_t hbuf = ebase, lbuf = ebase + kEpiChunk;
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {  // 16-byte chunk q = complex 4q .. 4q + 3 (8 halves)
                     uint32_t hw[4], lw[4];
@@ -395,7 +399,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
             }
             tc_fence_before();
-            named_bar_sync(2, 128);  // all four epilogue warps finished reading TMEM
+            named_bar_sync(2, 256);  // all eight epilogue warps finished reading TMEM
             if (warp == 6 && lane == 0) {
                 if (rank == 0) mbar_arrive_local(smem_u32(acc_empty));
                 else mbar_arrive_cluster(smem_u32(acc_empty), 0);
@@ -526,6 +530,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------- host side
+// Experiment switches (FM_COV_DBG, not for production): 2 = no MMA, 4 = plane epilogue skips its chunks.
+static int dbg_flags() {
+    static const int v = std::getenv("FM_COV_DBG") ? std::atoi(std::getenv("FM_COV_DBG")) : 0;
+    return v;
+}
+
 }  // namespace cov
 }  // namespace fmk
 
@@ -606,9 +616,10 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
     const int64_t pairs = std::min<int64_t>(tiles, std::max(1, sm_count / 2));
     const dim3 grid(static_cast<unsigned>(2 * pairs));
     auto go = [&](auto kern) {
-        kern<<<grid, kThreads, kSmemBytes, stream>>>(map, rmap, mmap, d_r, d_status, static_cast<int>(m),
+        kern<<<grid, epi == 2 ? kThreadsP : kThreads, kSmemBytes, stream>>>(map, rmap, mmap, d_r, d_status, static_cast<int>(m),
                                                      static_cast<int>(n), tiles_per_frame, static_cast<int>(tiles),
-                                                     scale, static_cast<float>(1.0 / static_cast<double>(n_true)));
+                                                     scale, static_cast<float>(1.0 / static_cast<double>(n_true)),
+                                                     dbg_flags());
     };
     if (epi == 2) go(cov_tc_kernel<2>);
     else if (epi == 1) go(cov_tc_kernel<1>);
