@@ -963,9 +963,10 @@ __global__ void __launch_bounds__(kNT, 2) k_gram_gh(const c32* __restrict__ Cin,
 
 template <int PC> struct WarpCfg {
     static constexpr int kLPC = 32 / PC;                   // lanes per column in the Jacobi
-    static constexpr int kWarps = PC <= 16 ? 8 : 3;        // frames per CTA
+    static constexpr int kWarps = PC <= 16 ? 8 : 4;        // frames per CTA
     static constexpr int kLd = PC + ((kLPC - PC) % 8 + 8) % 8;  // ld = LPC (mod 8): conflict-free 16-B rows
-    static constexpr size_t kBytes = sizeof(c64) * (2 * PC * PC + 2 * PC * kLd) + sizeof(double) * PC + sizeof(int) * PC;
+    // L, L_H (reused for T once Y is formed), Y (in-place pair-lane Jacobi)
+    static constexpr size_t kBytes = sizeof(c64) * (2 * PC * PC + PC * kLd) + sizeof(double) * PC + sizeof(int) * PC;
     static constexpr size_t kWarpBytes = (kBytes + 15) / 16 * 16;
 };
 
@@ -1056,8 +1057,7 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
     c64* L = reinterpret_cast<c64*>(dsm + warp * W::kWarpBytes);
     c64* LH = L + PC * PC;
     c64* Ya = LH + PC * PC;
-    c64* Yb = Ya + PC * ld;
-    double* sig = reinterpret_cast<double*>(Yb + PC * ld);
+    double* sig = reinterpret_cast<double*>(Ya + PC * ld);
     int* order = reinterpret_cast<int*>(sig + PC);
     const c64* Gf = Gin + static_cast<size_t>(f) * p * p;
     const c64* Hf = Hin + static_cast<size_t>(f) * p * p;
@@ -1076,7 +1076,7 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
     }
     if (lane == 0 && !(dmin > static_cast<double>(p) * eps_of<float>::value * dmax))
         atomicOr(&status[f], kFrameNoConv);
-    for (int e = lane; e < PC * ld; e += 32) Ya[e] = Yb[e] = mk(0.0, 0.0);  // rows >= p stay zero
+    for (int e = lane; e < PC * ld; e += 32) Ya[e] = mk(0.0, 0.0);  // rows >= p stay zero
     __syncwarp();
     // Y(i, :) solves y L_H^H = R(i, :) (forward substitution, lane per row); Y -> Ya (ld).
     // Reciprocal pivots first; two partial sums per step for a shorter FMA chain.
@@ -1202,7 +1202,7 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
             break;
         }
     }
-    c64* nxt = Yb;
+    c64* nxt = LH;  // free after Y was formed: holds T (p x k, ld = p)
     const int c = lane;
     const long long T2 = clock64();
     // singular values, descending order (ties: lower index first)
@@ -1233,13 +1233,13 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
             acc.im *= inv_s;
             for (int j = i + 1; j < p; ++j) {
                 const c64 rij = conj(L[i * p + j]);
-                const c64 tj = Tm[kk * ld + j];
+                const c64 tj = Tm[kk * p + j];
                 acc.re -= rij.re * tj.re - rij.im * tj.im;
                 acc.im -= rij.re * tj.im + rij.im * tj.re;
             }
             const double rii = L[i * p + i].re;
             const double inv = rii > 0.0 ? 1.0 / rii : 0.0;
-            Tm[kk * ld + i] = mk(acc.re * inv, acc.im * inv);
+            Tm[kk * p + i] = mk(acc.re * inv, acc.im * inv);
         }
         double lam = sig[cc];
         lam *= lam;  // eigenvalue of B' = Y Y^H
@@ -1251,7 +1251,7 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
     }
     __syncwarp();
     c64* Tf = Tout + static_cast<size_t>(f) * p * k;
-    for (int e = lane; e < p * k; e += 32) Tf[e] = Tm[(e / p) * ld + (e % p)];
+    for (int e = lane; e < p * k; e += 32) Tf[e] = Tm[e];  // T stored compactly (ld p) in L_H
     if (lane == 0 && sweeps == 0) atomicOr(&status[f], kFrameNoConv);
     if (lane == 0 && dbg) dbg[f] = sweeps;
     const long long T3 = clock64();
