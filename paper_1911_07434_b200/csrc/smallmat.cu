@@ -30,6 +30,7 @@ constexpr int kNW = kNT / 32;
 constexpr int kRC = 64;   // rows per staged Gram chunk
 constexpr int kRCP = 65;  // padded column stride (conflict-free 16-B column reads)
 __device__ int* g_phase_dbg = nullptr;
+__device__ int g_mixed_jacobi = 1;  // fp32 Jacobi sweeps before the fp64 ones (FM_JACOBI_FP64=1 -> 0)
 
 // G(i, j) = sum_r conj(X_i[r]) Y_j[r] over column-major p x m operands. Threads own entries
 // (HERM: upper triangle, mirrored); rows staged kRC at a time in padded shared memory and
@@ -961,6 +962,8 @@ __global__ void __launch_bounds__(kNT, 2) k_gram_gh(const c32* __restrict__ Cin,
     }
 }
 
+static __device__ __forceinline__ bool mixed_jacobi() { return g_mixed_jacobi != 0; }
+
 template <int PC> struct WarpCfg {
     static constexpr int kLPC = 32 / PC;                   // lanes per column in the Jacobi
     static constexpr int kWarps = PC <= 16 ? 8 : 4;        // frames per CTA
@@ -1125,6 +1128,69 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
     const double tol = 8.0 * 2.220446049250313e-16 * p;
     c64* cur = Ya;
     int sweeps = 0;
+    // Phase 1 (fp32): sweeps on a complex64 copy of Y (in the L_H region, free until T is formed) until
+    // every rotated pair has |g| / sqrt(al be) < 1e-6; the fp64 phase below then restores exact column
+    // orthogonality (the fp32 rotations perturb Y by ~1e-6 relative, far inside the error budget of the
+    // fp16-operand covariance). FM_JACOBI_FP64=1 skips this phase.
+    if (mixed_jacobi()) {
+        c32* y32 = reinterpret_cast<c32*>(LH);
+        for (int e = lane; e < PC * ld; e += 32) y32[e] = mk(static_cast<float>(Ya[e].re), static_cast<float>(Ya[e].im));
+        __syncwarp();
+        const float tol32 = 1e-6f;
+        for (int sweep = 0; sweep < 12; ++sweep) {
+            bool rot_any = false;
+            for (int rnd = 0; rnd < n1; ++rnd) {
+                int i = rnd + slot, j = rnd - slot;
+                if (i >= n1) i -= n1;
+                if (j < 0) j += n1;
+                if (slot == 0) j = n1;
+                const int lo = act ? min(i, j) : 0, hi = act ? max(i, j) : 0;
+                c32* xlo = y32 + lo * ld + sub;
+                c32* xhi = y32 + hi * ld + sub;
+                c32 x[RPL], y[RPL];
+                float al = 0.f, be = 0.f;
+                c32 ga = mk(0.f, 0.f);
+#pragma unroll
+                for (int t = 0; t < RPL; ++t) {
+                    x[t] = xlo[t * LPP];
+                    y[t] = xhi[t * LPP];
+                    al = fmaf(x[t].re, x[t].re, fmaf(x[t].im, x[t].im, al));
+                    be = fmaf(y[t].re, y[t].re, fmaf(y[t].im, y[t].im, be));
+                    cmac_conj(ga, x[t], y[t]);
+                }
+#pragma unroll
+                for (int o = 1; o < LPP; o <<= 1) {
+                    al += __shfl_xor_sync(0xffffffffu, al, o);
+                    be += __shfl_xor_sync(0xffffffffu, be, o);
+                    ga.re += __shfl_xor_sync(0xffffffffu, ga.re, o);
+                    ga.im += __shfl_xor_sync(0xffffffffu, ga.im, o);
+                }
+                const float g2 = ga.re * ga.re + ga.im * ga.im;
+                const bool rotate = act && (g2 > tol32 * tol32 * al * be) && g2 > 0.f;
+                if (rotate) {
+                    const float ig = rsqrtf(g2);
+                    const float zeta = (be - al) * (0.5f * ig);
+                    const float tf = copysignf(1.0f, zeta) / (fabsf(zeta) + sqrtf(fmaf(zeta, zeta, 1.0f)));
+                    const float cs = rsqrtf(fmaf(tf, tf, 1.0f));
+                    const float sn = cs * tf;
+                    const c32 se = mk(sn * ga.re * ig, sn * ga.im * ig);
+#pragma unroll
+                    for (int t2 = 0; t2 < RPL; ++t2) {
+                        const c32 u = x[t2], v = y[t2];
+                        xlo[t2 * LPP] = mk(fmaf(cs, u.re, -fmaf(se.re, v.re, se.im * v.im)),
+                                           fmaf(cs, u.im, -fmaf(se.re, v.im, -se.im * v.re)));
+                        xhi[t2 * LPP] = mk(fmaf(cs, v.re, fmaf(se.re, u.re, -se.im * u.im)),
+                                           fmaf(cs, v.im, fmaf(se.re, u.im, se.im * u.re)));
+                    }
+                }
+                rot_any |= rotate;
+                __syncwarp();
+            }
+            if (!__any_sync(0xffffffffu, rot_any)) break;
+        }
+        for (int e = lane; e < PC * ld; e += 32) Ya[e] = to64(y32[e]);
+        __syncwarp();
+    }
     for (int sweep = 0; sweep < 40; ++sweep) {
         bool rot_any = false;
         bool big = false;  // some rotation of this sweep had |g|^2 >= 1e-14 al be
@@ -1558,6 +1624,12 @@ cudaError_t fm_launch_final_split(const void* C, const void* V, void* Hw, void* 
                                                           static_cast<c64*>(basis), m, p, k);
         return cudaGetLastError();
     };
+    static const bool init_mixed = [] {
+        const int v = std::getenv("FM_JACOBI_FP64") ? 0 : 1;
+        cudaMemcpyToSymbol(smb::g_mixed_jacobi, &v, sizeof(v));
+        return true;
+    }();
+    (void)init_mixed;
     using namespace smb;
     if (p <= 8)
         return go(k_gram_gh<8>, k_small_warp<8>, k_basis_ct<8>, 8, WarpCfg<8>::kWarps, WarpCfg<8>::kWarpBytes);
