@@ -996,13 +996,26 @@ __device__ __forceinline__ void warp_chol_lower(c64* A, int p, double& dmin, dou
         }
         if (lane == 0) A[k * p + k] = mk(dk > 0.0 ? sqrt(dk) : 0.0, 0.0);
         __syncwarp();
-        if (lane > k && lane < p) {
-            for (int j = k + 1; j <= lane; ++j) {
-                const c64 lj = A[k * p + j];
-                c64 a = A[j * p + lane];
-                a.re -= li.re * lj.re + li.im * lj.im;  // li * conj(lj)
-                a.im -= li.im * lj.re - li.re * lj.im;
-                A[j * p + lane] = a;
+        if (lane > k && lane < p) {  // batches of 8: all loads before the stores
+            for (int j0 = k + 1; j0 <= lane; j0 += 8) {
+                c64 lj[8], a[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int j = j0 + u;
+                    if (j <= lane) {
+                        lj[u] = A[k * p + j];
+                        a[u] = A[j * p + lane];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int j = j0 + u;
+                    if (j <= lane) {
+                        a[u].re -= li.re * lj[u].re + li.im * lj[u].im;  // li * conj(lj)
+                        a[u].im -= li.im * lj[u].re - li.re * lj[u].im;
+                        A[j * p + lane] = a[u];
+                    }
+                }
             }
         }
         __syncwarp();
@@ -1065,9 +1078,24 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
     const c64* Gf = Gin + static_cast<size_t>(f) * p * p;
     const c64* Hf = Hin + static_cast<size_t>(f) * p * p;
     const long long T0 = clock64();
-    for (int e = lane; e < p * p; e += 32) {
-        L[e] = Gf[e];
-        LH[e] = Hf[e];
+    for (int e0 = 0; e0 < p * p; e0 += 8 * 32) {  // 16 loads in flight per lane
+        c64 g[8], hh[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + lane + 32 * u;
+            if (e < p * p) {
+                g[u] = Gf[e];
+                hh[u] = Hf[e];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + lane + 32 * u;
+            if (e < p * p) {
+                L[e] = g[u];
+                LH[e] = hh[u];
+            }
+        }
     }
     __syncwarp();
     double dmin, dmax;
@@ -1430,14 +1458,30 @@ __global__ void __launch_bounds__(32 * PivCfg<PC>::kWarps)
         __syncwarp();
         uint32_t live = __ballot_sync(0xffffffffu, lane < p && !done);
         if (lane < p && !done) {  // A(i, j) -= l_i conj(l_j) over live columns only
-            while (live) {
-                const int j = __ffs(live) - 1;
-                live &= live - 1;
-                const c64 lj = L[k * p + j];
-                c64 a = A[j * p + lane];
-                a.re -= li.re * lj.re + li.im * lj.im;
-                a.im -= li.im * lj.re - li.re * lj.im;
-                A[j * p + lane] = a;
+            while (live) {  // batches of up to 8 live columns: loads first, then stores
+                int js[8];
+                c64 lj[8], a[8];
+                int cnt = 0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    js[u] = live ? __ffs(live) - 1 : -1;
+                    if (live) live &= live - 1;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (js[u] >= 0) {
+                        lj[u] = L[k * p + js[u]];
+                        a[u] = A[js[u] * p + lane];
+                        ++cnt;
+                    }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (js[u] >= 0) {
+                        a[u].re -= li.re * lj[u].re + li.im * lj[u].im;
+                        a[u].im -= li.im * lj[u].re - li.re * lj[u].im;
+                        A[js[u] * p + lane] = a[u];
+                    }
+                (void)cnt;
             }
         }
         __syncwarp();
