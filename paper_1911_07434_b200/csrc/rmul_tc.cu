@@ -592,7 +592,8 @@ cudaError_t fm_launch_rmul_tc(const float* d_r, const float* d_omega, const floa
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
     }
-    const int64_t pairs = std::min<int64_t>(tiles, std::max(1, sm_count / 2));
+    static const int cap_pairs = std::getenv("FM_TC_PAIRS") ? std::atoi(std::getenv("FM_TC_PAIRS")) : 0;  // experiment
+    const int64_t pairs = std::min<int64_t>(tiles, std::max(1, cap_pairs > 0 ? cap_pairs : sm_count / 2));
     const dim3 grid(static_cast<unsigned>(2 * pairs));
     auto go = [&](auto kern, int smem) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -663,7 +664,8 @@ cudaError_t fm_launch_rmul_planes(const void* planes_hi, const void* planes_lo, 
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
     }
-    const int64_t pairs = std::min<int64_t>(tiles, std::max(1, sm_count / 2));
+    static const int cap_pairs = std::getenv("FM_TC_PAIRS") ? std::atoi(std::getenv("FM_TC_PAIRS")) : 0;  // experiment
+    const int64_t pairs = std::min<int64_t>(tiles, std::max(1, cap_pairs > 0 ? cap_pairs : sm_count / 2));
     const dim3 grid(static_cast<unsigned>(2 * pairs));
     auto go = [&](auto kern, int smem) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
