@@ -417,6 +417,10 @@ struct fm_plan_s {
     int32_t* status_dev = nullptr;
     float* omega_pinned = nullptr;
     int32_t* status_pinned = nullptr;
+    // host path: chunked H2D on a plan-owned copy stream; [0..kHostChunks) chunk-ready, [kHostChunks] fork
+    static constexpr int kHostChunks = 8;
+    cudaStream_t copy_s = nullptr;
+    cudaEvent_t copy_ev[kHostChunks + 1] = {};
     size_t bytes = 0;
     // optional per-stage CUDA events (covariance | subspace | autocorr | spectrum+peaks),
     // one set of 5 per recorded batch (ring of kMaxProf batches), summed by fm_plan_stage_times
@@ -456,6 +460,9 @@ struct fm_plan_s {
             if (e) cudaEventDestroy(e);
         for (cudaStream_t q : sub)
             if (q) cudaStreamDestroy(q);
+        for (cudaEvent_t e : copy_ev)
+            if (e) cudaEventDestroy(e);
+        if (copy_s) cudaStreamDestroy(copy_s);
         if (omega_pinned) cudaFreeHost(omega_pinned);
         if (status_pinned) cudaFreeHost(status_pinned);
         cudaSetDevice(prev);
@@ -974,20 +981,61 @@ extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const fl
         chk(pl->get(&pl->status_dev, B));
         if (d.method == FM_METHOD_FAST2) chk(cudaMallocHost(&pl->omega_pinned, sizeof(float) * B * M * P));
         chk(cudaMallocHost(&pl->status_pinned, sizeof(int32_t) * B));
+        chk(cudaStreamCreateWithFlags(&pl->copy_s, cudaStreamNonBlocking));
+        for (cudaEvent_t& ev : pl->copy_ev) chk(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         if (e != cudaSuccess) return fm_fail_cuda(e, "fm_estimate_batch_host staging", __FILE__, __LINE__);
     }
-    FM_CUDA_OK(cudaMemcpyAsync(pl->x_dev, h_x, sizeof(float) * frames * M * N * 2, cudaMemcpyHostToDevice, s));
+    // The host path is PCIe-bound (X is 8 B per snapshot element): X crosses in chunks of >= kChunkMin
+    // frames on the plan's copy stream, the Omega / index draw runs on the host while chunk 0 copies,
+    // and chunk c computes on the caller's stream while chunk c+1 copies. Frames are independent, so
+    // per-chunk runs give the same per-frame results as one run over the batch.
+    constexpr int64_t kChunkMin = 128;
+    // measured c2 (1024 frames, scripts_e2e_chunks.py): 1 chunk 21.3 ms, 2: 20.8, 4: 20.56, 8: 22.4;
+    // the plain 1.07 GB pinned H2D alone takes 20.3 ms
+    int64_t max_ch = 4;
+    if (const char* e = getenv("FM_HOST_CHUNKS")) max_ch = std::max(1, std::min<int>(atoi(e), fm_plan_s::kHostChunks));
+    const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(max_ch, frames / kChunkMin));
+    const int64_t cs = (frames + nch - 1) / nch;
+    cudaStream_t cp = pl->copy_s;
+    FM_CUDA_OK(cudaEventRecord(pl->copy_ev[fm_plan_s::kHostChunks], s));  // staging free once s is here
+    FM_CUDA_OK(cudaStreamWaitEvent(cp, pl->copy_ev[fm_plan_s::kHostChunks], 0));
     std::vector<int32_t> idx_host;
-    if (d.method == FM_METHOD_FAST2) {
-        fm_draw_omega_batch(frames, draw_seeds, d.m, d.p, pl->omega_pinned);
-        FM_CUDA_OK(cudaMemcpyAsync(pl->omega_dev, pl->omega_pinned, sizeof(float) * frames * M * P,
-                                   cudaMemcpyHostToDevice, s));
-    } else if (d.method == FM_METHOD_FAST1) {
-        idx_host.resize(static_cast<size_t>(frames) * P);
-        fm_status st = fm_draw_indices_batch(frames, draw_seeds, d.m, d.p, idx_host.data());
+    for (int64_t c = 0; c < nch; ++c) {
+        const int64_t f0 = c * cs, fc = std::min(cs, frames - f0);
+        const size_t xo = static_cast<size_t>(f0) * M * N * 2;
+        FM_CUDA_OK(cudaMemcpyAsync(pl->x_dev + xo, h_x + xo, sizeof(float) * fc * M * N * 2, cudaMemcpyHostToDevice, cp));
+        if (c == 0 && d.method == FM_METHOD_FAST2) {
+            fm_draw_omega_batch(frames, draw_seeds, d.m, d.p, pl->omega_pinned);
+            FM_CUDA_OK(cudaMemcpyAsync(pl->omega_dev, pl->omega_pinned, sizeof(float) * frames * M * P,
+                                       cudaMemcpyHostToDevice, cp));
+        } else if (c == 0 && d.method == FM_METHOD_FAST1) {
+            idx_host.resize(static_cast<size_t>(frames) * P);
+            fm_status st = fm_draw_indices_batch(frames, draw_seeds, d.m, d.p, idx_host.data());
+            if (st != FM_OK) return st;
+            FM_CUDA_OK(cudaMemcpyAsync(pl->idx_dev, idx_host.data(), sizeof(int32_t) * idx_host.size(),
+                                       cudaMemcpyHostToDevice, cp));
+        }
+        FM_CUDA_OK(cudaEventRecord(pl->copy_ev[c], cp));
+    }
+    auto chunk_io = [&](int64_t f0) {
+        fm_batch_io io{};
+        io.x = pl->x_dev + static_cast<size_t>(f0) * M * N * 2;
+        io.omega = pl->omega_dev ? pl->omega_dev + static_cast<size_t>(f0) * M * P : nullptr;
+        io.indices = pl->idx_dev ? pl->idx_dev + static_cast<size_t>(f0) * P : nullptr;
+        io.spectrum = out->spectrum ? pl->spec_dev + static_cast<size_t>(f0) * L : nullptr;
+        io.peak_cells = pl->cells_dev + static_cast<size_t>(f0) * K;
+        io.peak_heights = pl->heights_dev + static_cast<size_t>(f0) * K;
+        io.baseline = pl->base_dev + f0;
+        io.peak_count = pl->count_dev + f0;
+        io.status = pl->status_dev + f0;
+        return io;
+    };
+    for (int64_t c = 0; c < nch; ++c) {
+        const int64_t f0 = c * cs, fc = std::min(cs, frames - f0);
+        FM_CUDA_OK(cudaStreamWaitEvent(s, pl->copy_ev[c], 0));
+        const fm_batch_io io = chunk_io(f0);
+        fm_status st = fm_run_batch(pl, fc, &io, stream);
         if (st != FM_OK) return st;
-        FM_CUDA_OK(cudaMemcpyAsync(pl->idx_dev, idx_host.data(), sizeof(int32_t) * idx_host.size(),
-                                   cudaMemcpyHostToDevice, s));
     }
     fm_batch_io io{};
     io.x = pl->x_dev;
@@ -999,8 +1047,7 @@ extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const fl
     io.baseline = pl->base_dev;
     io.peak_count = pl->count_dev;
     io.status = pl->status_dev;
-    fm_status st = fm_run_batch(pl, frames, &io, stream);
-    if (st != FM_OK) return st;
+    fm_status st = FM_OK;
     std::vector<int32_t> attempts(static_cast<size_t>(frames), 1);
     if (d.method == FM_METHOD_FAST2) {
         // R/src/estimators.cpp:114-137: up to 3 sub-seeded redraws per rank-deficient frame.
@@ -1022,7 +1069,8 @@ extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const fl
                 }
             }
             if (!any) break;
-            st = fm_rerun_frames(pl, frames, nullptr, &io, stream);
+            // whole batch again (R of the chunked runs is not kept); unflagged frames reproduce exactly
+            st = nch == 1 ? fm_rerun_frames(pl, frames, nullptr, &io, stream) : fm_run_batch(pl, frames, &io, stream);
             if (st != FM_OK) return st;
         }
     }
