@@ -31,6 +31,7 @@ typedef int32_t fm_status;
 #define FM_ESINGULAR 4
 #define FM_ECUDA 5
 #define FM_ENOTSUP 6
+#define FM_EIO 7 /* file I/O (std::runtime_error in the reference's io.cpp) */
 
 /* Per-frame status bits written by the batched kernels. */
 #define FM_FRAME_OK 0
@@ -150,6 +151,32 @@ typedef struct fm_host_out {
 } fm_host_out;
 fm_status fm_estimate_batch_host(fm_plan plan, int64_t frames, const float* h_x, const uint64_t* draw_seeds,
                                  fm_host_out* out, void* stream);
+
+/* ------------------------------------------------------------------ frame I/O (host)
+ * FMCX binary matrix, R/include/fastmusic/io.hpp:17-21 / R/src/io.cpp:66-109: little-endian "FMCX",
+ * u32 version 1, u32 rows, u32 cols, rows*cols complex64 row-major — one M x N file is one frame of
+ * fm_batch_io.x. Errors: FM_EIO for open failure / bad magic / unsupported version / truncated payload
+ * (the reference's std::runtime_error), FM_EINVAL for non-finite entries on write (ensure_finite) or a
+ * dimension mismatch on read. */
+/* write_matrix_binary from a row-major complex64 matrix */
+fm_status fm_fmcx_write(const char* path, int64_t rows, int64_t cols, const float* a);
+fm_status fm_fmcx_read_header(const char* path, int64_t* rows, int64_t* cols);
+/* read_matrix_binary into row-major complex64; rows/cols must match the header */
+fm_status fm_fmcx_read(const char* path, int64_t rows, int64_t cols, float* a);
+/* the same two on a column-major complex128 CxMat (R/src/io.cpp:71-109 exactly) */
+fm_status fm_z_fmcx_write(const char* path, int64_t rows, int64_t cols, const double* a);
+fm_status fm_z_fmcx_read(const char* path, int64_t rows, int64_t cols, double* a);
+/* Batch ingest: frame f of x (frames x m x n complex64, e.g. the pinned buffer handed to
+ * fm_estimate_batch_host) from / to paths[f]; threaded over frames (threads <= 0: all cores). */
+fm_status fm_fmcx_read_frames(const char* const* paths, int64_t frames, int64_t m, int64_t n, float* x,
+                              int32_t threads);
+fm_status fm_fmcx_write_frames(const char* const* paths, int64_t frames, int64_t m, int64_t n, const float* x,
+                               int32_t threads);
+/* write_matrix_csv, R/src/io.cpp:111-122 (column-major complex128) */
+fm_status fm_z_write_matrix_csv(const char* path, int64_t rows, int64_t cols, const double* a);
+/* write_spectrum_csv, R/src/io.cpp:124-131 on theta_l = theta0 + ((theta1-theta0)*l)/(L-1) */
+fm_status fm_write_spectrum_csv(const char* path, int64_t grid_size, double theta0, double theta1,
+                                const double* values);
 
 /* ------------------------------------------------------------------ reference single-matrix API
  * complex128, column-major; computed on the GPU in fp64 (facade path of

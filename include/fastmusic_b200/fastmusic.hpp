@@ -33,6 +33,7 @@ class Dense {
 public:
     Dense() = default;
     Dense(Index r, Index c) : r_(r), c_(c), d_(static_cast<std::size_t>(r * c)) {}
+    explicit Dense(Index n) : Dense(n, 1) {}  // column vector, as Eigen's VectorX(n)
     static Dense Zero(Index r, Index c) { return Dense(r, c); }
     static Dense Identity(Index r, Index c) {
         Dense m(r, c);
@@ -173,6 +174,12 @@ SubspaceEstimate fast_music_1(const HermitianMatrix& s, Index k, const Fast1Para
 SubspaceEstimate fast_music_2(const HermitianMatrix& s, Index k, const Fast2Params& params);
 PseudoSpectrum music_spectrum(const SubspaceEstimate& estimate, const AngleGrid& grid, double d, double lambda);
 PeakSet extract_peaks(const PseudoSpectrum& p, Index k, Index min_separation_cells);
+
+// io.hpp:17-27 (matrix / spectrum files; scene files belong to the FMCW front end, out of scope)
+void write_matrix_binary(const std::string& path, const CxMat& a);
+CxMat read_matrix_binary(const std::string& path);
+void write_matrix_csv(const std::string& path, const CxMat& a);
+void write_spectrum_csv(const std::string& path, const PseudoSpectrum& spectrum);
 
 // Batched complex64 pipeline over device-resident frames (fm_plan); one per host thread.
 class BatchEstimator {

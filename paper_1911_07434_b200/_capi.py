@@ -13,7 +13,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfastmusic_b200.so")
 
-FM_OK, FM_EINVAL, FM_ERANK, FM_ENOCONV, FM_ESINGULAR, FM_ECUDA, FM_ENOTSUP = range(7)
+FM_OK, FM_EINVAL, FM_ERANK, FM_ENOCONV, FM_ESINGULAR, FM_ECUDA, FM_ENOTSUP, FM_EIO = range(8)
 FRAME_OK, FRAME_RANK, FRAME_NOCONV, FRAME_RANGE, FRAME_NONFINITE = 0, 1, 2, 4, 8
 METHOD = {"exact": 0, "fast1": 1, "fast2": 2}
 
@@ -26,6 +26,8 @@ EXPORTED = [
     "fm_plan_launches_per_batch", "fm_plan_set_profiling", "fm_plan_stage_times", "fm_plan_set_concurrency", "fm_estimate_batch_host",
     "fm_z_spatial_covariance", "fm_z_exact_signal_subspace", "fm_z_fast_music_1", "fm_z_fast_music_2",
     "fm_z_music_spectrum", "fm_z_extract_peaks",
+    "fm_fmcx_write", "fm_fmcx_read_header", "fm_fmcx_read", "fm_z_fmcx_write", "fm_z_fmcx_read",
+    "fm_fmcx_read_frames", "fm_fmcx_write_frames", "fm_z_write_matrix_csv", "fm_write_spectrum_csv",
 ]
 
 
@@ -87,6 +89,15 @@ def _load():
         "fm_z_fast_music_2": (i32, [i64, vp, i64, i64, i32, u64, vp, vp, vp, vp]),
         "fm_z_music_spectrum": (i32, [i64, i64, vp, i64, dbl, dbl, dbl, dbl, vp]),
         "fm_z_extract_peaks": (i32, [vp, i64, i64, i64, vp, vp, vp, vp, vp]),
+        "fm_fmcx_write": (i32, [C.c_char_p, i64, i64, vp]),
+        "fm_fmcx_read_header": (i32, [C.c_char_p, vp, vp]),
+        "fm_fmcx_read": (i32, [C.c_char_p, i64, i64, vp]),
+        "fm_z_fmcx_write": (i32, [C.c_char_p, i64, i64, vp]),
+        "fm_z_fmcx_read": (i32, [C.c_char_p, i64, i64, vp]),
+        "fm_fmcx_read_frames": (i32, [vp, i64, i64, i64, vp, i32]),
+        "fm_fmcx_write_frames": (i32, [vp, i64, i64, i64, vp, i32]),
+        "fm_z_write_matrix_csv": (i32, [C.c_char_p, i64, i64, vp]),
+        "fm_write_spectrum_csv": (i32, [C.c_char_p, i64, dbl, dbl, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -55,6 +55,8 @@ def _check(st: int, column: int = -1):
         raise SingularMatrixError(msg)
     if st == _capi.FM_ENOTSUP:
         raise NotImplementedError(msg)
+    if st == _capi.FM_EIO:
+        raise OSError(msg)
     raise CudaError(msg)
 
 
@@ -287,6 +289,72 @@ def extract_peaks(p: PseudoSpectrum, k: int, min_separation_cells: int) -> PeakS
     n = count.value
     cl = [int(c) for c in cells[:n]]
     return PeakSet([p.grid.theta(c) for c in cl], [float(h) for h in heights[:n]], base.value, bool(short.value), cl)
+
+
+# ------------------------------------------------------------------ frame I/O (R/src/io.cpp:66-131)
+def _paths(paths):
+    import os
+    enc = [os.fsencode(q) for q in paths]
+    return (C.c_char_p * max(1, len(enc)))(*enc), len(enc)
+
+
+def write_matrix_binary(path, a) -> None:
+    """write_matrix_binary, R/src/io.cpp:71-86 (FMCX: complex64 row-major; complex128 input is cast per part)."""
+    a = np.asarray(a)
+    if a.ndim != 2:
+        raise ValueError("write_matrix_binary: 2-D matrix required")
+    if a.dtype == np.complex64:
+        c = np.ascontiguousarray(a)
+        _check(LIB.fm_fmcx_write(str(path).encode(), a.shape[0], a.shape[1], ptr(c) if c.size else None))
+    else:
+        z = _cmat(a)
+        _check(LIB.fm_z_fmcx_write(str(path).encode(), a.shape[0], a.shape[1], ptr(z) if z.size else None))
+
+
+def read_matrix_binary(path) -> np.ndarray:
+    """read_matrix_binary, R/src/io.cpp:88-109; returns the complex64 payload as a (rows, cols) array."""
+    r, c = C.c_int64(0), C.c_int64(0)
+    _check(LIB.fm_fmcx_read_header(str(path).encode(), C.byref(r), C.byref(c)))
+    out = np.empty((r.value, c.value), np.complex64)
+    _check(LIB.fm_fmcx_read(str(path).encode(), r.value, c.value, ptr(out) if out.size else None))
+    return out
+
+
+def read_frames(paths, m: int, n: int, out=None, threads: int = 0) -> np.ndarray:
+    """Batch ingest: one M x N FMCX file per frame into x[f] (complex64 [frames, m, n]; pass a pinned
+    buffer as `out` to feed BatchPlan.estimate_host without another copy)."""
+    arr, cnt = _paths(paths)
+    x = out if out is not None else np.empty((cnt, m, n), np.complex64)
+    if x.dtype != np.complex64 or x.shape != (cnt, m, n) or not x.flags.c_contiguous:
+        raise ValueError("read_frames: out must be C-contiguous complex64 [frames, m, n]")
+    _check(LIB.fm_fmcx_read_frames(C.cast(arr, C.c_void_p), cnt, m, n, ptr(x), threads))
+    return x
+
+
+def write_frames(paths, x, threads: int = 0) -> None:
+    """One FMCX file per frame of x (complex64 [frames, m, n])."""
+    x = np.ascontiguousarray(x, np.complex64)
+    arr, cnt = _paths(paths)
+    if x.ndim != 3 or x.shape[0] != cnt:
+        raise ValueError("write_frames: x must be [len(paths), m, n]")
+    _check(LIB.fm_fmcx_write_frames(C.cast(arr, C.c_void_p), cnt, x.shape[1], x.shape[2], ptr(x), threads))
+
+
+def write_matrix_csv(path, a) -> None:
+    """write_matrix_csv, R/src/io.cpp:111-122."""
+    z = _cmat(a)
+    if z.ndim != 2:
+        raise ValueError("write_matrix_csv: 2-D matrix required")
+    _check(LIB.fm_z_write_matrix_csv(str(path).encode(), z.shape[0], z.shape[1], ptr(z) if z.size else None))
+
+
+def write_spectrum_csv(path, spectrum: PseudoSpectrum) -> None:
+    """write_spectrum_csv, R/src/io.cpp:124-131."""
+    v = np.ascontiguousarray(spectrum.values, np.float64)
+    if v.size != spectrum.grid.size:
+        raise ValueError("write_spectrum_csv: values / grid size mismatch")
+    _check(LIB.fm_write_spectrum_csv(str(path).encode(), spectrum.grid.size, spectrum.grid.theta0,
+                                     spectrum.grid.theta1, ptr(v)))
 
 
 # ------------------------------------------------------------------ batched plan

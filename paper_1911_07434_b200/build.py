@@ -19,7 +19,7 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build", "fastmusic_b200")
 LIB = os.path.join(PKG, "libfastmusic_b200.so")
 CU_SOURCES = ["cov_tc.cu", "rmul_tc.cu", "subspace.cu", "smallmat.cu", "spectrum.cu", "jacobi.cu", "capi.cu"]
-CXX_SOURCES = ["facade.cpp"]
+CXX_SOURCES = ["facade.cpp", "io.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]

@@ -85,6 +85,9 @@ fm_status fail(fm_status s, const std::string& msg) {
 
 }  // namespace
 
+// last-error setter shared with the host-only translation units (io.cpp)
+fm_status fm_set_error(fm_status s, const std::string& msg) { return fail(s, msg); }
+
 fm_status fm_fail_cuda(cudaError_t e, const char* expr, const char* file, int line) {
     char buf[512];
     std::snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e), cudaGetErrorString(e),
@@ -240,6 +243,7 @@ extern "C" const char* fm_status_string(fm_status s) {
         case FM_ESINGULAR: return "singular matrix";
         case FM_ECUDA: return "cuda error";
         case FM_ENOTSUP: return "not supported";
+        case FM_EIO: return "i/o error";
     }
     return "unknown";
 }

@@ -172,6 +172,30 @@ PeakSet extract_peaks(const PseudoSpectrum& p, Index k, Index min_separation_cel
     return out;
 }
 
+// R/src/io.cpp:71-131 (the file formats themselves live in csrc/io.cpp)
+void write_matrix_binary(const std::string& path, const CxMat& a) {
+    check(fm_z_fmcx_write(path.c_str(), a.rows(), a.cols(), raw(a)));
+}
+
+CxMat read_matrix_binary(const std::string& path) {
+    int64_t rows = 0, cols = 0;
+    check(fm_fmcx_read_header(path.c_str(), &rows, &cols));
+    CxMat a(rows, cols);
+    check(fm_z_fmcx_read(path.c_str(), rows, cols, raw(a)));
+    return a;
+}
+
+void write_matrix_csv(const std::string& path, const CxMat& a) {
+    check(fm_z_write_matrix_csv(path.c_str(), a.rows(), a.cols(), raw(a)));
+}
+
+void write_spectrum_csv(const std::string& path, const PseudoSpectrum& spectrum) {
+    if (spectrum.values.size() != spectrum.grid.size())
+        throw std::invalid_argument("write_spectrum_csv: values / grid size mismatch");
+    check(fm_write_spectrum_csv(path.c_str(), spectrum.grid.size(), spectrum.grid.theta0(), spectrum.grid.theta1(),
+                                spectrum.values.data()));
+}
+
 BatchEstimator::BatchEstimator(const fm_plan_desc& desc, int device) { check(fm_plan_create(&desc, device, &plan_)); }
 
 BatchEstimator::~BatchEstimator() {

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
+#include <string>
 
 #include "fastmusic_b200/fastmusic.hpp"
 
@@ -16,7 +17,52 @@ static double lcg(std::uint64_t& s) {  // deterministic noise in [-0.5, 0.5)
     return static_cast<double>(s >> 11) * (1.0 / 9007199254740992.0) - 0.5;
 }
 
-int main() {
+// "io <dir>": R/tests/test_io.cpp through the facade (host-only, runs without a GPU)
+static int io_mode(const std::string& dir) {
+    CxMat a(7, 3);
+    std::uint64_t st = 5;
+    for (Index i = 0; i < 7; ++i)
+        for (Index j = 0; j < 3; ++j) a(i, j) = Complex(lcg(st), lcg(st));
+    write_matrix_binary(dir + "/mat.bin", a);
+    const CxMat back = read_matrix_binary(dir + "/mat.bin");
+    double err = 0.0, nrm = 0.0;
+    for (Index i = 0; i < a.size(); ++i) {
+        err += std::norm(back(i) - a(i));
+        nrm += std::norm(a(i));
+    }
+    std::printf("io_roundtrip %ld %ld %.3g\n", static_cast<long>(back.rows()), static_cast<long>(back.cols()),
+                std::sqrt(err / nrm));
+    std::FILE* f = std::fopen((dir + "/junk.bin").c_str(), "wb");
+    std::fputs("NOPE furthermore", f);
+    std::fclose(f);
+    try {
+        (void)read_matrix_binary(dir + "/junk.bin");
+        std::printf("io_badmagic no-throw\n");
+    } catch (const std::runtime_error&) {
+        std::printf("io_badmagic runtime_error\n");
+    }
+    CxMat bad(2, 2);
+    bad(1, 0) = Complex(std::nan(""), 0.0);
+    try {
+        write_matrix_binary(dir + "/nan.bin", bad);
+        std::printf("io_nonfinite no-throw\n");
+    } catch (const std::invalid_argument&) {
+        std::printf("io_nonfinite invalid_argument\n");
+    }
+    CxMat eye(2, 2);
+    eye(0, 0) = eye(1, 1) = Complex(1.0, 0.0);
+    write_matrix_csv(dir + "/mat.csv", eye);
+    PseudoSpectrum p{AngleGrid(3), RealVec(3), Method::Exact, false};
+    p.values(0) = 0.5;
+    p.values(1) = 1.5;
+    p.values(2) = 0.25;
+    write_spectrum_csv(dir + "/spec.csv", p);
+    std::printf("io_csv written\n");
+    return 0;
+}
+
+int main(int argc, char** argv) {
+    if (argc == 3 && std::string(argv[1]) == "io") return io_mode(argv[2]);
     const Index m = 16, n = 64;
     const double pi = 3.14159265358979323846, d = 0.5, lam = 1.0;
     const double th[2] = {-20.0 * pi / 180.0, 25.0 * pi / 180.0};

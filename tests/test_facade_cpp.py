@@ -29,6 +29,26 @@ def test_facade_driver_compiles_and_links(tmp_path):
     _build(tmp_path)
 
 
+def test_facade_driver_io(tmp_path):
+    """The facade's io.hpp functions (host-only): R/tests/test_io.cpp's checks from C++, files compared
+    byte for byte with the oracle's restatement of R/src/io.cpp."""
+    import numpy as np
+    from oracle import io_oracle as IO
+    exe = _build(tmp_path)
+    d = tmp_path / "io"
+    d.mkdir()
+    r = subprocess.run([exe, "io", str(d)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stderr
+    lines = {ln.split()[0]: ln.split()[1:] for ln in r.stdout.strip().splitlines()}
+    assert lines["io_roundtrip"][:2] == ["7", "3"] and float(lines["io_roundtrip"][2]) < 1e-6
+    assert lines["io_badmagic"] == ["runtime_error"]
+    assert lines["io_nonfinite"] == ["invalid_argument"]
+    assert (d / "mat.csv").read_text() == IO.matrix_csv_text(np.eye(2))
+    assert (d / "spec.csv").read_text() == IO.spectrum_csv_text([0.5, 1.5, 0.25], 0.0, np.pi)
+    a = IO.fmcx_parse((d / "mat.bin").read_bytes())
+    assert (d / "mat.bin").read_bytes() == IO.fmcx_bytes(a)
+
+
 @pytest.mark.gpu
 def test_facade_driver_runs(tmp_path):
     exe = _build(tmp_path)

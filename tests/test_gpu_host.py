@@ -74,3 +74,22 @@ def test_host_path_redraws_rank_deficient_frames(fm):
     assert np.all(host["status"][ok] == 0) and np.all(host["attempts"][ok] == 1)
     assert np.array_equal(host["peak_cells"][ok], dev["peak_cells"][ok])
     assert np.array_equal(host["spectrum"][ok], dev["spectrum"][ok])
+
+
+def test_host_path_from_frame_files(fm, tmp_path):
+    """SURVEY §8(f)1 ingest: one FMCX file per frame -> fm_fmcx_read_frames straight into pinned staging ->
+    fm_estimate_batch_host; identical to the device run on the in-memory frames."""
+    import torch
+    frames = 260
+    x, _, _ = fm.generate_frames(M, N, K, 33, 0, frames)
+    paths = [tmp_path / f"frame_{f:04d}.fmcx" for f in range(frames)]
+    fm.write_frames(paths, x)
+    pinned = torch.empty((frames, M, N), dtype=torch.complex64).pin_memory().numpy()
+    fm.read_frames(paths, M, N, out=pinned)
+    assert np.array_equal(pinned, x)
+    seeds = np.array([fm.derive(79, f) for f in range(frames)], np.uint64)
+    dev = _device_run(fm, "fast2", x, seeds, 721)
+    host = _host_run(fm, "fast2", pinned, seeds, 721)
+    assert np.all(host["status"] == 0)
+    assert np.array_equal(host["peak_cells"], dev["peak_cells"])
+    assert np.array_equal(host["spectrum"], dev["spectrum"])
