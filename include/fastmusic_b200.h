@@ -152,6 +152,14 @@ typedef struct fm_host_out {
 fm_status fm_estimate_batch_host(fm_plan plan, int64_t frames, const float* h_x, const uint64_t* draw_seeds,
                                  fm_host_out* out, void* stream);
 
+/* Batched temporal covariance, DEVICE pointers: x frames x M x N complex64 row-major ->
+ * t_out frames x N x N complex64 row-major, T = X^H X / M (tensor-core covariance kernel on X^H; same
+ * precision contract as fm_run_batch's R). status: frames FM_FRAME_* bits (RANGE / NONFINITE), zeroed by
+ * the call. work: device scratch for X^H (frames x N x (M + M % 2) complex64), or NULL for a stream-ordered
+ * allocation per call. Asynchronous on `stream`. */
+fm_status fm_temporal_covariance_batch(const float* x, int64_t frames, int64_t m, int64_t n, float* t_out,
+                                       int32_t* status, float* work, void* stream);
+
 /* ------------------------------------------------------------------ frame I/O (host)
  * FMCX binary matrix, R/include/fastmusic/io.hpp:17-21 / R/src/io.cpp:66-109: little-endian "FMCX",
  * u32 version 1, u32 rows, u32 cols, rows*cols complex64 row-major — one M x N file is one frame of
@@ -184,6 +192,8 @@ fm_status fm_write_spectrum_csv(const char* path, int64_t grid_size, double thet
  * kernels (R/src/estimators.cpp:19-23 semantics). */
 /* spatial_covariance, R/src/scene.cpp:157-159 (+ HermitianMatrix symmetrisation) */
 fm_status fm_z_spatial_covariance(int64_t m, int64_t n, const double* y, double* s_out);
+/* temporal_covariance, R/src/scene.cpp:140-153,161-163: T = Y^H Y / M (N x N), fp64 on the GPU */
+fm_status fm_z_temporal_covariance(int64_t m, int64_t n, const double* y, double* t_out);
 /* exact_signal_subspace, R/src/estimators.cpp:73-85 */
 fm_status fm_z_exact_signal_subspace(int64_t m, const double* s, int64_t k, double* basis, double* eigenvalues,
                                      double* cost_seconds);

@@ -169,6 +169,7 @@ struct PeakSet {
 
 CxVec steering_vector(double theta, Index m, double d, double lambda);
 HermitianMatrix spatial_covariance(const CxMat& y);
+HermitianMatrix temporal_covariance(const CxMat& y);  // scene.hpp:72, T = Y^H Y / M
 SubspaceEstimate exact_signal_subspace(const HermitianMatrix& s, Index k);
 SubspaceEstimate fast_music_1(const HermitianMatrix& s, Index k, const Fast1Params& params);
 SubspaceEstimate fast_music_2(const HermitianMatrix& s, Index k, const Fast2Params& params);

@@ -201,6 +201,16 @@ def spatial_covariance(y: np.ndarray) -> np.ndarray:
     return hermitian(s)
 
 
+def temporal_covariance(y: np.ndarray) -> np.ndarray:
+    """R/src/scene.cpp:140-153,161-163: T = Y^H Y / M (N x N), then 0.5 (T + T^H)."""
+    y = np.asarray(y, np.complex128)
+    if y.shape[0] < 1 or y.shape[1] < 1:
+        raise ValueError("covariance: empty signal matrix")
+    if not np.all(np.isfinite(y)):
+        raise ValueError("covariance: non-finite entries")
+    return hermitian((y.conj().T @ y) / y.shape[0])
+
+
 def hermitian(a: np.ndarray) -> np.ndarray:
     """HermitianMatrix ctor, R/src/linalg.cpp:46-52."""
     a = np.asarray(a, np.complex128)

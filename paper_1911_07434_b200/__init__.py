@@ -8,7 +8,8 @@ from .api import (AngleGrid, BatchPlan, CudaError, Fast1Params, Fast2Params, Non
                   PseudoSpectrum, RankDeficiencyError, SingularMatrixError, SubspaceEstimate, baseline_grid, derive,
                   draw_indices_batch, draw_omega_batch, exact_signal_subspace, extract_peaks, fast_music_1,
                   fast_music_2, gaussian_matrix_real, generate_frames, hermitian, music_spectrum, normals,
-                  read_frames, read_matrix_binary, sample_without_replacement, spatial_covariance, steering_vector,
+                  read_frames, read_matrix_binary, sample_without_replacement, spatial_covariance, steering_vector, temporal_covariance,
+                  temporal_covariance_batch,
                   write_frames, write_matrix_binary, write_matrix_csv, write_spectrum_csv)
 from ._capi import LIB_PATH  # noqa: F401
 

@@ -219,6 +219,34 @@ def spatial_covariance(y) -> np.ndarray:
     return s
 
 
+def temporal_covariance(y) -> np.ndarray:
+    """R/src/scene.cpp:161-163 (T = Y^H Y / M, N x N) — on the GPU in fp64."""
+    y = _cmat(y)
+    if y.ndim != 2 or y.shape[0] < 1 or y.shape[1] < 1:
+        raise ValueError("covariance: empty signal matrix")
+    t = np.empty((y.shape[1], y.shape[1]), np.complex128, order="F")
+    _check(LIB.fm_z_temporal_covariance(y.shape[0], y.shape[1], ptr(y), ptr(t)))
+    return t
+
+
+def temporal_covariance_batch(x, out=None, status=None, stream=None, work=None):
+    """Batched T_f = X_f^H X_f / M on the device (torch tensors: x complex64 [frames, M, N] or its float32
+    view) -> complex64 [frames, N, N]; per-frame FM_FRAME_* bits in `status` (int32 [frames]). `work`:
+    optional complex64 scratch of frames * N * (M + M % 2) elements (else allocated per call)."""
+    import torch
+    frames, m = x.shape[0], x.shape[1]
+    n = x.shape[2] if x.dtype == torch.complex64 else x.shape[2] // 2
+    if out is None:
+        out = torch.empty((frames, n, n), dtype=torch.complex64, device=x.device)
+    if status is None:
+        status = torch.empty((frames,), dtype=torch.int32, device=x.device)
+    s = None if stream is None else C.c_void_p(stream.cuda_stream)
+    if work is not None and work.numel() * work.element_size() < 8 * frames * n * (m + m % 2):
+        raise ValueError("temporal_covariance_batch: work too small")
+    _check(LIB.fm_temporal_covariance_batch(ptr(x), frames, m, n, ptr(out), ptr(status), ptr(work), s))
+    return out, status
+
+
 def _est_out(m, k):
     return np.empty((m, k), np.complex128, order="F"), np.empty(k, np.float64), C.c_double(0.0)
 

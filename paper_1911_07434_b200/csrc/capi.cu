@@ -1153,6 +1153,74 @@ extern "C" fm_status fm_z_spatial_covariance(int64_t m, int64_t n, const double*
     return FM_OK;
 }
 
+// ------------------------------------------------------------------ temporal covariance
+// temporal_covariance, R/src/scene.cpp:140-153,161-163: T = Y^H Y / M (N x N, lower rankUpdate of Y^H,
+// mirrored, symmetrised) — the spatial kernels applied to Y^H.
+extern "C" fm_status fm_z_temporal_covariance(int64_t m, int64_t n, const double* y, double* t_out) {
+    if (m < 1 || n < 1) return fail(FM_EINVAL, "covariance: empty signal matrix");
+    if (!y || !t_out) return fail(FM_EINVAL, "covariance: null pointer");
+    if (!all_finite(y, 2 * m * n)) return fail(FM_EINVAL, "covariance: non-finite entries");
+    std::vector<double> yh(static_cast<size_t>(2 * m * n));  // Y^H, N x M column-major
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t j = 0; j < n; ++j) {
+            const size_t s = (static_cast<size_t>(j) * m + i) * 2, d = (static_cast<size_t>(i) * n + j) * 2;
+            yh[d] = y[s];
+            yh[d + 1] = -y[s + 1];
+        }
+    return fm_z_spatial_covariance(n, m, yh.data(), t_out);
+}
+
+namespace {
+// Y = X^H per frame: x (frames x M x N, row-major complex64) -> y (frames x N x Mp, Mp = M rounded up to
+// even with a zero column: the covariance kernel's TMA row pitch must be a multiple of 16 B; a zero
+// snapshot adds nothing). 32 x 32 tiles through shared memory, coalesced reads and writes.
+__global__ void k_conj_transpose(const float2* __restrict__ x, float2* __restrict__ y, int m, int n, int mp,
+                                 int f0) {
+    __shared__ float2 tile[32][33];
+    const int64_t f = f0 + blockIdx.z;
+    const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+    const float2* xf = x + f * m * n;
+    float2* yf = y + f * n * mp;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int i = i0 + r, j = j0 + threadIdx.x;
+        tile[r][threadIdx.x] = (i < m && j < n) ? xf[static_cast<int64_t>(i) * n + j] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int j = j0 + r, i = i0 + threadIdx.x;
+        if (j < n && i < mp) {
+            const float2 v = tile[threadIdx.x][r];
+            yf[static_cast<int64_t>(j) * mp + i] = make_float2(v.x, -v.y);
+        }
+    }
+}
+}  // namespace
+
+extern "C" fm_status fm_temporal_covariance_batch(const float* x, int64_t frames, int64_t m, int64_t n,
+                                                  float* t_out, int32_t* status, float* work, void* stream) {
+    if (frames < 1 || m < 1 || n < 1) return fail(FM_EINVAL, "temporal_covariance: empty signal matrix");
+    if (!x || !t_out || !status) return fail(FM_EINVAL, "temporal_covariance: null pointer");
+    if (frames * n > 0x7fffffff || m > 0x3fffffff) return fail(FM_EINVAL, "temporal_covariance: batch too large");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t mp = m + (m & 1);
+    float* y = work;
+    if (!y) FM_CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&y), sizeof(float) * 2 * frames * n * mp, s));
+    FM_CUDA_OK(cudaMemsetAsync(status, 0, sizeof(int32_t) * frames, s));
+    const dim3 blk(32, 8);
+    for (int64_t f0 = 0; f0 < frames; f0 += 65535) {
+        const dim3 grd(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((mp + 31) / 32),
+                       static_cast<unsigned>(std::min<int64_t>(65535, frames - f0)));
+        k_conj_transpose<<<grd, blk, 0, s>>>(reinterpret_cast<const float2*>(x), reinterpret_cast<float2*>(y),
+                                             static_cast<int>(m), static_cast<int>(n), static_cast<int>(mp),
+                                             static_cast<int>(f0));
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = fm_launch_cov_tc(y, t_out, status, frames, n, mp, s, nullptr, nullptr, nullptr, m);
+    if (!work) cudaFreeAsync(y, s);
+    if (e != cudaSuccess) return fm_fail_cuda(e, "fm_temporal_covariance_batch", __FILE__, __LINE__);
+    return FM_OK;
+}
+
 static fm_status z_nystrom_common(int64_t m, const double* s, int64_t k, int64_t p, int32_t t, uint64_t seed,
                                   bool fast2, double* basis, double* eigenvalues, double* cost_seconds,
                                   int64_t* deficient_column) {

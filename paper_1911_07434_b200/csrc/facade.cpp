@@ -104,6 +104,13 @@ HermitianMatrix spatial_covariance(const CxMat& y) {
     return HermitianMatrix(s);
 }
 
+HermitianMatrix temporal_covariance(const CxMat& y) {
+    if (y.rows() < 1 || y.cols() < 1) throw std::invalid_argument("covariance: empty signal matrix");
+    CxMat t(y.cols(), y.cols());
+    check(fm_z_temporal_covariance(y.rows(), y.cols(), raw(y), raw(t)));
+    return HermitianMatrix(t);
+}
+
 static SubspaceEstimate make_estimate(Index m, Index k, Method method) {
     SubspaceEstimate out;
     out.basis = CxMat(m, k);
