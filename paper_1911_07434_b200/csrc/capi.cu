@@ -55,7 +55,7 @@ cudaError_t fm_launch_orth_split(const void* C, void* Vout, void* Lw, int32_t* p
                                  int m, int p, cudaStream_t s);
 cudaError_t fm_launch_rmul_planes(const void* planes_hi, const void* planes_lo, const float* d_scale,
                                   const float* d_omega, const float* d_v, float* d_c, int64_t frames, int64_t m,
-                                  int64_t p, cudaStream_t stream);
+                                  int64_t p, cudaStream_t stream, bool hi_only);
 cudaError_t fm_launch_final_split(const void* C, const void* V, void* Hw, void* Gw, void* Tw, void* basis, double* eig,
                                   int32_t* status, int frames, int m, int p, int k, cudaStream_t s,
                                   double* eig_next = nullptr);
@@ -785,9 +785,14 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     };
     fm_status st = FM_OK;
     // C = R Omega (omega) or C = R V: fp16 planes -> rmul_planes_kernel, complex64 R -> tf32 kernel / SIMT
-    auto rmul = [&](const float* omega, const float* v, float* c, int p) -> fm_status {
+    // Range-finder products (all but the last) read only the hi plane of R (R to 2^-12 s_f): they only
+    // shape span(V), and the last product, which feeds the Nystrom step, reads both planes. Measured over
+    // 1024 c2 frames vs the fp64 oracle: worst spectrum error 0.00556 -> 0.00557 dB, no peak changes,
+    // step 1.191 -> 1.140 ms (scripts_precision_sweep.py). FM_RMUL_HI_ONLY=0 reads both planes everywhere.
+    const bool hi_only_env = !(std::getenv("FM_RMUL_HI_ONLY") && std::atoi(std::getenv("FM_RMUL_HI_ONLY")) == 0);
+    auto rmul = [&](const float* omega, const float* v, float* c, int p, bool range_only = false) -> fm_status {
         if (pv.hi)
-            FM_LAUNCH(fm_launch_rmul_planes(pv.hi, pv.lo, pv.scale, omega, v, c, F, M, p, s));
+            FM_LAUNCH(fm_launch_rmul_planes(pv.hi, pv.lo, pv.scale, omega, v, c, F, M, p, s, range_only && hi_only_env));
         else if (tc_rmul(M, p))
             FM_LAUNCH(fm_launch_rmul_tc(R, omega, v, c, F, M, p, s));
         else
@@ -795,10 +800,11 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
         return FM_OK;
     };
     if (d.method == FM_METHOD_FAST2) {
-        if ((st = rmul(io->omega, nullptr, w.C, P)) != FM_OK) return st;
+        // the first t products only shape the range (V); the last one feeds the Nystrom step
+        if ((st = rmul(io->omega, nullptr, w.C, P, d.t > 0)) != FM_OK) return st;
         for (int it = 0; it < d.t; ++it) {
             if ((st = orth(false, nullptr)) != FM_OK) return st;
-            if ((st = rmul(nullptr, w.V, w.C, P)) != FM_OK) return st;
+            if ((st = rmul(nullptr, w.V, w.C, P, it + 1 < d.t)) != FM_OK) return st;
         }
         if (tiled) {
             if (split_final())

@@ -343,7 +343,7 @@ __device__ __forceinline__ void split8(const float (&x)[8], uint4& hi, uint4& lo
     lo = make_uint4(pack_h2(l[0], l[1]), pack_h2(l[2], l[3]), pack_h2(l[4], l[5]), pack_h2(l[6], l[7]));
 }
 
-template <int PH, bool REAL>
+template <int PH, bool REAL, bool LO>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     rmul_planes_kernel(const __grid_constant__ CUtensorMap hmap, const __grid_constant__ CUtensorMap lmap,
                        const __grid_constant__ CUtensorMap vmap, const float* __restrict__ rscale,
@@ -402,9 +402,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     uint8_t* st = smem + s * C::kStageBytes;
                     mbar_wait(smem_u32(&empty[s]), ((g / kPStages) & 1) ^ 1);
                     const uint32_t fb = smem_u32(&full[s]);
-                    mbar_arrive_expect_tx(fb, 2 * kABytes + vbytes);
+                    mbar_arrive_expect_tx(fb, (LO ? 2 : 1) * kABytes + vbytes);
                     tma_3d(smem_u32(st), &hmap, fb, kPKc * kc, y, frame);
-                    tma_3d(smem_u32(st + C::kOffLo), &lmap, fb, kPKc * kc, y, frame);
+                    if (LO) tma_3d(smem_u32(st + C::kOffLo), &lmap, fb, kPKc * kc, y, frame);
                     if (REAL) tma_3d(smem_u32(st + C::kOffV), &vmap, fb, 0, 32 * kc, frame);
                     else tma_3d(smem_u32(st + C::kOffV), &vmap, fb, kPKc * kc, 0, frame);
                 }
@@ -429,7 +429,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         const uint32_t o = 32u * ks;
                         umma_f16_2sm_(d, desc_sw128(st + o), desc_sw128(st + C::kOffB1 + o), id1,
                                       (kc > 0 || ks > 0) ? 1u : 0u);
-                        umma_f16_2sm_(d, desc_sw128(st + C::kOffLo + o), desc_sw128(st + C::kOffB2 + o), id2, 1u);
+                        if (LO)
+                            umma_f16_2sm_(d, desc_sw128(st + C::kOffLo + o), desc_sw128(st + C::kOffB2 + o), id2, 1u);
                     }
                     umma_commit_mc(smem_u32(&empty[s]));
                 }
@@ -617,9 +618,10 @@ extern "C" int32_t fm_debug_rmul_tc(const float* d_r, const float* d_omega, cons
 }
 
 // C = R V / C = R Omega from the fp16 hi / lo planes of R / s_f (M <= 256, M even, p % 4 == 0, p <= 32).
+// hi_only: skip the lo plane (R represented to 2^-12 s_f instead of 2^-24 s_f; half the R bytes read).
 cudaError_t fm_launch_rmul_planes(const void* planes_hi, const void* planes_lo, const float* d_scale,
                                   const float* d_omega, const float* d_v, float* d_c, int64_t frames, int64_t m,
-                                  int64_t p, cudaStream_t stream) {
+                                  int64_t p, cudaStream_t stream, bool hi_only) {
     using namespace fmk::rmtc;
     if (frames < 1 || m < 2 || (m & 1) || m > 256 || p < 4 || p > 32 || (p & 3) || (!d_omega == !d_v))
         return cudaErrorInvalidValue;
@@ -674,7 +676,16 @@ cudaError_t fm_launch_rmul_planes(const void* planes_hi, const void* planes_lo, 
                                                tiles_per_frame, static_cast<int>(tiles));
         return cudaGetLastError();
     };
+    if (hi_only) {
+        if (p <= 16)
+            return d_omega ? go(rmul_planes_kernel<16, true, false>, PCfg<16>::kSmem)
+                           : go(rmul_planes_kernel<16, false, false>, PCfg<16>::kSmem);
+        return d_omega ? go(rmul_planes_kernel<32, true, false>, PCfg<32>::kSmem)
+                       : go(rmul_planes_kernel<32, false, false>, PCfg<32>::kSmem);
+    }
     if (p <= 16)
-        return d_omega ? go(rmul_planes_kernel<16, true>, PCfg<16>::kSmem) : go(rmul_planes_kernel<16, false>, PCfg<16>::kSmem);
-    return d_omega ? go(rmul_planes_kernel<32, true>, PCfg<32>::kSmem) : go(rmul_planes_kernel<32, false>, PCfg<32>::kSmem);
+        return d_omega ? go(rmul_planes_kernel<16, true, true>, PCfg<16>::kSmem)
+                       : go(rmul_planes_kernel<16, false, true>, PCfg<16>::kSmem);
+    return d_omega ? go(rmul_planes_kernel<32, true, true>, PCfg<32>::kSmem)
+                   : go(rmul_planes_kernel<32, false, true>, PCfg<32>::kSmem);
 }
