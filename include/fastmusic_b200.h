@@ -203,6 +203,11 @@ fm_status fm_z_fast_music_1(int64_t m, const double* s, int64_t k, int64_t p, ui
 /* fast_music_2, R/src/estimators.cpp:104-139; *deficient_column set on FM_ERANK */
 fm_status fm_z_fast_music_2(int64_t m, const double* s, int64_t k, int64_t p, int32_t t, uint64_t seed,
                             double* basis, double* eigenvalues, double* cost_seconds, int64_t* deficient_column);
+/* block_lanczos_subspace, R/src/estimators.cpp:154-222 (block Krylov, full reorthogonalisation, top-K Ritz
+ * values stable to 1e-10 relative on two consecutive checks); fp64 on the GPU, M <= 384, block <= 64.
+ * FM_ENOCONV at the iteration cap with the last relative change in *last_change (may be NULL). */
+fm_status fm_z_block_lanczos_subspace(int64_t m, const double* s, int64_t k, int64_t block, int32_t max_iterations,
+                                      double* basis, double* eigenvalues, double* cost_seconds, double* last_change);
 /* music_spectrum, R/src/spectrum.cpp:50-68 on theta_l = theta0 + ((theta1-theta0)*l)/(L-1) */
 fm_status fm_z_music_spectrum(int64_t m, int64_t kb, const double* basis, int64_t grid_size, double theta0,
                               double theta1, double d, double lambda, double* values);

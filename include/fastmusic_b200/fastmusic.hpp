@@ -173,6 +173,8 @@ HermitianMatrix temporal_covariance(const CxMat& y);  // scene.hpp:72, T = Y^H Y
 SubspaceEstimate exact_signal_subspace(const HermitianMatrix& s, Index k);
 SubspaceEstimate fast_music_1(const HermitianMatrix& s, Index k, const Fast1Params& params);
 SubspaceEstimate fast_music_2(const HermitianMatrix& s, Index k, const Fast2Params& params);
+// estimators.hpp:45-50 (the paper's accurate baseline; fp64 on the GPU)
+SubspaceEstimate block_lanczos_subspace(const HermitianMatrix& s, Index k, Index block, int max_iterations);
 PseudoSpectrum music_spectrum(const SubspaceEstimate& estimate, const AngleGrid& grid, double d, double lambda);
 PeakSet extract_peaks(const PseudoSpectrum& p, Index k, Index min_separation_cells);
 

@@ -236,6 +236,24 @@ def thin_svd(a: np.ndarray):
     return u, s, vh.conj().T
 
 
+def _colpiv_rank(a: np.ndarray, r: np.ndarray) -> int:
+    """Eigen ColPivHouseholderQR::rank() on the pivoted R of a: pivots counted while the remaining column
+    norm stays above (maxColNorm*eps)^2/rows*(rows-k) (bug-941 rule), then |R_ii| > eps*diagsize*maxpivot."""
+    rows, cols = a.shape
+    diag = np.abs(np.diag(r))
+    size = min(rows, cols)
+    max_col_norm = np.max(np.linalg.norm(a, axis=0))
+    thr_helper = (max_col_norm * EPS64) ** 2 / rows
+    nonzero = size
+    for k in range(size):
+        if np.linalg.norm(r[k:, k]) ** 2 < thr_helper * (rows - k):
+            nonzero = k
+            break
+    maxpivot = np.max(diag) if size else 0.0
+    prem = maxpivot * EPS64 * size
+    return int(np.sum(diag[:nonzero] > prem))
+
+
 def qr_orthonormal(a: np.ndarray) -> np.ndarray:
     """R/src/linalg.cpp:127-141 — column-pivoted Householder QR.
 
@@ -248,25 +266,18 @@ def qr_orthonormal(a: np.ndarray) -> np.ndarray:
     if cols < 1 or rows < cols:
         raise ValueError("qr_orthonormal: need rows >= cols >= 1")
     q, r, piv = scipy.linalg.qr(a, mode="economic", pivoting=True)
-    diag = np.abs(np.diag(r))
-    size = min(rows, cols)
-    # nonzero pivots (Eigen bug-941 rule): remaining column norm at step k equals
-    # the norm of R[k:, k] for the chosen pivot column.
-    max_col_norm = np.max(np.linalg.norm(a, axis=0))
-    thr_helper = (max_col_norm * EPS64) ** 2 / rows
-    nonzero = size
-    for k in range(size):
-        if np.linalg.norm(r[k:, k]) ** 2 < thr_helper * (rows - k):
-            nonzero = k
-            break
-    maxpivot = np.max(diag) if size else 0.0
-    prem = maxpivot * EPS64 * size
-    rank = int(np.sum(diag[:nonzero] > prem))
+    rank = _colpiv_rank(a, r)
     if rank < cols:
         col = int(piv[rank])
         raise RankDeficiencyError(
             f"qr_orthonormal: rank {rank} < {cols} columns; column {col} is dependent", col)
     return q
+
+
+def orthonormal_range(z: np.ndarray) -> np.ndarray:
+    """R/src/estimators.cpp:143-149: Q of ColPivHouseholderQR(z) restricted to its numerical rank."""
+    q, r, piv = scipy.linalg.qr(z, mode="economic", pivoting=True)
+    return q[:, :_colpiv_rank(z, r)]
 
 
 def pseudo_inverse(a: np.ndarray, rel_tol: float = 0.0) -> np.ndarray:
@@ -386,6 +397,59 @@ class AngleGrid:
         span = self.theta1 - self.theta0
         i = np.arange(self.size, dtype=np.float64)
         return self.theta0 + (span * i) / float(self.size - 1)
+
+
+def block_lanczos_subspace(s, k, block, max_iterations):
+    """R/src/estimators.cpp:154-222 — block Krylov with full reorthogonalisation; converged when the top-K
+    Ritz values change by <= 1e-10 relative on two consecutive checks."""
+    s = hermitian(s)
+    m = s.shape[0]
+    if k < 1 or k >= m:
+        raise ValueError("block_lanczos_subspace: need 1 <= K < M")
+    if block < k:
+        raise ValueError("block_lanczos_subspace: need block >= K")
+    if max_iterations < 1:
+        raise ValueError("block_lanczos_subspace: iters >= 1")
+    tol = 1e-10
+    q = qr_orthonormal(gaussian_matrix_real(m, min(block, m), 0x6C616E637A6F).astype(np.complex128))
+    basis = q
+    h = np.zeros((0, 0), np.complex128)
+    prev = None
+    last_change = float("inf")
+    stable = 0
+    for _ in range(max_iterations):
+        w = s @ q
+        old, new = h.shape[0], w.shape[1]
+        strip = basis.conj().T @ w
+        hn = np.zeros((old + new, old + new), np.complex128)
+        hn[:old, :old] = h
+        hn[:old, old:] = strip[:old]
+        hn[old:, :old] = strip[:old].conj().T
+        hn[old:, old:] = strip[old:]
+        h = hn
+        ev, vec = hermitian_eig(hermitian(h))
+        vals = ev[:min(k, h.shape[0])]
+
+        def estimate():
+            return SubspaceEstimate(basis @ vec[:, :k], clamp_nonnegative(vals), "lanczos")
+
+        if prev is not None and len(prev) == len(vals) == k:
+            change = float(np.max(np.abs(vals - prev) / np.maximum(np.abs(vals), 1e-300)))
+            last_change = change
+            stable = stable + 1 if change <= tol else 0
+            if stable >= 2:
+                return estimate()
+        prev = vals
+        room = m - basis.shape[1]
+        if room <= 0:
+            return estimate()
+        z = w - basis @ (basis.conj().T @ w)
+        z = z - basis @ (basis.conj().T @ z)
+        q = orthonormal_range(z[:, :min(z.shape[1], room)])
+        if q.shape[1] == 0:
+            return estimate()
+        basis = np.hstack([basis, q])
+    raise NonConvergenceError("block_lanczos_subspace: no convergence within iteration cap", last_change)
 
 
 def baseline_grid(l: int) -> AngleGrid:

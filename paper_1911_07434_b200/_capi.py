@@ -26,7 +26,7 @@ EXPORTED = [
     "fm_plan_launches_per_batch", "fm_plan_set_profiling", "fm_plan_stage_times", "fm_plan_set_concurrency", "fm_estimate_batch_host",
     "fm_z_spatial_covariance", "fm_z_exact_signal_subspace", "fm_z_fast_music_1", "fm_z_fast_music_2",
     "fm_z_music_spectrum", "fm_z_extract_peaks",
-    "fm_z_temporal_covariance", "fm_temporal_covariance_batch",
+    "fm_z_temporal_covariance", "fm_temporal_covariance_batch", "fm_z_block_lanczos_subspace",
     "fm_fmcx_write", "fm_fmcx_read_header", "fm_fmcx_read", "fm_z_fmcx_write", "fm_z_fmcx_read",
     "fm_fmcx_read_frames", "fm_fmcx_write_frames", "fm_z_write_matrix_csv", "fm_write_spectrum_csv",
 ]
@@ -91,6 +91,7 @@ def _load():
         "fm_z_music_spectrum": (i32, [i64, i64, vp, i64, dbl, dbl, dbl, dbl, vp]),
         "fm_z_extract_peaks": (i32, [vp, i64, i64, i64, vp, vp, vp, vp, vp]),
         "fm_z_temporal_covariance": (i32, [i64, i64, vp, vp]),
+        "fm_z_block_lanczos_subspace": (i32, [i64, vp, i64, i64, i32, vp, vp, vp, vp]),
         "fm_temporal_covariance_batch": (i32, [vp, i64, i64, i64, vp, vp, vp, vp]),
         "fm_fmcx_write": (i32, [C.c_char_p, i64, i64, vp]),
         "fm_fmcx_read_header": (i32, [C.c_char_p, vp, vp]),

@@ -262,6 +262,27 @@ def exact_signal_subspace(s, k: int) -> SubspaceEstimate:
     return SubspaceEstimate(b, e, "exact", cost.value)
 
 
+def block_lanczos_subspace(s, k: int, block: int, max_iterations: int) -> SubspaceEstimate:
+    """R/src/estimators.cpp:154-222 — block Krylov with full reorthogonalisation, fp64 on the GPU.
+    NonConvergenceError(residual = last relative Ritz-value change) at the iteration cap."""
+    s = hermitian(s)
+    m = s.shape[0]
+    if k < 1 or k >= m:
+        raise ValueError("block_lanczos_subspace: need 1 <= K < M")
+    if block < k:
+        raise ValueError("block_lanczos_subspace: need block >= K")
+    if max_iterations < 1:
+        raise ValueError("block_lanczos_subspace: iters >= 1")
+    b, e, cost = _est_out(m, k)
+    last = C.c_double(0.0)
+    st = LIB.fm_z_block_lanczos_subspace(m, ptr(s), k, block, max_iterations, ptr(b), ptr(e), C.byref(cost),
+                                         C.byref(last))
+    if st == _capi.FM_ENOCONV:
+        raise NonConvergenceError(_capi.last_error(), last.value)
+    _check(st)
+    return SubspaceEstimate(b, e, "lanczos", cost.value)
+
+
 def fast_music_1(s, k: int, params: Fast1Params) -> SubspaceEstimate:
     """R/src/estimators.cpp:87-102."""
     s = hermitian(s)

@@ -150,6 +150,20 @@ SubspaceEstimate fast_music_2(const HermitianMatrix& s, Index k, const Fast2Para
     return out;
 }
 
+SubspaceEstimate block_lanczos_subspace(const HermitianMatrix& s, Index k, Index block, int max_iterations) {
+    const Index m = s.dim();
+    if (k < 1 || k >= m) throw std::invalid_argument("block_lanczos_subspace: need 1 <= K < M");
+    if (block < k) throw std::invalid_argument("block_lanczos_subspace: need block >= K");
+    if (max_iterations < 1) throw std::invalid_argument("block_lanczos_subspace: iters >= 1");
+    SubspaceEstimate out = make_estimate(m, k, Method::Lanczos);
+    double last = 0.0;
+    const fm_status st = fm_z_block_lanczos_subspace(m, raw(s.mat()), k, block, max_iterations, raw(out.basis),
+                                                     out.eigenvalues.data(), &out.cost_seconds, &last);
+    if (st == FM_ENOCONV) throw NonConvergenceError(fm_last_error(), last);
+    check(st);
+    return out;
+}
+
 PseudoSpectrum music_spectrum(const SubspaceEstimate& estimate, const AngleGrid& grid, double d, double lambda) {
     const Index m = estimate.basis.rows();
     if (m < 1) throw std::invalid_argument("music_spectrum: empty basis");

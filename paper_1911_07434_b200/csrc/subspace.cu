@@ -137,7 +137,8 @@ template <typename T, int MODE>
 __global__ void __launch_bounds__(kNT) k_qr(const cplx<T>* __restrict__ Cin, c64* __restrict__ work,
                                              cplx<T>* __restrict__ Vout, c64* __restrict__ Rt,
                                              int32_t* __restrict__ status, int32_t* __restrict__ defcol,
-                                             const int32_t* __restrict__ fmap, int m, int p) {
+                                             const int32_t* __restrict__ fmap, int m, int p,
+                                             int32_t* __restrict__ rank_out = nullptr) {
     __shared__ double nrm2[64];
     __shared__ c64 rdiag[64];
     __shared__ double tau[64];
@@ -246,6 +247,7 @@ __global__ void __launch_bounds__(kNT) k_qr(const cplx<T>* __restrict__ Cin, c64
         const double thr = maxpivot * eps * static_cast<double>(p);
         int rank = 0;
         for (int k = 0; k < nonzero; ++k) rank += sqrt(norm2(rdiag[k])) > thr ? 1 : 0;
+        if (rank_out) rank_out[f] = rank;
         if (rank < p) {
             atomicOr(&status[f], kFrameRank);
             if (defcol) defcol[f] = perm[rank];
@@ -973,6 +975,19 @@ cudaError_t fm_launch_qr(const void* C, void* work, void* Vout, void* Rt, int32_
                                                     static_cast<cplx<T>*>(Vout), nullptr, status, defcol, fmap, m, p);
     return cudaGetLastError();
 }
+
+// One matrix: Q (first p columns, column-major) and the Eigen ColPivHouseholderQR rank (orthonormal_range of
+// the block-Lanczos expansion, R/src/estimators.cpp:143-149: Q(:, 0:rank) spans the range).
+template <typename T>
+cudaError_t fm_launch_qr_rank(const void* C, void* work, void* Vout, int32_t* status, int32_t* rank_out, int m, int p,
+                              cudaStream_t s) {
+    if (p > 64 || p < 1 || m < p) return cudaErrorInvalidValue;
+    sub::k_qr<T, 0><<<1, sub::kNT, 0, s>>>(static_cast<const cplx<T>*>(C), static_cast<c64*>(work),
+                                           static_cast<cplx<T>*>(Vout), nullptr, status, nullptr, nullptr, m, p,
+                                           rank_out);
+    return cudaGetLastError();
+}
+template cudaError_t fm_launch_qr_rank<double>(const void*, void*, void*, int32_t*, int32_t*, int, int, cudaStream_t);
 
 cudaError_t fm_launch_cholqr(const void* C, void* work, void* Vout, void* Rt, int32_t* status, const int32_t* fmap,
                              int frames, int m, int p, bool final_mode, const void* Vin, void* Hout, cudaStream_t s) {
