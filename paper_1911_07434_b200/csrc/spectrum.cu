@@ -738,11 +738,13 @@ __device__ long long* g_peak_dbg = nullptr;  // debug: per-frame phase cycles
 //     sorted list accepting picks with |dc| >= min_sep from every accepted pick (= the greedy);
 //  3. baseline = max over cells with |l - pick| > min_sep for every pick (bitmask), init 0;
 //  4. picks in ascending cell order, padded with -1 / 0.
+// cap_in > 0 bounds the candidate list (shared memory for long grids): a frame with more strict maxima writes
+// count = -1 and leaves; k_peaks_only(only_flagged = 1) redoes it (same protocol as k_peaks_warp).
 __global__ void __launch_bounds__(kNT) k_peaks_cta(const double* __restrict__ values, int L, int K, int min_sep,
-                                                   PeakOut out) {
+                                                   PeakOut out, int cap_in) {
     const long long T0 = clock64();
     extern __shared__ uint8_t psm[];
-    const int cap = max(1, (L - 1) / 2);
+    const int cap = cap_in > 0 ? cap_in : max(1, (L - 1) / 2);
     int n2 = 1;
     while (n2 < cap) n2 <<= 1;
     const int nmask = (L + 31) / 32;
@@ -790,6 +792,10 @@ __global__ void __launch_bounds__(kNT) k_peaks_cta(const double* __restrict__ va
     for (int w = 0; w < kNW; ++w) {
         if (w < warp) off += s_cnt[w];
         nc += s_cnt[w];
+    }
+    if (nc > cap) {  // block-uniform
+        if (threadIdx.x == 0) out.count[f] = -1;
+        return;
     }
     for (int g = g0; g < g1; ++g) {
         const int u = g - g0;
@@ -1056,17 +1062,26 @@ cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K,
         cap_hint = std::atoi(ov);
         warp_kernel = true;
     }
-    if (!block_kernel && !warp_kernel) {  // CTA per frame, exact candidate capacity
-        const int capc = std::max(1, (L - 1) / 2);
-        int n2 = 1;
-        while (n2 < capc) n2 <<= 1;
-        const size_t smem = sizeof(double) * L + static_cast<size_t>(n2) * 12 + sizeof(uint32_t) * ((L + 31) / 32) + 16;
+    if (!block_kernel && !warp_kernel) {  // CTA per frame: exact candidate capacity, else the cap hint
+        const int exact = std::max(1, (L - 1) / 2);
+        auto cta_smem = [&](int capc) {
+            int n2 = 1;
+            while (n2 < capc) n2 <<= 1;
+            return sizeof(double) * L + static_cast<size_t>(n2) * 12 + sizeof(uint32_t) * ((L + 31) / 32) + 16;
+        };
+        int capc = exact;
+        if (const char* ce = std::getenv("FM_PEAKS_CTA_CAP"))  // test hook: capped CTA kernel + fallback
+            capc = std::min(exact, std::max(1, std::atoi(ce)));
+        else if (cta_smem(capc) > 200 * 1024 && cap_hint > 0)
+            capc = std::min(exact, cap_hint);
+        const size_t smem = cta_smem(capc);
         if (smem <= 200 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(spec::k_peaks_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  static_cast<int>(smem));
             if (e != cudaSuccess) return e;
-            spec::k_peaks_cta<<<frames, spec::kNT, smem, s>>>(values, L, K, min_sep, out);
-            return cudaGetLastError();
+            spec::k_peaks_cta<<<frames, spec::kNT, smem, s>>>(values, L, K, min_sep, out, capc < exact ? capc : 0);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            return capc < exact ? block(1) : cudaSuccess;
         }
     }
     if (!block_kernel) {  // warp per frame

@@ -206,6 +206,32 @@ def test_peaks_match_oracle_random(fm, oracle):
         assert got.baseline == ref.baseline and got.shortfall == ref.shortfall
 
 
+@pytest.mark.parametrize("cap", ["1", "7", "40"])
+def test_peaks_cta_capacity_falls_back(fm, oracle, monkeypatch, cap):
+    """CTA peak kernel with a bounded candidate list (long grids: values + candidates must fit shared
+    memory; the pipeline bounds it by 2M + 64): frames with more maxima are redone, results unchanged."""
+    monkeypatch.setenv("FM_PEAKS_CTA_CAP", cap)
+    rng = np.random.default_rng(12)
+    for _ in range(20):
+        n = int(rng.integers(20, 400))
+        v = rng.random(n)
+        k, sep = int(rng.integers(1, 9)), int(rng.integers(0, 5))
+        got = fm.extract_peaks(fm.PseudoSpectrum(fm.AngleGrid(n), v), k, sep)
+        ref = oracle.extract_peaks(v, k, sep)
+        assert got.cells == ref.cells and got.heights == ref.heights
+        assert got.baseline == ref.baseline and got.shortfall == ref.shortfall
+
+
+def test_peaks_cta_capacity_falls_back_long_grid(fm, oracle):
+    """A grid long enough (L = 18001, c4's) that the exact candidate list does not fit shared memory and
+    more maxima than any MUSIC spectrum of M = 64 has: the capped CTA kernel hands the frame to the fallback."""
+    rng = np.random.default_rng(13)
+    v = rng.random(18001)
+    got = fm.extract_peaks(fm.PseudoSpectrum(fm.AngleGrid(18001), v), 16, 3)
+    ref = oracle.extract_peaks(v, 16, 3)
+    assert got.cells == ref.cells and got.heights == ref.heights and got.baseline == ref.baseline
+
+
 @pytest.mark.parametrize("cap", ["4", "1"])
 def test_peaks_candidate_overflow_falls_back(fm, oracle, monkeypatch, cap):
     """Warp peak kernel with a tiny candidate capacity (the pipeline uses 2M + 64): frames with more
