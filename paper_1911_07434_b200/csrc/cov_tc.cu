@@ -36,9 +36,18 @@ namespace cov {
 
 constexpr int kRows = 128;          // rows of X per CTA (half of the UMMA M=256 tile)
 constexpr int kChunk = 16;          // complex snapshots per pipeline stage (one UMMA K-slice)
-constexpr int kStagesS = 3;         // fp32 staging ring (TMA destination), general tiles (A and B sides)
-constexpr int kStagesO = 3;         // fp16 operand ring (UMMA source), general tiles
-constexpr int kMaxStages = 6;       // diagonal-only launches (M <= 256): half-size stages, twice as many
+// Ring depths (stages). General tiles stage the A and B sides (32 KB fp32 per staging stage, 16 KB fp16 per
+// operand stage); diagonal-only launches (M <= 256) stage one side (16 KB / 8 KB). The TMA staging ring is
+// the deeper one: the bytes in flight per CTA bound the X stream (off-diagonal tiles re-read 256-row slabs
+// of X from L2). Measured on one box (scripts_cov_ring.sh, FM_COV_RING): general 3/3 -> 4/2 takes the c4
+// covariance 3.28 -> 3.16 ms; diagonal 6/6 -> 8/4 takes c2's 0.350 -> 0.343 ms.
+constexpr int kStagesS = 4;         // fp32 staging ring (TMA destination), general tiles
+constexpr int kStagesO = 2;         // fp16 operand ring (UMMA source), general tiles
+constexpr int kDiagS = 8;           // diagonal-only launches
+constexpr int kDiagO = 4;
+constexpr int kMaxStages = 8;
+static_assert(kStagesS <= kMaxStages && kStagesO <= kMaxStages && kDiagS <= kMaxStages && kDiagO <= kMaxStages,
+              "ring barriers");
 constexpr int kStageBytes = kRows * kChunk * 8;   // 16 KB fp32 per operand side
 constexpr int kPlaneBytes = kRows * kChunk * 2;   // 4 KB fp16 per plane (Re or Im)
 constexpr int kOpBytes = 2 * kPlaneBytes;         // 8 KB per operand side
@@ -46,7 +55,7 @@ constexpr int kThreads = 320;                     // w0 TMA, w1 MMA, w2..w5 conv
 constexpr int kThreadsP = 448;                    // plane epilogue: w6..w13, two warps per TMEM lane quarter
 constexpr int kSmemStaging = kStagesS * 2 * kStageBytes;
 constexpr int kSmemOperand = kStagesO * 2 * kOpBytes;
-constexpr int kSmemBarriers = 512;  // 4 x 6 ring barriers + acc + exchange slots + tmem slot (256 used)
+constexpr int kSmemBarriers = 512;  // 4 x 8 ring barriers + acc + exchange slots + tmem slot (~300 B used)
 constexpr int kEpiLd = 33;                                  // padded row (float2) of the transpose tile
 constexpr int kEpiChunk = 4096;                             // 32 rows x 16 complex fp32 (one TMA store box)
 constexpr int kEpiWarpBytes = 4 * kEpiChunk;                // [diag buf0 | diag buf1 | mirror buf0 | mirror buf1]
@@ -91,11 +100,13 @@ __device__ __forceinline__ void tile_coords(int t, int& bi, int& bj) {
 // occupies 128 B, its 16-byte chunk c (2 complex) sits at chunk slot c ^ (r & 7)) into the
 // Re/Im fp16 UMMA planes. Tracks max |x| (fp16 range check) and non-finite inputs.
 // Lane mapping keeps both the swizzled reads and the core-matrix writes bank-conflict free.
+// kJ = 2: four converter warps (32 rows each); kJ = 1: eight converter warps (16 rows each).
+template <int kJ>
 __device__ __forceinline__ void convert_tile(const uint8_t* stage, uint8_t* op, int cw, int lane, int row_base,
                                              int m_rows, float& amax, bool& nonfinite) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const int r = 32 * cw + (lane & 7) + 8 * (lane >> 4) + 16 * j;
+    for (int j = 0; j < kJ; ++j) {
+        const int r = 16 * kJ * cw + (lane & 7) + 8 * (lane >> 4) + 16 * j;
         const int q = (lane >> 3) & 1;  // which 8-complex half of the 16-complex chunk
         const bool valid = (row_base + r) < m_rows;
         const uint8_t* src = stage + r * 128;
@@ -139,18 +150,25 @@ __device__ __forceinline__ void convert_tile(const uint8_t* stage, uint8_t* op, 
 // kEpi: 0 generic-store fallback (odd M), 1 TMA-stored complex64 R, 2 TMA-stored fp16 hi/lo planes of
 // R / s_f (M <= 256: one tile per frame; s_f = smallest power of two >= max_i R_ii, exchanged between the
 // two CTAs of the pair; rmap / mmap are the hi / lo plane maps, rscale[f] = s_f).
-template <int kEpi>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEpi == 2 ? kThreadsP : kThreads, 1)
+// kConv8: four more converter warps after the epilogue warps (eight in all, 16 rows each). The redundant
+// operand conversion of multi-tile frames (every 256-row block of X is converted once per tile it feeds,
+// 4x at M = 1024) makes the converters the bottleneck there.
+template <int kEpi, bool kConv8>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((kEpi == 2 ? kThreadsP : kThreads) + (kConv8 ? 128 : 0), 1)
     cov_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap rmap,
                   const __grid_constant__ CUtensorMap mmap, float* __restrict__ r_out, int32_t* __restrict__ status,
                   int m, int n, int tiles_per_frame, int total_tiles, float* __restrict__ rscale,
-                  float inv_n_true, int dbg) {
+                  float inv_n_true, int dbg, int ring) {
     constexpr bool kTmaStore = kEpi >= 1;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* staging = smem;
-    uint8_t* operand = smem + kSmemStaging;
-    uint8_t* epi_bytes = operand + kSmemOperand;  // 1024-aligned (128B-swizzled TMA store boxes)
+    // diagonal-only launches split the staging + operand region 96 KB / 48 KB, general tiles 128 KB / 32 KB
+    static_assert(kDiagS * kStageBytes + kDiagO * kOpBytes <= kSmemStaging + kSmemOperand, "diag rings");
+    // ring: (general staging, general operand, diag staging, diag operand) depths, packed 4 x 8 bits
+    const int gS = ring & 0xff, gO = (ring >> 8) & 0xff, dS = (ring >> 16) & 0xff, dO = (ring >> 24) & 0xff;
+    uint8_t* operand = smem + (tiles_per_frame == 1 ? dS * kStageBytes : gS * 2 * kStageBytes);
+    uint8_t* epi_bytes = smem + kSmemStaging + kSmemOperand;  // 1024-aligned (128B-swizzled TMA store boxes)
     uint64_t* bars = reinterpret_cast<uint64_t*>(epi_bytes + kSmemEpilogue);
     uint64_t* stage_full = bars;
     uint64_t* stage_empty = bars + kMaxStages;
@@ -173,7 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEpi == 2 ? kThreads
     const int nk = (n + kChunk - 1) / kChunk;
     // ring geometry: diagonal-only launches (one tile per frame) use half-size stages, twice as many
     const bool diag_only = tiles_per_frame == 1;
-    const int nS = diag_only ? kMaxStages : kStagesS, nO = diag_only ? kMaxStages : kStagesO;
+    const int nS = diag_only ? dS : gS, nO = diag_only ? dO : gO;
     const int sStride = diag_only ? kStageBytes : 2 * kStageBytes, oStride = diag_only ? kOpBytes : 2 * kOpBytes;
 
     if (threadIdx.x == 0) {
@@ -265,9 +283,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEpi == 2 ? kThreads
                 umma_commit_mc(smem_u32(acc_full));
             }
         }
-    } else if (warp < 6) {
-        // ---------------- converters (warps 2..5)
-        const int cw = warp - 2;
+    } else if (warp < 6 || (kConv8 && warp >= (kEpi == 2 ? kThreadsP : kThreads) / 32)) {
+        // ---------------- converters (warps 2..5, plus the four after the epilogue warps when kConv8)
+        constexpr int kFirstExtra = (kEpi == 2 ? kThreadsP : kThreads) / 32;
+        constexpr int kJ = kConv8 ? 1 : 2;
+        const int cw = warp < 6 ? warp - 2 : 4 + warp - kFirstExtra;
         int g = 0;
         for (int tile = pair; tile < total_tiles; tile += npairs) {
             const int frame = tile / tiles_per_frame;
@@ -285,10 +305,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEpi == 2 ? kThreads
                 mbar_wait(smem_u32(&op_empty[o]), ((g / nO) & 1) ^ 1);
                 const uint8_t* st = staging + s * sStride;
                 uint8_t* op = operand + o * oStride;
-                convert_tile(st, op, cw, lane, row_a, m, amax, nonfinite);
-                if (!diag) convert_tile(st + kStageBytes, op + kOpBytes, cw, lane, row_b, m, amax, nonfinite);
+                convert_tile<kJ>(st, op, cw, lane, row_a, m, amax, nonfinite);
+                if (!diag) convert_tile<kJ>(st + kStageBytes, op + kOpBytes, cw, lane, row_b, m, amax, nonfinite);
                 fence_proxy_async();
-                named_bar_sync(1, 128);  // all four converter warps done with this stage
+                named_bar_sync(1, kConv8 ? 256 : 128);  // all converter warps done with this stage
                 if (warp == 2 && lane == 0) {
                     mbar_arrive_local(smem_u32(&stage_empty[s]));
                     if (rank == 0) mbar_arrive_local(smem_u32(&op_full[o]));
@@ -592,16 +612,30 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
         rmap = map;  // unused by the fallback epilogue
         mmap = map;
     }
-    static bool attr_set[3] = {false, false, false};
-    if (!attr_set[epi]) {
-        cudaError_t e = epi == 2 ? cudaFuncSetAttribute(cov_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                        kSmemBytes)
-                        : epi == 1 ? cudaFuncSetAttribute(cov_tc_kernel<1>,
-                                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes)
-                                   : cudaFuncSetAttribute(cov_tc_kernel<0>,
-                                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    static const bool conv4 = std::getenv("FM_COV_CONV4") != nullptr;  // comparison: four converter warps
+    // ring depths (stages) general staging / operand, diagonal-only staging / operand; FM_COV_RING=a,b,c,d
+    int rs[4] = {kStagesS, kStagesO, kDiagS, kDiagO};
+    if (const char* r = std::getenv("FM_COV_RING")) {
+        int v[4];
+        if (std::sscanf(r, "%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3]) == 4 && v[0] * 2 * kStageBytes + v[1] * 2 * kOpBytes <=
+                kSmemStaging + kSmemOperand && v[2] * kStageBytes + v[3] * kOpBytes <= kSmemStaging + kSmemOperand &&
+            v[0] >= 2 && v[1] >= 2 && v[2] >= 2 && v[3] >= 2 && v[2] <= kMaxStages && v[3] <= kMaxStages &&
+            v[0] <= kMaxStages && v[1] <= kMaxStages)
+            for (int i = 0; i < 4; ++i) rs[i] = v[i];
+    }
+    const int ring = rs[0] | (rs[1] << 8) | (rs[2] << 16) | (rs[3] << 24);
+    auto set_attr = [](auto kern) {
+        return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    };
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaSuccess;
+        for (cudaError_t x : {set_attr(cov_tc_kernel<0, false>), set_attr(cov_tc_kernel<1, false>),
+                              set_attr(cov_tc_kernel<2, false>), set_attr(cov_tc_kernel<0, true>),
+                              set_attr(cov_tc_kernel<1, true>), set_attr(cov_tc_kernel<2, true>)})
+            if (e == cudaSuccess) e = x;
         if (e != cudaSuccess) return e;
-        attr_set[epi] = true;
+        attr_set = true;
     }
     const int nb = static_cast<int>((m + 255) / 256);
     const int tiles_per_frame = nb * (nb + 1) / 2;
@@ -616,14 +650,21 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
     static const int cap_pairs = std::getenv("FM_TC_PAIRS") ? std::atoi(std::getenv("FM_TC_PAIRS")) : 0;  // experiment
     const int64_t pairs = std::min<int64_t>(tiles, std::max(1, cap_pairs > 0 ? cap_pairs : sm_count / 2));
     const dim3 grid(static_cast<unsigned>(2 * pairs));
-    auto go = [&](auto kern) {
-        kern<<<grid, epi == 2 ? kThreadsP : kThreads, kSmemBytes, stream>>>(map, rmap, mmap, d_r, d_status, static_cast<int>(m),
+    auto go = [&](auto kern, bool conv8) {
+        const int threads = (epi == 2 ? kThreadsP : kThreads) + (conv8 ? 128 : 0);
+        kern<<<grid, threads, kSmemBytes, stream>>>(map, rmap, mmap, d_r, d_status, static_cast<int>(m),
                                                      static_cast<int>(n), tiles_per_frame, static_cast<int>(tiles),
                                                      scale, static_cast<float>(1.0 / static_cast<double>(n_true)),
-                                                     dbg_flags());
+                                                     dbg_flags(), ring);
     };
-    if (epi == 2) go(cov_tc_kernel<2>);
-    else if (epi == 1) go(cov_tc_kernel<1>);
-    else go(cov_tc_kernel<0>);
+    if (conv4) {
+        if (epi == 2) go(cov_tc_kernel<2, false>, false);
+        else if (epi == 1) go(cov_tc_kernel<1, false>, false);
+        else go(cov_tc_kernel<0, false>, false);
+    } else {
+        if (epi == 2) go(cov_tc_kernel<2, true>, true);
+        else if (epi == 1) go(cov_tc_kernel<1, true>, true);
+        else go(cov_tc_kernel<0, true>, true);
+    }
     return cudaGetLastError();
 }
