@@ -159,3 +159,48 @@ def test_exact_certified_frames_match_jacobi(fm, oracle):
     assert np.max(np.abs(a["eigenvalues"] - b["eigenvalues"]) / b["eigenvalues"][:, :1]) < 1e-5
     for f in range(len(x)):
         assert oracle.spectrum_db_error(a["spectrum"][f].astype(np.float64), b["spectrum"][f].astype(np.float64)) < DB_TOL
+
+
+def _full_batch(fm, oracle, cfg, nsub, nframes):
+    import torch
+    from tests.gpu_helpers import draws, plan_for
+    frames = list(range(nframes))
+    x, _, _ = fm.generate_frames(cfg.spec.m, cfg.spec.n, cfg.spec.k, cfg.base_seed, 0, len(frames),
+                                 theta_lo_deg=cfg.spec.theta_lo_deg, theta_hi_deg=cfg.spec.theta_hi_deg,
+                                 min_sep_deg=cfg.spec.min_sep_deg, snr_lo_db=cfg.spec.snr_lo_db,
+                                 snr_hi_db=cfg.spec.snr_hi_db)
+    plan = plan_for(fm, cfg, len(frames))
+    plan.set_concurrency(nsub)
+    om, ix = draws(fm, oracle, cfg, frames)
+    xd = torch.from_numpy(np.ascontiguousarray(x).view(np.float32)).cuda()
+    out = plan.outputs(len(frames), spectrum=True, basis=True)
+    plan.run(len(frames), xd, torch.from_numpy(om).cuda() if om is not None else None,
+             torch.from_numpy(ix).cuda() if ix is not None else None, out)
+    torch.cuda.synchronize()
+    res = {k: v.cpu().numpy() for k, v in out.items()}
+    plan.close()
+    return x, res
+
+
+@pytest.mark.parametrize("name,nframes,nsample", [("c2", 1024, 24), ("c3", 1024, 16), ("c5", 512, 16), ("c4", 256, 2)])
+def test_full_size_batch_properties(fm, oracle, cfgs, name, nframes, nsample):
+    """BASELINE configs at their full batch sizes: every frame OK; orthonormal bases; positive spectra;
+    outputs bitwise independent of the sub-batch split; peaks and spectra of a frame sample identical to
+    the oracle (scripts_precision_sweep.py covers whole batches)."""
+    cfg = cfgs[name]
+    x, a = _full_batch(fm, oracle, cfg, 2, nframes)
+    _, b = _full_batch(fm, oracle, cfg, 1, nframes)
+    for key in ("peak_cells", "peak_count", "peak_heights", "baseline", "spectrum", "basis", "eigenvalues", "status"):
+        assert np.array_equal(a[key], b[key]), key
+    assert np.all(a["status"] == 0)
+    assert np.all(a["peak_count"] == cfg.spec.k)
+    assert np.all(a["spectrum"] > 0) and np.all(np.isfinite(a["spectrum"]))
+    bas = a["basis"][..., 0] + 1j * a["basis"][..., 1]  # [f, K, M]
+    gram = np.einsum("fkm,flm->fkl", bas.conj(), bas)
+    assert np.max(np.abs(gram - np.eye(cfg.spec.k))) < 1e-12
+    assert np.all(np.diff(a["eigenvalues"], axis=1) <= 0)  # descending
+    sample = [int(f) for f in np.random.default_rng(7).choice(nframes, nsample, replace=False)]
+    res = {k: v[sample] for k, v in a.items()}
+    worst, mism = compare_frames(oracle, cfg, x[sample], sample, res)
+    assert not mism, mism
+    assert worst <= DB_TOL, worst
