@@ -1,5 +1,6 @@
 """Precision sweep: GPU pipeline vs the fp64 oracle on many frames of one BASELINE config, for each setting
-of an experiment switch (env var toggled between runs in one process). Prints per setting: worst spectrum
+of an experiment switch (env var toggled between runs in one process; "-" = one run with the defaults).
+Prints per setting: worst spectrum
 dB error (within 40 dB of max), 99th percentile, frames whose peak cells differ."""
 import json
 import os
@@ -34,8 +35,9 @@ def main():
     x, _, _ = O.generate_batch(cfg.base_seed, frames, cfg.spec)
     with ProcessPoolExecutor(max_workers=os.cpu_count()) as ex:
         refs = sorted(ex.map(_ref, [(i, f, x[i]) for i, f in enumerate(frames)], chunksize=4))
-    for val in ("0", "1"):
-        os.environ[var] = val
+    for val in (("0", "1") if var != "-" else ("-",)):
+        if var != "-":
+            os.environ[var] = val
         res = run_gpu(fm, O, cfg, x, frames, basis=False)
         errs, mism = [], []
         for i, p_ref, cells in refs:
