@@ -46,6 +46,9 @@ CONFIGS = {
                scene=dict(theta_lo_deg=-70.0, theta_hi_deg=70.0, min_sep_deg=1.0, snr_lo_db=20.0, snr_hi_db=20.0)),
     "c5": dict(m=256, n=512, k=8, method="exact", p=0, t=1, L=3601, frames=512, seed=2,
                scene=dict(theta_lo_deg=-60.0, theta_hi_deg=60.0, min_sep_deg=3.0, snr_lo_db=20.0, snr_hi_db=20.0)),
+    # extension: config 3 with BASELINE's norm^2-weighted column sampling (not in the reference)
+    "c3n": dict(m=256, n=512, k=8, method="fast1_norm2", p=32, t=1, L=3601, frames=1024, seed=2,
+                scene=dict(theta_lo_deg=-60.0, theta_hi_deg=60.0, min_sep_deg=3.0, snr_lo_db=10.0, snr_hi_db=30.0)),
 }
 
 
@@ -68,6 +71,9 @@ def algorithmic(cfg):
     elif cfg["method"] == "fast1":
         w_rf = 0.0
         q = 8.0 * m * n + 8.0 * p + 4.0 * L + 8.0 * k
+    elif cfg["method"] == "fast1_norm2":  # sampled sketch (a gather), one product R V
+        w_rf = 8.0 * m * m * p
+        q = 8.0 * m * n + 4.0 * m + 4.0 * L + 8.0 * k
     else:
         w_rf = 0.0
         q = 8.0 * m * n + 4.0 * L + 8.0 * k
@@ -243,6 +249,8 @@ def run_ours(args):
         omega = torch.from_numpy(fm.draw_omega_batch(dseeds, M, P)).to(dev)
     elif cfgd["method"] == "fast1":
         idx = torch.from_numpy(fm.draw_indices_batch(dseeds, M, P)).to(dev)
+    elif cfgd["method"] == "fast1_norm2":  # uniforms of the weighted sampler travel in the omega slot
+        omega = torch.from_numpy(fm.draw_uniforms_batch(dseeds, M)).to(dev)
     xd = xh.to(dev)
     plan = fm.BatchPlan(M, N, K, cfgd["method"], p=P, t=cfgd["t"], grid_size=L, max_frames=B, device=local)
     nsub = args.subbatches if args.subbatches > 0 else (2 if B >= 512 else 1)
@@ -307,7 +315,8 @@ def run_ours(args):
         te = torch.tensor([el], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        h2d = B * M * N * 8 + (B * M * P * 4 if cfgd["method"] == "fast2" else B * P * 4 if cfgd["method"] == "fast1" else 0)
+        h2d = B * M * N * 8 + (B * M * P * 4 if cfgd["method"] == "fast2" else B * P * 4 if cfgd["method"] == "fast1"
+                               else B * M * 4 if cfgd["method"] == "fast1_norm2" else 0)
         d2h = B * K * 4 + B * 4 + B * 4
         e2e = {"value": world * B * e2e_steps / float(te.item()), "unit": "frames/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": e2e_steps, "path": "fm_estimate_batch_host (pinned host X, "

@@ -44,6 +44,10 @@ typedef int32_t fm_status;
 #define FM_METHOD_EXACT 0
 #define FM_METHOD_FAST1 1
 #define FM_METHOD_FAST2 2
+/* Extension (BASELINE config 3's wording, not in the reference): p columns of R drawn without
+ * replacement with probability proportional to their squared norm (Efraimidis-Spirakis keys log(u_j) / w_j,
+ * u_j host uniforms from the reference RNG), orthonormalised, one product R V, Nystrom tail as fast2. */
+#define FM_METHOD_FAST1_NORM2 3
 
 int32_t fm_abi_version(void);
 const char* fm_status_string(fm_status s);
@@ -67,6 +71,8 @@ fm_status fm_gaussian_matrix_real(int64_t m, int64_t p, uint64_t seed, double* o
  * from seeds[f] (fast2), or indices (frames x p int32) from seeds[f] (fast1). */
 fm_status fm_draw_omega_batch(int64_t frames, const uint64_t* seeds, int64_t m, int64_t p, float* omega);
 fm_status fm_draw_indices_batch(int64_t frames, const uint64_t* seeds, int64_t m, int64_t p, int32_t* indices);
+/* FM_METHOD_FAST1_NORM2 draws: u[f][j] = (float) Rng(seeds[f]).uniform01(), j < m (frames x m) */
+fm_status fm_draw_uniforms_batch(int64_t frames, const uint64_t* seeds, int64_t m, float* u);
 
 /* Synthetic BASELINE frames: frame f of a batch uses seed derive(base_seed, f0 + f).
  * x: frames x m x n complex64 interleaved row-major. angles (frames x k rad) / snr (frames)
@@ -105,7 +111,7 @@ fm_status fm_plan_workspace_bytes(fm_plan plan, int64_t* bytes);
 
 typedef struct fm_batch_io {
     const float* x;          /* frames x M x N complex64, row-major (FMCX order) */
-    const float* omega;      /* fast2: frames x M x p, row-major; else NULL */
+    const float* omega;      /* fast2: frames x M x p, row-major; fast1_norm2: frames x M uniforms; else NULL */
     const int32_t* indices;  /* fast1: frames x p sorted column indices; else NULL */
     float* spectrum;         /* frames x L fp32 pseudo-spectrum, or NULL */
     int32_t* peak_cells;     /* frames x K grid cells ascending (-1 past count) */

@@ -399,6 +399,49 @@ class AngleGrid:
         return self.theta0 + (span * i) / float(self.size - 1)
 
 
+def norm2_sample_indices(s: np.ndarray, c: int, seed: int) -> np.ndarray:
+    """EXTENSION, not in the reference (BASELINE config 3's wording): c column indices of S drawn
+    without replacement with probability proportional to ||S(:, j)||^2 — Efraimidis-Spirakis: the c largest
+    keys log(u_j) / w_j (ties: lower j; w_j = 0 never preferred), u_j = float32(j-th uniform01 of Rng(seed)).
+    Returned ascending. Restates the library's k_norm2_select."""
+    m = s.shape[0]
+    w = np.sum(np.abs(s) ** 2, axis=0)
+    u = uniform_stream(seed, m).astype(np.float32).astype(np.float64)
+    keys = np.full(m, -np.inf)
+    pos = w > 0
+    keys[pos] = np.log(u[pos]) / w[pos]
+    order = sorted(range(m), key=lambda j: (-keys[j], j))
+    return np.sort(np.array(order[:c], dtype=np.int64))
+
+
+def fast_music_1_norm2(s, k, c, seed, max_attempts=4, indices=None):
+    """EXTENSION (see norm2_sample_indices): the fast2 tail with the sketch S(:, I) in place of S Omega and
+    one power step — V = qr_orthonormal(S(:, I)), C = S V, W = pinv(V^H C), rank_restricted_subspace(C, W).
+    Rank-deficient samples are redrawn with derive(seed, 0xF257 + attempt) like fast_music_2.
+    `indices` fixes the selection (to check the tail on a given sample)."""
+    m = s.shape[0]
+    if k < 1 or k >= m:
+        raise ValueError("fast_music_1_norm2: need 1 <= K < M")
+    if c < k or c > m:
+        raise ValueError("fast_music_1_norm2: need K <= p <= M")
+    attempt = 0
+    while True:
+        draw_seed = seed if attempt == 0 else derive(seed, 0xF257 + attempt)
+        try:
+            idx = indices if indices is not None else norm2_sample_indices(s, c, draw_seed)
+            v = qr_orthonormal(s[:, idx])
+            cc = s @ v
+            w = pseudo_inverse(v.conj().T @ cc)
+            out = rank_restricted_subspace(cc, w, k, "fast1_norm2")
+            out.attempts = attempt + 1
+            out.indices = idx
+            return out
+        except RankDeficiencyError:
+            if attempt + 1 >= max_attempts or indices is not None:
+                raise
+        attempt += 1
+
+
 def block_lanczos_subspace(s, k, block, max_iterations):
     """R/src/estimators.cpp:154-222 — block Krylov with full reorthogonalisation; converged when the top-K
     Ritz values change by <= 1e-10 relative on two consecutive checks."""
@@ -570,7 +613,10 @@ def baseline_configs():
                     256, 18001, p=32, t=2, base_seed=4)
     c5 = PathConfig("c5", "exact", SceneSpec(256, 512, 8, -60.0, 60.0, 3.0, 20.0, 20.0),
                     512, 3601, base_seed=2)
-    return {c.name: c for c in (c1, c2, c3, c4, c5)}
+    # extension: config 3 with BASELINE's own sampling wording (norm^2-weighted; not in the reference, F6)
+    c3n = PathConfig("c3n", "fast1_norm2", SceneSpec(256, 512, 8, -60.0, 60.0, 3.0, 10.0, 30.0),
+                     1024, 3601, p=32, base_seed=2)
+    return {c.name: c for c in (c1, c2, c3, c4, c5, c3n)}
 
 
 def frame_inputs(cfg: PathConfig, f: int):
@@ -578,7 +624,7 @@ def frame_inputs(cfg: PathConfig, f: int):
     s = frame_seed(cfg.base_seed, f)
     if cfg.method == "fast2":
         return {"seed": derive(s, 4)}
-    if cfg.method == "fast1":
+    if cfg.method in ("fast1", "fast1_norm2"):
         return {"seed": derive(s, 3)}
     return {}
 
@@ -593,6 +639,8 @@ def run_frame(cfg: PathConfig, x: np.ndarray, f: int, grid: AngleGrid | None = N
         est = fast_music_2(s, k, cfg.p, cfg.t, fin["seed"])
     elif cfg.method == "fast1":
         est = fast_music_1(s, k, cfg.p, fin["seed"])
+    elif cfg.method == "fast1_norm2":
+        est = fast_music_1_norm2(s, k, cfg.p, fin["seed"])
     else:
         est = exact_signal_subspace(s, k)
     spec = music_spectrum(est.basis, grid, a_mat=a_mat)

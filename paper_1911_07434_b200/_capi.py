@@ -15,13 +15,13 @@ LIB_PATH = os.path.join(_HERE, "libfastmusic_b200.so")
 
 FM_OK, FM_EINVAL, FM_ERANK, FM_ENOCONV, FM_ESINGULAR, FM_ECUDA, FM_ENOTSUP, FM_EIO = range(8)
 FRAME_OK, FRAME_RANK, FRAME_NOCONV, FRAME_RANGE, FRAME_NONFINITE = 0, 1, 2, 4, 8
-METHOD = {"exact": 0, "fast1": 1, "fast2": 2}
+METHOD = {"exact": 0, "fast1": 1, "fast2": 2, "fast1_norm2": 3}
 
 # Every symbol declared in include/fastmusic_b200.h (checked by tests/test_capi_symbols.py).
 EXPORTED = [
     "fm_abi_version", "fm_status_string", "fm_last_error", "fm_device_info",
     "fm_rng_derive", "fm_rng_normals", "fm_sample_without_replacement", "fm_gaussian_matrix_real",
-    "fm_draw_omega_batch", "fm_draw_indices_batch", "fm_generate_frames",
+    "fm_draw_omega_batch", "fm_draw_indices_batch", "fm_draw_uniforms_batch", "fm_generate_frames",
     "fm_plan_create", "fm_plan_destroy", "fm_plan_workspace_bytes", "fm_run_batch", "fm_rerun_frames",
     "fm_plan_launches_per_batch", "fm_plan_set_profiling", "fm_plan_stage_times", "fm_plan_set_concurrency", "fm_estimate_batch_host",
     "fm_z_spatial_covariance", "fm_z_exact_signal_subspace", "fm_z_fast_music_1", "fm_z_fast_music_2",
@@ -73,6 +73,7 @@ def _load():
         "fm_gaussian_matrix_real": (i32, [i64, i64, u64, vp]),
         "fm_draw_omega_batch": (i32, [i64, vp, i64, i64, vp]),
         "fm_draw_indices_batch": (i32, [i64, vp, i64, i64, vp]),
+        "fm_draw_uniforms_batch": (i32, [i64, vp, i64, vp]),
         "fm_generate_frames": (i32, [vp, u64, i64, i64, vp, vp, vp, i32]),
         "fm_plan_create": (i32, [vp, i32, vp]),
         "fm_plan_destroy": (i32, [vp]),

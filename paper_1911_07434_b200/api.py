@@ -184,6 +184,14 @@ def draw_indices_batch(seeds, m: int, p: int) -> np.ndarray:
     return out
 
 
+def draw_uniforms_batch(seeds, m: int) -> np.ndarray:
+    """fast1_norm2 draws: u[f][j] = float32(Rng(seeds[f]).uniform01()), j < m."""
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    out = np.empty((seeds.size, m), np.float32)
+    _check(LIB.fm_draw_uniforms_batch(seeds.size, ptr(seeds), m, ptr(out)))
+    return out
+
+
 def generate_frames(m, n, k, base_seed, f0, frames, theta_lo_deg=-60.0, theta_hi_deg=60.0, min_sep_deg=3.0,
                     snr_lo_db=10.0, snr_hi_db=30.0, fixed_angles_deg=None, d=0.5, lam=1.0, threads=0, out=None):
     """Synthetic BASELINE frames; returns (x complex64 [frames, m, n], angles, snr)."""

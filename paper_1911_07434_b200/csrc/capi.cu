@@ -121,6 +121,87 @@ __global__ void k_basis_to_c32(const double* __restrict__ basis, float* __restri
     if (i < n) u32[i] = static_cast<float>(basis[i]);
 }
 
+// FM_METHOD_FAST1_NORM2 column selection (extension: BASELINE config 3's "columns of R sampled with
+// probability proportional to squared column norm"; not in the reference). One CTA per frame:
+// w_j = sum_i |R_ij|^2 (R Hermitian: the row norms; from the fp16 hi/lo planes the common factor s_f^2 is
+// dropped, which leaves the order of the keys unchanged), Efraimidis-Spirakis keys log(u_j) / w_j (the
+// p largest, ties to the lower index, give a weighted sample without replacement), bitonic sort in shared
+// memory, Omega = E_I (M x p row-major, I ascending) for the fast2 product kernel.
+__global__ void k_norm2_select(const float* __restrict__ R, const __half* __restrict__ hi, const __half* __restrict__ lo,
+                               const float* __restrict__ u, float* __restrict__ omega, int m, int p, int n2) {
+    extern __shared__ uint8_t nsm[];
+    double* key = reinterpret_cast<double*>(nsm);
+    int* idx = reinterpret_cast<int*>(key + n2);
+    const int f = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    // row norms: one warp per row, coalesced (the row is 2M reals: fp16 hi + lo planes, or fp32)
+    for (int j = warp; j < m; j += nw) {
+        const size_t row = (static_cast<size_t>(f) * m + j) * 2 * m;
+        double w = 0.0;
+        if (hi && (m & 3) == 0) {  // 16-byte rows: 8 halves per load from each plane
+            const uint4* h4 = reinterpret_cast<const uint4*>(hi + row);
+            const uint4* l4 = reinterpret_cast<const uint4*>(lo + row);
+            for (int e = lane; e < m / 4; e += 32) {
+                const uint4 a = h4[e], b = l4[e];
+                const __half2* ha = reinterpret_cast<const __half2*>(&a);
+                const __half2* hb = reinterpret_cast<const __half2*>(&b);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 x = __half22float2(ha[q]), y = __half22float2(hb[q]);
+                    const double v0 = static_cast<double>(x.x) + static_cast<double>(y.x);
+                    const double v1 = static_cast<double>(x.y) + static_cast<double>(y.y);
+                    w += v0 * v0 + v1 * v1;
+                }
+            }
+        } else if (hi) {
+            for (int e = lane; e < 2 * m; e += 32) {
+                const double v = static_cast<double>(__half2float(hi[row + e])) + static_cast<double>(__half2float(lo[row + e]));
+                w += v * v;
+            }
+        } else {
+            for (int e = lane; e < 2 * m; e += 32) {
+                const double v = R[row + e];
+                w += v * v;
+            }
+        }
+        w = fmk::warp_sum(w);
+        if (lane == 0) key[j] = w > 0.0 ? log(static_cast<double>(u[static_cast<size_t>(f) * m + j])) / w : -INFINITY;
+    }
+    for (int j = threadIdx.x; j < n2; j += blockDim.x) {
+        if (j >= m) key[j] = -INFINITY;
+        idx[j] = j < m ? j : 0x7fffffff;
+    }
+    __syncthreads();
+    // bitonic sort: key descending, index ascending
+    for (int k2 = 2; k2 <= n2; k2 <<= 1)
+        for (int jj = k2 >> 1; jj > 0; jj >>= 1) {
+            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                const int o = i ^ jj;
+                if (o > i) {
+                    const bool o_first = key[o] > key[i] || (key[o] == key[i] && idx[o] < idx[i]);
+                    if (((i & k2) == 0) ? o_first : !o_first) {
+                        const double tk = key[i];
+                        key[i] = key[o];
+                        key[o] = tk;
+                        const int ti = idx[i];
+                        idx[i] = idx[o];
+                        idx[o] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    // the p selected indices ascending: rank of each among the first p
+    float* om = omega + static_cast<size_t>(f) * m * p;
+    for (int e = threadIdx.x; e < m * p; e += blockDim.x) om[e] = 0.f;
+    __syncthreads();
+    for (int a = threadIdx.x; a < p; a += blockDim.x) {
+        int rank = 0;
+        for (int b = 0; b < p; ++b) rank += idx[b] < idx[a] ? 1 : 0;
+        om[static_cast<size_t>(idx[a]) * p + rank] = 1.f;
+    }
+}
+
 __device__ double* g_exact_ratio = nullptr;  // debug: per-frame residual / gap
 
 // Frame certified iff no flag from the iteration and max_k ||R u_k - lambda_k u_k|| <= tol * gap,
@@ -289,6 +370,15 @@ extern "C" fm_status fm_draw_omega_batch(int64_t frames, const uint64_t* seeds, 
     if (frames < 0 || m < 1 || p < 1) return fail(FM_EINVAL, "fm_draw_omega_batch: bad arguments");
     parallel_for(frames, hw_threads(0), [&](int64_t f) {
         fmhost::gaussian_matrix_real(m, p, seeds[f], omega + static_cast<size_t>(f) * m * p);
+    });
+    return FM_OK;
+}
+
+extern "C" fm_status fm_draw_uniforms_batch(int64_t frames, const uint64_t* seeds, int64_t m, float* u) {
+    if (frames < 0 || m < 1 || (frames > 0 && (!seeds || !u))) return fail(FM_EINVAL, "fm_draw_uniforms_batch: bad arguments");
+    parallel_for(frames, hw_threads(0), [&](int64_t f) {
+        fmhost::Rng r(seeds[f]);
+        for (int64_t j = 0; j < m; ++j) u[static_cast<size_t>(f) * m + j] = static_cast<float>(r.uniform01());
     });
     return FM_OK;
 }
@@ -490,11 +580,13 @@ static fm_status validate_desc(const fm_plan_desc* d) {
     if (!d) return fail(FM_EINVAL, "fm_plan_create: null descriptor");
     if (d->m < 2) return fail(FM_EINVAL, "plan: need M >= 2");
     if (d->n < 1) return fail(FM_EINVAL, "plan: need N >= 1");
-    const char* who = d->method == FM_METHOD_FAST2 ? "fast_music_2" : d->method == FM_METHOD_FAST1 ? "fast_music_1"
-                                                                                                 : "exact_signal_subspace";
+    const char* who = d->method == FM_METHOD_FAST2         ? "fast_music_2"
+                      : d->method == FM_METHOD_FAST1       ? "fast_music_1"
+                      : d->method == FM_METHOD_FAST1_NORM2 ? "fast_music_1_norm2"
+                                                           : "exact_signal_subspace";
     if (d->k < 1 || d->k >= d->m) return fail(FM_EINVAL, std::string(who) + ": need 1 <= K < M");
     if (d->k > 64) return fail(FM_ENOTSUP, "plan: K <= 64 supported");
-    if (d->method == FM_METHOD_FAST1 || d->method == FM_METHOD_FAST2) {
+    if (d->method == FM_METHOD_FAST1 || d->method == FM_METHOD_FAST2 || d->method == FM_METHOD_FAST1_NORM2) {
         if (d->p < d->k || d->p > d->m) return fail(FM_EINVAL, std::string(who) + ": need K <= p <= M");
         if (d->p > 64) return fail(FM_ENOTSUP, "plan: p <= 64 supported");
     } else if (d->method != FM_METHOD_EXACT) {
@@ -542,6 +634,7 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
     chk(pl->get(&pl->scratch_status, B));
     chk(pl->get(&pl->rscale, B));
     if (desc->n & 1) chk(pl->get(&pl->x_pad, B * M * (static_cast<size_t>(desc->n) + 1) * 2));
+    if (desc->method == FM_METHOD_FAST1_NORM2) chk(pl->get(&pl->omega_e, B * M * P));  // selection Omega = E_I
     if (pl->pe > 0) {
         chk(pl->get(&pl->omega_e, B * M * pl->pe));
         chk(pl->get(&pl->u32, B * K * M * 2));
@@ -622,7 +715,7 @@ static bool tc_rmul(int m, int p) {
 static bool plane_mode(const fm_plan_s* pl) {
     static const bool off = std::getenv("FM_NO_PLANES") != nullptr;
     // fast2 only: the exact method's Jacobi fallback and fast1's gather read complex64 R
-    return !off && pl->d.method == FM_METHOD_FAST2 && pl->d.m <= 256 &&
+    return !off && (pl->d.method == FM_METHOD_FAST2 || pl->d.method == FM_METHOD_FAST1_NORM2) && pl->d.m <= 256 &&
            tc_rmul(static_cast<int>(pl->d.m), static_cast<int>(pl->d.p));
 }
 struct Planes {  // per-sub-batch view; hi == nullptr: complex64 R
@@ -653,6 +746,7 @@ extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
     const int fin = tiled ? (split_final() ? 3 : 1) : 2;  // gram, small-warp, basis | fused | cholqr, nystrom
     const int orth = tiled && split_final() ? 3 : 1;  // gram, pivoted chol, rows solve | fused
     if (plan->d.method == FM_METHOD_FAST2) n += 1 + t * (orth + 1) + fin;  // rmul, t x (orth, rmul), final
+    else if (plan->d.method == FM_METHOD_FAST1_NORM2) n += 1 + 1 + (orth + 1) + fin;  // select, rmul, orth, rmul, final
     else if (plan->d.method == FM_METHOD_FAST1) n += 1 + fin;      // gather, final
     else if (plan->pe > 0) n += 1 + 1 + kExactIters * (3 + 1) + 3 + 1 + 1 + 1 + 1 + 1;  // see run_post_cov
     else n += 1;                                                    // jacobi
@@ -734,7 +828,7 @@ static fm_batch_io io_view(fm_plan pl, const fm_batch_io* io, int64_t f0) {
     const size_t M = d.m, N = d.n, P = d.p, K = d.k, L = d.grid_size;
     fm_batch_io o = *io;
     o.x = io->x + f0 * M * N * 2;
-    if (io->omega) o.omega = io->omega + f0 * M * P;
+    if (io->omega) o.omega = io->omega + f0 * M * (d.method == FM_METHOD_FAST1_NORM2 ? 1 : P);
     if (io->indices) o.indices = io->indices + f0 * P;
     if (io->spectrum) o.spectrum = io->spectrum + f0 * L;
     o.peak_cells = io->peak_cells + f0 * K;
@@ -799,12 +893,25 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
             FM_LAUNCH(fm_launch_rmul<float>(R, omega, v, c, nullptr, F, M, p, omega != nullptr, s));
         return FM_OK;
     };
-    if (d.method == FM_METHOD_FAST2) {
+    if (d.method == FM_METHOD_FAST2 || d.method == FM_METHOD_FAST1_NORM2) {
+        const float* omega = io->omega;
+        int tt = d.t;
+        if (d.method == FM_METHOD_FAST1_NORM2) {  // Omega = E_I from the norm^2-weighted selection, one power step
+            int n2 = 1;
+            while (n2 < static_cast<int>(M)) n2 <<= 1;
+            const int smem = n2 * static_cast<int>(sizeof(double) + sizeof(int));
+            if (smem > 48 * 1024) FM_CUDA_OK(cudaFuncSetAttribute(k_norm2_select, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            k_norm2_select<<<F, 256, smem, s>>>(pv.hi ? nullptr : R, static_cast<const __half*>(pv.hi),
+                                                static_cast<const __half*>(pv.lo), io->omega, w.omega_e, M, P, n2);
+            FM_LAUNCH(cudaGetLastError());
+            omega = w.omega_e;
+            tt = 1;
+        }
         // the first t products only shape the range (V); the last one feeds the Nystrom step
-        if ((st = rmul(io->omega, nullptr, w.C, P, d.t > 0)) != FM_OK) return st;
-        for (int it = 0; it < d.t; ++it) {
+        if ((st = rmul(omega, nullptr, w.C, P, tt > 0)) != FM_OK) return st;
+        for (int it = 0; it < tt; ++it) {
             if ((st = orth(false, nullptr)) != FM_OK) return st;
-            if ((st = rmul(nullptr, w.V, w.C, P, it + 1 < d.t)) != FM_OK) return st;
+            if ((st = rmul(nullptr, w.V, w.C, P, it + 1 < tt)) != FM_OK) return st;
         }
         if (tiled) {
             if (split_final())
@@ -875,6 +982,8 @@ static fm_status check_io(fm_plan pl, int64_t frames, const fm_batch_io* io) {
     if (!io->x || !io->peak_cells || !io->peak_heights || !io->baseline || !io->peak_count || !io->status)
         return fail(FM_EINVAL, "fm_run_batch: x, peak outputs and status are required");
     if (pl->d.method == FM_METHOD_FAST2 && !io->omega) return fail(FM_EINVAL, "fm_run_batch: fast2 needs omega");
+    if (pl->d.method == FM_METHOD_FAST1_NORM2 && !io->omega)
+        return fail(FM_EINVAL, "fm_run_batch: fast1_norm2 needs the uniforms in io->omega");
     if (pl->d.method == FM_METHOD_FAST1 && !io->indices) return fail(FM_EINVAL, "fm_run_batch: fast1 needs indices");
     return FM_OK;
 }
@@ -981,7 +1090,7 @@ extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const fl
             if (e == cudaSuccess) e = x;
         };
         chk(pl->get(&pl->x_dev, B * M * N * 2));
-        chk(pl->get(&pl->omega_dev, d.method == FM_METHOD_FAST2 ? B * M * P : 0));
+        chk(pl->get(&pl->omega_dev, d.method == FM_METHOD_FAST2 ? B * M * P : d.method == FM_METHOD_FAST1_NORM2 ? B * M : 0));
         chk(pl->get(&pl->idx_dev, d.method == FM_METHOD_FAST1 ? B * P : 0));
         chk(pl->get(&pl->spec_dev, B * L));
         chk(pl->get(&pl->cells_dev, B * K));
@@ -990,6 +1099,7 @@ extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const fl
         chk(pl->get(&pl->count_dev, B));
         chk(pl->get(&pl->status_dev, B));
         if (d.method == FM_METHOD_FAST2) chk(cudaMallocHost(&pl->omega_pinned, sizeof(float) * B * M * P));
+        if (d.method == FM_METHOD_FAST1_NORM2) chk(cudaMallocHost(&pl->omega_pinned, sizeof(float) * B * M));
         chk(cudaMallocHost(&pl->status_pinned, sizeof(int32_t) * B));
         chk(cudaStreamCreateWithFlags(&pl->copy_s, cudaStreamNonBlocking));
         for (cudaEvent_t& ev : pl->copy_ev) chk(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1014,9 +1124,11 @@ extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const fl
         const int64_t f0 = c * cs, fc = std::min(cs, frames - f0);
         const size_t xo = static_cast<size_t>(f0) * M * N * 2;
         FM_CUDA_OK(cudaMemcpyAsync(pl->x_dev + xo, h_x + xo, sizeof(float) * fc * M * N * 2, cudaMemcpyHostToDevice, cp));
-        if (c == 0 && d.method == FM_METHOD_FAST2) {
-            fm_draw_omega_batch(frames, draw_seeds, d.m, d.p, pl->omega_pinned);
-            FM_CUDA_OK(cudaMemcpyAsync(pl->omega_dev, pl->omega_pinned, sizeof(float) * frames * M * P,
+        if (c == 0 && (d.method == FM_METHOD_FAST2 || d.method == FM_METHOD_FAST1_NORM2)) {
+            const size_t per = d.method == FM_METHOD_FAST2 ? M * P : M;
+            if (d.method == FM_METHOD_FAST2) fm_draw_omega_batch(frames, draw_seeds, d.m, d.p, pl->omega_pinned);
+            else fm_draw_uniforms_batch(frames, draw_seeds, d.m, pl->omega_pinned);
+            FM_CUDA_OK(cudaMemcpyAsync(pl->omega_dev, pl->omega_pinned, sizeof(float) * frames * per,
                                        cudaMemcpyHostToDevice, cp));
         } else if (c == 0 && d.method == FM_METHOD_FAST1) {
             idx_host.resize(static_cast<size_t>(frames) * P);
@@ -1030,7 +1142,8 @@ extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const fl
     auto chunk_io = [&](int64_t f0) {
         fm_batch_io io{};
         io.x = pl->x_dev + static_cast<size_t>(f0) * M * N * 2;
-        io.omega = pl->omega_dev ? pl->omega_dev + static_cast<size_t>(f0) * M * P : nullptr;
+        io.omega = pl->omega_dev ? pl->omega_dev + static_cast<size_t>(f0) * M * (d.method == FM_METHOD_FAST2 ? P : 1)
+                                 : nullptr;
         io.indices = pl->idx_dev ? pl->idx_dev + static_cast<size_t>(f0) * P : nullptr;
         io.spectrum = out->spectrum ? pl->spec_dev + static_cast<size_t>(f0) * L : nullptr;
         io.peak_cells = pl->cells_dev + static_cast<size_t>(f0) * K;
@@ -1059,8 +1172,9 @@ extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const fl
     io.status = pl->status_dev;
     fm_status st = FM_OK;
     std::vector<int32_t> attempts(static_cast<size_t>(frames), 1);
-    if (d.method == FM_METHOD_FAST2) {
+    if (d.method == FM_METHOD_FAST2 || d.method == FM_METHOD_FAST1_NORM2) {
         // R/src/estimators.cpp:114-137: up to 3 sub-seeded redraws per rank-deficient frame.
+        const size_t per = d.method == FM_METHOD_FAST2 ? M * P : M;
         std::vector<uint64_t> seeds(draw_seeds, draw_seeds + frames);
         for (int attempt = 1; attempt < 4; ++attempt) {
             FM_CUDA_OK(cudaMemcpyAsync(pl->status_pinned, pl->status_dev, sizeof(int32_t) * frames,
@@ -1072,10 +1186,11 @@ extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const fl
                     any = true;
                     attempts[f] = attempt + 1;
                     const uint64_t ds = fmhost::Rng::derive(draw_seeds[f], 0xF257u + static_cast<uint64_t>(attempt));
-                    fmhost::gaussian_matrix_real(d.m, d.p, ds, pl->omega_pinned + static_cast<size_t>(f) * M * P);
-                    FM_CUDA_OK(cudaMemcpyAsync(pl->omega_dev + static_cast<size_t>(f) * M * P,
-                                               pl->omega_pinned + static_cast<size_t>(f) * M * P,
-                                               sizeof(float) * M * P, cudaMemcpyHostToDevice, s));
+                    float* dst = pl->omega_pinned + static_cast<size_t>(f) * per;
+                    if (d.method == FM_METHOD_FAST2) fmhost::gaussian_matrix_real(d.m, d.p, ds, dst);
+                    else fm_draw_uniforms_batch(1, &ds, d.m, dst);
+                    FM_CUDA_OK(cudaMemcpyAsync(pl->omega_dev + static_cast<size_t>(f) * per, dst, sizeof(float) * per,
+                                               cudaMemcpyHostToDevice, s));
                 }
             }
             if (!any) break;

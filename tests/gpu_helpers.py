@@ -14,6 +14,8 @@ def draws(fm, oracle, cfg, frames):
         return fm.draw_omega_batch([fm.derive(s, 4) for s in fseeds], cfg.spec.m, cfg.p), None
     if cfg.method == "fast1":
         return None, fm.draw_indices_batch([fm.derive(s, 3) for s in fseeds], cfg.spec.m, cfg.p)
+    if cfg.method == "fast1_norm2":  # uniforms travel in the omega slot
+        return fm.draw_uniforms_batch([fm.derive(s, 3) for s in fseeds], cfg.spec.m), None
     return None, None
 
 

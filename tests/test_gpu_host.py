@@ -15,7 +15,8 @@ def _device_run(fm, method, x, seeds, grid):
     frames = len(x)
     plan = fm.BatchPlan(M, N, K, method, p=P if method != "exact" else 0, t=1, grid_size=grid, max_frames=frames)
     xd = torch.from_numpy(np.ascontiguousarray(x).view(np.float32)).cuda()
-    om = torch.from_numpy(fm.draw_omega_batch(seeds, M, P)).cuda() if method == "fast2" else None
+    om = (torch.from_numpy(fm.draw_omega_batch(seeds, M, P)).cuda() if method == "fast2" else
+          torch.from_numpy(fm.draw_uniforms_batch(seeds, M)).cuda() if method == "fast1_norm2" else None)
     ix = torch.from_numpy(fm.draw_indices_batch(seeds, M, P)).cuda() if method == "fast1" else None
     out = plan.outputs(frames, spectrum=True)
     plan.run(frames, xd, om, ix, out)
@@ -42,7 +43,8 @@ def _host_run(fm, method, x, seeds, grid, max_frames=None):
 
 # 300 / 260 frames -> 2 chunks of 150 / 130; 130 -> 1 chunk; 5 frames in a larger plan
 @pytest.mark.parametrize("method,frames,max_frames", [("fast2", 300, None), ("fast1", 260, None),
-                                                      ("exact", 130, None), ("fast2", 5, 64)])
+                                                      ("exact", 130, None), ("fast2", 5, 64),
+                                                      ("fast1_norm2", 270, None)])
 def test_host_path_matches_device_run(fm, method, frames, max_frames):
     x, _, _ = fm.generate_frames(M, N, K, 31, 0, frames)
     seeds = np.array([fm.derive(77, f) for f in range(frames)], np.uint64)

@@ -204,3 +204,34 @@ def test_full_size_batch_properties(fm, oracle, cfgs, name, nframes, nsample):
     worst, mism = compare_frames(oracle, cfg, x[sample], sample, res)
     assert not mism, mism
     assert worst <= DB_TOL, worst
+
+
+def test_norm2_sampling_tail_on_the_same_covariance(fm, oracle, cfgs):
+    """fast1_norm2 (extension, BASELINE c3's sampling wording): with R exported (complex64, no fp16 planes) the
+    oracle run on that same R draws the same columns, so peaks must match exactly and spectra to rounding."""
+    cfg = cfgs["c3n"]
+    frames = list(range(10))
+    x = _data(oracle, cfg, frames)
+    res = run_gpu(fm, oracle, cfg, x, frames, covariance=True)
+    assert np.all(res["status"] == 0), res["status"]
+    grid = oracle.baseline_grid(cfg.grid_size)
+    for i, f in enumerate(frames):
+        r = res["cov_c"][i].astype(np.complex128)
+        est = oracle.fast_music_1_norm2(r, cfg.spec.k, cfg.p, oracle.frame_inputs(cfg, f)["seed"])
+        spec = oracle.music_spectrum(est.basis, grid)
+        pk = oracle.extract_peaks(spec, cfg.spec.k, cfg.min_sep_cells, grid)
+        n = int(res["peak_count"][i])
+        assert [int(c) for c in res["peak_cells"][i][:n]] == pk.cells, f
+        assert oracle.spectrum_db_error(res["spectrum"][i].astype(np.float64), spec) < 0.01, f
+
+
+def test_norm2_sampling_parity(fm, oracle, cfgs):
+    """fast1_norm2 on the production path (fp16-plane R) against the oracle on the fp64 covariance."""
+    cfg = cfgs["c3n"]
+    frames = list(range(16))
+    x = _data(oracle, cfg, frames)
+    res = run_gpu(fm, oracle, cfg, x, frames)
+    assert np.all(res["status"] == 0), res["status"]
+    worst, mism = compare_frames(oracle, cfg, x, frames, res)
+    assert not mism, mism
+    assert worst <= DB_TOL, worst
