@@ -23,6 +23,7 @@ CXX_SOURCES = ["facade.cpp", "io.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+EXTRA = os.environ.get("FM_NVCC_FLAGS", "").split()  # experiment switches, e.g. -DFM_COV_MAXNREG=72
 
 
 def _headers():
@@ -45,7 +46,7 @@ def _compile(src, force, headers):
     if not force and not _stale(obj, src, headers):
         return obj, None
     if src.endswith(".cu"):
-        cmd = [NVCC] + ARCH + COMMON + ["-lineinfo", "-Xptxas", "-v", "-c", src, "-o", obj]
+        cmd = [NVCC] + ARCH + COMMON + EXTRA + ["-lineinfo", "-Xptxas", "-v", "-c", src, "-o", obj]
     else:
         cmd = [NVCC, "-x", "cu"] + ARCH + COMMON + ["-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -52,13 +52,15 @@ cudaError_t fm_launch_final_tiled(const void* C, const void* V, const void* H, v
 cudaError_t fm_launch_rmul_tc(const float* d_r, const float* d_omega, const float* d_v, float* d_c, int64_t frames,
                               int64_t m, int64_t p, cudaStream_t stream);
 cudaError_t fm_launch_orth_split(const void* C, void* Vout, void* Lw, int32_t* permw, int32_t* status, int frames,
-                                 int m, int p, cudaStream_t s);
+                                 int m, int p, cudaStream_t s, const void* gpart = nullptr);
 cudaError_t fm_launch_rmul_planes(const void* planes_hi, const void* planes_lo, const float* d_scale,
                                   const float* d_omega, const float* d_v, float* d_c, int64_t frames, int64_t m,
-                                  int64_t p, cudaStream_t stream, bool hi_only);
+                                  int64_t p, cudaStream_t stream, bool hi_only, int gram = 0, double* gpart = nullptr,
+                                  double* hpart = nullptr);
 cudaError_t fm_launch_final_split(const void* C, const void* V, void* Hw, void* Gw, void* Tw, void* basis, double* eig,
                                   int32_t* status, int frames, int m, int p, int k, cudaStream_t s,
-                                  double* eig_next = nullptr);
+                                  double* eig_next = nullptr, const void* gpart = nullptr,
+                                  const void* hpart = nullptr);
 cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, int k, cudaStream_t s);
 cudaError_t fm_launch_spectrum_peaks(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
                                      double* spec64, int K, int min_sep, int32_t* cells, double* heights,
@@ -499,6 +501,8 @@ struct fm_plan_s {
     float* u32 = nullptr;       // frames x K x M complex64 (U for R U)
     float* ru = nullptr;        // frames x K x M complex64
     double* eig_next = nullptr; // frames
+    double* gpart = nullptr;    // frames x 2 x p x p complex: G halves from the product epilogue (plane path)
+    double* hpart = nullptr;    // frames x 2 x p x p complex: H = V^H C halves (last product)
     // host-path staging
     float* x_dev = nullptr;
     float* omega_dev = nullptr;
@@ -635,6 +639,10 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
     chk(pl->get(&pl->rscale, B));
     if (desc->n & 1) chk(pl->get(&pl->x_pad, B * M * (static_cast<size_t>(desc->n) + 1) * 2));
     if (desc->method == FM_METHOD_FAST1_NORM2) chk(pl->get(&pl->omega_e, B * M * P));  // selection Omega = E_I
+    if ((desc->method == FM_METHOD_FAST2 || desc->method == FM_METHOD_FAST1_NORM2) && M <= 256 && P <= 16) {
+        chk(pl->get(&pl->gpart, B * 2 * P * P * 2));  // Gram halves from the product epilogue (plane path)
+        chk(pl->get(&pl->hpart, B * 2 * P * P * 2));
+    }
     if (pl->pe > 0) {
         chk(pl->get(&pl->omega_e, B * M * pl->pe));
         chk(pl->get(&pl->u32, B * K * M * 2));
@@ -743,8 +751,10 @@ extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
     const int t = plan->d.t;
     int n = 1 /*cov*/ + 1 /*clear*/ + 3 /*autocorr, spectrum, peaks*/ + (plan->x_pad ? 1 : 0) /*odd-N pad*/;
     const bool tiled = plan->d.p <= 32 && (plan->d.p % 4) == 0;
-    const int fin = tiled ? (split_final() ? 3 : 1) : 2;  // gram, small-warp, basis | fused | cholqr, nystrom
-    const int orth = tiled && split_final() ? 3 : 1;  // gram, pivoted chol, rows solve | fused
+    // Gram epilogue (plane path, p <= 16): the Gram kernels are folded into the products
+    const int gepi = tiled && split_final() && plane_mode(plan) && plan->d.p <= 16 && !std::getenv("FM_NO_GRAM_EPI") ? 1 : 0;
+    const int fin = tiled ? (split_final() ? 3 - gepi : 1) : 2;  // gram, small-warp, basis | fused | cholqr, nystrom
+    const int orth = tiled && split_final() ? 3 - gepi : 1;  // gram, pivoted chol, rows solve | fused
     if (plan->d.method == FM_METHOD_FAST2) n += 1 + t * (orth + 1) + fin;  // rmul, t x (orth, rmul), final
     else if (plan->d.method == FM_METHOD_FAST1_NORM2) n += 1 + 1 + (orth + 1) + fin;  // select, rmul, orth, rmul, final
     else if (plan->d.method == FM_METHOD_FAST1) n += 1 + fin;      // gather, final
@@ -798,6 +808,8 @@ struct WorkView {
     float* u32;
     float* ru;
     double* eig_next;
+    double* gpart;
+    double* hpart;
 };
 
 static WorkView work_view(fm_plan pl, int64_t f0) {
@@ -810,6 +822,8 @@ static WorkView work_view(fm_plan pl, int64_t f0) {
     w.u32 = pl->u32 ? pl->u32 + f0 * K * M * 2 : nullptr;
     w.ru = pl->ru ? pl->ru + f0 * K * M * 2 : nullptr;
     w.eig_next = pl->eig_next ? pl->eig_next + f0 : nullptr;
+    w.gpart = pl->gpart ? pl->gpart + f0 * 2 * P * P * 2 : nullptr;
+    w.hpart = pl->hpart ? pl->hpart + f0 * 2 * P * P * 2 : nullptr;
     w.C = pl->C + f0 * P * M * 2;
     w.V = pl->V + f0 * P * M * 2;
     w.work = pl->work + f0 * wsz;
@@ -853,10 +867,15 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     FM_CUDA_OK(cudaGetLastError());
     const bool warp_path = P <= 32;  // block-per-frame small-matrix kernels (smallmat.cu)
     const bool tiled = P <= 32 && (P % 4) == 0;  // register-tiled Gram + fused final stage
+    // Gram epilogue (plane path, p <= 16): the products also form G = C^H C (and H = V^H C on the last one),
+    // so the orthonormalisation / final stage skip their Gram kernels. FM_NO_GRAM_EPI=1: separate kernels.
+    static const bool no_gram_epi = std::getenv("FM_NO_GRAM_EPI") != nullptr;
+    const bool gepi = pv.hi && w.gpart && P <= 16 && tiled && split_final() && !no_gram_epi;
     auto orth = [&](bool final_mode, const void* vin) -> fm_status {
         if (tiled && !final_mode) {
             if (split_final())
-                FM_LAUNCH(fm_launch_orth_split(w.C, w.V, w.Rt, reinterpret_cast<int32_t*>(w.H), io->status, F, M, P, s));
+                FM_LAUNCH(fm_launch_orth_split(w.C, w.V, w.Rt, reinterpret_cast<int32_t*>(w.H), io->status, F, M, P, s,
+                                               gepi ? w.gpart : nullptr));
             else
                 FM_LAUNCH(fm_launch_orth_tiled(w.C, w.V, io->status, F, M, P, s));
             return FM_OK;
@@ -884,9 +903,11 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     // 1024 c2 frames vs the fp64 oracle: worst spectrum error 0.00556 -> 0.00557 dB, no peak changes,
     // step 1.191 -> 1.140 ms (scripts_precision_sweep.py). FM_RMUL_HI_ONLY=0 reads both planes everywhere.
     const bool hi_only_env = !(std::getenv("FM_RMUL_HI_ONLY") && std::atoi(std::getenv("FM_RMUL_HI_ONLY")) == 0);
-    auto rmul = [&](const float* omega, const float* v, float* c, int p, bool range_only = false) -> fm_status {
+    auto rmul = [&](const float* omega, const float* v, float* c, int p, bool range_only = false,
+                    int gram = 0) -> fm_status {
         if (pv.hi)
-            FM_LAUNCH(fm_launch_rmul_planes(pv.hi, pv.lo, pv.scale, omega, v, c, F, M, p, s, range_only && hi_only_env));
+            FM_LAUNCH(fm_launch_rmul_planes(pv.hi, pv.lo, pv.scale, omega, v, c, F, M, p, s, range_only && hi_only_env,
+                                            gepi ? gram : 0, w.gpart, w.hpart));
         else if (tc_rmul(M, p))
             FM_LAUNCH(fm_launch_rmul_tc(R, omega, v, c, F, M, p, s));
         else
@@ -908,14 +929,15 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
             tt = 1;
         }
         // the first t products only shape the range (V); the last one feeds the Nystrom step
-        if ((st = rmul(omega, nullptr, w.C, P, tt > 0)) != FM_OK) return st;
+        if ((st = rmul(omega, nullptr, w.C, P, tt > 0, 1)) != FM_OK) return st;
         for (int it = 0; it < tt; ++it) {
             if ((st = orth(false, nullptr)) != FM_OK) return st;
-            if ((st = rmul(nullptr, w.V, w.C, P, it + 1 < tt)) != FM_OK) return st;
+            if ((st = rmul(nullptr, w.V, w.C, P, it + 1 < tt, it + 1 < tt ? 1 : 2)) != FM_OK) return st;
         }
         if (tiled) {
             if (split_final())
-                FM_LAUNCH(fm_launch_final_split(w.C, w.V, w.H, w.Rt, w.work, basis, eig, io->status, F, M, P, K, s));
+                FM_LAUNCH(fm_launch_final_split(w.C, w.V, w.H, w.Rt, w.work, basis, eig, io->status, F, M, P, K, s,
+                                                nullptr, gepi ? w.gpart : nullptr, gepi ? w.hpart : nullptr));
             else
                 FM_LAUNCH(fm_launch_final_tiled(w.C, w.V, nullptr, basis, eig, io->status, F, M, P, K, s));
         } else {

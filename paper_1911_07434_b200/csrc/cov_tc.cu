@@ -63,6 +63,12 @@ constexpr int kSmemEpilogue = 4 * kEpiWarpBytes;            // >= 4 * 32 * kEpiL
 static_assert(kSmemEpilogue >= 4 * 32 * kEpiLd * 8, "epilogue region");
 constexpr int kSmemBytes = 1024 + kSmemStaging + kSmemOperand + kSmemEpilogue + kSmemBarriers;
 
+// Staging + operand bytes of a packed ring (general S, general O, diag S, diag O), rounded up to 1 KB.
+__host__ __device__ constexpr int ring_region_bytes(int ring, bool diag_only) {
+    return diag_only ? (((ring >> 16) & 0xff) * kStageBytes + ((ring >> 24) & 0xff) * kOpBytes + 1023) / 1024 * 1024
+                     : ((ring & 0xff) * 2 * kStageBytes + ((ring >> 8) & 0xff) * 2 * kOpBytes + 1023) / 1024 * 1024;
+}
+
 // PTX wrappers: tc_common.cuh
 using namespace fmk::tc;
 
@@ -154,7 +160,12 @@ __device__ __forceinline__ void convert_tile(const uint8_t* stage, uint8_t* op, 
 // operand conversion of multi-tile frames (every 256-row block of X is converted once per tile it feeds,
 // 4x at M = 1024) makes the converters the bottleneck there.
 template <int kEpi, bool kConv8>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((kEpi == 2 ? kThreadsP : kThreads) + (kConv8 ? 128 : 0), 1)
+#ifdef FM_COV_MAXNREG  // experiment: register cap so fp64 kernels of another sub-batch can co-reside
+#define FM_COV_BOUNDS(t) __maxnreg__(FM_COV_MAXNREG)
+#else
+#define FM_COV_BOUNDS(t) __launch_bounds__(t, 1)
+#endif
+__global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP : kThreads) + (kConv8 ? 128 : 0))
     cov_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap rmap,
                   const __grid_constant__ CUtensorMap mmap, float* __restrict__ r_out, int32_t* __restrict__ status,
                   int m, int n, int tiles_per_frame, int total_tiles, float* __restrict__ rscale,
@@ -168,7 +179,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((kEpi == 2 ? kThread
     // ring: (general staging, general operand, diag staging, diag operand) depths, packed 4 x 8 bits
     const int gS = ring & 0xff, gO = (ring >> 8) & 0xff, dS = (ring >> 16) & 0xff, dO = (ring >> 24) & 0xff;
     uint8_t* operand = smem + (tiles_per_frame == 1 ? dS * kStageBytes : gS * 2 * kStageBytes);
-    uint8_t* epi_bytes = smem + kSmemStaging + kSmemOperand;  // 1024-aligned (128B-swizzled TMA store boxes)
+    // epilogue region right after the rings (1024-aligned for the 128B-swizzled TMA store boxes)
+    uint8_t* epi_bytes = smem + ring_region_bytes(ring, tiles_per_frame == 1);
     uint64_t* bars = reinterpret_cast<uint64_t*>(epi_bytes + kSmemEpilogue);
     uint64_t* stage_full = bars;
     uint64_t* stage_empty = bars + kMaxStages;
@@ -612,7 +624,11 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
         rmap = map;  // unused by the fallback epilogue
         mmap = map;
     }
-    static const bool conv4 = std::getenv("FM_COV_CONV4") != nullptr;  // comparison: four converter warps
+    // four converter warps for diagonal-only launches (M <= 256: one tile per frame, no redundant conversion;
+    // c2 covariance 0.342 -> 0.333 ms, scripts_coresidency.sh), eight for multi-tile frames.
+    // FM_COV_CONV4 / FM_COV_CONV8 force either (comparison).
+    static const bool force4 = std::getenv("FM_COV_CONV4") != nullptr, force8 = std::getenv("FM_COV_CONV8") != nullptr;
+    const bool conv4 = force4 || (!force8 && m <= 256);
     // ring depths (stages) general staging / operand, diagonal-only staging / operand; FM_COV_RING=a,b,c,d
     int rs[4] = {kStagesS, kStagesO, kDiagS, kDiagO};
     if (const char* r = std::getenv("FM_COV_RING")) {
@@ -652,7 +668,8 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
     const dim3 grid(static_cast<unsigned>(2 * pairs));
     auto go = [&](auto kern, bool conv8) {
         const int threads = (epi == 2 ? kThreadsP : kThreads) + (conv8 ? 128 : 0);
-        kern<<<grid, threads, kSmemBytes, stream>>>(map, rmap, mmap, d_r, d_status, static_cast<int>(m),
+        const int smem = 1024 + ring_region_bytes(ring, tiles_per_frame == 1) + kSmemEpilogue + kSmemBarriers;
+        kern<<<grid, threads, smem, stream>>>(map, rmap, mmap, d_r, d_status, static_cast<int>(m),
                                                      static_cast<int>(n), tiles_per_frame, static_cast<int>(tiles),
                                                      scale, static_cast<float>(1.0 / static_cast<double>(n_true)),
                                                      dbg_flags(), ring);

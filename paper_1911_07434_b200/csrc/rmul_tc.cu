@@ -343,19 +343,43 @@ __device__ __forceinline__ void split8(const float (&x)[8], uint4& hi, uint4& lo
     lo = make_uint4(pack_h2(l[0], l[1]), pack_h2(l[2], l[3]), pack_h2(l[4], l[5]), pack_h2(l[6], l[7]));
 }
 
-template <int PH, bool REAL, bool LO>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// Gram epilogue (GM > 0, PH = 16, M <= 256): the epilogue also forms this CTA's 128-row partial of
+// G = C^H C (GM >= 1) and of H = V^H C (GM = 2) in fp64 from the complex64 C it writes (the values the
+// separate Gram kernels would read back), as upper 4 x 4 tiles mirrored (tiled_gram2's convention,
+// smallmat.cu). Partials: gpart / hpart[(frame * 2 + rank) * p * p], column-major; consumers add the
+// two CTA halves. Replaces k_gram_only / k_gram_gh on the power-iteration path.
+template <int GM>
+__host__ __device__ constexpr int plane_stages() {  // the fp64 C and V tiles of GM = 2 leave room for 3 stages
+    return GM == 2 ? 3 : kPStages;
+}
+template <int PH, int GM>
+__host__ __device__ constexpr int plane_gram_off() {  // fp64 tiles after the stages and barriers
+    return plane_stages<GM>() * PCfg<PH>::kStageBytes + 256;
+}
+template <int PH, int GM>
+__host__ __device__ constexpr int plane_smem() {
+    return 1024 + plane_gram_off<PH, GM>() + (GM == 0 ? 0 : (GM == 2 ? 2 : 1) * kRows * (PH + 1) * 16);
+}
+
+constexpr int kThreadsG = kThreads + 128;  // Gram epilogue: w10..w13 form the Gram halves
+
+template <int PH, bool REAL, bool LO, int GM = 0>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM ? kThreadsG : kThreads, 1)
     rmul_planes_kernel(const __grid_constant__ CUtensorMap hmap, const __grid_constant__ CUtensorMap lmap,
                        const __grid_constant__ CUtensorMap vmap, const float* __restrict__ rscale,
-                       float* __restrict__ c_out, int m, int p, int tiles_per_frame, int total_tiles) {
+                       float* __restrict__ c_out, int m, int p, int tiles_per_frame, int total_tiles,
+                       const float* __restrict__ v_in, double* __restrict__ gpart, double* __restrict__ hpart,
+                       int gdbg) {
+    static_assert(GM == 0 || PH == 16, "Gram epilogue: PH = 16");
+    constexpr int NST = plane_stages<GM>();
     using C = PCfg<PH>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024 - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023)) & 1023);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kPStages * C::kStageBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * C::kStageBytes);
     uint64_t* full = bars;
-    uint64_t* op_full = bars + kPStages;
-    uint64_t* empty = bars + 2 * kPStages;
-    uint64_t* acc_full = bars + 3 * kPStages;
+    uint64_t* op_full = bars + NST;
+    uint64_t* empty = bars + 2 * NST;
+    uint64_t* acc_full = bars + 3 * NST;
     uint64_t* acc_empty = acc_full + kAcc;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + kAcc);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -364,7 +388,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int nk = (2 * m + kPKc - 1) / kPKc;
     const uint32_t vbytes = REAL ? 32u * p * 4u : static_cast<uint32_t>(p) * 256u;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kPStages; ++s) {
+        for (int s = 0; s < NST; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
             mbar_init(smem_u32(&op_full[s]), 2);
             mbar_init(smem_u32(&empty[s]), 1);
@@ -398,9 +422,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int frame = tile / tiles_per_frame, rb = tile % tiles_per_frame;
                 const int y = 256 * rb + 128 * static_cast<int>(rank);
                 for (int kc = 0; kc < nk; ++kc, ++g) {
-                    const int s = g % kPStages;
+                    const int s = g % NST;
                     uint8_t* st = smem + s * C::kStageBytes;
-                    mbar_wait(smem_u32(&empty[s]), ((g / kPStages) & 1) ^ 1);
+                    mbar_wait(smem_u32(&empty[s]), ((g / NST) & 1) ^ 1);
                     const uint32_t fb = smem_u32(&full[s]);
                     mbar_arrive_expect_tx(fb, (LO ? 2 : 1) * kABytes + vbytes);
                     tma_3d(smem_u32(st), &hmap, fb, kPKc * kc, y, frame);
@@ -420,8 +444,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 const uint32_t d = tmem + static_cast<uint32_t>(b * C::kN1);
                 for (int kc = 0; kc < nk; ++kc, ++g) {
-                    const int s = g % kPStages;
-                    mbar_wait_cluster(smem_u32(&op_full[s]), (g / kPStages) & 1);
+                    const int s = g % NST;
+                    mbar_wait_cluster(smem_u32(&op_full[s]), (g / NST) & 1);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + s * C::kStageBytes);
 #pragma unroll
@@ -444,9 +468,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int g = 0;
         for (int tile = pair; tile < total_tiles; tile += npairs) {
             for (int kc = 0; kc < nk; ++kc, ++g) {
-                const int s = g % kPStages;
+                const int s = g % NST;
                 uint8_t* st = smem + s * C::kStageBytes;
-                mbar_wait(smem_u32(&full[s]), (g / kPStages) & 1);
+                mbar_wait(smem_u32(&full[s]), (g / NST) & 1);
 #pragma unroll
                 for (int u = 0; u < PH / 16; ++u) {
                     const int c = bc + 16 * u;
@@ -499,6 +523,73 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
             }
         }
+    } else if (warp >= kThreads / 32) {
+        if constexpr (GM > 0) {
+            // Gram warps: per frame, this CTA's 128-row halves of G = C^H C (and H = V^H C for GM = 2) in fp64
+            // from the tile the epilogue staged; upper 4 x 4 tiles, mirrored (tiled_gram2's convention).
+            constexpr int ld = PH + 1;
+            const fmk::c64* sC = reinterpret_cast<const fmk::c64*>(smem + plane_gram_off<PH, GM>());
+            const fmk::c64* sV = sC + kRows * ld;
+            constexpr int RG = GM == 2 ? 4 : 8;  // row groups (consecutive lanes) per 4 x 4 tile
+            const int et = threadIdx.x - kThreads;
+            const int nb = p >> 2, t1 = nb * (nb + 1) / 2;
+            const int gt = et / RG, rg = et % RG;
+            const bool second = gt >= t1;
+            const bool active = gt < (GM == 2 ? 2 : 1) * t1;
+            int ti = 0, tj = 0;
+            if (active) {
+                int rem = second ? gt - t1 : gt;
+                while (rem >= nb - ti) { rem -= nb - ti; ++ti; }
+                tj = ti + rem;
+            }
+            const fmk::c64* xs = second ? sV : sC;
+            for (int tile = pair; tile < total_tiles; tile += npairs) {
+                const int frame = tile / tiles_per_frame;
+                fmk::c64 acc[4][4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) acc[a][b] = fmk::mk(0.0, 0.0);
+                named_bar_sync(4, 256);  // tile full
+                if (active && !(gdbg & 1)) {
+#pragma unroll 4
+                    for (int r = rg; r < kRows; r += RG) {
+                        fmk::c64 x[4], y[4];
+#pragma unroll
+                        for (int a = 0; a < 4; ++a) {
+                            x[a] = xs[r * ld + 4 * ti + a];
+                            y[a] = sC[r * ld + 4 * tj + a];
+                        }
+#pragma unroll
+                        for (int a = 0; a < 4; ++a)
+#pragma unroll
+                            for (int b = 0; b < 4; ++b) fmk::cmac_conj(acc[a][b], x[a], y[b]);
+                    }
+                }
+                if (tile + npairs < total_tiles) named_bar_arrive(5, 256);  // tile free for the next frame
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+#pragma unroll
+                        for (int o = 1; o < RG; o <<= 1) {
+                            acc[a][b].re += __shfl_xor_sync(0xffffffffu, acc[a][b].re, o);
+                            acc[a][b].im += __shfl_xor_sync(0xffffffffu, acc[a][b].im, o);
+                        }
+                if (active && rg == 0) {
+                    fmk::c64* G = reinterpret_cast<fmk::c64*>(second ? hpart : gpart) +
+                                  (static_cast<size_t>(frame) * 2 + rank) * p * p;
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const int i = 4 * ti + a, j = 4 * tj + b;
+                            G[j * p + i] = acc[a][b];
+                            if (ti != tj) G[i * p + j] = fmk::conj(acc[a][b]);
+                        }
+                }
+            }
+        }
     } else {
         // epilogue: C = s_f (D_hi + D_lo), column-major p x M complex
         const int quarter = warp & 3;
@@ -532,6 +623,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         cf[static_cast<size_t>(c) * m + row] =
                             make_float2(sf * (__uint_as_float(v[c]) + __uint_as_float(v[2 * PH + c])),
                                         sf * (__uint_as_float(v[PH + c]) + __uint_as_float(v[3 * PH + c])));
+            }
+            if constexpr (GM > 0) {
+                // hand this row of C (and of V) to the Gram warps through the shared tile; rows >= m are zero.
+                // Barrier 5: the Gram warps finished reading the previous frame's tile; barrier 4: tile full.
+                constexpr int ld = PH + 1;
+                fmk::c64* sC = reinterpret_cast<fmk::c64*>(smem + plane_gram_off<PH, GM>());
+                fmk::c64* sV = sC + kRows * ld;
+                const int lr = 32 * quarter + lane;
+                const bool ok = row < m;
+                float2 vv[PH];
+                if constexpr (GM == 2) {
+                    const float2* vf = reinterpret_cast<const float2*>(v_in) + static_cast<size_t>(frame) * m * p;
+#pragma unroll
+                    for (int c = 0; c < PH; ++c) vv[c] = (ok && c < p) ? vf[static_cast<size_t>(c) * m + row] : make_float2(0.f, 0.f);
+                }
+                if (t > 0) named_bar_sync(5, 256);
+#pragma unroll
+                for (int c = 0; c < PH; ++c) {  // the complex64 values written to C, widened once
+                    const float re = sf * (__uint_as_float(v[c]) + __uint_as_float(v[2 * PH + c]));
+                    const float im = sf * (__uint_as_float(v[PH + c]) + __uint_as_float(v[3 * PH + c]));
+                    sC[lr * ld + c] = (ok && c < p) ? fmk::mk(static_cast<double>(re), static_cast<double>(im))
+                                                    : fmk::mk(0.0, 0.0);
+                }
+                if constexpr (GM == 2) {
+#pragma unroll
+                    for (int c = 0; c < PH; ++c)
+                        sV[lr * ld + c] = fmk::mk(static_cast<double>(vv[c].x), static_cast<double>(vv[c].y));
+                }
+                named_bar_arrive(4, 256);
             }
         }
     }
@@ -619,9 +739,12 @@ extern "C" int32_t fm_debug_rmul_tc(const float* d_r, const float* d_omega, cons
 
 // C = R V / C = R Omega from the fp16 hi / lo planes of R / s_f (M <= 256, M even, p % 4 == 0, p <= 32).
 // hi_only: skip the lo plane (R represented to 2^-12 s_f instead of 2^-24 s_f; half the R bytes read).
+// gram: 0 none, 1 G partials -> gpart, 2 G and H = V^H C partials -> gpart, hpart (p <= 16, V products only
+// for 2); see rmul_planes_kernel.
 cudaError_t fm_launch_rmul_planes(const void* planes_hi, const void* planes_lo, const float* d_scale,
                                   const float* d_omega, const float* d_v, float* d_c, int64_t frames, int64_t m,
-                                  int64_t p, cudaStream_t stream, bool hi_only) {
+                                  int64_t p, cudaStream_t stream, bool hi_only, int gram, double* gpart,
+                                  double* hpart) {
     using namespace fmk::rmtc;
     if (frames < 1 || m < 2 || (m & 1) || m > 256 || p < 4 || p > 32 || (p & 3) || (!d_omega == !d_v))
         return cudaErrorInvalidValue;
@@ -669,13 +792,26 @@ cudaError_t fm_launch_rmul_planes(const void* planes_hi, const void* planes_lo, 
     static const int cap_pairs = std::getenv("FM_TC_PAIRS") ? std::atoi(std::getenv("FM_TC_PAIRS")) : 0;  // experiment
     const int64_t pairs = std::min<int64_t>(tiles, std::max(1, cap_pairs > 0 ? cap_pairs : sm_count / 2));
     const dim3 grid(static_cast<unsigned>(2 * pairs));
+    static const int gdbg = std::getenv("FM_GRAM_DBG") ? std::atoi(std::getenv("FM_GRAM_DBG")) : 0;  // experiment
     auto go = [&](auto kern, int smem) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        kern<<<grid, kThreads, smem, stream>>>(hmap, lmap, vmap, d_scale, d_c, static_cast<int>(m), static_cast<int>(p),
-                                               tiles_per_frame, static_cast<int>(tiles));
+        kern<<<grid, gram > 0 ? kThreadsG : kThreads, smem, stream>>>(hmap, lmap, vmap, d_scale, d_c, static_cast<int>(m),
+                                                                       static_cast<int>(p), tiles_per_frame,
+                                                                       static_cast<int>(tiles), d_v, gpart, hpart, gdbg);
         return cudaGetLastError();
     };
+    if (gram > 0) {
+        if (p > 16 || !gpart || (gram == 2 && (!hpart || d_omega))) return cudaErrorInvalidValue;
+        if (gram == 2)
+            return hi_only ? go(rmul_planes_kernel<16, false, false, 2>, plane_smem<16, 2>())
+                           : go(rmul_planes_kernel<16, false, true, 2>, plane_smem<16, 2>());
+        if (d_omega)
+            return hi_only ? go(rmul_planes_kernel<16, true, false, 1>, plane_smem<16, 1>())
+                           : go(rmul_planes_kernel<16, true, true, 1>, plane_smem<16, 1>());
+        return hi_only ? go(rmul_planes_kernel<16, false, false, 1>, plane_smem<16, 1>())
+                       : go(rmul_planes_kernel<16, false, true, 1>, plane_smem<16, 1>());
+    }
     if (hi_only) {
         if (p <= 16)
             return d_omega ? go(rmul_planes_kernel<16, true, false>, PCfg<16>::kSmem)

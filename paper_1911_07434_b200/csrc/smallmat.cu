@@ -1062,7 +1062,8 @@ template <int PC>
 __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
     k_small_warp(const c64* __restrict__ Gin, const c64* __restrict__ Hin, c64* __restrict__ Tout,
                  double* __restrict__ eig, int32_t* __restrict__ status, int frames, int p, int k,
-                 int32_t* __restrict__ dbg, double* __restrict__ eig_next) {
+                 int32_t* __restrict__ dbg, double* __restrict__ eig_next, const c64* __restrict__ gpart,
+                 const c64* __restrict__ hpart) {
     using W = WarpCfg<PC>;
     constexpr int LPC = W::kLPC;
     extern __shared__ uint8_t dsm[];
@@ -1078,6 +1079,17 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
     const c64* Gf = Gin + static_cast<size_t>(f) * p * p;
     const c64* Hf = Hin + static_cast<size_t>(f) * p * p;
     const long long T0 = clock64();
+    if (gpart) {  // G, H halves from the product kernel's epilogue; H symmetrised as k_gram_gh does
+        const size_t pp = static_cast<size_t>(p) * p;
+        const c64* g0 = gpart + static_cast<size_t>(f) * 2 * pp;
+        const c64* h0 = hpart + static_cast<size_t>(f) * 2 * pp;
+        for (int e = lane; e < p * p; e += 32) {
+            const int i = e % p, j = e / p;
+            const c64 a = h0[e] + h0[pp + e], b = h0[i * p + j] + h0[pp + i * p + j];
+            L[e] = g0[e] + g0[pp + e];
+            LH[e] = mk(0.5 * (a.re + b.re), 0.5 * (a.im - b.im));
+        }
+    } else
     for (int e0 = 0; e0 < p * p; e0 += 8 * 32) {  // 16 loads in flight per lane
         c64 g[8], hh[8];
 #pragma unroll
@@ -1411,7 +1423,7 @@ template <int PC> struct PivCfg {
 template <int PC>
 __global__ void __launch_bounds__(32 * PivCfg<PC>::kWarps)
     k_cholpiv_warp(c64* __restrict__ GL, int32_t* __restrict__ perm_out, int32_t* __restrict__ status, int frames,
-                   int m, int p) {
+                   int m, int p, const c64* __restrict__ gpart) {
     extern __shared__ uint8_t dsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int f = blockIdx.x * PivCfg<PC>::kWarps + warp;
@@ -1420,9 +1432,17 @@ __global__ void __launch_bounds__(32 * PivCfg<PC>::kWarps)
     c64* L = A + PC * PC;
     double* d = reinterpret_cast<double*>(L + PC * PC);
     c64* GLf = GL + static_cast<size_t>(f) * p * p;
-    for (int e = lane; e < p * p; e += 32) {
-        A[e] = GLf[e];
-        L[e] = mk(0.0, 0.0);
+    if (gpart) {  // G = sum of the two CTA halves formed in the product kernel's epilogue (rmul_tc.cu)
+        const c64* g0 = gpart + static_cast<size_t>(f) * 2 * p * p;
+        for (int e = lane; e < p * p; e += 32) {
+            A[e] = g0[e] + g0[p * p + e];
+            L[e] = mk(0.0, 0.0);
+        }
+    } else {
+        for (int e = lane; e < p * p; e += 32) {
+            A[e] = GLf[e];
+            L[e] = mk(0.0, 0.0);
+        }
     }
     __syncwarp();
     bool done = lane >= p;  // lane i <-> original row / column i
@@ -1618,19 +1638,24 @@ cudaError_t fm_launch_final_tiled(const void* C, const void* V, const void* H, v
 }
 
 // Split orthonormalisation: G -> Lw (in place), perm -> permw, V = C P R^-1 -> Vout.
+// gpart != nullptr: G halves already formed by the product kernel (rmul_planes_kernel GM >= 1), no Gram launch.
 cudaError_t fm_launch_orth_split(const void* C, void* Vout, void* Lw, int32_t* permw, int32_t* status, int frames,
-                                 int m, int p, cudaStream_t s) {
+                                 int m, int p, cudaStream_t s, const void* gpart) {
     if (p > 32 || (p & 3) || m < p || frames < 1) return cudaErrorInvalidValue;
     auto go = [&](auto gram, auto piv, auto solve, int pc, int pw, size_t pbytes) {
         const size_t gsm = sizeof(c64) * pc * pc + sizeof(c64) * 3 * 64 * (pc + 1);
-        cudaError_t e = cudaFuncSetAttribute(gram, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsm));
-        if (e != cudaSuccess) return e;
-        gram<<<frames, smb::kNT, gsm, s>>>(static_cast<const c32*>(C), static_cast<c64*>(Lw), m, p);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
+        cudaError_t e = cudaSuccess;
+        if (!gpart) {
+            e = cudaFuncSetAttribute(gram, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsm));
+            if (e != cudaSuccess) return e;
+            gram<<<frames, smb::kNT, gsm, s>>>(static_cast<const c32*>(C), static_cast<c64*>(Lw), m, p);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+        }
         e = cudaFuncSetAttribute(piv, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pw * pbytes));
         if (e != cudaSuccess) return e;
-        piv<<<(frames + pw - 1) / pw, 32 * pw, pw * pbytes, s>>>(static_cast<c64*>(Lw), permw, status, frames, m, p);
+        piv<<<(frames + pw - 1) / pw, 32 * pw, pw * pbytes, s>>>(static_cast<c64*>(Lw), permw, status, frames, m, p,
+                                                                 static_cast<const c64*>(gpart));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         solve<<<dim3((m + 127) / 128, frames), 128, 0, s>>>(static_cast<const c32*>(C), static_cast<const c64*>(Lw),
                                                             permw, static_cast<c32*>(Vout), m, p);
@@ -1646,23 +1671,29 @@ cudaError_t fm_launch_orth_split(const void* C, void* Vout, void* Lw, int32_t* p
 }
 
 // Split final stage: G -> Gw, Herm(H) -> Hw (in place for fast1), T -> Tw (p x k per frame).
+// gpart / hpart != nullptr: G and H halves already formed by the product kernel (GM = 2), no Gram launch.
 cudaError_t fm_launch_final_split(const void* C, const void* V, void* Hw, void* Gw, void* Tw, void* basis, double* eig,
                                   int32_t* status, int frames, int m, int p, int k, cudaStream_t s,
-                                  double* eig_next) {
+                                  double* eig_next, const void* gpart, const void* hpart) {
     if (p > 32 || (p & 3) || k > p || m < p || frames < 1) return cudaErrorInvalidValue;
     auto go = [&](auto gram, auto small, auto bas, int pc, int warps, size_t warp_bytes) {
         const size_t gsm = sizeof(c64) * 2 * pc * pc + sizeof(c64) * 3 * 64 * (pc + 1);
-        cudaError_t e = cudaFuncSetAttribute(gram, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsm));
-        if (e != cudaSuccess) return e;
-        gram<<<frames, smb::kNT, gsm, s>>>(static_cast<const c32*>(C), static_cast<const c32*>(V),
-                                           static_cast<c64*>(Gw), static_cast<c64*>(Hw), m, p);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        cudaError_t e = cudaSuccess;
+        if (!gpart) {
+            e = cudaFuncSetAttribute(gram, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsm));
+            if (e != cudaSuccess) return e;
+            gram<<<frames, smb::kNT, gsm, s>>>(static_cast<const c32*>(C), static_cast<const c32*>(V),
+                                               static_cast<c64*>(Gw), static_cast<c64*>(Hw), m, p);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
         const size_t wsm = warp_bytes * warps;
         e = cudaFuncSetAttribute(small, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm));
         if (e != cudaSuccess) return e;
         small<<<(frames + warps - 1) / warps, 32 * warps, wsm, s>>>(static_cast<const c64*>(Gw),
                                                                     static_cast<const c64*>(Hw), static_cast<c64*>(Tw),
-                                                                    eig, status, frames, p, k, g_sweep_dbg, eig_next);
+                                                                    eig, status, frames, p, k, g_sweep_dbg, eig_next,
+                                                                    static_cast<const c64*>(gpart),
+                                                                    static_cast<const c64*>(hpart));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         bas<<<dim3((m + 127) / 128, frames), 128, 0, s>>>(static_cast<const c32*>(C), static_cast<const c64*>(Tw),
                                                           static_cast<c64*>(basis), m, p, k);
