@@ -907,6 +907,243 @@ __global__ void __launch_bounds__(kNT) k_peaks_cta(const double* __restrict__ va
     }
 }
 
+// Peaks, one 128-thread CTA per frame (R/src/spectrum.cpp:97-188):
+//  1. values -> shared memory (coalesced, 8 loads in flight per thread);
+//  2. strict interior maxima (leftmost-plateau rule, as block_peaks), 32 consecutive cells per warp step, compacted
+//     in cell order (ballots -> per-warp counts -> prefix); the exact capacity floor((L-1)/2) holds them all
+//     (strict maxima are never adjacent);
+//  3. warp 0 runs the greedy as K argmax rounds over the list: the best (height desc, cell asc) candidate not
+//     yet excluded is the reference walk's next acceptance (a candidate that clashes with an accepted pick stays
+//     rejected), then candidates with |c - s| < min_sep (and c == s) are excluded; no sort;
+//  4. baseline = max over cells with |l - s| > min_sep for every pick (bitmask), init 0; picks ascending.
+constexpr int kPRT = 128;
+constexpr int kPCL = 8;  // register-held candidates per lane (256 per frame)
+__global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict__ values, int L, int K, int min_sep,
+                                                      PeakOut out) {
+    extern __shared__ uint8_t prs[];
+    const int cap = max(1, (L - 1) / 2);
+    const int nmask = (L + 31) / 32;
+    double* sv = reinterpret_cast<double*>(prs);              // L
+    int* cl = reinterpret_cast<int*>(sv + L);                  // cap candidate cells (ascending)
+    uint8_t* ex = reinterpret_cast<uint8_t*>(cl + cap);        // cap exclusion flags
+    uint32_t* near = reinterpret_cast<uint32_t*>(ex + ((cap + 15) & ~15));  // nmask
+    uint32_t* bal_s = near + nmask;                                          // (L - 2 + 31) / 32 ballots
+    __shared__ int s_cnt[kPRT / 32];
+    __shared__ int s_sel[64];
+    __shared__ double s_selh[64];
+    __shared__ int s_nsel;
+    __shared__ double s_wmax[kPRT / 32];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int f = blockIdx.x;
+    const double* v = values + static_cast<size_t>(f) * L;
+    const long long T0 = clock64();
+    for (int l0 = tid; l0 < L; l0 += 8 * kPRT) {
+        double tmp[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int l = l0 + u * kPRT;
+            tmp[u] = l < L ? __ldcs(v + l) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int l = l0 + u * kPRT;
+            if (l < L) sv[l] = tmp[u];
+        }
+    }
+    for (int w = tid; w < nmask; w += kPRT) near[w] = 0u;
+    __syncthreads();
+    const long long T1 = clock64();
+    // candidates: 32 consecutive cells per warp step (lane = cell, conflict-free shared reads), warp w owning the
+    // contiguous groups [w gpw, (w + 1) gpw); ballots -> per-warp counts -> block prefix -> cell-ordered list
+    auto is_max = [&](int l) -> bool {
+        if (l < 1 || l >= L - 1) return false;
+        const double x = sv[l], xm = sv[l - 1], xp = sv[l + 1];
+        if (!(x > xm)) return false;
+        if (xp < x) return true;
+        if (!(xp == x)) return false;
+        int r = l + 1;  // plateau: leftmost cell is the maximum if the run then falls
+        while (r + 1 < L && sv[r + 1] == x) ++r;
+        return (r + 1 < L) && sv[r + 1] < x;
+    };
+    const int ngroups = (L - 2 + 31) / 32;
+    const int gpw = (ngroups + kPRT / 32 - 1) / (kPRT / 32);
+    const int g0 = warp * gpw, g1 = min(ngroups, g0 + gpw);
+    int cnt = 0;
+    for (int gb = g0; gb < g1; gb += 4) {  // four groups' loads in flight
+        double xv[4], xm[4], xp[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int l = 1 + 32 * (gb + u) + lane;
+            const bool in = gb + u < g1 && l < L - 1;
+            xv[u] = in ? sv[l] : 0.0;
+            xm[u] = in ? sv[l - 1] : 0.0;
+            xp[u] = in ? sv[l + 1] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (gb + u >= g1) break;  // warp-uniform
+            const int l = 1 + 32 * (gb + u) + lane;
+            bool mx = l < L - 1 && xv[u] > xm[u] && xp[u] <= xv[u];
+            if (mx && xp[u] == xv[u]) mx = is_max(l);  // plateau
+            const uint32_t bal = __ballot_sync(0xffffffffu, mx);
+            if (lane == 0) bal_s[gb + u] = bal;
+            cnt += __popc(bal);
+        }
+    }
+    if (lane == 0) s_cnt[warp] = cnt;
+    __syncthreads();
+    int off = 0, base = 0;
+#pragma unroll
+    for (int w = 0; w < kPRT / 32; ++w) {
+        off += w < warp ? s_cnt[w] : 0;
+        base += s_cnt[w];
+    }
+    for (int g = g0; g < g1; ++g) {
+        const uint32_t bal = bal_s[g];
+        if ((bal >> lane) & 1u) {
+            const int pos = off + __popc(bal & ((1u << lane) - 1u));
+            cl[pos] = 1 + 32 * g + lane;
+            ex[pos] = 0;
+        }
+        off += __popc(bal);
+    }
+    __syncthreads();
+    const int nc = base;
+    const long long T2 = clock64();
+    if (warp == 0 && nc <= 32 * kPCL) {  // greedy rounds, candidates in registers (any MUSIC
+        // spectrum: < M maxima); lane holds list entries lane + 32 u (ascending cells within the lane)
+        double hv[kPCL];
+        int cv[kPCL];
+        uint32_t live = 0u;
+#pragma unroll
+        for (int u = 0; u < kPCL; ++u) {
+            const int j = lane + 32 * u;
+            cv[u] = j < nc ? cl[j] : 0x7fffffff;
+            hv[u] = j < nc ? sv[cv[u]] : -1.0;
+            if (j < nc) live |= 1u << u;
+        }
+        int nsel = 0;
+        for (; nsel < K; ++nsel) {
+            double h = -1.0;
+            int c = 0x7fffffff;
+#pragma unroll
+            for (int u = 0; u < kPCL; ++u)
+                if (((live >> u) & 1u) && better_w(hv[u], cv[u], h, c)) {
+                    h = hv[u];
+                    c = cv[u];
+                }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double oh = __shfl_xor_sync(0xffffffffu, h, o);
+                const int oc = __shfl_xor_sync(0xffffffffu, c, o);
+                if (better_w(oh, oc, h, c)) {
+                    h = oh;
+                    c = oc;
+                }
+            }
+            if (c == 0x7fffffff) break;
+            if (lane == 0) {
+                s_sel[nsel] = c;
+                s_selh[nsel] = h;
+            }
+#pragma unroll
+            for (int u = 0; u < kPCL; ++u)  // clash: |c_u - s| < min_sep, and c_u == s
+                if (abs(cv[u] - c) < min_sep || cv[u] == c) live &= ~(1u << u);
+            for (int d = lane - min_sep; d <= min_sep; d += 32) {
+                const int l = c + d;
+                if (l >= 0 && l < L) atomicOr(&near[l >> 5], 1u << (l & 31));
+            }
+        }
+        if (lane == 0) s_nsel = nsel;
+    } else if (warp == 0) {  // greedy rounds over the compacted list in shared memory
+        int nsel = 0;
+        for (; nsel < K; ++nsel) {
+            double h = -1.0;
+            int c = 0x7fffffff, jb = -1;
+            for (int j = lane; j < nc; j += 32)
+                if (!ex[j]) {
+                    const int cj = cl[j];
+                    const double hj = sv[cj];
+                    if (better_w(hj, cj, h, c)) {
+                        h = hj;
+                        c = cj;
+                        jb = j;
+                    }
+                }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double oh = __shfl_xor_sync(0xffffffffu, h, o);
+                const int oc = __shfl_xor_sync(0xffffffffu, c, o);
+                const int oj = __shfl_xor_sync(0xffffffffu, jb, o);
+                if (better_w(oh, oc, h, c)) {
+                    h = oh;
+                    c = oc;
+                    jb = oj;
+                }
+            }
+            if (c == 0x7fffffff) break;
+            if (lane == 0) {
+                s_sel[nsel] = c;
+                s_selh[nsel] = h;
+            }
+            // clash band around the pick: the list is in cell order, so walk outwards from its index
+            for (int d = lane; ; d += 32) {
+                bool any = false;
+                const int jl = jb - d, jr = jb + d;
+                if (jl >= 0 && (c - cl[jl] < min_sep || jl == jb)) {
+                    ex[jl] = 1;
+                    any = true;
+                }
+                if (jr < nc && cl[jr] - c < min_sep) {
+                    ex[jr] = 1;
+                    any = true;
+                }
+                if (!__any_sync(0xffffffffu, any)) break;
+            }
+            for (int d = lane - min_sep; d <= min_sep; d += 32) {
+                const int l = c + d;
+                if (l >= 0 && l < L) atomicOr(&near[l >> 5], 1u << (l & 31));
+            }
+            __syncwarp();
+        }
+        if (lane == 0) s_nsel = nsel;
+    }
+    __syncthreads();
+    if (tid == 0 && g_peak_dbg) {
+        const long long T3 = clock64();
+        g_peak_dbg[f * 4 + 0] = T1 - T0;
+        g_peak_dbg[f * 4 + 1] = T2 - T1;
+        g_peak_dbg[f * 4 + 2] = T3 - T2;
+        g_peak_dbg[f * 4 + 3] = nc;
+    }
+    double p0 = 0.0;
+    for (int l = tid; l < L; l += kPRT)
+        if (!((near[l >> 5] >> (l & 31)) & 1u)) p0 = fmax(p0, sv[l]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) p0 = fmax(p0, __shfl_xor_sync(0xffffffffu, p0, o));
+    if (lane == 0) s_wmax[warp] = p0;
+    __syncthreads();
+    const int nsel = s_nsel;
+    for (int xk = tid; xk < K; xk += kPRT) {
+        if (xk < nsel) {
+            const int c = s_sel[xk];
+            int rank = 0;
+            for (int y = 0; y < nsel; ++y) rank += s_sel[y] < c ? 1 : 0;
+            out.cells[static_cast<size_t>(f) * K + rank] = c;
+            out.heights[static_cast<size_t>(f) * K + rank] = s_selh[xk];
+        } else {
+            out.cells[static_cast<size_t>(f) * K + xk] = -1;
+            out.heights[static_cast<size_t>(f) * K + xk] = 0.0;
+        }
+    }
+    if (tid == 0) {
+        double b = 0.0;
+        for (int w = 0; w < kPRT / 32; ++w) b = fmax(b, s_wmax[w]);
+        out.baseline[f] = b;
+        out.count[f] = nsel;
+    }
+}
+
 // Peaks only, on caller-provided fp64 values (facade extract_peaks).
 __global__ void __launch_bounds__(kNT) k_peaks_only(const double* __restrict__ values, int L, int K, int min_sep,
                                                     PeakOut out, int32_t* __restrict__ overflow_flag,
@@ -1058,6 +1295,17 @@ cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K,
     };
     static const bool warp_env = std::getenv("FM_WARP_PEAKS") != nullptr;
     bool warp_kernel = warp_env;
+    static const bool sort_env = std::getenv("FM_SORT_PEAKS") != nullptr;  // comparison: sort-based k_peaks_cta
+    const int cap_r = std::max(1, (L - 1) / 2);
+    const size_t smem_r = sizeof(double) * L + sizeof(int) * cap_r + ((cap_r + 15) & ~15) + sizeof(uint32_t) * 2 * ((L + 31) / 32);
+    if (!block_kernel && !warp_kernel && !sort_env && !std::getenv("FM_PEAKS_CAP") && !std::getenv("FM_PEAKS_CTA_CAP") &&
+        smem_r <= 200 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(spec::k_peaks_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem_r));
+        if (e != cudaSuccess) return e;
+        spec::k_peaks_rounds<<<frames, spec::kPRT, smem_r, s>>>(values, L, K, min_sep, out);
+        return cudaGetLastError();
+    }
     if (const char* ov = std::getenv("FM_PEAKS_CAP")) {  // test hook: warp kernel + capacity fallback path
         cap_hint = std::atoi(ov);
         warp_kernel = true;

@@ -246,3 +246,16 @@ def test_peaks_candidate_overflow_falls_back(fm, oracle, monkeypatch, cap):
         ref = oracle.extract_peaks(v, k, sep)
         assert got.cells == ref.cells and got.heights == ref.heights
         assert got.baseline == ref.baseline and got.shortfall == ref.shortfall
+
+
+def test_peaks_rounds_long_grids_wide_bands(fm, oracle):
+    """K-round argmax peak kernel (the batch path's default) on long grids with many maxima, wide
+    separation bands, large K and plateau-heavy integer data: identical to the reference's sort + greedy walk."""
+    rng = np.random.default_rng(21)
+    for n, k, sep in ((3601, 8, 3), (18001, 16, 3), (3601, 64, 40), (1801, 33, 0), (5000, 20, 150), (2, 1, 1), (3, 4, 1)):
+        for ints in (False, True):
+            v = rng.integers(0, 4, size=n).astype(float) if ints else rng.random(n)
+            got = fm.extract_peaks(fm.PseudoSpectrum(fm.AngleGrid(n), v), k, sep)
+            ref = oracle.extract_peaks(v, k, sep)
+            assert got.cells == ref.cells and got.heights == ref.heights, (n, k, sep, ints)
+            assert got.baseline == ref.baseline and got.shortfall == ref.shortfall, (n, k, sep, ints)
