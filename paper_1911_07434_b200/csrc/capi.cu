@@ -69,6 +69,8 @@ cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K,
                                  double* heights, double* baseline, int32_t* count, int32_t* overflow,
                                  cudaStream_t s, int cap_hint = 0);
 cudaError_t fm_launch_orthocheck(const void* basis, int frames, int m, int k, double* dev, cudaStream_t s);
+cudaError_t fm_launch_spectrum_dmma(const void* t, const void* zpow, int frames, int m, int L, float* spec32,
+                                    double* spec64, cudaStream_t s);
 cudaError_t fm_launch_spectrum_multi(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
                                      double* spec64, cudaStream_t s, bool symmetric);
 template <typename T>
@@ -286,6 +288,26 @@ std::vector<double> zgrid_host(int64_t L, double theta0, double theta1, double d
     return z;
 }
 
+// Power tables of the mirror-symmetric spectrum GEMM (spectrum.cu k_spectrum_dmma): for the first nq = (L + 1) / 2
+// grid points, zhi[a][q] = e^{j 16 a phi_q} (a < ceil(M / 16)) then zlo[b][q] = e^{j b phi_q} (b < 16), with
+// phi_q = 2 pi d sin(theta_q) / lambda as zgrid_host; each angle formed in fp64 and passed to glibc cos / sin.
+std::vector<double> zpow_host(int64_t L, double theta0, double theta1, double d, double lambda, int64_t m) {
+    const int64_t nq = (L + 1) / 2, na = (m + 15) / 16;
+    std::vector<double> z(static_cast<size_t>(2 * (na + 16) * nq));
+    const double span = theta1 - theta0;
+    for (int64_t q = 0; q < nq; ++q) {
+        const double th = theta0 + (span * static_cast<double>(q)) / static_cast<double>(L - 1);
+        const double step = 2.0 * kPi * d * std::sin(th) / lambda;
+        for (int64_t a = 0; a < na + 16; ++a) {
+            const double mult = a < na ? 16.0 * static_cast<double>(a) : static_cast<double>(a - na);
+            const double ang = mult * step;
+            z[2 * (a * nq + q)] = std::cos(ang);
+            z[2 * (a * nq + q) + 1] = std::sin(ang);
+        }
+    }
+    return z;
+}
+
 int hw_threads(int32_t req) {
     if (req > 0) return req;
     const unsigned h = std::thread::hardware_concurrency();
@@ -491,6 +513,7 @@ struct fm_plan_s {
     double* t = nullptr;      // frames x M complex128
     double* spec64 = nullptr; // frames x L (fp64 spectrum for peak picking)
     double* zgrid = nullptr;  // L complex128
+    double* zpow = nullptr;   // mirror-symmetric grids: (ceil(M / 16) + 16) x ceil(L / 2) complex128 power tables
     int32_t* scratch_status = nullptr;  // frames
     float* x_pad = nullptr;             // odd N: frames x M x (N + 1) complex64
     float* rscale = nullptr;            // frames: s_f of the fp16 hi/lo R planes (plane mode)
@@ -670,6 +693,15 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
     if (e != cudaSuccess) {
         delete pl;
         return fm_fail_cuda(e, "fm_plan_create zgrid", __FILE__, __LINE__);
+    }
+    if (desc->theta0 == -desc->theta1) {
+        const auto zp = zpow_host(desc->grid_size, desc->theta0, desc->theta1, desc->d, desc->lambda, desc->m);
+        e = pl->get(&pl->zpow, zp.size());
+        if (e == cudaSuccess) e = cudaMemcpy(pl->zpow, zp.data(), sizeof(double) * zp.size(), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            delete pl;
+            return fm_fail_cuda(e, "fm_plan_create zpow", __FILE__, __LINE__);
+        }
     }
     *out = pl;
     return FM_OK;
@@ -989,8 +1021,14 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     // FM_NO_SYM_SPECTRUM=1 forces the per-point kernel (comparison)
     static const bool no_sym = std::getenv("FM_NO_SYM_SPECTRUM") != nullptr;
     const bool sym = !no_sym && d.theta0 == -d.theta1;
-    FM_LAUNCH(fm_launch_spectrum_multi(w.t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, w.spec64,
-                                       s, sym));
+    // mirror-symmetric grids: the spectrum as two fp64 GEMMs on the FP64 tensor cores (k_spectrum_dmma);
+    // FM_SPECTRUM_FMA=1 keeps the fp64 power-recurrence kernel (comparison)
+    static const bool fma_spec = std::getenv("FM_SPECTRUM_FMA") != nullptr;
+    if (sym && pl->zpow && !fma_spec)
+        FM_LAUNCH(fm_launch_spectrum_dmma(w.t, pl->zpow, F, M, static_cast<int>(d.grid_size), io->spectrum, w.spec64, s));
+    else
+        FM_LAUNCH(fm_launch_spectrum_multi(w.t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, w.spec64,
+                                           s, sym));
     FM_LAUNCH(fm_launch_peaks_only(w.spec64, F, static_cast<int>(d.grid_size), K, static_cast<int>(d.min_sep_cells),
                                    io->peak_cells, io->peak_heights, io->baseline, io->peak_count, w.scratch, s,
                                    2 * M + 64));

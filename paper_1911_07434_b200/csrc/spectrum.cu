@@ -577,6 +577,141 @@ __global__ void __launch_bounds__(kNT, 2) k_spectrum_sym(const c64* __restrict__
     }
 }
 
+// Mirror-symmetric grids on the FP64 tensor cores (mma.sync m8n8k4 f64): with pairs (q, L-1-q) as in
+// k_spectrum_sym, A(f, q) = sum_delta Re t_f,delta cos(delta phi_q) and B(f, q) = sum_delta Im t_f,delta
+// sin(delta phi_q) are two real GEMMs T_re x Zc and T_im x Zs over delta = 1..M-1 (K), frames (M dim) and
+// pairs (N dim); d(theta_q) = c0 - 2 (A - B), d(-theta_q) = c0 - 2 (A + B) with c0 = M - Re t_0, P = 1 /
+// max(d, 1e-12 M) (R/src/spectrum.cpp:37-46, 50-68). The powers z_q^delta = e^{j delta phi_q}, delta = 16a + b,
+// are formed per K-chunk as zhi[a][q] * zlo[b][q] from two host tables (angles 16a phi_q and b phi_q, glibc),
+// instead of the fp64 recurrence. fp64 throughout; the tensor core does 256 FMAs per warp instruction.
+constexpr int kSDF = 64;   // frames per CTA tile
+constexpr int kSDQ = 64;   // pairs per CTA tile
+constexpr int kSDK = 16;   // delta per chunk
+constexpr int kSDT = 256;  // threads (8 warps: 2 along frames x 4 along pairs; warp tile 32 x 16)
+constexpr int kTLd = kSDK + 1;  // complex128 row pitch of the T chunk
+constexpr int kZLd = kSDQ + 4;
+constexpr int kSDSmem = 2 * (kSDF * kTLd * 16 + 2 * kSDK * kZLd * 8);  // double-buffered T and Z chunks
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__global__ void __launch_bounds__(kSDT, 2) k_spectrum_dmma(const c64* __restrict__ t, const c64* __restrict__ zpow,
+                                                          int frames, int m, int L, float* __restrict__ spec32,
+                                                          double* __restrict__ spec64) {
+    extern __shared__ __align__(16) uint8_t sdm[];
+    c64* Tb = reinterpret_cast<c64*>(sdm);                          // [2][kSDF][kTLd]
+    double* Zb = reinterpret_cast<double*>(Tb + 2 * kSDF * kTLd);   // [2][2 (cos, sin)][kSDK][kZLd]
+    const int nq = (L + 1) / 2;
+    const int na = (m + kSDK - 1) / kSDK;
+    const c64* zhi = zpow;                                 // [na][nq]
+    const c64* zlo = zpow + static_cast<size_t>(na) * nq;  // [16][nq]
+    const int f0 = blockIdx.y * kSDF, q0 = blockIdx.x * kSDQ;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wm = warp & 1, wn = warp >> 1;  // warp tile: frames 32 wm .., pairs 16 wn ..
+    // Z builder: thread -> pair column zq, four delta rows zb0 .. zb0 + 3 of each chunk
+    const int zq = tid & (kSDQ - 1), zb0 = (tid >> 6) * 4;
+    const bool zin = q0 + zq < nq;
+    c64 zl[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) zl[u] = zin ? zlo[static_cast<size_t>(zb0 + u) * nq + q0 + zq] : mk(0.0, 0.0);
+    auto issue_t = [&](int a, int buf) {  // T chunk a -> buffer (cp.async; delta = 0, delta >= m, f >= frames -> 0)
+        c64* T = Tb + buf * kSDF * kTLd;
+#pragma unroll
+        for (int u = 0; u < kSDF * kSDK / kSDT; ++u) {
+            const int e = tid + u * kSDT;
+            const int fr = e / kSDK, dl = e % kSDK, de = a * kSDK + dl;
+            const bool ok = f0 + fr < frames && de >= 1 && de < m;
+            cp_async16(T + fr * kTLd + dl, ok ? t + static_cast<size_t>(f0 + fr) * m + de : t, ok ? 16 : 0);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto put_z = [&](c64 zh, int buf) {
+        double* Zc = Zb + buf * 2 * kSDK * kZLd;
+        double* Zs = Zc + kSDK * kZLd;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const c64 z = zh * zl[u];
+            Zc[(zb0 + u) * kZLd + zq] = z.re;
+            Zs[(zb0 + u) * kZLd + zq] = z.im;
+        }
+    };
+    double ac[4][2][2], as[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) ac[i][j][0] = ac[i][j][1] = as[i][j][0] = as[i][j][1] = 0.0;
+    issue_t(0, 0);
+    put_z(zin ? zhi[q0 + zq] : mk(0.0, 0.0), 0);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    for (int a = 0; a < na; ++a) {
+        const int buf = a & 1;
+        const bool more = a + 1 < na;
+        c64 zn = mk(0.0, 0.0);
+        if (more) {  // next chunk in flight while this one is consumed
+            issue_t(a + 1, buf ^ 1);
+            if (zin) zn = zhi[static_cast<size_t>(a + 1) * nq + q0 + zq];
+        }
+        const c64* T = Tb + buf * kSDF * kTLd;
+        const double* Zc = Zb + buf * 2 * kSDK * kZLd;
+        const double* Zs = Zc + kSDK * kZLd;
+#pragma unroll
+        for (int k4 = 0; k4 < kSDK / 4; ++k4) {
+            c64 av[4];
+            double bc[2], bs[2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = T[(32 * wm + 8 * i + (lane >> 2)) * kTLd + 4 * k4 + (lane & 3)];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int r = 4 * k4 + (lane & 3), c = 16 * wn + 8 * j + (lane >> 2);
+                bc[j] = Zc[r * kZLd + c];
+                bs[j] = Zs[r * kZLd + c];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    dmma(ac[i][j], av[i].re, bc[j]);
+                    dmma(as[i][j], av[i].im, bs[j]);
+                }
+        }
+        if (more) put_z(zn, buf ^ 1);  // buffer buf ^ 1 was released by the barrier that ended chunk a - 1
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+    }
+    const double floor_v = 1e-12 * static_cast<double>(m);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int f = f0 + 32 * wm + 8 * i + (lane >> 2);
+        if (f >= frames) continue;
+        const double c0 = static_cast<double>(m) - t[static_cast<size_t>(f) * m].re;
+        const size_t o = static_cast<size_t>(f) * L;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int q = q0 + 16 * wn + 8 * j + 2 * (lane & 3) + h;
+                if (q >= nq) continue;
+                const int qm = L - 1 - q;
+                const double A = ac[i][j][h], B = as[i][j][h];
+                const double Pp = 1.0 / fmax(c0 - 2.0 * (A - B), floor_v);
+                if (spec32) spec32[o + q] = static_cast<float>(Pp);
+                spec64[o + q] = Pp;
+                if (qm != q) {
+                    const double Pm = 1.0 / fmax(c0 - 2.0 * (A + B), floor_v);
+                    if (spec32) spec32[o + qm] = static_cast<float>(Pm);
+                    spec64[o + qm] = Pm;
+                }
+            }
+    }
+}
+
 // Peaks, one WARP per frame (R/src/spectrum.cpp:97-188, same rules as block_peaks):
 //  1. strict interior maxima with leftmost-plateau rule, found 32 cells at a time (coalesced
 //     loads) and compacted in cell order with ballot/popc; capacity ceil((L-2)/2) is exact
@@ -1244,6 +1379,19 @@ cudaError_t fm_launch_spectrum_peaks(const void* t, const void* zgrid, int frame
     spec::PeakOut out{cells, heights, baseline, count};
     spec::k_spectrum_peaks<<<frames, spec::kNT, smem, s>>>(static_cast<const c64*>(t), static_cast<const c64*>(zgrid),
                                                            m, L, spec32, spec64, K, min_sep, out, status);
+    return cudaGetLastError();
+}
+
+// zpow: [ceil(m / 16)][nq] e^{j 16 a phi_q} then [16][nq] e^{j b phi_q} (fm_zpow_host); mirror-symmetric grids.
+cudaError_t fm_launch_spectrum_dmma(const void* t, const void* zpow, int frames, int m, int L, float* spec32,
+                                    double* spec64, cudaStream_t s) {
+    const int nq = (L + 1) / 2;
+    dim3 grid((nq + spec::kSDQ - 1) / spec::kSDQ, (frames + spec::kSDF - 1) / spec::kSDF);
+    const cudaError_t attr = cudaFuncSetAttribute(spec::k_spectrum_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  spec::kSDSmem);
+    if (attr != cudaSuccess) return attr;
+    spec::k_spectrum_dmma<<<grid, spec::kSDT, spec::kSDSmem, s>>>(static_cast<const c64*>(t), static_cast<const c64*>(zpow),
+                                                                   frames, m, L, spec32, spec64);
     return cudaGetLastError();
 }
 
