@@ -663,7 +663,9 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
     }
-    static const int cap_pairs = std::getenv("FM_TC_PAIRS") ? std::atoi(std::getenv("FM_TC_PAIRS")) : 0;  // experiment
+    static const int cap_pairs = std::getenv("FM_COV_PAIRS")  ? std::atoi(std::getenv("FM_COV_PAIRS"))
+                                 : std::getenv("FM_TC_PAIRS") ? std::atoi(std::getenv("FM_TC_PAIRS"))
+                                                              : 0;  // experiment: covariance grid width
     const int64_t pairs = std::min<int64_t>(tiles, std::max(1, cap_pairs > 0 ? cap_pairs : sm_count / 2));
     const dim3 grid(static_cast<unsigned>(2 * pairs));
     auto go = [&](auto kern, bool conv8) {

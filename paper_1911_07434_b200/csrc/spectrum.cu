@@ -34,6 +34,9 @@ namespace fmk {
 namespace spec {
 
 constexpr int kNT = 256;
+#ifndef FM_FFT_MINB
+#define FM_FFT_MINB 4  // four CTAs per SM (64 registers): 60.7 -> 52.7 us at c2 (scripts_fft_minb.sh)
+#endif
 constexpr int kNW = kNT / 32;
 
 // t_delta, delta = 0..M-1, for frame blockIdx.x. Thread i owns lags i and M-1-i, so every
@@ -172,7 +175,7 @@ __device__ void fft_stockham(c64* a, int logn, int cnt, const c64* tw) {
     else if (rem == 1) fft_pass<2>(a, logn, cnt, p, tw + off);
 }
 
-__global__ void __launch_bounds__(kNT, 2) k_autocorr_fft(const c64* __restrict__ basis, c64* __restrict__ t, int m, int k,
+__global__ void __launch_bounds__(kNT, FM_FFT_MINB) k_autocorr_fft(const c64* __restrict__ basis, c64* __restrict__ t, int m, int k,
                                                    int logn, int grp) {
     extern __shared__ c64 fsm[];
     const int nfft = 1 << logn;
