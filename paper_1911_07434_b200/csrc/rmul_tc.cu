@@ -361,7 +361,8 @@ __host__ __device__ constexpr int plane_smem() {
     return 1024 + plane_gram_off<PH, GM>() + (GM == 0 ? 0 : (GM == 2 ? 2 : 1) * kRows * (PH + 1) * 16);
 }
 
-constexpr int kThreadsG = kThreads + 128;  // Gram epilogue: w10..w13 form the Gram halves
+constexpr int kThreadsG = kThreads + 128;
+__device__ long long* g_gram_dbg = nullptr;  // debug: per-frame (wait at tile-full, Gram compute) cycles, CTA 0  // Gram epilogue: w10..w13 form the Gram halves
 
 template <int PH, bool REAL, bool LO, int GM = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM ? kThreadsG : kThreads, 1)
@@ -550,7 +551,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM ? kThreadsG : kTh
                 for (int a = 0; a < 4; ++a)
 #pragma unroll
                     for (int b = 0; b < 4; ++b) acc[a][b] = fmk::mk(0.0, 0.0);
+                const long long Tw0 = clock64();
                 named_bar_sync(4, 256);  // tile full
+                const long long Tw1 = clock64();
                 if (active && !(gdbg & 1)) {
 #pragma unroll 4
                     for (int r = rg; r < kRows; r += RG) {
@@ -565,6 +568,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM ? kThreadsG : kTh
 #pragma unroll
                             for (int b = 0; b < 4; ++b) fmk::cmac_conj(acc[a][b], x[a], y[b]);
                     }
+                }
+                if (g_gram_dbg && blockIdx.x == 0 && threadIdx.x == kThreads) {
+                    const int it = (tile - pair) / npairs;
+                    g_gram_dbg[2 * it] = Tw1 - Tw0;
+                    g_gram_dbg[2 * it + 1] = clock64() - Tw1;
                 }
                 if (tile + npairs < total_tiles) named_bar_arrive(5, 256);  // tile free for the next frame
 #pragma unroll
@@ -727,6 +735,10 @@ cudaError_t fm_launch_rmul_tc(const float* d_r, const float* d_omega, const floa
     if (p <= 16)
         return d_omega ? go(rmul_tc_kernel<16, true>, Cfg<16>::kSmem) : go(rmul_tc_kernel<16, false>, Cfg<16>::kSmem);
     return d_omega ? go(rmul_tc_kernel<32, true>, Cfg<32>::kSmem) : go(rmul_tc_kernel<32, false>, Cfg<32>::kSmem);
+}
+
+extern "C" int32_t fm_debug_set_gram_buffer(long long* d) {
+    return cudaMemcpyToSymbol(fmk::rmtc::g_gram_dbg, &d, sizeof(d)) == cudaSuccess ? 0 : 1;
 }
 
 // Debug entry (not part of the public header): run the tensor-core product synchronously.

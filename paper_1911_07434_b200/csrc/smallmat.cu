@@ -26,6 +26,19 @@ namespace fmk {
 namespace smb {
 
 constexpr int kNT = 256;
+// latency-bound small-matrix kernels: frames (warps) per CTA and register caps (tuning switches)
+#ifndef FM_SMALL_WARPS
+#define FM_SMALL_WARPS 4  // 93.4 -> 91.9 us at c2 (scripts_small_tune.sh)
+#endif
+#ifndef FM_PIV_WARPS
+#define FM_PIV_WARPS 4  // 22.4 -> 21.2 us
+#endif
+#ifndef FM_SOLVE_MINB
+#define FM_SOLVE_MINB 1
+#endif
+#ifndef FM_BASIS_MINB
+#define FM_BASIS_MINB 1
+#endif
 constexpr int kNW = kNT / 32;
 constexpr int kRC = 64;   // rows per staged Gram chunk
 constexpr int kRCP = 65;  // padded column stride (conflict-free 16-B column reads)
@@ -966,7 +979,7 @@ static __device__ __forceinline__ bool mixed_jacobi() { return g_mixed_jacobi !=
 
 template <int PC> struct WarpCfg {
     static constexpr int kLPC = 32 / PC;                   // lanes per column in the Jacobi
-    static constexpr int kWarps = PC <= 16 ? 8 : 4;        // frames per CTA
+    static constexpr int kWarps = PC <= 16 ? FM_SMALL_WARPS : 4;  // frames per CTA
     static constexpr int kLd = PC + ((kLPC - PC) % 8 + 8) % 8;  // ld = LPC (mod 8): conflict-free 16-B rows
     // L, L_H (reused for T once Y is formed), Y (in-place pair-lane Jacobi)
     static constexpr size_t kBytes = sizeof(c64) * (2 * PC * PC + PC * kLd) + sizeof(double) * PC + sizeof(int) * PC;
@@ -1370,7 +1383,7 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
 }
 
 template <int PC>
-__global__ void __launch_bounds__(128) k_basis_ct(const c32* __restrict__ Cin, const c64* __restrict__ Tin,
+__global__ void __launch_bounds__(128, FM_BASIS_MINB) k_basis_ct(const c32* __restrict__ Cin, const c64* __restrict__ Tin,
                                                   c64* __restrict__ basis, int m, int p, int k) {
     __shared__ c64 Ts[PC * PC];
     const int f = blockIdx.y;
@@ -1416,7 +1429,7 @@ __global__ void __launch_bounds__(kNT, 2) k_gram_only(const c32* __restrict__ Ci
 }
 
 template <int PC> struct PivCfg {
-    static constexpr int kWarps = PC <= 16 ? 8 : 4;
+    static constexpr int kWarps = PC <= 16 ? FM_PIV_WARPS : 4;
     static constexpr size_t kWarpBytes = sizeof(c64) * 2 * PC * PC + sizeof(double) * PC;
 };
 
@@ -1525,7 +1538,7 @@ __global__ void __launch_bounds__(32 * PivCfg<PC>::kWarps)
 }
 
 template <int PC>
-__global__ void __launch_bounds__(128) k_rows_solve(const c32* __restrict__ Cin, const c64* __restrict__ Lin,
+__global__ void __launch_bounds__(128, FM_SOLVE_MINB) k_rows_solve(const c32* __restrict__ Cin, const c64* __restrict__ Lin,
                                                     const int32_t* __restrict__ perm_in, c32* __restrict__ Vout, int m,
                                                     int p) {
     __shared__ c64 Lp[PC * PC];  // Lp[a * PC + j] = conj-free L_p(j, a) = L[a * p + perm[j]], a < j
