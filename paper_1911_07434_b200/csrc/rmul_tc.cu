@@ -361,11 +361,18 @@ __host__ __device__ constexpr int plane_smem() {
     return 1024 + plane_gram_off<PH, GM>() + (GM == 0 ? 0 : (GM == 2 ? 2 : 1) * kRows * (PH + 1) * 16);
 }
 
-constexpr int kThreadsG = kThreads + 128;
+constexpr int kThreadsG = kThreads + 128;  // GM = 1: four Gram warps (10 G tiles x 8 row groups)
+#ifndef FM_GRAM_RG2
+#define FM_GRAM_RG2 4  // 4 (four Gram warps, 80 active): 123 us; 8 (five warps): 128 us (scripts_ab_build.sh)
+#endif
+// GM = 2: 10 G + 10 H tiles x FM_GRAM_RG2 row groups (8: five Gram warps; 4: four)
+constexpr int kThreadsG2 = kThreads + (FM_GRAM_RG2 == 8 ? 160 : 128);
+template <int GM> __host__ __device__ constexpr int gram_threads() { return GM == 2 ? kThreadsG2 : kThreadsG; }
+template <int GM> __host__ __device__ constexpr int handoff_count() { return gram_threads<GM>() - kThreads + 128; }
 __device__ long long* g_gram_dbg = nullptr;  // debug: per-frame (wait at tile-full, Gram compute) cycles, CTA 0  // Gram epilogue: w10..w13 form the Gram halves
 
 template <int PH, bool REAL, bool LO, int GM = 0>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM ? kThreadsG : kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM ? gram_threads<GM>() : kThreads, 1)
     rmul_planes_kernel(const __grid_constant__ CUtensorMap hmap, const __grid_constant__ CUtensorMap lmap,
                        const __grid_constant__ CUtensorMap vmap, const float* __restrict__ rscale,
                        float* __restrict__ c_out, int m, int p, int tiles_per_frame, int total_tiles,
@@ -531,7 +538,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM ? kThreadsG : kTh
             constexpr int ld = PH + 1;
             const fmk::c64* sC = reinterpret_cast<const fmk::c64*>(smem + plane_gram_off<PH, GM>());
             const fmk::c64* sV = sC + kRows * ld;
-            constexpr int RG = GM == 2 ? 4 : 8;  // row groups (consecutive lanes) per 4 x 4 tile
+            constexpr int RG = GM == 2 ? FM_GRAM_RG2 : 8;  // row groups (consecutive lanes) per 4 x 4 tile
             const int et = threadIdx.x - kThreads;
             const int nb = p >> 2, t1 = nb * (nb + 1) / 2;
             const int gt = et / RG, rg = et % RG;
@@ -552,7 +559,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM ? kThreadsG : kTh
 #pragma unroll
                     for (int b = 0; b < 4; ++b) acc[a][b] = fmk::mk(0.0, 0.0);
                 const long long Tw0 = clock64();
-                named_bar_sync(4, 256);  // tile full
+                named_bar_sync(4, handoff_count<GM>());  // tile full
                 const long long Tw1 = clock64();
                 if (active && !(gdbg & 1)) {
 #pragma unroll 4
@@ -574,7 +581,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM ? kThreadsG : kTh
                     g_gram_dbg[2 * it] = Tw1 - Tw0;
                     g_gram_dbg[2 * it + 1] = clock64() - Tw1;
                 }
-                if (tile + npairs < total_tiles) named_bar_arrive(5, 256);  // tile free for the next frame
+                if (tile + npairs < total_tiles) named_bar_arrive(5, handoff_count<GM>());  // tile free for the next frame
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -646,7 +653,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM ? kThreadsG : kTh
 #pragma unroll
                     for (int c = 0; c < PH; ++c) vv[c] = (ok && c < p) ? vf[static_cast<size_t>(c) * m + row] : make_float2(0.f, 0.f);
                 }
-                if (t > 0) named_bar_sync(5, 256);
+                if (t > 0) named_bar_sync(5, handoff_count<GM>());
 #pragma unroll
                 for (int c = 0; c < PH; ++c) {  // the complex64 values written to C, widened once
                     const float re = sf * (__uint_as_float(v[c]) + __uint_as_float(v[2 * PH + c]));
@@ -659,7 +666,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM ? kThreadsG : kTh
                     for (int c = 0; c < PH; ++c)
                         sV[lr * ld + c] = fmk::mk(static_cast<double>(vv[c].x), static_cast<double>(vv[c].y));
                 }
-                named_bar_arrive(4, 256);
+                named_bar_arrive(4, handoff_count<GM>());
             }
         }
     }
@@ -808,7 +815,7 @@ cudaError_t fm_launch_rmul_planes(const void* planes_hi, const void* planes_lo, 
     auto go = [&](auto kern, int smem) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        kern<<<grid, gram > 0 ? kThreadsG : kThreads, smem, stream>>>(hmap, lmap, vmap, d_scale, d_c, static_cast<int>(m),
+        kern<<<grid, gram == 2 ? kThreadsG2 : gram == 1 ? kThreadsG : kThreads, smem, stream>>>(hmap, lmap, vmap, d_scale, d_c, static_cast<int>(m),
                                                                        static_cast<int>(p), tiles_per_frame,
                                                                        static_cast<int>(tiles), d_v, gpart, hpart, gdbg);
         return cudaGetLastError();
