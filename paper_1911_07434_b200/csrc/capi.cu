@@ -71,6 +71,8 @@ cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K,
 cudaError_t fm_launch_orthocheck(const void* basis, int frames, int m, int k, double* dev, cudaStream_t s);
 cudaError_t fm_launch_spectrum_dmma(const void* t, const void* zpow, int frames, int m, int L, float* spec32,
                                     double* spec64, cudaStream_t s);
+cudaError_t fm_launch_spectrum_i8(const void* t, const int8_t* zd, int8_t* td, double* tscale, int frames, int m, int L,
+                                  float* spec32, double* spec64, cudaStream_t s);
 cudaError_t fm_launch_spectrum_multi(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
                                      double* spec64, cudaStream_t s, bool symmetric);
 template <typename T>
@@ -308,6 +310,37 @@ std::vector<double> zpow_host(int64_t L, double theta0, double theta1, double d,
     return z;
 }
 
+// Digits of the spectrum's cos / sin table for the int8 Ozaki kernel (spectrum.cu k_spectrum_i8): for pair
+// column q < nq and delta < m, z = (cos, sin)(delta phi_q) (angle formed in fp64, glibc), written as 5 signed
+// base-128 digits of z / 2, in mma B-fragment order [s][cs][q / 8][delta / 32][lane][2 x u32] (column q % 8 = lane / 4,
+// k = 4 (lane % 4) + 16 word + byte); zero padding to nqp = nq up to 32 and mk = m up to 32.
+std::vector<int8_t> zdig_host(int64_t L, double theta0, double theta1, double d, double lambda, int64_t m) {
+    constexpr int kS = 5;
+    const int64_t nq = (L + 1) / 2, nqp = (nq + 31) / 32 * 32, nkb = (m + 31) / 32, npb = nqp / 8;
+    std::vector<int8_t> z(static_cast<size_t>(kS * 2 * nqp * nkb * 32), 0);
+    const double span = theta1 - theta0;
+    for (int64_t q = 0; q < nq; ++q) {
+        const double th = theta0 + (span * static_cast<double>(q)) / static_cast<double>(L - 1);
+        const double step = 2.0 * kPi * d * std::sin(th) / lambda;
+        const int64_t pb = q / 8, col = q % 8;
+        for (int64_t dl = 0; dl < m; ++dl) {
+            const double ang = static_cast<double>(dl) * step;
+            double r[2] = {0.5 * std::cos(ang), 0.5 * std::sin(ang)};
+            const int64_t kb = dl / 32, k = dl % 32;
+            const int64_t lane = col * 4 + (k & 15) / 4, word = k / 16;
+            for (int sl = 0; sl < kS; ++sl)
+                for (int cs = 0; cs < 2; ++cs) {
+                    const double x = 128.0 * r[cs];
+                    const double dg = std::nearbyint(x);
+                    r[cs] = x - dg;
+                    z[static_cast<size_t>(((((sl * 2 + cs) * npb + pb) * nkb + kb) * 32 + lane) * 2 + word) * 4 + (k & 3)] =
+                        static_cast<int8_t>(dg);
+                }
+        }
+    }
+    return z;
+}
+
 int hw_threads(int32_t req) {
     if (req > 0) return req;
     const unsigned h = std::thread::hardware_concurrency();
@@ -514,6 +547,10 @@ struct fm_plan_s {
     double* spec64 = nullptr; // frames x L (fp64 spectrum for peak picking)
     double* zgrid = nullptr;  // L complex128
     double* zpow = nullptr;   // mirror-symmetric grids: (ceil(M / 16) + 16) x ceil(L / 2) complex128 power tables
+    int8_t* zdig = nullptr;   // mirror-symmetric grids: int8 digits of the cos / sin table (Ozaki spectrum)
+    int8_t* tdig = nullptr;   // per batch: int8 digits of t (frames padded per sub-batch)
+    double* tscale = nullptr; // per batch: power-of-two scale of each frame's t
+    size_t tdig_rows = 0;     // frame rows of tdig / tscale (sub-batch i uses rows f0 + 64 i ..)
     int32_t* scratch_status = nullptr;  // frames
     float* x_pad = nullptr;             // odd N: frames x M x (N + 1) complex64
     float* rscale = nullptr;            // frames: s_f of the fp16 hi/lo R planes (plane mode)
@@ -695,6 +732,17 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
         return fm_fail_cuda(e, "fm_plan_create zgrid", __FILE__, __LINE__);
     }
     if (desc->theta0 == -desc->theta1) {
+        const auto zdg = zdig_host(desc->grid_size, desc->theta0, desc->theta1, desc->d, desc->lambda, desc->m);
+        const size_t mk = (static_cast<size_t>(desc->m) + 31) / 32 * 32;
+        e = pl->get(&pl->zdig, zdg.size());
+        if (e == cudaSuccess) e = cudaMemcpy(pl->zdig, zdg.data(), zdg.size(), cudaMemcpyHostToDevice);
+        pl->tdig_rows = B + 64 * 16;
+        if (e == cudaSuccess) e = pl->get(&pl->tdig, pl->tdig_rows * 5 * 2 * mk);
+        if (e == cudaSuccess) e = pl->get(&pl->tscale, pl->tdig_rows);
+        if (e != cudaSuccess) {
+            delete pl;
+            return fm_fail_cuda(e, "fm_plan_create zdig", __FILE__, __LINE__);
+        }
         const auto zp = zpow_host(desc->grid_size, desc->theta0, desc->theta1, desc->d, desc->lambda, desc->m);
         e = pl->get(&pl->zpow, zp.size());
         if (e == cudaSuccess) e = cudaMemcpy(pl->zpow, zp.data(), sizeof(double) * zp.size(), cudaMemcpyHostToDevice);
@@ -842,9 +890,10 @@ struct WorkView {
     double* eig_next;
     double* gpart;
     double* hpart;
+    size_t dslot;  // first frame row of this sub-batch's region in tdig / tscale
 };
 
-static WorkView work_view(fm_plan pl, int64_t f0) {
+static WorkView work_view(fm_plan pl, int64_t f0, int sub = 0) {
     const auto& d = pl->d;
     const size_t M = d.m, P = d.method == FM_METHOD_EXACT ? pl->pe : d.p, K = d.k;
     const size_t MP = (M + 15) / 16 * 16;
@@ -854,6 +903,7 @@ static WorkView work_view(fm_plan pl, int64_t f0) {
     w.u32 = pl->u32 ? pl->u32 + f0 * K * M * 2 : nullptr;
     w.ru = pl->ru ? pl->ru + f0 * K * M * 2 : nullptr;
     w.eig_next = pl->eig_next ? pl->eig_next + f0 : nullptr;
+    w.dslot = static_cast<size_t>(f0) + 64 * static_cast<size_t>(sub);
     w.gpart = pl->gpart ? pl->gpart + f0 * 2 * P * P * 2 : nullptr;
     w.hpart = pl->hpart ? pl->hpart + f0 * 2 * P * P * 2 : nullptr;
     w.C = pl->C + f0 * P * M * 2;
@@ -1024,7 +1074,15 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     // mirror-symmetric grids: the spectrum as two fp64 GEMMs on the FP64 tensor cores (k_spectrum_dmma);
     // FM_SPECTRUM_FMA=1 keeps the fp64 power-recurrence kernel (comparison)
     static const bool fma_spec = std::getenv("FM_SPECTRUM_FMA") != nullptr;
-    if (sym && pl->zpow && !fma_spec)
+    static const bool dmma_spec = std::getenv("FM_SPECTRUM_DMMA") != nullptr;
+    const bool dig_fits = w.dslot + (static_cast<size_t>(F) + 63) / 64 * 64 <= pl->tdig_rows;
+    if (sym && pl->zdig && dig_fits && !fma_spec && !dmma_spec) {
+        // int8 tensor cores, fp64-exact digit splitting (k_spectrum_i8); sub-batch regions of the digit buffer
+        // start at f0 + 64 * (f0 / 64 ...) -- frames are offset by w.t, so place the region by the t offset
+        const size_t mk = (static_cast<size_t>(M) + 31) / 32 * 32;
+        FM_LAUNCH(fm_launch_spectrum_i8(w.t, pl->zdig, pl->tdig + w.dslot * 5 * 2 * mk, pl->tscale + w.dslot, F, M,
+                                        static_cast<int>(d.grid_size), io->spectrum, w.spec64, s));
+    } else if (sym && pl->zpow && !fma_spec)
         FM_LAUNCH(fm_launch_spectrum_dmma(w.t, pl->zpow, F, M, static_cast<int>(d.grid_size), io->spectrum, w.spec64, s));
     else
         FM_LAUNCH(fm_launch_spectrum_multi(w.t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, w.spec64,
@@ -1110,7 +1168,7 @@ extern "C" fm_status fm_run_batch(fm_plan pl, int64_t frames, const fm_batch_io*
                                        pl->d.n));
         }
         if (i == 0) mark(pl, 1, q);
-        st = run_post_cov(pl, nf, &o, R, q, work_view(pl, f0), i == 0, pv);
+        st = run_post_cov(pl, nf, &o, R, q, work_view(pl, f0, i), i == 0, pv);
         if (st != FM_OK) return st;
         FM_CUDA_OK(cudaEventRecord(pl->sub_ev[1 + i], q));
         FM_CUDA_OK(cudaStreamWaitEvent(s, pl->sub_ev[1 + i], 0));
