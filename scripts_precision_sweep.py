@@ -3,6 +3,9 @@ of an experiment switch (env var toggled between runs in one process; "-" = one 
 Prints per setting: worst spectrum
 dB error (within 40 dB of max), 99th percentile, frames whose peak cells differ."""
 import json
+import os as _os
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    _os.environ.setdefault(_v, "1")  # one BLAS thread per oracle worker (the pool uses every core)
 import os
 import sys
 from concurrent.futures import ProcessPoolExecutor
