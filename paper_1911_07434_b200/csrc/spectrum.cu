@@ -728,6 +728,11 @@ __global__ void __launch_bounds__(kSDT, 2) k_spectrum_dmma(const c64* __restrict
 #ifndef FM_I8_STAGES
 #define FM_I8_STAGES 4
 #endif
+#ifdef FM_I8_VOLATILE
+#define FM_I8_ASM asm volatile
+#else
+#define FM_I8_ASM asm  // pure int8 MMAs (no volatile): the shared loads can be scheduled around them
+#endif
 #ifndef FM_I8_NB
 #define FM_I8_NB 1
 #endif
@@ -850,7 +855,7 @@ __global__ void __launch_bounds__(kOT, 3 - kONB) k_spectrum_i8(const int8_t* __r
                         int(&c)[4] = acc[a + b][x][n];
                         const uint4 A = av[a][x];
                         const uint2 B = bv[x][n];
-                        asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                        FM_I8_ASM("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
                                      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
                                      : "r"(A.x), "r"(A.y), "r"(A.z), "r"(A.w), "r"(B.x), "r"(B.y));
                     }
