@@ -27,6 +27,9 @@ namespace smb {
 
 constexpr int kNT = 256;
 // latency-bound small-matrix kernels: frames (warps) per CTA and register caps (tuning switches)
+#ifndef FM_JACOBI_TOL32
+#define FM_JACOBI_TOL32 1e-6f  // fp32 Jacobi phase: sweep until every rotation is below this (then fp64 sweeps)
+#endif
 #ifndef FM_SMALL_WARPS
 #define FM_SMALL_WARPS 4  // 93.4 -> 91.9 us at c2 (scripts_small_tune.sh)
 #endif
@@ -1189,7 +1192,7 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
         c32* y32 = reinterpret_cast<c32*>(LH);
         for (int e = lane; e < PC * ld; e += 32) y32[e] = mk(static_cast<float>(Ya[e].re), static_cast<float>(Ya[e].im));
         __syncwarp();
-        const float tol32 = 1e-6f;
+        const float tol32 = FM_JACOBI_TOL32;
         for (int sweep = 0; sweep < 12; ++sweep) {
             bool rot_any = false;
             for (int rnd = 0; rnd < n1; ++rnd) {
