@@ -253,7 +253,9 @@ def run_ours(args):
         omega = torch.from_numpy(fm.draw_uniforms_batch(dseeds, M)).to(dev)
     xd = xh.to(dev)
     plan = fm.BatchPlan(M, N, K, cfgd["method"], p=P, t=cfgd["t"], grid_size=L, max_frames=B, device=local)
-    nsub = args.subbatches if args.subbatches > 0 else (2 if B >= 512 else 1)
+    # same rule as the library's automatic choice (capi.cu auto_subbatches): one sub-batch on the p <= 16 plane path
+    plane_gram = cfgd["method"] in ("fast2", "fast1_norm2") and M <= 256 and P <= 16
+    nsub = args.subbatches if args.subbatches > 0 else (1 if plane_gram or B < 512 else 2)
     plan.set_concurrency(nsub)
     fsub = (B + nsub - 1) // nsub  # frames in sub-batch 0 (the one the stage events time)
     out = plan.outputs(B, spectrum=True)

@@ -830,6 +830,9 @@ extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
     if (!plan) return 0;
     const int t = plan->d.t;
     int n = 1 /*cov*/ + 1 /*clear*/ + 3 /*autocorr, spectrum, peaks*/ + (plan->x_pad ? 1 : 0) /*odd-N pad*/;
+    // int8 spectrum: + the digit split of t (k_slice_t), see run_post_cov
+    if (plan->zdig && plan->d.theta0 == -plan->d.theta1 && !std::getenv("FM_SPECTRUM_FMA") && !std::getenv("FM_SPECTRUM_DMMA"))
+        n += 1;
     const bool tiled = plan->d.p <= 32 && (plan->d.p % 4) == 0;
     // Gram epilogue (plane path, p <= 16): the Gram kernels are folded into the products
     const int gepi = tiled && split_final() && plane_mode(plan) && plan->d.p <= 16 && !std::getenv("FM_NO_GRAM_EPI") ? 1 : 0;
@@ -1109,7 +1112,11 @@ static fm_status check_io(fm_plan pl, int64_t frames, const fm_batch_io* io) {
 static int auto_subbatches(fm_plan pl, int64_t frames) {
     if (pl->nsub > 0) return static_cast<int>(std::min<int64_t>(pl->nsub, frames));
     if (const char* e = std::getenv("FM_SUBBATCHES")) return std::max(1, std::atoi(e));
-    return frames >= 512 ? 2 : 1;  // measured on c2 (scripts_sweep_nsub.sh): 1.29 / 1.22 / 1.24 ms for 1 / 2 / 4
+    // Two concurrent sub-batches for large batches, except on the p <= 16 plane path (Gram halves in the products),
+    // whose kernels no longer gain from the overlap: c2 1.036 / 1.043 ms for 1 / 2; c3 1.408 / 1.286, c5 0.964 /
+    // 0.952, c3n 2.181 / 2.069 (scripts_nsub_cfg.sh).
+    if (pl->gpart) return 1;
+    return frames >= 512 ? 2 : 1;
 }
 
 extern "C" fm_status fm_run_batch(fm_plan pl, int64_t frames, const fm_batch_io* io, void* stream) {
