@@ -27,6 +27,9 @@ namespace smb {
 
 constexpr int kNT = 256;
 // latency-bound small-matrix kernels: frames (warps) per CTA and register caps (tuning switches)
+#ifndef FM_GRAM_RG32
+#define FM_GRAM_RG32 4
+#endif
 #ifndef FM_JACOBI_TOL32
 #define FM_JACOBI_TOL32 1e-6f  // fp32 Jacobi phase: sweep until every rotation is below this (then fp64 sweeps)
 #endif
@@ -461,6 +464,10 @@ __device__ int warp_jacobi_herm(c64* A, c64* Z, int n, double* prm) {
 constexpr int kRG = 8;      // row groups (consecutive lanes)
 constexpr int kRCH = 64;    // rows per staged chunk
 
+// Row groups per tile: 8 for p <= 16; 4 for p = 32 (the 36 upper tiles of G then fit one pass of 256 threads,
+// and G + H two passes instead of three).
+template <int PC> struct GramRG { static constexpr int value = PC > 16 ? FM_GRAM_RG32 : 8; };
+
 template <int PC, typename T1, typename T2>
 __device__ void tiled_gram2(const T1* __restrict__ X1, bool herm1, const T1* __restrict__ Y1, const T2* __restrict__ X2,
                             const T2* __restrict__ Y2, int m, int p, c64* stage, c64* G1, c64* G2) {
@@ -476,7 +483,8 @@ __device__ void tiled_gram2(const T1* __restrict__ X1, bool herm1, const T1* __r
     const int ld = p + 1;
     c64* sX1 = stage;
     c64* sX2 = sX1 + kRCH * ld;
-    const int rg = threadIdx.x % kRG;
+    constexpr int kRGt = GramRG<PC>::value;
+    const int rg = threadIdx.x % kRGt;
     // software pipeline over row chunks: the next chunk's elements are loaded into registers
     // (all in flight together) while the current chunk is consumed from shared memory
     constexpr int kEPT = (PC * kRCH + kNT - 1) / kNT;  // elements per thread per chunk per operand
@@ -493,8 +501,8 @@ __device__ void tiled_gram2(const T1* __restrict__ X1, bool herm1, const T1* __r
             if (X2) n2[u] = ok ? X2[static_cast<size_t>(c) * m + r0 + r] : c32{0.f, 0.f};
         }
     };
-    for (int pass = 0; pass * (kNT / kRG) < ntiles; ++pass) {
-        const int tile = pass * (kNT / kRG) + threadIdx.x / kRG;
+    for (int pass = 0; pass * (kNT / kRGt) < ntiles; ++pass) {
+        const int tile = pass * (kNT / kRGt) + threadIdx.x / kRGt;
         const bool active = tile < ntiles;
         const bool second = tile >= t1;
         int ti = 0, tj = 0;
@@ -532,7 +540,7 @@ __device__ void tiled_gram2(const T1* __restrict__ X1, bool herm1, const T1* __r
             if (active) {
                 const c64* xs = second ? sX2 : sX1;
                 const c64* ys = sX1;
-                for (int r = rg; r < rn; r += kRG) {
+                for (int r = rg; r < rn; r += kRGt) {
                     c64 x[4], y[4];
 #pragma unroll
                     for (int a = 0; a < 4; ++a) {
@@ -552,7 +560,7 @@ __device__ void tiled_gram2(const T1* __restrict__ X1, bool herm1, const T1* __r
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
 #pragma unroll
-                for (int o = 1; o < kRG; o <<= 1) {
+                for (int o = 1; o < kRGt; o <<= 1) {
                     acc[a][b].re += __shfl_xor_sync(0xffffffffu, acc[a][b].re, o);
                     acc[a][b].im += __shfl_xor_sync(0xffffffffu, acc[a][b].im, o);
                 }
