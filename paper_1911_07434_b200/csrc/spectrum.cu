@@ -825,7 +825,12 @@ __global__ void __launch_bounds__(kOT, 3 - kONB) k_spectrum_i8(const int8_t* __r
                 for (int e = 0; e < 4; ++e) acc[sg][x][n][e] = 0;
     for (int i = 0; i < kONS - 1 && i < nkb; ++i) issue(i, i);
     for (int kb = 0; kb < nkb; ++kb) {
-        if (kb + 1 < nkb) asm volatile("cp.async.wait_group %0;" ::"n"(kONS - 2) : "memory");
+        // groups committed after block kb: min(kONS - 2, nkb - 1 - kb); wait until block kb has landed
+        static_assert(kONS >= 2 && kONS <= 5, "ring depth");
+        const int after = min(kONS - 2, nkb - 1 - kb);
+        if (after >= 3) asm volatile("cp.async.wait_group 3;" ::: "memory");
+        else if (after == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+        else if (after == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
         else asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();  // block kb staged; block kb - 1's buffer is free
         if (kb + kONS - 1 < nkb) issue(kb + kONS - 1, (kb + kONS - 1) % kONS);

@@ -7,7 +7,7 @@ Gate (BASELINE.json north_star): identical peak grid indices, and pseudo-spectra
 import numpy as np
 import pytest
 
-from tests.gpu_helpers import compare_frames, run_gpu
+from tests.gpu_helpers import compare_frames, draws, plan_for, run_gpu
 
 pytestmark = pytest.mark.gpu
 
@@ -235,3 +235,32 @@ def test_norm2_sampling_parity(fm, oracle, cfgs):
     worst, mism = compare_frames(oracle, cfg, x, frames, res)
     assert not mism, mism
     assert worst <= DB_TOL, worst
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,nf", [("c2", 300), ("c3", 200), ("c2", 64)])
+def test_batch_is_deterministic(fm, oracle, cfgs, name, nf):
+    """The batch path is bitwise repeatable: the same frames through one plan five times give identical
+    spectra, peak records and bases (catches staging races in the pipelined kernels, e.g. a cp.async ring
+    consumed before its group landed, which the tolerance-level parity tests can miss)."""
+    import torch
+    cfg = cfgs[name]
+    frames = list(range(nf))
+    x, _, _ = oracle.generate_batch(cfg.base_seed, frames, cfg.spec)
+    plan = plan_for(fm, cfg, nf)
+    om, ix = draws(fm, oracle, cfg, frames)
+    xd = torch.from_numpy(np.ascontiguousarray(x).view(np.float32)).cuda()
+    omd = torch.from_numpy(om).cuda() if om is not None else None
+    ixd = torch.from_numpy(ix).cuda() if ix is not None else None
+    ref = None
+    for _ in range(5):
+        out = plan.outputs(nf, spectrum=True, basis=True)
+        plan.run(nf, xd, omd, ixd, out)
+        torch.cuda.synchronize()
+        res = {k: v.cpu().numpy() for k, v in out.items()}
+        if ref is None:
+            ref = res
+            continue
+        for k in ("spectrum", "peak_cells", "peak_heights", "baseline", "peak_count", "status", "basis"):
+            assert np.array_equal(res[k], ref[k]), k
+    plan.close()
