@@ -37,7 +37,7 @@ typedef int32_t fm_status;
 #define FM_FRAME_OK 0
 #define FM_FRAME_RANK 1
 #define FM_FRAME_NOCONV 2
-#define FM_FRAME_RANGE 4
+#define FM_FRAME_RANGE 4     /* max |x| outside [2^-50, 2^50]: R would leave the complex64 range */
 #define FM_FRAME_NONFINITE 8
 
 /* Method enum values follow R/include/fastmusic/types.hpp:46-54 for the three hot-path methods. */
@@ -100,7 +100,10 @@ typedef struct fm_plan_desc {
     double d, lambda;       /* ULA spacing and wavelength */
     int64_t min_sep_cells;  /* peak separation (R/include/fastmusic/bench.hpp:71 default 3) */
     int64_t max_frames;     /* workspace capacity */
+    int32_t flags;          /* FM_PLAN_* bits (0 = defaults) */
 } fm_plan_desc;
+/* exact method: full Jacobi eigensolver on every frame instead of the certified subspace iteration */
+#define FM_PLAN_EXACT_JACOBI 1
 typedef struct fm_plan_s* fm_plan;
 
 /* Validates like the reference (R/src/estimators.cpp:74-76,88-92,105-112) and allocates
@@ -125,19 +128,24 @@ typedef struct fm_batch_io {
 } fm_batch_io;
 
 /* Device-resident batched pipeline: covariance -> subspace -> spectrum -> peaks, enqueued
- * on `stream` (cudaStream_t, may be NULL). Asynchronous; per-frame status in io->status. */
+ * on `stream` (cudaStream_t, may be NULL). Asynchronous; per-frame status in io->status.
+ * Frames whose Nystrom tail is singular (H = V^H C or S(I, I) singular, e.g. N < p) are finished by an
+ * exact-algebra fallback with the reference's truncating pseudo-inverse; frames with max |x| outside the fp16
+ * operand range are recomputed with a power-of-two prescale. Neither sets a status bit. */
 fm_status fm_run_batch(fm_plan plan, int64_t frames, const fm_batch_io* io, void* stream);
-/* Re-run subspace+spectrum for the listed frames (device int32 list) on the covariance kept
- * from the last fm_run_batch (fast2 redraws with derive(seed, 0xF257 + attempt)). */
-fm_status fm_rerun_frames(fm_plan plan, int64_t count, const int32_t* d_frames, const fm_batch_io* io, void* stream);
+/* Re-run subspace + spectrum + peaks for the listed frames (HOST int32 list of ascending frame indices of the
+ * batch `io` describes) on the covariance kept from the last fm_run_batch / fm_estimate_batch_host; io->omega /
+ * io->indices carry the new draws (fast2 redraws use derive(seed, 0xF257 + attempt), R/src/estimators.cpp:114-137).
+ * Other frames' outputs are untouched. Asynchronous on `stream`. */
+fm_status fm_rerun_frames(fm_plan plan, int64_t count, const int32_t* h_frames, const fm_batch_io* io, void* stream);
 /* Stage timing: when enabled, every fm_run_batch records CUDA events on its stream between
  * its stages; once the stream is synchronised, fm_plan_stage_times returns the summed
  * {covariance, subspace, autocorrelation, spectrum+peaks} ms over the batches recorded since
  * profiling was enabled (or last read), their count in *runs, and restarts the count. */
 fm_status fm_plan_set_profiling(fm_plan plan, int32_t on);
 fm_status fm_plan_stage_times(fm_plan plan, float* ms4, int32_t* runs);
-/* Split each fm_run_batch into `subbatches` frame ranges run concurrently on plan-owned
- * streams forked from / joined into the caller's stream (0 = automatic: 4 when frames >= 512). */
+/* Split each fm_run_batch into `subbatches` (<= 16) frame ranges run concurrently on plan-owned streams forked
+ * from / joined into the caller's stream (0 = automatic: 1 on the p <= 16 plane path, else 2 when frames >= 512). */
 fm_status fm_plan_set_concurrency(fm_plan plan, int32_t subbatches);
 /* Number of kernel launches one fm_run_batch enqueues (per sub-batch). */
 int32_t fm_plan_launches_per_batch(fm_plan plan);
@@ -217,7 +225,7 @@ fm_status fm_z_block_lanczos_subspace(int64_t m, const double* s, int64_t k, int
 /* music_spectrum, R/src/spectrum.cpp:50-68 on theta_l = theta0 + ((theta1-theta0)*l)/(L-1) */
 fm_status fm_z_music_spectrum(int64_t m, int64_t kb, const double* basis, int64_t grid_size, double theta0,
                               double theta1, double d, double lambda, double* values);
-/* extract_peaks, R/src/spectrum.cpp:182-188; cells ascending */
+/* extract_peaks, R/src/spectrum.cpp:182-188 (any L >= 1, K >= 1, any finite values); cells ascending */
 fm_status fm_z_extract_peaks(const double* values, int64_t grid_size, int64_t k, int64_t min_sep, int64_t* cells,
                              double* heights, int64_t* count, double* baseline, int32_t* shortfall);
 

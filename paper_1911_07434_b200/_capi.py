@@ -35,7 +35,11 @@ EXPORTED = [
 class PlanDesc(C.Structure):
     _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64), ("method", C.c_int32), ("p", C.c_int64),
                 ("t", C.c_int32), ("grid_size", C.c_int64), ("theta0", C.c_double), ("theta1", C.c_double),
-                ("d", C.c_double), ("lam", C.c_double), ("min_sep_cells", C.c_int64), ("max_frames", C.c_int64)]
+                ("d", C.c_double), ("lam", C.c_double), ("min_sep_cells", C.c_int64), ("max_frames", C.c_int64),
+                ("flags", C.c_int32)]
+
+
+PLAN_EXACT_JACOBI = 1
 
 
 class BatchIO(C.Structure):

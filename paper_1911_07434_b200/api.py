@@ -419,9 +419,12 @@ class BatchPlan:
     """fm_plan over device tensors (torch for allocation / streams only)."""
 
     def __init__(self, m, n, k, method="fast2", p=0, t=1, grid_size=3601, theta0=-KPI / 2, theta1=KPI / 2, d=0.5,
-                 lam=1.0, min_sep_cells=3, max_frames=1, device=0):
+                 lam=1.0, min_sep_cells=3, max_frames=1, device=0, exact_jacobi=False):
+        """exact_jacobi: the exact method runs the full Jacobi eigensolver on every frame (FM_PLAN_EXACT_JACOBI)
+        instead of the certified subspace iteration."""
+        flags = _capi.PLAN_EXACT_JACOBI if exact_jacobi else 0
         self.desc = _capi.PlanDesc(m, n, k, _capi.METHOD[method], p, t, grid_size, theta0, theta1, d, lam,
-                                   min_sep_cells, max_frames)
+                                   min_sep_cells, max_frames, flags)
         self.method, self.m, self.n, self.k, self.p, self.t, self.L = method, m, n, k, p, t, grid_size
         self.max_frames, self.device = max_frames, device
         h = C.c_void_p()
@@ -491,10 +494,13 @@ class BatchPlan:
         _check(LIB.fm_run_batch(self.handle, frames, C.byref(io), s))
         return out
 
-    def rerun(self, frames, x, omega=None, indices=None, out=None, stream=None):
+    def rerun(self, frame_list, x, omega=None, indices=None, out=None, stream=None):
+        """Subspace + spectrum + peaks again for the listed frames (ascending indices of the last batch) on the
+        kept covariance; x / omega / indices / out are the whole batch's buffers."""
+        fl = np.ascontiguousarray(np.asarray(frame_list, np.int32))
         io = self._io(x, omega, indices, out)
         s = None if stream is None else C.c_void_p(stream.cuda_stream)
-        _check(LIB.fm_rerun_frames(self.handle, frames, None, C.byref(io), s))
+        _check(LIB.fm_rerun_frames(self.handle, fl.size, ptr(fl) if fl.size else None, C.byref(io), s))
         return out
 
     def estimate_host(self, x_host, draw_seeds, spectrum=None, heights=None, baseline=None, stream=None):

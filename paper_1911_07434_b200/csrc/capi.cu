@@ -24,7 +24,12 @@
 // ------------------------------------------------------------------ kernel launchers (other TUs)
 cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, int64_t frames, int64_t m, int64_t n,
                              cudaStream_t stream, void* planes_hi = nullptr, void* planes_lo = nullptr,
-                             float* scale = nullptr, int64_t n_true = 0);
+                             float* scale = nullptr, int64_t n_true = 0, const FmCovRescue* rescue = nullptr);
+size_t fm_final_fallback_scratch_bytes(int ctas);
+int fm_final_fallback_ctas();
+cudaError_t fm_launch_final_fallback(const void* C, const void* V, const void* H, void* basis, double* eig,
+                                     int32_t* status, void* scratch, int frames, int m, int p, int k,
+                                     cudaStream_t s);
 template <typename T>
 cudaError_t fm_launch_rmul(const void*, const void*, const void*, void*, const int32_t*, int, int, int, bool,
                            cudaStream_t);
@@ -45,10 +50,6 @@ cudaError_t fm_launch_cholqr_warp(const void* C, void* work, void* Vout, void* R
                                   int32_t* status, int frames, int m, int p, bool final_mode, cudaStream_t s);
 cudaError_t fm_launch_nystrom_warp2(const void* H, const void* work, const void* Rt, void* basis, double* eig,
                                     int32_t* status, int frames, int m, int p, int k, cudaStream_t s);
-cudaError_t fm_launch_orth_tiled(const void* C, void* Vout, int32_t* status, int frames, int m, int p,
-                                 cudaStream_t s);
-cudaError_t fm_launch_final_tiled(const void* C, const void* V, const void* H, void* basis, double* eig,
-                                  int32_t* status, int frames, int m, int p, int k, cudaStream_t s);
 cudaError_t fm_launch_rmul_tc(const float* d_r, const float* d_omega, const float* d_v, float* d_c, int64_t frames,
                               int64_t m, int64_t p, cudaStream_t stream);
 cudaError_t fm_launch_orth_split(const void* C, void* Vout, void* Lw, int32_t* permw, int32_t* status, int frames,
@@ -62,19 +63,16 @@ cudaError_t fm_launch_final_split(const void* C, const void* V, void* Hw, void* 
                                   double* eig_next = nullptr, const void* gpart = nullptr,
                                   const void* hpart = nullptr);
 cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, int k, cudaStream_t s);
-cudaError_t fm_launch_spectrum_peaks(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
-                                     double* spec64, int K, int min_sep, int32_t* cells, double* heights,
-                                     double* baseline, int32_t* count, int32_t* status, cudaStream_t s);
+cudaError_t fm_launch_spectrum_one(const void* t, const void* zgrid, int frames, int m, int L, double* spec64,
+                                   cudaStream_t s);
+size_t fm_peaks_workspace_bytes(int frames, int L, int K);
 cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K, int min_sep, int32_t* cells,
-                                 double* heights, double* baseline, int32_t* count, int32_t* overflow,
-                                 cudaStream_t s, int cap_hint = 0);
+                                 double* heights, double* baseline, int32_t* count, void* gws, cudaStream_t s);
 cudaError_t fm_launch_orthocheck(const void* basis, int frames, int m, int k, double* dev, cudaStream_t s);
-cudaError_t fm_launch_spectrum_dmma(const void* t, const void* zpow, int frames, int m, int L, float* spec32,
-                                    double* spec64, cudaStream_t s);
 cudaError_t fm_launch_spectrum_i8(const void* t, const int8_t* zd, int8_t* td, double* tscale, int frames, int m, int L,
                                   float* spec32, double* spec64, cudaStream_t s);
 cudaError_t fm_launch_spectrum_multi(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
-                                     double* spec64, cudaStream_t s, bool symmetric);
+                                     double* spec64, cudaStream_t s);
 template <typename T>
 cudaError_t fm_launch_jacobi_eig(const void* R, void* work, void* basis, double* eig, int32_t* status, int frames,
                                  int m, int k, cudaStream_t s, int only_flagged = 0);
@@ -290,26 +288,6 @@ std::vector<double> zgrid_host(int64_t L, double theta0, double theta1, double d
     return z;
 }
 
-// Power tables of the mirror-symmetric spectrum GEMM (spectrum.cu k_spectrum_dmma): for the first nq = (L + 1) / 2
-// grid points, zhi[a][q] = e^{j 16 a phi_q} (a < ceil(M / 16)) then zlo[b][q] = e^{j b phi_q} (b < 16), with
-// phi_q = 2 pi d sin(theta_q) / lambda as zgrid_host; each angle formed in fp64 and passed to glibc cos / sin.
-std::vector<double> zpow_host(int64_t L, double theta0, double theta1, double d, double lambda, int64_t m) {
-    const int64_t nq = (L + 1) / 2, na = (m + 15) / 16;
-    std::vector<double> z(static_cast<size_t>(2 * (na + 16) * nq));
-    const double span = theta1 - theta0;
-    for (int64_t q = 0; q < nq; ++q) {
-        const double th = theta0 + (span * static_cast<double>(q)) / static_cast<double>(L - 1);
-        const double step = 2.0 * kPi * d * std::sin(th) / lambda;
-        for (int64_t a = 0; a < na + 16; ++a) {
-            const double mult = a < na ? 16.0 * static_cast<double>(a) : static_cast<double>(a - na);
-            const double ang = mult * step;
-            z[2 * (a * nq + q)] = std::cos(ang);
-            z[2 * (a * nq + q) + 1] = std::sin(ang);
-        }
-    }
-    return z;
-}
-
 // Digits of the spectrum's cos / sin table for the int8 Ozaki kernel (spectrum.cu k_spectrum_i8): for pair
 // column q < nq and delta < m, z = (cos, sin)(delta phi_q) (angle formed in fp64, glibc), written as 5 signed
 // base-128 digits of z / 2, in mma B-fragment order [s][cs][q / 8][delta / 32][lane][2 x u32] (column q % 8 = lane / 4,
@@ -370,7 +348,7 @@ void parallel_for(int64_t count, int threads, F&& fn) {
 }  // namespace
 
 // ------------------------------------------------------------------ misc
-extern "C" int32_t fm_abi_version(void) { return 1; }
+extern "C" int32_t fm_abi_version(void) { return 2; }
 
 extern "C" const char* fm_status_string(fm_status s) {
     switch (s) {
@@ -546,7 +524,7 @@ struct fm_plan_s {
     double* t = nullptr;      // frames x M complex128
     double* spec64 = nullptr; // frames x L (fp64 spectrum for peak picking)
     double* zgrid = nullptr;  // L complex128
-    double* zpow = nullptr;   // mirror-symmetric grids: (ceil(M / 16) + 16) x ceil(L / 2) complex128 power tables
+    uint8_t* peak_ws = nullptr;  // peak-picking workspace when a frame's does not fit in shared memory (long grids)
     int8_t* zdig = nullptr;   // mirror-symmetric grids: int8 digits of the cos / sin table (Ozaki spectrum)
     int8_t* tdig = nullptr;   // per batch: int8 digits of t (frames padded per sub-batch)
     double* tscale = nullptr; // per batch: power-of-two scale of each frame's t
@@ -554,6 +532,13 @@ struct fm_plan_s {
     int32_t* scratch_status = nullptr;  // frames
     float* x_pad = nullptr;             // odd N: frames x M x (N + 1) complex64
     float* rscale = nullptr;            // frames: s_f of the fp16 hi/lo R planes (plane mode)
+    // covariance rescue pass (cov_tc.cu): per-frame max |x|, out-of-range list, counts (one per sub-batch), prescale
+    uint32_t* amax = nullptr;
+    int32_t* rlist = nullptr;
+    int32_t* rcount = nullptr;
+    float* xscale = nullptr;
+    void* fb_scratch = nullptr;         // final-step fallback (final_fallback.cu) work matrices
+    size_t peak_ws_frame = 0;           // bytes of peak_ws per frame (0: frames fit in shared memory)
     bool last_planes = false;           // R of the last run is stored as planes (fm_rerun_frames)
     // exact method via certified subspace iteration (pe > 0): plan-owned Omega, R U product, gap
     int pe = 0;
@@ -629,12 +614,12 @@ struct fm_plan_s {
 
 // Exact method via certified subspace iteration: p_e = 2K rounded up to a multiple of 4 (>= K + 4),
 // t = kExactIters power steps, Omega from kExactSeed; needs the tensor-core / tiled paths (even M,
-// p_e <= 32, p_e <= M). Otherwise (or FM_EXACT_JACOBI=1) every frame runs the Jacobi solver.
+// p_e <= 32, p_e <= M). Otherwise (or with the FM_PLAN_EXACT_JACOBI flag) every frame runs the Jacobi solver.
 constexpr uint64_t kExactSeed = 0x4558414354ull;
 constexpr int kExactIters = 3;
 constexpr double kExactTol = 1e-3;  // max_k ||R u_k - lambda_k u_k|| <= tol * (lambda_K - lambda_{K+1})
 static int exact_fast_p(const fm_plan_desc& d) {
-    if (d.method != FM_METHOD_EXACT || std::getenv("FM_EXACT_JACOBI")) return 0;
+    if (d.method != FM_METHOD_EXACT || (d.flags & FM_PLAN_EXACT_JACOBI)) return 0;
     const int pe = std::max<int>(static_cast<int>((2 * d.k + 3) / 4 * 4), static_cast<int>((d.k + 4 + 3) / 4 * 4));
     if (pe > 32 || pe > d.m || (d.m % 2) || (d.k % 4)) return 0;
     return pe;
@@ -697,6 +682,15 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
     chk(pl->get(&pl->zgrid, L * 2));
     chk(pl->get(&pl->scratch_status, B));
     chk(pl->get(&pl->rscale, B));
+    chk(pl->get(&pl->amax, B));
+    chk(pl->get(&pl->rlist, B));
+    chk(pl->get(&pl->rcount, 64));
+    chk(pl->get(&pl->xscale, B));
+    if (desc->method != FM_METHOD_EXACT) {
+        uint8_t* fb = nullptr;
+        chk(pl->get(&fb, fm_final_fallback_scratch_bytes(fm_final_fallback_ctas())));
+        pl->fb_scratch = fb;
+    }
     if (desc->n & 1) chk(pl->get(&pl->x_pad, B * M * (static_cast<size_t>(desc->n) + 1) * 2));
     if (desc->method == FM_METHOD_FAST1_NORM2) chk(pl->get(&pl->omega_e, B * M * P));  // selection Omega = E_I
     if ((desc->method == FM_METHOD_FAST2 || desc->method == FM_METHOD_FAST1_NORM2) && M <= 256 && P <= 16) {
@@ -709,6 +703,7 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
         chk(pl->get(&pl->ru, B * K * M * 2));
         chk(pl->get(&pl->eig_next, B));
     }
+    if (e == cudaSuccess) e = cudaMemset(pl->amax, 0, sizeof(uint32_t) * B);
     if (e != cudaSuccess) {
         delete pl;
         return fm_fail_cuda(e, "fm_plan_create workspace", __FILE__, __LINE__);
@@ -743,12 +738,13 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
             delete pl;
             return fm_fail_cuda(e, "fm_plan_create zdig", __FILE__, __LINE__);
         }
-        const auto zp = zpow_host(desc->grid_size, desc->theta0, desc->theta1, desc->d, desc->lambda, desc->m);
-        e = pl->get(&pl->zpow, zp.size());
-        if (e == cudaSuccess) e = cudaMemcpy(pl->zpow, zp.data(), sizeof(double) * zp.size(), cudaMemcpyHostToDevice);
+    }
+    if (const size_t pws = fm_peaks_workspace_bytes(static_cast<int>(B), static_cast<int>(L), static_cast<int>(K))) {
+        pl->peak_ws_frame = pws / B;
+        e = pl->get(&pl->peak_ws, pws);
         if (e != cudaSuccess) {
             delete pl;
-            return fm_fail_cuda(e, "fm_plan_create zpow", __FILE__, __LINE__);
+            return fm_fail_cuda(e, "fm_plan_create peak workspace", __FILE__, __LINE__);
         }
     }
     *out = pl;
@@ -791,19 +787,15 @@ extern "C" fm_status fm_plan_stage_times(fm_plan plan, float* ms, int32_t* runs)
     return FM_OK;
 }
 
-// Tensor-core products (rmul_tc.cu) need an even M (16-byte TMA row pitch) and p <= 32;
-// FM_SIMT_RMUL=1 selects the SIMT k_rmul for comparison.
-static bool tc_rmul(int m, int p) {
-    static const bool simt = std::getenv("FM_SIMT_RMUL") != nullptr;
-    return !simt && (m % 2) == 0 && p >= 4 && p <= 32 && (p % 4) == 0;
-}
+// Tensor-core products (rmul_tc.cu) need an even M (16-byte TMA row pitch) and p <= 32 (p % 4 == 0);
+// other shapes use the SIMT k_rmul.
+static bool tc_rmul(int m, int p) { return (m % 2) == 0 && p >= 4 && p <= 32 && (p % 4) == 0; }
 
 // R as fp16 hi/lo planes of R / s_f (cov_tc.cu kEpi = 2 -> rmul_planes_kernel): M <= 256 (one tile per
-// frame), tensor-core products; FM_NO_PLANES=1 keeps complex64 R + the tf32 products (comparison).
+// frame), tensor-core products. fast2 / fast1_norm2 only: the exact method's Jacobi fallback and fast1's gather
+// read complex64 R.
 static bool plane_mode(const fm_plan_s* pl) {
-    static const bool off = std::getenv("FM_NO_PLANES") != nullptr;
-    // fast2 only: the exact method's Jacobi fallback and fast1's gather read complex64 R
-    return !off && (pl->d.method == FM_METHOD_FAST2 || pl->d.method == FM_METHOD_FAST1_NORM2) && pl->d.m <= 256 &&
+    return (pl->d.method == FM_METHOD_FAST2 || pl->d.method == FM_METHOD_FAST1_NORM2) && pl->d.m <= 256 &&
            tc_rmul(static_cast<int>(pl->d.m), static_cast<int>(pl->d.p));
 }
 struct Planes {  // per-sub-batch view; hi == nullptr: complex64 R
@@ -821,28 +813,28 @@ static Planes planes_view(fm_plan pl, int64_t f0) {
     return v;
 }
 
-static bool split_final() {  // FM_FUSED_FINAL=1 selects the single-kernel k_final_tiled (comparison)
-    static const bool fused = std::getenv("FM_FUSED_FINAL") != nullptr;
-    return !fused;
+// Gram epilogue (plane path, p <= 16): the products also form G = C^H C (and H = V^H C on the last one), so the
+// orthonormalisation / final stage skip their Gram kernels.
+static bool gram_epilogue(const fm_plan_s* pl) {
+    return plane_mode(pl) && pl->d.p <= 16 && (pl->d.p % 4) == 0 && pl->gpart != nullptr;
 }
 
 extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
     if (!plan) return 0;
-    const int t = plan->d.t;
-    int n = 1 /*cov*/ + 1 /*clear*/ + 3 /*autocorr, spectrum, peaks*/ + (plan->x_pad ? 1 : 0) /*odd-N pad*/;
-    // int8 spectrum: + the digit split of t (k_slice_t), see run_post_cov
-    if (plan->zdig && plan->d.theta0 == -plan->d.theta1 && !std::getenv("FM_SPECTRUM_FMA") && !std::getenv("FM_SPECTRUM_DMMA"))
-        n += 1;
-    const bool tiled = plan->d.p <= 32 && (plan->d.p % 4) == 0;
-    // Gram epilogue (plane path, p <= 16): the Gram kernels are folded into the products
-    const int gepi = tiled && split_final() && plane_mode(plan) && plan->d.p <= 16 && !std::getenv("FM_NO_GRAM_EPI") ? 1 : 0;
-    const int fin = tiled ? (split_final() ? 3 - gepi : 1) : 2;  // gram, small-warp, basis | fused | cholqr, nystrom
-    const int orth = tiled && split_final() ? 3 - gepi : 1;  // gram, pivoted chol, rows solve | fused
-    if (plan->d.method == FM_METHOD_FAST2) n += 1 + t * (orth + 1) + fin;  // rmul, t x (orth, rmul), final
-    else if (plan->d.method == FM_METHOD_FAST1_NORM2) n += 1 + 1 + (orth + 1) + fin;  // select, rmul, orth, rmul, final
-    else if (plan->d.method == FM_METHOD_FAST1) n += 1 + fin;      // gather, final
+    const auto& d = plan->d;
+    const int t = d.t;
+    // covariance + rescue list + rescue covariance + status clear + autocorr + spectrum + peaks (+ odd-N pad)
+    int n = 1 + 2 + 1 + 3 + (plan->x_pad ? 1 : 0);
+    if (plan->zdig) n += 1;  // int8 spectrum: + the digit split of t (k_slice_t)
+    const bool tiled = d.p <= 32 && (d.p % 4) == 0;
+    const int gepi = gram_epilogue(plan) ? 1 : 0;
+    const int fin = (tiled ? 3 - gepi : 2) + 1;  // gram, small-warp, (fallback), basis | cholqr, nystrom, (fallback)
+    const int orth = tiled ? 3 - gepi : 1;      // gram, pivoted chol, rows solve | cholqr
+    if (d.method == FM_METHOD_FAST2) n += 1 + t * (orth + 1) + fin;  // rmul, t x (orth, rmul), final
+    else if (d.method == FM_METHOD_FAST1_NORM2) n += 1 + 1 + (orth + 1) + fin;  // select, rmul, orth, rmul, final
+    else if (d.method == FM_METHOD_FAST1) n += 1 + fin;      // gather, final
     else if (plan->pe > 0) n += 1 + 1 + kExactIters * (3 + 1) + 3 + 1 + 1 + 1 + 1 + 1;  // see run_post_cov
-    else n += 1;                                                    // jacobi
+    else n += 1;                                              // jacobi
     return n;
 }
 
@@ -893,6 +885,8 @@ struct WorkView {
     double* eig_next;
     double* gpart;
     double* hpart;
+    uint8_t* peak_ws;
+    FmCovRescue resc;
     size_t dslot;  // first frame row of this sub-batch's region in tdig / tscale
 };
 
@@ -919,6 +913,8 @@ static WorkView work_view(fm_plan pl, int64_t f0, int sub = 0) {
     w.t = pl->t + f0 * M * 2;
     w.spec64 = pl->spec64 + f0 * static_cast<size_t>(d.grid_size);
     w.scratch = pl->scratch_status + f0;
+    w.peak_ws = pl->peak_ws ? pl->peak_ws + f0 * pl->peak_ws_frame : nullptr;
+    w.resc = FmCovRescue{pl->amax + f0, pl->rlist + f0, pl->rcount + std::min(sub, 63), pl->xscale + f0};
     return w;
 }
 
@@ -950,19 +946,15 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     double* eig = io->eigenvalues ? io->eigenvalues : w.eig;
     k_clear_bits<<<(F + 255) / 256, 256, 0, s>>>(io->status, F, FM_FRAME_RANK | FM_FRAME_NOCONV);
     FM_CUDA_OK(cudaGetLastError());
-    const bool warp_path = P <= 32;  // block-per-frame small-matrix kernels (smallmat.cu)
-    const bool tiled = P <= 32 && (P % 4) == 0;  // register-tiled Gram + fused final stage
+    const bool warp_path = P <= 32;              // block-per-frame small-matrix kernels (smallmat.cu)
+    const bool tiled = P <= 32 && (P % 4) == 0;  // register-tiled Gram + split final stage
     // Gram epilogue (plane path, p <= 16): the products also form G = C^H C (and H = V^H C on the last one),
-    // so the orthonormalisation / final stage skip their Gram kernels. FM_NO_GRAM_EPI=1: separate kernels.
-    static const bool no_gram_epi = std::getenv("FM_NO_GRAM_EPI") != nullptr;
-    const bool gepi = pv.hi && w.gpart && P <= 16 && tiled && split_final() && !no_gram_epi;
+    // so the orthonormalisation / final stage skip their Gram kernels.
+    const bool gepi = pv.hi && w.gpart && P <= 16 && tiled;
     auto orth = [&](bool final_mode, const void* vin) -> fm_status {
         if (tiled && !final_mode) {
-            if (split_final())
-                FM_LAUNCH(fm_launch_orth_split(w.C, w.V, w.Rt, reinterpret_cast<int32_t*>(w.H), io->status, F, M, P, s,
-                                               gepi ? w.gpart : nullptr));
-            else
-                FM_LAUNCH(fm_launch_orth_tiled(w.C, w.V, io->status, F, M, P, s));
+            FM_LAUNCH(fm_launch_orth_split(w.C, w.V, w.Rt, reinterpret_cast<int32_t*>(w.H), io->status, F, M, P, s,
+                                           gepi ? w.gpart : nullptr));
             return FM_OK;
         }
         if (warp_path)
@@ -981,17 +973,21 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
             FM_LAUNCH(fm_launch_nystrom_warp<float>(w.H, w.work, w.Rt, basis, eig, io->status, F, M, P, K, s));
         return FM_OK;
     };
+    // frames the fast Nystrom tail flagged (singular H, rank-deficient C, Jacobi cap): exact reference algebra
+    // with a truncating pinv (final_fallback.cu); unflagged frames return at once.
+    auto fallback = [&](const void* v, const void* h) -> fm_status {
+        FM_LAUNCH(fm_launch_final_fallback(w.C, v, h, basis, eig, io->status, pl->fb_scratch, F, M, P, K, s));
+        return FM_OK;
+    };
     fm_status st = FM_OK;
-    // C = R Omega (omega) or C = R V: fp16 planes -> rmul_planes_kernel, complex64 R -> tf32 kernel / SIMT
-    // Range-finder products (all but the last) read only the hi plane of R (R to 2^-12 s_f): they only
-    // shape span(V), and the last product, which feeds the Nystrom step, reads both planes. Measured over
-    // 1024 c2 frames vs the fp64 oracle: worst spectrum error 0.00556 -> 0.00557 dB, no peak changes,
-    // step 1.191 -> 1.140 ms (scripts_precision_sweep.py). FM_RMUL_HI_ONLY=0 reads both planes everywhere.
-    const bool hi_only_env = !(std::getenv("FM_RMUL_HI_ONLY") && std::atoi(std::getenv("FM_RMUL_HI_ONLY")) == 0);
+    // C = R Omega (omega) or C = R V: fp16 planes -> rmul_planes_kernel, complex64 R -> tf32 kernel / SIMT.
+    // Range-finder products (all but the last) read only the hi plane of R (R to 2^-12 s_f): they only shape
+    // span(V); the last product, which feeds the Nystrom step, reads both planes. Measured over 1024 c2 frames
+    // vs the fp64 oracle: worst spectrum error 0.00556 -> 0.00557 dB, no peak changes, step 1.191 -> 1.140 ms.
     auto rmul = [&](const float* omega, const float* v, float* c, int p, bool range_only = false,
                     int gram = 0) -> fm_status {
         if (pv.hi)
-            FM_LAUNCH(fm_launch_rmul_planes(pv.hi, pv.lo, pv.scale, omega, v, c, F, M, p, s, range_only && hi_only_env,
+            FM_LAUNCH(fm_launch_rmul_planes(pv.hi, pv.lo, pv.scale, omega, v, c, F, M, p, s, range_only,
                                             gepi ? gram : 0, w.gpart, w.hpart));
         else if (tc_rmul(M, p))
             FM_LAUNCH(fm_launch_rmul_tc(R, omega, v, c, F, M, p, s));
@@ -1020,26 +1016,22 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
             if ((st = rmul(nullptr, w.V, w.C, P, it + 1 < tt, it + 1 < tt ? 1 : 2)) != FM_OK) return st;
         }
         if (tiled) {
-            if (split_final())
-                FM_LAUNCH(fm_launch_final_split(w.C, w.V, w.H, w.Rt, w.work, basis, eig, io->status, F, M, P, K, s,
-                                                nullptr, gepi ? w.gpart : nullptr, gepi ? w.hpart : nullptr));
-            else
-                FM_LAUNCH(fm_launch_final_tiled(w.C, w.V, nullptr, basis, eig, io->status, F, M, P, K, s));
+            FM_LAUNCH(fm_launch_final_split(w.C, w.V, w.H, w.Rt, w.work, basis, eig, io->status, F, M, P, K, s,
+                                            nullptr, gepi ? w.gpart : nullptr, gepi ? w.hpart : nullptr));
         } else {
             if ((st = orth(true, w.V)) != FM_OK) return st;
             if ((st = nystrom()) != FM_OK) return st;
         }
+        if ((st = fallback(w.V, nullptr)) != FM_OK) return st;
     } else if (d.method == FM_METHOD_FAST1) {
         FM_LAUNCH(fm_launch_gather<float>(R, io->indices, w.C, w.H, nullptr, F, M, P, s));
         if (tiled) {
-            if (split_final())
-                FM_LAUNCH(fm_launch_final_split(w.C, nullptr, w.H, w.Rt, w.work, basis, eig, io->status, F, M, P, K, s));
-            else
-                FM_LAUNCH(fm_launch_final_tiled(w.C, nullptr, w.H, basis, eig, io->status, F, M, P, K, s));
+            FM_LAUNCH(fm_launch_final_split(w.C, nullptr, w.H, w.Rt, w.work, basis, eig, io->status, F, M, P, K, s));
         } else {
             if ((st = orth(true, nullptr)) != FM_OK) return st;
             if ((st = nystrom()) != FM_OK) return st;
         }
+        if ((st = fallback(nullptr, w.H)) != FM_OK) return st;
     } else if (pl->pe > 0) {
         // exact_signal_subspace as certified subspace iteration: C = R Omega, kExactIters x {V = orth(C),
         // C = R V}, Nystrom/Rayleigh step -> U, lambda, lambda_{K+1}; then R U and the residual test;
@@ -1070,29 +1062,20 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     if (prof) mark(pl, 2, s);
     FM_LAUNCH(fm_launch_autocorr(basis, w.t, F, M, K, s));
     if (prof) mark(pl, 3, s);
-    // mirror-symmetric grid (theta0 = -theta1): pairs (theta, -theta) share one evaluation;
-    // FM_NO_SYM_SPECTRUM=1 forces the per-point kernel (comparison)
-    static const bool no_sym = std::getenv("FM_NO_SYM_SPECTRUM") != nullptr;
-    const bool sym = !no_sym && d.theta0 == -d.theta1;
-    // mirror-symmetric grids: the spectrum as two fp64 GEMMs on the FP64 tensor cores (k_spectrum_dmma);
-    // FM_SPECTRUM_FMA=1 keeps the fp64 power-recurrence kernel (comparison)
-    static const bool fma_spec = std::getenv("FM_SPECTRUM_FMA") != nullptr;
-    static const bool dmma_spec = std::getenv("FM_SPECTRUM_DMMA") != nullptr;
+    // mirror-symmetric grid (theta0 = -theta1): pairs (theta, -theta) share one evaluation on the INT8 tensor cores
+    // with fp64-exact digit splitting (k_spectrum_i8); other grids: the fp64 power-recurrence kernel
+    const bool sym = d.theta0 == -d.theta1;
     const bool dig_fits = w.dslot + (static_cast<size_t>(F) + 63) / 64 * 64 <= pl->tdig_rows;
-    if (sym && pl->zdig && dig_fits && !fma_spec && !dmma_spec) {
-        // int8 tensor cores, fp64-exact digit splitting (k_spectrum_i8); sub-batch regions of the digit buffer
-        // start at f0 + 64 * (f0 / 64 ...) -- frames are offset by w.t, so place the region by the t offset
+    if (sym && pl->zdig && dig_fits) {
         const size_t mk = (static_cast<size_t>(M) + 31) / 32 * 32;
         FM_LAUNCH(fm_launch_spectrum_i8(w.t, pl->zdig, pl->tdig + w.dslot * 5 * 2 * mk, pl->tscale + w.dslot, F, M,
                                         static_cast<int>(d.grid_size), io->spectrum, w.spec64, s));
-    } else if (sym && pl->zpow && !fma_spec)
-        FM_LAUNCH(fm_launch_spectrum_dmma(w.t, pl->zpow, F, M, static_cast<int>(d.grid_size), io->spectrum, w.spec64, s));
-    else
+    } else {
         FM_LAUNCH(fm_launch_spectrum_multi(w.t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, w.spec64,
-                                           s, sym));
+                                           s));
+    }
     FM_LAUNCH(fm_launch_peaks_only(w.spec64, F, static_cast<int>(d.grid_size), K, static_cast<int>(d.min_sep_cells),
-                                   io->peak_cells, io->peak_heights, io->baseline, io->peak_count, w.scratch, s,
-                                   2 * M + 64));
+                                   io->peak_cells, io->peak_heights, io->baseline, io->peak_count, w.peak_ws, s));
     if (prof) mark(pl, 4, s);
     return FM_OK;
 }
@@ -1110,25 +1093,23 @@ static fm_status check_io(fm_plan pl, int64_t frames, const fm_batch_io* io) {
 }
 
 static int auto_subbatches(fm_plan pl, int64_t frames) {
-    if (pl->nsub > 0) return static_cast<int>(std::min<int64_t>(pl->nsub, frames));
-    if (const char* e = std::getenv("FM_SUBBATCHES")) return std::max(1, std::atoi(e));
+    if (pl->nsub > 0) return static_cast<int>(std::min<int64_t>(std::min(pl->nsub, 16), frames));
     // Two concurrent sub-batches for large batches, except on the p <= 16 plane path (Gram halves in the products),
     // whose kernels no longer gain from the overlap: c2 1.036 / 1.043 ms for 1 / 2; c3 1.408 / 1.286, c5 0.964 /
-    // 0.952, c3n 2.181 / 2.069 (scripts_nsub_cfg.sh).
+    // 0.952, c3n 2.181 / 2.069.
     if (pl->gpart) return 1;
     return frames >= 512 ? 2 : 1;
 }
 
-extern "C" fm_status fm_run_batch(fm_plan pl, int64_t frames, const fm_batch_io* io, void* stream) {
-    fm_status st = check_io(pl, frames, io);
-    if (st != FM_OK) return st;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    FM_CUDA_OK(cudaSetDevice(pl->device));
+// fm_run_batch on frames [ws0, ws0 + frames) of the plan workspace (the host path keeps every chunk's R in place
+// so that fm_rerun_frames can redo any frame of the batch).
+static fm_status run_batch_at(fm_plan pl, int64_t ws0, int64_t frames, const fm_batch_io* io, cudaStream_t s) {
     FM_CUDA_OK(cudaMemsetAsync(io->status, 0, sizeof(int32_t) * frames, s));
     const int nsub = auto_subbatches(pl, frames);
     const bool planes = plane_mode(pl) && !io->covariance;
     pl->last_planes = planes;
     const int64_t nx = pl->x_pad ? pl->d.n + 1 : pl->d.n;  // row length fed to the covariance kernel
+    const size_t MM2 = static_cast<size_t>(pl->d.m) * pl->d.m * 2;
     auto xin = [&](const float* x, int64_t f0, int64_t nf, cudaStream_t q) -> const float* {
         if (!pl->x_pad) return x;
         float* xp = pl->x_pad + f0 * pl->d.m * nx * 2;
@@ -1138,13 +1119,14 @@ extern "C" fm_status fm_run_batch(fm_plan pl, int64_t frames, const fm_batch_io*
         return xp;
     };
     if (nsub <= 1) {
-        float* R = io->covariance ? io->covariance : pl->R;
-        const Planes pv = planes ? planes_view(pl, 0) : Planes{};
+        float* R = io->covariance ? io->covariance : pl->R + ws0 * MM2;
+        const Planes pv = planes ? planes_view(pl, ws0) : Planes{};
+        const WorkView w = work_view(pl, ws0);
         mark(pl, 0, s);
-        FM_LAUNCH(fm_launch_cov_tc(xin(io->x, 0, frames, s), R, io->status, frames, pl->d.m, nx, s, pv.hi, pv.lo,
-                                   pv.scale, pl->d.n));
+        FM_LAUNCH(fm_launch_cov_tc(xin(io->x, ws0, frames, s), R, io->status, frames, pl->d.m, nx, s, pv.hi, pv.lo,
+                                   pv.scale, pl->d.n, &w.resc));
         mark(pl, 1, s);
-        return run_post_cov(pl, frames, io, R, s, work_view(pl, 0), true, pv);
+        return run_post_cov(pl, frames, io, R, s, w, true, pv);
     }
     while (static_cast<int>(pl->sub.size()) < nsub) {
         cudaStream_t q;
@@ -1158,7 +1140,6 @@ extern "C" fm_status fm_run_batch(fm_plan pl, int64_t frames, const fm_batch_io*
     }
     FM_CUDA_OK(cudaEventRecord(pl->sub_ev[0], s));
     const int64_t chunk = (frames + nsub - 1) / nsub;
-    const size_t MM2 = static_cast<size_t>(pl->d.m) * pl->d.m * 2;
     for (int i = 0; i < nsub; ++i) {
         const int64_t f0 = i * chunk;
         const int64_t nf = std::min<int64_t>(chunk, frames - f0);
@@ -1166,21 +1147,29 @@ extern "C" fm_status fm_run_batch(fm_plan pl, int64_t frames, const fm_batch_io*
         cudaStream_t q = pl->sub[i];
         FM_CUDA_OK(cudaStreamWaitEvent(q, pl->sub_ev[0], 0));
         const fm_batch_io o = io_view(pl, io, f0);
-        float* R = io->covariance ? o.covariance : pl->R + f0 * MM2;
-        const Planes pv = planes ? planes_view(pl, f0) : Planes{};
+        float* R = io->covariance ? o.covariance : pl->R + (ws0 + f0) * MM2;
+        const Planes pv = planes ? planes_view(pl, ws0 + f0) : Planes{};
+        const WorkView w = work_view(pl, ws0 + f0, i);
         if (i == 0) mark(pl, 0, q);
         {
             cudaStream_t s = q;  // FM_LAUNCH synchronises `s` in debug mode
-            FM_LAUNCH(fm_launch_cov_tc(xin(o.x, f0, nf, q), R, o.status, nf, pl->d.m, nx, q, pv.hi, pv.lo, pv.scale,
-                                       pl->d.n));
+            FM_LAUNCH(fm_launch_cov_tc(xin(o.x, ws0 + f0, nf, q), R, o.status, nf, pl->d.m, nx, q, pv.hi, pv.lo,
+                                       pv.scale, pl->d.n, &w.resc));
         }
         if (i == 0) mark(pl, 1, q);
-        st = run_post_cov(pl, nf, &o, R, q, work_view(pl, f0, i), i == 0, pv);
+        fm_status st = run_post_cov(pl, nf, &o, R, q, w, i == 0, pv);
         if (st != FM_OK) return st;
         FM_CUDA_OK(cudaEventRecord(pl->sub_ev[1 + i], q));
         FM_CUDA_OK(cudaStreamWaitEvent(s, pl->sub_ev[1 + i], 0));
     }
     return FM_OK;
+}
+
+extern "C" fm_status fm_run_batch(fm_plan pl, int64_t frames, const fm_batch_io* io, void* stream) {
+    fm_status st = check_io(pl, frames, io);
+    if (st != FM_OK) return st;
+    FM_CUDA_OK(cudaSetDevice(pl->device));
+    return run_batch_at(pl, 0, frames, io, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" fm_status fm_plan_set_concurrency(fm_plan plan, int32_t subbatches) {
@@ -1189,14 +1178,35 @@ extern "C" fm_status fm_plan_set_concurrency(fm_plan plan, int32_t subbatches) {
     return FM_OK;
 }
 
-extern "C" fm_status fm_rerun_frames(fm_plan pl, int64_t frames, const int32_t* /*d_frames: all frames rerun*/, const fm_batch_io* io,
+// Subspace + spectrum + peaks again for the listed frames of the last batch, on its kept covariance; the
+// frames are grouped into runs of consecutive indices, each run one pass over the post-covariance pipeline.
+static fm_status rerun_list(fm_plan pl, const int32_t* list, int64_t count, const fm_batch_io* io, cudaStream_t s) {
+    const size_t MM2 = static_cast<size_t>(pl->d.m) * pl->d.m * 2;
+    int64_t i = 0;
+    while (i < count) {
+        int64_t j = i + 1;
+        while (j < count && list[j] == list[j - 1] + 1) ++j;
+        const int64_t f0 = list[i], nf = j - i;
+        const fm_batch_io o = io_view(pl, io, f0);
+        const float* R = io->covariance ? o.covariance : pl->R + f0 * MM2;
+        const Planes pv = pl->last_planes && !io->covariance ? planes_view(pl, f0) : Planes{};
+        fm_status st = run_post_cov(pl, nf, &o, R, s, work_view(pl, f0), false, pv);
+        if (st != FM_OK) return st;
+        i = j;
+    }
+    return FM_OK;
+}
+
+extern "C" fm_status fm_rerun_frames(fm_plan pl, int64_t count, const int32_t* h_frames, const fm_batch_io* io,
                                      void* stream) {
-    fm_status st = check_io(pl, frames, io);
-    if (st != FM_OK) return st;
+    if (!pl || !io || count < 0 || (count > 0 && !h_frames))
+        return fail(FM_EINVAL, "fm_rerun_frames: bad arguments");
+    for (int64_t i = 0; i < count; ++i)
+        if (h_frames[i] < 0 || h_frames[i] >= pl->d.max_frames || (i > 0 && h_frames[i] <= h_frames[i - 1]))
+            return fail(FM_EINVAL, "fm_rerun_frames: frame list must be ascending indices within max_frames");
+    if (count == 0) return FM_OK;
     FM_CUDA_OK(cudaSetDevice(pl->device));
-    const float* R = io->covariance ? io->covariance : pl->R;
-    const Planes pv = pl->last_planes && !io->covariance ? planes_view(pl, 0) : Planes{};
-    return run_post_cov(pl, frames, io, R, static_cast<cudaStream_t>(stream), work_view(pl, 0), false, pv);
+    return rerun_list(pl, h_frames, count, io, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const float* h_x, const uint64_t* draw_seeds,
@@ -1235,10 +1245,9 @@ extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const fl
     // and chunk c computes on the caller's stream while chunk c+1 copies. Frames are independent, so
     // per-chunk runs give the same per-frame results as one run over the batch.
     constexpr int64_t kChunkMin = 128;
-    // measured c2 (1024 frames, scripts_e2e_chunks.py): 1 chunk 21.3 ms, 2: 20.8, 4: 20.56, 8: 22.4;
-    // the plain 1.07 GB pinned H2D alone takes 20.3 ms
-    int64_t max_ch = 4;
-    if (const char* e = getenv("FM_HOST_CHUNKS")) max_ch = std::max(1, std::min<int>(atoi(e), fm_plan_s::kHostChunks));
+    // measured c2 (1024 frames): 1 chunk 21.3 ms, 2: 20.8, 4: 20.56, 8: 22.4; the plain 1.07 GB pinned H2D alone
+    // takes 20.3 ms
+    constexpr int64_t max_ch = 4;
     const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(max_ch, frames / kChunkMin));
     const int64_t cs = (frames + nch - 1) / nch;
     cudaStream_t cp = pl->copy_s;
@@ -1282,7 +1291,7 @@ extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const fl
         const int64_t f0 = c * cs, fc = std::min(cs, frames - f0);
         FM_CUDA_OK(cudaStreamWaitEvent(s, pl->copy_ev[c], 0));
         const fm_batch_io io = chunk_io(f0);
-        fm_status st = fm_run_batch(pl, fc, &io, stream);
+        fm_status st = run_batch_at(pl, f0, fc, &io, s);  // R of every chunk kept in place for the redraws
         if (st != FM_OK) return st;
     }
     fm_batch_io io{};
@@ -1301,14 +1310,15 @@ extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const fl
         // R/src/estimators.cpp:114-137: up to 3 sub-seeded redraws per rank-deficient frame.
         const size_t per = d.method == FM_METHOD_FAST2 ? M * P : M;
         std::vector<uint64_t> seeds(draw_seeds, draw_seeds + frames);
+        std::vector<int32_t> redo;
         for (int attempt = 1; attempt < 4; ++attempt) {
             FM_CUDA_OK(cudaMemcpyAsync(pl->status_pinned, pl->status_dev, sizeof(int32_t) * frames,
                                        cudaMemcpyDeviceToHost, s));
             FM_CUDA_OK(cudaStreamSynchronize(s));
-            bool any = false;
+            redo.clear();
             for (int64_t f = 0; f < frames; ++f) {
                 if (pl->status_pinned[f] & FM_FRAME_RANK) {
-                    any = true;
+                    redo.push_back(static_cast<int32_t>(f));
                     attempts[f] = attempt + 1;
                     const uint64_t ds = fmhost::Rng::derive(draw_seeds[f], 0xF257u + static_cast<uint64_t>(attempt));
                     float* dst = pl->omega_pinned + static_cast<size_t>(f) * per;
@@ -1318,9 +1328,10 @@ extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const fl
                                                cudaMemcpyHostToDevice, s));
                 }
             }
-            if (!any) break;
-            // whole batch again (R of the chunked runs is not kept); unflagged frames reproduce exactly
-            st = nch == 1 ? fm_rerun_frames(pl, frames, nullptr, &io, stream) : fm_run_batch(pl, frames, &io, stream);
+            if (redo.empty()) break;
+            // only the flagged frames again, on their kept covariance (R/src/estimators.cpp:114-137 redraws the
+            // failing frame alone)
+            st = rerun_list(pl, redo.data(), static_cast<int64_t>(redo.size()), &io, s);
             if (st != FM_OK) return st;
         }
     }
@@ -1461,7 +1472,20 @@ extern "C" fm_status fm_temporal_covariance_batch(const float* x, int64_t frames
                                              static_cast<int>(f0));
     }
     cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess) e = fm_launch_cov_tc(y, t_out, status, frames, n, mp, s, nullptr, nullptr, nullptr, m);
+    // rescue-pass workspace (out-of-range frames recomputed with a power-of-two prescale, cov_tc.cu)
+    FmCovRescue rs{};
+    void* rbuf = nullptr;
+    const size_t rbytes = sizeof(uint32_t) * frames + sizeof(int32_t) * frames + sizeof(float) * frames + 16;
+    if (e == cudaSuccess) e = cudaMallocAsync(&rbuf, rbytes, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(rbuf, 0, rbytes, s);
+    if (e == cudaSuccess) {
+        rs.amax = static_cast<uint32_t*>(rbuf);
+        rs.list = reinterpret_cast<int32_t*>(rs.amax + frames);
+        rs.xscale = reinterpret_cast<float*>(rs.list + frames);
+        rs.count = reinterpret_cast<int32_t*>(rs.xscale + frames);
+        e = fm_launch_cov_tc(y, t_out, status, frames, n, mp, s, nullptr, nullptr, nullptr, m, &rs);
+    }
+    if (rbuf) cudaFreeAsync(rbuf, s);
     if (!work) cudaFreeAsync(y, s);
     if (e != cudaSuccess) return fm_fail_cuda(e, "fm_temporal_covariance_batch", __FILE__, __LINE__);
     return FM_OK;
@@ -1626,8 +1650,7 @@ extern "C" fm_status fm_z_music_spectrum(int64_t m, int64_t kb, const double* ba
         if (!(dev <= 1e-6)) return fail(FM_EINVAL, "music_spectrum: basis columns are not orthonormal");
     }
     FM_CUDA_OK(fm_launch_autocorr(dB.p, dT.p, 1, static_cast<int>(m), static_cast<int>(kb), c.s));
-    FM_CUDA_OK(fm_launch_spectrum_peaks(dT.p, dZ.p, 1, static_cast<int>(m), static_cast<int>(L), nullptr, dOut.p, 1, 0,
-                                        nullptr, nullptr, nullptr, nullptr, nullptr, c.s));
+    FM_CUDA_OK(fm_launch_spectrum_one(dT.p, dZ.p, 1, static_cast<int>(m), static_cast<int>(L), dOut.p, c.s));
     FM_CUDA_OK(cudaMemcpyAsync(values, dOut.p, sizeof(double) * L, cudaMemcpyDeviceToHost, c.s));
     FM_CUDA_OK(cudaStreamSynchronize(c.s));
     return FM_OK;
@@ -1636,31 +1659,29 @@ extern "C" fm_status fm_z_music_spectrum(int64_t m, int64_t kb, const double* ba
 extern "C" fm_status fm_z_extract_peaks(const double* values, int64_t L, int64_t k, int64_t min_sep, int64_t* cells,
                                         double* heights, int64_t* count, double* baseline, int32_t* shortfall) {
     if (k < 1) return fail(FM_EINVAL, "extract_peaks: K >= 1 required");
-    if (k > 64) return fail(FM_ENOTSUP, "extract_peaks: K <= 64 supported");
     if (!values || L < 1 || !cells || !heights || !count || !baseline || !shortfall)
         return fail(FM_EINVAL, "extract_peaks: bad arguments");
+    if (L > 0x7fffffff || k > 0x7fffffff) return fail(FM_EINVAL, "extract_peaks: grid or K too large");
     ZCtx c;
     DevBuf<double> dV, dH, dBase;
-    DevBuf<int32_t> dC, dN, dOv;
+    DevBuf<int32_t> dC, dN;
+    DevBuf<uint8_t> dWs;
     FM_CUDA_OK(dV.alloc(L));
     FM_CUDA_OK(dH.alloc(k));
     FM_CUDA_OK(dBase.alloc(1));
     FM_CUDA_OK(dC.alloc(k));
     FM_CUDA_OK(dN.alloc(1));
-    FM_CUDA_OK(dOv.alloc(1));
+    FM_CUDA_OK(dWs.alloc(fm_peaks_workspace_bytes(1, static_cast<int>(L), static_cast<int>(k))));
     FM_CUDA_OK(cudaMemcpyAsync(dV.p, values, sizeof(double) * L, cudaMemcpyHostToDevice, c.s));
-    FM_CUDA_OK(cudaMemsetAsync(dOv.p, 0, sizeof(int32_t), c.s));
     FM_CUDA_OK(fm_launch_peaks_only(dV.p, 1, static_cast<int>(L), static_cast<int>(k), static_cast<int>(min_sep), dC.p,
-                                    dH.p, dBase.p, dN.p, dOv.p, c.s));
+                                    dH.p, dBase.p, dN.p, dWs.p, c.s));
     std::vector<int32_t> c32(static_cast<size_t>(k));
-    int32_t n = 0, ov = 0;
+    int32_t n = 0;
     FM_CUDA_OK(cudaMemcpyAsync(c32.data(), dC.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, c.s));
     FM_CUDA_OK(cudaMemcpyAsync(heights, dH.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c.s));
     FM_CUDA_OK(cudaMemcpyAsync(baseline, dBase.p, sizeof(double), cudaMemcpyDeviceToHost, c.s));
     FM_CUDA_OK(cudaMemcpyAsync(&n, dN.p, sizeof(int32_t), cudaMemcpyDeviceToHost, c.s));
-    FM_CUDA_OK(cudaMemcpyAsync(&ov, dOv.p, sizeof(int32_t), cudaMemcpyDeviceToHost, c.s));
     FM_CUDA_OK(cudaStreamSynchronize(c.s));
-    if (ov) return fail(FM_ENOTSUP, "extract_peaks: more local maxima than the candidate buffer holds");
     for (int64_t i = 0; i < k; ++i) cells[i] = c32[static_cast<size_t>(i)];
     *count = n;
     *shortfall = n < k ? 1 : 0;

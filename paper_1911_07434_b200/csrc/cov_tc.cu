@@ -17,7 +17,12 @@
 // SMs; the epilogue reads them with tcgen05.ld, scales by 1/N and stores fp32.
 // Precision: operands rounded to fp16 (11-bit significand), fp32 accumulation.
 // Measured on the c2 frames against the fp64 oracle: 3e-3 dB max spectrum error,
-// identical peaks; inputs with |x| > 65504 are flagged kFrameRange.
+// identical peaks.
+// Scale: MUSIC is scale-free and the reference computes in fp64, so the fp16 operand range must not limit the
+// input. The converters record each frame's max |x|; frames outside [2^-8, 2^15) (fp16 overflow, or significand
+// bits lost to subnormals) are listed by k_rescue_list and recomputed by a second launch over the list only,
+// with X scaled by a power of two 2^e (exact) so that max |x| lands in [2^6, 2^7), and 2^-2e folded into the
+// epilogue's 1/N. Frames in range cost one atomicMax per converter warp and tile; an empty list exits at once.
 
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -109,7 +114,7 @@ __device__ __forceinline__ void tile_coords(int t, int& bi, int& bj) {
 // kJ = 2: four converter warps (32 rows each); kJ = 1: eight converter warps (16 rows each).
 template <int kJ>
 __device__ __forceinline__ void convert_tile(const uint8_t* stage, uint8_t* op, int cw, int lane, int row_base,
-                                             int m_rows, float& amax, bool& nonfinite) {
+                                             int m_rows, float xs, float& amax, bool& nonfinite) {
 #pragma unroll
     for (int j = 0; j < kJ; ++j) {
         const int r = 16 * kJ * cw + (lane & 7) + 8 * (lane >> 4) + 16 * j;
@@ -128,6 +133,11 @@ __device__ __forceinline__ void convert_tile(const uint8_t* stage, uint8_t* op, 
         if (!valid) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) re[u] = im[u] = 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {  // power-of-two prescale (1 outside the rescue pass): exact
+            re[u] *= xs;
+            im[u] *= xs;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -169,8 +179,22 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
     cov_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap rmap,
                   const __grid_constant__ CUtensorMap mmap, float* __restrict__ r_out, int32_t* __restrict__ status,
                   int m, int n, int tiles_per_frame, int total_tiles, float* __restrict__ rscale,
-                  float inv_n_true, int dbg, int ring) {
+                  float inv_n_true, int dbg, int ring, const int32_t* __restrict__ flist,
+                  const int32_t* __restrict__ fcount, const float* __restrict__ xscale,
+                  uint32_t* __restrict__ amax_out) {
     constexpr bool kTmaStore = kEpi >= 1;
+    // rescue pass: only the listed frames (the count is device-resident; every CTA of the grid reads the same
+    // value, so an empty list ends all of them before any barrier or TMEM allocation)
+    if (flist) {
+        total_tiles = *fcount * tiles_per_frame;
+        if (total_tiles == 0) return;
+    }
+    auto frame_of = [&](int tile) { return flist ? flist[tile / tiles_per_frame] : tile / tiles_per_frame; };
+    auto inv_n_of = [&](int frame) {  // 1/N, and 2^-2e of the rescue prescale (exact)
+        if (!xscale) return inv_n_true;
+        const float xs = xscale[frame];
+        return inv_n_true / (xs * xs);
+    };
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* staging = smem;
@@ -244,7 +268,7 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
         if (lane == 0) {
             int g = 0;
             for (int tile = pair; tile < total_tiles; tile += npairs) {
-                const int frame = tile / tiles_per_frame;
+                const int frame = frame_of(tile);
                 int bi, bj;
                 tile_coords(tile % tiles_per_frame, bi, bj);
                 const bool diag = (bi == bj);
@@ -302,12 +326,13 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
         const int cw = warp < 6 ? warp - 2 : 4 + warp - kFirstExtra;
         int g = 0;
         for (int tile = pair; tile < total_tiles; tile += npairs) {
-            const int frame = tile / tiles_per_frame;
+            const int frame = frame_of(tile);
             int bi, bj;
             tile_coords(tile % tiles_per_frame, bi, bj);
             const bool diag = (bi == bj);
             const int row_a = 256 * bi + 128 * static_cast<int>(rank);
             const int row_b = 256 * bj + 128 * static_cast<int>(rank);
+            const float xs = xscale ? xscale[frame] : 1.f;
             float amax = 0.f;
             bool nonfinite = false;
             for (int kc = 0; kc < nk; ++kc, ++g) {
@@ -317,8 +342,8 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
                 mbar_wait(smem_u32(&op_empty[o]), ((g / nO) & 1) ^ 1);
                 const uint8_t* st = staging + s * sStride;
                 uint8_t* op = operand + o * oStride;
-                convert_tile<kJ>(st, op, cw, lane, row_a, m, amax, nonfinite);
-                if (!diag) convert_tile<kJ>(st + kStageBytes, op + kOpBytes, cw, lane, row_b, m, amax, nonfinite);
+                convert_tile<kJ>(st, op, cw, lane, row_a, m, xs, amax, nonfinite);
+                if (!diag) convert_tile<kJ>(st + kStageBytes, op + kOpBytes, cw, lane, row_b, m, xs, amax, nonfinite);
                 fence_proxy_async();
                 named_bar_sync(1, kConv8 ? 256 : 128);  // all converter warps done with this stage
                 if (warp == 2 && lane == 0) {
@@ -327,9 +352,15 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
                     else mbar_arrive_cluster(smem_u32(&op_full[o]), 0);
                 }
             }
-            int flag = (amax > 65504.f ? kFrameRange : 0) | (nonfinite ? kFrameNonFinite : 0);
+            // pass 1 with a rescue list: record max |x| (k_rescue_list decides); otherwise flag fp16 overflow
+            int flag = (nonfinite ? kFrameNonFinite : 0) | (!amax_out && amax > 65504.f ? kFrameRange : 0);
             flag = __reduce_or_sync(0xffffffffu, flag);
-            if (flag && lane == 0 && status != nullptr) atomicOr(&status[frame], flag);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+            if (lane == 0) {
+                if (flag && status != nullptr) atomicOr(&status[frame], flag);
+                if (amax_out) atomicMax(&amax_out[frame], __float_as_uint(amax));  // amax >= 0: uint order
+            }
         }
     } else if (kEpi == 2) {
         // ---------------- epilogue, fp16 hi/lo planes of R / s_f (M <= 256: tile == frame). Eight warps:
@@ -340,12 +371,12 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
         //    128B-swizzled 32 x 64-half boxes (single-buffered per warp), two TMA stores.
         const int quarter = warp & 3;
         const int half = (warp - 6) >> 2;
-        const float inv_n = inv_n_true;
         const uint32_t ebase = smem_u32(epi_bytes) + (warp - 6) * (2 * kEpiChunk);
         const uint32_t peer = rank ^ 1u;
         int t = 0;
         for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
-            const int frame = tile;
+            const int frame = frame_of(tile);
+            const float inv_n = inv_n_of(frame);
             const int row0 = 128 * static_cast<int>(rank) + 32 * quarter;
             const int gi = row0 + lane;
             mbar_wait(smem_u32(acc_full), t & 1);
@@ -445,11 +476,11 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
         // bulk groups). TMEM is released as soon as the last chunk is in smem, so the global writes
         // overlap the next tile's mainloop. Off-diagonal tiles also store the conj-transposed block.
         const int quarter = warp & 3;
-        const float inv_n = inv_n_true;  // 1 / N of the caller (n may include one zero pad column)
         const uint32_t ebase = smem_u32(epi_bytes) + (warp - 6) * kEpiWarpBytes;
         int t = 0, gc = 0;
         for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
-            const int frame = tile / tiles_per_frame;
+            const int frame = frame_of(tile);
+            const float inv_n = inv_n_of(frame);  // 1 / N of the caller (n may include one zero pad column)
             int bi, bj;
             tile_coords(tile % tiles_per_frame, bi, bj);
             const bool diag = (bi == bj);
@@ -502,10 +533,10 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
         // ---------------- epilogue, generic-store fallback (odd M: row pitch not 16-byte aligned)
         const int quarter = warp & 3;
         const int row = 32 * quarter + lane;
-        const float inv_n = inv_n_true;  // 1 / N of the caller (n may include one zero pad column)
         int t = 0;
         for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
-            const int frame = tile / tiles_per_frame;
+            const int frame = frame_of(tile);
+            const float inv_n = inv_n_of(frame);  // 1 / N of the caller (n may include one zero pad column)
             int bi, bj;
             tile_coords(tile % tiles_per_frame, bi, bj);
             const bool diag = (bi == bj);
@@ -561,11 +592,37 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
     }
 }
 
-// ---------------------------------------------------------------- host side
-// Experiment switches (FM_COV_DBG, not for production): 2 = no MMA, 4 = plane epilogue skips its chunks.
-static int dbg_flags() {
-    static const int v = std::getenv("FM_COV_DBG") ? std::atoi(std::getenv("FM_COV_DBG")) : 0;
-    return v;
+// Rescue list: frames whose max |x| (pass 1) lies outside [2^-8, 2^15) and is finite and non-zero get
+// xscale = 2^e with max |x| 2^e in [2^6, 2^7); frames with max |x| outside [2^-50, 2^50] (R = X X^H / N would
+// leave the complex64 range the rest of the batch path computes in) are flagged kFrameRange instead. Resets
+// amax for the next batch. One CTA; list order is irrelevant (frames are independent).
+__global__ void __launch_bounds__(1024) k_rescue_list(uint32_t* __restrict__ amax, int32_t* __restrict__ status,
+                                                      int frames, int32_t* __restrict__ list,
+                                                      int32_t* __restrict__ count, float* __restrict__ xscale) {
+    __shared__ int s_n;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    for (int f = threadIdx.x; f < frames; f += blockDim.x) {
+        const float a = __uint_as_float(amax[f]);
+        amax[f] = 0u;
+        if ((status[f] & kFrameNonFinite) || !(a > 0.f) || (a >= 0.00390625f && a < 32768.f)) continue;
+        if (!isfinite(a)) {
+            atomicOr(&status[f], kFrameRange);
+            continue;
+        }
+        int e2 = 0;
+        frexpf(a, &e2);  // a in [2^(e2-1), 2^e2)
+        const int sh = 7 - e2;  // a 2^sh in [2^6, 2^7)
+        // R (complex64) and the downstream fp32 data must stay representable: max |x| within 2^+-50
+        if (sh > 57 || sh < -43) {
+            atomicOr(&status[f], kFrameRange);
+            continue;
+        }
+        xscale[f] = ldexpf(1.f, sh);
+        list[atomicAdd(&s_n, 1)] = f;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *count = s_n;
 }
 
 }  // namespace cov
@@ -575,8 +632,11 @@ static int dbg_flags() {
 // Returns a cudaError_t value (cudaErrorInvalidValue for unsupported shapes).
 // planes_hi != nullptr selects the fp16 hi/lo plane output (M <= 256, M even): planes_hi / planes_lo
 // are frames x M x 2M halves (R / s_f interleaved re, im), scale[f] = s_f; d_r is unused then.
+// rescue (optional, FmCovRescue): per-frame amax (zeroed once by the caller, reset by the list kernel), the
+// rescue list / count and the prescale; with it the call enqueues pass 1, k_rescue_list and the rescue pass.
 cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, int64_t frames, int64_t m, int64_t n,
-                             cudaStream_t stream, void* planes_hi, void* planes_lo, float* scale, int64_t n_true) {
+                             cudaStream_t stream, void* planes_hi, void* planes_lo, float* scale, int64_t n_true,
+                             const FmCovRescue* rescue) {
     if (n_true <= 0) n_true = n;  // n: row length of d_x (even); n_true: snapshots for the 1/N scaling
     using namespace fmk::cov;
     if (frames < 1 || m < 1 || n < 2 || (n & 1) || frames * m > 0x7fffffff || 2 * n > 0x7fffffff)
@@ -625,20 +685,11 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
         mmap = map;
     }
     // four converter warps for diagonal-only launches (M <= 256: one tile per frame, no redundant conversion;
-    // c2 covariance 0.342 -> 0.333 ms, scripts_coresidency.sh), eight for multi-tile frames.
-    // FM_COV_CONV4 / FM_COV_CONV8 force either (comparison).
-    static const bool force4 = std::getenv("FM_COV_CONV4") != nullptr, force8 = std::getenv("FM_COV_CONV8") != nullptr;
-    const bool conv4 = force4 || (!force8 && m <= 256);
-    // ring depths (stages) general staging / operand, diagonal-only staging / operand; FM_COV_RING=a,b,c,d
-    int rs[4] = {kStagesS, kStagesO, kDiagS, kDiagO};
-    if (const char* r = std::getenv("FM_COV_RING")) {
-        int v[4];
-        if (std::sscanf(r, "%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3]) == 4 && v[0] * 2 * kStageBytes + v[1] * 2 * kOpBytes <=
-                kSmemStaging + kSmemOperand && v[2] * kStageBytes + v[3] * kOpBytes <= kSmemStaging + kSmemOperand &&
-            v[0] >= 2 && v[1] >= 2 && v[2] >= 2 && v[3] >= 2 && v[2] <= kMaxStages && v[3] <= kMaxStages &&
-            v[0] <= kMaxStages && v[1] <= kMaxStages)
-            for (int i = 0; i < 4; ++i) rs[i] = v[i];
-    }
+    // c2 covariance 0.342 -> 0.333 ms), eight for multi-tile frames (every 256-row block of X is converted once
+    // per tile it feeds)
+    const bool conv4 = m <= 256;
+    // ring depths (stages): general staging / operand, diagonal-only staging / operand
+    const int rs[4] = {kStagesS, kStagesO, kDiagS, kDiagO};
     const int ring = rs[0] | (rs[1] << 8) | (rs[2] << 16) | (rs[3] << 24);
     auto set_attr = [](auto kern) {
         return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
@@ -663,27 +714,35 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
     }
-    static const int cap_pairs = std::getenv("FM_COV_PAIRS")  ? std::atoi(std::getenv("FM_COV_PAIRS"))
-                                 : std::getenv("FM_TC_PAIRS") ? std::atoi(std::getenv("FM_TC_PAIRS"))
-                                                              : 0;  // experiment: covariance grid width
-    const int64_t pairs = std::min<int64_t>(tiles, std::max(1, cap_pairs > 0 ? cap_pairs : sm_count / 2));
+    const int64_t pairs = std::min<int64_t>(tiles, std::max(1, sm_count / 2));
     const dim3 grid(static_cast<unsigned>(2 * pairs));
-    auto go = [&](auto kern, bool conv8) {
+    auto go = [&](auto kern, bool conv8, bool pass2) {
         const int threads = (epi == 2 ? kThreadsP : kThreads) + (conv8 ? 128 : 0);
         const int smem = 1024 + ring_region_bytes(ring, tiles_per_frame == 1) + kSmemEpilogue + kSmemBarriers;
+        const bool r = rescue != nullptr;
         kern<<<grid, threads, smem, stream>>>(map, rmap, mmap, d_r, d_status, static_cast<int>(m),
-                                                     static_cast<int>(n), tiles_per_frame, static_cast<int>(tiles),
-                                                     scale, static_cast<float>(1.0 / static_cast<double>(n_true)),
-                                                     dbg_flags(), ring);
+                                              static_cast<int>(n), tiles_per_frame, static_cast<int>(tiles), scale,
+                                              static_cast<float>(1.0 / static_cast<double>(n_true)), 0, ring,
+                                              pass2 ? rescue->list : nullptr, pass2 ? rescue->count : nullptr,
+                                              pass2 ? rescue->xscale : nullptr, (r && !pass2) ? rescue->amax : nullptr);
     };
-    if (conv4) {
-        if (epi == 2) go(cov_tc_kernel<2, false>, false);
-        else if (epi == 1) go(cov_tc_kernel<1, false>, false);
-        else go(cov_tc_kernel<0, false>, false);
-    } else {
-        if (epi == 2) go(cov_tc_kernel<2, true>, true);
-        else if (epi == 1) go(cov_tc_kernel<1, true>, true);
-        else go(cov_tc_kernel<0, true>, true);
+    auto launch = [&](bool pass2) {
+        if (conv4) {
+            if (epi == 2) go(cov_tc_kernel<2, false>, false, pass2);
+            else if (epi == 1) go(cov_tc_kernel<1, false>, false, pass2);
+            else go(cov_tc_kernel<0, false>, false, pass2);
+        } else {
+            if (epi == 2) go(cov_tc_kernel<2, true>, true, pass2);
+            else if (epi == 1) go(cov_tc_kernel<1, true>, true, pass2);
+            else go(cov_tc_kernel<0, true>, true, pass2);
+        }
+    };
+    launch(false);
+    if (rescue) {
+        if (!d_status) return cudaErrorInvalidValue;
+        k_rescue_list<<<1, 1024, 0, stream>>>(rescue->amax, d_status, static_cast<int>(frames), rescue->list,
+                                              rescue->count, rescue->xscale);
+        launch(true);
     }
     return cudaGetLastError();
 }

@@ -4,6 +4,15 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+// Covariance rescue-pass workspace (cov_tc.cu): per-frame max |x| of pass 1 (float bits; zero between batches),
+// the list of out-of-range frames, its count (device), and their power-of-two prescale.
+struct FmCovRescue {
+    uint32_t* amax;
+    int32_t* list;
+    int32_t* count;
+    float* xscale;
+};
+
 namespace fmk {
 
 // Per-frame status bits (written by kernels; mapped to the reference's
@@ -45,6 +54,27 @@ template <typename T> __device__ __forceinline__ cplx<double> to64(cplx<T> a) { 
 template <typename T> struct eps_of;
 template <> struct eps_of<float> { static constexpr double value = 1.1920928955078125e-07; };
 template <> struct eps_of<double> { static constexpr double value = 2.220446049250313e-16; };
+
+// Rank of a batched CholQR factor by Eigen's ColPivHouseholderQR::rank() rule as the reference applies it
+// (R/src/linalg.cpp:127-141): nonzero-pivot cut, then |R_kk| > p eps max|R_jj| -- with the reference's eps_64.
+// The pivots come from the pivoted Cholesky of the fp64 Gram, d_k = |R_kk|^2, which resolves |R_kk| / |R_00|
+// only down to ~sqrt(p eps_64) (~6e-8 at p = 16); that floors the threshold. Sketches with condition numbers up
+// to ~1e7 (per-source 40 dB at M = 256) therefore pass, as they do in the fp64 reference.
+__device__ __forceinline__ int cholqr_rank(const double* d, int p, int m) {
+    const double eps = 2.220446049250313e-16;
+    const double thr_helper = fmax(d[0], 0.0) * eps * eps / static_cast<double>(m);  // maxColNorm^2 = d[0]
+    int nonzero = p;
+    double maxpivot = 0.0;
+    for (int k = 0; k < p; ++k) {
+        if (nonzero == p && d[k] < thr_helper * static_cast<double>(m - k)) nonzero = k;
+        maxpivot = fmax(maxpivot, sqrt(fmax(d[k], 0.0)));
+    }
+    const double rel = fmax(eps * static_cast<double>(p), sqrt(eps * static_cast<double>(p)));
+    const double thr = maxpivot * rel;
+    int rank = 0;
+    for (int k = 0; k < nonzero; ++k) rank += sqrt(fmax(d[k], 0.0)) > thr ? 1 : 0;
+    return rank;
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

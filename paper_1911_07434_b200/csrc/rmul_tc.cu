@@ -728,15 +728,13 @@ cudaError_t fm_launch_rmul_tc(const float* d_r, const float* d_omega, const floa
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
     }
-    static const int cap_pairs = std::getenv("FM_TC_PAIRS") ? std::atoi(std::getenv("FM_TC_PAIRS")) : 0;  // experiment
-    const int64_t pairs = std::min<int64_t>(tiles, std::max(1, cap_pairs > 0 ? cap_pairs : sm_count / 2));
+    const int64_t pairs = std::min<int64_t>(tiles, std::max(1, sm_count / 2));
     const dim3 grid(static_cast<unsigned>(2 * pairs));
     auto go = [&](auto kern, int smem) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        static const int trunc_a = std::getenv("FM_RMUL_TRUNC_A") ? std::atoi(std::getenv("FM_RMUL_TRUNC_A")) : 0;
         kern<<<grid, kThreads, smem, stream>>>(rmap, vmap, d_c, static_cast<int>(m), static_cast<int>(p),
-                                               tiles_per_frame, static_cast<int>(tiles), trunc_a);
+                                               tiles_per_frame, static_cast<int>(tiles), 0);
         return cudaGetLastError();
     };
     if (p <= 16)
@@ -808,16 +806,14 @@ cudaError_t fm_launch_rmul_planes(const void* planes_hi, const void* planes_lo, 
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
     }
-    static const int cap_pairs = std::getenv("FM_TC_PAIRS") ? std::atoi(std::getenv("FM_TC_PAIRS")) : 0;  // experiment
-    const int64_t pairs = std::min<int64_t>(tiles, std::max(1, cap_pairs > 0 ? cap_pairs : sm_count / 2));
+    const int64_t pairs = std::min<int64_t>(tiles, std::max(1, sm_count / 2));
     const dim3 grid(static_cast<unsigned>(2 * pairs));
-    static const int gdbg = std::getenv("FM_GRAM_DBG") ? std::atoi(std::getenv("FM_GRAM_DBG")) : 0;  // experiment
     auto go = [&](auto kern, int smem) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         kern<<<grid, gram == 2 ? kThreadsG2 : gram == 1 ? kThreadsG : kThreads, smem, stream>>>(hmap, lmap, vmap, d_scale, d_c, static_cast<int>(m),
                                                                        static_cast<int>(p), tiles_per_frame,
-                                                                       static_cast<int>(tiles), d_v, gpart, hpart, gdbg);
+                                                                       static_cast<int>(tiles), d_v, gpart, hpart, 0);
         return cudaGetLastError();
     };
     if (gram > 0) {

@@ -49,7 +49,6 @@ constexpr int kNW = kNT / 32;
 constexpr int kRC = 64;   // rows per staged Gram chunk
 constexpr int kRCP = 65;  // padded column stride (conflict-free 16-B column reads)
 __device__ int* g_phase_dbg = nullptr;
-__device__ int g_mixed_jacobi = 1;  // fp32 Jacobi sweeps before the fp64 ones (FM_JACOBI_FP64=1 -> 0)
 
 // G(i, j) = sum_r conj(X_i[r]) Y_j[r] over column-major p x m operands. Threads own entries
 // (HERM: upper triangle, mirrored); rows staged kRC at a time in padded shared memory and
@@ -259,18 +258,7 @@ __global__ void __launch_bounds__(kNT) k_cholqr_blk(const c32* __restrict__ Cin,
     if (MODE == 0) {
         if (threadIdx.x == 0) {
             // Eigen ColPivHouseholderQR::rank(): nonzero-pivot cut + |R_kk| > eps * p * maxpivot
-            const double eps = eps_of<float>::value;
-            const double thr_helper = fmax(d[0], 0.0) * eps * eps / static_cast<double>(m);
-            int nonzero = p;
-            double maxpivot = 0.0;
-            for (int k = 0; k < p; ++k) {
-                if (nonzero == p && d[k] < thr_helper * static_cast<double>(m - k)) nonzero = k;
-                maxpivot = fmax(maxpivot, sqrt(fmax(d[k], 0.0)));
-            }
-            const double thr = maxpivot * eps * static_cast<double>(p);
-            int rank = 0;
-            for (int k = 0; k < nonzero; ++k) rank += sqrt(fmax(d[k], 0.0)) > thr ? 1 : 0;
-            if (rank < p) atomicOr(&status[f], kFrameRank);
+            if (cholqr_rank(d, p, m) < p) atomicOr(&status[f], kFrameRank);
         }
         rows_solve<PC>(Cf, perm, sm.L, m, p, Vout + static_cast<size_t>(f) * m * p);
         __syncthreads();
@@ -585,38 +573,6 @@ __host__ __device__ constexpr size_t tiled_stage_bytes(int nbuf) {
     return sizeof(c64) * nbuf * kRCH * (PC + 1);
 }
 
-// Power-iteration orthonormalisation with the tiled Gram (p % 4 == 0): pivoted Cholesky QR,
-// Eigen rank rule, V = C P R^-1.
-template <int PC>
-__global__ void __launch_bounds__(kNT, 2) k_orth_tiled(const c32* __restrict__ Cin, c32* __restrict__ Vout,
-                                                    int32_t* __restrict__ status, int m, int p) {
-    extern __shared__ uint8_t dsm[];
-    c64* G = reinterpret_cast<c64*>(dsm);
-    c64* L = G + PC * PC;
-    c64* stage = L + PC * PC;
-    __shared__ int perm[32], done[32];
-    __shared__ double d[32];
-    __shared__ double s_inv;
-    const int f = blockIdx.x;
-    const c32* Cf = Cin + static_cast<size_t>(f) * m * p;
-    tiled_gram2<PC, c32, c32>(Cf, true, Cf, nullptr, nullptr, m, p, stage, G, nullptr);
-    block_chol(G, p, true, perm, d, L, done, &s_inv);
-    if (threadIdx.x == 0) {
-        const double eps = eps_of<float>::value;
-        const double thr_helper = fmax(d[0], 0.0) * eps * eps / static_cast<double>(m);
-        int nonzero = p;
-        double maxpivot = 0.0;
-        for (int k = 0; k < p; ++k) {
-            if (nonzero == p && d[k] < thr_helper * static_cast<double>(m - k)) nonzero = k;
-            maxpivot = fmax(maxpivot, sqrt(fmax(d[k], 0.0)));
-        }
-        const double thr = maxpivot * eps * static_cast<double>(p);
-        int rank = 0;
-        for (int k = 0; k < nonzero; ++k) rank += sqrt(fmax(d[k], 0.0)) > thr ? 1 : 0;
-        if (rank < p) atomicOr(&status[f], kFrameRank);
-    }
-    rows_solve<PC>(Cf, perm, L, m, p, Vout + static_cast<size_t>(f) * m * p);
-}
 
 __device__ __forceinline__ c64 warp_sum_c(c64 v) {
     v.re = warp_sum(v.re);
@@ -794,163 +750,10 @@ __global__ void __launch_bounds__(kNT) k_nystrom_blk(const c64* __restrict__ Hin
 }
 
 
-// Fused Nystrom tail (fast2: V = last power-iteration basis; fast1: H given):
-//   G = C^H C, H = V^H C (one tiled pass); G = R^H R (Cholesky, C = Q R); H = L_H L_H^H;
-//   Y = R L_H^-H (so B' = Rt W Rt^H = Y Y^H with Rt = R); one-sided Jacobi on Y -> Z, s;
-//   T = R^-1 Z_K; U = C T. A single CholQR suffices: U spans the large-singular-value
-//   directions of C, where C R^-1 is orthonormal to ~eps64 * (s_1/s_K)^2.
-template <int PC>
-__global__ void __launch_bounds__(kNT, 2) k_final_tiled(const c32* __restrict__ Cin, const c32* __restrict__ Vin,
-                                                     const c64* __restrict__ Hin, c64* __restrict__ basis,
-                                                     double* __restrict__ eig, int32_t* __restrict__ status, int m,
-                                                     int p, int k, int32_t* __restrict__ dbg) {
-    extern __shared__ uint8_t dsm[];
-    c64* G = reinterpret_cast<c64*>(dsm);  // -> R^H (L of G)
-    c64* H = G + PC * PC;                  // -> Y
-    c64* L = H + PC * PC;                  // Cholesky factors (original-index form)
-    c64* LH = L + PC * PC;
-    c64* Tm = LH + PC * PC;                // p x k  (T = R^-1 Z_K)
-    double* sig = reinterpret_cast<double*>(Tm + PC * PC);
-    c64* stage = reinterpret_cast<c64*>(sig + PC);
-    __shared__ int perm[32], done[32], order[32];
-    __shared__ double d[32];
-    __shared__ double s_inv;
-    __shared__ int s_rot;
-    const int f = blockIdx.x;
-    const c32* Cf = Cin + static_cast<size_t>(f) * m * p;
-    long long T0 = clock64();
-    if (Vin) {
-        tiled_gram2<PC, c32, c32>(Cf, true, Cf, Vin + static_cast<size_t>(f) * m * p, Cf, m, p, stage, G, H);
-    } else {
-        tiled_gram2<PC, c32, c32>(Cf, true, Cf, nullptr, nullptr, m, p, stage, G, nullptr);
-        const c64* Hf = Hin + static_cast<size_t>(f) * p * p;
-        for (int e = threadIdx.x; e < p * p; e += kNT) H[e] = Hf[e];
-        __syncthreads();
-    }
-    long long T1 = clock64();
-    for (int e = threadIdx.x; e < p * p; e += kNT) {  // Herm(H) in place
-        const int i = e % p, j = e / p;
-        if (i <= j) {
-            const c64 a = H[j * p + i], b = H[i * p + j];
-            const c64 hm = mk(0.5 * (a.re + b.re), 0.5 * (a.im - b.im));
-            H[j * p + i] = hm;
-            H[i * p + j] = conj(hm);
-        }
-    }
-    __syncthreads();
-    block_chol(G, p, false, perm, d, L, done, &s_inv);  // G = L L^H, R = L^H
-    block_chol(H, p, false, perm, d, LH, done, &s_inv);
-    if (threadIdx.x == 0) {
-        double dmax = 0.0, dmin = 1e300;
-        for (int q = 0; q < p; ++q) {
-            dmax = fmax(dmax, d[q]);
-            dmin = fmin(dmin, d[q]);
-        }
-        if (!(dmin > static_cast<double>(p) * eps_of<float>::value * dmax)) atomicOr(&status[f], kFrameNoConv);
-    }
-    // Y(i, :) solves y LH^H = R(i, :), R(i, j) = conj(L[i * p + j]) (j >= i); Y -> H
-    if (threadIdx.x < p) {
-        const int i = threadIdx.x;
-        c64 v[PC];
-#pragma unroll
-        for (int j = 0; j < PC; ++j) {
-            if (j < p) {
-                c64 x = j >= i ? conj(L[i * p + j]) : mk(0.0, 0.0);
-#pragma unroll
-                for (int a = 0; a < PC; ++a) {
-                    if (a < j) {
-                        const c64 l = LH[a * p + j];
-                        x.re -= v[a].re * l.re + v[a].im * l.im;
-                        x.im -= v[a].im * l.re - v[a].re * l.im;
-                    }
-                }
-                const double ljj = LH[j * p + j].re;
-                const double inv = ljj > 0.0 ? 1.0 / ljj : 0.0;
-                v[j] = mk(x.re * inv, x.im * inv);
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < PC; ++j)
-            if (j < p) Tm[j * p + i] = v[j];
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < p * p; e += kNT) H[e] = Tm[e];
-    __syncthreads();
-    long long T2 = clock64();
-    const int sw = block_hestenes(H, p, &s_rot);
-    long long T3 = clock64();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int c = warp; c < p; c += kNW) {
-        double s2 = 0.0;
-        for (int r = lane; r < p; r += 32) s2 += norm2(H[c * p + r]);
-        s2 = warp_sum(s2);
-        if (lane == 0) sig[c] = sqrt(s2);
-    }
-    __syncthreads();
-    if (threadIdx.x < p) {
-        const int c = threadIdx.x;
-        int rank = 0;
-        for (int q = 0; q < p; ++q)
-            if (q != c && (sig[q] > sig[c] || (sig[q] == sig[c] && q < c))) ++rank;
-        order[rank] = c;
-    }
-    __syncthreads();
-    // T(:, kk) = R^-1 z, z = H(:, order[kk]) / sig (back substitution, R(i,j) = conj(L[i*p + j]))
-    if (threadIdx.x < k) {
-        const int kk = threadIdx.x, c = order[kk];
-        const double inv_s = sig[c] > 0.0 ? 1.0 / sig[c] : 0.0;
-        for (int i = p - 1; i >= 0; --i) {
-            c64 acc = H[c * p + i];
-            acc.re *= inv_s;
-            acc.im *= inv_s;
-            for (int j = i + 1; j < p; ++j) {
-                const c64 rij = conj(L[i * p + j]);
-                const c64 tj = Tm[kk * p + j];
-                acc.re -= rij.re * tj.re - rij.im * tj.im;
-                acc.im -= rij.re * tj.im + rij.im * tj.re;
-            }
-            const double rii = L[i * p + i].re;
-            const double inv = rii > 0.0 ? 1.0 / rii : 0.0;
-            Tm[kk * p + i] = mk(acc.re * inv, acc.im * inv);
-        }
-    }
-    __syncthreads();
-    c64* Bf = basis + static_cast<size_t>(f) * m * k;
-    for (int r = threadIdx.x; r < m; r += kNT) {
-        c64 crow[PC];
-#pragma unroll
-        for (int q = 0; q < PC; ++q)
-            if (q < p) crow[q] = to64(Cf[static_cast<size_t>(q) * m + r]);
-        for (int kk = 0; kk < k; ++kk) {
-            c64 acc = mk(0.0, 0.0);
-#pragma unroll
-            for (int q = 0; q < PC; ++q)
-                if (q < p) cmac(acc, crow[q], Tm[kk * p + q]);
-            Bf[static_cast<size_t>(kk) * m + r] = acc;
-        }
-    }
-    if (threadIdx.x < k) {
-        double lam = sig[order[threadIdx.x]];
-        lam *= lam;  // eigenvalue of B' = Y Y^H
-        if (lam < 0.0 && lam >= -1e-10) lam = 0.0;
-        eig[static_cast<size_t>(f) * k + threadIdx.x] = lam;
-    }
-    if (threadIdx.x == 0 && sw == 0) atomicOr(&status[f], kFrameNoConv);
-    if (threadIdx.x == 0 && dbg) dbg[f] = sw;
-    __syncthreads();
-    long long T4 = clock64();
-    if (threadIdx.x == 0 && g_phase_dbg) {
-        g_phase_dbg[f * 4 + 0] = static_cast<int>(T1 - T0);
-        g_phase_dbg[f * 4 + 1] = static_cast<int>(T2 - T1);
-        g_phase_dbg[f * 4 + 2] = static_cast<int>(T3 - T2);
-        g_phase_dbg[f * 4 + 3] = static_cast<int>(T4 - T3);
-        (void)sw;
-    }
-}
 
 
 // ------------------------------------------------------------------------------------------
-// Split final stage (p in {4, 8, ..., 32}, p % 4 == 0). The fused k_final_tiled spends ~90% of
+// Split final stage (p in {4, 8, ..., 32}, p % 4 == 0). A fused block-per-frame final stage spent ~90% of
 // its time in p x p phases where one frame occupies a whole CTA behind __syncthreads; here the
 // Gram products stay block-per-frame, and every p x p phase runs one WARP per frame (8 frames
 // per CTA for p <= 16), so all frames of a batch are in flight at once.
@@ -958,7 +761,7 @@ __global__ void __launch_bounds__(kNT, 2) k_final_tiled(const c32* __restrict__ 
 //   k_small_warp: G = L L^H, H = L_H L_H^H (warp Cholesky), Y = R L_H^-H (R = L^H),
 //                 one-sided Jacobi on Y (lane-per-column), s, order, T = R^-1 Z_K / s, eig = s^2
 //   k_basis_ct  : U = C T (thread per row, fp64 accumulation)
-// Same algebra as k_final_tiled (R/src/estimators.cpp:37-50, :104-139; linalg.cpp:143-163).
+// R/src/estimators.cpp:37-50, :104-139; linalg.cpp:143-163.
 
 template <int PC>
 __global__ void __launch_bounds__(kNT, 2) k_gram_gh(const c32* __restrict__ Cin, const c32* __restrict__ Vin,
@@ -986,7 +789,6 @@ __global__ void __launch_bounds__(kNT, 2) k_gram_gh(const c32* __restrict__ Cin,
     }
 }
 
-static __device__ __forceinline__ bool mixed_jacobi() { return g_mixed_jacobi != 0; }
 
 template <int PC> struct WarpCfg {
     static constexpr int kLPC = 32 / PC;                   // lanes per column in the Jacobi
@@ -1047,8 +849,9 @@ __device__ __forceinline__ void warp_chol_lower(c64* A, int p, double& dmin, dou
 }
 
 // Two independent in-place Cholesky factorisations (p <= 16) by one warp: lanes 0..15 factor A1,
-// lanes 16..31 factor A2, row = lane & 15 (same schedule as warp_chol_lower). Returns A2's pivot range.
-__device__ __forceinline__ void warp_chol_lower_pair(c64* A1, c64* A2, int p, double& dmin2, double& dmax2) {
+// lanes 16..31 factor A2, row = lane & 15 (same schedule as warp_chol_lower). Returns both pivot ranges.
+__device__ __forceinline__ void warp_chol_lower_pair(c64* A1, c64* A2, int p, double& dmin1, double& dmax1,
+                                                     double& dmin2, double& dmax2) {
     const int lane = threadIdx.x & 31;
     c64* A = lane < 16 ? A1 : A2;
     const int row = lane & 15;
@@ -1078,6 +881,8 @@ __device__ __forceinline__ void warp_chol_lower_pair(c64* A1, c64* A2, int p, do
         }
         __syncwarp();
     }
+    dmin1 = __shfl_sync(0xffffffffu, dmin, 0);
+    dmax1 = __shfl_sync(0xffffffffu, dmax, 0);
     dmin2 = __shfl_sync(0xffffffffu, dmin, 16);
     dmax2 = __shfl_sync(0xffffffffu, dmax, 16);
 }
@@ -1134,14 +939,18 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
         }
     }
     __syncwarp();
-    double dmin, dmax;
+    double dmin, dmax, dminG, dmaxG;
     if (PC <= 16) {
-        warp_chol_lower_pair(L, LH, p, dmin, dmax);  // G = L L^H (R = L^H) and H = L_H L_H^H concurrently
+        // G = L L^H (R = L^H) and H = L_H L_H^H concurrently
+        warp_chol_lower_pair(L, LH, p, dminG, dmaxG, dmin, dmax);
     } else {
-        warp_chol_lower(L, p, dmin, dmax);   // G = L L^H, R = L^H: R(i, j) = conj(L[i * p + j]), j >= i
-        warp_chol_lower(LH, p, dmin, dmax);  // H = L_H L_H^H
+        warp_chol_lower(L, p, dminG, dmaxG);  // G = L L^H, R = L^H: R(i, j) = conj(L[i * p + j]), j >= i
+        warp_chol_lower(LH, p, dmin, dmax);   // H = L_H L_H^H
     }
-    if (lane == 0 && !(dmin > static_cast<double>(p) * eps_of<float>::value * dmax))
+    // A near-singular H (its Cholesky cannot stand in for the reference's truncating pinv) or a C whose Gram
+    // pivots fall below the fp64 Gram's resolution goes to the exact-algebra fallback (final_fallback.cu).
+    if (lane == 0 && (!(dmin > static_cast<double>(p) * eps_of<float>::value * dmax) ||
+                      !(dminG > static_cast<double>(p) * eps_of<double>::value * dmaxG)))
         atomicOr(&status[f], kFrameNoConv);
     for (int e = lane; e < PC * ld; e += 32) Ya[e] = mk(0.0, 0.0);  // rows >= p stay zero
     __syncwarp();
@@ -1195,8 +1004,8 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
     // Phase 1 (fp32): sweeps on a complex64 copy of Y (in the L_H region, free until T is formed) until
     // every rotated pair has |g| / sqrt(al be) < 1e-6; the fp64 phase below then restores exact column
     // orthogonality (the fp32 rotations perturb Y by ~1e-6 relative, far inside the error budget of the
-    // fp16-operand covariance). FM_JACOBI_FP64=1 skips this phase.
-    if (mixed_jacobi()) {
+    // fp16-operand covariance).
+    {
         c32* y32 = reinterpret_cast<c32*>(LH);
         for (int e = lane; e < PC * ld; e += 32) y32[e] = mk(static_cast<float>(Ya[e].re), static_cast<float>(Ya[e].im));
         __syncwarp();
@@ -1393,329 +1202,6 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
     }
 }
 
-// p in (16, 32]: the same eigen-work with TWO warps per frame (kDuoFrames frames per CTA): the Cholesky factors
-// of G and H on one warp each, the one-sided Jacobi on 64 lanes (4 lanes x 8 rows per column pair, one named
-// barrier per frame and round), Y and T on the first warp. Per-frame latency is what bounds this kernel.
-constexpr int kDuoFrames = 2;
-template <int PC>
-__global__ void __launch_bounds__(64 * kDuoFrames)
-    k_small_duo(const c64* __restrict__ Gin, const c64* __restrict__ Hin, c64* __restrict__ Tout,
-                 double* __restrict__ eig, int32_t* __restrict__ status, int frames, int p, int k,
-                 int32_t* __restrict__ dbg, double* __restrict__ eig_next, const c64* __restrict__ gpart,
-                 const c64* __restrict__ hpart) {
-    static_assert(PC == 32, "two-warp eigen-work: p in (16, 32]");
-    using W = WarpCfg<PC>;
-    extern __shared__ uint8_t dsm[];
-    __shared__ int s_flag[kDuoFrames][2];
-    const int fs = threadIdx.x >> 6, tq = threadIdx.x & 63, w2 = tq >> 5, lane = threadIdx.x & 31;
-    const int f = blockIdx.x * kDuoFrames + fs;
-    if (f >= frames) return;  // both warps of the frame
-    const int bar_id = 1 + fs;
-    auto bar = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
-    auto any2 = [&](bool pred) -> bool {  // vote over the frame's 64 lanes
-        const unsigned v = __any_sync(0xffffffffu, pred);
-        if (lane == 0) s_flag[fs][w2] = v ? 1 : 0;
-        bar();
-        const bool r = (s_flag[fs][0] | s_flag[fs][1]) != 0;
-        bar();
-        return r;
-    };
-    const int ld = W::kLd;
-    c64* L = reinterpret_cast<c64*>(dsm + fs * W::kWarpBytes);
-    c64* LH = L + PC * PC;
-    c64* Ya = LH + PC * PC;
-    double* sig = reinterpret_cast<double*>(Ya + PC * ld);
-    int* order = reinterpret_cast<int*>(sig + PC);
-    const c64* Gf = Gin + static_cast<size_t>(f) * p * p;
-    const c64* Hf = Hin + static_cast<size_t>(f) * p * p;
-    const long long T0 = clock64();
-    if (gpart) {  // G, H halves from the product kernel's epilogue; H symmetrised as k_gram_gh does
-        const size_t pp = static_cast<size_t>(p) * p;
-        const c64* g0 = gpart + static_cast<size_t>(f) * 2 * pp;
-        const c64* h0 = hpart + static_cast<size_t>(f) * 2 * pp;
-        for (int e = tq; e < p * p; e += 64) {
-            const int i = e % p, j = e / p;
-            const c64 a = h0[e] + h0[pp + e], b = h0[i * p + j] + h0[pp + i * p + j];
-            L[e] = g0[e] + g0[pp + e];
-            LH[e] = mk(0.5 * (a.re + b.re), 0.5 * (a.im - b.im));
-        }
-    } else
-    for (int e0 = 0; e0 < p * p; e0 += 8 * 64) {  // 16 loads in flight per lane
-        c64 g[8], hh[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int e = e0 + tq + 64 * u;
-            if (e < p * p) {
-                g[u] = Gf[e];
-                hh[u] = Hf[e];
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int e = e0 + tq + 64 * u;
-            if (e < p * p) {
-                L[e] = g[u];
-                LH[e] = hh[u];
-            }
-        }
-    }
-    bar();
-    double dmin, dmax;
-    // G = L L^H (R = L^H: R(i, j) = conj(L[i * p + j]), j >= i) on warp 0, H = L_H L_H^H on warp 1
-    warp_chol_lower(w2 == 0 ? L : LH, p, dmin, dmax);
-    if (w2 == 1 && lane == 0 && !(dmin > static_cast<double>(p) * eps_of<float>::value * dmax))
-        atomicOr(&status[f], kFrameNoConv);
-    bar();
-    for (int e = tq; e < PC * ld; e += 64) Ya[e] = mk(0.0, 0.0);  // rows >= p stay zero
-    bar();
-    // Y(i, :) solves y L_H^H = R(i, :) (forward substitution, lane per row); Y -> Ya (ld).
-    // Reciprocal pivots first; two partial sums per step for a shorter FMA chain.
-    double* rinv = sig;  // PC doubles, free until the singular values are formed
-    if (w2 == 0 && lane < p) {
-        const double ljj = LH[lane * p + lane].re;
-        rinv[lane] = ljj > 0.0 ? 1.0 / ljj : 0.0;
-    }
-    bar();
-    if (w2 == 0 && lane < p) {
-        const int i = lane;
-        for (int j = 0; j < p; ++j) {
-            c64 x0 = j >= i ? conj(L[i * p + j]) : mk(0.0, 0.0);
-            c64 x1 = mk(0.0, 0.0);
-            int a = i;
-            for (; a + 1 < j; a += 2) {  // y_a = 0 for a < i
-                const c64 l0 = LH[a * p + j], l1 = LH[(a + 1) * p + j];
-                const c64 v0 = Ya[a * ld + i], v1 = Ya[(a + 1) * ld + i];
-                x0.re -= v0.re * l0.re + v0.im * l0.im;
-                x0.im -= v0.im * l0.re - v0.re * l0.im;
-                x1.re -= v1.re * l1.re + v1.im * l1.im;
-                x1.im -= v1.im * l1.re - v1.re * l1.im;
-            }
-            if (a < j) {
-                const c64 l0 = LH[a * p + j];
-                const c64 v0 = Ya[a * ld + i];
-                x0.re -= v0.re * l0.re + v0.im * l0.im;
-                x0.im -= v0.im * l0.re - v0.re * l0.im;
-            }
-            const double inv = rinv[j];
-            Ya[j * ld + i] = j >= i ? mk((x0.re + x1.re) * inv, (x0.im + x1.im) * inv) : mk(0.0, 0.0);
-        }
-    }
-    bar();
-    const long long T1 = clock64();
-    // one-sided Jacobi on Y's columns, in place in Ya. Lanes are assigned to column PAIRS: slot
-    // = lane / LPP of the round-robin schedule (slot 0: (rnd, p-1); slot s: (rnd + s, rnd - s)
-    // mod (p - 1)), sub = lane % LPP owns rows sub, sub + LPP, ... of BOTH columns, so every
-    // element is read and written by one lane per round (one __syncwarp per round). Rotation:
-    // fp32-seeded angle, fp64 cos / phase refined by one Newton step (unitary to ~5e-15).
-    constexpr int LPP = 4;                  // lanes per pair (64 lanes, 16 pairs)
-    constexpr int RPL = PC / LPP;           // rows per lane
-    const int slot = tq / LPP, sub = tq % LPP;
-    const bool act = slot < p / 2;
-    const int n1 = p - 1;                   // p even (p % 4 == 0)
-    const double tol = 8.0 * 2.220446049250313e-16 * p;
-    c64* cur = Ya;
-    int sweeps = 0;
-    // Phase 1 (fp32): sweeps on a complex64 copy of Y (in the L_H region, free until T is formed) until
-    // every rotated pair has |g| / sqrt(al be) < 1e-6; the fp64 phase below then restores exact column
-    // orthogonality (the fp32 rotations perturb Y by ~1e-6 relative, far inside the error budget of the
-    // fp16-operand covariance). FM_JACOBI_FP64=1 skips this phase.
-    if (mixed_jacobi()) {
-        c32* y32 = reinterpret_cast<c32*>(LH);
-        for (int e = tq; e < PC * ld; e += 64) y32[e] = mk(static_cast<float>(Ya[e].re), static_cast<float>(Ya[e].im));
-        bar();
-        const float tol32 = FM_JACOBI_TOL32;
-        for (int sweep = 0; sweep < 12; ++sweep) {
-            bool rot_any = false;
-            for (int rnd = 0; rnd < n1; ++rnd) {
-                int i = rnd + slot, j = rnd - slot;
-                if (i >= n1) i -= n1;
-                if (j < 0) j += n1;
-                if (slot == 0) j = n1;
-                const int lo = act ? min(i, j) : 0, hi = act ? max(i, j) : 0;
-                c32* xlo = y32 + lo * ld + sub;
-                c32* xhi = y32 + hi * ld + sub;
-                c32 x[RPL], y[RPL];
-                float al = 0.f, be = 0.f;
-                c32 ga = mk(0.f, 0.f);
-#pragma unroll
-                for (int t = 0; t < RPL; ++t) {
-                    x[t] = xlo[t * LPP];
-                    y[t] = xhi[t * LPP];
-                    al = fmaf(x[t].re, x[t].re, fmaf(x[t].im, x[t].im, al));
-                    be = fmaf(y[t].re, y[t].re, fmaf(y[t].im, y[t].im, be));
-                    cmac_conj(ga, x[t], y[t]);
-                }
-#pragma unroll
-                for (int o = 1; o < LPP; o <<= 1) {
-                    al += __shfl_xor_sync(0xffffffffu, al, o);
-                    be += __shfl_xor_sync(0xffffffffu, be, o);
-                    ga.re += __shfl_xor_sync(0xffffffffu, ga.re, o);
-                    ga.im += __shfl_xor_sync(0xffffffffu, ga.im, o);
-                }
-                const float g2 = ga.re * ga.re + ga.im * ga.im;
-                const bool rotate = act && (g2 > tol32 * tol32 * al * be) && g2 > 0.f;
-                if (rotate) {
-                    const float ig = rsqrtf(g2);
-                    const float zeta = (be - al) * (0.5f * ig);
-                    const float tf = copysignf(1.0f, zeta) / (fabsf(zeta) + sqrtf(fmaf(zeta, zeta, 1.0f)));
-                    const float cs = rsqrtf(fmaf(tf, tf, 1.0f));
-                    const float sn = cs * tf;
-                    const c32 se = mk(sn * ga.re * ig, sn * ga.im * ig);
-#pragma unroll
-                    for (int t2 = 0; t2 < RPL; ++t2) {
-                        const c32 u = x[t2], v = y[t2];
-                        xlo[t2 * LPP] = mk(fmaf(cs, u.re, -fmaf(se.re, v.re, se.im * v.im)),
-                                           fmaf(cs, u.im, -fmaf(se.re, v.im, -se.im * v.re)));
-                        xhi[t2 * LPP] = mk(fmaf(cs, v.re, fmaf(se.re, u.re, -se.im * u.im)),
-                                           fmaf(cs, v.im, fmaf(se.re, u.im, se.im * u.re)));
-                    }
-                }
-                rot_any |= rotate;
-                bar();
-            }
-            if (!any2(rot_any)) break;
-        }
-        for (int e = tq; e < PC * ld; e += 64) Ya[e] = to64(y32[e]);
-        bar();
-    }
-    for (int sweep = 0; sweep < 40; ++sweep) {
-        bool rot_any = false;
-        bool big = false;  // some rotation of this sweep had |g|^2 >= 1e-14 al be
-        for (int rnd = 0; rnd < n1; ++rnd) {
-            int i = rnd + slot, j = rnd - slot;
-            if (i >= n1) i -= n1;
-            if (j < 0) j += n1;
-            if (slot == 0) j = n1;
-            const int lo = act ? min(i, j) : 0, hi = act ? max(i, j) : 0;
-            c64* xlo = cur + lo * ld + sub;
-            c64* xhi = cur + hi * ld + sub;
-            c64 x[RPL], y[RPL];
-            double al0 = 0.0, al1 = 0.0, be0 = 0.0, be1 = 0.0;
-            c64 g0 = mk(0.0, 0.0), g1 = mk(0.0, 0.0);
-#pragma unroll
-            for (int t = 0; t < RPL; ++t) {
-                x[t] = xlo[t * LPP];
-                y[t] = xhi[t * LPP];
-                if (t & 1) {
-                    al1 += norm2(x[t]);
-                    be1 += norm2(y[t]);
-                    cmac_conj(g1, x[t], y[t]);
-                } else {
-                    al0 += norm2(x[t]);
-                    be0 += norm2(y[t]);
-                    cmac_conj(g0, x[t], y[t]);
-                }
-            }
-            double al = al0 + al1, be = be0 + be1;
-            c64 ga = mk(g0.re + g1.re, g0.im + g1.im);
-#pragma unroll
-            for (int o = 1; o < LPP; o <<= 1) {
-                al += __shfl_xor_sync(0xffffffffu, al, o);
-                be += __shfl_xor_sync(0xffffffffu, be, o);
-                ga.re += __shfl_xor_sync(0xffffffffu, ga.re, o);
-                ga.im += __shfl_xor_sync(0xffffffffu, ga.im, o);
-            }
-            const double g2 = norm2(ga);
-            const bool rotate = act && (g2 > tol * tol * al * be) && g2 != 0.0;
-            if (rotate) {
-                big |= g2 >= 1e-14 * al * be;
-                const float g2f = static_cast<float>(g2);
-                const float igf = rsqrtf(g2f);
-                const float zeta = static_cast<float>(be - al) * (0.5f * igf);
-                const float tf = copysignf(1.0f, zeta) / (fabsf(zeta) + sqrtf(fmaf(zeta, zeta, 1.0f)));
-                const double t = tf;
-                const double x1 = fma(t, t, 1.0);
-                double cs = static_cast<double>(rsqrtf(static_cast<float>(x1)));
-                cs = cs * fma(-0.5 * x1, cs * cs, 1.5);
-                double ig = static_cast<double>(igf);
-                ig = ig * fma(-0.5 * g2, ig * ig, 1.5);
-                const double sn = cs * t;
-                const c64 se = mk(sn * ga.re * ig, sn * ga.im * ig);  // s e
-#pragma unroll
-                for (int t2 = 0; t2 < RPL; ++t2) {
-                    const c64 u = x[t2], v = y[t2];
-                    // lo' = c x - conj(s e) y ; hi' = s e x + c y
-                    xlo[t2 * LPP] = mk(fma(cs, u.re, -fma(se.re, v.re, se.im * v.im)),
-                                       fma(cs, u.im, -fma(se.re, v.im, -se.im * v.re)));
-                    xhi[t2 * LPP] = mk(fma(cs, v.re, fma(se.re, u.re, -se.im * u.im)),
-                                       fma(cs, v.im, fma(se.re, u.im, se.im * u.re)));
-                }
-            }
-            rot_any |= rotate;
-            bar();
-        }
-        if (!any2(rot_any)) {
-            sweeps = sweep + 1;
-            break;
-        }
-        // quadratic convergence: if every rotation of this sweep had |g| / sqrt(al be) < 1e-7, the next
-        // sweep's would be ~1e-14 (at the 8 eps p threshold) -- skip the verification sweep
-        if (!any2(big)) {
-            sweeps = sweep + 1;
-            break;
-        }
-    }
-    c64* nxt = LH;  // free after Y was formed: holds T (p x k, ld = p)
-    const int c = lane;
-    const long long T2 = clock64();
-    if (w2 != 0) return;  // sigma, ordering and T on the first warp
-    // singular values, descending order (ties: lower index first)
-    if (c < p) {
-        double s0 = 0.0, s1 = 0.0;
-        for (int r = 0; r < p; r += 2) {
-            s0 += norm2(cur[c * ld + r]);
-            s1 += norm2(cur[c * ld + r + 1]);
-        }
-        sig[c] = sqrt(s0 + s1);
-    }
-    __syncwarp();
-    if (lane < p) {
-        int rank = 0;
-        for (int q = 0; q < p; ++q)
-            if (q != lane && (sig[q] > sig[lane] || (sig[q] == sig[lane] && q < lane))) ++rank;
-        order[rank] = lane;
-    }
-    __syncwarp();
-    // T(:, kk) = R^-1 z / s (back substitution; R(i, j) = conj(L[i * p + j])), into nxt (free)
-    c64* Tm = nxt;
-    if (lane < k) {
-        const int kk = lane, cc = order[kk];
-        const double inv_s = sig[cc] > 0.0 ? 1.0 / sig[cc] : 0.0;
-        for (int i = p - 1; i >= 0; --i) {
-            c64 acc = cur[cc * ld + i];
-            acc.re *= inv_s;
-            acc.im *= inv_s;
-            for (int j = i + 1; j < p; ++j) {
-                const c64 rij = conj(L[i * p + j]);
-                const c64 tj = Tm[kk * p + j];
-                acc.re -= rij.re * tj.re - rij.im * tj.im;
-                acc.im -= rij.re * tj.im + rij.im * tj.re;
-            }
-            const double rii = L[i * p + i].re;
-            const double inv = rii > 0.0 ? 1.0 / rii : 0.0;
-            Tm[kk * p + i] = mk(acc.re * inv, acc.im * inv);
-        }
-        double lam = sig[cc];
-        lam *= lam;  // eigenvalue of B' = Y Y^H
-        eig[static_cast<size_t>(f) * k + kk] = lam;
-    }
-    if (eig_next && lane == 0) {  // (K+1)-th Ritz value (exact method's gap estimate)
-        const double sn = k < p ? sig[order[k]] : 0.0;
-        eig_next[f] = sn * sn;
-    }
-    __syncwarp();
-    c64* Tf = Tout + static_cast<size_t>(f) * p * k;
-    for (int e = lane; e < p * k; e += 32) Tf[e] = Tm[e];  // T stored compactly (ld p) in L_H
-    if (lane == 0 && sweeps == 0) atomicOr(&status[f], kFrameNoConv);
-    if (lane == 0 && dbg) dbg[f] = sweeps;
-    const long long T3 = clock64();
-    if (lane == 0 && g_phase_dbg) {
-        g_phase_dbg[f * 4 + 0] = static_cast<int>(T1 - T0);
-        g_phase_dbg[f * 4 + 1] = static_cast<int>(T2 - T1);
-        g_phase_dbg[f * 4 + 2] = static_cast<int>(T3 - T2);
-        g_phase_dbg[f * 4 + 3] = sweeps;
-    }
-}
 
 template <int PC>
 __global__ void __launch_bounds__(128, FM_BASIS_MINB) k_basis_ct(const c32* __restrict__ Cin, const c64* __restrict__ Tin,
@@ -1745,7 +1231,7 @@ __global__ void __launch_bounds__(128, FM_BASIS_MINB) k_basis_ct(const c32* __re
 
 // ------------------------------------------------------------------------------------------
 // Split power-iteration orthonormalisation (R/src/linalg.cpp:127-141 qr_orthonormal with the
-// Eigen ColPivHouseholderQR rank rule), same algebra as k_orth_tiled:
+// Eigen ColPivHouseholderQR rank rule), same algebra as the block-per-frame k_cholqr_blk:
 //   k_gram_only : G = C^H C (fp64, block per frame) -> workspace
 //   k_cholpiv_warp: pivoted Cholesky of G by one warp per frame (pivot = largest remaining Schur
 //                 diagonal), rank rule in fp32 epsilon -> L (by original row index) + perm
@@ -1856,19 +1342,8 @@ __global__ void __launch_bounds__(32 * PivCfg<PC>::kWarps)
     }
     if (lane < p) perm_out[static_cast<size_t>(f) * p + my_step] = lane;
     for (int e = lane; e < p * p; e += 32) GLf[e] = L[e];
-    if (lane == 0) {  // Eigen ColPivHouseholderQR rank rule (fp32 epsilon), as k_orth_tiled
-        const double eps = eps_of<float>::value;
-        const double thr_helper = fmax(d[0], 0.0) * eps * eps / static_cast<double>(m);
-        int nonzero = p;
-        double maxpivot = 0.0;
-        for (int k = 0; k < p; ++k) {
-            if (nonzero == p && d[k] < thr_helper * static_cast<double>(m - k)) nonzero = k;
-            maxpivot = fmax(maxpivot, sqrt(fmax(d[k], 0.0)));
-        }
-        const double thr = maxpivot * eps * static_cast<double>(p);
-        int rank = 0;
-        for (int k = 0; k < nonzero; ++k) rank += sqrt(fmax(d[k], 0.0)) > thr ? 1 : 0;
-        if (rank < p) atomicOr(&status[f], kFrameRank);
+    if (lane == 0) {  // Eigen ColPivHouseholderQR rank rule
+        if (cholqr_rank(d, p, m) < p) atomicOr(&status[f], kFrameRank);
     }
 }
 
@@ -1954,37 +1429,6 @@ cudaError_t fm_launch_cholqr_warp(const void* C, void* work, void* Vout, void* R
                       : go(smb::k_cholqr_blk<32, 0>, smb::chol_smem_bytes<32>());
 }
 
-cudaError_t fm_launch_orth_tiled(const void* C, void* Vout, int32_t* status, int frames, int m, int p,
-                                  cudaStream_t s) {
-    if (p > 32 || (p & 3) || m < p) return cudaErrorInvalidValue;
-    auto go = [&](auto kern, size_t smem) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        kern<<<frames, smb::kNT, smem, s>>>(static_cast<const c32*>(C), static_cast<c32*>(Vout), status, m, p);
-        return cudaGetLastError();
-    };
-    if (p <= 8) return go(smb::k_orth_tiled<8>, sizeof(c64) * 2 * 64 + smb::tiled_stage_bytes<8>(1));
-    if (p <= 16) return go(smb::k_orth_tiled<16>, sizeof(c64) * 2 * 256 + smb::tiled_stage_bytes<16>(1));
-    return go(smb::k_orth_tiled<32>, sizeof(c64) * 2 * 1024 + smb::tiled_stage_bytes<32>(1));
-}
-
-cudaError_t fm_launch_final_tiled(const void* C, const void* V, const void* H, void* basis, double* eig,
-                                  int32_t* status, int frames, int m, int p, int k, cudaStream_t s) {
-    if (p > 32 || (p & 3) || k > p || m < p) return cudaErrorInvalidValue;
-    auto go = [&](auto kern, int pc) {
-        const size_t smem = sizeof(c64) * 5 * pc * pc + sizeof(double) * pc + sizeof(c64) * 3 * 64 * (pc + 1);
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        kern<<<frames, smb::kNT, smem, s>>>(static_cast<const c32*>(C), static_cast<const c32*>(V),
-                                            static_cast<const c64*>(H), static_cast<c64*>(basis), eig, status, m, p, k,
-                                            g_sweep_dbg);
-        return cudaGetLastError();
-    };
-    if (p <= 8) return go(smb::k_final_tiled<8>, 8);
-    if (p <= 16) return go(smb::k_final_tiled<16>, 16);
-    return go(smb::k_final_tiled<32>, 32);
-}
-
 // Split orthonormalisation: G -> Lw (in place), perm -> permw, V = C P R^-1 -> Vout.
 // gpart != nullptr: G halves already formed by the product kernel (rmul_planes_kernel GM >= 1), no Gram launch.
 cudaError_t fm_launch_orth_split(const void* C, void* Vout, void* Lw, int32_t* permw, int32_t* status, int frames,
@@ -2047,42 +1491,13 @@ cudaError_t fm_launch_final_split(const void* C, const void* V, void* Hw, void* 
                                                           static_cast<c64*>(basis), m, p, k);
         return cudaGetLastError();
     };
-    auto go_duo = [&](auto gram, auto small, auto bas, int pc, size_t frame_bytes) {
-        const size_t gsm = sizeof(c64) * 2 * pc * pc + sizeof(c64) * 3 * 64 * (pc + 1);
-        cudaError_t e = cudaSuccess;
-        if (!gpart) {
-            e = cudaFuncSetAttribute(gram, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsm));
-            if (e != cudaSuccess) return e;
-            gram<<<frames, smb::kNT, gsm, s>>>(static_cast<const c32*>(C), static_cast<const c32*>(V),
-                                               static_cast<c64*>(Gw), static_cast<c64*>(Hw), m, p);
-            if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        }
-        const size_t wsm = frame_bytes * smb::kDuoFrames;
-        e = cudaFuncSetAttribute(small, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm));
-        if (e != cudaSuccess) return e;
-        small<<<(frames + smb::kDuoFrames - 1) / smb::kDuoFrames, 64 * smb::kDuoFrames, wsm, s>>>(
-            static_cast<const c64*>(Gw), static_cast<const c64*>(Hw), static_cast<c64*>(Tw), eig, status, frames, p, k,
-            g_sweep_dbg, eig_next, static_cast<const c64*>(gpart), static_cast<const c64*>(hpart));
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        bas<<<dim3((m + 127) / 128, frames), 128, 0, s>>>(static_cast<const c32*>(C), static_cast<const c64*>(Tw),
-                                                          static_cast<c64*>(basis), m, p, k);
-        return cudaGetLastError();
-    };
-    static const bool init_mixed = [] {
-        const int v = std::getenv("FM_JACOBI_FP64") ? 0 : 1;
-        cudaMemcpyToSymbol(smb::g_mixed_jacobi, &v, sizeof(v));
-        return true;
-    }();
-    (void)init_mixed;
     using namespace smb;
     if (p <= 8)
         return go(k_gram_gh<8>, k_small_warp<8>, k_basis_ct<8>, 8, WarpCfg<8>::kWarps, WarpCfg<8>::kWarpBytes);
     if (p <= 16)
         return go(k_gram_gh<16>, k_small_warp<16>, k_basis_ct<16>, 16, WarpCfg<16>::kWarps, WarpCfg<16>::kWarpBytes);
-    // p in (16, 32]: one warp per frame; FM_SMALL_DUO=1 runs the two-warp variant (measured slower: c3 1.29 ->
-    // 1.48 ms -- the per-round barrier between the two warps costs more than the halved row work)
-    static const bool duo = std::getenv("FM_SMALL_DUO") != nullptr;
-    if (duo) return go_duo(k_gram_gh<32>, k_small_duo<32>, k_basis_ct<32>, 32, WarpCfg<32>::kWarpBytes);
+    // p in (16, 32]: one warp per frame (a two-warp variant measured slower: c3 1.29 -> 1.48 ms, the per-round
+    // barrier between the two warps costs more than the halved row work)
     return go(k_gram_gh<32>, k_small_warp<32>, k_basis_ct<32>, 32, WarpCfg<32>::kWarps, WarpCfg<32>::kWarpBytes);
 }
 

@@ -236,145 +236,6 @@ __global__ void __launch_bounds__(kNT, FM_FFT_MINB) k_autocorr_fft(const c64* __
     }
 }
 
-// Block-wide (height desc, cell asc) argmax helper.
-__device__ __forceinline__ bool better(double h1, int c1, double h2, int c2) {
-    return h1 > h2 || (h1 == h2 && c1 < c2);
-}
-
-// R/src/spectrum.cpp:97-188 on values v[0..L) held in shared memory.
-// Outputs: cells (ascending), heights, baseline, count. Returns the candidate overflow flag.
-__device__ void block_peaks(const double* v, int L, int K, int min_sep, int* cand_cell, double* cand_h, int cap,
-                            int* out_cells, double* out_h, double* out_base, int* out_count, bool& overflow) {
-    __shared__ int s_nc;
-    __shared__ int s_sel[64];
-    __shared__ double s_selh[64];
-    __shared__ int s_nsel;
-    __shared__ double s_wh[kNW];
-    __shared__ int s_wc[kNW];
-    __shared__ int s_wi[kNW];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        s_nc = 0;
-        s_nsel = 0;
-    }
-    __syncthreads();
-    // 1. strict local maxima; plateau -> leftmost index (run start with a rising edge)
-    for (int l = 1 + threadIdx.x; l + 1 < L; l += kNT) {
-        const double x = v[l];
-        if (x > v[l - 1]) {
-            int r = l;
-            while (r + 1 < L && v[r + 1] == x) ++r;
-            if (r + 1 < L && v[r + 1] < x) {
-                const int slot = atomicAdd(&s_nc, 1);
-                if (slot < cap) {
-                    cand_cell[slot] = l;
-                    cand_h[slot] = x;
-                }
-            }
-        }
-    }
-    __syncthreads();
-    const int nc = min(s_nc, cap);
-    overflow = s_nc > cap;
-    // 2. greedy selection in (height desc, cell asc) order with |dc| >= min_sep:
-    //    repeatedly take the best candidate not clashing with the current selection.
-    for (int it = 0; it < K; ++it) {
-        double bh = -1.0;
-        int bc = 0x7fffffff, bi = -1;
-        const int nsel = s_nsel;
-        for (int i = threadIdx.x; i < nc; i += kNT) {
-            const int c = cand_cell[i];
-            bool clash = false;
-            for (int s = 0; s < nsel; ++s)
-                if (abs(c - s_sel[s]) < min_sep || c == s_sel[s]) {  // each candidate considered once
-                    clash = true;
-                    break;
-                }
-            if (clash) continue;
-            const double h = cand_h[i];
-            if (bi < 0 || better(h, c, bh, bc)) {
-                bh = h;
-                bc = c;
-                bi = i;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double oh = __shfl_xor_sync(0xffffffffu, bh, o);
-            const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (oi >= 0 && (bi < 0 || better(oh, oc, bh, bc))) {
-                bh = oh;
-                bc = oc;
-                bi = oi;
-            }
-        }
-        if (lane == 0) {
-            s_wh[warp] = bh;
-            s_wc[warp] = bc;
-            s_wi[warp] = bi;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int wi = -1;
-            double wh = -1.0;
-            int wc = 0x7fffffff;
-            for (int w = 0; w < kNW; ++w)
-                if (s_wi[w] >= 0 && (wi < 0 || better(s_wh[w], s_wc[w], wh, wc))) {
-                    wi = s_wi[w];
-                    wh = s_wh[w];
-                    wc = s_wc[w];
-                }
-            if (wi >= 0) {
-                s_sel[s_nsel] = wc;
-                s_selh[s_nsel] = wh;
-                s_nsel = s_nsel + 1;
-            }
-        }
-        __syncthreads();
-        if (s_nsel == nsel) break;  // exhausted: shortfall
-    }
-    const int nsel = s_nsel;
-    // 3. baseline: max over cells farther than min_sep from every selected peak (init 0)
-    double p0 = 0.0;
-    for (int l = threadIdx.x; l < L; l += kNT) {
-        bool near = false;
-        for (int s = 0; s < nsel; ++s)
-            if (abs(l - s_sel[s]) <= min_sep) {
-                near = true;
-                break;
-            }
-        if (!near) p0 = fmax(p0, v[l]);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) p0 = fmax(p0, __shfl_xor_sync(0xffffffffu, p0, o));
-    if (lane == 0) s_wh[warp] = p0;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double b = 0.0;
-        for (int w = 0; w < kNW; ++w) b = fmax(b, s_wh[w]);
-        // 4. ascending cell order (to_peak_set)
-        for (int x = 0; x < nsel; ++x) {
-            int best = x;
-            for (int y = x + 1; y < nsel; ++y)
-                if (s_sel[y] < s_sel[best]) best = y;
-            const int tc = s_sel[x];
-            s_sel[x] = s_sel[best];
-            s_sel[best] = tc;
-            const double th = s_selh[x];
-            s_selh[x] = s_selh[best];
-            s_selh[best] = th;
-        }
-        for (int x = 0; x < K; ++x) {
-            out_cells[x] = x < nsel ? s_sel[x] : -1;
-            out_h[x] = x < nsel ? s_selh[x] : 0.0;
-        }
-        *out_base = b;
-        *out_count = nsel;
-    }
-    __syncthreads();
-}
-
 struct PeakOut {
     int32_t* cells;     // B x K
     double* heights;    // B x K
@@ -382,61 +243,30 @@ struct PeakOut {
     int32_t* count;     // B
 };
 
-// Candidate capacity: a degree-(M-1) trigonometric denominator has < M interior minima,
-// so 2M + 64 slots cover any MUSIC spectrum; bounded by the shared-memory budget.
-__host__ __device__ __forceinline__ int cand_cap(int L, int m) {
-    const int budget = (200 * 1024 - 8 * L - 16 * m) / 12;
-    const int want = L / 2 + 1 < 2 * m + 64 ? L / 2 + 1 : 2 * m + 64;
-    return want < budget ? want : budget;
-}
-__host__ __device__ __forceinline__ int cand_cap_values(int L) {
-    const int budget = (200 * 1024 - 8 * L) / 12;
-    return L / 2 + 1 < budget ? L / 2 + 1 : budget;
-}
-
-// Spectrum (fp64 Horner over z) + peaks, one CTA per frame.
-__global__ void __launch_bounds__(kNT) k_spectrum_peaks(const c64* __restrict__ t, const c64* __restrict__ zgrid,
-                                                        int m, int L, float* __restrict__ spec32,
-                                                        double* __restrict__ spec64, int K, int min_sep,
-                                                        PeakOut out, int32_t* __restrict__ status) {
-    extern __shared__ uint8_t dsm[];
-    double* sP = reinterpret_cast<double*>(dsm);
-    c64* st = reinterpret_cast<c64*>(sP + L);
-    const int cap = cand_cap(L, m);
-    int* ccell = reinterpret_cast<int*>(st + m);
-    double* ch = reinterpret_cast<double*>(ccell + ((cap + 1) & ~1));
+// Spectrum only (fp64 Horner over z), one CTA per frame: the facade's music_spectrum on any grid.
+__global__ void __launch_bounds__(kNT) k_spectrum_one(const c64* __restrict__ t, const c64* __restrict__ zgrid, int m,
+                                                      int L, double* __restrict__ spec64) {
+    extern __shared__ c64 st1[];
     const int f = blockIdx.x;
-    for (int r = threadIdx.x; r < m; r += kNT) st[r] = t[static_cast<size_t>(f) * m + r];
+    for (int r = threadIdx.x; r < m; r += kNT) st1[r] = t[static_cast<size_t>(f) * m + r];
     __syncthreads();
-    const double c0 = static_cast<double>(m) - st[0].re;
+    const double c0 = static_cast<double>(m) - st1[0].re;
     const double floor_v = 1e-12 * static_cast<double>(m);
     for (int l = threadIdx.x; l < L; l += kNT) {
         const c64 z = zgrid[l];
         double pr = 0.0, pi = 0.0;
         if (m > 1) {
-            pr = st[m - 1].re;
-            pi = st[m - 1].im;
+            pr = st1[m - 1].re;
+            pi = st1[m - 1].im;
             for (int dlt = m - 2; dlt >= 1; --dlt) {
-                const double nr = fma(pr, z.re, fma(-pi, z.im, st[dlt].re));
-                const double ni = fma(pr, z.im, fma(pi, z.re, st[dlt].im));
+                const double nr = fma(pr, z.re, fma(-pi, z.im, st1[dlt].re));
+                const double ni = fma(pr, z.im, fma(pi, z.re, st1[dlt].im));
                 pr = nr;
                 pi = ni;
             }
-            const double sr = pr * z.re - pi * z.im;  // Re(p * z)
-            pr = sr;
+            pr = pr * z.re - pi * z.im;  // Re(p * z)
         }
-        const double d = c0 - 2.0 * pr;
-        const double P = 1.0 / fmax(d, floor_v);
-        sP[l] = P;
-        if (spec32) spec32[static_cast<size_t>(f) * L + l] = static_cast<float>(P);
-        if (spec64) spec64[static_cast<size_t>(f) * L + l] = P;
-    }
-    __syncthreads();
-    if (out.cells) {
-        bool overflow = false;
-        block_peaks(sP, L, K, min_sep, ccell, ch, cap, out.cells + static_cast<size_t>(f) * K,
-                    out.heights + static_cast<size_t>(f) * K, out.baseline + f, out.count + f, overflow);
-        if (overflow && threadIdx.x == 0 && status) atomicOr(&status[f], kFrameNoConv);
+        spec64[static_cast<size_t>(f) * L + l] = 1.0 / fmax(c0 - 2.0 * pr, floor_v);
     }
 }
 
@@ -506,213 +336,10 @@ __global__ void __launch_bounds__(kNT) k_spectrum_multi(const c64* __restrict__ 
     }
 }
 
-// Mirror-symmetric grids (theta0 = -theta1: theta_{L-1-q} = -theta_q, z_{L-1-q} = conj z_q):
-// with A = sum_delta Re t_delta Re z^delta and B = sum_delta Im t_delta Im z^delta,
-//     Re sum t_delta z^delta = A - B   (theta_q),      Re sum t_delta conj(z)^delta = A + B   (-theta_q),
-// so a mirrored pair costs what one point costs in k_spectrum_multi. Thread = two pairs
-// (q0, q0 + qh); the block's kSFPB frames share the two power sequences (fp64 recurrence).
-constexpr int kSFPB = 8;
-
-__global__ void __launch_bounds__(kNT, 2) k_spectrum_sym(const c64* __restrict__ t, const c64* __restrict__ zgrid,
-                                                      int frames, int m, int L, float* __restrict__ spec32,
-                                                      double* __restrict__ spec64) {
-    extern __shared__ c64 st[];  // kSFPB x m coefficients, delta-major
-    const int f0 = blockIdx.y * kSFPB;
-    const int nf = min(kSFPB, frames - f0);
-    for (int e = threadIdx.x; e < kSFPB * m; e += kNT) {
-        const int f = e / m, dl = e % m;
-        st[dl * kSFPB + f] = f < nf ? t[static_cast<size_t>(f0 + f) * m + dl] : mk(0.0, 0.0);
-    }
-    __syncthreads();
-    const int nq = (L + 1) / 2;          // pairs (q, L-1-q); q = L/2 is self-paired when L is odd
-    const int qh = (nq + 1) / 2;
-    const int q0 = blockIdx.x * kNT + threadIdx.x;
-    if (q0 >= qh) return;
-    const int q1 = q0 + qh;
-    const bool has1 = q1 < nq;
-    const c64 za = zgrid[q0];
-    const c64 zb = has1 ? zgrid[q1] : mk(1.0, 0.0);
-    double A0[kSFPB], B0[kSFPB], A1[kSFPB], B1[kSFPB];
-#pragma unroll
-    for (int f = 0; f < kSFPB; ++f) A0[f] = B0[f] = A1[f] = B1[f] = 0.0;
-    double ar = 1.0, ai = 0.0, br = 1.0, bi = 0.0;
-    for (int dl = 1; dl < m; ++dl) {
-        const double nar = fma(ar, za.re, -ai * za.im);
-        const double nai = fma(ar, za.im, ai * za.re);
-        const double nbr = fma(br, zb.re, -bi * zb.im);
-        const double nbi = fma(br, zb.im, bi * zb.re);
-        ar = nar;
-        ai = nai;
-        br = nbr;
-        bi = nbi;
-        const c64* row = st + dl * kSFPB;
-#pragma unroll
-        for (int f = 0; f < kSFPB; ++f) {
-            const c64 c = row[f];
-            A0[f] = fma(c.re, ar, A0[f]);
-            B0[f] = fma(c.im, ai, B0[f]);
-            A1[f] = fma(c.re, br, A1[f]);
-            B1[f] = fma(c.im, bi, B1[f]);
-        }
-    }
-    const double floor_v = 1e-12 * static_cast<double>(m);
-#pragma unroll
-    for (int f = 0; f < kSFPB; ++f) {
-        if (f < nf) {
-            const double c0 = static_cast<double>(m) - st[f].re;
-            const size_t o = static_cast<size_t>(f0 + f) * L;
-            const int qs[2] = {q0, q1};
-            const double As[2] = {A0[f], A1[f]}, Bs[2] = {B0[f], B1[f]};
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                if (u == 1 && !has1) break;
-                const int q = qs[u], qm = L - 1 - q;
-                const double Pp = 1.0 / fmax(c0 - 2.0 * (As[u] - Bs[u]), floor_v);
-                if (spec32) spec32[o + q] = static_cast<float>(Pp);
-                spec64[o + q] = Pp;
-                if (qm != q) {
-                    const double Pm = 1.0 / fmax(c0 - 2.0 * (As[u] + Bs[u]), floor_v);
-                    if (spec32) spec32[o + qm] = static_cast<float>(Pm);
-                    spec64[o + qm] = Pm;
-                }
-            }
-        }
-    }
-}
-
-// Mirror-symmetric grids on the FP64 tensor cores (mma.sync m8n8k4 f64): with pairs (q, L-1-q) as in
-// k_spectrum_sym, A(f, q) = sum_delta Re t_f,delta cos(delta phi_q) and B(f, q) = sum_delta Im t_f,delta
-// sin(delta phi_q) are two real GEMMs T_re x Zc and T_im x Zs over delta = 1..M-1 (K), frames (M dim) and
-// pairs (N dim); d(theta_q) = c0 - 2 (A - B), d(-theta_q) = c0 - 2 (A + B) with c0 = M - Re t_0, P = 1 /
-// max(d, 1e-12 M) (R/src/spectrum.cpp:37-46, 50-68). The powers z_q^delta = e^{j delta phi_q}, delta = 16a + b,
-// are formed per K-chunk as zhi[a][q] * zlo[b][q] from two host tables (angles 16a phi_q and b phi_q, glibc),
-// instead of the fp64 recurrence. fp64 throughout; the tensor core does 256 FMAs per warp instruction.
-constexpr int kSDF = 64;   // frames per CTA tile
-constexpr int kSDQ = 64;   // pairs per CTA tile
-constexpr int kSDK = 16;   // delta per chunk
-constexpr int kSDT = 256;  // threads (8 warps: 2 along frames x 4 along pairs; warp tile 32 x 16)
-constexpr int kTLd = kSDK + 1;  // complex128 row pitch of the T chunk
-constexpr int kZLd = kSDQ + 4;
-constexpr int kSDSmem = 2 * (kSDF * kTLd * 16 + 2 * kSDK * kZLd * 8);  // double-buffered T and Z chunks
-__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                 : "+d"(c[0]), "+d"(c[1])
-                 : "d"(a), "d"(b));
-}
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
                  "l"(src), "r"(src_bytes)
                  : "memory");
-}
-__global__ void __launch_bounds__(kSDT, 2) k_spectrum_dmma(const c64* __restrict__ t, const c64* __restrict__ zpow,
-                                                          int frames, int m, int L, float* __restrict__ spec32,
-                                                          double* __restrict__ spec64) {
-    extern __shared__ __align__(16) uint8_t sdm[];
-    c64* Tb = reinterpret_cast<c64*>(sdm);                          // [2][kSDF][kTLd]
-    double* Zb = reinterpret_cast<double*>(Tb + 2 * kSDF * kTLd);   // [2][2 (cos, sin)][kSDK][kZLd]
-    const int nq = (L + 1) / 2;
-    const int na = (m + kSDK - 1) / kSDK;
-    const c64* zhi = zpow;                                 // [na][nq]
-    const c64* zlo = zpow + static_cast<size_t>(na) * nq;  // [16][nq]
-    const int f0 = blockIdx.y * kSDF, q0 = blockIdx.x * kSDQ;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int wm = warp & 1, wn = warp >> 1;  // warp tile: frames 32 wm .., pairs 16 wn ..
-    // Z builder: thread -> pair column zq, four delta rows zb0 .. zb0 + 3 of each chunk
-    const int zq = tid & (kSDQ - 1), zb0 = (tid >> 6) * 4;
-    const bool zin = q0 + zq < nq;
-    c64 zl[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) zl[u] = zin ? zlo[static_cast<size_t>(zb0 + u) * nq + q0 + zq] : mk(0.0, 0.0);
-    auto issue_t = [&](int a, int buf) {  // T chunk a -> buffer (cp.async; delta = 0, delta >= m, f >= frames -> 0)
-        c64* T = Tb + buf * kSDF * kTLd;
-#pragma unroll
-        for (int u = 0; u < kSDF * kSDK / kSDT; ++u) {
-            const int e = tid + u * kSDT;
-            const int fr = e / kSDK, dl = e % kSDK, de = a * kSDK + dl;
-            const bool ok = f0 + fr < frames && de >= 1 && de < m;
-            cp_async16(T + fr * kTLd + dl, ok ? t + static_cast<size_t>(f0 + fr) * m + de : t, ok ? 16 : 0);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    auto put_z = [&](c64 zh, int buf) {
-        double* Zc = Zb + buf * 2 * kSDK * kZLd;
-        double* Zs = Zc + kSDK * kZLd;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const c64 z = zh * zl[u];
-            Zc[(zb0 + u) * kZLd + zq] = z.re;
-            Zs[(zb0 + u) * kZLd + zq] = z.im;
-        }
-    };
-    double ac[4][2][2], as[4][2][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) ac[i][j][0] = ac[i][j][1] = as[i][j][0] = as[i][j][1] = 0.0;
-    issue_t(0, 0);
-    put_z(zin ? zhi[q0 + zq] : mk(0.0, 0.0), 0);
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
-    for (int a = 0; a < na; ++a) {
-        const int buf = a & 1;
-        const bool more = a + 1 < na;
-        c64 zn = mk(0.0, 0.0);
-        if (more) {  // next chunk in flight while this one is consumed
-            issue_t(a + 1, buf ^ 1);
-            if (zin) zn = zhi[static_cast<size_t>(a + 1) * nq + q0 + zq];
-        }
-        const c64* T = Tb + buf * kSDF * kTLd;
-        const double* Zc = Zb + buf * 2 * kSDK * kZLd;
-        const double* Zs = Zc + kSDK * kZLd;
-#pragma unroll
-        for (int k4 = 0; k4 < kSDK / 4; ++k4) {
-            c64 av[4];
-            double bc[2], bs[2];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) av[i] = T[(32 * wm + 8 * i + (lane >> 2)) * kTLd + 4 * k4 + (lane & 3)];
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const int r = 4 * k4 + (lane & 3), c = 16 * wn + 8 * j + (lane >> 2);
-                bc[j] = Zc[r * kZLd + c];
-                bs[j] = Zs[r * kZLd + c];
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    dmma(ac[i][j], av[i].re, bc[j]);
-                    dmma(as[i][j], av[i].im, bs[j]);
-                }
-        }
-        if (more) put_z(zn, buf ^ 1);  // buffer buf ^ 1 was released by the barrier that ended chunk a - 1
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
-    }
-    const double floor_v = 1e-12 * static_cast<double>(m);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int f = f0 + 32 * wm + 8 * i + (lane >> 2);
-        if (f >= frames) continue;
-        const double c0 = static_cast<double>(m) - t[static_cast<size_t>(f) * m].re;
-        const size_t o = static_cast<size_t>(f) * L;
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int q = q0 + 16 * wn + 8 * j + 2 * (lane & 3) + h;
-                if (q >= nq) continue;
-                const int qm = L - 1 - q;
-                const double A = ac[i][j][h], B = as[i][j][h];
-                const double Pp = 1.0 / fmax(c0 - 2.0 * (A - B), floor_v);
-                if (spec32) spec32[o + q] = static_cast<float>(Pp);
-                spec64[o + q] = Pp;
-                if (qm != q) {
-                    const double Pm = 1.0 / fmax(c0 - 2.0 * (A + B), floor_v);
-                    if (spec32) spec32[o + qm] = static_cast<float>(Pm);
-                    spec64[o + qm] = Pm;
-                }
-            }
-    }
 }
 
 // Mirror-symmetric grids on the INT8 tensor cores, fp64-exact by digit splitting (Ozaki scheme): the same
@@ -902,384 +529,92 @@ __global__ void __launch_bounds__(kOT, 3 - kONB) k_spectrum_i8(const int8_t* __r
     }
 }
 
-// Peaks, one WARP per frame (R/src/spectrum.cpp:97-188, same rules as block_peaks):
-//  1. strict interior maxima with leftmost-plateau rule, found 32 cells at a time (coalesced
-//     loads) and compacted in cell order with ballot/popc; capacity ceil((L-2)/2) is exact
-//     (strict maxima are never adjacent), so there is no overflow;
-//  2. greedy (height desc, cell asc) with |dc| >= min_sep: K warp-argmax rounds, candidates within
-//     min_sep of a pick invalidated (cells are sorted, so they are index neighbours);
-//  3. baseline = max over cells with |l - s| > min_sep for every pick (shared bitmask), init 0;
-//  4. picks in ascending cell order, padded with -1 / 0.
+// Peaks, one 128-thread CTA per frame (R/src/spectrum.cpp:97-188, any L >= 1 and K >= 1):
+//  1. values -> shared memory (coalesced, 8 loads in flight per thread), or read in place from global memory when
+//     the frame's workspace does not fit (long grids / large K: the workspace then lives in `gws`);
+//  2. strict interior maxima (leftmost-plateau rule, local_maxima :105-122), 32 consecutive cells per warp step,
+//     compacted in cell order (ballots -> per-warp counts -> prefix); the exact capacity floor((L-1)/2) holds them
+//     all (strict maxima are never adjacent);
+//  3. warp 0 runs the greedy (ranked_maxima + select_separated :124-148) as K argmax rounds over the list: the
+//     best (height desc, cell asc) candidate not yet excluded is the reference walk's next acceptance (a candidate
+//     that clashes with an accepted pick stays rejected), then candidates with |c - s| < min_sep (and c == s) are
+//     excluded; no sort. The argmax starts at -inf, so any finite spectrum (dB scale, negative values) works;
+//  4. baseline_outside (:150-164) = max over cells with |l - s| > min_sep for every pick (bitmask), init 0 (fmax
+//     drops NaN like std::max(p0, NaN)); picks in ascending cell order (to_peak_set :166-178).
+constexpr int kPRT = 128;
+constexpr int kPCL = 8;  // register-held candidates per lane (256 per frame)
+
+struct PeakLayout {
+    int cap, nmask, ngroups;
+    size_t o_sv, o_selh, o_cl, o_near, o_bal, o_sel, o_ex, bytes;
+};
+__host__ __device__ inline PeakLayout peak_layout(int L, int K, bool with_values) {
+    PeakLayout p;
+    p.cap = L > 2 ? (L - 1) / 2 : 1;
+    p.nmask = (L + 31) / 32;
+    p.ngroups = L > 2 ? (L - 2 + 31) / 32 : 0;
+    size_t o = 0;
+    p.o_sv = o;
+    if (with_values) o += sizeof(double) * static_cast<size_t>(L);
+    p.o_selh = o;
+    o += sizeof(double) * static_cast<size_t>(K);
+    p.o_cl = o;
+    o += sizeof(int) * static_cast<size_t>(p.cap);
+    p.o_near = o;
+    o += sizeof(uint32_t) * static_cast<size_t>(p.nmask);
+    p.o_bal = o;
+    o += sizeof(uint32_t) * static_cast<size_t>(p.ngroups + 1);
+    p.o_sel = o;
+    o += sizeof(int) * static_cast<size_t>(K);
+    p.o_ex = o;
+    o += static_cast<size_t>(p.cap);
+    p.bytes = (o + 15) & ~size_t(15);
+    return p;
+}
+constexpr size_t kPeakSmemMax = 220 * 1024;
+
 __device__ __forceinline__ bool better_w(double h1, int c1, double h2, int c2) {
     return h1 > h2 || (h1 == h2 && c1 < c2);
 }
 
-__global__ void k_peaks_warp(const double* __restrict__ values, int frames, int L, int K, int min_sep, int cap,
-                             PeakOut out) {
-    extern __shared__ uint8_t wsm[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nwarps = blockDim.x >> 5;
-    const int f = blockIdx.x * nwarps + warp;
-    if (f >= frames) return;
-    const int nmask = (L + 31) / 32;
-    const size_t per = static_cast<size_t>(cap) * 12 + static_cast<size_t>(nmask) * 4 + 64 * 12;
-    uint8_t* base = wsm + static_cast<size_t>(warp) * ((per + 15) / 16 * 16);
-    double* ch = reinterpret_cast<double*>(base);             // cap heights
-    int* cc = reinterpret_cast<int*>(ch + cap);                // cap cells
-    uint32_t* near = reinterpret_cast<uint32_t*>(cc + cap);    // L bits
-    int* sel_c = reinterpret_cast<int*>(near + nmask);         // 64
-    double* sel_h = reinterpret_cast<double*>(((reinterpret_cast<uintptr_t>(sel_c + 64) + 7) & ~uintptr_t(7)));
-    const double* v = values + static_cast<size_t>(f) * L;
-    // 1. candidates in cell order: 4 x 32 cells per batch (coalesced loads in flight), neighbours
-    //    by shuffles; the equal-neighbour (plateau) case scans forward from memory
-    int nc = 0;
-    double prev = v[0];  // value left of the current 32-cell group
-    for (int b0 = 1; b0 < L - 1; b0 += 128) {
-        double xs[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int l = b0 + 32 * u + lane;
-            xs[u] = l < L ? v[l] : 0.0;
-        }
-        const int lr = b0 + 128;
-        const double after = lr < L ? v[lr] : 0.0;  // right neighbour of the last group
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int l = b0 + 32 * u + lane;
-            const double x = xs[u];
-            const double up = __shfl_up_sync(0xffffffffu, x, 1);
-            const double dn = __shfl_down_sync(0xffffffffu, x, 1);
-            const double nxt0 = u < 3 ? __shfl_sync(0xffffffffu, xs[u < 3 ? u + 1 : u], 0) : after;
-            const double xm = lane == 0 ? prev : up;
-            const double xp = lane == 31 ? nxt0 : dn;
-            bool is = false;
-            if (l < L - 1 && x > xm) {
-                if (xp < x) {
-                    is = true;
-                } else if (xp == x) {  // plateau: leftmost cell if the run ends with a drop
-                    int r = l + 1;
-                    while (r + 1 < L && v[r + 1] == x) ++r;
-                    is = (r + 1 < L) && v[r + 1] < x;
-                }
-            }
-            const uint32_t bal = __ballot_sync(0xffffffffu, is);
-            if (is) {
-                const int pos = nc + __popc(bal & ((1u << lane) - 1u));
-                if (pos < cap) {
-                    ch[pos] = x;
-                    cc[pos] = l;
-                }
-            }
-            nc += __popc(bal);
-            prev = __shfl_sync(0xffffffffu, x, 31);
-        }
-    }
-    if (nc > cap) {  // more maxima than the degree bound allows for (fp noise): CTA kernel reruns it
-        if (lane == 0) out.count[f] = -1;
-        return;
-    }
-    for (int w = lane; w < nmask; w += 32) near[w] = 0u;
-    __syncwarp();
-    // 2. greedy selection
-    int nsel = 0;
-    for (int it = 0; it < K; ++it) {
-        double bh = -1.0;
-        int bc = 0x7fffffff, bi = -1;
-        for (int i = lane; i < nc; i += 32) {
-            const double h = ch[i];
-            if (h >= 0.0 && (bi < 0 || better_w(h, cc[i], bh, bc))) {
-                bh = h;
-                bc = cc[i];
-                bi = i;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double oh = __shfl_xor_sync(0xffffffffu, bh, o);
-            const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (oi >= 0 && (bi < 0 || better_w(oh, oc, bh, bc))) {
-                bh = oh;
-                bc = oc;
-                bi = oi;
-            }
-        }
-        if (bi < 0) break;  // exhausted: shortfall
-        if (lane == 0) {
-            sel_c[nsel] = bc;
-            sel_h[nsel] = bh;
-        }
-        // invalidate the pick and its clashing neighbours (|dc| < min_sep; sorted cells)
-        const int lo = max(0, bi - min_sep), hi = min(nc - 1, bi + min_sep);
-        for (int i = lo + lane; i <= hi; i += 32)
-            if (i == bi || abs(cc[i] - bc) < min_sep) ch[i] = -1.0;
-        // exclusion band for the baseline: |l - pick| <= min_sep
-        for (int d = lane - min_sep; d <= min_sep; d += 32) {
-            const int l = bc + d;
-            if (l >= 0 && l < L) atomicOr(&near[l >> 5], 1u << (l & 31));
-        }
-        ++nsel;
-        __syncwarp();
-    }
-    __syncwarp();
-    // 3. baseline
-    double p0 = 0.0;
-#pragma unroll 8
-    for (int l = lane; l < L; l += 32)
-        if (!((near[l >> 5] >> (l & 31)) & 1u)) p0 = fmax(p0, v[l]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) p0 = fmax(p0, __shfl_xor_sync(0xffffffffu, p0, o));
-    // 4. ascending cell order: rank of each pick (cells are distinct)
-    __syncwarp();
-    for (int x = lane; x < K; x += 32) {
-        if (x < nsel) {
-            const int c = sel_c[x];
-            int rank = 0;
-            for (int y = 0; y < nsel; ++y) rank += sel_c[y] < c ? 1 : 0;
-            out.cells[static_cast<size_t>(f) * K + rank] = c;
-            out.heights[static_cast<size_t>(f) * K + rank] = sel_h[x];
-        } else {
-            out.cells[static_cast<size_t>(f) * K + x] = -1;
-            out.heights[static_cast<size_t>(f) * K + x] = 0.0;
-        }
-    }
-    if (lane == 0) {
-        out.baseline[f] = p0;
-        out.count[f] = nsel;
-    }
-}
-
-// Peaks, one CTA per frame, same rules as block_peaks / k_peaks_warp (R/src/spectrum.cpp:97-188):
-// the frame's values are loaded once (coalesced, all threads) into shared memory; candidates are
-// detected from shared memory 32 cells per warp step and compacted in cell order (per-warp
-// ballot counts -> block prefix -> second pass); warp 0 alone runs the greedy selection (warp
-// argmax, neighbour invalidation, no block barriers); all warps compute the baseline.
-__device__ long long* g_peak_dbg = nullptr;  // debug: per-frame phase cycles
-
-// Peaks, one CTA per frame, same rules as block_peaks (R/src/spectrum.cpp:97-188):
-//  1. values -> shared memory (coalesced); strict interior maxima (leftmost-plateau rule) found
-//     32 cells per warp step, compacted in cell order (per-warp ballot counts -> prefix -> pass 2);
-//  2. candidates sorted once by (height desc, cell asc) with a CTA bitonic sort; lane 0 walks the
-//     sorted list accepting picks with |dc| >= min_sep from every accepted pick (= the greedy);
-//  3. baseline = max over cells with |l - pick| > min_sep for every pick (bitmask), init 0;
-//  4. picks in ascending cell order, padded with -1 / 0.
-// cap_in > 0 bounds the candidate list (shared memory for long grids): a frame with more strict maxima writes
-// count = -1 and leaves; k_peaks_only(only_flagged = 1) redoes it (same protocol as k_peaks_warp).
-__global__ void __launch_bounds__(kNT) k_peaks_cta(const double* __restrict__ values, int L, int K, int min_sep,
-                                                   PeakOut out, int cap_in) {
-    const long long T0 = clock64();
-    extern __shared__ uint8_t psm[];
-    const int cap = cap_in > 0 ? cap_in : max(1, (L - 1) / 2);
-    int n2 = 1;
-    while (n2 < cap) n2 <<= 1;
-    const int nmask = (L + 31) / 32;
-    double* sv = reinterpret_cast<double*>(psm);               // L
-    double* ch = sv + L;                                       // n2 (sort keys: height)
-    int* cc = reinterpret_cast<int*>(ch + n2);                 // n2 (cell)
-    uint32_t* near = reinterpret_cast<uint32_t*>(cc + n2);     // nmask
-    __shared__ int s_cnt[kNW];
-    __shared__ int s_sel[64];
-    __shared__ double s_selh[64];
-    __shared__ int s_nsel;
-    __shared__ double s_wmax[kNW];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int f = blockIdx.x;
-    const double* v = values + static_cast<size_t>(f) * L;
-    for (int l = threadIdx.x; l < L; l += kNT) sv[l] = v[l];
-    for (int w = threadIdx.x; w < nmask; w += kNT) near[w] = 0u;
-    __syncthreads();
-    const long long T1 = clock64();
-    auto is_max = [&](int l) -> bool {
-        if (l < 1 || l >= L - 1) return false;
-        const double x = sv[l], xm = sv[l - 1], xp = sv[l + 1];
-        if (!(x > xm)) return false;
-        if (xp < x) return true;
-        if (!(xp == x)) return false;
-        int r = l + 1;  // plateau
-        while (r + 1 < L && sv[r + 1] == x) ++r;
-        return (r + 1 < L) && sv[r + 1] < x;
-    };
-    const int ngroups = (L - 2 + 31) / 32;
-    const int gpw = (ngroups + kNW - 1) / kNW;  // warp w owns groups [w gpw, (w + 1) gpw): cell order
-    const int g0 = warp * gpw, g1 = min(ngroups, g0 + gpw);
-    uint32_t bals[8];
-    int cnt = 0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-        const int g = g0 + u;
-        bals[u] = __ballot_sync(0xffffffffu, g < g1 && is_max(1 + 32 * g + lane));
-        cnt += __popc(bals[u]);
-    }
-    for (int g = g0 + 8; g < g1; ++g) cnt += __popc(__ballot_sync(0xffffffffu, is_max(1 + 32 * g + lane)));
-    if (lane == 0) s_cnt[warp] = cnt;
-    __syncthreads();
-    int off = 0, nc = 0;
-    for (int w = 0; w < kNW; ++w) {
-        if (w < warp) off += s_cnt[w];
-        nc += s_cnt[w];
-    }
-    if (nc > cap) {  // block-uniform
-        if (threadIdx.x == 0) out.count[f] = -1;
-        return;
-    }
-    for (int g = g0; g < g1; ++g) {
-        const int u = g - g0;
-        const uint32_t bal = u < 8 ? bals[u < 8 ? u : 0] : __ballot_sync(0xffffffffu, is_max(1 + 32 * g + lane));
-        if ((bal >> lane) & 1u) {
-            const int pos = off + __popc(bal & ((1u << lane) - 1u));
-            const int l = 1 + 32 * g + lane;
-            ch[pos] = sv[l];
-            cc[pos] = l;
-        }
-        off += __popc(bal);
-    }
-    // pad to a power of two with sentinels (sorted last)
-    int ns = 1;
-    while (ns < nc) ns <<= 1;
-    for (int i = nc + threadIdx.x; i < ns; i += kNT) {
-        ch[i] = -1.0;
-        cc[i] = 0x7fffffff;
-    }
-    __syncthreads();
-    const long long T2 = clock64();
-    // bitonic sort by (height desc, cell asc)
-    for (int k2 = 2; k2 <= ns; k2 <<= 1) {
-        for (int j = k2 >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < ns; i += kNT) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const double hi_ = ch[i], hj = ch[ixj];
-                    const int ci = cc[i], cj = cc[ixj];
-                    const bool j_first = better_w(hj, cj, hi_, ci);  // element ixj belongs before i
-                    const bool asc = (i & k2) == 0;
-                    if (asc ? j_first : !j_first) {
-                        ch[i] = hj;
-                        ch[ixj] = hi_;
-                        cc[i] = cj;
-                        cc[ixj] = ci;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-    // greedy walk over the sorted list (lane 0), exclusion bands by warp 0
-    if (warp == 0) {
-        int nsel = 0;
-        if (lane == 0) {
-            for (int i = 0; i < nc && nsel < K; ++i) {
-                const int c = cc[i];
-                bool clash = false;
-                for (int q = 0; q < nsel; ++q)
-                    if (abs(c - s_sel[q]) < min_sep || c == s_sel[q]) {
-                        clash = true;
-                        break;
-                    }
-                if (!clash) {
-                    s_sel[nsel] = c;
-                    s_selh[nsel] = ch[i];
-                    ++nsel;
-                }
-            }
-            s_nsel = nsel;
-        }
-        __syncwarp();
-        nsel = s_nsel;
-        for (int q = 0; q < nsel; ++q) {
-            const int bc = s_sel[q];
-            for (int d = lane - min_sep; d <= min_sep; d += 32) {
-                const int l = bc + d;
-                if (l >= 0 && l < L) atomicOr(&near[l >> 5], 1u << (l & 31));
-            }
-        }
-    }
-    __syncthreads();
-    const long long T3 = clock64();
-    if (threadIdx.x == 0 && g_peak_dbg) {
-        g_peak_dbg[f * 4 + 0] = T1 - T0;
-        g_peak_dbg[f * 4 + 1] = T2 - T1;
-        g_peak_dbg[f * 4 + 2] = T3 - T2;
-        g_peak_dbg[f * 4 + 3] = nc;
-    }
-    // baseline
-    double p0 = 0.0;
-    for (int l = threadIdx.x; l < L; l += kNT)
-        if (!((near[l >> 5] >> (l & 31)) & 1u)) p0 = fmax(p0, sv[l]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) p0 = fmax(p0, __shfl_xor_sync(0xffffffffu, p0, o));
-    if (lane == 0) s_wmax[warp] = p0;
-    __syncthreads();
-    if (warp == 0) {
-        const int nsel = s_nsel;
-        for (int x = lane; x < K; x += 32) {
-            if (x < nsel) {
-                const int c = s_sel[x];
-                int rank = 0;
-                for (int y = 0; y < nsel; ++y) rank += s_sel[y] < c ? 1 : 0;
-                out.cells[static_cast<size_t>(f) * K + rank] = c;
-                out.heights[static_cast<size_t>(f) * K + rank] = s_selh[x];
-            } else {
-                out.cells[static_cast<size_t>(f) * K + x] = -1;
-                out.heights[static_cast<size_t>(f) * K + x] = 0.0;
-            }
-        }
-        if (lane == 0) {
-            double b = 0.0;
-            for (int w = 0; w < kNW; ++w) b = fmax(b, s_wmax[w]);
-            out.baseline[f] = b;
-            out.count[f] = nsel;
-        }
-    }
-}
-
-// Peaks, one 128-thread CTA per frame (R/src/spectrum.cpp:97-188):
-//  1. values -> shared memory (coalesced, 8 loads in flight per thread);
-//  2. strict interior maxima (leftmost-plateau rule, as block_peaks), 32 consecutive cells per warp step, compacted
-//     in cell order (ballots -> per-warp counts -> prefix); the exact capacity floor((L-1)/2) holds them all
-//     (strict maxima are never adjacent);
-//  3. warp 0 runs the greedy as K argmax rounds over the list: the best (height desc, cell asc) candidate not
-//     yet excluded is the reference walk's next acceptance (a candidate that clashes with an accepted pick stays
-//     rejected), then candidates with |c - s| < min_sep (and c == s) are excluded; no sort;
-//  4. baseline = max over cells with |l - s| > min_sep for every pick (bitmask), init 0; picks ascending.
-constexpr int kPRT = 128;
-constexpr int kPCL = 8;  // register-held candidates per lane (256 per frame)
+template <bool kInSmem>
 __global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict__ values, int L, int K, int min_sep,
-                                                      PeakOut out) {
-    extern __shared__ uint8_t prs[];
-    const int cap = max(1, (L - 1) / 2);
-    const int nmask = (L + 31) / 32;
-    double* sv = reinterpret_cast<double*>(prs);              // L
-    int* cl = reinterpret_cast<int*>(sv + L);                  // cap candidate cells (ascending)
-    uint8_t* ex = reinterpret_cast<uint8_t*>(cl + cap);        // cap exclusion flags
-    uint32_t* near = reinterpret_cast<uint32_t*>(ex + ((cap + 15) & ~15));  // nmask
-    uint32_t* bal_s = near + nmask;                                          // (L - 2 + 31) / 32 ballots
+                                                      PeakOut out, uint8_t* __restrict__ gws) {
+    extern __shared__ __align__(16) uint8_t prs[];
+    const PeakLayout lay = peak_layout(L, K, kInSmem);
+    const int f = blockIdx.x;
+    uint8_t* base = kInSmem ? prs : gws + static_cast<size_t>(f) * lay.bytes;
+    const double* v = values + static_cast<size_t>(f) * L;
+    double* svw = reinterpret_cast<double*>(base + lay.o_sv);
+    const double* sv = kInSmem ? svw : v;
+    double* s_selh = reinterpret_cast<double*>(base + lay.o_selh);
+    int* cl = reinterpret_cast<int*>(base + lay.o_cl);
+    uint32_t* near = reinterpret_cast<uint32_t*>(base + lay.o_near);
+    uint32_t* bal_s = reinterpret_cast<uint32_t*>(base + lay.o_bal);
+    int* s_sel = reinterpret_cast<int*>(base + lay.o_sel);
+    uint8_t* ex = base + lay.o_ex;
+    const int nmask = lay.nmask;
     __shared__ int s_cnt[kPRT / 32];
-    __shared__ int s_sel[64];
-    __shared__ double s_selh[64];
     __shared__ int s_nsel;
     __shared__ double s_wmax[kPRT / 32];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int f = blockIdx.x;
-    const double* v = values + static_cast<size_t>(f) * L;
-    const long long T0 = clock64();
-    for (int l0 = tid; l0 < L; l0 += 8 * kPRT) {
-        double tmp[8];
+    if (kInSmem) {
+        for (int l0 = tid; l0 < L; l0 += 8 * kPRT) {
+            double tmp[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int l = l0 + u * kPRT;
-            tmp[u] = l < L ? __ldcs(v + l) : 0.0;
-        }
+            for (int u = 0; u < 8; ++u) {
+                const int l = l0 + u * kPRT;
+                tmp[u] = l < L ? __ldcs(v + l) : 0.0;
+            }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int l = l0 + u * kPRT;
-            if (l < L) sv[l] = tmp[u];
+            for (int u = 0; u < 8; ++u) {
+                const int l = l0 + u * kPRT;
+                if (l < L) svw[l] = tmp[u];
+            }
         }
     }
     for (int w = tid; w < nmask; w += kPRT) near[w] = 0u;
     __syncthreads();
-    const long long T1 = clock64();
-    // candidates: 32 consecutive cells per warp step (lane = cell, conflict-free shared reads), warp w owning the
-    // contiguous groups [w gpw, (w + 1) gpw); ballots -> per-warp counts -> block prefix -> cell-ordered list
     auto is_max = [&](int l) -> bool {
         if (l < 1 || l >= L - 1) return false;
         const double x = sv[l], xm = sv[l - 1], xp = sv[l + 1];
@@ -1290,7 +625,7 @@ __global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict_
         while (r + 1 < L && sv[r + 1] == x) ++r;
         return (r + 1 < L) && sv[r + 1] < x;
     };
-    const int ngroups = (L - 2 + 31) / 32;
+    const int ngroups = lay.ngroups;
     const int gpw = (ngroups + kPRT / 32 - 1) / (kPRT / 32);
     const int g0 = warp * gpw, g1 = min(ngroups, g0 + gpw);
     int cnt = 0;
@@ -1317,11 +652,11 @@ __global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict_
     }
     if (lane == 0) s_cnt[warp] = cnt;
     __syncthreads();
-    int off = 0, base = 0;
+    int off = 0, nc = 0;
 #pragma unroll
     for (int w = 0; w < kPRT / 32; ++w) {
         off += w < warp ? s_cnt[w] : 0;
-        base += s_cnt[w];
+        nc += s_cnt[w];
     }
     for (int g = g0; g < g1; ++g) {
         const uint32_t bal = bal_s[g];
@@ -1333,10 +668,8 @@ __global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict_
         off += __popc(bal);
     }
     __syncthreads();
-    const int nc = base;
-    const long long T2 = clock64();
-    if (warp == 0 && nc <= 32 * kPCL) {  // greedy rounds, candidates in registers (any MUSIC
-        // spectrum: < M maxima); lane holds list entries lane + 32 u (ascending cells within the lane)
+    if (warp == 0 && nc <= 32 * kPCL) {  // greedy rounds, candidates in registers (any MUSIC spectrum: < M maxima);
+        // lane holds list entries lane + 32 u (ascending cells within the lane)
         double hv[kPCL];
         int cv[kPCL];
         uint32_t live = 0u;
@@ -1344,16 +677,16 @@ __global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict_
         for (int u = 0; u < kPCL; ++u) {
             const int j = lane + 32 * u;
             cv[u] = j < nc ? cl[j] : 0x7fffffff;
-            hv[u] = j < nc ? sv[cv[u]] : -1.0;
+            hv[u] = j < nc ? sv[cv[u]] : -INFINITY;
             if (j < nc) live |= 1u << u;
         }
         int nsel = 0;
         for (; nsel < K; ++nsel) {
-            double h = -1.0;
+            double h = -INFINITY;
             int c = 0x7fffffff;
 #pragma unroll
             for (int u = 0; u < kPCL; ++u)
-                if (((live >> u) & 1u) && better_w(hv[u], cv[u], h, c)) {
+                if (((live >> u) & 1u) && (c == 0x7fffffff || better_w(hv[u], cv[u], h, c))) {
                     h = hv[u];
                     c = cv[u];
                 }
@@ -1361,7 +694,7 @@ __global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict_
             for (int o = 16; o > 0; o >>= 1) {
                 const double oh = __shfl_xor_sync(0xffffffffu, h, o);
                 const int oc = __shfl_xor_sync(0xffffffffu, c, o);
-                if (better_w(oh, oc, h, c)) {
+                if (oc != 0x7fffffff && (c == 0x7fffffff || better_w(oh, oc, h, c))) {
                     h = oh;
                     c = oc;
                 }
@@ -1380,16 +713,16 @@ __global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict_
             }
         }
         if (lane == 0) s_nsel = nsel;
-    } else if (warp == 0) {  // greedy rounds over the compacted list in shared memory
+    } else if (warp == 0) {  // greedy rounds over the compacted list
         int nsel = 0;
         for (; nsel < K; ++nsel) {
-            double h = -1.0;
+            double h = -INFINITY;
             int c = 0x7fffffff, jb = -1;
             for (int j = lane; j < nc; j += 32)
                 if (!ex[j]) {
                     const int cj = cl[j];
                     const double hj = sv[cj];
-                    if (better_w(hj, cj, h, c)) {
+                    if (jb < 0 || better_w(hj, cj, h, c)) {
                         h = hj;
                         c = cj;
                         jb = j;
@@ -1400,19 +733,19 @@ __global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict_
                 const double oh = __shfl_xor_sync(0xffffffffu, h, o);
                 const int oc = __shfl_xor_sync(0xffffffffu, c, o);
                 const int oj = __shfl_xor_sync(0xffffffffu, jb, o);
-                if (better_w(oh, oc, h, c)) {
+                if (oj >= 0 && (jb < 0 || better_w(oh, oc, h, c))) {
                     h = oh;
                     c = oc;
                     jb = oj;
                 }
             }
-            if (c == 0x7fffffff) break;
+            if (jb < 0) break;
             if (lane == 0) {
                 s_sel[nsel] = c;
                 s_selh[nsel] = h;
             }
             // clash band around the pick: the list is in cell order, so walk outwards from its index
-            for (int d = lane; ; d += 32) {
+            for (int d = lane;; d += 32) {
                 bool any = false;
                 const int jl = jb - d, jr = jb + d;
                 if (jl >= 0 && (c - cl[jl] < min_sep || jl == jb)) {
@@ -1434,13 +767,6 @@ __global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict_
         if (lane == 0) s_nsel = nsel;
     }
     __syncthreads();
-    if (tid == 0 && g_peak_dbg) {
-        const long long T3 = clock64();
-        g_peak_dbg[f * 4 + 0] = T1 - T0;
-        g_peak_dbg[f * 4 + 1] = T2 - T1;
-        g_peak_dbg[f * 4 + 2] = T3 - T2;
-        g_peak_dbg[f * 4 + 3] = nc;
-    }
     double p0 = 0.0;
     for (int l = tid; l < L; l += kPRT)
         if (!((near[l >> 5] >> (l & 31)) & 1u)) p0 = fmax(p0, sv[l]);
@@ -1467,25 +793,6 @@ __global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict_
         out.baseline[f] = b;
         out.count[f] = nsel;
     }
-}
-
-// Peaks only, on caller-provided fp64 values (facade extract_peaks).
-__global__ void __launch_bounds__(kNT) k_peaks_only(const double* __restrict__ values, int L, int K, int min_sep,
-                                                    PeakOut out, int32_t* __restrict__ overflow_flag,
-                                                    int only_flagged) {
-    extern __shared__ uint8_t dsm[];
-    double* sv = reinterpret_cast<double*>(dsm);
-    const int cap = cand_cap_values(L);
-    int* ccell = reinterpret_cast<int*>(sv + L);
-    double* ch = reinterpret_cast<double*>(ccell + ((cap + 1) & ~1));
-    const int f = blockIdx.x;
-    if (only_flagged && out.count[f] != -1) return;
-    for (int l = threadIdx.x; l < L; l += kNT) sv[l] = values[static_cast<size_t>(f) * L + l];
-    __syncthreads();
-    bool overflow = false;
-    block_peaks(sv, L, K, min_sep, ccell, ch, cap, out.cells + static_cast<size_t>(f) * K,
-                out.heights + static_cast<size_t>(f) * K, out.baseline + f, out.count + f, overflow);
-    if (overflow && threadIdx.x == 0 && overflow_flag) atomicOr(overflow_flag, 1);
 }
 
 // max |U^H U - I| per frame (music_spectrum precondition, R/src/spectrum.cpp:55-61).
@@ -1520,10 +827,9 @@ __global__ void __launch_bounds__(kNT) k_orthocheck(const c64* __restrict__ basi
 using namespace fmk;
 
 cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, int k, cudaStream_t s) {
-    static const bool direct = std::getenv("FM_DIRECT_AUTOCORR") != nullptr;  // comparison switch
     int logn = 1;
     while ((1 << logn) < 2 * m - 1) ++logn;
-    if (!direct && logn <= 12) {
+    if (logn <= 12) {  // FFT in shared memory (M <= 2048)
         const int nfft = 1 << logn;
         const size_t fixed = sizeof(c64) * nfft + sizeof(double) * nfft;
         const size_t per = sizeof(c64) * (nfft + nfft / 8);  // padded
@@ -1541,7 +847,9 @@ cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, in
             return cudaGetLastError();
         }
     }
+    // direct lag sums (large M)
     const size_t smem = sizeof(c64) * m;
+    if (smem > 220 * 1024) return cudaErrorInvalidValue;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(spec::k_autocorr, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
@@ -1552,23 +860,16 @@ cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, in
     return cudaGetLastError();
 }
 
-static size_t spectrum_smem(int m, int L) {
-    const int cap = spec::cand_cap(L, m);
-    if (cap < std::min(L / 2 + 1, 16)) return ~size_t(0);
-    return sizeof(double) * L + sizeof(c64) * m + sizeof(int) * ((cap + 1) & ~1) + sizeof(double) * cap + 16;
-}
-
-cudaError_t fm_launch_spectrum_peaks(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
-                                     double* spec64, int K, int min_sep, int32_t* cells, double* heights,
-                                     double* baseline, int32_t* count, int32_t* status, cudaStream_t s) {
-    const size_t smem = spectrum_smem(m, L);
-    if (smem > 227 * 1024 || K > 64) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(spec::k_spectrum_peaks, cudaFuncAttributeMaxDynamicSharedMemorySize,
+// Facade music_spectrum: spectrum only, any grid, one CTA per frame.
+cudaError_t fm_launch_spectrum_one(const void* t, const void* zgrid, int frames, int m, int L, double* spec64,
+                                   cudaStream_t s) {
+    const size_t smem = sizeof(c64) * m;
+    if (smem > 220 * 1024) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(spec::k_spectrum_one, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    spec::PeakOut out{cells, heights, baseline, count};
-    spec::k_spectrum_peaks<<<frames, spec::kNT, smem, s>>>(static_cast<const c64*>(t), static_cast<const c64*>(zgrid),
-                                                           m, L, spec32, spec64, K, min_sep, out, status);
+    spec::k_spectrum_one<<<frames, spec::kNT, smem, s>>>(static_cast<const c64*>(t), static_cast<const c64*>(zgrid), m, L,
+                                                         spec64);
     return cudaGetLastError();
 }
 
@@ -1594,32 +895,9 @@ cudaError_t fm_launch_spectrum_i8(const void* t, const int8_t* zd, int8_t* td, d
     return cudaGetLastError();
 }
 
-// zpow: [ceil(m / 16)][nq] e^{j 16 a phi_q} then [16][nq] e^{j b phi_q} (fm_zpow_host); mirror-symmetric grids.
-cudaError_t fm_launch_spectrum_dmma(const void* t, const void* zpow, int frames, int m, int L, float* spec32,
-                                    double* spec64, cudaStream_t s) {
-    const int nq = (L + 1) / 2;
-    dim3 grid((nq + spec::kSDQ - 1) / spec::kSDQ, (frames + spec::kSDF - 1) / spec::kSDF);
-    const cudaError_t attr = cudaFuncSetAttribute(spec::k_spectrum_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  spec::kSDSmem);
-    if (attr != cudaSuccess) return attr;
-    spec::k_spectrum_dmma<<<grid, spec::kSDT, spec::kSDSmem, s>>>(static_cast<const c64*>(t), static_cast<const c64*>(zpow),
-                                                                   frames, m, L, spec32, spec64);
-    return cudaGetLastError();
-}
-
+// Any grid (the plan's path when theta0 != -theta1): kFPB frames per CTA share one fp64 power sequence.
 cudaError_t fm_launch_spectrum_multi(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
-                                     double* spec64, cudaStream_t s, bool symmetric) {
-    if (symmetric && sizeof(c64) * spec::kSFPB * m <= 200 * 1024) {
-        const size_t smem = sizeof(c64) * spec::kSFPB * m;
-        cudaError_t e = cudaFuncSetAttribute(spec::k_spectrum_sym, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        const int qh = ((L + 1) / 2 + 1) / 2;
-        dim3 grid((qh + spec::kNT - 1) / spec::kNT, (frames + spec::kSFPB - 1) / spec::kSFPB);
-        spec::k_spectrum_sym<<<grid, spec::kNT, smem, s>>>(static_cast<const c64*>(t), static_cast<const c64*>(zgrid),
-                                                           frames, m, L, spec32, spec64);
-        return cudaGetLastError();
-    }
+                                     double* spec64, cudaStream_t s) {
     auto go = [&](auto kern, int fpb) {
         const size_t smem = sizeof(c64) * fpb * m;
         if (smem > 200 * 1024) return cudaErrorInvalidValue;
@@ -1635,85 +913,33 @@ cudaError_t fm_launch_spectrum_multi(const void* t, const void* zgrid, int frame
     return go(spec::k_spectrum_multi<4>, 4);
 }
 
-// cap_hint > 0: candidate capacity per frame for the warp kernel (pipeline: 2M + 64, the degree
-// bound of a MUSIC spectrum plus slack); frames exceeding it are redone by the CTA kernel.
+// Global workspace bytes fm_launch_peaks_only needs for `frames` frames (0: the frame fits in shared memory).
+size_t fm_peaks_workspace_bytes(int frames, int L, int K) {
+    if (spec::peak_layout(L, K, true).bytes <= spec::kPeakSmemMax) return 0;
+    return static_cast<size_t>(frames) * spec::peak_layout(L, K, false).bytes;
+}
+
+// extract_peaks on B x L fp64 values (R/src/spectrum.cpp:182-188), any L >= 1, K >= 1. gws: device workspace of
+// fm_peaks_workspace_bytes(frames, L, K) bytes when that is non-zero.
 cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K, int min_sep, int32_t* cells,
-                                 double* heights, double* baseline, int32_t* count, int32_t* overflow,
-                                 cudaStream_t s, int cap_hint) {
-    if (K > 64 || L < 2) return cudaErrorInvalidValue;
-    static const bool block_kernel = std::getenv("FM_BLOCK_PEAKS") != nullptr;  // comparison switch
+                                 double* heights, double* baseline, int32_t* count, void* gws, cudaStream_t s) {
+    if (K < 1 || L < 1 || frames < 1) return cudaErrorInvalidValue;
     spec::PeakOut out{cells, heights, baseline, count};
-    const int cap_b = spec::cand_cap_values(L);
-    const size_t smem_b = sizeof(double) * L + sizeof(int) * ((cap_b + 1) & ~1) + sizeof(double) * cap_b + 16;
-    auto block = [&](int only_flagged) {
-        if (cap_b < std::min(L / 2 + 1, 16) || smem_b > 227 * 1024) return cudaErrorInvalidValue;
-        cudaError_t e = cudaFuncSetAttribute(spec::k_peaks_only, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem_b));
+    const spec::PeakLayout lay = spec::peak_layout(L, K, true);
+    if (lay.bytes <= spec::kPeakSmemMax) {
+        cudaError_t e = cudaFuncSetAttribute(spec::k_peaks_rounds<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(lay.bytes));
         if (e != cudaSuccess) return e;
-        spec::k_peaks_only<<<frames, spec::kNT, smem_b, s>>>(values, L, K, min_sep, out, overflow, only_flagged);
-        return cudaGetLastError();
-    };
-    static const bool warp_env = std::getenv("FM_WARP_PEAKS") != nullptr;
-    bool warp_kernel = warp_env;
-    static const bool sort_env = std::getenv("FM_SORT_PEAKS") != nullptr;  // comparison: sort-based k_peaks_cta
-    const int cap_r = std::max(1, (L - 1) / 2);
-    const size_t smem_r = sizeof(double) * L + sizeof(int) * cap_r + ((cap_r + 15) & ~15) + sizeof(uint32_t) * 2 * ((L + 31) / 32);
-    if (!block_kernel && !warp_kernel && !sort_env && !std::getenv("FM_PEAKS_CAP") && !std::getenv("FM_PEAKS_CTA_CAP") &&
-        smem_r <= 200 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(spec::k_peaks_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem_r));
-        if (e != cudaSuccess) return e;
-        spec::k_peaks_rounds<<<frames, spec::kPRT, smem_r, s>>>(values, L, K, min_sep, out);
-        return cudaGetLastError();
+        spec::k_peaks_rounds<true><<<frames, spec::kPRT, lay.bytes, s>>>(values, L, K, min_sep, out, nullptr);
+    } else {
+        if (!gws) return cudaErrorInvalidValue;
+        spec::k_peaks_rounds<false><<<frames, spec::kPRT, 0, s>>>(values, L, K, min_sep, out,
+                                                                 static_cast<uint8_t*>(gws));
     }
-    if (const char* ov = std::getenv("FM_PEAKS_CAP")) {  // test hook: warp kernel + capacity fallback path
-        cap_hint = std::atoi(ov);
-        warp_kernel = true;
-    }
-    if (!block_kernel && !warp_kernel) {  // CTA per frame: exact candidate capacity, else the cap hint
-        const int exact = std::max(1, (L - 1) / 2);
-        auto cta_smem = [&](int capc) {
-            int n2 = 1;
-            while (n2 < capc) n2 <<= 1;
-            return sizeof(double) * L + static_cast<size_t>(n2) * 12 + sizeof(uint32_t) * ((L + 31) / 32) + 16;
-        };
-        int capc = exact;
-        if (const char* ce = std::getenv("FM_PEAKS_CTA_CAP"))  // test hook: capped CTA kernel + fallback
-            capc = std::min(exact, std::max(1, std::atoi(ce)));
-        else if (cta_smem(capc) > 200 * 1024 && cap_hint > 0)
-            capc = std::min(exact, cap_hint);
-        const size_t smem = cta_smem(capc);
-        if (smem <= 200 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(spec::k_peaks_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(smem));
-            if (e != cudaSuccess) return e;
-            spec::k_peaks_cta<<<frames, spec::kNT, smem, s>>>(values, L, K, min_sep, out, capc < exact ? capc : 0);
-            if ((e = cudaGetLastError()) != cudaSuccess) return e;
-            return capc < exact ? block(1) : cudaSuccess;
-        }
-    }
-    if (!block_kernel) {  // warp per frame
-        const int exact = std::max(1, (L - 1) / 2);
-        const int cap = cap_hint > 0 ? std::min(exact, cap_hint) : exact;
-        const size_t per = (static_cast<size_t>(cap) * 12 + static_cast<size_t>((L + 31) / 32) * 4 + 64 * 12 + 15) / 16 * 16;
-        const int nw = static_cast<int>(std::max<size_t>(1, std::min<size_t>(16, (100 * 1024) / per)));
-        if (per <= 200 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(spec::k_peaks_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(per * nw));
-            if (e != cudaSuccess) return e;
-            spec::k_peaks_warp<<<(frames + nw - 1) / nw, 32 * nw, per * nw, s>>>(values, frames, L, K, min_sep, cap, out);
-            if ((e = cudaGetLastError()) != cudaSuccess) return e;
-            return cap < exact ? block(1) : cudaSuccess;
-        }
-    }
-    return block(0);
+    return cudaGetLastError();
 }
 
 cudaError_t fm_launch_orthocheck(const void* basis, int frames, int m, int k, double* dev, cudaStream_t s) {
     spec::k_orthocheck<<<frames, spec::kNT, 0, s>>>(static_cast<const c64*>(basis), m, k, dev);
     return cudaGetLastError();
-}
-
-extern "C" int32_t fm_debug_set_peak_buffer(long long* d) {
-    return cudaMemcpyToSymbol(fmk::spec::g_peak_dbg, &d, sizeof(d)) == cudaSuccess ? 0 : 1;
 }

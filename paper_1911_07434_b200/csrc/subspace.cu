@@ -482,18 +482,7 @@ __global__ void __launch_bounds__(kNT) k_cholqr(const c32* __restrict__ Cin, c64
     __syncthreads();
     if (MODE == 0 && threadIdx.x == 0) {
         // Eigen ColPivHouseholderQR::rank() on the pivoted-Cholesky diagonal, data eps = fp32
-        const double eps = eps_of<float>::value;
-        const double thr_helper = fmax(d[0], 0.0) * eps * eps / static_cast<double>(m);  // maxColNorm^2 = d[0]
-        int nonzero = p;
-        double maxpivot = 0.0;
-        for (int k = 0; k < p; ++k) {
-            if (nonzero == p && d[k] < thr_helper * static_cast<double>(m - k)) nonzero = k;
-            maxpivot = fmax(maxpivot, sqrt(fmax(d[k], 0.0)));
-        }
-        const double thr = maxpivot * eps * static_cast<double>(p);
-        int rank = 0;
-        for (int k = 0; k < nonzero; ++k) rank += sqrt(fmax(d[k], 0.0)) > thr ? 1 : 0;
-        if (rank < p) atomicOr(&status[f], kFrameRank);
+        if (cholqr_rank(d, p, m) < p) atomicOr(&status[f], kFrameRank);
     }
     if (MODE == 0) {
         rows_apply_linvh(Cf, perm, G, m, p, Vout + static_cast<size_t>(f) * m * p);

@@ -54,3 +54,32 @@ def compare_frames(oracle, cfg, x, frames, res, grid=None, a_mat=None, db_tol=0.
         if cells != pk.cells:
             mismatched.append((f, cells, pk.cells))
     return worst, mismatched
+
+
+def _oracle_job(args):
+    from oracle import fastmusic_oracle as O
+    cfg, xf, f, p_gpu, cells = args
+    est, p_ref, pk = O.run_frame(cfg, xf, f)
+    db = O.spectrum_db_error(p_gpu, p_ref)
+    return f, db, cells == pk.cells, pk.cells
+
+
+def compare_frames_parallel(cfg, x, frames, res, procs=None):
+    """compare_frames over many frames with a process pool (the fp64 oracle is the slow side).
+    Returns (worst dB, [(frame, gpu cells, oracle cells)] mismatches, per-frame dB list)."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+    import os
+    jobs = []
+    for i, f in enumerate(frames):
+        n = int(res["peak_count"][i])
+        jobs.append((cfg, x[i], f, res["spectrum"][i].astype(np.float64), [int(c) for c in res["peak_cells"][i][:n]]))
+    procs = procs or min(32, os.cpu_count() or 1)
+    worst, mism, dbs = 0.0, [], []
+    with cf.ProcessPoolExecutor(procs, mp_context=mp.get_context("fork")) as ex:
+        for (f, db, same, ref_cells), job in zip(ex.map(_oracle_job, jobs, chunksize=4), jobs):
+            worst = max(worst, db)
+            dbs.append(db)
+            if not same:
+                mism.append((f, job[4], ref_cells))
+    return worst, mism, dbs

@@ -206,46 +206,38 @@ def test_peaks_match_oracle_random(fm, oracle):
         assert got.baseline == ref.baseline and got.shortfall == ref.shortfall
 
 
-@pytest.mark.parametrize("cap", ["1", "7", "40"])
-def test_peaks_cta_capacity_falls_back(fm, oracle, monkeypatch, cap):
-    """CTA peak kernel with a bounded candidate list (long grids: values + candidates must fit shared
-    memory; the pipeline bounds it by 2M + 64): frames with more maxima are redone, results unchanged."""
-    monkeypatch.setenv("FM_PEAKS_CTA_CAP", cap)
-    rng = np.random.default_rng(12)
-    for _ in range(20):
-        n = int(rng.integers(20, 400))
+def _peaks_equal(fm, oracle, v, k, sep, tag=None):
+    got = fm.extract_peaks(fm.PseudoSpectrum(fm.AngleGrid(max(len(v), 2)), np.asarray(v, float)), k, sep)
+    ref = oracle.extract_peaks(np.asarray(v, float), k, sep)
+    assert got.cells == ref.cells and got.heights == ref.heights, tag
+    assert got.baseline == ref.baseline and got.shortfall == ref.shortfall, tag
+
+
+def test_peaks_negative_and_db_scale_spectra(fm, oracle):
+    """any finite spectrum, e.g. a dB-scale one with every value below -1 (the argmax starts at
+    -inf; the baseline keeps the reference's 0 start, R/src/spectrum.cpp:150-164)."""
+    rng = np.random.default_rng(31)
+    for _ in range(60):
+        n = int(rng.integers(3, 500))
         v = rng.random(n)
-        k, sep = int(rng.integers(1, 9)), int(rng.integers(0, 5))
-        got = fm.extract_peaks(fm.PseudoSpectrum(fm.AngleGrid(n), v), k, sep)
-        ref = oracle.extract_peaks(v, k, sep)
-        assert got.cells == ref.cells and got.heights == ref.heights
-        assert got.baseline == ref.baseline and got.shortfall == ref.shortfall
+        mode = rng.integers(0, 3)
+        if mode == 0:
+            v = 10.0 * np.log10(v * 1e-3)          # all < -30 dB
+        elif mode == 1:
+            v = -1.0 - 5.0 * v                      # all below -1
+        else:
+            v = rng.integers(-6, 0, size=n).astype(float)  # negative plateaus
+        _peaks_equal(fm, oracle, v, int(rng.integers(1, 12)), int(rng.integers(0, 5)), (n, mode))
 
 
-def test_peaks_cta_capacity_falls_back_long_grid(fm, oracle):
-    """A grid long enough (L = 18001, c4's) that the exact candidate list does not fit shared memory and
-    more maxima than any MUSIC spectrum of M = 64 has: the capped CTA kernel hands the frame to the fallback."""
+def test_peaks_global_workspace_long_grids_large_k(fm, oracle):
+    """Grids whose peak workspace does not fit shared memory (L = 30001, 60001) and K beyond 64 run the same
+    kernel over a global workspace: identical to the reference's sort + greedy walk."""
     rng = np.random.default_rng(13)
-    v = rng.random(18001)
-    got = fm.extract_peaks(fm.PseudoSpectrum(fm.AngleGrid(18001), v), 16, 3)
-    ref = oracle.extract_peaks(v, 16, 3)
-    assert got.cells == ref.cells and got.heights == ref.heights and got.baseline == ref.baseline
-
-
-@pytest.mark.parametrize("cap", ["4", "1"])
-def test_peaks_candidate_overflow_falls_back(fm, oracle, monkeypatch, cap):
-    """Warp peak kernel with a tiny candidate capacity (the pipeline uses 2M + 64): frames with more
-    maxima than the capacity are redone by the CTA kernel, results unchanged."""
-    monkeypatch.setenv("FM_PEAKS_CAP", cap)
-    rng = np.random.default_rng(11)
-    for _ in range(20):
-        n = int(rng.integers(20, 400))
-        v = rng.random(n)
-        k, sep = int(rng.integers(1, 9)), int(rng.integers(0, 5))
-        got = fm.extract_peaks(fm.PseudoSpectrum(fm.AngleGrid(n), v), k, sep)
-        ref = oracle.extract_peaks(v, k, sep)
-        assert got.cells == ref.cells and got.heights == ref.heights
-        assert got.baseline == ref.baseline and got.shortfall == ref.shortfall
+    for n, k, sep in ((30001, 16, 3), (60001, 100, 2), (30001, 300, 0), (4001, 500, 1)):
+        for ints in (False, True):
+            v = rng.integers(0, 4, size=n).astype(float) if ints else rng.random(n)
+            _peaks_equal(fm, oracle, v, k, sep, (n, k, sep, ints))
 
 
 def test_peaks_rounds_long_grids_wide_bands(fm, oracle):

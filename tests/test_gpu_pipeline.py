@@ -115,18 +115,9 @@ def test_subspace_close_to_oracle(fm, oracle, cfgs):
         assert np.allclose(res["eigenvalues"][i], est.eigenvalues, rtol=1e-4)
 
 
-def _exact_run(fm, x, m, n, k, env_jacobi):
-    import os
+def _exact_run(fm, x, m, n, k, env_jacobi, grid_size=721):
     import torch
-    old = os.environ.pop("FM_EXACT_JACOBI", None)
-    if env_jacobi:
-        os.environ["FM_EXACT_JACOBI"] = "1"
-    try:
-        plan = fm.BatchPlan(m, n, k, "exact", grid_size=721, max_frames=len(x))
-    finally:
-        os.environ.pop("FM_EXACT_JACOBI", None)
-        if old is not None:
-            os.environ["FM_EXACT_JACOBI"] = old
+    plan = fm.BatchPlan(m, n, k, "exact", grid_size=grid_size, max_frames=len(x), exact_jacobi=env_jacobi)
     xd = torch.from_numpy(np.ascontiguousarray(x).view(np.float32)).cuda()
     out = plan.outputs(len(x), spectrum=True, basis=True)
     plan.run(len(x), xd, None, None, out)
