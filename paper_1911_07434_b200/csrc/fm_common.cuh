@@ -76,6 +76,37 @@ __device__ __forceinline__ int cholqr_rank(const double* d, int p, int m) {
     return rank;
 }
 
+// 2^-e for the power of two 2^e nearest below sqrt(v) (v > 0 normal double): exact rescaling factor.
+__device__ __forceinline__ double pow2_inv_sqrt_scale(double v) {
+    int e2 = ((__double2hiint(v) >> 20) & 0x7ff) - 1023;  // v = 1.x 2^e2
+    int eh = e2 >> 1;                                     // floor(e2 / 2)
+    eh = eh < -500 ? -500 : (eh > 500 ? 500 : eh);
+    return __hiloint2double((1023 - eh) << 20, 0);
+}
+
+// One-sided Jacobi rotation of the column pair (x, y), al = |x|^2, be = |y|^2, g = x^H y, g2 = |g|^2 > 0:
+// c, s (fp64) and s e with e = g / |g|, so that x' = c x - conj(s e) y, y' = s e x + c y are orthogonal.
+// The angle is seeded in fp32 (short MUFU latency) from quantities normalised by a power of two near |g|
+// (exact), so data of any scale neither underflows nor overflows the fp32 seed; c and 1/|g| are refined to
+// fp64 by a Newton step (unitary to ~5e-15).
+__device__ __forceinline__ void jacobi_rotation(double al, double be, c64 ga, double g2, double& cs, c64& se) {
+    const double sc = pow2_inv_sqrt_scale(g2);
+    const double g2n = g2 * sc * sc;  // [1, 4)
+    const float igf = rsqrtf(static_cast<float>(g2n));
+    const float zeta = static_cast<float>((be - al) * sc) * (0.5f * igf);
+    const float tf = copysignf(1.0f, zeta) / (fabsf(zeta) + sqrtf(fmaf(zeta, zeta, 1.0f)));
+    const double t = tf;
+    const double x1 = fma(t, t, 1.0);
+    double c = static_cast<double>(rsqrtf(static_cast<float>(x1)));
+    c = c * fma(-0.5 * x1, c * c, 1.5);
+    double ig = static_cast<double>(igf);
+    ig = ig * fma(-0.5 * g2n, ig * ig, 1.5);
+    ig *= sc;  // 1 / |g|
+    const double sn = c * t;
+    cs = c;
+    se = mk(sn * ga.re * ig, sn * ga.im * ig);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -100,6 +100,17 @@ __global__ void __launch_bounds__(kNT) k_jacobi_eig(const cplx<T>* __restrict__ 
         }
         __syncthreads();
     }
+    // power-of-two normalisation (exact): A = 2^-e (R + mu I) with max_c |R_cc| + mu in [1, 2) -- the column
+    // products below then stay inside the fp32 range for inputs of any scale; lambda is scaled back at the end
+    __shared__ double s_dmax;
+    if (threadIdx.x == 0) s_dmax = 0.0;
+    __syncthreads();
+    for (int c = threadIdx.x; c < m; c += kNT) {
+        const double v = fabs(static_cast<double>(Rf[static_cast<size_t>(c) * m + c].re)) + s_mu;
+        if (v > 0.0 && v < 1e300) atomicMax(reinterpret_cast<unsigned long long*>(&s_dmax), __double_as_longlong(v));
+    }
+    __syncthreads();
+    const double nsc = s_dmax > 0.0 ? pow2_inv_sqrt_scale(s_dmax * s_dmax) : 1.0;  // 2^-e
     const T mu = static_cast<T>(s_mu);
     // A[c][r] = R(r, c) = conj(R[c][r]) (row-major Hermitian R), padded with zeros
     for (int e = threadIdx.x; e < mp * mp; e += kNT) {
@@ -107,7 +118,7 @@ __global__ void __launch_bounds__(kNT) k_jacobi_eig(const cplx<T>* __restrict__ 
         cplx<T> v = mk<T>(0, 0);
         if (c < m && r < m) v = conj(Rf[static_cast<size_t>(c) * m + r]);
         if (c == r && c < m) v.re += mu;
-        A[static_cast<size_t>(c) * mp + r] = v;
+        A[static_cast<size_t>(c) * mp + r] = mk<T>(static_cast<T>(v.re * nsc), static_cast<T>(v.im * nsc));
     }
     __syncthreads();
 
@@ -187,7 +198,7 @@ __global__ void __launch_bounds__(kNT) k_jacobi_eig(const cplx<T>* __restrict__ 
         Bf[static_cast<size_t>(q) * m + r] = mk(a.re * inv, a.im * inv);
     }
     if (threadIdx.x < k) {
-        double lam = s_sig[s_sel[threadIdx.x]] - static_cast<double>(mu);
+        double lam = s_sig[s_sel[threadIdx.x]] / nsc - static_cast<double>(mu);
         if (lam < 0.0 && lam >= -1e-10) lam = 0.0;
         eig[static_cast<size_t>(f) * k + threadIdx.x] = lam;
     }

@@ -624,20 +624,13 @@ __device__ int block_hestenes(c64* a, int n, int* s_rot) {
                 ga = warp_sum_c(ga);
                 const double g2 = norm2(ga);
                 if (!(g2 > tol * tol * al * be) || g2 == 0.0) continue;
-                const float gf = sqrtf(static_cast<float>(g2));
-                const float zeta = static_cast<float>(be - al) / (2.0f * gf);
-                const float tf = (zeta >= 0.0f ? 1.0f : -1.0f) / (fabsf(zeta) + sqrtf(1.0f + zeta * zeta));
-                const double t = tf;
-                const double c = rsqrt(1.0 + t * t);
-                const double s = c * t;
-                double ig = static_cast<double>(rsqrtf(static_cast<float>(g2)));
-                ig = ig * (1.5 - 0.5 * g2 * ig * ig);  // Newton: 1/|g| to fp64
-                ig = ig * (1.5 - 0.5 * g2 * ig * ig);
-                const c64 e = mk(ga.re * ig, ga.im * ig);
+                double c;
+                c64 e;  // s e
+                jacobi_rotation(al, be, ga, g2, c, e);
                 for (int r = lane; r < n; r += 32) {
                     const c64 x = ai[r], y = aj[r];
-                    ai[r] = mk(c * x.re - s * (e.re * y.re + e.im * y.im), c * x.im - s * (e.re * y.im - e.im * y.re));
-                    aj[r] = mk(s * (e.re * x.re - e.im * x.im) + c * y.re, s * (e.re * x.im + e.im * x.re) + c * y.im);
+                    ai[r] = mk(c * x.re - (e.re * y.re + e.im * y.im), c * x.im - (e.re * y.im - e.im * y.re));
+                    aj[r] = mk((e.re * x.re - e.im * x.im) + c * y.re, (e.re * x.im + e.im * x.re) + c * y.im);
                 }
                 if (lane == 0) *s_rot = 1;
             }
@@ -987,6 +980,22 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
         }
     }
     __syncwarp();
+    // Y to unit scale by a power of two (exact): the Jacobi below then sees the same numbers for any input scale
+    // (X * 2^-20 .. X * 2^12); singular values -- and the eigenvalues s^2 -- are scaled back at the end, and
+    // the columns' directions (hence T) are unaffected.
+    double yscale2 = 1.0;  // 2^(2e): eigenvalue factor
+    {
+        double ymax = 0.0;
+        for (int e = lane; e < p * ld; e += 32) ymax = fmax(ymax, norm2(Ya[e]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ymax = fmax(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
+        if (ymax > 0.0 && ymax < 1e300) {
+            const double sc = pow2_inv_sqrt_scale(ymax);  // 2^-e, |Y|max 2^-e in [1, 2)
+            yscale2 = 1.0 / (sc * sc);
+            for (int e = lane; e < PC * ld; e += 32) Ya[e] = mk(Ya[e].re * sc, Ya[e].im * sc);
+        }
+    }
+    __syncwarp();
     const long long T1 = clock64();
     // one-sided Jacobi on Y's columns, in place in Ya. Lanes are assigned to column PAIRS: slot
     // = lane / LPP of the round-robin schedule (slot 0: (rnd, p-1); slot s: (rnd + s, rnd - s)
@@ -1105,18 +1114,9 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
             const bool rotate = act && (g2 > tol * tol * al * be) && g2 != 0.0;
             if (rotate) {
                 big |= g2 >= 1e-14 * al * be;
-                const float g2f = static_cast<float>(g2);
-                const float igf = rsqrtf(g2f);
-                const float zeta = static_cast<float>(be - al) * (0.5f * igf);
-                const float tf = copysignf(1.0f, zeta) / (fabsf(zeta) + sqrtf(fmaf(zeta, zeta, 1.0f)));
-                const double t = tf;
-                const double x1 = fma(t, t, 1.0);
-                double cs = static_cast<double>(rsqrtf(static_cast<float>(x1)));
-                cs = cs * fma(-0.5 * x1, cs * cs, 1.5);
-                double ig = static_cast<double>(igf);
-                ig = ig * fma(-0.5 * g2, ig * ig, 1.5);
-                const double sn = cs * t;
-                const c64 se = mk(sn * ga.re * ig, sn * ga.im * ig);  // s e
+                double cs;
+                c64 se;  // s e
+                jacobi_rotation(al, be, ga, g2, cs, se);
 #pragma unroll
                 for (int t2 = 0; t2 < RPL; ++t2) {
                     const c64 u = x[t2], v = y[t2];
@@ -1151,7 +1151,9 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
             s0 += norm2(cur[c * ld + r]);
             s1 += norm2(cur[c * ld + r + 1]);
         }
-        sig[c] = sqrt(s0 + s1);
+        const double sv = sqrt(s0 + s1);
+        sig[c] = sv <= 1e300 ? sv : -1.0;  // NaN / inf (corrupt input): ranked last, frame flagged below
+        if (!(sv <= 1e300)) atomicOr(&status[f], kFrameNoConv);
     }
     __syncwarp();
     if (lane < p) {
@@ -1181,12 +1183,12 @@ __global__ void __launch_bounds__(32 * WarpCfg<PC>::kWarps)
             Tm[kk * p + i] = mk(acc.re * inv, acc.im * inv);
         }
         double lam = sig[cc];
-        lam *= lam;  // eigenvalue of B' = Y Y^H
+        lam *= lam * yscale2;  // eigenvalue of B' = Y Y^H
         eig[static_cast<size_t>(f) * k + kk] = lam;
     }
     if (eig_next && lane == 0) {  // (K+1)-th Ritz value (exact method's gap estimate)
         const double sn = k < p ? sig[order[k]] : 0.0;
-        eig_next[f] = sn * sn;
+        eig_next[f] = sn * sn * yscale2;
     }
     __syncwarp();
     c64* Tf = Tout + static_cast<size_t>(f) * p * k;

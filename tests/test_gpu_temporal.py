@@ -54,14 +54,24 @@ def test_temporal_covariance_batch(fm, oracle, m, n):
         assert np.max(np.abs(got - got.conj().T)) <= 1e-6 * np.abs(ref).max()
 
 
-def test_temporal_covariance_batch_flags(fm):
+def test_temporal_covariance_batch_flags(fm, oracle):
+    """Out-of-fp16-range frames (x 1e5, x 2^-30) are recomputed with a power-of-two prescale (cov_tc.cu rescue
+    pass) and match the fp64 covariance; only frames beyond the complex64 range (2^+-50) are flagged RANGE."""
     import torch
     m, n = 32, 48
-    x, _, _ = fm.generate_frames(m, n, 2, 52, 0, 3)
+    x, _, _ = fm.generate_frames(m, n, 2, 52, 0, 5)
     x[1, 3, 5] = complex(np.nan, 0)
-    x[2] *= 1e5  # |x|^2 ~ 1e10 overflows the fp16 operand range
+    x[2] *= np.float32(1e5)      # |x| ~ 1e5 overflows the fp16 operand range unscaled
+    x[3] *= np.float32(2.0 ** -30)  # fp16 subnormal / zero unscaled
+    x[4] *= np.float32(2.0 ** 60)   # R would overflow complex64
     t, st = fm.temporal_covariance_batch(torch.from_numpy(x).cuda())
+    torch.cuda.synchronize()
     st = st.cpu().numpy()
-    assert st[0] == 0
+    t = t.cpu().numpy()
+    assert st[0] == 0 and st[2] == 0 and st[3] == 0
     assert st[1] & _capi.FRAME_NONFINITE
-    assert st[2] & _capi.FRAME_RANGE
+    assert st[4] & _capi.FRAME_RANGE
+    for f in (0, 2, 3):
+        ref = oracle.temporal_covariance(x[f].astype(np.complex128))
+        rel = np.linalg.norm(t[f].astype(np.complex128) - ref) / np.linalg.norm(ref)
+        assert rel < 2e-4, (f, rel)
