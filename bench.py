@@ -10,10 +10,13 @@ L2 flush is needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
 
-Multi-GPU (torchrun, one process per GPU): frames are sharded (rank r owns frames
-[r*B, (r+1)*B) of the stream, weak scaling); after each step the peak records are
-all-gathered over NCCL (the path's only collective). Timing: CUDA events on the launching
-stream, barrier + synchronize on both sides, max over ranks.
+Multi-GPU (one process per GPU; `--gpus N` launches the N ranks itself through torch.distributed.run when
+WORLD_SIZE is unset): --scaling strong (default) splits every global batch of B frames into
+contiguous ranges [g B/G, (g+1) B/G); --scaling weak gives every GPU B frames. Small shards keep several
+batches in flight (--depth, paper_1911_07434_b200/shard.py FrameStream). After each batch the peak
+records are all-gathered over NCCL (the path's only collective); at N > 1 a weak-scaling companion number is
+measured in the same run. Timing: CUDA events bracketing every plan stream, barrier + synchronize on both sides,
+max over ranks.
 """
 from __future__ import annotations
 
@@ -196,7 +199,7 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic (seeded BASELINE frame model, DESIGN.md §3)",
         "config": config_dict(args.config, cfgd, 1),
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port", "cpu_model": cpu_model(),
                          "sample": f"{per_step} frames per step (one per core) of {args.config}; oracle fp64 "
                                    f"restatement of the reference path (numpy/scipy LAPACK, 1 BLAS thread/worker)"},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -205,13 +208,18 @@ def run_reference(args):
     return 0
 
 
-def config_dict(name, cfgd, world):
+def config_dict(name, cfgd, world, mode="strong", per_gpu=None, depth=1):
+    per_gpu = cfgd["frames"] if per_gpu is None else per_gpu
+    gfr = cfgd["frames"] if mode == "strong" else cfgd["frames"] * world
+    xb = per_gpu * cfgd["m"] * cfgd["n"] * 8
+    l2 = ("inputs larger than L2 (X = %.2f GiB per GPU step)" % (xb / 2**30) if xb > 3 * 126 * 2**20 else
+          "X = %.0f MB per GPU step; consecutive steps cycle through >= 3 x L2 of distinct X copies" % (xb / 1e6))
     return {"workload": f"{name}: fast-MUSIC {cfgd['method']} M={cfgd['m']} N={cfgd['n']} K={cfgd['k']} "
                         f"p={cfgd['p']} t={cfgd['t']} L={cfgd['L']}",
-            "frames_per_gpu": cfgd["frames"], "global_frames_per_step": cfgd["frames"] * world,
-            "grid": "[-90, 90] deg", "l2": "inputs larger than L2 (X = %.2f GiB per GPU step)" %
-            (cfgd["frames"] * cfgd["m"] * cfgd["n"] * 8 / 2**30),
-            "parallelism": f"frames sharded over {world} GPU(s), NCCL all-gather of peak records"}
+            "frames_per_gpu": per_gpu, "global_frames_per_step": gfr, "grid": "[-90, 90] deg", "l2": l2,
+            "parallelism": (f"{mode} scaling: frames of each {gfr}-frame batch sharded over {world} GPU(s) "
+                            f"[g B/G, (g+1) B/G), NCCL all-gather of peak records" if mode == "strong" else
+                            f"weak scaling: {per_gpu} frames per GPU, NCCL all-gather of peak records")}
 
 
 # ----------------------------------------------------------------------------- ours
@@ -221,7 +229,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_1911_07434_b200 as fm
-    from paper_1911_07434_b200.shard import gather_records, pack_records, shard_range
+    from paper_1911_07434_b200.shard import FrameStream, shard_range, unshard_records
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -232,16 +240,18 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
 
     cfgd = CONFIGS[args.config]
-    B, M, N, K, P, L = cfgd["frames"], cfgd["m"], cfgd["n"], cfgd["k"], cfgd["p"], cfgd["L"]
     if args.frames:
-        B = args.frames
-        cfgd = dict(cfgd, frames=B)
-    f0, _ = shard_range(rank, world, B)
+        cfgd = dict(cfgd, frames=args.frames)
+    B, M, N, K, P, L = cfgd["frames"], cfgd["m"], cfgd["n"], cfgd["k"], cfgd["p"], cfgd["L"]
+    mode = args.scaling
+    f0, n = shard_range(rank, world, B, mode)
+    nmax = max(shard_range(g, world, B, mode)[1] for g in range(world))
+    gfr = B if mode == "strong" else B * world  # global frames per step
     # synthetic input for this rank's frames, generated on the host (pinned), staged once
-    xh = torch.empty((B, M, N, 2), dtype=torch.float32, pin_memory=True)
-    xnp = xh.numpy().view(np.complex64).reshape(B, M, N)
-    fm.generate_frames(M, N, K, cfgd["seed"], f0, B, out=xnp, **cfgd["scene"])
-    fseeds = np.array([fm.derive(cfgd["seed"], f0 + f) for f in range(B)], np.uint64)
+    xh = torch.empty((n, M, N, 2), dtype=torch.float32, pin_memory=True)
+    xnp = xh.numpy().view(np.complex64).reshape(n, M, N)
+    fm.generate_frames(M, N, K, cfgd["seed"], f0, n, out=xnp, **cfgd["scene"])
+    fseeds = np.array([fm.derive(cfgd["seed"], f0 + f) for f in range(n)], np.uint64)
     tag = 4 if cfgd["method"] == "fast2" else 3
     dseeds = np.array([fm.derive(int(s), tag) for s in fseeds], np.uint64)
     omega = idx = None
@@ -252,140 +262,200 @@ def run_ours(args):
     elif cfgd["method"] == "fast1_norm2":  # uniforms of the weighted sampler travel in the omega slot
         omega = torch.from_numpy(fm.draw_uniforms_batch(dseeds, M)).to(dev)
     xd = xh.to(dev)
-    plan = fm.BatchPlan(M, N, K, cfgd["method"], p=P, t=cfgd["t"], grid_size=L, max_frames=B, device=local)
-    # same rule as the library's automatic choice (capi.cu auto_subbatches): one sub-batch on the p <= 16 plane path
-    plane_gram = cfgd["method"] in ("fast2", "fast1_norm2") and M <= 256 and P <= 16
-    nsub = args.subbatches if args.subbatches > 0 else (1 if plane_gram or B < 512 else 2)
-    plan.set_concurrency(nsub)
-    fsub = (B + nsub - 1) // nsub  # frames in sub-batch 0 (the one the stage events time)
-    out = plan.outputs(B, spectrum=True)
-    stream = torch.cuda.Stream(device=dev)
-    gather = None
-    rec = torch.empty((B, K + 2), dtype=torch.int32, device=dev)
-    if world > 1:
-        gather = torch.empty((world, B, K + 2), dtype=torch.int32, device=dev)
+    # batches in flight: small shards leave too little work per kernel to hide ramps and tails
+    depth = args.depth if args.depth > 0 else (1 if n >= 512 else 2)
 
-    def step():
-        plan.run(B, xd, omega, idx, out, stream=stream)
-        if world > 1:
-            with torch.cuda.stream(stream):
-                pack_records(out["peak_cells"], out["peak_count"], out["status"], out=rec)
-                gather_records(rec, world, out=gather)
+    def make_plan(i):
+        p = fm.BatchPlan(M, N, K, cfgd["method"], p=P, t=cfgd["t"], grid_size=L, max_frames=n, device=local)
+        if args.subbatches > 0:
+            p.set_concurrency(args.subbatches)
+        return p
 
-    for _ in range(max(3, args.warmup)):
-        step()
+    streams = [torch.cuda.Stream(device=dev) for _ in range(depth)]
+    fs = FrameStream(make_plan, n, nmax, K, world, depth, streams, dev, spectrum=True)
+    plan0 = fs.plans[0]
+    main_s = torch.cuda.current_stream(dev)
+
+    # L2 hygiene: steps cycle through enough copies of X that every step reads its input from HBM (> 3x L2 in all)
+    nbuf = max(depth, -(-3 * 126 * 2**20 // (n * M * N * 8)))
+    xs = [xd] + [xd.clone() for _ in range(nbuf - 1)]
+    ctr = [0]
+
+    def run_steps(count):
+        gathered = None
+        for _ in range(count):
+            _, gathered = fs.step(xs[ctr[0] % nbuf], omega, idx)
+            ctr[0] += 1
+        return gathered
+
+    run_steps(max(3, args.warmup) + depth)
     torch.cuda.synchronize()
-    status = out["status"].cpu().numpy()
-    counts = out["peak_count"].cpu().numpy()
+    out0 = fs.output(0)
+    status = out0["status"].cpu().numpy()
+    counts = out0["peak_count"].cpu().numpy()
 
-    # ---------------- timed region
-    plan.set_profiling(True)
+    # ---------------- timed region: barrier + synchronize, events on the main stream bracketing every plan stream
+    plan0.set_profiling(True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
+        e0.record(main_s)
+        for s in streams:
+            s.wait_event(e0)
+        gathered = run_steps(args.steps)
+        for s in streams:
+            ev = torch.cuda.Event()
+            ev.record(s)
+            main_s.wait_event(ev)
+        e1.record(main_s)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    stage_sum, runs = plan.stage_times_ms()
-    plan.set_profiling(False)
+    stage_sum, runs = plan0.stage_times_ms()
+    plan0.set_profiling(False)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = world * B * args.steps / (ms_max / 1e3)
+    value = gfr * args.steps / (ms_max / 1e3)
+    recs = unshard_records(gathered, world, B, mode) if world > 1 else None
 
-    # ---------------- e2e through the reference-facing host-buffer C-ABI call
+    # ---------------- weak-scaling companion (N > 1, strong default): B frames per rank, same timing rules
+    weak = None
+    if world > 1 and mode == "strong" and not args.no_weak:
+        xw = torch.empty((B, M, N, 2), dtype=torch.float32, device=dev)
+        xw.view(-1)[: xd.numel()].copy_(xd.view(-1))
+        reps = (B + n - 1) // n
+        for r in range(1, reps):
+            lo = r * n
+            hi = min(B, lo + n)
+            xw[lo:hi].copy_(xd[: hi - lo])
+        omw = omega.repeat(reps, 1, 1)[:B].contiguous() if omega is not None else None
+        ixw = idx.repeat(reps, 1)[:B].contiguous() if idx is not None else None
+        fw = FrameStream(lambda i: fm.BatchPlan(M, N, K, cfgd["method"], p=P, t=cfgd["t"], grid_size=L,
+                                                max_frames=B, device=local), B, B, K, world, 1, [streams[0]], dev)
+        for _ in range(3):
+            fw.step(xw, omw, ixw)
+        dist.barrier()
+        torch.cuda.synchronize()
+        w0 = torch.cuda.Event(enable_timing=True)
+        w1 = torch.cuda.Event(enable_timing=True)
+        w0.record(streams[0])
+        for _ in range(args.steps):
+            fw.step(xw, omw, ixw)
+        w1.record(streams[0])
+        torch.cuda.synchronize()
+        dist.barrier()
+        tw = torch.tensor([w0.elapsed_time(w1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+        weak = {"value": world * B * args.steps / (float(tw.item()) / 1e3), "unit": "frames/s",
+                "frames_per_gpu": B, "global_frames_per_step": world * B, "ms_per_step": float(tw.item()) / args.steps}
+        fw.close()
+        del xw
+
+    # ---------------- e2e through the reference-facing host-buffer C-ABI call (this rank's shard)
     e2e = None
     if not args.no_e2e:
         draw = None if cfgd["method"] == "exact" else dseeds
-        res = plan.estimate_host(xnp, draw)  # warm-up (allocates staging)
+        res = plan0.estimate_host(xnp, draw)  # warm-up (allocates staging)
         e2e_steps = max(1, min(args.e2e_steps, args.steps))
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            res = plan.estimate_host(xnp, draw)
+            res = plan0.estimate_host(xnp, draw)
         el = time.perf_counter() - t0
         te = torch.tensor([el], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        h2d = B * M * N * 8 + (B * M * P * 4 if cfgd["method"] == "fast2" else B * P * 4 if cfgd["method"] == "fast1"
-                               else B * M * 4 if cfgd["method"] == "fast1_norm2" else 0)
-        d2h = B * K * 4 + B * 4 + B * 4
-        e2e = {"value": world * B * e2e_steps / float(te.item()), "unit": "frames/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "steps": e2e_steps, "path": "fm_estimate_batch_host (pinned host X, "
-                                                                  "host draws of Omega, redraw check, D2H peaks)"}
-        same = np.array_equal(res["peak_cells"], out["peak_cells"].cpu().numpy())
+        h2d = n * M * N * 8 + (n * M * P * 4 if cfgd["method"] == "fast2" else n * P * 4 if cfgd["method"] == "fast1"
+                               else n * M * 4 if cfgd["method"] == "fast1_norm2" else 0)
+        d2h = n * K * 4 + n * 4 + n * 4
+        e2e = {"value": gfr * e2e_steps / float(te.item()), "unit": "frames/s", "h2d_bytes_per_step": h2d * world,
+               "d2h_bytes_per_step": d2h * world, "steps": e2e_steps,
+               "path": "fm_estimate_batch_host (pinned host X, host draws of Omega, redraw check, D2H peaks)"}
+        same = np.array_equal(res["peak_cells"], out0["peak_cells"].cpu().numpy())
         e2e["peaks_match_device_run"] = bool(same)
 
     if rank != 0:
+        fs.close()
         if world > 1:
             dist.destroy_process_group()
         return 0
 
-    # ---------------- roofline of the dominant kernel, timed alone: one sub-batch (the whole
-    # batch in one launch per kernel), CUDA events on the plan's launch stream around each stage
+    # ---------------- roofline of the dominant kernel, timed alone: one sub-batch (the whole shard in one launch
+    # per kernel), CUDA events on the plan's launch stream around each stage
     hbm, bf16, bf16_sus, src = load_peaks()
     alg = algorithmic(cfgd)
-    stage_ms = {k: v / max(runs, 1) for k, v in stage_sum.items()}  # sub-batch 0 (fsub frames), in-step
-    plan.set_concurrency(1)
-    plan.set_profiling(True)
+    stage_ms = {k: v / max(runs, 1) for k, v in stage_sum.items()}
+    plan0.set_concurrency(1)
+    plan0.set_profiling(True)
+    out_r = fs.output(0)
     for _ in range(args.roof_steps):
-        plan.run(B, xd, omega, idx, out, stream=stream)
+        plan0.run(n, xd, omega, idx, out_r, stream=streams[0])
     torch.cuda.synchronize()
-    alone_sum, alone_runs = plan.stage_times_ms()
-    plan.set_profiling(False)
-    plan.set_concurrency(nsub)
-    alone_ms = {k: v / max(alone_runs, 1) for k, v in alone_sum.items()}  # all B frames, one launch per kernel
+    alone_sum, alone_runs = plan0.stage_times_ms()
+    plan0.set_profiling(False)
+    alone_ms = {k: v / max(alone_runs, 1) for k, v in alone_sum.items()}  # all n frames, one launch per kernel
     prof = {}
     try:
         with open(os.path.join(ROOT, "profiles", f"ncu_summary_{args.config}.json")) as f:
             prof = json.load(f)
     except Exception:
         pass
-    bytes_launch = B * (8.0 * M * N + 8.0 * M * M)  # algorithmic: X read once + R (complex64) written once
-    achieved = bytes_launch / (alone_ms["covariance"] / 1e3) / 1e9
+    x_bytes = n * 8.0 * M * N                  # SURVEY §8(d) algorithmic bytes of the covariance: X read once
+    r_bytes = n * 8.0 * M * M                  # + R written once (complex64, or its two fp16 planes)
+    cov_ms = alone_ms["covariance"]
     cov_prof = prof.get("cov_tc_kernel", {})
-    roof = {"bound": "hbm", "kernel": "fmk::cov::cov_tc_kernel (tcgen05 cta_group::2 + TMA)", "achieved": achieved,
-            "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "peak_source": src,
-            "bytes_per_launch": bytes_launch, "launch_ms": alone_ms["covariance"],
-            "share_of_step": alone_ms["covariance"] / sum(alone_ms.values()),
-            "traffic": (cov_prof["dram_bytes"] * B / cov_prof["frames"]) if "dram_bytes" in cov_prof else None,
+    roof = {"bound": "hbm", "kernel": "fmk::cov::cov_tc_kernel (tcgen05 cta_group::2 + TMA)",
+            "achieved": x_bytes / (cov_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": x_bytes / (cov_ms / 1e3) / 1e9 / hbm, "peak_source": src,
+            "bytes_def": "SURVEY §8(d): X read (8 M N per frame) only",
+            "bytes_per_launch": x_bytes, "launch_ms": cov_ms,
+            "frac_incl_r_write": (x_bytes + r_bytes) / (cov_ms / 1e3) / 1e9 / hbm,
+            "share_of_step": cov_ms / sum(alone_ms.values()),
+            "traffic": (cov_prof["dram_bytes"] * n / cov_prof["frames"]) if "dram_bytes" in cov_prof else None,
             "traffic_source": cov_prof.get("source")}
+    step_prof = prof.get("step", {})
     p_tf32 = bf16 / 2.0
-    t_roof_ms = max(B * alg["q_frame"] / (hbm * 1e9), B * alg["w_frame"] / (p_tf32 * 1e12)) * 1e3
+    t_roof_ms = max(gfr * alg["q_frame"] / world / (hbm * 1e9), gfr * alg["w_frame"] / world / (p_tf32 * 1e12)) * 1e3
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "c64",
+        "scaling": mode, "vs_baseline": None, "dtype": "c64",
         "data": "synthetic (seeded BASELINE frame model, DESIGN.md §3)",
-        "config": config_dict(args.config, cfgd, world),
+        "config": config_dict(args.config, cfgd, world, mode, n, depth),
         "roofline": roof,
         "roofline_path": {"t_roof_ms_per_step": t_roof_ms, "t_meas_ms_per_step": ms_max / args.steps,
                           "frac": t_roof_ms / (ms_max / args.steps),
-                          "def": "SURVEY.md §8d: max(B*Q/HBM, B*W/P_TF32), P_TF32 = measured bf16/2, 1xTF32 strict"},
+                          "def": "SURVEY.md §8d: max(B*Q/HBM, B*W/P_TF32) per GPU, P_TF32 = measured bf16/2, "
+                                 "1xTF32 strict",
+                          "dram_bytes_per_frame_ncu": step_prof.get("dram_bytes_per_frame"),
+                          "algorithmic_bytes_per_frame": alg["q_frame"],
+                          "dram_over_algorithmic": (step_prof["dram_bytes_per_frame"] / alg["q_frame"])
+                          if "dram_bytes_per_frame" in step_prof else None,
+                          "dram_source": step_prof.get("source")},
         "stages_ms_per_step": stage_ms,
-        "stages_note": f"CUDA-event durations of sub-batch 0 ({fsub} of {B} frames); {nsub} sub-batches run "
-                       f"concurrently on plan-owned streams",
+        "stages_note": f"CUDA-event durations in plan 0's stream ({n} frames per batch, {depth} batch(es) in flight)",
         "stages_alone_ms": alone_ms,
-        "stages_alone_note": f"all {B} frames in one launch per kernel (concurrency 1), {args.roof_steps} runs",
-        "subbatches": nsub,
-        "gpu_launches": args.steps * plan.launches_per_batch() * nsub,
+        "stages_alone_note": f"all {n} frames in one launch per kernel (concurrency 1), {args.roof_steps} runs",
+        "batches_in_flight": depth,
+        "gpu_launches": args.steps * plan0.launches_per_batch(),
         "clocks": clk.summary(),
         "e2e": e2e,
         "frames_ok": int((status == 0).sum()), "frames_full_peaks": int((counts == K).sum()),
     }
+    if weak is not None:
+        line["weak_scaling"] = weak
+    if recs is not None:
+        line["gathered_records"] = {"frames": int(recs.shape[0]), "ok": int((recs[:, K + 1] == 0).sum().item())}
     if world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        ns = min(B, max(cores, args.cpu_frames))
+        ns = min(n, max(cores, args.cpu_frames))
         frames = list(range(ns))
         import multiprocessing as mp
         pool = mp.get_context("fork").Pool(cores, initializer=_worker_init, initargs=(args.config,))
@@ -393,20 +463,52 @@ def run_ours(args):
         wall, res = cpu_reference_run(args.config, xnp[:ns], frames, cores, pool)
         pool.close()
         pool.join()
-        gp = out["peak_cells"].cpu().numpy()
-        gs = out["spectrum"].cpu().numpy()
+        gp = out0["peak_cells"].cpu().numpy()
+        gs = out0["spectrum"].cpu().numpy()
         from oracle import fastmusic_oracle as O
         same = sum(1 for f, cells, spec, _ in res if list(gp[f][:len(cells)]) == cells)
         dbs = [O.spectrum_db_error(gs[f].astype("float64"), spec.astype("float64")) for f, _, spec, _ in res]
         line["cpu_baseline"] = {"value": ns / wall, "unit": "frames/s", "cores": cores, "kind": "port",
+                                "cpu_model": cpu_model(),
                                 "sample": f"first {ns} frames of the {args.config} batch, oracle fp64 restatement "
                                           f"(numpy/scipy), one frame per worker process, pool warmed on "
                                           f"{min(cores, ns)} frames first"}
         line["parity_sample"] = {"frames": ns, "peaks_identical": same, "max_db_err_vs_port": max(dbs)}
     print(json.dumps(line), flush=True)
+    fs.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` without torchrun: launch N ranks (one process per GPU) through torch.distributed.run."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but only {have} CUDA device(s) visible"}), flush=True)
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -423,9 +525,19 @@ def main():
     ap.add_argument("--cpu-frames", type=int, default=64)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: each global batch's frames split over the GPUs (SURVEY §8e); weak: a batch per GPU")
+    ap.add_argument("--depth", type=int, default=0, help="batches in flight per GPU (0 = auto)")
+    ap.add_argument("--no-weak", action="store_true", help="skip the weak-scaling companion measurement (N > 1)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None and args.gpus > 1:
+        return spawn_ranks(args)
+    if ws is not None and int(ws) != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={ws}"}), flush=True)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

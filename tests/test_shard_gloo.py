@@ -1,5 +1,6 @@
-"""N>1 path on CPU: world_size-2 gloo process group exercising the frame sharding and the
-peak-record all-gather used by bench.py's multi-GPU run."""
+"""N>1 path on CPU: world_size-2 gloo process groups running bench.py's multi-GPU step logic
+(paper_1911_07434_b200/shard.py: strong / weak frame sharding, FrameStream with batches in flight, peak-record
+pack -> all-gather -> unshard) with a stub plan in place of the CUDA pipeline."""
 import os
 import socket
 
@@ -18,31 +19,54 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, frames, k, q):
+class StubPlan:
+    """Stands in for BatchPlan: frame f of the shard gets cells (gid * 10 + j), count K, status gid % 3, where gid is
+    the global frame index carried in x[f, 0] (plus 1000 * the batch counter so in-flight batches differ)."""
+
+    def __init__(self, k):
+        self.k = k
+
+    def outputs(self, frames, spectrum=False):
+        return {"peak_cells": torch.empty((frames, self.k), dtype=torch.int32),
+                "peak_count": torch.empty((frames,), dtype=torch.int32),
+                "status": torch.empty((frames,), dtype=torch.int32)}
+
+    def run(self, frames, x, omega, indices, out, stream=None):
+        gid = x[:frames, 0].to(torch.int32)
+        out["peak_cells"].copy_(gid[:, None] * 10 + torch.arange(self.k, dtype=torch.int32)[None, :])
+        out["peak_count"].fill_(self.k)
+        out["status"].copy_(gid % 3)
+
+
+def _worker(rank, world, port, total, k, mode, depth, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1911_07434_b200 import derive
-        from paper_1911_07434_b200.shard import gather_records, pack_records, shard_range
-        f0, nf = shard_range(rank, world, frames)
+        from paper_1911_07434_b200.shard import FrameStream, shard_range, unshard_records
+        f0, n = shard_range(rank, world, total, mode)
+        nmax = max(shard_range(g, world, total, mode)[1] for g in range(world))
+        fs = FrameStream(lambda i: StubPlan(k), n, nmax, k, world, depth)
+        got = []
+        for b in range(3):  # three batches through `depth` plans round-robin
+            x = torch.tensor([[1000 * b + f0 + f] for f in range(n)], dtype=torch.float64)
+            _, g = fs.step(x)
+            got.append(unshard_records(g, world, total, mode).numpy().copy())
         # per-frame draw seeds depend only on the global frame index (shard-invariant)
-        seeds = [derive(derive(2, f0 + f), 4) for f in range(nf)]
-        cells = torch.tensor([[(f0 + f) * 10 + j for j in range(k)] for f in range(nf)], dtype=torch.int32)
-        count = torch.full((nf,), k, dtype=torch.int32)
-        status = torch.tensor([(f0 + f) % 3 for f in range(nf)], dtype=torch.int32)
-        g = gather_records(pack_records(cells, count, status), world)
-        q.put((rank, g.numpy().copy(), seeds))
+        seeds = [derive(derive(2, f0 + f), 4) for f in range(n)]
+        q.put((rank, got, seeds, f0, n))
     finally:
         dist.destroy_process_group()
 
 
-def test_sharded_gather_world2():
-    world, frames, k = 2, 5, 3
+@pytest.mark.parametrize("mode,total,depth", [("strong", 5, 2), ("strong", 8, 1), ("weak", 3, 2)])
+def test_frame_stream_world2(mode, total, depth):
+    world, k = 2, 3
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, frames, k, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, total, k, mode, depth, q)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=120) for _ in range(world)]
@@ -50,15 +74,39 @@ def test_sharded_gather_world2():
         p.join(timeout=60)
         assert p.exitcode == 0
     from paper_1911_07434_b200 import derive
-    expect = np.array([[f * 10 + j for j in range(k)] + [k, f % 3] for f in range(world * frames)], np.int32)
-    for rank, g, seeds in out:
-        assert g.shape == (world, frames, k + 2)
-        assert np.array_equal(g.reshape(-1, k + 2), expect)
-        assert seeds == [derive(derive(2, rank * frames + f), 4) for f in range(frames)]
+    gframes = total if mode == "strong" else total * world
+    for rank, got, seeds, f0, n in out:
+        assert len(got) == 3
+        for b, recs in enumerate(got):
+            gid = np.arange(gframes) + 1000 * b
+            expect = np.concatenate([gid[:, None] * 10 + np.arange(k)[None, :], np.full((gframes, 1), k),
+                                     (gid % 3)[:, None]], 1).astype(np.int32)
+            assert recs.shape == (gframes, k + 2)
+            assert np.array_equal(recs, expect), (rank, b)
+        assert seeds == [derive(derive(2, f0 + f), 4) for f in range(n)]
+    # strong: the shards tile the batch contiguously
+    if mode == "strong":
+        spans = sorted((f0, n) for _, _, _, f0, n in out)
+        assert spans[0][0] == 0 and spans[0][0] + spans[0][1] == spans[1][0] and sum(s[1] for s in spans) == total
 
 
 def test_shard_range_validation():
     from paper_1911_07434_b200.shard import shard_range
-    assert shard_range(3, 8, 128) == (384, 128)
+    assert shard_range(3, 8, 1024) == (384, 128)
+    assert shard_range(3, 8, 128, "weak") == (384, 128)
+    assert [shard_range(g, 3, 10) for g in range(3)] == [(0, 4), (4, 3), (7, 3)]
     with pytest.raises(ValueError):
         shard_range(8, 8, 1)
+    with pytest.raises(ValueError):
+        shard_range(0, 2, 4, "diagonal")
+
+
+def test_bench_refuses_mismatched_world(tmp_path):
+    """bench.py --gpus N under a launcher with WORLD_SIZE != N exits non-zero instead of silently running N = 1."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl", "reference"],
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2 and "WORLD_SIZE" in r.stdout
