@@ -263,12 +263,18 @@ def run_ours(args):
         omega = torch.from_numpy(fm.draw_uniforms_batch(dseeds, M)).to(dev)
     xd = xh.to(dev)
     # batches in flight: small shards leave too little work per kernel to hide ramps and tails
-    depth = args.depth if args.depth > 0 else (1 if n >= 512 else 2)
+    # (measured at N = 1, c2, tools/bench_sweep.sh: 1024 frames 0.954 / 1.075 / 1.105 M frames/s at depth 1 / 2 / 3;
+    # 128-frame shards 0.37 / 0.54 / 0.65 / 0.71 M at depth 1 .. 4)
+    depth = args.depth if args.depth > 0 else (3 if n >= 512 else 4 if n >= 256 else 6)
+
+    # CUDA-graph replay of whole batches: small shards are otherwise bound by the host's launch rate
+    graphs = args.graphs == "on" or (args.graphs == "auto" and depth <= 2)
 
     def make_plan(i):
         p = fm.BatchPlan(M, N, K, cfgd["method"], p=P, t=cfgd["t"], grid_size=L, max_frames=n, device=local)
         if args.subbatches > 0:
             p.set_concurrency(args.subbatches)
+        p.set_graphs(graphs)
         return p
 
     streams = [torch.cuda.Stream(device=dev) for _ in range(depth)]
@@ -295,7 +301,8 @@ def run_ours(args):
     counts = out0["peak_count"].cpu().numpy()
 
     # ---------------- timed region: barrier + synchronize, events on the main stream bracketing every plan stream
-    plan0.set_profiling(True)
+    # (per-stage events only without graphs: a profiled batch is enqueued kernel by kernel)
+    plan0.set_profiling(not graphs)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -439,8 +446,10 @@ def run_ours(args):
                           "dram_over_algorithmic": (step_prof["dram_bytes_per_frame"] / alg["q_frame"])
                           if "dram_bytes_per_frame" in step_prof else None,
                           "dram_source": step_prof.get("source")},
-        "stages_ms_per_step": stage_ms,
-        "stages_note": f"CUDA-event durations in plan 0's stream ({n} frames per batch, {depth} batch(es) in flight)",
+        "stages_ms_per_step": stage_ms if not graphs else None,
+        "stages_note": f"CUDA-event durations in plan 0's stream ({n} frames per batch, {depth} batch(es) in flight)"
+                       if not graphs else "not recorded in-step: batches replayed from CUDA graphs",
+        "cuda_graphs": graphs,
         "stages_alone_ms": alone_ms,
         "stages_alone_note": f"all {n} frames in one launch per kernel (concurrency 1), {args.roof_steps} runs",
         "batches_in_flight": depth,
@@ -528,6 +537,8 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: each global batch's frames split over the GPUs (SURVEY §8e); weak: a batch per GPU")
     ap.add_argument("--depth", type=int, default=0, help="batches in flight per GPU (0 = auto)")
+    ap.add_argument("--graphs", default="auto", choices=["auto", "on", "off"],
+                    help="replay batches from CUDA graphs (auto: when at most 2 batches are in flight)")
     ap.add_argument("--no-weak", action="store_true", help="skip the weak-scaling companion measurement (N > 1)")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -147,6 +147,10 @@ fm_status fm_plan_stage_times(fm_plan plan, float* ms4, int32_t* runs);
 /* Split each fm_run_batch into `subbatches` (<= 16) frame ranges run concurrently on plan-owned streams forked
  * from / joined into the caller's stream (0 = automatic: 1 on the p <= 16 plane path, else 2 when frames >= 512). */
 fm_status fm_plan_set_concurrency(fm_plan plan, int32_t subbatches);
+/* CUDA-graph replay (on != 0): the first fm_run_batch with a given (frames, io) on a non-NULL stream is captured
+ * into a graph and every later identical call replays it with one launch (small batches are otherwise bound by
+ * the host's launch rate). Not used while profiling. Captured graphs are dropped by fm_plan_set_concurrency. */
+fm_status fm_plan_set_graphs(fm_plan plan, int32_t on);
 /* Number of kernel launches one fm_run_batch enqueues (per sub-batch). */
 int32_t fm_plan_launches_per_batch(fm_plan plan);
 

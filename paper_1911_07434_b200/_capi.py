@@ -23,7 +23,7 @@ EXPORTED = [
     "fm_rng_derive", "fm_rng_normals", "fm_sample_without_replacement", "fm_gaussian_matrix_real",
     "fm_draw_omega_batch", "fm_draw_indices_batch", "fm_draw_uniforms_batch", "fm_generate_frames",
     "fm_plan_create", "fm_plan_destroy", "fm_plan_workspace_bytes", "fm_run_batch", "fm_rerun_frames",
-    "fm_plan_launches_per_batch", "fm_plan_set_profiling", "fm_plan_stage_times", "fm_plan_set_concurrency", "fm_estimate_batch_host",
+    "fm_plan_launches_per_batch", "fm_plan_set_profiling", "fm_plan_stage_times", "fm_plan_set_concurrency", "fm_plan_set_graphs", "fm_estimate_batch_host",
     "fm_z_spatial_covariance", "fm_z_exact_signal_subspace", "fm_z_fast_music_1", "fm_z_fast_music_2",
     "fm_z_music_spectrum", "fm_z_extract_peaks",
     "fm_z_temporal_covariance", "fm_temporal_covariance_batch", "fm_z_block_lanczos_subspace",
@@ -88,6 +88,7 @@ def _load():
         "fm_plan_set_profiling": (i32, [vp, i32]),
         "fm_plan_stage_times": (i32, [vp, vp, vp]),
         "fm_plan_set_concurrency": (i32, [vp, i32]),
+        "fm_plan_set_graphs": (i32, [vp, i32]),
         "fm_estimate_batch_host": (i32, [vp, i64, vp, vp, vp, vp]),
         "fm_z_spatial_covariance": (i32, [i64, i64, vp, vp]),
         "fm_z_exact_signal_subspace": (i32, [i64, vp, i64, vp, vp, vp]),

@@ -459,6 +459,10 @@ class BatchPlan:
         """Run each batch as `subbatches` concurrent frame ranges (0 = automatic)."""
         _check(LIB.fm_plan_set_concurrency(self.handle, subbatches))
 
+    def set_graphs(self, on: bool = True):
+        """Replay identical batches (same frames and buffers) from a captured CUDA graph (one launch per batch)."""
+        _check(LIB.fm_plan_set_graphs(self.handle, 1 if on else 0))
+
     def launches_per_batch(self) -> int:
         return int(LIB.fm_plan_launches_per_batch(self.handle))
 

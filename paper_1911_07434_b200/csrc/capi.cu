@@ -577,6 +577,15 @@ struct fm_plan_s {
     std::vector<cudaStream_t> sub;
     std::vector<cudaEvent_t> sub_ev;  // [0] fork, [1..] joins
     std::vector<void*> allocs;
+    // CUDA-graph replay of whole batches (fm_plan_set_graphs): one graph per (frames, io) seen, replayed with a
+    // single launch -- the enqueue cost of a small batch (~40 launches) would otherwise exceed its GPU time
+    struct GraphEntry {
+        int64_t frames;
+        fm_batch_io io;
+        cudaGraphExec_t exec;
+    };
+    bool use_graphs = false;
+    std::vector<GraphEntry> graphs;
 
     template <typename T>
     cudaError_t get(T** p, size_t count) {
@@ -605,6 +614,8 @@ struct fm_plan_s {
             if (q) cudaStreamDestroy(q);
         for (cudaEvent_t e : copy_ev)
             if (e) cudaEventDestroy(e);
+        for (auto& g : graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
         if (copy_s) cudaStreamDestroy(copy_s);
         if (omega_pinned) cudaFreeHost(omega_pinned);
         if (status_pinned) cudaFreeHost(status_pinned);
@@ -1169,11 +1180,45 @@ extern "C" fm_status fm_run_batch(fm_plan pl, int64_t frames, const fm_batch_io*
     fm_status st = check_io(pl, frames, io);
     if (st != FM_OK) return st;
     FM_CUDA_OK(cudaSetDevice(pl->device));
-    return run_batch_at(pl, 0, frames, io, static_cast<cudaStream_t>(stream));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!pl->use_graphs || !s || pl->profiling || debug_sync()) return run_batch_at(pl, 0, frames, io, s);
+    for (auto& g : pl->graphs)
+        if (g.frames == frames && std::memcmp(&g.io, io, sizeof(fm_batch_io)) == 0) {
+            FM_CUDA_OK(cudaGraphLaunch(g.exec, s));
+            return FM_OK;
+        }
+    // first batch with these buffers: capture the whole enqueue sequence (sub-batch forks included) once
+    FM_CUDA_OK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    st = run_batch_at(pl, 0, frames, io, s);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+    if (st != FM_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+    }
+    FM_CUDA_OK(ce);
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    FM_CUDA_OK(ie);
+    pl->graphs.push_back({frames, *io, exec});
+    FM_CUDA_OK(cudaGraphLaunch(exec, s));
+    return FM_OK;
+}
+
+extern "C" fm_status fm_plan_set_graphs(fm_plan plan, int32_t on) {
+    if (!plan) return fail(FM_EINVAL, "fm_plan_set_graphs: null plan");
+    plan->use_graphs = on != 0;
+    return FM_OK;
 }
 
 extern "C" fm_status fm_plan_set_concurrency(fm_plan plan, int32_t subbatches) {
     if (!plan || subbatches < 0) return fail(FM_EINVAL, "fm_plan_set_concurrency: bad arguments");
+    if (plan->nsub != subbatches) {  // captured graphs hold the old split
+        for (auto& g : plan->graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+        plan->graphs.clear();
+    }
     plan->nsub = subbatches;
     return FM_OK;
 }
