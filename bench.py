@@ -271,7 +271,8 @@ def run_ours(args):
     graphs = args.graphs == "on" or (args.graphs == "auto" and depth <= 2)
 
     def make_plan(i):
-        p = fm.BatchPlan(M, N, K, cfgd["method"], p=P, t=cfgd["t"], grid_size=L, max_frames=n, device=local)
+        p = fm.BatchPlan(M, N, K, cfgd["method"], p=P, t=cfgd["t"], grid_size=L, max_frames=n, device=local,
+                         exact_jacobi=args.exact_jacobi)
         if args.subbatches > 0:
             p.set_concurrency(args.subbatches)
         p.set_graphs(graphs)
@@ -450,6 +451,8 @@ def run_ours(args):
         "stages_note": f"CUDA-event durations in plan 0's stream ({n} frames per batch, {depth} batch(es) in flight)"
                        if not graphs else "not recorded in-step: batches replayed from CUDA graphs",
         "cuda_graphs": graphs,
+        "exact_solver": ("jacobi (every frame)" if args.exact_jacobi else "certified subspace iteration + Jacobi for "
+                         "uncertified frames") if cfgd["method"] == "exact" else None,
         "stages_alone_ms": alone_ms,
         "stages_alone_note": f"all {n} frames in one launch per kernel (concurrency 1), {args.roof_steps} runs",
         "batches_in_flight": depth,
@@ -537,6 +540,8 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: each global batch's frames split over the GPUs (SURVEY §8e); weak: a batch per GPU")
     ap.add_argument("--depth", type=int, default=0, help="batches in flight per GPU (0 = auto)")
+    ap.add_argument("--exact-jacobi", action="store_true",
+                    help="exact method (c5): the full Jacobi eigensolver on every frame (no certified iteration)")
     ap.add_argument("--graphs", default="auto", choices=["auto", "on", "off"],
                     help="replay batches from CUDA graphs (auto: when at most 2 batches are in flight)")
     ap.add_argument("--no-weak", action="store_true", help="skip the weak-scaling companion measurement (N > 1)")

@@ -62,12 +62,18 @@ cudaError_t fm_launch_final_split(const void* C, const void* V, void* Hw, void* 
                                   int32_t* status, int frames, int m, int p, int k, cudaStream_t s,
                                   double* eig_next = nullptr, const void* gpart = nullptr,
                                   const void* hpart = nullptr);
-cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, int k, cudaStream_t s);
-cudaError_t fm_launch_spectrum_one(const void* t, const void* zgrid, int frames, int m, int L, double* spec64,
-                                   cudaStream_t s);
+cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, int k, cudaStream_t s,
+                               const int32_t* only = nullptr);
+cudaError_t fm_launch_exact_residual(const void* R, const void* basis, double* cert, int frames, int m, int k,
+                                     cudaStream_t s);
+cudaError_t fm_launch_exact_check(const double* cert, const double* spec64, const int32_t* iter_status, int32_t* status,
+                                  int frames, int m, int L, cudaStream_t s);
+cudaError_t fm_launch_spectrum_one(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
+                                   double* spec64, cudaStream_t s, const int32_t* only = nullptr);
 size_t fm_peaks_workspace_bytes(int frames, int L, int K);
 cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K, int min_sep, int32_t* cells,
-                                 double* heights, double* baseline, int32_t* count, void* gws, cudaStream_t s);
+                                 double* heights, double* baseline, int32_t* count, void* gws, cudaStream_t s,
+                                 const int32_t* only = nullptr);
 cudaError_t fm_launch_orthocheck(const void* basis, int frames, int m, int k, double* dev, cudaStream_t s);
 cudaError_t fm_launch_spectrum_i8(const void* t, const int8_t* zd, int8_t* td, double* tscale, int frames, int m, int L,
                                   float* spec32, double* spec64, cudaStream_t s);
@@ -116,13 +122,6 @@ __global__ void k_pad_rows(const float2* __restrict__ x, float2* __restrict__ xp
     const float2* src = x + row * n;
     float2* dst = xp + row * (n + 1);
     for (int j = threadIdx.x; j <= n; j += blockDim.x) dst[j] = j < n ? src[j] : make_float2(0.f, 0.f);
-}
-
-// Exact method, certification of the subspace iteration (run_post_cov): U (complex128, K x M
-// column-major) -> complex64 for the tensor-core product R U.
-__global__ void k_basis_to_c32(const double* __restrict__ basis, float* __restrict__ u32, int64_t n) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < n) u32[i] = static_cast<float>(basis[i]);
 }
 
 // FM_METHOD_FAST1_NORM2 column selection (extension: BASELINE config 3's "columns of R sampled with
@@ -205,41 +204,6 @@ __global__ void k_norm2_select(const float* __restrict__ R, const __half* __rest
         om[static_cast<size_t>(idx[a]) * p + rank] = 1.f;
     }
 }
-
-__device__ double* g_exact_ratio = nullptr;  // debug: per-frame residual / gap
-
-// Frame certified iff no flag from the iteration and max_k ||R u_k - lambda_k u_k|| <= tol * gap,
-// gap = lambda_K - lambda_{K+1} (Ritz). Uncertified frames get kFrameRefine (Jacobi reruns them).
-// One warp per frame.
-__global__ void k_exact_certify(const float* __restrict__ ru, const double* __restrict__ basis,
-                                const double* __restrict__ eig, const double* __restrict__ eig_next,
-                                const int32_t* __restrict__ iter_status, int32_t* __restrict__ status, int frames,
-                                int m, int k, double tol) {
-    const int f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (f >= frames) return;
-    const float* rf = ru + static_cast<size_t>(f) * k * m * 2;
-    const double* uf = basis + static_cast<size_t>(f) * k * m * 2;
-    double worst = 0.0;
-    for (int kk = 0; kk < k; ++kk) {
-        const double lam = eig[static_cast<size_t>(f) * k + kk];
-        double s2 = 0.0;
-        for (int r = lane; r < m; r += 32) {
-            const size_t o = (static_cast<size_t>(kk) * m + r) * 2;
-            const double dr = static_cast<double>(rf[o]) - lam * uf[o];
-            const double di = static_cast<double>(rf[o + 1]) - lam * uf[o + 1];
-            s2 += dr * dr + di * di;
-        }
-        worst = fmax(worst, fmk::warp_sum(s2));
-    }
-    if (lane == 0) {
-        const double gap = eig[static_cast<size_t>(f) * k + k - 1] - eig_next[f];
-        const double ratio = gap > 0.0 ? sqrt(worst) / gap : 1e300;
-        if (g_exact_ratio) g_exact_ratio[f] = ratio;
-        if (iter_status[f] != 0 || !(ratio <= tol)) status[f] |= fmk::kFrameRefine;
-    }
-}
-
 
 // fp64 covariance for the single-matrix facade path (R/src/scene.cpp:138-159 +
 // R/src/linalg.cpp:46-52): y column-major M x N; output S column-major, exactly Hermitian.
@@ -543,9 +507,7 @@ struct fm_plan_s {
     // exact method via certified subspace iteration (pe > 0): plan-owned Omega, R U product, gap
     int pe = 0;
     float* omega_e = nullptr;   // frames x M x pe fp32
-    float* u32 = nullptr;       // frames x K x M complex64 (U for R U)
-    float* ru = nullptr;        // frames x K x M complex64
-    double* eig_next = nullptr; // frames
+    double* cert = nullptr;     // frames: sin-theta bound of the iteration's basis (exact.cu)
     double* gpart = nullptr;    // frames x 2 x p x p complex: G halves from the product epilogue (plane path)
     double* hpart = nullptr;    // frames x 2 x p x p complex: H = V^H C halves (last product)
     // host-path staging
@@ -628,7 +590,6 @@ struct fm_plan_s {
 // p_e <= 32, p_e <= M). Otherwise (or with the FM_PLAN_EXACT_JACOBI flag) every frame runs the Jacobi solver.
 constexpr uint64_t kExactSeed = 0x4558414354ull;
 constexpr int kExactIters = 3;
-constexpr double kExactTol = 1e-3;  // max_k ||R u_k - lambda_k u_k|| <= tol * (lambda_K - lambda_{K+1})
 static int exact_fast_p(const fm_plan_desc& d) {
     if (d.method != FM_METHOD_EXACT || (d.flags & FM_PLAN_EXACT_JACOBI)) return 0;
     const int pe = std::max<int>(static_cast<int>((2 * d.k + 3) / 4 * 4), static_cast<int>((d.k + 4 + 3) / 4 * 4));
@@ -710,9 +671,7 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
     }
     if (pl->pe > 0) {
         chk(pl->get(&pl->omega_e, B * M * pl->pe));
-        chk(pl->get(&pl->u32, B * K * M * 2));
-        chk(pl->get(&pl->ru, B * K * M * 2));
-        chk(pl->get(&pl->eig_next, B));
+        chk(pl->get(&pl->cert, B));
     }
     if (e == cudaSuccess) e = cudaMemset(pl->amax, 0, sizeof(uint32_t) * B);
     if (e != cudaSuccess) {
@@ -844,7 +803,7 @@ extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
     if (d.method == FM_METHOD_FAST2) n += 1 + t * (orth + 1) + fin;  // rmul, t x (orth, rmul), final
     else if (d.method == FM_METHOD_FAST1_NORM2) n += 1 + 1 + (orth + 1) + fin;  // select, rmul, orth, rmul, final
     else if (d.method == FM_METHOD_FAST1) n += 1 + fin;      // gather, final
-    else if (plan->pe > 0) n += 1 + 1 + kExactIters * (3 + 1) + 3 + 1 + 1 + 1 + 1 + 1;  // see run_post_cov
+    else if (plan->pe > 0) n += 1 + 1 + kExactIters * (3 + 1) + 3 + 1 + 6;  // see run_post_cov
     else n += 1;                                              // jacobi
     return n;
 }
@@ -891,9 +850,7 @@ struct WorkView {
     double* spec64;
     int32_t* scratch;
     float* omega_e;
-    float* u32;
-    float* ru;
-    double* eig_next;
+    double* cert;
     double* gpart;
     double* hpart;
     uint8_t* peak_ws;
@@ -908,9 +865,7 @@ static WorkView work_view(fm_plan pl, int64_t f0, int sub = 0) {
     const size_t wsz = d.method == FM_METHOD_EXACT ? MP * MP * 2 : 2 * P * M * 2;
     WorkView w;
     w.omega_e = pl->omega_e ? pl->omega_e + f0 * M * P : nullptr;
-    w.u32 = pl->u32 ? pl->u32 + f0 * K * M * 2 : nullptr;
-    w.ru = pl->ru ? pl->ru + f0 * K * M * 2 : nullptr;
-    w.eig_next = pl->eig_next ? pl->eig_next + f0 : nullptr;
+    w.cert = pl->cert ? pl->cert + f0 : nullptr;
     w.dslot = static_cast<size_t>(f0) + 64 * static_cast<size_t>(sub);
     w.gpart = pl->gpart ? pl->gpart + f0 * 2 * P * P * 2 : nullptr;
     w.hpart = pl->hpart ? pl->hpart + f0 * 2 * P * P * 2 : nullptr;
@@ -1045,8 +1000,8 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
         if ((st = fallback(nullptr, w.H)) != FM_OK) return st;
     } else if (pl->pe > 0) {
         // exact_signal_subspace as certified subspace iteration: C = R Omega, kExactIters x {V = orth(C),
-        // C = R V}, Nystrom/Rayleigh step -> U, lambda, lambda_{K+1}; then R U and the residual test;
-        // frames not certified (or flagged by the iteration) rerun the Jacobi eigensolver below.
+        // C = R V}, Nystrom/Rayleigh step -> U; then the fp64 residual bound (exact.cu) -- checked against the
+        // spectrum after the peaks below; frames not certified rerun the Jacobi eigensolver.
         const int PE = pl->pe;
         k_clear_bits<<<(F + 255) / 256, 256, 0, s>>>(w.scratch, F, ~0);
         FM_CUDA_OK(cudaGetLastError());
@@ -1055,18 +1010,8 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
             FM_LAUNCH(fm_launch_orth_split(w.C, w.V, w.Rt, reinterpret_cast<int32_t*>(w.H), w.scratch, F, M, PE, s));
             if ((st = rmul(nullptr, w.V, w.C, PE)) != FM_OK) return st;
         }
-        FM_LAUNCH(fm_launch_final_split(w.C, w.V, w.H, w.Rt, w.work, basis, eig, w.scratch, F, M, PE, K, s,
-                                        w.eig_next));
-        const int64_t nb = static_cast<int64_t>(F) * K * M * 2;
-        k_basis_to_c32<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, s>>>(basis, w.u32, nb);
-        FM_CUDA_OK(cudaGetLastError());
-        if ((st = rmul(nullptr, w.u32, w.ru, K)) != FM_OK) return st;
-        k_exact_certify<<<(F + 7) / 8, 256, 0, s>>>(w.ru, basis, eig, w.eig_next, w.scratch, io->status, F, M, K,
-                                                     kExactTol);
-        FM_CUDA_OK(cudaGetLastError());
-        FM_LAUNCH(fm_launch_jacobi_eig<float>(R, w.work, basis, eig, io->status, F, M, K, s, 1));
-        k_clear_bits<<<(F + 255) / 256, 256, 0, s>>>(io->status, F, fmk::kFrameRefine);
-        FM_CUDA_OK(cudaGetLastError());
+        FM_LAUNCH(fm_launch_final_split(w.C, w.V, w.H, w.Rt, w.work, basis, eig, w.scratch, F, M, PE, K, s));
+        FM_LAUNCH(fm_launch_exact_residual(R, basis, w.cert, F, M, K, s));
     } else {
         FM_LAUNCH(fm_launch_jacobi_eig<float>(R, w.work, basis, eig, io->status, F, M, K, s));
     }
@@ -1087,6 +1032,20 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     }
     FM_LAUNCH(fm_launch_peaks_only(w.spec64, F, static_cast<int>(d.grid_size), K, static_cast<int>(d.min_sep_cells),
                                    io->peak_cells, io->peak_heights, io->baseline, io->peak_count, w.peak_ws, s));
+    if (pl->pe > 0) {
+        // exact method: the certificate against this spectrum's deepest denominator; frames it does not cover (or
+        // that the iteration flagged) are recomputed by the Jacobi eigensolver, then their spectrum and peaks
+        FM_LAUNCH(fm_launch_exact_check(w.cert, w.spec64, w.scratch, io->status, F, M, static_cast<int>(d.grid_size), s));
+        FM_LAUNCH(fm_launch_jacobi_eig<float>(R, w.work, basis, eig, io->status, F, M, K, s, 1));
+        FM_LAUNCH(fm_launch_autocorr(basis, w.t, F, M, K, s, io->status));
+        FM_LAUNCH(fm_launch_spectrum_one(w.t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, w.spec64, s,
+                                         io->status));
+        FM_LAUNCH(fm_launch_peaks_only(w.spec64, F, static_cast<int>(d.grid_size), K, static_cast<int>(d.min_sep_cells),
+                                       io->peak_cells, io->peak_heights, io->baseline, io->peak_count, w.peak_ws, s,
+                                       io->status));
+        k_clear_bits<<<(F + 255) / 256, 256, 0, s>>>(io->status, F, fmk::kFrameRefine);
+        FM_CUDA_OK(cudaGetLastError());
+    }
     if (prof) mark(pl, 4, s);
     return FM_OK;
 }
@@ -1695,7 +1654,7 @@ extern "C" fm_status fm_z_music_spectrum(int64_t m, int64_t kb, const double* ba
         if (!(dev <= 1e-6)) return fail(FM_EINVAL, "music_spectrum: basis columns are not orthonormal");
     }
     FM_CUDA_OK(fm_launch_autocorr(dB.p, dT.p, 1, static_cast<int>(m), static_cast<int>(kb), c.s));
-    FM_CUDA_OK(fm_launch_spectrum_one(dT.p, dZ.p, 1, static_cast<int>(m), static_cast<int>(L), dOut.p, c.s));
+    FM_CUDA_OK(fm_launch_spectrum_one(dT.p, dZ.p, 1, static_cast<int>(m), static_cast<int>(L), nullptr, dOut.p, c.s));
     FM_CUDA_OK(cudaMemcpyAsync(values, dOut.p, sizeof(double) * L, cudaMemcpyDeviceToHost, c.s));
     FM_CUDA_OK(cudaStreamSynchronize(c.s));
     return FM_OK;
@@ -1731,9 +1690,4 @@ extern "C" fm_status fm_z_extract_peaks(const double* values, int64_t L, int64_t
     *count = n;
     *shortfall = n < k ? 1 : 0;
     return FM_OK;
-}
-
-// Debug (not in the public header): per-frame residual / gap of the exact method's certification.
-extern "C" int32_t fm_debug_set_exact_ratio_buffer(double* d) {
-    return cudaMemcpyToSymbol(g_exact_ratio, &d, sizeof(d)) == cudaSuccess ? 0 : 1;
 }

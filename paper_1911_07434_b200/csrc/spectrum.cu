@@ -41,7 +41,9 @@ constexpr int kNW = kNT / 32;
 
 // t_delta, delta = 0..M-1, for frame blockIdx.x. Thread i owns lags i and M-1-i, so every
 // thread performs M+1 products per basis column (the triangle of lags is load-balanced).
-__global__ void __launch_bounds__(kNT) k_autocorr(const c64* __restrict__ basis, c64* __restrict__ t, int m, int k) {
+__global__ void __launch_bounds__(kNT) k_autocorr(const c64* __restrict__ basis, c64* __restrict__ t, int m, int k,
+                                                  const int32_t* __restrict__ only) {
+    if (only && !(only[blockIdx.x] & kFrameRefine)) return;
     extern __shared__ c64 col[];  // one basis column (M complex)
     const int f = blockIdx.x;
     const c64* Uf = basis + static_cast<size_t>(f) * m * k;
@@ -176,7 +178,8 @@ __device__ void fft_stockham(c64* a, int logn, int cnt, const c64* tw) {
 }
 
 __global__ void __launch_bounds__(kNT, FM_FFT_MINB) k_autocorr_fft(const c64* __restrict__ basis, c64* __restrict__ t, int m, int k,
-                                                   int logn, int grp) {
+                                                   int logn, int grp, const int32_t* __restrict__ only) {
+    if (only && !(only[blockIdx.x] & kFrameRefine)) return;
     extern __shared__ c64 fsm[];
     const int nfft = 1 << logn;
     c64* tw = fsm;                                         // < nfft entries: per-pass w1 tables
@@ -243,11 +246,14 @@ struct PeakOut {
     int32_t* count;     // B
 };
 
-// Spectrum only (fp64 Horner over z), one CTA per frame: the facade's music_spectrum on any grid.
+// Spectrum only (fp64 Horner over z), one CTA per frame, any grid: the facade's music_spectrum, and the exact
+// method's recomputation of the frames the Jacobi solver redid (only != nullptr: frames with kFrameRefine).
 __global__ void __launch_bounds__(kNT) k_spectrum_one(const c64* __restrict__ t, const c64* __restrict__ zgrid, int m,
-                                                      int L, double* __restrict__ spec64) {
+                                                      int L, float* __restrict__ spec32, double* __restrict__ spec64,
+                                                      const int32_t* __restrict__ only) {
     extern __shared__ c64 st1[];
     const int f = blockIdx.x;
+    if (only && !(only[f] & kFrameRefine)) return;
     for (int r = threadIdx.x; r < m; r += kNT) st1[r] = t[static_cast<size_t>(f) * m + r];
     __syncthreads();
     const double c0 = static_cast<double>(m) - st1[0].re;
@@ -266,7 +272,9 @@ __global__ void __launch_bounds__(kNT) k_spectrum_one(const c64* __restrict__ t,
             }
             pr = pr * z.re - pi * z.im;  // Re(p * z)
         }
-        spec64[static_cast<size_t>(f) * L + l] = 1.0 / fmax(c0 - 2.0 * pr, floor_v);
+        const double P = 1.0 / fmax(c0 - 2.0 * pr, floor_v);
+        spec64[static_cast<size_t>(f) * L + l] = P;
+        if (spec32) spec32[static_cast<size_t>(f) * L + l] = static_cast<float>(P);
     }
 }
 
@@ -579,10 +587,12 @@ __device__ __forceinline__ bool better_w(double h1, int c1, double h2, int c2) {
 
 template <bool kInSmem>
 __global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict__ values, int L, int K, int min_sep,
-                                                      PeakOut out, uint8_t* __restrict__ gws) {
+                                                      PeakOut out, uint8_t* __restrict__ gws,
+                                                      const int32_t* __restrict__ only) {
     extern __shared__ __align__(16) uint8_t prs[];
     const PeakLayout lay = peak_layout(L, K, kInSmem);
     const int f = blockIdx.x;
+    if (only && !(only[f] & kFrameRefine)) return;
     uint8_t* base = kInSmem ? prs : gws + static_cast<size_t>(f) * lay.bytes;
     const double* v = values + static_cast<size_t>(f) * L;
     double* svw = reinterpret_cast<double*>(base + lay.o_sv);
@@ -826,7 +836,8 @@ __global__ void __launch_bounds__(kNT) k_orthocheck(const c64* __restrict__ basi
 
 using namespace fmk;
 
-cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, int k, cudaStream_t s) {
+cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, int k, cudaStream_t s,
+                               const int32_t* only) {
     int logn = 1;
     while ((1 << logn) < 2 * m - 1) ++logn;
     if (logn <= 12) {  // FFT in shared memory (M <= 2048)
@@ -843,7 +854,7 @@ cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, in
                                                  static_cast<int>(smem));
             if (e != cudaSuccess) return e;
             spec::k_autocorr_fft<<<frames, spec::kNT, smem, s>>>(static_cast<const c64*>(basis), static_cast<c64*>(t),
-                                                                 m, k, logn, grp);
+                                                                 m, k, logn, grp, only);
             return cudaGetLastError();
         }
     }
@@ -856,20 +867,20 @@ cudaError_t fm_launch_autocorr(const void* basis, void* t, int frames, int m, in
         if (e != cudaSuccess) return e;
     }
     const int threads = std::min(spec::kNT, std::max(32, ((m + 1) / 2 + 31) / 32 * 32));
-    spec::k_autocorr<<<frames, threads, smem, s>>>(static_cast<const c64*>(basis), static_cast<c64*>(t), m, k);
+    spec::k_autocorr<<<frames, threads, smem, s>>>(static_cast<const c64*>(basis), static_cast<c64*>(t), m, k, only);
     return cudaGetLastError();
 }
 
 // Facade music_spectrum: spectrum only, any grid, one CTA per frame.
-cudaError_t fm_launch_spectrum_one(const void* t, const void* zgrid, int frames, int m, int L, double* spec64,
-                                   cudaStream_t s) {
+cudaError_t fm_launch_spectrum_one(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
+                                   double* spec64, cudaStream_t s, const int32_t* only) {
     const size_t smem = sizeof(c64) * m;
     if (smem > 220 * 1024) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(spec::k_spectrum_one, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     spec::k_spectrum_one<<<frames, spec::kNT, smem, s>>>(static_cast<const c64*>(t), static_cast<const c64*>(zgrid), m, L,
-                                                         spec64);
+                                                         spec32, spec64, only);
     return cudaGetLastError();
 }
 
@@ -922,7 +933,8 @@ size_t fm_peaks_workspace_bytes(int frames, int L, int K) {
 // extract_peaks on B x L fp64 values (R/src/spectrum.cpp:182-188), any L >= 1, K >= 1. gws: device workspace of
 // fm_peaks_workspace_bytes(frames, L, K) bytes when that is non-zero.
 cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K, int min_sep, int32_t* cells,
-                                 double* heights, double* baseline, int32_t* count, void* gws, cudaStream_t s) {
+                                 double* heights, double* baseline, int32_t* count, void* gws, cudaStream_t s,
+                                 const int32_t* only) {
     if (K < 1 || L < 1 || frames < 1) return cudaErrorInvalidValue;
     spec::PeakOut out{cells, heights, baseline, count};
     const spec::PeakLayout lay = spec::peak_layout(L, K, true);
@@ -930,11 +942,11 @@ cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K,
         cudaError_t e = cudaFuncSetAttribute(spec::k_peaks_rounds<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(lay.bytes));
         if (e != cudaSuccess) return e;
-        spec::k_peaks_rounds<true><<<frames, spec::kPRT, lay.bytes, s>>>(values, L, K, min_sep, out, nullptr);
+        spec::k_peaks_rounds<true><<<frames, spec::kPRT, lay.bytes, s>>>(values, L, K, min_sep, out, nullptr, only);
     } else {
         if (!gws) return cudaErrorInvalidValue;
         spec::k_peaks_rounds<false><<<frames, spec::kPRT, 0, s>>>(values, L, K, min_sep, out,
-                                                                 static_cast<uint8_t*>(gws));
+                                                                 static_cast<uint8_t*>(gws), only);
     }
     return cudaGetLastError();
 }
