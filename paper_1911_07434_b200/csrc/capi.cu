@@ -81,7 +81,7 @@ cudaError_t fm_launch_spectrum_multi(const void* t, const void* zgrid, int frame
                                      double* spec64, cudaStream_t s);
 template <typename T>
 cudaError_t fm_launch_jacobi_eig(const void* R, void* work, void* basis, double* eig, int32_t* status, int frames,
-                                 int m, int k, cudaStream_t s, int only_flagged = 0);
+                                 int m, int k, cudaStream_t s, int only_flagged = 0, void* work32 = nullptr);
 
 namespace {
 
@@ -508,6 +508,7 @@ struct fm_plan_s {
     int pe = 0;
     float* omega_e = nullptr;   // frames x M x pe fp32
     double* cert = nullptr;     // frames: sin-theta bound of the iteration's basis (exact.cu)
+    float* work32 = nullptr;    // exact method: fp32 Jacobi stage, frames x MP x MP complex64
     double* gpart = nullptr;    // frames x 2 x p x p complex: G halves from the product epilogue (plane path)
     double* hpart = nullptr;    // frames x 2 x p x p complex: H = V^H C halves (last product)
     // host-path staging
@@ -677,6 +678,14 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
     if (e != cudaSuccess) {
         delete pl;
         return fm_fail_cuda(e, "fm_plan_create workspace", __FILE__, __LINE__);
+    }
+    if (desc->method == FM_METHOD_EXACT && e == cudaSuccess) {
+        const size_t mp = (M + 15) / 16 * 16;
+        e = pl->get(&pl->work32, B * mp * mp * 2);
+        if (e != cudaSuccess) {
+            delete pl;
+            return fm_fail_cuda(e, "fm_plan_create jacobi workspace", __FILE__, __LINE__);
+        }
     }
     if (pl->pe > 0) {  // fixed Gaussian start blocks, one per frame slot
         std::vector<float> om(B * M * pl->pe);
@@ -851,6 +860,7 @@ struct WorkView {
     int32_t* scratch;
     float* omega_e;
     double* cert;
+    float* work32;
     double* gpart;
     double* hpart;
     uint8_t* peak_ws;
@@ -866,6 +876,7 @@ static WorkView work_view(fm_plan pl, int64_t f0, int sub = 0) {
     WorkView w;
     w.omega_e = pl->omega_e ? pl->omega_e + f0 * M * P : nullptr;
     w.cert = pl->cert ? pl->cert + f0 : nullptr;
+    w.work32 = pl->work32 ? pl->work32 + f0 * ((M + 15) / 16 * 16) * ((M + 15) / 16 * 16) * 2 : nullptr;
     w.dslot = static_cast<size_t>(f0) + 64 * static_cast<size_t>(sub);
     w.gpart = pl->gpart ? pl->gpart + f0 * 2 * P * P * 2 : nullptr;
     w.hpart = pl->hpart ? pl->hpart + f0 * 2 * P * P * 2 : nullptr;
@@ -1013,7 +1024,7 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
         FM_LAUNCH(fm_launch_final_split(w.C, w.V, w.H, w.Rt, w.work, basis, eig, w.scratch, F, M, PE, K, s));
         FM_LAUNCH(fm_launch_exact_residual(R, basis, w.cert, F, M, K, s));
     } else {
-        FM_LAUNCH(fm_launch_jacobi_eig<float>(R, w.work, basis, eig, io->status, F, M, K, s));
+        FM_LAUNCH(fm_launch_jacobi_eig<float>(R, w.work, basis, eig, io->status, F, M, K, s, 0, w.work32));
     }
     if (prof) mark(pl, 2, s);
     FM_LAUNCH(fm_launch_autocorr(basis, w.t, F, M, K, s));
@@ -1036,7 +1047,7 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
         // exact method: the certificate against this spectrum's deepest denominator; frames it does not cover (or
         // that the iteration flagged) are recomputed by the Jacobi eigensolver, then their spectrum and peaks
         FM_LAUNCH(fm_launch_exact_check(w.cert, w.spec64, w.scratch, io->status, F, M, static_cast<int>(d.grid_size), s));
-        FM_LAUNCH(fm_launch_jacobi_eig<float>(R, w.work, basis, eig, io->status, F, M, K, s, 1));
+        FM_LAUNCH(fm_launch_jacobi_eig<float>(R, w.work, basis, eig, io->status, F, M, K, s, 1, w.work32));
         FM_LAUNCH(fm_launch_autocorr(basis, w.t, F, M, K, s, io->status));
         FM_LAUNCH(fm_launch_spectrum_one(w.t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, w.spec64, s,
                                          io->status));

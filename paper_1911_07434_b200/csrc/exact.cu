@@ -46,17 +46,30 @@ __global__ void __launch_bounds__(kT) k_exact_residual(const c32* __restrict__ R
     __syncthreads();
     const c32* Rf = R + static_cast<size_t>(f) * m * m;
     double tr = 0.0;
-    // (R U)(r, :) by one warp per row: lanes split the columns c (coalesced row reads), fp64 accumulation
+    // (R U)(r, :) by one warp per row: lanes split the columns c (coalesced row reads, all of a 256-column chunk
+    // issued before the fp64 FMAs consume them), fp64 accumulation
     for (int r = warp; r < m; r += kT / 32) {
         c64 acc[kMaxK];
 #pragma unroll
         for (int q = 0; q < kMaxK; ++q) acc[q] = mk(0.0, 0.0);
-        for (int c = lane; c < m; c += 32) {
-            const c64 a = to64(Rf[static_cast<size_t>(r) * m + c]);
-            if (c == r) tr += a.re;
+        const c32* row = Rf + static_cast<size_t>(r) * m;
+        for (int c0 = 0; c0 < m; c0 += 256) {
+            c32 a32[8];
 #pragma unroll
-            for (int q = 0; q < kMaxK; ++q)
-                if (q < k) cmac(acc[q], a, U[q * m + c]);
+            for (int j = 0; j < 8; ++j) {
+                const int c = c0 + lane + 32 * j;
+                a32[j] = c < m ? row[c] : mk(0.f, 0.f);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int c = c0 + lane + 32 * j;
+                if (c >= m) break;
+                const c64 a = to64(a32[j]);
+                if (c == r) tr += a.re;
+#pragma unroll
+                for (int q = 0; q < kMaxK; ++q)
+                    if (q < k) cmac(acc[q], a, U[q * m + c]);
+            }
         }
 #pragma unroll
         for (int q = 0; q < kMaxK; ++q) {

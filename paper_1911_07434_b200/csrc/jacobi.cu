@@ -15,6 +15,10 @@
 // global / L2) ~ (nb + nb^2/2) block-times instead of once per column pair.
 // fp64 facade path: a Gershgorin shift mu makes indefinite Hermitian input PSD (eigenvectors
 // unchanged; lambda = sigma - mu), so the signed descending order of the reference is kept.
+// Batch path (complex64 R): fp32 sweeps to fp32 convergence, then fp64 sweeps polish the fp32-converged columns
+// (kModePolish: A starts from the fp32 A, widened exactly) -- the fp32 stage alone leaves the column orthogonality
+// at ~1e-6, which moves the MUSIC spectrum by up to ~0.08 dB at c5; after the polish the columns are the exact
+// singular vectors of a matrix within ~eps_32 |R| of R, like the rest of the complex64 path.
 
 #include <cuda_runtime.h>
 
@@ -61,10 +65,17 @@ __device__ __forceinline__ bool pair_rotate(cplx<T>* ai, cplx<T>* aj, int mp, in
     return true;
 }
 
+constexpr int kModeOnlyFlagged = 1;  // frames with kFrameRefine only (the exact method's uncertified frames)
+constexpr int kModePolish = 2;       // A starts from A0 (fp32 stage), R (complex64) only sets the scale
+constexpr int kModeNoStatus = 4;     // do not flag non-convergence (the fp32 stage; the polish decides)
+
 template <typename T>
-__global__ void __launch_bounds__(kNT) k_jacobi_eig(const cplx<T>* __restrict__ R, cplx<T>* __restrict__ work,
-                                                    c64* __restrict__ basis, double* __restrict__ eig,
-                                                    int32_t* __restrict__ status, int m, int k, int only_flagged) {
+__global__ void __launch_bounds__(kNT) k_jacobi_eig(const void* __restrict__ Rv, const cplx<float>* __restrict__ A0,
+                                                    cplx<T>* __restrict__ work, c64* __restrict__ basis,
+                                                    double* __restrict__ eig, int32_t* __restrict__ status, int m,
+                                                    int k, int mode) {
+    const int only_flagged = mode & kModeOnlyFlagged;
+    const bool polish = (mode & kModePolish) != 0;
     extern __shared__ uint8_t dsm[];
     const int mp = (m + kB - 1) / kB * kB;
     const int nb = mp / kB;
@@ -76,14 +87,20 @@ __global__ void __launch_bounds__(kNT) k_jacobi_eig(const cplx<T>* __restrict__ 
     const int f = blockIdx.x;
     if (only_flagged && !(status[f] & kFrameRefine)) return;  // certified by the subspace iteration
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const cplx<T>* Rf = R + static_cast<size_t>(f) * m * m;
+    // R: cplx<T> (mode 0) or the batch's complex64 R (polish: only its diagonal, for the scale)
+    const cplx<T>* Rf = static_cast<const cplx<T>*>(Rv) + static_cast<size_t>(f) * m * m;
+    const cplx<float>* Rf32 = static_cast<const cplx<float>*>(Rv) + static_cast<size_t>(f) * m * m;
+    auto rdiag = [&](int c) -> double {
+        return polish ? static_cast<double>(Rf32[static_cast<size_t>(c) * m + c].re)
+                      : static_cast<double>(Rf[static_cast<size_t>(c) * m + c].re);
+    };
     cplx<T>* A = work + static_cast<size_t>(f) * mp * mp;
     const T tol = T(4) * static_cast<T>(eps_of<T>::value) * sqrt(static_cast<T>(mp));
 
     // Gershgorin shift (fp64 facade path only): mu = max(0, -min_i (R_ii - sum_{j!=i} |R_ij|))
     if (threadIdx.x == 0) s_mu = 0.0;
     __syncthreads();
-    if (sizeof(T) == 8) {
+    if (sizeof(T) == 8 && !polish) {
         for (int c = warp; c < m; c += kNW) {
             double off = 0.0;
             for (int r = lane; r < m; r += 32)
@@ -106,19 +123,25 @@ __global__ void __launch_bounds__(kNT) k_jacobi_eig(const cplx<T>* __restrict__ 
     if (threadIdx.x == 0) s_dmax = 0.0;
     __syncthreads();
     for (int c = threadIdx.x; c < m; c += kNT) {
-        const double v = fabs(static_cast<double>(Rf[static_cast<size_t>(c) * m + c].re)) + s_mu;
+        const double v = fabs(rdiag(c)) + s_mu;
         if (v > 0.0 && v < 1e300) atomicMax(reinterpret_cast<unsigned long long*>(&s_dmax), __double_as_longlong(v));
     }
     __syncthreads();
     const double nsc = s_dmax > 0.0 ? pow2_inv_sqrt_scale(s_dmax * s_dmax) : 1.0;  // 2^-e
     const T mu = static_cast<T>(s_mu);
     // A[c][r] = R(r, c) = conj(R[c][r]) (row-major Hermitian R), padded with zeros
-    for (int e = threadIdx.x; e < mp * mp; e += kNT) {
-        const int c = e / mp, r = e % mp;
-        cplx<T> v = mk<T>(0, 0);
-        if (c < m && r < m) v = conj(Rf[static_cast<size_t>(c) * m + r]);
-        if (c == r && c < m) v.re += mu;
-        A[static_cast<size_t>(c) * mp + r] = mk<T>(static_cast<T>(v.re * nsc), static_cast<T>(v.im * nsc));
+    if (polish) {  // the fp32 stage's columns (already scaled by nsc), widened exactly
+        const cplx<float>* A0f = A0 + static_cast<size_t>(f) * mp * mp;
+        for (int e = threadIdx.x; e < mp * mp; e += kNT)
+            A[e] = mk<T>(static_cast<T>(A0f[e].re), static_cast<T>(A0f[e].im));
+    } else {
+        for (int e = threadIdx.x; e < mp * mp; e += kNT) {
+            const int c = e / mp, r = e % mp;
+            cplx<T> v = mk<T>(0, 0);
+            if (c < m && r < m) v = conj(Rf[static_cast<size_t>(c) * m + r]);
+            if (c == r && c < m) v.re += mu;
+            A[static_cast<size_t>(c) * mp + r] = mk<T>(static_cast<T>(v.re * nsc), static_cast<T>(v.im * nsc));
+        }
     }
     __syncthreads();
 
@@ -202,7 +225,7 @@ __global__ void __launch_bounds__(kNT) k_jacobi_eig(const cplx<T>* __restrict__ 
         if (lam < 0.0 && lam >= -1e-10) lam = 0.0;
         eig[static_cast<size_t>(f) * k + threadIdx.x] = lam;
     }
-    if (threadIdx.x == 0 && !converged) atomicOr(&status[f], kFrameNoConv);
+    if (threadIdx.x == 0 && !converged && !(mode & kModeNoStatus)) atomicOr(&status[f], kFrameNoConv);
 }
 
 }  // namespace jac
@@ -211,20 +234,33 @@ __global__ void __launch_bounds__(kNT) k_jacobi_eig(const cplx<T>* __restrict__ 
 using namespace fmk;
 
 template <typename T>
-cudaError_t fm_launch_jacobi_eig(const void* R, void* work, void* basis, double* eig, int32_t* status, int frames,
-                                 int m, int k, cudaStream_t s, int only_flagged) {
+static cudaError_t launch_jac(const void* R, const void* a0, void* wk, void* basis, double* eig, int32_t* status,
+                              int frames, int m, int k, int mode, cudaStream_t s) {
     const int mp = (m + jac::kB - 1) / jac::kB * jac::kB;
     const size_t smem = 2 * jac::kB * static_cast<size_t>(mp) * sizeof(cplx<T>);
     if (mp > 1024 || k > 64 || smem > 200 * 1024) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(jac::k_jacobi_eig<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    jac::k_jacobi_eig<T><<<frames, jac::kNT, smem, s>>>(static_cast<const cplx<T>*>(R), static_cast<cplx<T>*>(work),
-                                                        static_cast<c64*>(basis), eig, status, m, k, only_flagged);
+    jac::k_jacobi_eig<T><<<frames, jac::kNT, smem, s>>>(R, static_cast<const cplx<float>*>(a0), static_cast<cplx<T>*>(wk),
+                                                        static_cast<c64*>(basis), eig, status, m, k, mode);
     return cudaGetLastError();
 }
 
+// T = double: fp64 on cplx<double> R (facade, Lanczos). T = float: complex64 R, fp32 sweeps into work32 (frames x
+// mp x mp complex64) then the fp64 polish into work (frames x mp x mp complex128).
+template <typename T>
+cudaError_t fm_launch_jacobi_eig(const void* R, void* work, void* basis, double* eig, int32_t* status, int frames,
+                                 int m, int k, cudaStream_t s, int only_flagged, void* work32) {
+    const int of = only_flagged ? jac::kModeOnlyFlagged : 0;
+    if (sizeof(T) == 8) return launch_jac<double>(R, nullptr, work, basis, eig, status, frames, m, k, of, s);
+    if (!work32) return cudaErrorInvalidValue;
+    cudaError_t e = launch_jac<float>(R, nullptr, work32, basis, eig, status, frames, m, k, of | jac::kModeNoStatus, s);
+    if (e != cudaSuccess) return e;
+    return launch_jac<double>(R, work32, work, basis, eig, status, frames, m, k, of | jac::kModePolish, s);
+}
+
 template cudaError_t fm_launch_jacobi_eig<float>(const void*, void*, void*, double*, int32_t*, int, int, int,
-                                                 cudaStream_t, int);
+                                                 cudaStream_t, int, void*);
 template cudaError_t fm_launch_jacobi_eig<double>(const void*, void*, void*, double*, int32_t*, int, int, int,
-                                                  cudaStream_t, int);
+                                                  cudaStream_t, int, void*);

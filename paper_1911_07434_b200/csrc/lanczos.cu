@@ -30,7 +30,7 @@ cudaError_t fm_launch_rmul(const void*, const void*, const void*, void*, const i
                            cudaStream_t);
 template <typename T>
 cudaError_t fm_launch_jacobi_eig(const void* R, void* work, void* basis, double* eig, int32_t* status, int frames,
-                                 int m, int k, cudaStream_t s, int only_flagged);
+                                 int m, int k, cudaStream_t s, int only_flagged, void* work32 = nullptr);
 template <typename T>
 cudaError_t fm_launch_qr_rank(const void* C, void* work, void* Vout, int32_t* status, int32_t* rank_out, int m, int p,
                               cudaStream_t s);
