@@ -75,7 +75,9 @@ cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K,
                                  double* heights, double* baseline, int32_t* count, void* gws, cudaStream_t s,
                                  const int32_t* only = nullptr);
 cudaError_t fm_launch_orthocheck(const void* basis, int frames, int m, int k, double* dev, cudaStream_t s);
-cudaError_t fm_launch_spectrum_i8(const void* t, const int8_t* zd, int8_t* td, double* tscale, int frames, int m, int L,
+int fm_spectrum_tc_pairs_pad(int L);
+int fm_spectrum_tc_canon_off(int row, int k);
+cudaError_t fm_launch_spectrum_tc(const void* t, const int8_t* zk, int8_t* tk, double* tscale, int frames, int m, int L,
                                   float* spec32, double* spec64, cudaStream_t s);
 cudaError_t fm_launch_spectrum_multi(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
                                      double* spec64, cudaStream_t s);
@@ -252,30 +254,28 @@ std::vector<double> zgrid_host(int64_t L, double theta0, double theta1, double d
     return z;
 }
 
-// Digits of the spectrum's cos / sin table for the int8 Ozaki kernel (spectrum.cu k_spectrum_i8): for pair
-// column q < nq and delta < m, z = (cos, sin)(delta phi_q) (angle formed in fp64, glibc), written as 5 signed
-// base-128 digits of z / 2, in mma B-fragment order [s][cs][q / 8][delta / 32][lane][2 x u32] (column q % 8 = lane / 4,
-// k = 4 (lane % 4) + 16 word + byte); zero padding to nqp = nq up to 32 and mk = m up to 32.
-std::vector<int8_t> zdig_host(int64_t L, double theta0, double theta1, double d, double lambda, int64_t m) {
+// Digits of the cos / sin table for the tcgen05 spectrum (spectrum_tc.cu): for pair q < nq and delta < m,
+// z = (cos, sin)(delta phi_q) (angle in fp64, glibc) as 5 signed base-128 digits of z / 2, in the zK layout
+// [pair tile of 48][K block of 32][plane = s * 2 + cs][canonical 48 x 32 tile] (zero padding past nq and m).
+std::vector<int8_t> zdig_host_k(int64_t L, double theta0, double theta1, double d, double lambda, int64_t m) {
     constexpr int kS = 5;
-    const int64_t nq = (L + 1) / 2, nqp = (nq + 31) / 32 * 32, nkb = (m + 31) / 32, npb = nqp / 8;
-    std::vector<int8_t> z(static_cast<size_t>(kS * 2 * nqp * nkb * 32), 0);
+    const int64_t nq = (L + 1) / 2, nqp = fm_spectrum_tc_pairs_pad(static_cast<int>(L)), mk = (m + 31) / 32 * 32;
+    std::vector<int8_t> z(static_cast<size_t>(kS * 2 * nqp * mk), 0);
     const double span = theta1 - theta0;
     for (int64_t q = 0; q < nq; ++q) {
         const double th = theta0 + (span * static_cast<double>(q)) / static_cast<double>(L - 1);
         const double step = 2.0 * kPi * d * std::sin(th) / lambda;
-        const int64_t pb = q / 8, col = q % 8;
         for (int64_t dl = 0; dl < m; ++dl) {
             const double ang = static_cast<double>(dl) * step;
             double r[2] = {0.5 * std::cos(ang), 0.5 * std::sin(ang)};
-            const int64_t kb = dl / 32, k = dl % 32;
-            const int64_t lane = col * 4 + (k & 15) / 4, word = k / 16;
             for (int sl = 0; sl < kS; ++sl)
                 for (int cs = 0; cs < 2; ++cs) {
                     const double x = 128.0 * r[cs];
                     const double dg = std::nearbyint(x);
                     r[cs] = x - dg;
-                    z[static_cast<size_t>(((((sl * 2 + cs) * npb + pb) * nkb + kb) * 32 + lane) * 2 + word) * 4 + (k & 3)] =
+                    const int64_t kb = dl / 32, plane = sl * 2 + cs;
+                    z[static_cast<size_t>(((q / 48 * (mk / 32) + kb) * 10 + plane) * 48 * 32 +
+                                          fm_spectrum_tc_canon_off(static_cast<int>(q % 48), static_cast<int>(dl % 32)))] =
                         static_cast<int8_t>(dg);
                 }
         }
@@ -489,7 +489,7 @@ struct fm_plan_s {
     double* spec64 = nullptr; // frames x L (fp64 spectrum for peak picking)
     double* zgrid = nullptr;  // L complex128
     uint8_t* peak_ws = nullptr;  // peak-picking workspace when a frame's does not fit in shared memory (long grids)
-    int8_t* zdig = nullptr;   // mirror-symmetric grids: int8 digits of the cos / sin table (Ozaki spectrum)
+    int8_t* zk = nullptr;     // mirror-symmetric grids: int8 digits of the cos / sin table (zdig_host_k)
     int8_t* tdig = nullptr;   // per batch: int8 digits of t (frames padded per sub-batch)
     double* tscale = nullptr; // per batch: power-of-two scale of each frame's t
     size_t tdig_rows = 0;     // frame rows of tdig / tscale (sub-batch i uses rows f0 + 64 i ..)
@@ -706,16 +706,16 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
         return fm_fail_cuda(e, "fm_plan_create zgrid", __FILE__, __LINE__);
     }
     if (desc->theta0 == -desc->theta1) {
-        const auto zdg = zdig_host(desc->grid_size, desc->theta0, desc->theta1, desc->d, desc->lambda, desc->m);
         const size_t mk = (static_cast<size_t>(desc->m) + 31) / 32 * 32;
-        e = pl->get(&pl->zdig, zdg.size());
-        if (e == cudaSuccess) e = cudaMemcpy(pl->zdig, zdg.data(), zdg.size(), cudaMemcpyHostToDevice);
-        pl->tdig_rows = B + 64 * 16;
+        const auto zkh = zdig_host_k(desc->grid_size, desc->theta0, desc->theta1, desc->d, desc->lambda, desc->m);
+        e = pl->get(&pl->zk, zkh.size());
+        if (e == cudaSuccess) e = cudaMemcpy(pl->zk, zkh.data(), zkh.size(), cudaMemcpyHostToDevice);
+        pl->tdig_rows = B + 128 * 16;
         if (e == cudaSuccess) e = pl->get(&pl->tdig, pl->tdig_rows * 5 * 2 * mk);
         if (e == cudaSuccess) e = pl->get(&pl->tscale, pl->tdig_rows);
         if (e != cudaSuccess) {
             delete pl;
-            return fm_fail_cuda(e, "fm_plan_create zdig", __FILE__, __LINE__);
+            return fm_fail_cuda(e, "fm_plan_create spectrum digits", __FILE__, __LINE__);
         }
     }
     if (const size_t pws = fm_peaks_workspace_bytes(static_cast<int>(B), static_cast<int>(L), static_cast<int>(K))) {
@@ -804,7 +804,7 @@ extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
     const int t = d.t;
     // covariance + rescue list + rescue covariance + status clear + autocorr + spectrum + peaks (+ odd-N pad)
     int n = 1 + 2 + 1 + 3 + (plan->x_pad ? 1 : 0);
-    if (plan->zdig) n += 1;  // int8 spectrum: + the digit split of t (k_slice_t)
+    if (plan->zk) n += 1;  // int8 spectrum: + the digit split of t (k_slice_tk)
     const bool tiled = d.p <= 32 && (d.p % 4) == 0;
     const int gepi = gram_epilogue(plan) ? 1 : 0;
     const int fin = (tiled ? 3 - gepi : 2) + 1;  // gram, small-warp, (fallback), basis | cholqr, nystrom, (fallback)
@@ -877,7 +877,7 @@ static WorkView work_view(fm_plan pl, int64_t f0, int sub = 0) {
     w.omega_e = pl->omega_e ? pl->omega_e + f0 * M * P : nullptr;
     w.cert = pl->cert ? pl->cert + f0 : nullptr;
     w.work32 = pl->work32 ? pl->work32 + f0 * ((M + 15) / 16 * 16) * ((M + 15) / 16 * 16) * 2 : nullptr;
-    w.dslot = static_cast<size_t>(f0) + 64 * static_cast<size_t>(sub);
+    w.dslot = static_cast<size_t>(f0) + 128 * static_cast<size_t>(sub);
     w.gpart = pl->gpart ? pl->gpart + f0 * 2 * P * P * 2 : nullptr;
     w.hpart = pl->hpart ? pl->hpart + f0 * 2 * P * P * 2 : nullptr;
     w.C = pl->C + f0 * P * M * 2;
@@ -1030,12 +1030,12 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     FM_LAUNCH(fm_launch_autocorr(basis, w.t, F, M, K, s));
     if (prof) mark(pl, 3, s);
     // mirror-symmetric grid (theta0 = -theta1): pairs (theta, -theta) share one evaluation on the INT8 tensor cores
-    // with fp64-exact digit splitting (k_spectrum_i8); other grids: the fp64 power-recurrence kernel
+    // (tcgen05 kind::i8) with fp64-exact digit splitting (spectrum_tc.cu); other grids: the fp64 power recurrence
     const bool sym = d.theta0 == -d.theta1;
-    const bool dig_fits = w.dslot + (static_cast<size_t>(F) + 63) / 64 * 64 <= pl->tdig_rows;
-    if (sym && pl->zdig && dig_fits) {
+    const bool dig_fits = w.dslot + (static_cast<size_t>(F) + 127) / 128 * 128 <= pl->tdig_rows;
+    if (sym && pl->zk && dig_fits) {
         const size_t mk = (static_cast<size_t>(M) + 31) / 32 * 32;
-        FM_LAUNCH(fm_launch_spectrum_i8(w.t, pl->zdig, pl->tdig + w.dslot * 5 * 2 * mk, pl->tscale + w.dslot, F, M,
+        FM_LAUNCH(fm_launch_spectrum_tc(w.t, pl->zk, pl->tdig + w.dslot * 5 * 2 * mk, pl->tscale + w.dslot, F, M,
                                         static_cast<int>(d.grid_size), io->spectrum, w.spec64, s));
     } else {
         FM_LAUNCH(fm_launch_spectrum_multi(w.t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, w.spec64,

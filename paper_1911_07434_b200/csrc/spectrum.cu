@@ -344,199 +344,6 @@ __global__ void __launch_bounds__(kNT) k_spectrum_multi(const c64* __restrict__ 
     }
 }
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-                 "l"(src), "r"(src_bytes)
-                 : "memory");
-}
-
-// Mirror-symmetric grids on the INT8 tensor cores, fp64-exact by digit splitting (Ozaki scheme): the same
-// sums A = T_re Zc, B = T_im Zs as k_spectrum_dmma, with every operand written as kOS signed base-128 digits,
-// v = scale * sum_s d_s 128^-(s+1), |d_s| <= 64 (per-frame power-of-two scale for T, scale 2 for the plan's
-// cos / sin table), and A = 2 sigma_f sum_{a+b <= kOS-1} 128^-(a+b+2) sum_delta dT_a dZ_b: each group
-// s = a + b accumulated exactly in int32 by mma.sync m16n8k32 s8 (|sum| <= kOS 64^2 M < 2^31 for M <= 1024),
-// the five groups combined in fp64 at the end. Truncation error ~1e-10 of the largest term (numpy model:
-// 2e-8 absolute on sums of magnitude 1e2) -- far inside the 0.05 dB gate.
-// Digits are stored in mma-fragment order so each lane stages one 16-byte (A) / 8-byte (B) word per tile:
-//   td: [s][ri][frame block of 16][delta block of 32][lane][4 x u32]  (rows g, g+8; k 4 t4.., 16 + 4 t4..)
-//   zd: [s][cs][pair block of 8][delta block of 32][lane][2 x u32]   (column g; k 4 t4.., 16 + 4 t4..)
-#ifndef FM_I8_STAGES
-#define FM_I8_STAGES 4
-#endif
-#ifdef FM_I8_VOLATILE
-#define FM_I8_ASM asm volatile
-#else
-#define FM_I8_ASM asm  // pure int8 MMAs (no volatile): the shared loads can be scheduled around them
-#endif
-#ifndef FM_I8_NB
-#define FM_I8_NB 1
-#endif
-constexpr int kOS = 5;     // digit slices per operand
-constexpr int kONB = FM_I8_NB;  // pair blocks (of 8) per warp
-constexpr int kOF = 64;    // frames per CTA (4 frame blocks)
-constexpr int kOQ = 16 * kONB;  // pairs per CTA (2 kONB pair blocks)
-constexpr int kOT = 256;   // 8 warps: 4 frame blocks x 2 (kONB pair blocks each)
-constexpr int kONS = FM_I8_STAGES;  // staging ring depth (delta blocks)
-constexpr int kOTB = kOS * 2 * 4 * 512;   // T digits of one delta block (bytes)
-constexpr int kOZB = kOS * 2 * (2 * kONB) * 256;   // Z digits of one delta block
-constexpr int kOSmem = kONS * (kOTB + kOZB);
-
-__device__ __forceinline__ size_t td_index(int s, int ri, int f, int d, int nfb, int nkb) {
-    const int fb = f >> 4, r = f & 15, kb = d >> 5, k = d & 31;
-    const int lane = ((r & 7) << 2) | ((k & 15) >> 2), w = ((k >> 4) << 1) | (r >> 3);
-    return ((((static_cast<size_t>(s * 2 + ri) * nfb + fb) * nkb + kb) * 32 + lane) * 4 + w) * 4 + (k & 3);
-}
-
-// Per-batch digits of t (frames of this call, blocks of 16 zero-padded by the launcher), scale[f].
-__global__ void __launch_bounds__(256) k_slice_t(const c64* __restrict__ t, int8_t* __restrict__ td,
-                                                 double* __restrict__ tscale, int m, int nkb, int nfb) {
-    __shared__ double red[8];
-    const int f = blockIdx.x, tid = threadIdx.x;
-    const c64* tf = t + static_cast<size_t>(f) * m;
-    double mx = 0.0;
-    for (int d = 1 + tid; d < m; d += 256) mx = fmax(mx, fmax(fabs(tf[d].re), fabs(tf[d].im)));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((tid & 31) == 0) red[tid >> 5] = mx;
-    __syncthreads();
-    mx = 0.0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) mx = fmax(mx, red[w]);
-    int e = 0;
-    frexp(2.0 * mx, &e);  // 2 mx < 2^e
-    const double scale = mx > 0.0 ? ldexp(1.0, e) : 1.0;
-    if (tid == 0) tscale[f] = scale;
-    const double inv = 1.0 / scale;  // exact (power of two)
-    for (int d = tid; d < 32 * nkb; d += 256) {
-        const bool live = d >= 1 && d < m;
-        double r[2] = {live ? tf[d].re * inv : 0.0, live ? tf[d].im * inv : 0.0};
-#pragma unroll
-        for (int sl = 0; sl < kOS; ++sl)
-#pragma unroll
-            for (int ri = 0; ri < 2; ++ri) {
-                const double x = 128.0 * r[ri];
-                const double dg = rint(x);
-                r[ri] = x - dg;
-                td[td_index(sl, ri, f, d, nfb, nkb)] = static_cast<int8_t>(dg);
-            }
-    }
-}
-
-__global__ void __launch_bounds__(kOT, 3 - kONB) k_spectrum_i8(const int8_t* __restrict__ td, const double* __restrict__ tscale,
-                                                       const int8_t* __restrict__ zd, const c64* __restrict__ t,
-                                                       int frames, int m, int nkb, int nfb, int npb, int L,
-                                                       float* __restrict__ spec32, double* __restrict__ spec64) {
-    extern __shared__ __align__(16) uint8_t osm[];
-    const int nq = (L + 1) / 2;
-    const int fb0 = blockIdx.y * (kOF / 16), pb0 = blockIdx.x * (kOQ / 8);
-    constexpr int kPB = 2 * kONB;  // pair blocks per CTA
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
-    const int wm = warp & 3, wn = warp >> 2;  // frame block wm, pair blocks kONB wn ..
-    auto stage_t = [&](int buf) { return osm + buf * (kOTB + kOZB); };
-    auto stage_z = [&](int buf) { return osm + buf * (kOTB + kOZB) + kOTB; };
-    auto issue = [&](int kb, int buf) {  // delta block kb: all slices of T (4 frame blocks) and Z (4 pair blocks)
-        uint8_t* st = stage_t(buf);
-        uint8_t* sz = stage_z(buf);
-        for (int e = tid; e < kOTB / 16; e += kOT) {  // (s, ri, fb) x 32 pieces of 16 B
-            const int piece = e & 31, q = e >> 5, fb = q & 3, sri = q >> 2;
-            const int8_t* src = td + ((static_cast<size_t>(sri) * nfb + fb0 + fb) * nkb + kb) * 512 + piece * 16;
-            cp_async16(st + (sri * 4 + fb) * 512 + piece * 16, src, 16);
-        }
-        for (int e = tid; e < kOZB / 16; e += kOT) {  // (s, cs, pb) x 16 pieces of 16 B
-            const int piece = e & 15, q = e >> 4, pb = q % kPB, scs = q / kPB;
-            const int8_t* src = zd + ((static_cast<size_t>(scs) * npb + pb0 + pb) * nkb + kb) * 256 + piece * 16;
-            cp_async16(sz + (scs * kPB + pb) * 256 + piece * 16, src, 16);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    int acc[kOS][2][kONB][4];  // [group s][A | B][pair block][fragment]
-#pragma unroll
-    for (int sg = 0; sg < kOS; ++sg)
-#pragma unroll
-        for (int x = 0; x < 2; ++x)
-#pragma unroll
-            for (int n = 0; n < kONB; ++n)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) acc[sg][x][n][e] = 0;
-    for (int i = 0; i < kONS - 1 && i < nkb; ++i) issue(i, i);
-    for (int kb = 0; kb < nkb; ++kb) {
-        // groups committed after block kb: min(kONS - 2, nkb - 1 - kb); wait until block kb has landed
-        static_assert(kONS >= 2 && kONS <= 5, "ring depth");
-        const int after = min(kONS - 2, nkb - 1 - kb);
-        if (after >= 3) asm volatile("cp.async.wait_group 3;" ::: "memory");
-        else if (after == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
-        else if (after == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
-        else asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncthreads();  // block kb staged; block kb - 1's buffer is free
-        if (kb + kONS - 1 < nkb) issue(kb + kONS - 1, (kb + kONS - 1) % kONS);
-        const int buf = kb % kONS;
-        const uint8_t* st = stage_t(buf);
-        const uint8_t* sz = stage_z(buf);
-        uint4 av[kOS][2];
-#pragma unroll
-        for (int sl = 0; sl < kOS; ++sl)
-#pragma unroll
-            for (int ri = 0; ri < 2; ++ri)
-                av[sl][ri] = *reinterpret_cast<const uint4*>(st + ((sl * 2 + ri) * 4 + wm) * 512 + lane * 16);
-#pragma unroll
-        for (int b = 0; b < kOS; ++b) {
-            uint2 bv[2][kONB];  // [cos | sin][pair block]
-#pragma unroll
-            for (int cs = 0; cs < 2; ++cs)
-#pragma unroll
-                for (int n = 0; n < kONB; ++n)
-                    bv[cs][n] = *reinterpret_cast<const uint2*>(sz + ((b * 2 + cs) * kPB + kONB * wn + n) * 256 + lane * 8);
-#pragma unroll
-            for (int a = 0; a + b < kOS; ++a)
-#pragma unroll
-                for (int x = 0; x < 2; ++x)
-#pragma unroll
-                    for (int n = 0; n < kONB; ++n) {
-                        int(&c)[4] = acc[a + b][x][n];
-                        const uint4 A = av[a][x];
-                        const uint2 B = bv[x][n];
-                        FM_I8_ASM("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-                                     : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-                                     : "r"(A.x), "r"(A.y), "r"(A.z), "r"(A.w), "r"(B.x), "r"(B.y));
-                    }
-        }
-    }
-    const double floor_v = 1e-12 * static_cast<double>(m);
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-        const int f = (fb0 + wm) * 16 + g + 8 * hh;
-        if (f >= frames) continue;
-        const double sc = 2.0 * tscale[f];
-        const double c0 = static_cast<double>(m) - t[static_cast<size_t>(f) * m].re;
-        const size_t o = static_cast<size_t>(f) * L;
-#pragma unroll
-        for (int n = 0; n < kONB; ++n)
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int q = (pb0 + kONB * wn + n) * 8 + 2 * t4 + u;
-                if (q >= nq) continue;
-                double A = 0.0, B = 0.0;
-#pragma unroll
-                for (int sg = kOS - 1; sg >= 0; --sg) {  // smallest groups first
-                    const double w = ldexp(1.0, -7 * (sg + 2));
-                    A = fma(static_cast<double>(acc[sg][0][n][2 * hh + u]), w, A);
-                    B = fma(static_cast<double>(acc[sg][1][n][2 * hh + u]), w, B);
-                }
-                A *= sc;
-                B *= sc;
-                const int qm = L - 1 - q;
-                const double Pp = 1.0 / fmax(c0 - 2.0 * (A - B), floor_v);
-                if (spec32) spec32[o + q] = static_cast<float>(Pp);
-                spec64[o + q] = Pp;
-                if (qm != q) {
-                    const double Pm = 1.0 / fmax(c0 - 2.0 * (A + B), floor_v);
-                    if (spec32) spec32[o + qm] = static_cast<float>(Pm);
-                    spec64[o + qm] = Pm;
-                }
-            }
-    }
-}
-
 // Peaks, one 128-thread CTA per frame (R/src/spectrum.cpp:97-188, any L >= 1 and K >= 1):
 //  1. values -> shared memory (coalesced, 8 loads in flight per thread), or read in place from global memory when
 //     the frame's workspace does not fit (long grids / large K: the workspace then lives in `gws`);
@@ -881,28 +688,6 @@ cudaError_t fm_launch_spectrum_one(const void* t, const void* zgrid, int frames,
     if (e != cudaSuccess) return e;
     spec::k_spectrum_one<<<frames, spec::kNT, smem, s>>>(static_cast<const c64*>(t), static_cast<const c64*>(zgrid), m, L,
                                                          spec32, spec64, only);
-    return cudaGetLastError();
-}
-
-// Ozaki int8 spectrum: zd = plan digits of cos / sin in fragment order (capi.cu zdig_host), td / tscale = per-batch
-// workspace (kOS * 2 * fpad * mk bytes, fpad doubles; fpad = frames rounded up to 64, mk = m rounded up to 32).
-cudaError_t fm_launch_spectrum_i8(const void* t, const int8_t* zd, int8_t* td, double* tscale, int frames, int m, int L,
-                                  float* spec32, double* spec64, cudaStream_t s) {
-    const int nkb = (m + 31) / 32;
-    const int fpad = (frames + spec::kOF - 1) / spec::kOF * spec::kOF, nfb = fpad / 16;
-    const int nq = (L + 1) / 2, npb = (nq + 31) / 32 * 4;  // zdig_host pads the pairs to 32
-    if (fpad > frames) {  // frames of the last tile beyond the batch: zero digits
-        cudaError_t e = cudaMemsetAsync(td, 0, static_cast<size_t>(spec::kOS) * 2 * fpad * nkb * 32, s);
-        if (e != cudaSuccess) return e;
-    }
-    spec::k_slice_t<<<frames, 256, 0, s>>>(static_cast<const c64*>(t), td, tscale, m, nkb, nfb);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(spec::k_spectrum_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, spec::kOSmem);
-    if (e != cudaSuccess) return e;
-    dim3 grid((nq + spec::kOQ - 1) / spec::kOQ, fpad / spec::kOF);
-    spec::k_spectrum_i8<<<grid, spec::kOT, spec::kOSmem, s>>>(td, tscale, zd, static_cast<const c64*>(t), frames, m, nkb,
-                                                              nfb, npb, L, spec32, spec64);
     return cudaGetLastError();
 }
 

@@ -9,7 +9,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KERNELS = ["cov_tc_kernel", "rmul_planes_kernel", "k_spectrum_i8", "k_small_warp", "k_peaks_rounds", "k_autocorr_fft"]
+KERNELS = ["cov_tc_kernel", "rmul_planes_kernel", "k_spectrum_tc", "k_small_warp", "k_peaks_rounds", "k_autocorr_fft"]
 WANT = {
     "duration_us": "gpu__time_duration.sum",
     "dram_read_bytes": "dram__bytes_read.sum",
