@@ -100,6 +100,23 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
+#ifdef FM_COV_TIMELINE  // experiment only: clock64 stamps of CTA 0's first 16 tiles (tools/experiments)
+__device__ long long g_cov_tl[16 * 16];
+#define COV_STAMP(tile_i, slot)                                                        \
+    do {                                                                               \
+        if (blockIdx.x == 0 && (tile_i) < 16) g_cov_tl[(tile_i) * 16 + (slot)] = clock64(); \
+    } while (0)
+#define COV_ADD(tile_i, slot, v)                                                        \
+    do {                                                                                \
+        if (blockIdx.x == 0 && (tile_i) < 16) g_cov_tl[(tile_i) * 16 + (slot)] += (v);  \
+    } while (0)
+#define COV_CLK() clock64()
+#else
+#define COV_STAMP(tile_i, slot)
+#define COV_ADD(tile_i, slot, v)
+#define COV_CLK() 0ll
+#endif
+
 // Lower-triangle tile enumeration: t -> (bi, bj) with bi >= bj.
 __device__ __forceinline__ void tile_coords(int t, int& bi, int& bj) {
     bi = 0;
@@ -221,7 +238,7 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
+    const uint32_t rank = __shfl_sync(0xffffffffu, cluster_rank(), 0);  // warp-uniform for the compiler
     const int pair = blockIdx.x >> 1;
     const int npairs = gridDim.x >> 1;
     const int nk = (n + kChunk - 1) / kChunk;
@@ -261,7 +278,7 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
     __syncthreads();
     cluster_sync_all();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform: MMA operands in uniform registers
 
     if (warp == 0) {
         // ---------------- TMA producer (one thread)
@@ -288,8 +305,8 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer (leader CTA, one thread)
-        if (rank == 0 && lane == 0) {
+        // ---------------- MMA issuer (leader CTA; the warp waits converged, one elected lane issues)
+        if (rank == 0) {
             const uint32_t id_pos = umma_idesc(false);
             const uint32_t id_neg = umma_idesc(true);
             int g = 0, t = 0;
@@ -299,24 +316,32 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
                 const bool diag = (bi == bj);
                 mbar_wait_cluster(smem_u32(acc_empty), (t & 1) ^ 1);  // both epilogues drained TMEM
                 tc_fence_after();
+                COV_STAMP(t, 0);
                 for (int kc = 0; kc < nk; ++kc, ++g) {
                     const int o = g % nO;
+                    const long long c0 = COV_CLK();
                     mbar_wait_cluster(smem_u32(&op_full[o]), (g / nO) & 1);
+                    COV_ADD(t, 9, COV_CLK() - c0);
                     tc_fence_after();
                     const uint32_t a = smem_u32(operand + o * oStride);
                     const uint32_t b = diag ? a : a + kOpBytes;
                     const uint64_t ar = umma_desc(a), ai = umma_desc(a + kPlaneBytes);
                     const uint64_t br = umma_desc(b), bim = umma_desc(b + kPlaneBytes);
                     const uint32_t acc = kc > 0 ? 1u : 0u;
-                    if (!(dbg & 2)) {
-                        umma_f16_2sm(tmem + 0, ar, br, id_pos, acc);
-                        umma_f16_2sm(tmem + 0, ai, bim, id_pos, 1u);
-                        umma_f16_2sm(tmem + 256, ai, br, id_pos, acc);
-                        umma_f16_2sm(tmem + 256, ar, bim, id_neg, 1u);
+                    if (elect_one()) {
+                        if (!(dbg & 2)) {
+                            umma_f16_2sm(tmem + 0, ar, br, id_pos, acc);
+                            umma_f16_2sm(tmem + 0, ai, bim, id_pos, 1u);
+                            umma_f16_2sm(tmem + 256, ai, br, id_pos, acc);
+                            umma_f16_2sm(tmem + 256, ar, bim, id_neg, 1u);
+                        }
+                        umma_commit_mc(smem_u32(&op_empty[o]));
                     }
-                    umma_commit_mc(smem_u32(&op_empty[o]));
+                    __syncwarp();
                 }
-                umma_commit_mc(smem_u32(acc_full));
+                if (elect_one()) umma_commit_mc(smem_u32(acc_full));
+                __syncwarp();
+                COV_STAMP(t, 1);
             }
         }
     } else if (warp < 6 || (kConv8 && warp >= (kEpi == 2 ? kThreadsP : kThreads) / 32)) {
@@ -324,8 +349,8 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
         constexpr int kFirstExtra = (kEpi == 2 ? kThreadsP : kThreads) / 32;
         constexpr int kJ = kConv8 ? 1 : 2;
         const int cw = warp < 6 ? warp - 2 : 4 + warp - kFirstExtra;
-        int g = 0;
-        for (int tile = pair; tile < total_tiles; tile += npairs) {
+        int g = 0, tt = 0;
+        for (int tile = pair; tile < total_tiles; tile += npairs, ++tt) {
             const int frame = frame_of(tile);
             int bi, bj;
             tile_coords(tile % tiles_per_frame, bi, bj);
@@ -338,8 +363,15 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
             for (int kc = 0; kc < nk; ++kc, ++g) {
                 const int s = g % nS;
                 const int o = g % nO;
+                const long long c0 = COV_CLK();
                 mbar_wait(smem_u32(&stage_full[s]), (g / nS) & 1);
+                const long long c1 = COV_CLK();
                 mbar_wait(smem_u32(&op_empty[o]), ((g / nO) & 1) ^ 1);
+                const long long c2 = COV_CLK();
+                if (warp == 2 && lane == 0) {
+                    COV_ADD(tt, 7, c1 - c0);
+                    COV_ADD(tt, 8, c2 - c1);
+                }
                 const uint8_t* st = staging + s * sStride;
                 uint8_t* op = operand + o * oStride;
                 convert_tile<kJ>(st, op, cw, lane, row_a, m, xs, amax, nonfinite);
@@ -347,6 +379,8 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
                 fence_proxy_async();
                 named_bar_sync(1, kConv8 ? 256 : 128);  // all converter warps done with this stage
                 if (warp == 2 && lane == 0) {
+                    if (kc == 0) COV_STAMP(tt, 5);
+                    if (kc == nk - 1) COV_STAMP(tt, 6);
                     mbar_arrive_local(smem_u32(&stage_empty[s]));
                     if (rank == 0) mbar_arrive_local(smem_u32(&op_full[o]));
                     else mbar_arrive_cluster(smem_u32(&op_full[o]), 0);
@@ -380,6 +414,7 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
             const int row0 = 128 * static_cast<int>(rank) + 32 * quarter;
             const int gi = row0 + lane;
             mbar_wait(smem_u32(acc_full), t & 1);
+            if (warp == 6 && lane == 0) COV_STAMP(t, 2);
             tc_fence_after();
             const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
             if (half == static_cast<int>(rank)) {
@@ -420,6 +455,7 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
                 if (rank == 0) rscale[frame] = sc;
             }
             named_bar_sync(2, 256);
+            if (warp == 6 && lane == 0) COV_STAMP(t, 3);
             const float mul = inv_n / *s_scale;  // power-of-two divisor: exact
             const int nchunks = (row0 < m && !(dbg & 4)) ? max(0, min(4, (m - 128 * half + 31) / 32)) : 0;
             for (int c = 0; c < nchunks; ++c) {
@@ -463,6 +499,7 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
             }
             tc_fence_before();
             named_bar_sync(2, 256);  // all eight epilogue warps finished reading TMEM
+            if (warp == 6 && lane == 0) COV_STAMP(t, 4);
             if (warp == 6 && lane == 0) {
                 if (rank == 0) mbar_arrive_local(smem_u32(acc_empty));
                 else mbar_arrive_cluster(smem_u32(acc_empty), 0);
@@ -627,6 +664,16 @@ __global__ void __launch_bounds__(1024) k_rescue_list(uint32_t* __restrict__ ama
 
 }  // namespace cov
 }  // namespace fmk
+
+#ifdef FM_COV_TIMELINE
+extern "C" int fm_debug_cov_timeline(long long* host, int zero) {
+    if (zero) {
+        static long long z[16 * 16] = {};
+        return static_cast<int>(cudaMemcpyToSymbol(fmk::cov::g_cov_tl, z, sizeof(z)));
+    }
+    return static_cast<int>(cudaMemcpyFromSymbol(host, fmk::cov::g_cov_tl, sizeof(long long) * 16 * 16));
+}
+#endif
 
 // Launch K1 for `frames` frames. Requirements: n even (TMA 16-byte row stride).
 // Returns a cudaError_t value (cudaErrorInvalidValue for unsupported shapes).

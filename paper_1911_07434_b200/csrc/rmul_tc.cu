@@ -112,7 +112,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + kAcc);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
+    const uint32_t rank = __shfl_sync(0xffffffffu, cluster_rank(), 0);  // warp-uniform for the compiler
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     const int nk = (2 * m + kKc - 1) / kKc;
     const uint32_t vbytes = REAL ? 16u * p * 4u : static_cast<uint32_t>(p) * 128u;
@@ -142,7 +142,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     __syncthreads();
     cluster_sync_all();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform: MMA operands in uniform registers
 
     if (warp == 0) {
         // ---------------- TMA producer: R rows + V (Omega) chunk per stage
@@ -164,8 +164,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer (leader CTA, one thread)
-        if (rank == 0 && lane == 0) {
+        // ---------------- MMA issuer (leader CTA; the warp waits converged, one elected lane issues)
+        if (rank == 0) {
             constexpr uint32_t id1 = idesc_tf32(C::kN1), id2 = idesc_tf32(C::kN2);
             int g = 0, t = 0;
             for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
@@ -178,16 +178,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     mbar_wait_cluster(smem_u32(&op_full[s]), (g / kStages) & 1);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + s * C::kStageBytes);
+                    if (elect_one()) {
 #pragma unroll
-                    for (int ks = 0; ks < kKc / 8; ++ks) {
-                        const uint32_t o = 32u * ks;
-                        umma_tf32_2sm(d, desc_sw128(st + o), desc_sw128(st + C::kOffB1 + o), id1,
-                                      (kc > 0 || ks > 0) ? 1u : 0u);
-                        umma_tf32_2sm(d, desc_sw128(st + kABytes + o), desc_sw128(st + C::kOffB2 + o), id2, 1u);
+                        for (int ks = 0; ks < kKc / 8; ++ks) {
+                            const uint32_t o = 32u * ks;
+                            umma_tf32_2sm(d, desc_sw128(st + o), desc_sw128(st + C::kOffB1 + o), id1,
+                                          (kc > 0 || ks > 0) ? 1u : 0u);
+                            umma_tf32_2sm(d, desc_sw128(st + kABytes + o), desc_sw128(st + C::kOffB2 + o), id2, 1u);
+                        }
+                        umma_commit_mc(smem_u32(&empty[s]));
                     }
-                    umma_commit_mc(smem_u32(&empty[s]));
+                    __syncwarp();
                 }
-                umma_commit_mc(smem_u32(&acc_full[b]));
+                if (elect_one()) umma_commit_mc(smem_u32(&acc_full[b]));
+                __syncwarp();
             }
         }
     } else if (warp < 6) {
@@ -391,7 +395,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM ? gram_threads<GM
     uint64_t* acc_empty = acc_full + kAcc;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + kAcc);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
+    const uint32_t rank = __shfl_sync(0xffffffffu, cluster_rank(), 0);  // warp-uniform for the compiler
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     const int nk = (2 * m + kPKc - 1) / kPKc;
     const uint32_t vbytes = REAL ? 32u * p * 4u : static_cast<uint32_t>(p) * 256u;
@@ -421,7 +425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM ? gram_threads<GM
     __syncthreads();
     cluster_sync_all();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform: MMA operands in uniform registers
 
     if (warp == 0) {
         if (lane == 0) {  // TMA producer
@@ -443,7 +447,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM ? gram_threads<GM
             }
         }
     } else if (warp == 1) {
-        if (rank == 0 && lane == 0) {  // MMA issuer
+        if (rank == 0) {  // MMA issuer: the warp waits converged, one elected lane issues
             constexpr uint32_t id1 = idesc_f16(C::kN1), id2 = idesc_f16(C::kN2);
             int g = 0, t = 0;
             for (int tile = pair; tile < total_tiles; tile += npairs, ++t) {
@@ -456,17 +460,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM ? gram_threads<GM
                     mbar_wait_cluster(smem_u32(&op_full[s]), (g / NST) & 1);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + s * C::kStageBytes);
+                    if (elect_one()) {
 #pragma unroll
-                    for (int ks = 0; ks < kPKc / 16; ++ks) {
-                        const uint32_t o = 32u * ks;
-                        umma_f16_2sm_(d, desc_sw128(st + o), desc_sw128(st + C::kOffB1 + o), id1,
-                                      (kc > 0 || ks > 0) ? 1u : 0u);
-                        if (LO)
-                            umma_f16_2sm_(d, desc_sw128(st + C::kOffLo + o), desc_sw128(st + C::kOffB2 + o), id2, 1u);
+                        for (int ks = 0; ks < kPKc / 16; ++ks) {
+                            const uint32_t o = 32u * ks;
+                            umma_f16_2sm_(d, desc_sw128(st + o), desc_sw128(st + C::kOffB1 + o), id1,
+                                          (kc > 0 || ks > 0) ? 1u : 0u);
+                            if (LO)
+                                umma_f16_2sm_(d, desc_sw128(st + C::kOffLo + o), desc_sw128(st + C::kOffB2 + o), id2,
+                                              1u);
+                        }
+                        umma_commit_mc(smem_u32(&empty[s]));
                     }
-                    umma_commit_mc(smem_u32(&empty[s]));
+                    __syncwarp();
                 }
-                umma_commit_mc(smem_u32(&acc_full[b]));
+                if (elect_one()) umma_commit_mc(smem_u32(&acc_full[b]));
+                __syncwarp();
             }
         }
     } else if (warp < 6) {

@@ -92,6 +92,15 @@ __device__ __forceinline__ void sts_v2(uint32_t a, float x, float y) {
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// One lane of a converged warp (elect.sync). MMA issue loops run on the whole warp and issue from the elected lane:
+// a loop gated on `lane == 0` makes ptxas wrap every tcgen05.mma in an ELECT / R2UR.BROADCAST / BRA.U.ANY
+// sequence that caps the issue rate far below the tensor pipe (tools/micro/umma_rate.cu: 148 vs 44 cycles per
+// M128 N48 MMA).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p;
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}" : "=r"(p));
+    return p != 0;
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
