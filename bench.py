@@ -52,7 +52,48 @@ CONFIGS = {
     # extension: config 3 with BASELINE's norm^2-weighted column sampling (not in the reference)
     "c3n": dict(m=256, n=512, k=8, method="fast1_norm2", p=32, t=1, L=3601, frames=1024, seed=2,
                 scene=dict(theta_lo_deg=-60.0, theta_hi_deg=60.0, min_sep_deg=3.0, snr_lo_db=10.0, snr_hi_db=30.0)),
+    # SURVEY §8(f)4 ToA path: fast2 on the temporal covariance T = X^H X / M (512 x 512) of seeded beat-signal
+    # frames (M = 256 antennas, N = 512 samples, K = 8 beats in [0.2, 2.9] rad/sample), beat grid [0, pi]
+    "toa": dict(m=256, n=512, k=8, method="fast2", p=16, t=2, L=3601, frames=1024, seed=6, temporal=True,
+                w0=0.0, w1=3.14159265358979323846, scene=None),
 }
+
+
+def dim_of(cfgd):
+    """Dimension of the covariance the subspace is estimated on: M (spatial) or N (ToA path, T = X^H X / M)."""
+    return cfgd["n"] if cfgd.get("temporal") else cfgd["m"]
+
+
+def beat_frames(m, n, k, seed, f0, frames, device):
+    """Seeded beat-signal frames for the ToA config, generated on the device (input data only): X(a, s) =
+    sum_k exp(j (phi_k + pi a sin(theta_k) + w_k s)) + noise at 20 dB (sigma^2 = K / 100), beat phases w_k drawn
+    in [0.2, 2.9] rad/sample with >= 0.05 separation. Returns a float32 view [frames, M, N, 2] on `device`."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(int(seed) * 1000003 + int(f0))
+    ws = torch.empty((frames, k), dtype=torch.float64)
+    for f in range(frames):
+        w = []
+        while len(w) < k:
+            c = 0.2 + 2.7 * float(torch.rand((), generator=g, dtype=torch.float64))
+            if all(abs(c - x) >= 0.05 for x in w):
+                w.append(c)
+        ws[f] = torch.tensor(sorted(w), dtype=torch.float64)
+    th = (torch.rand((frames, k), generator=g, dtype=torch.float64) * 2.0 - 1.0) * (torch.pi / 3.0)
+    ph = torch.rand((frames, k), generator=g, dtype=torch.float64) * (2.0 * torch.pi)
+    ws, th, ph = ws.to(device), th.to(device), ph.to(device)
+    a = torch.arange(m, dtype=torch.float64, device=device)
+    sidx = torch.arange(n, dtype=torch.float64, device=device)
+    x = torch.empty((frames, m, n), dtype=torch.complex64, device=device)
+    gd = torch.Generator(device=device).manual_seed(int(seed) * 7919 + int(f0))
+    sig = (k / 100.0) ** 0.5
+    for f0c in range(0, frames, 64):
+        f1 = min(frames, f0c + 64)
+        ang = (ph[f0c:f1, :, None, None] + torch.pi * torch.sin(th[f0c:f1, :, None, None]) * a[None, None, :, None]
+               + ws[f0c:f1, :, None, None] * sidx[None, None, None, :])
+        xs = torch.polar(torch.ones_like(ang), ang).sum(1)
+        nz = torch.randn((f1 - f0c, m, n, 2), generator=gd, dtype=torch.float64, device=device) * (sig / 2 ** 0.5)
+        x[f0c:f1] = (xs + torch.complex(nz[..., 0], nz[..., 1])).to(torch.complex64)
+    return torch.view_as_real(x)
 
 
 def load_peaks():
@@ -67,19 +108,22 @@ def load_peaks():
 def algorithmic(cfg):
     """SURVEY.md §8d per-frame work (real flops, complex MAC = 8) and bytes."""
     m, n, k, p, t, L = cfg["m"], cfg["n"], cfg["k"], cfg["p"], cfg["t"], cfg["L"]
+    x_bytes = 8.0 * m * n
+    if cfg.get("temporal"):  # ToA path: the N x N covariance T over M "snapshots"
+        m, n = n, m
     w_cov = 4.0 * m * (m + 1) * n
     if cfg["method"] == "fast2":
         w_rf = 4.0 * m * m * p + 8.0 * t * m * m * p
-        q = 8.0 * m * n + 4.0 * m * p + 4.0 * L + 8.0 * k
+        q = x_bytes + 4.0 * m * p + 4.0 * L + 8.0 * k
     elif cfg["method"] == "fast1":
         w_rf = 0.0
-        q = 8.0 * m * n + 8.0 * p + 4.0 * L + 8.0 * k
+        q = x_bytes + 8.0 * p + 4.0 * L + 8.0 * k
     elif cfg["method"] == "fast1_norm2":  # sampled sketch (a gather), one product R V
         w_rf = 8.0 * m * m * p
-        q = 8.0 * m * n + 4.0 * m + 4.0 * L + 8.0 * k
+        q = x_bytes + 4.0 * m + 4.0 * L + 8.0 * k
     else:
         w_rf = 0.0
-        q = 8.0 * m * n + 4.0 * L + 8.0 * k
+        q = x_bytes + 4.0 * L + 8.0 * k
     w_spec = 8.0 * k * m * L
     return {"w_cov": w_cov, "w_rf": w_rf, "w_spec": w_spec, "w_frame": w_cov + w_rf + w_spec, "q_frame": q}
 
@@ -138,16 +182,24 @@ _W = {}
 
 def _worker_init(cfg_name):
     from oracle import fastmusic_oracle as O
+    if cfg_name == "toa":
+        cfg = O.ToaConfig()
+        _W.update(O=O, cfg=cfg, toa=True,
+                  A=O.beat_steering_matrix(O.beat_grid(cfg.grid_size, cfg.w0, cfg.w1), cfg.spec.n))
+        return
     cfg = O.baseline_configs()[cfg_name]
     grid = O.baseline_grid(cfg.grid_size)
-    _W.update(O=O, cfg=cfg, grid=grid, A=O.steering_matrix(grid, cfg.spec.m))
+    _W.update(O=O, cfg=cfg, grid=grid, A=O.steering_matrix(grid, cfg.spec.m), toa=False)
 
 
 def _worker_frame(args):
     f, x = args
     O, cfg = _W["O"], _W["cfg"]
     t0 = time.perf_counter()
-    est, spec, pk = O.run_frame(cfg, x, f, _W["grid"], _W["A"])
+    if _W["toa"]:
+        est, spec, pk = O.run_toa_frame(cfg, x, f, _W["A"])
+    else:
+        est, spec, pk = O.run_frame(cfg, x, f, _W["grid"], _W["A"])
     return f, pk.cells, spec.astype("float32"), time.perf_counter() - t0
 
 
@@ -177,11 +229,14 @@ def run_reference(args):
 
     from oracle import fastmusic_oracle as O
     cfgd = CONFIGS[args.config]
-    cfg = O.baseline_configs()[args.config]
     cores = os.cpu_count() or 1
     per_step = max(1, min(cfgd["frames"], cores))
     nsamp = per_step * 4
-    xs, _, _ = O.generate_batch(cfg.base_seed, range(nsamp), cfg.spec)
+    if cfgd.get("temporal"):
+        xs, _ = O.generate_toa_batch(cfgd["seed"], range(nsamp), O.ToaConfig().spec)
+    else:
+        cfg = O.baseline_configs()[args.config]
+        xs, _, _ = O.generate_batch(cfg.base_seed, range(nsamp), cfg.spec)
     pool = mp.get_context("fork").Pool(cores, initializer=_worker_init, initargs=(args.config,))
     times = []
     for i in range(args.warmup + args.steps):
@@ -216,7 +271,9 @@ def config_dict(name, cfgd, world, mode="strong", per_gpu=None, depth=1):
           "X = %.0f MB per GPU step; consecutive steps cycle through >= 3 x L2 of distinct X copies" % (xb / 1e6))
     return {"workload": f"{name}: fast-MUSIC {cfgd['method']} M={cfgd['m']} N={cfgd['n']} K={cfgd['k']} "
                         f"p={cfgd['p']} t={cfgd['t']} L={cfgd['L']}",
-            "frames_per_gpu": per_gpu, "global_frames_per_step": gfr, "grid": "[-90, 90] deg", "l2": l2,
+            "frames_per_gpu": per_gpu, "global_frames_per_step": gfr,
+            "grid": "beat phase [0, pi] rad/sample (ToA path on T = X^H X / M)" if cfgd.get("temporal")
+            else "[-90, 90] deg", "l2": l2,
             "parallelism": (f"{mode} scaling: frames of each {gfr}-frame batch sharded over {world} GPU(s) "
                             f"[g B/G, (g+1) B/G), NCCL all-gather of peak records" if mode == "strong" else
                             f"weak scaling: {per_gpu} frames per GPU, NCCL all-gather of peak records")}
@@ -250,17 +307,21 @@ def run_ours(args):
     # synthetic input for this rank's frames, generated on the host (pinned), staged once
     xh = torch.empty((n, M, N, 2), dtype=torch.float32, pin_memory=True)
     xnp = xh.numpy().view(np.complex64).reshape(n, M, N)
-    fm.generate_frames(M, N, K, cfgd["seed"], f0, n, out=xnp, **cfgd["scene"])
+    D = dim_of(cfgd)  # dimension of the covariance (M, or N on the ToA path)
+    if cfgd.get("temporal"):
+        xh.copy_(beat_frames(M, N, K, cfgd["seed"], f0, n, dev).cpu())
+    else:
+        fm.generate_frames(M, N, K, cfgd["seed"], f0, n, out=xnp, **cfgd["scene"])
     fseeds = np.array([fm.derive(cfgd["seed"], f0 + f) for f in range(n)], np.uint64)
     tag = 4 if cfgd["method"] == "fast2" else 3
     dseeds = np.array([fm.derive(int(s), tag) for s in fseeds], np.uint64)
     omega = idx = None
     if cfgd["method"] == "fast2":
-        omega = torch.from_numpy(fm.draw_omega_batch(dseeds, M, P)).to(dev)
+        omega = torch.from_numpy(fm.draw_omega_batch(dseeds, D, P)).to(dev)
     elif cfgd["method"] == "fast1":
-        idx = torch.from_numpy(fm.draw_indices_batch(dseeds, M, P)).to(dev)
+        idx = torch.from_numpy(fm.draw_indices_batch(dseeds, D, P)).to(dev)
     elif cfgd["method"] == "fast1_norm2":  # uniforms of the weighted sampler travel in the omega slot
-        omega = torch.from_numpy(fm.draw_uniforms_batch(dseeds, M)).to(dev)
+        omega = torch.from_numpy(fm.draw_uniforms_batch(dseeds, D)).to(dev)
     xd = xh.to(dev)
     # batches in flight: small shards leave too little work per kernel to hide ramps and tails
     # (measured at N = 1, c2, tools/bench_sweep.sh: 1024 frames 0.954 / 1.075 / 1.105 M frames/s at depth 1 / 2 / 3;
@@ -271,8 +332,9 @@ def run_ours(args):
     graphs = args.graphs == "on" or (args.graphs == "auto" and depth <= 2)
 
     def make_plan(i):
+        grid = dict(theta0=cfgd["w0"], theta1=cfgd["w1"], temporal=True) if cfgd.get("temporal") else {}
         p = fm.BatchPlan(M, N, K, cfgd["method"], p=P, t=cfgd["t"], grid_size=L, max_frames=n, device=local,
-                         exact_jacobi=args.exact_jacobi)
+                         exact_jacobi=args.exact_jacobi, **grid)
         if args.subbatches > 0:
             p.set_concurrency(args.subbatches)
         p.set_graphs(graphs)
@@ -344,8 +406,10 @@ def run_ours(args):
             xw[lo:hi].copy_(xd[: hi - lo])
         omw = omega.repeat(reps, 1, 1)[:B].contiguous() if omega is not None else None
         ixw = idx.repeat(reps, 1)[:B].contiguous() if idx is not None else None
-        fw = FrameStream(lambda i: fm.BatchPlan(M, N, K, cfgd["method"], p=P, t=cfgd["t"], grid_size=L,
-                                                max_frames=B, device=local), B, B, K, world, 1, [streams[0]], dev)
+        fw = FrameStream(lambda i: fm.BatchPlan(
+            M, N, K, cfgd["method"], p=P, t=cfgd["t"], grid_size=L, max_frames=B, device=local,
+            **(dict(theta0=cfgd["w0"], theta1=cfgd["w1"], temporal=True) if cfgd.get("temporal") else {})),
+            B, B, K, world, 1, [streams[0]], dev)
         for _ in range(3):
             fw.step(xw, omw, ixw)
         dist.barrier()
@@ -416,7 +480,7 @@ def run_ours(args):
     except Exception:
         pass
     x_bytes = n * 8.0 * M * N                  # SURVEY §8(d) algorithmic bytes of the covariance: X read once
-    r_bytes = n * 8.0 * M * M                  # + R written once (complex64, or its two fp16 planes)
+    r_bytes = n * 8.0 * D * D                  # + R (or T) written once (complex64, or its two fp16 planes)
     cov_ms = alone_ms["covariance"]
     cov_prof = prof.get("cov_tc_kernel", {})
     roof = {"bound": "hbm", "kernel": "fmk::cov::cov_tc_kernel (tcgen05 cta_group::2 + TMA)",

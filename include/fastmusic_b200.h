@@ -104,6 +104,14 @@ typedef struct fm_plan_desc {
 } fm_plan_desc;
 /* exact method: full Jacobi eigensolver on every frame instead of the certified subspace iteration */
 #define FM_PLAN_EXACT_JACOBI 1
+/* ToA path (SURVEY.md §8(f)4, R/PAPER.md §II-B "the estimation of ToAs may be similarly accomplished with T"):
+ * the pipeline runs on the temporal covariance T = X^H X / M (N x N, temporal_covariance R/src/scene.cpp:161-163)
+ * instead of R. X keeps its M x N layout; K, p and the per-frame draws (omega frames x N x p, indices < N, basis
+ * frames x K x N, covariance export frames x N x N) refer to the N-dimensional problem (1 <= K < N, p <= N). The
+ * grid is the beat phase per sample, w_l = theta0 + (theta1 - theta0) l / (L - 1) in radians (w = mu tau T_s, the
+ * delay_shift of R/src/scene.cpp:91; d and lambda are ignored), and the spectrum scans the steering of T's range,
+ * b_n(w) = exp(-j w n). */
+#define FM_PLAN_TEMPORAL 2
 typedef struct fm_plan_s* fm_plan;
 
 /* Validates like the reference (R/src/estimators.cpp:74-76,88-92,105-112) and allocates
@@ -170,11 +178,11 @@ typedef struct fm_host_out {
 fm_status fm_estimate_batch_host(fm_plan plan, int64_t frames, const float* h_x, const uint64_t* draw_seeds,
                                  fm_host_out* out, void* stream);
 
-/* Batched temporal covariance, DEVICE pointers: x frames x M x N complex64 row-major ->
- * t_out frames x N x N complex64 row-major, T = X^H X / M (tensor-core covariance kernel on X^H; same
- * precision contract as fm_run_batch's R). status: frames FM_FRAME_* bits (RANGE / NONFINITE), zeroed by
- * the call. work: device scratch for X^H (frames x N x (M + M % 2) complex64), or NULL for a stream-ordered
- * allocation per call. Asynchronous on `stream`. */
+/* Batched temporal covariance (temporal_covariance R/src/scene.cpp:140-153,161-163), DEVICE
+ * pointers: x frames x M x N complex64 row-major -> t_out frames x N x N complex64 row-major, T = X^H X / M (the
+ * tensor-core covariance kernel reading X in its stored order; same precision contract as fm_run_batch's R).
+ * status: frames FM_FRAME_* bits (RANGE / NONFINITE), zeroed by the call. work: device scratch used only for odd N
+ * (frames x M x (N + 1) complex64), or NULL for a stream-ordered allocation. Asynchronous on `stream`. */
 fm_status fm_temporal_covariance_batch(const float* x, int64_t frames, int64_t m, int64_t n, float* t_out,
                                        int32_t* status, float* work, void* stream);
 

@@ -648,6 +648,107 @@ def run_frame(cfg: PathConfig, x: np.ndarray, f: int, grid: AngleGrid | None = N
     return est, spec, peaks
 
 
+# --------------------------------------------------------------------------- ToA path
+@dataclass
+class ToaSpec:
+    """Seeded beat-signal frames (the reference's discrete beat model, R/include/fastmusic/scene.hpp:57-66:
+    Y(m, n) = sum_k alpha_k rho_k kappa_k^n vartheta_k^m + noise) parametrised directly by the per-sample beat
+    phase w_k (kappa_k = exp(j w_k) = delay_shift, R/src/scene.cpp:91) instead of an FMCW chirp."""
+    m: int = 256
+    n: int = 512
+    k: int = 8
+    w_lo: float = 0.2
+    w_hi: float = 2.9
+    min_sep: float = 0.05
+    theta_lo_deg: float = -60.0
+    theta_hi_deg: float = 60.0
+    snr_db: float = 20.0
+
+
+def generate_toa_frame(fseed: int, spec: ToaSpec):
+    """One frame X (M x N complex64) and its sorted beat phases. Draws: Rng(derive(fseed, 1)) uniforms for the
+    beat phases (rejection sampling with min separation, the angle pattern of R/src/bench.cpp:191-214), then the K
+    angles, then the K gain phases (alpha_k rho_k = exp(j 2 pi u)); noise from Rng(derive(fseed, 2)) normals,
+    row-major (re, im), variance sigma^2 = K / 10^(SNR/10) (R/src/bench.cpp:262-264)."""
+    u = uniform_stream(derive(fseed, 1), 100000)
+    pos = 0
+    w = []
+    while len(w) < spec.k:
+        if pos >= u.size - 2 * spec.k:
+            raise RuntimeError("generate_toa_frame: cannot place targets at this separation")
+        c = spec.w_lo + (spec.w_hi - spec.w_lo) * u[pos]
+        pos += 1
+        if all(abs(c - x) >= spec.min_sep for x in w):
+            w.append(c)
+    w = np.sort(np.array(w))
+    lo, hi = spec.theta_lo_deg * KPI / 180.0, spec.theta_hi_deg * KPI / 180.0
+    th = lo + (hi - lo) * u[pos:pos + spec.k]
+    ph = 2.0 * KPI * u[pos + spec.k:pos + 2 * spec.k]
+    mm = np.arange(spec.m, dtype=np.float64)[:, None]
+    nn = np.arange(spec.n, dtype=np.float64)[None, :]
+    x = np.zeros((spec.m, spec.n), np.complex128)
+    for k in range(spec.k):
+        x += np.exp(1j * (ph[k] + KPI * np.sin(th[k]) * mm + w[k] * nn))
+    sigma2 = spec.k / 10.0 ** (spec.snr_db / 10.0)
+    z = normal_stream(derive(fseed, 2), 2 * spec.m * spec.n).reshape(spec.m, spec.n, 2)
+    x += np.sqrt(sigma2 / 2.0) * (z[..., 0] + 1j * z[..., 1])
+    return x.astype(np.complex64), w
+
+
+def generate_toa_batch(base_seed: int, frames, spec: ToaSpec):
+    xs, ws = zip(*(generate_toa_frame(frame_seed(base_seed, f), spec) for f in frames))
+    return np.stack(xs), np.stack(ws)
+
+
+def beat_grid(l: int, w0: float, w1: float) -> np.ndarray:
+    """Beat phases w_l = w0 + ((w1 - w0) l) / (L - 1) (the AngleGrid formula, R/src/spectrum.cpp:26-28)."""
+    return np.array([w0 + ((w1 - w0) * i) / (l - 1) for i in range(l)], np.float64)
+
+
+def beat_steering_matrix(w: np.ndarray, n: int) -> np.ndarray:
+    """Columns b_n(w) = exp(-j w n): the steering of T = Y^H Y / M, whose range is spanned by the conjugated
+    beat vectors conj(kappa_k^n) (std::polar(1, -w n) as R/src/scene.cpp:79)."""
+    out = np.empty((n, w.size), np.complex128)
+    for l in range(w.size):
+        ang = -w[l] * np.arange(n, dtype=np.float64)
+        out[:, l] = np.cos(ang) + 1j * np.sin(ang)
+    return out
+
+
+def toa_spectrum(basis: np.ndarray, w: np.ndarray, b_mat=None) -> np.ndarray:
+    """music_spectrum (R/src/spectrum.cpp:50-68) on the beat grid: P = 1 / max(N - ||U^H b(w)||^2, 1e-12 N)."""
+    n = basis.shape[0]
+    if b_mat is None:
+        b_mat = beat_steering_matrix(w, n)
+    return 1.0 / np.maximum(music_denominator(basis, b_mat), 1e-12 * n)
+
+
+@dataclass
+class ToaConfig:
+    name: str = "toa"
+    spec: ToaSpec = field(default_factory=ToaSpec)
+    frames: int = 1024
+    grid_size: int = 3601
+    w0: float = 0.0
+    w1: float = KPI
+    p: int = 16
+    t: int = 2
+    base_seed: int = 6
+    min_sep_cells: int = 3
+    method: str = "fast2"
+
+
+def run_toa_frame(cfg: ToaConfig, x: np.ndarray, f: int, b_mat=None):
+    """ToA path for one frame: T = temporal_covariance(Y) (R/src/scene.cpp:161-163) -> fast_music_2 on T
+    (R/src/estimators.cpp:104-139, Omega of dimension N from derive(frame seed, 4)) -> beat spectrum -> peaks."""
+    t = temporal_covariance(x)
+    seed = derive(frame_seed(cfg.base_seed, f), 4)
+    est = fast_music_2(t, cfg.spec.k, cfg.p, cfg.t, seed)
+    w = beat_grid(cfg.grid_size, cfg.w0, cfg.w1)
+    spec = toa_spectrum(est.basis, w, b_mat)
+    return est, spec, extract_peaks(spec, cfg.spec.k, cfg.min_sep_cells)
+
+
 def spectrum_db_error(p_test: np.ndarray, p_ref: np.ndarray, dyn_db: float = 40.0) -> float:
     """max |10 log10(P/P_ref)| where P_ref >= max(P_ref) * 10^(-dyn/10) (BASELINE gate)."""
     p_ref = np.asarray(p_ref, np.float64)

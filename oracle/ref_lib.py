@@ -28,6 +28,7 @@ def lib():
         sig = {
             "ref_steering_vector": [dbl, i64, dbl, dbl, vp],
             "ref_spatial_covariance": [vp, i64, i64, vp],
+            "ref_temporal_covariance": [vp, i64, i64, vp],
             "ref_exact_signal_subspace": [vp, i64, i64, vp, vp],
             "ref_fast_music_1": [vp, i64, i64, i64, u64, vp, vp],
             "ref_fast_music_2": [vp, i64, i64, i64, C.c_int, u64, vp, vp, vp],
@@ -65,6 +66,15 @@ def spatial_covariance(y):
     if st:
         raise ValueError(STATUS[st])
     return s
+
+
+def temporal_covariance(y):
+    y = _cm(y)
+    t = np.empty((y.shape[1], y.shape[1]), np.complex128, order="F")
+    st = lib().ref_temporal_covariance(_p(y), y.shape[0], y.shape[1], _p(t))
+    if st:
+        raise ValueError(STATUS[st])
+    return t
 
 
 def _estimate(fn, s, k, *args):

@@ -55,6 +55,11 @@ int ref_spatial_covariance(const double* y, int64_t m, int64_t n, double* s_out)
     return guard([&] { store(spatial_covariance(load(y, m, n)).mat(), s_out); }, nullptr);
 }
 
+// temporal_covariance (R/src/scene.cpp:161-163): y M x N -> T N x N
+int ref_temporal_covariance(const double* y, int64_t m, int64_t n, double* t_out) {
+    return guard([&] { store(temporal_covariance(load(y, m, n)).mat(), t_out); }, nullptr);
+}
+
 int ref_exact_signal_subspace(const double* s, int64_t m, int64_t k, double* basis, double* eig) {
     return guard([&] { store_estimate(exact_signal_subspace(HermitianMatrix(load(s, m, m)), k), basis, eig); }, nullptr);
 }

@@ -40,6 +40,7 @@ class PlanDesc(C.Structure):
 
 
 PLAN_EXACT_JACOBI = 1
+PLAN_TEMPORAL = 2
 
 
 class BatchIO(C.Structure):

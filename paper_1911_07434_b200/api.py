@@ -239,8 +239,9 @@ def temporal_covariance(y) -> np.ndarray:
 
 def temporal_covariance_batch(x, out=None, status=None, stream=None, work=None):
     """Batched T_f = X_f^H X_f / M on the device (torch tensors: x complex64 [frames, M, N] or its float32
-    view) -> complex64 [frames, N, N]; per-frame FM_FRAME_* bits in `status` (int32 [frames]). `work`:
-    optional complex64 scratch of frames * N * (M + M % 2) elements (else allocated per call)."""
+    view) -> complex64 [frames, N, N]; per-frame FM_FRAME_* bits in `status` (int32 [frames]). X is read in its
+    stored order (no transpose pass). `work`: optional complex64 scratch used only for odd N, frames * M * (N + 1)
+    elements (else allocated per call)."""
     import torch
     frames, m = x.shape[0], x.shape[1]
     n = x.shape[2] if x.dtype == torch.complex64 else x.shape[2] // 2
@@ -249,7 +250,7 @@ def temporal_covariance_batch(x, out=None, status=None, stream=None, work=None):
     if status is None:
         status = torch.empty((frames,), dtype=torch.int32, device=x.device)
     s = None if stream is None else C.c_void_p(stream.cuda_stream)
-    if work is not None and work.numel() * work.element_size() < 8 * frames * n * (m + m % 2):
+    if work is not None and (n % 2) and work.numel() * work.element_size() < 8 * frames * m * (n + 1):
         raise ValueError("temporal_covariance_batch: work too small")
     _check(LIB.fm_temporal_covariance_batch(ptr(x), frames, m, n, ptr(out), ptr(status), ptr(work), s))
     return out, status
@@ -419,13 +420,17 @@ class BatchPlan:
     """fm_plan over device tensors (torch for allocation / streams only)."""
 
     def __init__(self, m, n, k, method="fast2", p=0, t=1, grid_size=3601, theta0=-KPI / 2, theta1=KPI / 2, d=0.5,
-                 lam=1.0, min_sep_cells=3, max_frames=1, device=0, exact_jacobi=False):
+                 lam=1.0, min_sep_cells=3, max_frames=1, device=0, exact_jacobi=False, temporal=False):
         """exact_jacobi: the exact method runs the full Jacobi eigensolver on every frame (FM_PLAN_EXACT_JACOBI)
-        instead of the certified subspace iteration."""
-        flags = _capi.PLAN_EXACT_JACOBI if exact_jacobi else 0
+        instead of the certified subspace iteration. temporal: the ToA path (FM_PLAN_TEMPORAL) -- the pipeline runs
+        on T = X^H X / M (N x N); theta0 / theta1 span the beat phase per sample w (radians), the spectrum scans
+        exp(-j w n); K, p, omega, indices, basis and the covariance export refer to dimension N."""
+        flags = (_capi.PLAN_EXACT_JACOBI if exact_jacobi else 0) | (_capi.PLAN_TEMPORAL if temporal else 0)
         self.desc = _capi.PlanDesc(m, n, k, _capi.METHOD[method], p, t, grid_size, theta0, theta1, d, lam,
                                    min_sep_cells, max_frames, flags)
         self.method, self.m, self.n, self.k, self.p, self.t, self.L = method, m, n, k, p, t, grid_size
+        self.temporal = temporal
+        self.dim = n if temporal else m  # dimension of the covariance the subspace is estimated on
         self.max_frames, self.device = max_frames, device
         h = C.c_void_p()
         _check(LIB.fm_plan_create(C.byref(self.desc), device, C.byref(h)))
@@ -479,10 +484,10 @@ class BatchPlan:
         if spectrum:
             o["spectrum"] = torch.empty((frames, self.L), dtype=torch.float32, device=dev)
         if basis:
-            o["basis"] = torch.empty((frames, self.k, self.m, 2), dtype=torch.float64, device=dev)
+            o["basis"] = torch.empty((frames, self.k, self.dim, 2), dtype=torch.float64, device=dev)
             o["eigenvalues"] = torch.empty((frames, self.k), dtype=torch.float64, device=dev)
         if covariance:
-            o["covariance"] = torch.empty((frames, self.m, self.m, 2), dtype=torch.float32, device=dev)
+            o["covariance"] = torch.empty((frames, self.dim, self.dim, 2), dtype=torch.float32, device=dev)
         return o
 
     def _io(self, x, omega, indices, out):

@@ -24,7 +24,8 @@
 // ------------------------------------------------------------------ kernel launchers (other TUs)
 cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, int64_t frames, int64_t m, int64_t n,
                              cudaStream_t stream, void* planes_hi = nullptr, void* planes_lo = nullptr,
-                             float* scale = nullptr, int64_t n_true = 0, const FmCovRescue* rescue = nullptr);
+                             float* scale = nullptr, int64_t n_true = 0, const FmCovRescue* rescue = nullptr,
+                             int64_t t_rows = 0);
 size_t fm_final_fallback_scratch_bytes(int ctas);
 int fm_final_fallback_ctas();
 cudaError_t fm_launch_final_fallback(const void* C, const void* V, const void* H, void* basis, double* eig,
@@ -240,14 +241,21 @@ struct DevBuf {
     }
 };
 
-std::vector<double> zgrid_host(int64_t L, double theta0, double theta1, double d, double lambda) {
-    // theta_l = theta0 + (span * l) / (L - 1)  (R/src/spectrum.cpp:26-28 for theta0 = 0, span = pi);
-    // step = 2 pi d sin(theta) / lambda exactly as R/src/scene.cpp:76.
+// Per-element phase step of grid point th: the ULA steering exp(j 2 pi d m sin(th) / lambda) exactly as
+// R/src/scene.cpp:76, or (ToA path, `beat`) th is a beat phase w per sample (delay_shift = exp(j mu tau T_s),
+// R/src/scene.cpp:91) and the steering of T = X^H X / M is conj(kappa^n) = exp(-j w n): T's range is spanned by
+// the conjugated beat vectors.
+inline double grid_step(double th, double d, double lambda, bool beat) {
+    return beat ? -th : 2.0 * kPi * d * std::sin(th) / lambda;
+}
+
+std::vector<double> zgrid_host(int64_t L, double theta0, double theta1, double d, double lambda, bool beat) {
+    // theta_l = theta0 + (span * l) / (L - 1)  (R/src/spectrum.cpp:26-28 for theta0 = 0, span = pi)
     std::vector<double> z(static_cast<size_t>(2 * L));
     const double span = theta1 - theta0;
     for (int64_t l = 0; l < L; ++l) {
         const double th = theta0 + (span * static_cast<double>(l)) / static_cast<double>(L - 1);
-        const double step = 2.0 * kPi * d * std::sin(th) / lambda;
+        const double step = grid_step(th, d, lambda, beat);
         z[2 * l] = std::cos(step);
         z[2 * l + 1] = std::sin(step);
     }
@@ -257,14 +265,15 @@ std::vector<double> zgrid_host(int64_t L, double theta0, double theta1, double d
 // Digits of the cos / sin table for the tcgen05 spectrum (spectrum_tc.cu): for pair q < nq and delta < m,
 // z = (cos, sin)(delta phi_q) (angle in fp64, glibc) as 5 signed base-128 digits of z / 2, in the zK layout
 // [pair tile of 48][K block of 32][plane = s * 2 + cs][canonical 48 x 32 tile] (zero padding past nq and m).
-std::vector<int8_t> zdig_host_k(int64_t L, double theta0, double theta1, double d, double lambda, int64_t m) {
+std::vector<int8_t> zdig_host_k(int64_t L, double theta0, double theta1, double d, double lambda, int64_t m,
+                                bool beat) {
     constexpr int kS = 5;
     const int64_t nq = (L + 1) / 2, nqp = fm_spectrum_tc_pairs_pad(static_cast<int>(L)), mk = (m + 31) / 32 * 32;
     std::vector<int8_t> z(static_cast<size_t>(kS * 2 * nqp * mk), 0);
     const double span = theta1 - theta0;
     for (int64_t q = 0; q < nq; ++q) {
         const double th = theta0 + (span * static_cast<double>(q)) / static_cast<double>(L - 1);
-        const double step = 2.0 * kPi * d * std::sin(th) / lambda;
+        const double step = grid_step(th, d, lambda, beat);
         for (int64_t dl = 0; dl < m; ++dl) {
             const double ang = static_cast<double>(dl) * step;
             double r[2] = {0.5 * std::cos(ang), 0.5 * std::sin(ang)};
@@ -494,7 +503,11 @@ struct fm_plan_s {
     double* tscale = nullptr; // per batch: power-of-two scale of each frame's t
     size_t tdig_rows = 0;     // frame rows of tdig / tscale (sub-batch i uses rows f0 + 64 i ..)
     int32_t* scratch_status = nullptr;  // frames
-    float* x_pad = nullptr;             // odd N: frames x M x (N + 1) complex64
+    float* x_pad = nullptr;             // odd X row length: frames x rows x (row length + 1) complex64
+    // ToA path (FM_PLAN_TEMPORAL): d describes the N-dimensional problem on T = X^H X / M (d.m = N, d.n = M);
+    // X itself is xrows x xlen per frame (M x N). Spatial plans: xrows = d.m, xlen = d.n.
+    bool temporal = false;
+    int64_t xrows = 0, xlen = 0;
     float* rscale = nullptr;            // frames: s_f of the fp16 hi/lo R planes (plane mode)
     // covariance rescue pass (cov_tc.cu): per-frame max |x|, out-of-range list, counts (one per sub-batch), prescale
     uint32_t* amax = nullptr;
@@ -627,12 +640,23 @@ static fm_status validate_desc(const fm_plan_desc* d) {
 extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm_plan* out) {
     if (!out) return fail(FM_EINVAL, "fm_plan_create: null out");
     *out = nullptr;
-    fm_status st = validate_desc(desc);
+    if (!desc) return fail(FM_EINVAL, "fm_plan_create: null descriptor");
+    fm_plan_desc vd = *desc;  // ToA path: validated as the N-dimensional problem on T (K < N, p <= N)
+    if (desc->flags & FM_PLAN_TEMPORAL) std::swap(vd.m, vd.n);
+    fm_status st = validate_desc(&vd);
     if (st != FM_OK) return st;
     FM_CUDA_OK(cudaSetDevice(device));
     auto* pl = new fm_plan_s();
     pl->d = *desc;
     pl->device = device;
+    pl->temporal = (desc->flags & FM_PLAN_TEMPORAL) != 0;
+    pl->xrows = desc->m;
+    pl->xlen = desc->n;
+    if (pl->temporal) {  // the pipeline runs on T = X^H X / M: dimension N, M "snapshots" (validated below)
+        pl->d.m = desc->n;
+        pl->d.n = desc->m;
+    }
+    desc = &pl->d;  // everything below sizes the N-dimensional problem in temporal mode
     const size_t B = static_cast<size_t>(desc->max_frames), M = desc->m, K = desc->k, L = desc->grid_size;
     pl->pe = exact_fast_p(*desc);
     const size_t P = desc->method == FM_METHOD_EXACT ? static_cast<size_t>(pl->pe) : static_cast<size_t>(desc->p);
@@ -664,7 +688,7 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
         chk(pl->get(&fb, fm_final_fallback_scratch_bytes(fm_final_fallback_ctas())));
         pl->fb_scratch = fb;
     }
-    if (desc->n & 1) chk(pl->get(&pl->x_pad, B * M * (static_cast<size_t>(desc->n) + 1) * 2));
+    if (pl->xlen & 1) chk(pl->get(&pl->x_pad, B * static_cast<size_t>(pl->xrows) * (static_cast<size_t>(pl->xlen) + 1) * 2));
     if (desc->method == FM_METHOD_FAST1_NORM2) chk(pl->get(&pl->omega_e, B * M * P));  // selection Omega = E_I
     if ((desc->method == FM_METHOD_FAST2 || desc->method == FM_METHOD_FAST1_NORM2) && M <= 256 && P <= 16) {
         chk(pl->get(&pl->gpart, B * 2 * P * P * 2));  // Gram halves from the product epilogue (plane path)
@@ -699,7 +723,7 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
             return fm_fail_cuda(e, "fm_plan_create exact omega", __FILE__, __LINE__);
         }
     }
-    const auto z = zgrid_host(desc->grid_size, desc->theta0, desc->theta1, desc->d, desc->lambda);
+    const auto z = zgrid_host(desc->grid_size, desc->theta0, desc->theta1, desc->d, desc->lambda, pl->temporal);
     e = cudaMemcpy(pl->zgrid, z.data(), sizeof(double) * z.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         delete pl;
@@ -707,7 +731,8 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
     }
     if (desc->theta0 == -desc->theta1) {
         const size_t mk = (static_cast<size_t>(desc->m) + 31) / 32 * 32;
-        const auto zkh = zdig_host_k(desc->grid_size, desc->theta0, desc->theta1, desc->d, desc->lambda, desc->m);
+        const auto zkh =
+            zdig_host_k(desc->grid_size, desc->theta0, desc->theta1, desc->d, desc->lambda, desc->m, pl->temporal);
         e = pl->get(&pl->zk, zkh.size());
         if (e == cudaSuccess) e = cudaMemcpy(pl->zk, zkh.data(), zkh.size(), cudaMemcpyHostToDevice);
         pl->tdig_rows = B + 128 * 16;
@@ -1089,14 +1114,15 @@ static fm_status run_batch_at(fm_plan pl, int64_t ws0, int64_t frames, const fm_
     const int nsub = auto_subbatches(pl, frames);
     const bool planes = plane_mode(pl) && !io->covariance;
     pl->last_planes = planes;
-    const int64_t nx = pl->x_pad ? pl->d.n + 1 : pl->d.n;  // row length fed to the covariance kernel
+    const int64_t nx = pl->x_pad ? pl->xlen + 1 : pl->xlen;  // X row length fed to the covariance kernel
+    const int64_t trows = pl->temporal ? pl->xrows : 0;     // temporal mode: contraction over X's rows
     const size_t MM2 = static_cast<size_t>(pl->d.m) * pl->d.m * 2;
     auto xin = [&](const float* x, int64_t f0, int64_t nf, cudaStream_t q) -> const float* {
         if (!pl->x_pad) return x;
-        float* xp = pl->x_pad + f0 * pl->d.m * nx * 2;
-        k_pad_rows<<<static_cast<unsigned>(nf * pl->d.m), 128, 0, q>>>(reinterpret_cast<const float2*>(x),
-                                                                      reinterpret_cast<float2*>(xp), nf * pl->d.m,
-                                                                      static_cast<int>(pl->d.n));
+        float* xp = pl->x_pad + f0 * pl->xrows * nx * 2;
+        k_pad_rows<<<static_cast<unsigned>(nf * pl->xrows), 128, 0, q>>>(reinterpret_cast<const float2*>(x),
+                                                                        reinterpret_cast<float2*>(xp), nf * pl->xrows,
+                                                                        static_cast<int>(pl->xlen));
         return xp;
     };
     if (nsub <= 1) {
@@ -1105,7 +1131,7 @@ static fm_status run_batch_at(fm_plan pl, int64_t ws0, int64_t frames, const fm_
         const WorkView w = work_view(pl, ws0);
         mark(pl, 0, s);
         FM_LAUNCH(fm_launch_cov_tc(xin(io->x, ws0, frames, s), R, io->status, frames, pl->d.m, nx, s, pv.hi, pv.lo,
-                                   pv.scale, pl->d.n, &w.resc));
+                                   pv.scale, pl->d.n, &w.resc, trows));
         mark(pl, 1, s);
         return run_post_cov(pl, frames, io, R, s, w, true, pv);
     }
@@ -1135,7 +1161,7 @@ static fm_status run_batch_at(fm_plan pl, int64_t ws0, int64_t frames, const fm_
         {
             cudaStream_t s = q;  // FM_LAUNCH synchronises `s` in debug mode
             FM_LAUNCH(fm_launch_cov_tc(xin(o.x, ws0 + f0, nf, q), R, o.status, nf, pl->d.m, nx, q, pv.hi, pv.lo,
-                                       pv.scale, pl->d.n, &w.resc));
+                                       pv.scale, pl->d.n, &w.resc, trows));
         }
         if (i == 0) mark(pl, 1, q);
         fm_status st = run_post_cov(pl, nf, &o, R, q, w, i == 0, pv);
@@ -1442,49 +1468,26 @@ extern "C" fm_status fm_z_temporal_covariance(int64_t m, int64_t n, const double
     return fm_z_spatial_covariance(n, m, yh.data(), t_out);
 }
 
-namespace {
-// Y = X^H per frame: x (frames x M x N, row-major complex64) -> y (frames x N x Mp, Mp = M rounded up to
-// even with a zero column: the covariance kernel's TMA row pitch must be a multiple of 16 B; a zero
-// snapshot adds nothing). 32 x 32 tiles through shared memory, coalesced reads and writes.
-__global__ void k_conj_transpose(const float2* __restrict__ x, float2* __restrict__ y, int m, int n, int mp,
-                                 int f0) {
-    __shared__ float2 tile[32][33];
-    const int64_t f = f0 + blockIdx.z;
-    const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
-    const float2* xf = x + f * m * n;
-    float2* yf = y + f * n * mp;
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-        const int i = i0 + r, j = j0 + threadIdx.x;
-        tile[r][threadIdx.x] = (i < m && j < n) ? xf[static_cast<int64_t>(i) * n + j] : make_float2(0.f, 0.f);
-    }
-    __syncthreads();
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-        const int j = j0 + r, i = i0 + threadIdx.x;
-        if (j < n && i < mp) {
-            const float2 v = tile[threadIdx.x][r];
-            yf[static_cast<int64_t>(j) * mp + i] = make_float2(v.x, -v.y);
-        }
-    }
-}
-}  // namespace
-
+// T = X^H X / M read straight from X's stored order (cov_tc.cu temporal mode: TMA boxes of 16 antenna rows x 128
+// snapshots, transposed by the converter warps); odd N pads each row with one zero snapshot into `work` first (the
+// TMA row pitch must be a multiple of 16 B), which adds nothing to T.
 extern "C" fm_status fm_temporal_covariance_batch(const float* x, int64_t frames, int64_t m, int64_t n,
                                                   float* t_out, int32_t* status, float* work, void* stream) {
     if (frames < 1 || m < 1 || n < 1) return fail(FM_EINVAL, "temporal_covariance: empty signal matrix");
     if (!x || !t_out || !status) return fail(FM_EINVAL, "temporal_covariance: null pointer");
-    if (frames * n > 0x7fffffff || m > 0x3fffffff) return fail(FM_EINVAL, "temporal_covariance: batch too large");
+    if (frames * n > 0x7fffffff || frames * m > 0x7fffffff) return fail(FM_EINVAL, "temporal_covariance: batch too large");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int64_t mp = m + (m & 1);
-    float* y = work;
-    if (!y) FM_CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&y), sizeof(float) * 2 * frames * n * mp, s));
+    const int64_t np = n + (n & 1);
+    const float* xin = x;
+    float* pad = nullptr;
     FM_CUDA_OK(cudaMemsetAsync(status, 0, sizeof(int32_t) * frames, s));
-    const dim3 blk(32, 8);
-    for (int64_t f0 = 0; f0 < frames; f0 += 65535) {
-        const dim3 grd(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((mp + 31) / 32),
-                       static_cast<unsigned>(std::min<int64_t>(65535, frames - f0)));
-        k_conj_transpose<<<grd, blk, 0, s>>>(reinterpret_cast<const float2*>(x), reinterpret_cast<float2*>(y),
-                                             static_cast<int>(m), static_cast<int>(n), static_cast<int>(mp),
-                                             static_cast<int>(f0));
+    if (n & 1) {
+        pad = work;
+        if (!pad) FM_CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&pad), sizeof(float) * 2 * frames * m * np, s));
+        k_pad_rows<<<static_cast<unsigned>(frames * m), 128, 0, s>>>(reinterpret_cast<const float2*>(x),
+                                                                    reinterpret_cast<float2*>(pad), frames * m,
+                                                                    static_cast<int>(n));
+        xin = pad;
     }
     cudaError_t e = cudaGetLastError();
     // rescue-pass workspace (out-of-range frames recomputed with a power-of-two prescale, cov_tc.cu)
@@ -1498,10 +1501,10 @@ extern "C" fm_status fm_temporal_covariance_batch(const float* x, int64_t frames
         rs.list = reinterpret_cast<int32_t*>(rs.amax + frames);
         rs.xscale = reinterpret_cast<float*>(rs.list + frames);
         rs.count = reinterpret_cast<int32_t*>(rs.xscale + frames);
-        e = fm_launch_cov_tc(y, t_out, status, frames, n, mp, s, nullptr, nullptr, nullptr, m, &rs);
+        e = fm_launch_cov_tc(xin, t_out, status, frames, n, np, s, nullptr, nullptr, nullptr, m, &rs, m);
     }
     if (rbuf) cudaFreeAsync(rbuf, s);
-    if (!work) cudaFreeAsync(y, s);
+    if (pad && !work) cudaFreeAsync(pad, s);
     if (e != cudaSuccess) return fm_fail_cuda(e, "fm_temporal_covariance_batch", __FILE__, __LINE__);
     return FM_OK;
 }
@@ -1655,7 +1658,7 @@ extern "C" fm_status fm_z_music_spectrum(int64_t m, int64_t kb, const double* ba
     FM_CUDA_OK(dDev.alloc(1));
     if (kb > 0)
         FM_CUDA_OK(cudaMemcpyAsync(dB.p, basis, sizeof(double) * 2 * m * kb, cudaMemcpyHostToDevice, c.s));
-    const auto z = zgrid_host(L, theta0, theta1, d, lambda);
+    const auto z = zgrid_host(L, theta0, theta1, d, lambda, false);
     FM_CUDA_OK(cudaMemcpyAsync(dZ.p, z.data(), sizeof(double) * z.size(), cudaMemcpyHostToDevice, c.s));
     if (kb > 0) {
         double dev = 0.0;

@@ -23,6 +23,11 @@
 // bits lost to subnormals) are listed by k_rescue_list and recomputed by a second launch over the list only,
 // with X scaled by a power of two 2^e (exact) so that max |x| lands in [2^6, 2^7), and 2^-2e folded into the
 // epilogue's 1/N. Frames in range cost one atomicMax per converter warp and tile; an empty list exits at once.
+// Temporal mode (temporal_covariance R/src/scene.cpp:140-153,161-163): T = X^H X / M is the same
+// Hermitian product on Z = X^H, whose operand rows are X's columns (snapshots) and whose contraction runs over X's
+// rows (antennas). X is read in its stored order: the TMA box is 16 antenna rows x 128 snapshots (a 3D map
+// {row length, M, frames}, so rows past M zero-fill instead of reading the next frame), and the converter warps
+// transpose while they convert (Z_ik = conj X_ki), writing the same K-major fp16 planes. No transpose pass.
 
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -176,6 +181,45 @@ __device__ __forceinline__ void convert_tile(const uint8_t* stage, uint8_t* op, 
     }
 }
 
+// Temporal mode: the staging tile is 16 antenna rows (K) x 128 snapshots (operand rows) of complex fp32, plain
+// (SWIZZLE_NONE) rows of 1 KB: element (k, r) at k * 1024 + r * 8. Same lane -> (row r, 8-K half q) mapping and
+// output layout as convert_tile; each lane gathers its 8 K values down a column (conflict-free: the 16 lanes of
+// a half read 128 contiguous bytes of one row). Z = X^H: the imaginary part is negated.
+template <int kJ>
+__device__ __forceinline__ void convert_tile_t(const uint8_t* stage, uint8_t* op, int cw, int lane, int row_base,
+                                               int m_rows, float xs, float& amax, bool& nonfinite) {
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+        const int r = 16 * kJ * cw + (lane & 7) + 8 * (lane >> 4) + 16 * j;
+        const int q = (lane >> 3) & 1;
+        const bool valid = (row_base + r) < m_rows;
+        float re[8], im[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const float2 v = *reinterpret_cast<const float2*>(stage + (8 * q + u) * 1024 + r * 8);
+            re[u] = valid ? v.x * xs : 0.f;
+            im[u] = valid ? -v.y * xs : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            amax = fmaxf(amax, fmaxf(fabsf(re[u]), fabsf(im[u])));
+            nonfinite |= !(isfinite(re[u]) && isfinite(im[u]));
+        }
+        uint4 pr, pi;
+        pr.x = pack_half2(re[0], re[1]);
+        pr.y = pack_half2(re[2], re[3]);
+        pr.z = pack_half2(re[4], re[5]);
+        pr.w = pack_half2(re[6], re[7]);
+        pi.x = pack_half2(im[0], im[1]);
+        pi.y = pack_half2(im[2], im[3]);
+        pi.z = pack_half2(im[4], im[5]);
+        pi.w = pack_half2(im[6], im[7]);
+        const int off = (r >> 3) * 256 + q * 128 + (r & 7) * 16;
+        *reinterpret_cast<uint4*>(op + off) = pr;
+        *reinterpret_cast<uint4*>(op + kPlaneBytes + off) = pi;
+    }
+}
+
 // Persistent: CTA pair `pair` processes tiles pair, pair + npairs, ... Warp roles:
 //   w0 TMA producer | w1 MMA issuer (leader) + TMEM owner | w2..w5 converters | w6..w9 epilogue.
 // The epilogue of tile i (TMEM -> fp32 R) overlaps the TMA + fp16 conversion of tile i + 1;
@@ -198,7 +242,7 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
                   int m, int n, int tiles_per_frame, int total_tiles, float* __restrict__ rscale,
                   float inv_n_true, int dbg, int ring, const int32_t* __restrict__ flist,
                   const int32_t* __restrict__ fcount, const float* __restrict__ xscale,
-                  uint32_t* __restrict__ amax_out) {
+                  uint32_t* __restrict__ amax_out, int temporal) {
     constexpr bool kTmaStore = kEpi >= 1;
     // rescue pass: only the listed frames (the count is device-resident; every CTA of the grid reads the same
     // value, so an empty list ends all of them before any barrier or TMEM allocation)
@@ -292,15 +336,23 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
                 const uint32_t bytes = diag ? kStageBytes : 2 * kStageBytes;
                 const int ya = frame * m + 256 * bi + 128 * static_cast<int>(rank);
                 const int yb = frame * m + 256 * bj + 128 * static_cast<int>(rank);
+                // temporal: x = first snapshot (float offset) of the operand rows, y = first antenna row, z = frame
+                const int ta = 2 * (256 * bi + 128 * static_cast<int>(rank));
+                const int tb = 2 * (256 * bj + 128 * static_cast<int>(rank));
                 for (int kc = 0; kc < nk; ++kc, ++g) {
                     const int s = g % nS;
                     mbar_wait(smem_u32(&stage_empty[s]), ((g / nS) & 1) ^ 1);
                     const uint32_t full = smem_u32(&stage_full[s]);
                     mbar_arrive_expect_tx(full, bytes);
                     uint8_t* st = staging + s * sStride;
-                    const int x = 2 * kChunk * kc;
-                    tma_load_2d(smem_u32(st), &xmap, full, x, ya);
-                    if (!diag) tma_load_2d(smem_u32(st + kStageBytes), &xmap, full, x, yb);
+                    if (temporal) {
+                        tma_load_3d(smem_u32(st), &xmap, full, ta, kChunk * kc, frame);
+                        if (!diag) tma_load_3d(smem_u32(st + kStageBytes), &xmap, full, tb, kChunk * kc, frame);
+                    } else {
+                        const int x = 2 * kChunk * kc;
+                        tma_load_2d(smem_u32(st), &xmap, full, x, ya);
+                        if (!diag) tma_load_2d(smem_u32(st + kStageBytes), &xmap, full, x, yb);
+                    }
                 }
             }
         }
@@ -374,8 +426,15 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
                 }
                 const uint8_t* st = staging + s * sStride;
                 uint8_t* op = operand + o * oStride;
-                convert_tile<kJ>(st, op, cw, lane, row_a, m, xs, amax, nonfinite);
-                if (!diag) convert_tile<kJ>(st + kStageBytes, op + kOpBytes, cw, lane, row_b, m, xs, amax, nonfinite);
+                if (temporal) {
+                    convert_tile_t<kJ>(st, op, cw, lane, row_a, m, xs, amax, nonfinite);
+                    if (!diag)
+                        convert_tile_t<kJ>(st + kStageBytes, op + kOpBytes, cw, lane, row_b, m, xs, amax, nonfinite);
+                } else {
+                    convert_tile<kJ>(st, op, cw, lane, row_a, m, xs, amax, nonfinite);
+                    if (!diag)
+                        convert_tile<kJ>(st + kStageBytes, op + kOpBytes, cw, lane, row_b, m, xs, amax, nonfinite);
+                }
                 fence_proxy_async();
                 named_bar_sync(1, kConv8 ? 256 : 128);  // all converter warps done with this stage
                 if (warp == 2 && lane == 0) {
@@ -683,24 +742,38 @@ extern "C" int fm_debug_cov_timeline(long long* host, int zero) {
 // rescue list / count and the prescale; with it the call enqueues pass 1, k_rescue_list and the rescue pass.
 cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, int64_t frames, int64_t m, int64_t n,
                              cudaStream_t stream, void* planes_hi, void* planes_lo, float* scale, int64_t n_true,
-                             const FmCovRescue* rescue) {
+                             const FmCovRescue* rescue, int64_t t_rows) {
     if (n_true <= 0) n_true = n;  // n: row length of d_x (even); n_true: snapshots for the 1/N scaling
     using namespace fmk::cov;
+    const bool temporal = t_rows > 0;  // d_x: frames x t_rows x n; output m x m (m <= n), contraction over t_rows
     if (frames < 1 || m < 1 || n < 2 || (n & 1) || frames * m > 0x7fffffff || 2 * n > 0x7fffffff)
         return cudaErrorInvalidValue;
+    if (temporal && (m > n || t_rows > 0x7fffffff || frames * t_rows > 0x7fffffff)) return cudaErrorInvalidValue;
     const bool planes = planes_hi != nullptr;
     if (planes && (m > 256 || (m & 1) || !planes_lo || !scale)) return cudaErrorInvalidValue;
     EncodeTiledFn enc = get_encode();
     if (!enc) return cudaErrorNotSupported;
     CUtensorMap map, rmap, mmap;
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * n), static_cast<cuuint64_t>(frames * m)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(8 * n)};
-    cuuint32_t box[2] = {32, 128};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(d_x), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult cr;
+    if (temporal) {  // boxes of 16 antenna rows x 128 snapshots, rows past t_rows zero-filled per frame
+        cuuint64_t tdims[3] = {static_cast<cuuint64_t>(2 * n), static_cast<cuuint64_t>(t_rows),
+                               static_cast<cuuint64_t>(frames)};
+        cuuint64_t tstr[2] = {static_cast<cuuint64_t>(8 * n), static_cast<cuuint64_t>(8 * n * t_rows)};
+        cuuint32_t tbox[3] = {256, 16, 1};
+        cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(d_x), tdims, tstr, tbox, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * n), static_cast<cuuint64_t>(frames * m)};
+        cuuint64_t strides[1] = {static_cast<cuuint64_t>(8 * n)};
+        cuuint32_t box[2] = {32, 128};
+        cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(d_x), dims, strides, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    const int64_t nk_len = temporal ? t_rows : n;  // contraction length seen by the kernel
     const int epi = planes ? 2 : ((m % 2) == 0 ? 1 : 0);  // R row pitch 8M bytes must be a multiple of 16
     if (epi == 2) {
         cuuint64_t pdims[3] = {static_cast<cuuint64_t>(2 * m), static_cast<cuuint64_t>(m),
@@ -768,10 +841,11 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
         const int smem = 1024 + ring_region_bytes(ring, tiles_per_frame == 1) + kSmemEpilogue + kSmemBarriers;
         const bool r = rescue != nullptr;
         kern<<<grid, threads, smem, stream>>>(map, rmap, mmap, d_r, d_status, static_cast<int>(m),
-                                              static_cast<int>(n), tiles_per_frame, static_cast<int>(tiles), scale,
-                                              static_cast<float>(1.0 / static_cast<double>(n_true)), 0, ring,
+                                              static_cast<int>(nk_len), tiles_per_frame, static_cast<int>(tiles),
+                                              scale, static_cast<float>(1.0 / static_cast<double>(n_true)), 0, ring,
                                               pass2 ? rescue->list : nullptr, pass2 ? rescue->count : nullptr,
-                                              pass2 ? rescue->xscale : nullptr, (r && !pass2) ? rescue->amax : nullptr);
+                                              pass2 ? rescue->xscale : nullptr, (r && !pass2) ? rescue->amax : nullptr,
+                                              temporal ? 1 : 0);
     };
     auto launch = [&](bool pass2) {
         if (conv4) {
