@@ -52,6 +52,9 @@ CONFIGS = {
     # extension: config 3 with BASELINE's norm^2-weighted column sampling (not in the reference)
     "c3n": dict(m=256, n=512, k=8, method="fast1_norm2", p=32, t=1, L=3601, frames=1024, seed=2,
                 scene=dict(theta_lo_deg=-60.0, theta_hi_deg=60.0, min_sep_deg=3.0, snr_lo_db=10.0, snr_hi_db=30.0)),
+    # SURVEY §8(f)3 block-Lanczos (the paper's accurate baseline; block = K, iteration cap 200) on the c2 frames
+    "c2lz": dict(m=256, n=512, k=8, method="lanczos", p=0, t=200, L=3601, frames=1024, seed=2,
+                 scene=dict(theta_lo_deg=-60.0, theta_hi_deg=60.0, min_sep_deg=3.0, snr_lo_db=10.0, snr_hi_db=30.0)),
     # SURVEY §8(f)4 ToA path: fast2 on the temporal covariance T = X^H X / M (512 x 512) of seeded beat-signal
     # frames (M = 256 antennas, N = 512 samples, K = 8 beats in [0.2, 2.9] rad/sample), beat grid [0, pi]
     "toa": dict(m=256, n=512, k=8, method="fast2", p=16, t=2, L=3601, frames=1024, seed=6, temporal=True,

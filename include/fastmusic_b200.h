@@ -44,10 +44,15 @@ typedef int32_t fm_status;
 #define FM_METHOD_EXACT 0
 #define FM_METHOD_FAST1 1
 #define FM_METHOD_FAST2 2
+/* block_lanczos_subspace (R/src/estimators.cpp:154-222, Method::Lanczos = 3): fm_plan_desc.p is the block
+ * (0 selects K, R/include/fastmusic/bench.hpp:61; block <= 16), .t the iteration cap (>= 1; the reference's bench
+ * uses 200). The whole Krylov loop runs on the device, one CTA per frame (lanczos_batch.cu); a frame that hits the
+ * cap, or needs more than 72 basis columns, is flagged FM_FRAME_NOCONV. No per-frame draws. */
+#define FM_METHOD_LANCZOS 3
 /* Extension (BASELINE config 3's wording, not in the reference): p columns of R drawn without
  * replacement with probability proportional to their squared norm (Efraimidis-Spirakis keys log(u_j) / w_j,
  * u_j host uniforms from the reference RNG), orthonormalised, one product R V, Nystrom tail as fast2. */
-#define FM_METHOD_FAST1_NORM2 3
+#define FM_METHOD_FAST1_NORM2 16
 
 int32_t fm_abi_version(void);
 const char* fm_status_string(fm_status s);
@@ -230,10 +235,19 @@ fm_status fm_z_fast_music_1(int64_t m, const double* s, int64_t k, int64_t p, ui
 fm_status fm_z_fast_music_2(int64_t m, const double* s, int64_t k, int64_t p, int32_t t, uint64_t seed,
                             double* basis, double* eigenvalues, double* cost_seconds, int64_t* deficient_column);
 /* block_lanczos_subspace, R/src/estimators.cpp:154-222 (block Krylov, full reorthogonalisation, top-K Ritz
- * values stable to 1e-10 relative on two consecutive checks); fp64 on the GPU, M <= 384, block <= 64.
+ * values stable to 1e-10 relative on two consecutive checks); fp64 on the GPU: the device Krylov loop of
+ * lanczos_batch.cu for block <= 16 and bases up to 72 columns, else the host-driven loop (M <= 384, block <= 64).
  * FM_ENOCONV at the iteration cap with the last relative change in *last_change (may be NULL). */
 fm_status fm_z_block_lanczos_subspace(int64_t m, const double* s, int64_t k, int64_t block, int32_t max_iterations,
                                       double* basis, double* eigenvalues, double* cost_seconds, double* last_change);
+/* Batched block_lanczos_subspace on DEVICE covariance matrices: s frames x M x M complex64
+ * (row-major, Hermitian), the whole Krylov loop of R/src/estimators.cpp:154-222 in fp64 on the device, one CTA per
+ * frame (lanczos_batch.cu). basis: frames x K x M complex128 (column-major per frame), eigenvalues frames x K,
+ * status frames FM_FRAME_* (NOCONV: iteration cap, or more than 72 basis columns needed), iterations (may be NULL):
+ * frames x (10000 * Krylov iterations + Jacobi sweeps). block <= 16. Asynchronous on `stream`. */
+fm_status fm_block_lanczos_batch(const float* s, int64_t frames, int64_t m, int64_t k, int64_t block,
+                                 int32_t max_iterations, double* basis, double* eigenvalues, int32_t* status,
+                                 int32_t* iterations, void* stream);
 /* music_spectrum, R/src/spectrum.cpp:50-68 on theta_l = theta0 + ((theta1-theta0)*l)/(L-1) */
 fm_status fm_z_music_spectrum(int64_t m, int64_t kb, const double* basis, int64_t grid_size, double theta0,
                               double theta1, double d, double lambda, double* values);

@@ -616,7 +616,11 @@ def baseline_configs():
     # extension: config 3 with BASELINE's own sampling wording (norm^2-weighted; not in the reference, F6)
     c3n = PathConfig("c3n", "fast1_norm2", SceneSpec(256, 512, 8, -60.0, 60.0, 3.0, 10.0, 30.0),
                      1024, 3601, p=32, base_seed=2)
-    return {c.name: c for c in (c1, c2, c3, c4, c5, c3n)}
+    # the paper's accurate baseline (block-Lanczos, block = K, cap 200 as R/include/fastmusic/bench.hpp:61-62)
+    # on the c2 frames
+    c2lz = PathConfig("c2lz", "lanczos", SceneSpec(256, 512, 8, -60.0, 60.0, 3.0, 10.0, 30.0),
+                      1024, 3601, p=0, t=200, base_seed=2)
+    return {c.name: c for c in (c1, c2, c3, c4, c5, c3n, c2lz)}
 
 
 def frame_inputs(cfg: PathConfig, f: int):
@@ -641,6 +645,8 @@ def run_frame(cfg: PathConfig, x: np.ndarray, f: int, grid: AngleGrid | None = N
         est = fast_music_1(s, k, cfg.p, fin["seed"])
     elif cfg.method == "fast1_norm2":
         est = fast_music_1_norm2(s, k, cfg.p, fin["seed"])
+    elif cfg.method == "lanczos":  # block = p (0 selects K, R/include/fastmusic/bench.hpp:61), cap t
+        est = block_lanczos_subspace(s, k, cfg.p or k, cfg.t)
     else:
         est = exact_signal_subspace(s, k)
     spec = music_spectrum(est.basis, grid, a_mat=a_mat)

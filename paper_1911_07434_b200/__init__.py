@@ -6,7 +6,7 @@ reference estimator API over that ABI. Importing fails loudly if the library is 
 """
 from .api import (AngleGrid, BatchPlan, CudaError, Fast1Params, Fast2Params, NonConvergenceError, PeakSet,  # noqa: F401
                   PseudoSpectrum, RankDeficiencyError, SingularMatrixError, SubspaceEstimate, baseline_grid,
-                  block_lanczos_subspace, derive,
+                  block_lanczos_batch, block_lanczos_subspace, derive,
                   draw_indices_batch, draw_omega_batch, draw_uniforms_batch, exact_signal_subspace, extract_peaks, fast_music_1,
                   fast_music_2, gaussian_matrix_real, generate_frames, hermitian, music_spectrum, normals,
                   read_frames, read_matrix_binary, sample_without_replacement, spatial_covariance, steering_vector, temporal_covariance,

@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libfastmusic_b200.so")
 
 FM_OK, FM_EINVAL, FM_ERANK, FM_ENOCONV, FM_ESINGULAR, FM_ECUDA, FM_ENOTSUP, FM_EIO = range(8)
 FRAME_OK, FRAME_RANK, FRAME_NOCONV, FRAME_RANGE, FRAME_NONFINITE = 0, 1, 2, 4, 8
-METHOD = {"exact": 0, "fast1": 1, "fast2": 2, "fast1_norm2": 3}
+METHOD = {"exact": 0, "fast1": 1, "fast2": 2, "lanczos": 3, "fast1_norm2": 16}
 
 # Every symbol declared in include/fastmusic_b200.h (checked by tests/test_capi_symbols.py).
 EXPORTED = [
@@ -27,6 +27,7 @@ EXPORTED = [
     "fm_z_spatial_covariance", "fm_z_exact_signal_subspace", "fm_z_fast_music_1", "fm_z_fast_music_2",
     "fm_z_music_spectrum", "fm_z_extract_peaks",
     "fm_z_temporal_covariance", "fm_temporal_covariance_batch", "fm_z_block_lanczos_subspace",
+    "fm_block_lanczos_batch",
     "fm_fmcx_write", "fm_fmcx_read_header", "fm_fmcx_read", "fm_z_fmcx_write", "fm_z_fmcx_read",
     "fm_fmcx_read_frames", "fm_fmcx_write_frames", "fm_z_write_matrix_csv", "fm_write_spectrum_csv",
 ]
@@ -99,6 +100,7 @@ def _load():
         "fm_z_extract_peaks": (i32, [vp, i64, i64, i64, vp, vp, vp, vp, vp]),
         "fm_z_temporal_covariance": (i32, [i64, i64, vp, vp]),
         "fm_z_block_lanczos_subspace": (i32, [i64, vp, i64, i64, i32, vp, vp, vp, vp]),
+        "fm_block_lanczos_batch": (i32, [vp, i64, i64, i64, i64, i32, vp, vp, vp, vp, vp]),
         "fm_temporal_covariance_batch": (i32, [vp, i64, i64, i64, vp, vp, vp, vp]),
         "fm_fmcx_write": (i32, [C.c_char_p, i64, i64, vp]),
         "fm_fmcx_read_header": (i32, [C.c_char_p, vp, vp]),

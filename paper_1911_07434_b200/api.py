@@ -256,6 +256,27 @@ def temporal_covariance_batch(x, out=None, status=None, stream=None, work=None):
     return out, status
 
 
+def block_lanczos_batch(s, k: int, block: int, max_iterations: int, stream=None):
+    """Batched block_lanczos_subspace on device covariance matrices (torch complex64 [frames, M, M], Hermitian):
+    returns (basis complex128 [frames, M, K], eigenvalues [frames, K], status int32 [frames], iterations int32
+    [frames] = 10000 * Krylov iterations + Jacobi sweeps) as device tensors."""
+    import torch
+    if s.dtype != torch.complex64 or s.dim() != 3 or s.shape[1] != s.shape[2]:
+        raise ValueError("block_lanczos_batch: need a complex64 [frames, M, M] device tensor")
+    s = s.contiguous()  # row-major per frame (a transposed view would read S^T = conj(S))
+    frames, m = s.shape[0], s.shape[1]
+    dev = s.device
+    basis = torch.empty((frames, k, m, 2), dtype=torch.float64, device=dev)
+    eig = torch.empty((frames, k), dtype=torch.float64, device=dev)
+    status = torch.empty((frames,), dtype=torch.int32, device=dev)
+    iters = torch.empty((frames,), dtype=torch.int32, device=dev)
+    q = None if stream is None else C.c_void_p(stream.cuda_stream)
+    _check(LIB.fm_block_lanczos_batch(ptr(s), frames, m, k, block, max_iterations, ptr(basis), ptr(eig), ptr(status),
+                                      ptr(iters), q))
+    b = torch.view_as_complex(basis).transpose(1, 2)
+    return b, eig, status, iters
+
+
 def _est_out(m, k):
     return np.empty((m, k), np.complex128, order="F"), np.empty(k, np.float64), C.c_double(0.0)
 

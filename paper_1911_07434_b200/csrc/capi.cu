@@ -27,6 +27,13 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
                              float* scale = nullptr, int64_t n_true = 0, const FmCovRescue* rescue = nullptr,
                              int64_t t_rows = 0);
 size_t fm_final_fallback_scratch_bytes(int ctas);
+template <typename TS>
+cudaError_t fm_launch_lanczos_batch(const void* S, const double* q0, double* basis_ws, double* w_ws, double* z_ws,
+                                    double* out_basis, double* out_eig, int32_t* status, double* last_change,
+                                    int32_t* iters, int frames, int m, int k, int b0, int max_iter, cudaStream_t s);
+int fm_lanczos_batch_bmax();
+int fm_lanczos_batch_nbmax();
+std::vector<double> fm_lanczos_start_block(int64_t m, int b);
 int fm_final_fallback_ctas();
 cudaError_t fm_launch_final_fallback(const void* C, const void* V, const void* H, void* basis, double* eig,
                                      int32_t* status, void* scratch, int frames, int m, int p, int k,
@@ -524,6 +531,12 @@ struct fm_plan_s {
     float* work32 = nullptr;    // exact method: fp32 Jacobi stage, frames x MP x MP complex64
     double* gpart = nullptr;    // frames x 2 x p x p complex: G halves from the product epilogue (plane path)
     double* hpart = nullptr;    // frames x 2 x p x p complex: H = V^H C halves (last product)
+    // block-Lanczos (FM_METHOD_LANCZOS, lanczos_batch.cu): shared start block, per-frame Krylov basis and blocks
+    double* lz_q0 = nullptr;     // M x block complex128
+    double* lz_basis = nullptr;  // frames x nbmax x M complex128
+    double* lz_w = nullptr;      // frames x M x bmax complex128
+    double* lz_z = nullptr;      // frames x M x bmax complex128
+    int lz_block = 0;
     // host-path staging
     float* x_dev = nullptr;
     float* omega_dev = nullptr;
@@ -618,12 +631,19 @@ static fm_status validate_desc(const fm_plan_desc* d) {
     const char* who = d->method == FM_METHOD_FAST2         ? "fast_music_2"
                       : d->method == FM_METHOD_FAST1       ? "fast_music_1"
                       : d->method == FM_METHOD_FAST1_NORM2 ? "fast_music_1_norm2"
+                      : d->method == FM_METHOD_LANCZOS     ? "block_lanczos_subspace"
                                                            : "exact_signal_subspace";
     if (d->k < 1 || d->k >= d->m) return fail(FM_EINVAL, std::string(who) + ": need 1 <= K < M");
     if (d->k > 64) return fail(FM_ENOTSUP, "plan: K <= 64 supported");
     if (d->method == FM_METHOD_FAST1 || d->method == FM_METHOD_FAST2 || d->method == FM_METHOD_FAST1_NORM2) {
         if (d->p < d->k || d->p > d->m) return fail(FM_EINVAL, std::string(who) + ": need K <= p <= M");
         if (d->p > 64) return fail(FM_ENOTSUP, "plan: p <= 64 supported");
+    } else if (d->method == FM_METHOD_LANCZOS) {  // p = block (0 selects K, R/include/fastmusic/bench.hpp:61)
+        const int64_t block = d->p > 0 ? d->p : d->k;
+        if (block < d->k) return fail(FM_EINVAL, "block_lanczos_subspace: need block >= K");
+        if (d->t < 1) return fail(FM_EINVAL, "block_lanczos_subspace: iters >= 1");
+        if (std::min<int64_t>(block, d->m) > fm_lanczos_batch_bmax())
+            return fail(FM_ENOTSUP, "plan: block_lanczos_subspace block <= 16 supported");
     } else if (d->method != FM_METHOD_EXACT) {
         return fail(FM_EINVAL, "plan: unknown method");
     }
@@ -659,7 +679,9 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
     desc = &pl->d;  // everything below sizes the N-dimensional problem in temporal mode
     const size_t B = static_cast<size_t>(desc->max_frames), M = desc->m, K = desc->k, L = desc->grid_size;
     pl->pe = exact_fast_p(*desc);
-    const size_t P = desc->method == FM_METHOD_EXACT ? static_cast<size_t>(pl->pe) : static_cast<size_t>(desc->p);
+    const size_t P = desc->method == FM_METHOD_EXACT     ? static_cast<size_t>(pl->pe)
+                     : desc->method == FM_METHOD_LANCZOS ? static_cast<size_t>(1)
+                                                         : static_cast<size_t>(desc->p);
     cudaError_t e = cudaSuccess;
     auto chk = [&](cudaError_t x) {
         if (e == cudaSuccess) e = x;
@@ -683,7 +705,17 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
     chk(pl->get(&pl->rlist, B));
     chk(pl->get(&pl->rcount, 64));
     chk(pl->get(&pl->xscale, B));
-    if (desc->method != FM_METHOD_EXACT) {
+    if (desc->method == FM_METHOD_LANCZOS) {
+        pl->lz_block = static_cast<int>(std::min<int64_t>(desc->p > 0 ? desc->p : desc->k, desc->m));
+        chk(pl->get(&pl->lz_q0, M * pl->lz_block * 2));
+        chk(pl->get(&pl->lz_basis, B * static_cast<size_t>(fm_lanczos_batch_nbmax()) * M * 2));
+        chk(pl->get(&pl->lz_w, B * M * static_cast<size_t>(fm_lanczos_batch_bmax()) * 2));
+        chk(pl->get(&pl->lz_z, B * M * static_cast<size_t>(fm_lanczos_batch_bmax()) * 2));
+        if (e == cudaSuccess) {
+            const auto q0 = fm_lanczos_start_block(static_cast<int64_t>(M), pl->lz_block);
+            e = cudaMemcpy(pl->lz_q0, q0.data(), sizeof(double) * q0.size(), cudaMemcpyHostToDevice);
+        }
+    } else if (desc->method != FM_METHOD_EXACT) {
         uint8_t* fb = nullptr;
         chk(pl->get(&fb, fm_final_fallback_scratch_bytes(fm_final_fallback_ctas())));
         pl->fb_scratch = fb;
@@ -837,6 +869,7 @@ extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
     if (d.method == FM_METHOD_FAST2) n += 1 + t * (orth + 1) + fin;  // rmul, t x (orth, rmul), final
     else if (d.method == FM_METHOD_FAST1_NORM2) n += 1 + 1 + (orth + 1) + fin;  // select, rmul, orth, rmul, final
     else if (d.method == FM_METHOD_FAST1) n += 1 + fin;      // gather, final
+    else if (d.method == FM_METHOD_LANCZOS) n += 1;          // the whole Krylov loop in one launch
     else if (plan->pe > 0) n += 1 + 1 + kExactIters * (3 + 1) + 3 + 1 + 6;  // see run_post_cov
     else n += 1;                                              // jacobi
     return n;
@@ -889,6 +922,9 @@ struct WorkView {
     double* gpart;
     double* hpart;
     uint8_t* peak_ws;
+    double* lz_basis;
+    double* lz_w;
+    double* lz_z;
     FmCovRescue resc;
     size_t dslot;  // first frame row of this sub-batch's region in tdig / tscale
 };
@@ -916,6 +952,10 @@ static WorkView work_view(fm_plan pl, int64_t f0, int sub = 0) {
     w.spec64 = pl->spec64 + f0 * static_cast<size_t>(d.grid_size);
     w.scratch = pl->scratch_status + f0;
     w.peak_ws = pl->peak_ws ? pl->peak_ws + f0 * pl->peak_ws_frame : nullptr;
+    const size_t nbm = static_cast<size_t>(fm_lanczos_batch_nbmax()), bm = static_cast<size_t>(fm_lanczos_batch_bmax());
+    w.lz_basis = pl->lz_basis ? pl->lz_basis + f0 * nbm * M * 2 : nullptr;
+    w.lz_w = pl->lz_w ? pl->lz_w + f0 * M * bm * 2 : nullptr;
+    w.lz_z = pl->lz_z ? pl->lz_z + f0 * M * bm * 2 : nullptr;
     w.resc = FmCovRescue{pl->amax + f0, pl->rlist + f0, pl->rcount + std::min(sub, 63), pl->xscale + f0};
     return w;
 }
@@ -1034,6 +1074,9 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
             if ((st = nystrom()) != FM_OK) return st;
         }
         if ((st = fallback(nullptr, w.H)) != FM_OK) return st;
+    } else if (d.method == FM_METHOD_LANCZOS) {
+        FM_LAUNCH(fm_launch_lanczos_batch<float>(R, pl->lz_q0, w.lz_basis, w.lz_w, w.lz_z, basis, eig, io->status,
+                                                 nullptr, nullptr, F, M, K, pl->lz_block, d.t, s));
     } else if (pl->pe > 0) {
         // exact_signal_subspace as certified subspace iteration: C = R Omega, kExactIters x {V = orth(C),
         // C = R V}, Nystrom/Rayleigh step -> U; then the fp64 residual bound (exact.cu) -- checked against the
@@ -1256,7 +1299,8 @@ extern "C" fm_status fm_estimate_batch_host(fm_plan pl, int64_t frames, const fl
         return fail(FM_EINVAL, "fm_estimate_batch_host: null argument");
     if (frames < 1 || frames > pl->d.max_frames) return fail(FM_EINVAL, "fm_estimate_batch_host: frames out of range");
     const auto& d = pl->d;
-    if (d.method != FM_METHOD_EXACT && !draw_seeds) return fail(FM_EINVAL, "fm_estimate_batch_host: seeds required");
+    if (d.method != FM_METHOD_EXACT && d.method != FM_METHOD_LANCZOS && !draw_seeds)
+        return fail(FM_EINVAL, "fm_estimate_batch_host: seeds required");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     FM_CUDA_OK(cudaSetDevice(pl->device));
     const size_t B = static_cast<size_t>(d.max_frames), M = d.m, N = d.n, P = d.p, K = d.k, L = d.grid_size;

@@ -31,6 +31,14 @@ cudaError_t fm_launch_rmul(const void*, const void*, const void*, void*, const i
 template <typename T>
 cudaError_t fm_launch_jacobi_eig(const void* R, void* work, void* basis, double* eig, int32_t* status, int frames,
                                  int m, int k, cudaStream_t s, int only_flagged, void* work32 = nullptr);
+template <typename TS>
+cudaError_t fm_launch_lanczos_batch(const void* S, const double* q0, double* basis_ws, double* w_ws, double* z_ws,
+                                    double* out_basis, double* out_eig, int32_t* status, double* last_change,
+                                    int32_t* iters, int frames, int m, int k, int b0, int max_iter, cudaStream_t s);
+int fm_lanczos_batch_bmax();
+int fm_lanczos_batch_nbmax();
+int32_t fm_lanczos_batch_cap_flag();
+std::vector<double> fm_lanczos_start_block(int64_t m, int b);
 template <typename T>
 cudaError_t fm_launch_qr_rank(const void* C, void* work, void* Vout, int32_t* status, int32_t* rank_out, int m, int p,
                               cudaStream_t s);
@@ -167,6 +175,48 @@ extern "C" fm_status fm_z_block_lanczos_subspace(int64_t m, const double* s, int
     LZ_CUDA(dRank.alloc(1));
     LZ_CUDA(cudaMemcpyAsync(dS.p, srow.data(), sizeof(double) * srow.size(), cudaMemcpyHostToDevice, q_));
     LZ_CUDA(cudaEventRecord(st.e0, q_));
+
+    // Device-resident Krylov loop (lanczos_batch.cu, one CTA): used whenever the block and the basis fit its shared
+    // memory; a frame that outgrows it (kFrameCap) falls through to the host-driven loop below.
+    if (b0 <= fm_lanczos_batch_bmax()) {
+        const auto q0 = fm_lanczos_start_block(m, b0);
+        Buf<double> dQ0, dLB, dLW, dLZ, dOut, dEig, dLast;
+        Buf<int32_t> dFl;
+        LZ_CUDA(dQ0.alloc(q0.size()));
+        LZ_CUDA(dLB.alloc(2 * m * static_cast<size_t>(fm_lanczos_batch_nbmax())));
+        LZ_CUDA(dLW.alloc(2 * m * static_cast<size_t>(fm_lanczos_batch_bmax())));
+        LZ_CUDA(dLZ.alloc(2 * m * static_cast<size_t>(fm_lanczos_batch_bmax())));
+        LZ_CUDA(dOut.alloc(2 * m * K));
+        LZ_CUDA(dEig.alloc(K));
+        LZ_CUDA(dLast.alloc(1));
+        LZ_CUDA(dFl.alloc(1));
+        LZ_CUDA(cudaMemcpyAsync(dQ0.p, q0.data(), sizeof(double) * q0.size(), cudaMemcpyHostToDevice, q_));
+        LZ_CUDA(cudaMemsetAsync(dFl.p, 0, sizeof(int32_t), q_));
+        LZ_CUDA(fm_launch_lanczos_batch<double>(dS.p, dQ0.p, dLB.p, dLW.p, dLZ.p, dOut.p, dEig.p, dFl.p, dLast.p,
+                                                nullptr, 1, M, K, b0, max_iterations, q_));
+        LZ_CUDA(cudaEventRecord(st.e1, q_));
+        int32_t fl = 0;
+        double chg = 0.0;
+        LZ_CUDA(cudaMemcpyAsync(&fl, dFl.p, sizeof(int32_t), cudaMemcpyDeviceToHost, q_));
+        LZ_CUDA(cudaMemcpyAsync(&chg, dLast.p, sizeof(double), cudaMemcpyDeviceToHost, q_));
+        LZ_CUDA(cudaMemcpyAsync(basis, dOut.p, sizeof(double) * 2 * m * K, cudaMemcpyDeviceToHost, q_));
+        LZ_CUDA(cudaMemcpyAsync(eigenvalues, dEig.p, sizeof(double) * K, cudaMemcpyDeviceToHost, q_));
+        LZ_CUDA(cudaStreamSynchronize(q_));
+        if (!(fl & fm_lanczos_batch_cap_flag())) {
+            float ms = 0.f;
+            LZ_CUDA(cudaEventElapsedTime(&ms, st.e0, st.e1));
+            if (cost_seconds) *cost_seconds = 1e-3 * ms;
+            if (last_change) *last_change = chg;
+            if (fl & fmk::kFrameNoConv) {
+                char msg[160];
+                std::snprintf(msg, sizeof msg,
+                              "block_lanczos_subspace: no convergence within iteration cap (last change %.3g)", chg);
+                return fm_set_error(FM_ENOCONV, msg);
+            }
+            return FM_OK;
+        }
+        LZ_CUDA(cudaEventRecord(st.e0, q_));
+    }
 
     // q = qr_orthonormal(gaussian_matrix(m, min(block, m), kStartSeed)): real Gaussian cast to complex
     {

@@ -81,3 +81,94 @@ def test_deterministic(fm):
     a = fm.block_lanczos_subspace(s, 3, 4, 100)
     b = fm.block_lanczos_subspace(s, 3, 4, 100)
     assert np.array_equal(a.basis, b.basis) and np.array_equal(a.eigenvalues, b.eigenvalues)
+
+
+# ---------------------------------------------------------------- batched plan method (lanczos_batch.cu)
+def test_batch_lanczos_c2_frames(fm, oracle):
+    """FM_METHOD_LANCZOS on c2 frames (block = K, cap 200): identical peak cells and spectra within 0.05 dB of
+    the oracle's block_lanczos_subspace on the fp64 covariance, Ritz values to the covariance precision."""
+    from tests.gpu_helpers import compare_frames, run_gpu
+    cfg = oracle.baseline_configs()["c2lz"]
+    frames = list(range(24))
+    x, _, _ = oracle.generate_batch(cfg.base_seed, frames, cfg.spec)
+    res = run_gpu(fm, oracle, cfg, x, frames)
+    assert np.all(res["status"] == 0), res["status"]
+    worst, mism = compare_frames(oracle, cfg, x, frames, res)
+    assert not mism, mism
+    assert worst <= 0.05, worst
+    for i in range(4):
+        s = oracle.spatial_covariance(x[i])
+        ref = oracle.block_lanczos_subspace(s, 8, 8, 200)
+        assert np.allclose(res["eigenvalues"][i], ref.eigenvalues, rtol=2e-4)
+        b = res["basis_c"][i]
+        assert np.max(np.abs(b.conj().T @ b - np.eye(8))) < 1e-9
+
+
+def test_batch_lanczos_matches_facade_on_exported_covariance(fm, oracle):
+    """The batch method on the plan's complex64 R equals the fp64 facade (same device loop) run on that R."""
+    from tests.gpu_helpers import run_gpu
+    cfg = oracle.baseline_configs()["c2lz"]
+    frames = [3, 7]
+    x, _, _ = oracle.generate_batch(cfg.base_seed, frames, cfg.spec)
+    res = run_gpu(fm, oracle, cfg, x, frames, covariance=True)
+    for i in range(len(frames)):
+        r = res["cov_c"][i].astype(np.complex128)
+        est = fm.block_lanczos_subspace(r, 8, 8, 200)
+        # the facade symmetrises 0.5 (R + R^H) as HermitianMatrix does; the batch reads R's lower triangle
+        # (conj of its columns), and the two triangles of the tensor-core R differ at complex64 rounding
+        assert proj_err(est.basis, res["basis_c"][i]) < 1e-7
+        assert np.allclose(est.eigenvalues, res["eigenvalues"][i], rtol=1e-7)
+
+
+@pytest.mark.parametrize("m,k,block", [(64, 3, 3), (48, 2, 5), (128, 4, 6)])
+def test_batch_lanczos_shapes(fm, oracle, m, k, block):
+    """Other shapes and blocks through the plan (fp16-free complex64 R path) against the oracle."""
+    from tests.gpu_helpers import compare_frames, run_gpu
+    spec = oracle.SceneSpec(m, 2 * m, k, -60.0, 60.0, 6.0, 15.0, 25.0)
+    cfg = oracle.PathConfig("lz", "lanczos", spec, 6, 1801, p=block, t=200, base_seed=7)
+    frames = list(range(6))
+    x, _, _ = oracle.generate_batch(cfg.base_seed, frames, spec)
+    res = run_gpu(fm, oracle, cfg, x, frames)
+    assert np.all(res["status"] == 0), res["status"]
+    worst, mism = compare_frames(oracle, cfg, x, frames, res)
+    assert not mism, mism
+    assert worst <= 0.05, worst
+
+
+def test_batch_lanczos_capacity(fm, oracle):
+    """A block-16 Krylov basis outgrows the device loop's 72 columns: the batch flags the frame NOCONV, the
+    facade finishes it with the host-driven loop and still matches the oracle."""
+    import torch
+    s = psd_with_spectrum(fm, gapped_spectrum(128, 4, 0.05), 71)
+    b, e, st, it = fm.block_lanczos_batch(torch.from_numpy(s[None].astype(np.complex64)).cuda(), 4, 16, 200)
+    torch.cuda.synchronize()
+    assert st.cpu().numpy()[0] & 2
+    got = fm.block_lanczos_subspace(s, 4, 16, 200)
+    ref = oracle.block_lanczos_subspace(s, 4, 16, 200)
+    assert proj_err(got.basis, ref.basis) < 1e-8
+
+
+def test_batch_lanczos_iteration_cap_flags_noconv(fm, oracle):
+    from tests.gpu_helpers import run_gpu
+    cfg = oracle.baseline_configs()["c2lz"]
+    cfg = oracle.PathConfig("lzcap", "lanczos", cfg.spec, 2, 3601, p=0, t=2, base_seed=2)
+    x, _, _ = oracle.generate_batch(cfg.base_seed, [0, 1], cfg.spec)
+    res = run_gpu(fm, oracle, cfg, x, [0, 1])
+    assert np.all(res["status"] & 2), res["status"]  # FM_FRAME_NOCONV
+
+
+def test_block_lanczos_batch_entry(fm, oracle):
+    """fm_block_lanczos_batch on device matrices: gapped spectra of several sizes against the oracle."""
+    import torch
+    frames = []
+    for i in range(6):
+        frames.append(psd_with_spectrum(fm, gapped_spectrum(40, 4, 0.3 + 0.05 * i), 80 + i))
+    s = torch.from_numpy(np.stack(frames).astype(np.complex64)).cuda()
+    b, e, st, it = fm.block_lanczos_batch(s, 4, 4, 200)
+    torch.cuda.synchronize()
+    assert np.all(st.cpu().numpy() == 0)
+    for i in range(6):
+        ref = oracle.block_lanczos_subspace(frames[i].astype(np.complex64).astype(np.complex128), 4, 4, 200)
+        assert proj_err(b[i].cpu().numpy(), ref.basis) < 1e-7
+        assert np.allclose(e[i].cpu().numpy(), ref.eigenvalues, rtol=1e-7)
+    assert np.all(it.cpu().numpy() // 10000 >= 3)
