@@ -206,6 +206,41 @@ def _worker_frame(args):
     return f, pk.cells, spec.astype("float32"), time.perf_counter() - t0
 
 
+def _ref_available(cfg_name):
+    """The reference's own path compiled here (oracle/_ref/libref_fastmusic.so: R/src/{scene,linalg,estimators,
+    spectrum}.cpp against the Eigen-API shim over OpenBLAS) covers every config but the norm^2-sampling extension."""
+    try:
+        from oracle import ref_lib
+    except Exception:
+        return False
+    return ref_lib.available() and CONFIGS[cfg_name]["method"] in ("fast2", "fast1", "exact", "lanczos")
+
+
+def _ref_worker_init(cfg_name):
+    from oracle import fastmusic_oracle as O
+    from oracle import ref_lib
+    _W.update(O=O, R=ref_lib, cfgd=CONFIGS[cfg_name])
+
+
+def _ref_worker_frame(args):
+    f, x = args
+    O, R, c = _W["O"], _W["R"], _W["cfgd"]
+    fs = O.frame_seed(c["seed"], f)
+    seed = O.derive(fs, 4 if c["method"] == "fast2" else 3) if c["method"] in ("fast2", "fast1") else 0
+    t0 = time.perf_counter()
+    st, cells, _ = R.run_frame(x, c["k"], c["method"], c["p"], c["t"], seed, c["L"], 3, bool(c.get("temporal")))
+    return f, cells, st, time.perf_counter() - t0
+
+
+def cpu_ref_run(cfg_name, xs, frames, cores, pool):
+    """The reference's own compiled path over `frames`, one frame per worker at a time (R/src/bench.cpp:59-86
+    pattern, one BLAS thread per worker); returns (wall_s, results). Grid: the reference's AngleGrid(L) = [0, pi]
+    (R/src/spectrum.cpp:18-28) -- the same L points and work as the GPU arm's [-90, 90] deg grid."""
+    t0 = time.perf_counter()
+    res = pool.map(_ref_worker_frame, [(f, xs[i]) for i, f in enumerate(frames)], chunksize=1)
+    return time.perf_counter() - t0, res
+
+
 def cpu_reference_run(cfg_name, xs, frames, cores, pool=None):
     """The oracle port (fp64 restatement of the reference path) over `frames`, one frame per
     worker at a time (R/src/bench.cpp:59-86 pattern); returns (wall_s, results)."""
@@ -240,11 +275,16 @@ def run_reference(args):
     else:
         cfg = O.baseline_configs()[args.config]
         xs, _, _ = O.generate_batch(cfg.base_seed, range(nsamp), cfg.spec)
-    pool = mp.get_context("fork").Pool(cores, initializer=_worker_init, initargs=(args.config,))
+    use_ref = _ref_available(args.config)
+    pool = mp.get_context("fork").Pool(cores, initializer=_ref_worker_init if use_ref else _worker_init,
+                                       initargs=(args.config,))
     times = []
     for i in range(args.warmup + args.steps):
         sl = [(i * per_step + j) % nsamp for j in range(per_step)]
-        wall, _ = cpu_reference_run(args.config, xs[sl], sl, cores, pool)
+        if use_ref:
+            wall, _ = cpu_ref_run(args.config, xs[sl], sl, cores, pool)
+        else:
+            wall, _ = cpu_reference_run(args.config, xs[sl], sl, cores, pool)
         if i >= args.warmup:
             times.append(wall)
     pool.close()
@@ -257,9 +297,14 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic (seeded BASELINE frame model, DESIGN.md §3)",
         "config": config_dict(args.config, cfgd, 1),
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port", "cpu_model": cpu_model(),
-                         "sample": f"{per_step} frames per step (one per core) of {args.config}; oracle fp64 "
-                                   f"restatement of the reference path (numpy/scipy LAPACK, 1 BLAS thread/worker)"},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "reference" if use_ref else "port",
+                         "cpu_model": cpu_model(),
+                         "sample": (f"{per_step} frames per step (one per core) of {args.config}; " +
+                                    ("the reference's own R/src/{scene,linalg,estimators,spectrum}.cpp compiled here "
+                                     "(oracle/_ref, Eigen-API shim over OpenBLAS, 1 BLAS thread per worker), "
+                                     "AngleGrid(L) = [0, pi]" if use_ref else
+                                     "oracle fp64 restatement of the reference path (numpy/scipy LAPACK, 1 BLAS "
+                                     "thread/worker)"))},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -537,9 +582,20 @@ def run_ours(args):
         ns = min(n, max(cores, args.cpu_frames))
         frames = list(range(ns))
         import multiprocessing as mp
+        use_ref = _ref_available(args.config)
+        ref_wall = None
+        if use_ref:  # timed: the reference's own compiled path; parity: the oracle port on the same frames
+            rpool = mp.get_context("fork").Pool(cores, initializer=_ref_worker_init, initargs=(args.config,))
+            cpu_ref_run(args.config, xnp[:cores], list(range(min(cores, ns))), cores, rpool)  # warm the workers
+            ref_wall, _ = cpu_ref_run(args.config, xnp[:ns], frames, cores, rpool)
+            rpool.close()
+            rpool.join()
+            ns_par = min(ns, max(cores, 16))
+        else:
+            ns_par = ns
         pool = mp.get_context("fork").Pool(cores, initializer=_worker_init, initargs=(args.config,))
-        cpu_reference_run(args.config, xnp[:cores], list(range(min(cores, ns))), cores, pool)  # warm the workers
-        wall, res = cpu_reference_run(args.config, xnp[:ns], frames, cores, pool)
+        cpu_reference_run(args.config, xnp[:cores], list(range(min(cores, ns_par))), cores, pool)  # warm the workers
+        wall, res = cpu_reference_run(args.config, xnp[:ns_par], list(range(ns_par)), cores, pool)
         pool.close()
         pool.join()
         gp = out0["peak_cells"].cpu().numpy()
@@ -547,12 +603,22 @@ def run_ours(args):
         from oracle import fastmusic_oracle as O
         same = sum(1 for f, cells, spec, _ in res if list(gp[f][:len(cells)]) == cells)
         dbs = [O.spectrum_db_error(gs[f].astype("float64"), spec.astype("float64")) for f, _, spec, _ in res]
-        line["cpu_baseline"] = {"value": ns / wall, "unit": "frames/s", "cores": cores, "kind": "port",
-                                "cpu_model": cpu_model(),
-                                "sample": f"first {ns} frames of the {args.config} batch, oracle fp64 restatement "
-                                          f"(numpy/scipy), one frame per worker process, pool warmed on "
-                                          f"{min(cores, ns)} frames first"}
-        line["parity_sample"] = {"frames": ns, "peaks_identical": same, "max_db_err_vs_port": max(dbs)}
+        if use_ref:
+            line["cpu_baseline"] = {"value": ns / ref_wall, "unit": "frames/s", "cores": cores, "kind": "reference",
+                                    "cpu_model": cpu_model(),
+                                    "sample": f"first {ns} frames of the {args.config} batch through the reference's "
+                                              f"own R/src/{{scene,linalg,estimators,spectrum}}.cpp compiled here "
+                                              f"(oracle/_ref, Eigen-API shim over OpenBLAS), one frame per worker "
+                                              f"process, 1 BLAS thread each, AngleGrid(L) = [0, pi]; pool warmed "
+                                              f"on {min(cores, ns)} frames first",
+                                    "port_value": ns_par / wall}
+        else:
+            line["cpu_baseline"] = {"value": ns / wall, "unit": "frames/s", "cores": cores, "kind": "port",
+                                    "cpu_model": cpu_model(),
+                                    "sample": f"first {ns} frames of the {args.config} batch, oracle fp64 restatement "
+                                              f"(numpy/scipy), one frame per worker process, pool warmed on "
+                                              f"{min(cores, ns)} frames first"}
+        line["parity_sample"] = {"frames": ns_par, "peaks_identical": same, "max_db_err_vs_port": max(dbs)}
     print(json.dumps(line), flush=True)
     fs.close()
     if world > 1:

@@ -36,6 +36,16 @@ fm_lapack_int scipy_LAPACKE_zungqr64_(int layout, fm_lapack_int m, fm_lapack_int
                                       fm_lapack_int lda, const void* tau);
 fm_lapack_int scipy_LAPACKE_zgeqp364_(int layout, fm_lapack_int m, fm_lapack_int n, void* a, fm_lapack_int lda,
                                       fm_lapack_int* jpvt, void* tau);
+// CBLAS of the same library: dense products and the Hermitian rank update run where Eigen would run its own
+// blocked, vectorised kernels (the eager loops over std::complex would time libgcc's __muldc3 instead)
+void scipy_cblas_zgemm64_(int layout, int ta, int tb, fm_lapack_int m, fm_lapack_int n, fm_lapack_int k,
+                          const void* alpha, const void* a, fm_lapack_int lda, const void* b, fm_lapack_int ldb,
+                          const void* beta, void* c, fm_lapack_int ldc);
+void scipy_cblas_dgemm64_(int layout, int ta, int tb, fm_lapack_int m, fm_lapack_int n, fm_lapack_int k, double alpha,
+                          const double* a, fm_lapack_int lda, const double* b, fm_lapack_int ldb, double beta,
+                          double* c, fm_lapack_int ldc);
+void scipy_cblas_zherk64_(int layout, int uplo, int trans, fm_lapack_int n, fm_lapack_int k, double alpha,
+                          const void* a, fm_lapack_int lda, double beta, void* c, fm_lapack_int ldc);
 }
 
 namespace Eigen {
@@ -256,6 +266,12 @@ public:
         template <typename Y>
         void rankUpdate(const Y& yy, RealScalar alpha) {
             const Matrix<S> y = yy;
+            if constexpr (std::is_same_v<S, std::complex<double>>) {  // lower triangle += alpha y y^H (zherk)
+                if (m->rows() > 0 && y.cols() > 0)
+                    scipy_cblas_zherk64_(102 /*ColMajor*/, 122 /*Lower*/, 111 /*NoTrans*/, m->rows(), y.cols(), alpha,
+                                         y.data(), y.rows(), 1.0, m->data(), m->rows());
+                return;
+            }
             for (Index j = 0; j < m->cols(); ++j)
                 for (Index i = j; i < m->rows(); ++i) {
                     S acc = S(0);
@@ -378,6 +394,30 @@ Matrix<internal::promote_t<A, B>> operator*(const Matrix<A, R1, C1>& a, const Ma
     using S = internal::promote_t<A, B>;
     if (a.cols() != b.rows()) throw std::logic_error("eigen_lite: product size mismatch");
     Matrix<S> o(a.rows(), b.cols());
+    if (a.rows() > 0 && b.cols() > 0 && a.cols() > 0) {
+        if constexpr (std::is_same_v<S, std::complex<double>>) {
+            auto promote = [](const auto& x) {  // real operands to complex
+                Matrix<S> o2(x.rows(), x.cols());
+                for (Index i = 0; i < x.size(); ++i) o2.data()[i] = S(x.data()[i]);
+                return o2;
+            };
+            const S one(1.0, 0.0), zero(0.0, 0.0);
+            const S* pa = nullptr;
+            const S* pb = nullptr;
+            Matrix<S> ac, bc;
+            if constexpr (std::is_same_v<A, S>) pa = a.data();
+            else pa = (ac = promote(a)).data();
+            if constexpr (std::is_same_v<B, S>) pb = b.data();
+            else pb = (bc = promote(b)).data();
+            scipy_cblas_zgemm64_(102, 111, 111, a.rows(), b.cols(), a.cols(), &one, pa, a.rows(), pb, b.rows(), &zero,
+                                 o.data(), o.rows());
+            return o;
+        } else if constexpr (std::is_same_v<S, double> && std::is_same_v<A, double> && std::is_same_v<B, double>) {
+            scipy_cblas_dgemm64_(102, 111, 111, a.rows(), b.cols(), a.cols(), 1.0, a.data(), a.rows(), b.data(),
+                                 b.rows(), 0.0, o.data(), o.rows());
+            return o;
+        }
+    }
     for (Index j = 0; j < b.cols(); ++j)
         for (Index q = 0; q < a.cols(); ++q) {
             const S bq = S(b(q, j));

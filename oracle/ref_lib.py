@@ -35,6 +35,7 @@ def lib():
             "ref_music_spectrum": [vp, i64, i64, i64, dbl, dbl, vp],
             "ref_extract_peaks": [vp, i64, i64, i64, vp, vp, vp, vp, vp],
             "ref_synthesize_beat_signal": [i64, i64, i64, vp, dbl, u64, vp],
+            "ref_run_frame": [vp, i64, i64, C.c_int, C.c_int, i64, i64, C.c_int, u64, i64, i64, vp, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -143,3 +144,18 @@ def synthesize_beat_signal(m, n, angles, noise_var, seed):
     if st:
         raise ValueError(STATUS[st])
     return y
+
+
+METHODS = {"exact": 0, "fast1": 1, "fast2": 2, "lanczos": 3}
+
+
+def run_frame(x, k, method, p, t, seed, L, min_sep=3, temporal=False, spectrum=False):
+    """The reference path for one frame (ref_run_frame): returns (status, cells, spectrum or None)."""
+    y = _cm(x)
+    cells = np.empty(max(k, 1), np.int64)
+    count = C.c_int64(0)
+    spec = np.empty(L, np.float64) if spectrum else None
+    st = lib().ref_run_frame(_p(y), y.shape[0], y.shape[1], 1 if temporal else 0, METHODS[method], k, p, t,
+                             C.c_uint64(seed), L, min_sep, _p(cells), C.byref(count),
+                             _p(spec) if spec is not None else None)
+    return st, [int(c) for c in cells[:count.value]], spec

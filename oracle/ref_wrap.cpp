@@ -105,6 +105,30 @@ int ref_extract_peaks(const double* values, int64_t L, int64_t k, int64_t min_se
     }, nullptr);
 }
 
+// The whole reference path for one frame, the CPU arm of bench.py (R/src/bench.cpp:574-591 pattern): covariance
+// (spatial, or temporal for the ToA path) -> estimator -> music_spectrum on AngleGrid(L) -> extract_peaks.
+// method: 0 exact, 1 fast1, 2 fast2, 3 block-Lanczos (block = p or K, cap t). Returns the status; cells (K) and
+// *count receive the peaks, spectrum (L, may be null) the pseudo-spectrum.
+int ref_run_frame(const double* y, int64_t m, int64_t n, int temporal, int method, int64_t k, int64_t p, int t,
+                  uint64_t seed, int64_t L, int64_t min_sep, int64_t* cells, int64_t* count, double* spectrum) {
+    return guard([&] {
+        const CxMat x = load(y, m, n);
+        const HermitianMatrix s = temporal ? temporal_covariance(x) : spatial_covariance(x);
+        SubspaceEstimate est;
+        if (method == 0) est = exact_signal_subspace(s, k);
+        else if (method == 1) est = fast_music_1(s, k, Fast1Params{p, seed});
+        else if (method == 2) est = fast_music_2(s, k, Fast2Params{p, t, seed});
+        else est = block_lanczos_subspace(s, k, p > 0 ? p : k, t);
+        const PseudoSpectrum ps = music_spectrum(est, AngleGrid(L), 0.5, 1.0);
+        const PeakSet pk = extract_peaks(ps, k, min_sep);
+        const AngleGrid grid(L);
+        *count = static_cast<int64_t>(pk.angles.size());
+        for (size_t i = 0; i < pk.angles.size(); ++i) cells[i] = static_cast<int64_t>(std::llround(pk.angles[i] / grid.spacing()));
+        if (spectrum)
+            for (Index l = 0; l < L; ++l) spectrum[l] = ps.values(l);
+    }, nullptr);
+}
+
 // Sample a frame with the reference's own FMCW beat-signal synthesis (R/src/scene.cpp:100-134) for fixture inputs.
 int ref_synthesize_beat_signal(int64_t m, int64_t n, int64_t k, const double* angles, double noise_var, uint64_t seed,
                                double* y) {
