@@ -230,7 +230,10 @@ __device__ __forceinline__ void convert_tile_t(const uint8_t* stage, uint8_t* op
 // kConv8: four more converter warps after the epilogue warps (eight in all, 16 rows each). The redundant
 // operand conversion of multi-tile frames (every 256-row block of X is converted once per tile it feeds,
 // 4x at M = 1024) makes the converters the bottleneck there.
-template <int kEpi, bool kConv8>
+// kSplit (with kConv8): the eight converter warps form two groups of four that take alternate pipeline stages
+// (each group converts whole stages, 32 rows per warp), so one stage's fixed costs -- the proxy fence, the group
+// barrier and the cross-CTA operand-ready arrive -- overlap the other group's conversion.
+template <int kEpi, bool kConv8, bool kSplit = false>
 #ifdef FM_COV_MAXNREG  // experiment: register cap so fp64 kernels of another sub-batch can co-reside
 #define FM_COV_BOUNDS(t) __maxnreg__(FM_COV_MAXNREG)
 #else
@@ -399,8 +402,11 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
     } else if (warp < 6 || (kConv8 && warp >= (kEpi == 2 ? kThreadsP : kThreads) / 32)) {
         // ---------------- converters (warps 2..5, plus the four after the epilogue warps when kConv8)
         constexpr int kFirstExtra = (kEpi == 2 ? kThreadsP : kThreads) / 32;
-        constexpr int kJ = kConv8 ? 1 : 2;
-        const int cw = warp < 6 ? warp - 2 : 4 + warp - kFirstExtra;
+        constexpr int kJ = (kConv8 && !kSplit) ? 1 : 2;
+        const int cwid = warp < 6 ? warp - 2 : 4 + warp - kFirstExtra;  // 0..7
+        const int grp = kSplit ? (cwid >> 2) : 0;                        // stage group (kSplit)
+        const int cw = kSplit ? (cwid & 3) : cwid;
+        const bool lead = kSplit ? (cwid & 3) == 0 : warp == 2;          // arrives for the group's stages
         int g = 0, tt = 0;
         for (int tile = pair; tile < total_tiles; tile += npairs, ++tt) {
             const int frame = frame_of(tile);
@@ -413,6 +419,7 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
             float amax = 0.f;
             bool nonfinite = false;
             for (int kc = 0; kc < nk; ++kc, ++g) {
+                if (kSplit && (g & 1) != grp) continue;  // nS, nO even: a ring slot always belongs to one group
                 const int s = g % nS;
                 const int o = g % nO;
                 const long long c0 = COV_CLK();
@@ -436,8 +443,8 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
                         convert_tile<kJ>(st + kStageBytes, op + kOpBytes, cw, lane, row_b, m, xs, amax, nonfinite);
                 }
                 fence_proxy_async();
-                named_bar_sync(1, kConv8 ? 256 : 128);  // all converter warps done with this stage
-                if (warp == 2 && lane == 0) {
+                named_bar_sync(kSplit ? 1 + 2 * grp : 1, (kConv8 && !kSplit) ? 256 : 128);  // stage converted
+                if (lead && lane == 0) {
                     if (kc == 0) COV_STAMP(tt, 5);
                     if (kc == nk - 1) COV_STAMP(tt, 6);
                     mbar_arrive_local(smem_u32(&stage_empty[s]));
@@ -804,10 +811,9 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
         rmap = map;  // unused by the fallback epilogue
         mmap = map;
     }
-    // four converter warps for diagonal-only launches (M <= 256: one tile per frame, no redundant conversion;
-    // c2 covariance 0.342 -> 0.333 ms), eight for multi-tile frames (every 256-row block of X is converted once
-    // per tile it feeds)
-    const bool conv4 = m <= 256;
+    // diagonal-only launches (M <= 256: one tile per frame): eight converter warps in two groups taking alternate
+    // stages (kSplit); multi-tile frames: eight warps splitting each stage's rows (every 256-row block of X is
+    // converted once per tile it feeds)
     // ring depths (stages): general staging / operand, diagonal-only staging / operand
     const int rs[4] = {kStagesS, kStagesO, kDiagS, kDiagO};
     const int ring = rs[0] | (rs[1] << 8) | (rs[2] << 16) | (rs[3] << 24);
@@ -817,9 +823,8 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaSuccess;
-        for (cudaError_t x : {set_attr(cov_tc_kernel<0, false>), set_attr(cov_tc_kernel<1, false>),
-                              set_attr(cov_tc_kernel<2, false>), set_attr(cov_tc_kernel<0, true>),
-                              set_attr(cov_tc_kernel<1, true>), set_attr(cov_tc_kernel<2, true>)})
+        for (cudaError_t x : {set_attr(cov_tc_kernel<0, true, true>), set_attr(cov_tc_kernel<1, true, true>),
+                              set_attr(cov_tc_kernel<2, true, true>)})
             if (e == cudaSuccess) e = x;
         if (e != cudaSuccess) return e;
         attr_set = true;
@@ -848,15 +853,11 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
                                               temporal ? 1 : 0);
     };
     auto launch = [&](bool pass2) {
-        if (conv4) {
-            if (epi == 2) go(cov_tc_kernel<2, false>, false, pass2);
-            else if (epi == 1) go(cov_tc_kernel<1, false>, false, pass2);
-            else go(cov_tc_kernel<0, false>, false, pass2);
-        } else {
-            if (epi == 2) go(cov_tc_kernel<2, true>, true, pass2);
-            else if (epi == 1) go(cov_tc_kernel<1, true>, true, pass2);
-            else go(cov_tc_kernel<0, true>, true, pass2);
-        }
+        // eight converter warps in two groups taking alternate stages (tools/ab_build.sh, tools/ab_cov_general.sh:
+        // c2 covariance 0.347 -> 0.324 ms, c4 3.25 -> 3.04 ms, the ToA path's T 0.746 -> 0.714 ms)
+        if (epi == 2) go(cov_tc_kernel<2, true, true>, true, pass2);
+        else if (epi == 1) go(cov_tc_kernel<1, true, true>, true, pass2);
+        else go(cov_tc_kernel<0, true, true>, true, pass2);
     };
     launch(false);
     if (rescue) {
