@@ -6,10 +6,12 @@
 //   W = S Q                       thread per row, S read down its columns (S Hermitian: S(i, j) = conj S(j, i), so
 //                                 the reads are coalesced), Q broadcast from the frame's basis columns
 //   strip = basis^H W             warp per entry
-//   h grows by the strip          kept in its Ritz basis: A = V^H h V with V the accumulated Jacobi rotations, so the
-//                                 new strip only needs V_old^H strip and the Hermitian new corner (warm start)
-//   Ritz values                   two-sided cyclic Jacobi on A (parallel round-robin pairs, complex rotations), V
-//                                 accumulated in shared memory; top-K of diag(A)
+//   h grows by the strip          kept raw in shared memory (A), the new corner symmetrised as HermitianMatrix does
+//   Ritz values                   Householder tridiagonalisation of a copy, then the top-K eigenvalues by Sturm
+//                                 multisection (16 probes per eigenvalue and round): per iteration O(n^3 / threads)
+//                                 with ~5 barriers per column, instead of sweeps of rotations
+//   Ritz vectors (once, at exit)  two-sided cyclic Jacobi on h (parallel round-robin pairs, complex rotations) with the
+//                                 rotations accumulated in shared memory; top-K of its diagonal
 //   convergence                   |vals - prev| / max(|vals|, 1e-300) <= 1e-10 on two consecutive checks
 //   z = W - basis (basis^H W),    twice (the reference's two Gram-Schmidt passes)
 //   q = orthonormal_range(z)      column-pivoted CGS2 with Eigen's ColPivHouseholderQR rank rule
@@ -25,6 +27,7 @@
 #include <cstdint>
 #include <algorithm>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/fastmusic_b200.h"
@@ -37,8 +40,26 @@ namespace lzb {
 constexpr int kThreads = 256;
 constexpr int kBMax = 16;   // block columns per expansion
 constexpr int kNBMax = 72;  // basis columns: A, V complex128 72 x 72 each in shared memory
+constexpr int kLd = kNBMax + 1;  // their leading dimension: 1168 B, so rows walked across columns are bank-conflict free
 constexpr int kMaxSweeps = 60;
 constexpr double kTol = 1e-10;  // R/src/estimators.cpp:160
+
+#ifdef FM_LZ_TIMELINE  // experiment only: clock64 per phase of block 0 (tools/lz_timeline.py)
+__device__ long long g_lz_tl[16];
+#define LZ_T0() long long lz_t0_ = clock64()
+#define LZ_MARK(slot)                                                 \
+    do {                                                              \
+        __syncthreads();                                              \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                    \
+            const long long now_ = clock64();                         \
+            g_lz_tl[slot] += now_ - lz_t0_;                           \
+            lz_t0_ = now_;                                            \
+        }                                                             \
+    } while (0)
+#else
+#define LZ_T0()
+#define LZ_MARK(slot)
+#endif
 
 struct Args {
     const void* S;        // frames x M x M (row-major, full Hermitian), complex64 or complex128
@@ -97,7 +118,7 @@ struct Rot {
     double t_g;  // t |A(p, q)| (diagonal update)
 };
 
-// Two-sided cyclic Jacobi on the Hermitian n x n leading block of A (column-major, leading dim kNBMax),
+// Two-sided cyclic Jacobi on the Hermitian n x n leading block of A (column-major, leading dim kLd),
 // accumulating the rotations into V's n x n block. Returns the number of sweeps (kMaxSweeps + 1: no convergence).
 // Rotation threshold: |A(p, q)| <= 2^-52 max_i |A(i, i)| is at the rounding level of the matrix (a purely relative
 // test, |A(p, q)| <= eps sqrt|A(p, p) A(q, q)|, keeps re-rotating the rounding noise that rotations of large entries
@@ -110,7 +131,7 @@ __device__ int jacobi_sweeps(c64* A, c64* V, int n, Rot* rot, int* s_any, double
         if (tid == 0) {
             *s_any = 0;
             double am = 0.0;
-            for (int x = 0; x < n; ++x) am = fmax(am, fabs(A[x + kNBMax * x].re));
+            for (int x = 0; x < n; ++x) am = fmax(am, fabs(A[x + kLd * x].re));
             *s_amax = am;
         }
         __syncthreads();
@@ -127,9 +148,9 @@ __device__ int jacobi_sweeps(c64* A, c64* V, int n, Rot* rot, int* s_any, double
                 o.e = mk(1.0, 0.0);
                 o.t_g = 0.0;
                 if (q < n) {
-                    const c64 apq = A[p + kNBMax * q];
+                    const c64 apq = A[p + kLd * q];
                     const double g = sqrt(norm2(apq));
-                    const double app = A[p + kNBMax * p].re, aqq = A[q + kNBMax * q].re;
+                    const double app = A[p + kLd * p].re, aqq = A[q + kLd * q].re;
                     // skip rotations below the relative accuracy of the pair (and denormal-size entries)
                     if (g > 1e-290 && g > thr) {
                         const double tau = (aqq - app) / (2.0 * g);
@@ -148,42 +169,76 @@ __device__ int jacobi_sweeps(c64* A, c64* V, int n, Rot* rot, int* s_any, double
                 rot[tid] = o;
             }
             __syncthreads();
-            // columns: A <- A J, V <- V J with J = [[c, s e], [-s conj(e), c]] on (p, q)
-            for (int it = tid; it < np * n; it += kThreads) {
-                const int t = it / n, row = it - t * n;
-                const Rot o = rot[t];
-                if (o.q < 0) continue;
-                const c64 ep = mk(o.s * o.e.re, o.s * o.e.im);  // s e
-                {
-                    const c64 ap = A[row + kNBMax * o.p], aq = A[row + kNBMax * o.q];
-                    A[row + kNBMax * o.p] = o.c * ap - conj(ep) * aq;
-                    A[row + kNBMax * o.q] = ep * ap + o.c * aq;
-                }
-                {
-                    const c64 vp = V[row + kNBMax * o.p], vq = V[row + kNBMax * o.q];
-                    V[row + kNBMax * o.p] = o.c * vp - conj(ep) * vq;
-                    V[row + kNBMax * o.q] = ep * vp + o.c * vq;
+            // columns: A <- A J, V <- V J with J = [[c, s e], [-s conj(e), c]] on (p, q); tpp threads per pair,
+            // the rotation in registers, two rows per pass (independent loads in flight)
+            const int tpp = kThreads / np;
+            const int pt = tid / tpp, sub = tid - pt * tpp;
+            if (pt < np) {
+                const Rot o = rot[pt];
+                if (o.q >= 0) {
+                    const c64 ep = mk(o.s * o.e.re, o.s * o.e.im);  // s e
+                    const c64 epc = conj(ep);
+                    c64* Ap = A + kLd * o.p;
+                    c64* Aq = A + kLd * o.q;
+                    c64* Vp = V + kLd * o.p;
+                    c64* Vq = V + kLd * o.q;
+                    for (int row = sub; row < n; row += 2 * tpp) {
+                        const int r2 = row + tpp;
+                        const bool two = r2 < n;
+                        const c64 ap = Ap[row], aq = Aq[row], vp = Vp[row], vq = Vq[row];
+                        c64 ap2 = mk(0.0, 0.0), aq2 = ap2, vp2 = ap2, vq2 = ap2;
+                        if (two) {
+                            ap2 = Ap[r2];
+                            aq2 = Aq[r2];
+                            vp2 = Vp[r2];
+                            vq2 = Vq[r2];
+                        }
+                        Ap[row] = o.c * ap - epc * aq;
+                        Aq[row] = ep * ap + o.c * aq;
+                        Vp[row] = o.c * vp - epc * vq;
+                        Vq[row] = ep * vp + o.c * vq;
+                        if (two) {
+                            Ap[r2] = o.c * ap2 - epc * aq2;
+                            Aq[r2] = ep * ap2 + o.c * aq2;
+                            Vp[r2] = o.c * vp2 - epc * vq2;
+                            Vq[r2] = ep * vp2 + o.c * vq2;
+                        }
+                    }
                 }
             }
             __syncthreads();
             // rows: A <- J^H A (J^H = [[c, -s e], [s conj(e), c]])
-            for (int it = tid; it < np * n; it += kThreads) {
-                const int t = it / n, col = it - t * n;
-                const Rot o = rot[t];
-                if (o.q < 0) continue;
-                const c64 ep = mk(o.s * o.e.re, o.s * o.e.im);
-                const c64 ap = A[o.p + kNBMax * col], aq = A[o.q + kNBMax * col];
-                A[o.p + kNBMax * col] = o.c * ap - ep * aq;
-                A[o.q + kNBMax * col] = conj(ep) * ap + o.c * aq;
+            if (pt < np) {
+                const Rot o = rot[pt];
+                if (o.q >= 0) {
+                    const c64 ep = mk(o.s * o.e.re, o.s * o.e.im);
+                    const c64 epc = conj(ep);
+                    for (int col = sub; col < n; col += 2 * tpp) {
+                        const int c2 = col + tpp;
+                        const bool two = c2 < n;
+                        const c64 ap = A[o.p + kLd * col], aq = A[o.q + kLd * col];
+                        c64 ap2 = mk(0.0, 0.0), aq2 = ap2;
+                        if (two) {
+                            ap2 = A[o.p + kLd * c2];
+                            aq2 = A[o.q + kLd * c2];
+                        }
+                        A[o.p + kLd * col] = o.c * ap - ep * aq;
+                        A[o.q + kLd * col] = epc * ap + o.c * aq;
+                        if (two) {
+                            A[o.p + kLd * c2] = o.c * ap2 - ep * aq2;
+                            A[o.q + kLd * c2] = epc * ap2 + o.c * aq2;
+                        }
+                    }
+                }
             }
             __syncthreads();
             if (tid < np) {  // the pair's closed form: zero off-diagonal, real diagonal
                 const Rot o = rot[tid];
                 if (o.q >= 0) {
-                    A[o.p + kNBMax * o.q] = mk(0.0, 0.0);
-                    A[o.q + kNBMax * o.p] = mk(0.0, 0.0);
-                    A[o.p + kNBMax * o.p].im = 0.0;
-                    A[o.q + kNBMax * o.q].im = 0.0;
+                    A[o.p + kLd * o.q] = mk(0.0, 0.0);
+                    A[o.q + kLd * o.p] = mk(0.0, 0.0);
+                    A[o.p + kLd * o.p].im = 0.0;
+                    A[o.q + kLd * o.q].im = 0.0;
                 }
             }
             __syncthreads();
@@ -249,12 +304,158 @@ __device__ __forceinline__ void block_sub(const c64* B, const c64* X, c64* Y, co
     }
 }
 
+
+// Householder tridiagonalisation of the Hermitian n x n block of T (column-major, leading dim kLd; destroyed):
+// T -> Q^H T Q real symmetric tridiagonal, diagonal d[i] and off-diagonal |e[i]| (the phases of a complex Hermitian
+// tridiagonal are a diagonal unitary similarity away). Step k: unit v on rows k+1.., p = T v, w = p - (v^H p) v,
+// T22 -= 2 (v w^H + w v^H). Scratch: vv, pp (kNBMax each).
+__device__ void tridiagonalize(c64* T, int n, double* d, double* e, c64* vv, c64* pp, double* red) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int kWarps = kThreads / 32;
+    for (int k = 0; k + 2 < n; ++k) {
+        const int L = n - k - 1;
+        const c64* x = T + (k + 1) + kLd * k;  // column k below the diagonal
+        // ||x||^2 and x0 (one warp)
+        if (warp == 0) {
+            double s2 = 0.0;
+            for (int i = lane; i < L; i += 32) s2 += norm2(x[i]);
+            s2 = warp_sum(s2);
+            if (lane == 0) red[0] = s2;
+        }
+        __syncthreads();
+        const double xn = sqrt(red[0]);
+        const c64 x0 = x[0];
+        const double ax0 = sqrt(norm2(x0));
+        if (xn == 0.0 || (L == 1 && x0.im == 0.0)) {  // nothing to annihilate
+            if (tid == 0) {
+                d[k] = T[k + kLd * k].re;
+                e[k] = sqrt(norm2(x0));
+            }
+            __syncthreads();
+            continue;
+        }
+        const c64 ph = ax0 > 0.0 ? mk(x0.re / ax0, x0.im / ax0) : mk(1.0, 0.0);
+        const c64 alpha = mk(-ph.re * xn, -ph.im * xn);          // x -> alpha e1
+        // v = (x - alpha e1) / ||x - alpha e1||,  ||x - alpha e1||^2 = 2 xn (xn + |x0|)
+        const double vnorm = sqrt(2.0 * xn * (xn + ax0));
+        for (int i = tid; i < L; i += kThreads) {
+            c64 v = x[i];
+            if (i == 0) v = v - alpha;
+            vv[i] = mk(v.re / vnorm, v.im / vnorm);
+        }
+        __syncthreads();
+        // p = T22 v (T22 = T[k+1.., k+1..]); warp per row group, lanes over columns
+        for (int i = warp; i < L; i += kWarps) {
+            c64 acc = mk(0.0, 0.0);
+            for (int j = lane; j < L; j += 32) cmac(acc, T[(k + 1 + i) + kLd * (k + 1 + j)], vv[j]);
+            acc.re = warp_sum(acc.re);
+            acc.im = warp_sum(acc.im);
+            if (lane == 0) pp[i] = acc;
+        }
+        __syncthreads();
+        if (warp == 0) {  // K = v^H p (real for Hermitian T22)
+            double kr = 0.0;
+            for (int i = lane; i < L; i += 32) kr += vv[i].re * pp[i].re + vv[i].im * pp[i].im;
+            kr = warp_sum(kr);
+            if (lane == 0) red[1] = kr;
+        }
+        __syncthreads();
+        const double kk = red[1];
+        for (int i = tid; i < L; i += kThreads) pp[i] = pp[i] - kk * vv[i];  // w
+        __syncthreads();
+        for (int it = tid; it < L * L; it += kThreads) {  // T22 -= 2 (v w^H + w v^H)
+            const int i = it % L, j = it / L;
+            const c64 a = vv[i] * conj(pp[j]) + pp[i] * conj(vv[j]);
+            c64& t = T[(k + 1 + i) + kLd * (k + 1 + j)];
+            t = t - 2.0 * a;
+        }
+        if (tid == 0) {
+            d[k] = T[k + kLd * k].re;
+            e[k] = xn;  // |alpha|
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (n >= 2) {
+            d[n - 2] = T[(n - 2) + kLd * (n - 2)].re;
+            e[n - 2] = sqrt(norm2(T[(n - 1) + kLd * (n - 2)]));
+        }
+        d[n - 1] = T[(n - 1) + kLd * (n - 1)].re;
+    }
+    __syncthreads();
+}
+
+// Number of eigenvalues of the symmetric tridiagonal (d, e) below x (Sturm sequence, with the LAPACK pivmin guard).
+__device__ __forceinline__ int sturm_below(const double* d, const double* e, int n, double x, double pivmin) {
+    int cnt = 0;
+    double q = d[0] - x;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+    for (int i = 1; i < n; ++i) {
+        q = (d[i] - x) - e[i - 1] * e[i - 1] / q;
+        if (fabs(q) < pivmin) q = -pivmin;
+        cnt += q < 0.0;
+    }
+    return cnt;
+}
+
+// The kk largest eigenvalues of (d, e), descending, to the bisection limit (relative 1e-17 of the spectrum span):
+// 16 threads per eigenvalue, each round evaluates 15 interior points and keeps the sub-interval holding it.
+__device__ void top_eigenvalues(const double* d, const double* e, int n, int kk, double* out, double* lohi) {
+    const int tid = threadIdx.x;
+    __shared__ double s_lo[kBMax], s_hi[kBMax];
+    __shared__ int s_cnt[kBMax][16];
+    if (tid == 0) {  // Gershgorin bounds
+        double lo = INFINITY, hi = -INFINITY, emax = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const double r = (i > 0 ? e[i - 1] : 0.0) + (i + 1 < n ? e[i] : 0.0);
+            lo = fmin(lo, d[i] - r);
+            hi = fmax(hi, d[i] + r);
+            if (i + 1 < n) emax = fmax(emax, e[i] * e[i]);
+        }
+        const double w = fmax(hi - lo, 1e-300);
+        lohi[0] = lo - 1e-14 * w;
+        lohi[1] = hi + 1e-14 * w;
+        lohi[2] = fmax(2.2250738585072014e-308, 2.220446049250313e-16 * emax);  // pivmin (LAPACK dstebz)
+    }
+    __syncthreads();
+    const int j = tid >> 4, u = tid & 15;  // eigenvalue j (0 = largest), probe u
+    if (j < kk && u == 0) {
+        s_lo[j] = lohi[0];
+        s_hi[j] = lohi[1];
+    }
+    __syncthreads();
+    const double pivmin = lohi[2];
+    for (int round = 0; round < 20; ++round) {  // 16^20 >> 2^64: converged well before
+        if (j < kk) {
+            const double lo = s_lo[j], hi = s_hi[j];
+            const double x = lo + (hi - lo) * (u + 1) / 16.0;
+            s_cnt[j][u] = u < 15 ? sturm_below(d, e, n, x, pivmin) : n;
+        }
+        __syncthreads();
+        if (j < kk && u == 0) {
+            // the (n - 1 - j)-th smallest eigenvalue (0-based) lies where the count first exceeds n - 1 - j
+            const int target = n - 1 - j;
+            const double lo = s_lo[j], hi = s_hi[j];
+            int b = 0;
+            while (b < 15 && s_cnt[j][b] <= target) ++b;
+            const double nlo = b == 0 ? lo : lo + (hi - lo) * b / 16.0;
+            const double nhi = lo + (hi - lo) * (b + 1) / 16.0;
+            s_lo[j] = nlo;
+            s_hi[j] = b == 15 ? hi : nhi;
+        }
+        __syncthreads();
+    }
+    if (j < kk && u == 0) out[j] = 0.5 * (s_lo[j] + s_hi[j]);
+    __syncthreads();
+}
+
 template <typename TS>
 __global__ void __launch_bounds__(kThreads, 1) k_lanczos_batch(Args a) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     c64* A = reinterpret_cast<c64*>(smem_raw);
-    c64* V = A + kNBMax * kNBMax;
-    c64* strip = V + kNBMax * kNBMax;                // kNBMax x kBMax, row-major [r][c]
+    c64* V = A + kLd * kNBMax;
+    c64* strip = V + kLd * kNBMax;                // kNBMax x kBMax, row-major [r][c]
     Rot* rot = reinterpret_cast<Rot*>(strip + kNBMax * kBMax);
     double* vals = reinterpret_cast<double*>(rot + kNBMax / 2);  // [kBMax]
     double* prev = vals + kBMax;                                   // [kBMax]
@@ -262,7 +463,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_lanczos_batch(Args a) {
     int* top = reinterpret_cast<int*>(nrm + kBMax);                // [kBMax]
     int* ctl = top + kBMax;  // [0] any rotation, [1] ncols, [2] bq, [3] done, [4] stable, [5] have_prev, [6] flags,
                              // [7] rank, [8] pivot, [9] iterations
-    double* dctl = reinterpret_cast<double*>(ctl + 16);  // [0] last change, [1] thr helper, [2] max pivot, [3] amax
+    double* dctl = reinterpret_cast<double*>(ctl + 16);  // [0] last change, [1] thr helper, [2] max pivot, [3] amax,
+                                                         // [4..5] tridiagonalisation, [6..8] bisection bounds
+    double* td = dctl + 16;                               // [kNBMax] tridiagonal diagonal
+    double* te = td + kNBMax;                             // [kNBMax] |off-diagonal|
+    c64* tv = reinterpret_cast<c64*>(te + kNBMax);        // [kNBMax] Householder vector
+    c64* tp = tv + kNBMax;                                // [kNBMax] T v / w
 
     const int f = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -288,6 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lanczos_batch(Args a) {
     }
     __syncthreads();
 
+    LZ_T0();
     for (int it = 0; it < a.max_iter; ++it) {
         const int ncols = ctl[1], bq = ctl[2], old = ncols - bq;
         // ---- W = S Q (Q = basis columns [old, ncols))
@@ -296,7 +503,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_lanczos_batch(Args a) {
 #pragma unroll
             for (int c = 0; c < kBMax; ++c) acc[c] = mk(0.0, 0.0);
             const c64* Qc = B + static_cast<size_t>(old) * M;
-            // eight independent S loads in flight per thread (one CTA per SM: the S stream is latency-bound)
+            // eight independent S loads in flight per thread (one CTA per SM: the S stream is latency-bound; a
+            // double-buffered variant with the next group's loads in flight measured slower, tools/lz_timeline.py)
             int j0 = 0;
             for (; j0 + 8 <= M; j0 += 8) {
                 c64 sv[8];
@@ -319,50 +527,38 @@ __global__ void __launch_bounds__(kThreads, 1) k_lanczos_batch(Args a) {
                 if (c < bq) W[i * kBMax + c] = acc[c];
         }
         __syncthreads();
+        LZ_MARK(0);  // W = S Q
         // ---- strip = basis^H W (ncols x bq)
         block_ah_x(B, W, strip, M, ncols, bq, warp, lane);
         __syncthreads();
-        // ---- extend A = V^H h V by the new block (warm start) and V by the identity
+        LZ_MARK(1);  // strip
+        // ---- extend h (raw, in A) by the strip: A[:old, new] = strip[:old], A[new, new] = Herm(strip[new])
         for (int e = tid; e < old * bq; e += kThreads) {
             const int x = e % old, c = e / old;
-            c64 acc = mk(0.0, 0.0);
-            for (int r = 0; r < old; ++r) cmac_conj(acc, V[r + kNBMax * x], strip[r * kBMax + c]);
-            A[x + kNBMax * (old + c)] = acc;
-            A[(old + c) + kNBMax * x] = conj(acc);
+            const c64 v = strip[x * kBMax + c];
+            A[x + kLd * (old + c)] = v;
+            A[(old + c) + kLd * x] = conj(v);
         }
         for (int e = tid; e < bq * bq; e += kThreads) {
             const int r = e % bq, c = e / bq;
             const c64 hrc = strip[(old + r) * kBMax + c], hcr = strip[(old + c) * kBMax + r];
-            A[(old + r) + kNBMax * (old + c)] = 0.5 * (hrc + conj(hcr));  // HermitianMatrix(h), R/src/linalg.cpp:51
-        }
-        for (int e = tid; e < ncols * bq; e += kThreads) {
-            const int x = e % ncols, c = e / ncols;
-            V[x + kNBMax * (old + c)] = mk(x == old + c ? 1.0 : 0.0, 0.0);
-            if (x < old) V[(old + c) + kNBMax * x] = mk(0.0, 0.0);
+            A[(old + r) + kLd * (old + c)] = 0.5 * (hrc + conj(hcr));  // HermitianMatrix(h), R/src/linalg.cpp:51
         }
         __syncthreads();
-        const int sweeps = jacobi_sweeps(A, V, ncols, rot, &ctl[0], &dctl[3]);
-        if (tid == 0) ctl[10] += sweeps;
-        // ---- Ritz values: top-K of diag(A), descending (ties: lower index)
+        // ---- Ritz values of h: tridiagonalise a copy (in V), top-K by multisection
+        for (int e = tid; e < ncols * ncols; e += kThreads) {
+            const int x = e % ncols, c = e / ncols;
+            V[x + kLd * c] = A[x + kLd * c];
+        }
+        __syncthreads();
+        const int kk0 = min(K, ncols);
+        LZ_MARK(2);  // extend + copy
+        tridiagonalize(V, ncols, td, te, tv, tp, dctl + 4);
+        LZ_MARK(3);  // tridiagonalise
+        top_eigenvalues(td, te, ncols, kk0, vals, dctl + 6);
+        LZ_MARK(4);  // bisection
         if (tid == 0) {
-            const int kk = min(K, ncols);
-            for (int j = 0; j < kk; ++j) {
-                int best = -1;
-                double bv = 0.0;
-                for (int x = 0; x < ncols; ++x) {
-                    bool used = false;
-                    for (int u = 0; u < j; ++u) used |= (top[u] == x);
-                    if (used) continue;
-                    const double v = A[x + kNBMax * x].re;
-                    if (best < 0 || v > bv) {
-                        best = x;
-                        bv = v;
-                    }
-                }
-                top[j] = best;
-                vals[j] = bv;
-            }
-            if (sweeps > kMaxSweeps) ctl[6] |= kFrameNoConv;
+            const int kk = kk0;
             int done = 0;
             if (ctl[5] && kk == K) {
                 double change = 0.0;
@@ -388,6 +584,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lanczos_batch(Args a) {
         __syncthreads();
         block_sub(B, Z, Z, strip, M, ncols, bq);
         __syncthreads();
+        LZ_MARK(5);  // two Gram-Schmidt passes
         // ---- q = orthonormal_range(z(:, 1:bz)): column-pivoted CGS2, Eigen ColPivHouseholderQR::rank() rule
         // (nonzero pivots while |R_kk|^2 >= (maxColNorm eps)^2 / rows (rows - k), then |R_kk| > eps size maxpivot)
         const int room = M - ncols;
@@ -444,6 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lanczos_batch(Args a) {
                 __syncthreads();
             }
         }
+        LZ_MARK(6);  // orthonormal_range
         if (tid == 0) {
             if (rank == 0) ctl[3] = 1;  // invariant Krylov space: the Ritz pairs are exact
             else if (ncols + rank > kNBMax) {
@@ -457,16 +655,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_lanczos_batch(Args a) {
         __syncthreads();
         if (ctl[3]) break;
     }
+    LZ_MARK(8);  // exit
     // ---- outputs (the estimate of the last Ritz problem); the iteration cap without convergence -> NOCONV
     const bool capped = !ctl[3];
     const int ncols = ctl[1];
     const int kk = min(K, ncols);
+    // Ritz vectors: one cyclic Jacobi on the final h (in A) with V = I; top-K of its diagonal
+    for (int e = tid; e < ncols * ncols; e += kThreads) {
+        const int x = e % ncols, c = e / ncols;
+        V[x + kLd * c] = mk(x == c ? 1.0 : 0.0, 0.0);
+    }
+    __syncthreads();
+    const int sweeps = jacobi_sweeps(A, V, ncols, rot, &ctl[0], &dctl[3]);
+    LZ_MARK(7);  // final Jacobi
+    if (tid == 0) {
+        ctl[10] = sweeps;
+        if (sweeps > kMaxSweeps) ctl[6] |= kFrameNoConv;
+        for (int j = 0; j < kk; ++j) {
+            int best = -1;
+            double bv = 0.0;
+            for (int x = 0; x < ncols; ++x) {
+                bool used = false;
+                for (int u = 0; u < j; ++u) used |= (top[u] == x);
+                if (used) continue;
+                const double v = A[x + kLd * x].re;
+                if (best < 0 || v > bv) {
+                    best = x;
+                    bv = v;
+                }
+            }
+            top[j] = best;
+            vals[j] = bv;
+        }
+    }
+    __syncthreads();
     double* ob = a.out_basis + static_cast<size_t>(f) * K * M * 2;
     for (int e = tid; e < M * K; e += kThreads) {
         const int j = e / M, i = e - j * M;
         c64 u = mk(0.0, 0.0);
         if (j < kk)
-            for (int r = 0; r < ncols; ++r) u = u + B[static_cast<size_t>(r) * M + i] * V[r + kNBMax * top[j]];
+            for (int r = 0; r < ncols; ++r) u = u + B[static_cast<size_t>(r) * M + i] * V[r + kLd * top[j]];
         ob[2 * e] = u.re;
         ob[2 * e + 1] = u.im;
     }
@@ -479,7 +707,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lanczos_batch(Args a) {
         int flags = ctl[6] | (capped ? kFrameNoConv : 0) | ((ctl[6] & kFrameCap) ? kFrameNoConv : 0);
         if (flags) atomicOr(&a.status[f], flags);
         if (a.last_change) a.last_change[f] = dctl[0];
-        if (a.iters) a.iters[f] = ctl[9] * 10000 + ctl[10];  // iterations, total Jacobi sweeps
+        if (a.iters) a.iters[f] = ctl[9] * 10000 + ctl[10];  // iterations, Jacobi sweeps of the final Ritz solve
     }
 }
 
@@ -513,8 +741,9 @@ std::vector<double> fm_lanczos_start_block(int64_t m, int b) {
 
 size_t fm_lanczos_batch_smem() {
     using namespace fmk::lzb;
-    return sizeof(fmk::c64) * (2 * kNBMax * kNBMax + kNBMax * kBMax) + sizeof(Rot) * (kNBMax / 2) +
-           sizeof(double) * 3 * kBMax + sizeof(int) * (kBMax + 16) + sizeof(double) * 4 + 64;
+    return sizeof(fmk::c64) * (2 * kLd * kNBMax + kNBMax * kBMax) + sizeof(Rot) * (kNBMax / 2) +
+           sizeof(double) * 3 * kBMax + sizeof(int) * (kBMax + 16) + sizeof(double) * (16 + 2 * kNBMax) +
+           sizeof(fmk::c64) * 2 * kNBMax + 64;
 }
 int fm_lanczos_batch_bmax() { return fmk::lzb::kBMax; }
 int fm_lanczos_batch_nbmax() { return fmk::lzb::kNBMax; }
@@ -584,3 +813,50 @@ extern "C" fm_status fm_block_lanczos_batch(const float* s, int64_t frames, int6
     if (e != cudaSuccess) return fm_fail_cuda(e, "fm_block_lanczos_batch", __FILE__, __LINE__);
     return FM_OK;
 }
+
+// Debug / test hook: the Ritz-value kernel path on one Hermitian matrix (h n x n complex128 column-major, n <= 72):
+// Householder tridiagonalisation + Sturm multisection, the kk largest eigenvalues descending into out (device).
+namespace fmk {
+namespace lzb {
+__global__ void __launch_bounds__(kThreads, 1) k_ritz_probe(const c64* h, int n, int kk, double* out) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    c64* T = reinterpret_cast<c64*>(smem_raw);
+    double* d = reinterpret_cast<double*>(T + kLd * kNBMax);
+    double* e = d + kNBMax;
+    c64* vv = reinterpret_cast<c64*>(e + kNBMax);
+    c64* pp = vv + kNBMax;
+    double* red = reinterpret_cast<double*>(pp + kNBMax);
+    for (int i = threadIdx.x; i < n * n; i += kThreads) T[(i % n) + kLd * (i / n)] = h[i];
+    __syncthreads();
+    tridiagonalize(T, n, d, e, vv, pp, red);
+    top_eigenvalues(d, e, n, kk, out, red + 4);
+}
+}  // namespace lzb
+}  // namespace fmk
+
+extern "C" fm_status fm_debug_ritz_values(const double* h, int32_t n, int32_t kk, double* out) {
+    using namespace fmk::lzb;
+    if (n < 2 || n > kNBMax || kk < 1 || kk > kBMax || kk > n) return fm_set_error(FM_EINVAL, "ritz probe: bad size");
+    const size_t smem = sizeof(fmk::c64) * (kLd * kNBMax + 2 * kNBMax) + sizeof(double) * (2 * kNBMax + 16);
+    double *dh = nullptr, *dout = nullptr;
+    cudaMalloc(&dh, sizeof(double) * 2 * n * n);
+    cudaMalloc(&dout, sizeof(double) * kk);
+    cudaMemcpy(dh, h, sizeof(double) * 2 * n * n, cudaMemcpyHostToDevice);
+    cudaFuncSetAttribute(k_ritz_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_ritz_probe<<<1, kThreads, smem>>>(reinterpret_cast<const fmk::c64*>(dh), n, kk, dout);
+    cudaError_t err = cudaMemcpy(out, dout, sizeof(double) * kk, cudaMemcpyDeviceToHost);
+    cudaFree(dh);
+    cudaFree(dout);
+    if (err != cudaSuccess) return fm_fail_cuda(err, "fm_debug_ritz_values", __FILE__, __LINE__);
+    return FM_OK;
+}
+
+#ifdef FM_LZ_TIMELINE
+extern "C" int fm_debug_lz_timeline(long long* host, int zero) {
+    if (zero) {
+        static long long z[16] = {};
+        return static_cast<int>(cudaMemcpyToSymbol(fmk::lzb::g_lz_tl, z, sizeof(z)));
+    }
+    return static_cast<int>(cudaMemcpyFromSymbol(host, fmk::lzb::g_lz_tl, sizeof(long long) * 16));
+}
+#endif

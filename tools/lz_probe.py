@@ -25,11 +25,11 @@ def main():
     torch.cuda.synchronize()
     r = out["covariance"]
     for _ in range(2):
-        fm.block_lanczos_batch(r, K, K, 200)
+        fm.block_lanczos_batch(torch.view_as_complex(r), K, K, 200)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    b, e, st, it = fm.block_lanczos_batch(r, K, K, 200)
+    b, e, st, it = fm.block_lanczos_batch(torch.view_as_complex(r), K, K, 200)
     e1.record()
     torch.cuda.synchronize()
     it = it.cpu().numpy()

@@ -67,7 +67,7 @@ def per_source(cfg, snr_db, frames=None):
 
 def cases():
     c = O.baseline_configs()
-    out = {name: (c[name], 1.0) for name in ("c1", "c2", "c3", "c4", "c5", "c3n")}
+    out = {name: (c[name], 1.0) for name in ("c1", "c2", "c3", "c4", "c5", "c3n", "c2lz")}
     for s in (-20, -12, 12):
         cfg = c["c2"]
         out[f"c2_scale2^{s}"] = (cfg, 2.0 ** s)
@@ -106,11 +106,61 @@ def run_case(fm, name, cfg, scale):
             "gate": {"db": 0.05, "pass": bool(e.max() <= 0.05 and not mism and not np.count_nonzero(st))}}
 
 
+_B = {}
+
+
+def _toa_ref(args):
+    cfg, i, f, xi = args
+    if "b" not in _B:
+        _B["b"] = O.beat_steering_matrix(O.beat_grid(cfg.grid_size, cfg.w0, cfg.w1), cfg.spec.n)
+    est, p_ref, pk = O.run_toa_frame(cfg, xi, f, _B["b"])
+    nb, rank = _margins(p_ref, pk.cells, cfg.spec.k)
+    return i, p_ref, pk.cells, nb, rank
+
+
+def run_toa_case(fm):
+    """The ToA path (FM_PLAN_TEMPORAL) on a whole 1024-frame batch of seeded beat frames vs the oracle."""
+    import torch
+    cfg = O.ToaConfig()
+    frames = list(range(cfg.frames))
+    x, _ = O.generate_toa_batch(cfg.base_seed, frames, cfg.spec)
+    sp = cfg.spec
+    plan = fm.BatchPlan(sp.m, sp.n, sp.k, "fast2", p=cfg.p, t=cfg.t, grid_size=cfg.grid_size, theta0=cfg.w0,
+                        theta1=cfg.w1, min_sep_cells=cfg.min_sep_cells, max_frames=len(frames), temporal=True)
+    om = torch.from_numpy(fm.draw_omega_batch([fm.derive(O.frame_seed(cfg.base_seed, f), 4) for f in frames],
+                                              sp.n, cfg.p)).cuda()
+    out = plan.outputs(len(frames), spectrum=True)
+    plan.run(len(frames), torch.from_numpy(np.ascontiguousarray(x).view(np.float32)).cuda(), om, None, out)
+    torch.cuda.synchronize()
+    res = {k: v.cpu().numpy() for k, v in out.items()}
+    with ProcessPoolExecutor(max_workers=min(os.cpu_count() or 1, 16)) as ex:
+        refs = sorted(ex.map(_toa_ref, [(cfg, i, f, x[i]) for i, f in enumerate(frames)], chunksize=4))
+    errs, mism, nbm, rkm = [], [], [], []
+    for i, p_ref, cells, nb, rank in refs:
+        errs.append(O.spectrum_db_error(res["spectrum"][i].astype(np.float64), p_ref))
+        nbm.append(nb)
+        rkm.append(rank)
+        got = [int(v) for v in res["peak_cells"][i][: int(res["peak_count"][i])]]
+        if got != cells:
+            mism.append({"frame": frames[i], "gpu": got, "oracle": cells, "nb_margin": nb, "rank_margin": rank})
+    e = np.array(errs)
+    st = res["status"]
+    return {"case": "toa", "config": "toa", "method": "fast2 on T = X^H X / M", "frames": len(frames), "scale": 1.0,
+            "worst_db": float(e.max()), "p99_db": float(np.percentile(e, 99)), "median_db": float(np.median(e)),
+            "n_mismatch": len(mism), "mismatches": mism[:10], "status_nonzero": int(np.count_nonzero(st)),
+            "status_values": sorted({int(v) for v in st}),
+            "min_neighbour_margin": float(np.min(nbm)), "min_rank_margin": float(np.min(rkm)),
+            "gate": {"db": 0.05, "pass": bool(e.max() <= 0.05 and not mism and not np.count_nonzero(st))}}
+
+
 def main():
     import paper_1911_07434_b200 as fm
     all_cases = cases()
-    names = sys.argv[1:] or list(all_cases)
+    names = sys.argv[1:] or list(all_cases) + ["toa"]
     for n in names:
+        if n == "toa":
+            print(json.dumps(run_toa_case(fm)), flush=True)
+            continue
         cfg, scale = all_cases[n]
         print(json.dumps(run_case(fm, n, cfg, scale)), flush=True)
 
