@@ -102,3 +102,25 @@ def test_live_reference_estimators(oracle):
         assert oracle.projector_error(oracle.exact_signal_subspace(s, k).basis, bx) < 1e-9
         spec = R.music_spectrum(b, 721)
         assert np.max(np.abs(oracle.music_spectrum(b, oracle.AngleGrid(721)) - spec) / spec) < 1e-9
+
+
+def test_live_reference_run_frame_matches_port(oracle):
+    """The CPU reference arm of bench.py (oracle/_ref ref_run_frame: the reference's covariance -> estimator ->
+    music_spectrum on AngleGrid(L) = [0, pi] -> extract_peaks) agrees with the port on the same grid."""
+    from oracle import ref_lib
+    if not ref_lib.available():
+        pytest.skip("oracle/_ref/libref_fastmusic.so not built (reference tree absent)")
+    cfg = oracle.baseline_configs()["c1"]
+    x, _, _ = oracle.generate_batch(cfg.base_seed, [0], cfg.spec)
+    seed = oracle.derive(oracle.frame_seed(cfg.base_seed, 0), 4)
+    st, cells, spec = ref_lib.run_frame(x[0], cfg.spec.k, "fast2", cfg.p, cfg.t, seed, cfg.grid_size, spectrum=True)
+    assert st == 0
+    grid = oracle.AngleGrid(cfg.grid_size)
+    est, p, pk = oracle.run_frame(cfg, x[0], 0, grid)
+    assert np.max(np.abs(p - spec) / spec) < 1e-8
+    # [0, pi] is mirror-symmetric in sin(theta): theta and pi - theta peaks tie to rounding, either may rank first
+    fold = lambda cs: sorted(min(c, cfg.grid_size - 1 - c) for c in cs)  # noqa: E731
+    assert fold(cells) == fold(pk.cells)
+    for method in ("exact", "lanczos"):
+        st, c2, _ = ref_lib.run_frame(x[0], cfg.spec.k, method, 0, 200, 0, cfg.grid_size)
+        assert st == 0 and len(c2) == cfg.spec.k
