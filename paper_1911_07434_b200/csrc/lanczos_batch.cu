@@ -10,8 +10,8 @@
 //   Ritz values                   Householder tridiagonalisation of a copy, then the top-K eigenvalues by Sturm
 //                                 multisection (16 probes per eigenvalue and round): per iteration O(n^3 / threads)
 //                                 with ~5 barriers per column, instead of sweeps of rotations
-//   Ritz vectors (once, at exit)  two-sided cyclic Jacobi on h (parallel round-robin pairs, complex rotations) with the
-//                                 rotations accumulated in shared memory; top-K of its diagonal
+//   Ritz vectors (once, at exit)  tridiagonalisation keeping the reflectors, inverse iteration on the real tridiagonal
+//                                 for the K Ritz values, Gram-Schmidt, phases and reflectors back (ritz_vectors)
 //   convergence                   |vals - prev| / max(|vals|, 1e-300) <= 1e-10 on two consecutive checks
 //   z = W - basis (basis^H W),    twice (the reference's two Gram-Schmidt passes)
 //   q = orthonormal_range(z)      column-pivoted CGS2 with Eigen's ColPivHouseholderQR rank rule
@@ -40,7 +40,9 @@ namespace lzb {
 constexpr int kThreads = 256;
 constexpr int kBMax = 16;   // block columns per expansion
 constexpr int kNBMax = 72;  // basis columns: A, V complex128 72 x 72 each in shared memory
-constexpr int kLd = kNBMax + 1;  // their leading dimension: 1168 B, so rows walked across columns are bank-conflict free
+constexpr int kLd = kNBMax + 1;
+static_assert(16 * kLd * 16 + 8 * 16 * 5 * kNBMax + 16 * kNBMax <= 16 * kLd * kNBMax,
+              "exit-time Ritz-vector scratch (Z, solver rows, phases) fits in A");  // their leading dimension: 1168 B, so rows walked across columns are bank-conflict free
 constexpr int kMaxSweeps = 60;
 constexpr double kTol = 1e-10;  // R/src/estimators.cpp:160
 
@@ -309,7 +311,10 @@ __device__ __forceinline__ void block_sub(const c64* B, const c64* X, c64* Y, co
 // T -> Q^H T Q real symmetric tridiagonal, diagonal d[i] and off-diagonal |e[i]| (the phases of a complex Hermitian
 // tridiagonal are a diagonal unitary similarity away). Step k: unit v on rows k+1.., p = T v, w = p - (v^H p) v,
 // T22 -= 2 (v w^H + w v^H). Scratch: vv, pp (kNBMax each).
-__device__ void tridiagonalize(c64* T, int n, double* d, double* e, c64* vv, c64* pp, double* red) {
+// keep (optional): the unit Householder vector of step k is left in column k below the diagonal and the complex
+// sub-diagonal entry in alph[k] (the back-transformation of the Ritz vectors needs both).
+__device__ void tridiagonalize(c64* T, int n, double* d, double* e, c64* vv, c64* pp, double* red,
+                               c64* alph = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int kWarps = kThreads / 32;
     for (int k = 0; k + 2 < n; ++k) {
@@ -330,7 +335,10 @@ __device__ void tridiagonalize(c64* T, int n, double* d, double* e, c64* vv, c64
             if (tid == 0) {
                 d[k] = T[k + kLd * k].re;
                 e[k] = sqrt(norm2(x0));
+                if (alph) alph[k] = x0;
             }
+            if (alph)
+                for (int i = tid; i < L; i += kThreads) T[(k + 1 + i) + kLd * k] = mk(0.0, 0.0);  // H_k = I
             __syncthreads();
             continue;
         }
@@ -372,15 +380,142 @@ __device__ void tridiagonalize(c64* T, int n, double* d, double* e, c64* vv, c64
         if (tid == 0) {
             d[k] = T[k + kLd * k].re;
             e[k] = xn;  // |alpha|
+            if (alph) alph[k] = alpha;
         }
         __syncthreads();
+        if (alph)
+            for (int i = tid; i < L; i += kThreads) T[(k + 1 + i) + kLd * k] = vv[i];
     }
     if (tid == 0) {
         if (n >= 2) {
             d[n - 2] = T[(n - 2) + kLd * (n - 2)].re;
             e[n - 2] = sqrt(norm2(T[(n - 1) + kLd * (n - 2)]));
+            if (alph) alph[n - 2] = T[(n - 1) + kLd * (n - 2)];
         }
         d[n - 1] = T[(n - 1) + kLd * (n - 1)].re;
+    }
+    __syncthreads();
+}
+
+// Eigenvectors of the Hermitian matrix tridiagonalize(..., alph) reduced (T holds the Householder vectors) for
+// its kk eigenvalues lam (descending): inverse iteration on the real tridiagonal (LU with partial pivoting, as
+// LAPACK dgttrf / dgttrs, two solves from a fixed start), modified Gram-Schmidt over the kk vectors (vectors of
+// close eigenvalues come out mixed; their span is what the projector needs), the diagonal phases taking the real
+// tridiagonal to the complex one, then the reflectors in reverse (one warp per vector). Z: n x kk, leading dim kLd.
+// Scratch: 5 * kNBMax doubles per vector.
+__device__ void ritz_vectors(const c64* T, const double* d, const double* e, const c64* alph, int n, int kk,
+                             const double* lam, c64* Z, double* scr) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int kWarps = kThreads / 32;
+    if (tid < kk) {  // one thread per eigenvalue: the tridiagonal solves are serial in n
+        double* dd = scr + tid * 5 * kNBMax;
+        double* du = dd + kNBMax;
+        double* du2 = du + kNBMax;
+        double* dl = du2 + kNBMax;
+        double* x = dl + kNBMax;
+        double tnorm = 0.0;
+        for (int i = 0; i < n; ++i) tnorm = fmax(tnorm, fabs(d[i]) + (i > 0 ? e[i - 1] : 0.0) + (i + 1 < n ? e[i] : 0.0));
+        const double tiny = fmax(2.220446049250313e-16 * tnorm, 1e-300);
+        const double l = lam[tid];
+        for (int i = 0; i < n; ++i) {
+            dd[i] = d[i] - l;
+            if (i + 1 < n) {
+                du[i] = e[i];
+                dl[i] = e[i];
+            }
+            du2[i] = 0.0;
+            x[i] = 1.0 + 0.001 * static_cast<double>((i * 7 + tid * 3) % 11);  // fixed, non-degenerate start
+        }
+        int piv = 0;  // bit i: rows i, i + 1 interchanged at step i (n <= 72 -> two words)
+        unsigned long long pv0 = 0ull, pv1 = 0ull;
+        for (int i = 0; i + 1 < n; ++i) {
+            if (fabs(dd[i]) >= fabs(dl[i])) {
+                if (dd[i] == 0.0) dd[i] = tiny;
+                const double fact = dl[i] / dd[i];
+                dl[i] = fact;
+                dd[i + 1] -= fact * du[i];
+            } else {
+                const double fact = dd[i] / dl[i];
+                dd[i] = dl[i];
+                dl[i] = fact;
+                const double tmp = du[i];
+                du[i] = dd[i + 1];
+                dd[i + 1] = tmp - fact * dd[i + 1];
+                if (i + 2 < n) {
+                    du2[i] = du[i + 1];
+                    du[i + 1] = -fact * du[i + 1];
+                }
+                if (i < 64) pv0 |= 1ull << i;
+                else pv1 |= 1ull << (i - 64);
+            }
+        }
+        if (dd[n - 1] == 0.0) dd[n - 1] = tiny;
+        for (int i = 0; i < n; ++i)
+            if (fabs(dd[i]) < tiny) dd[i] = dd[i] < 0.0 ? -tiny : tiny;
+        (void)piv;
+        for (int rep = 0; rep < 2; ++rep) {
+            for (int i = 0; i + 1 < n; ++i) {  // L solve with the interchanges
+                const bool sw = i < 64 ? (pv0 >> i) & 1ull : (pv1 >> (i - 64)) & 1ull;
+                if (!sw) {
+                    x[i + 1] -= dl[i] * x[i];
+                } else {
+                    const double t = x[i];
+                    x[i] = x[i + 1];
+                    x[i + 1] = t - dl[i] * x[i];
+                }
+            }
+            x[n - 1] /= dd[n - 1];  // U solve (diag dd, super du, second super du2)
+            if (n >= 2) x[n - 2] = (x[n - 2] - du[n - 2] * x[n - 1]) / dd[n - 2];
+            for (int i = n - 3; i >= 0; --i) x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) / dd[i];
+            double nr = 0.0;
+            for (int i = 0; i < n; ++i) nr = fmax(nr, fabs(x[i]));
+            const double s = nr > 0.0 ? 1.0 / nr : 1.0;
+            for (int i = 0; i < n; ++i) x[i] *= s;
+        }
+        for (int i = 0; i < n; ++i) Z[i + kLd * tid] = mk(x[i], 0.0);
+    }
+    __syncthreads();
+    if (warp == 0) {  // modified Gram-Schmidt over the kk real vectors (one warp, lanes over rows)
+        for (int j = 0; j < kk; ++j) {
+            for (int q = 0; q < j; ++q) {
+                double dot = 0.0;
+                for (int i = lane; i < n; i += 32) dot += Z[i + kLd * q].re * Z[i + kLd * j].re;
+                dot = warp_sum(dot);
+                for (int i = lane; i < n; i += 32) Z[i + kLd * j].re -= dot * Z[i + kLd * q].re;
+                __syncwarp();
+            }
+            double nr = 0.0;
+            for (int i = lane; i < n; i += 32) nr += Z[i + kLd * j].re * Z[i + kLd * j].re;
+            nr = warp_sum(nr);
+            const double s = nr > 0.0 ? 1.0 / sqrt(nr) : 0.0;
+            for (int i = lane; i < n; i += 32) Z[i + kLd * j].re *= s;
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    for (int j = warp; j < kk; j += kWarps) {  // phases, then Q = H_0 ... H_{n-3} applied from the right end
+        c64* z = Z + kLd * j;
+        if (lane == 0) {
+            c64 ph = mk(1.0, 0.0);
+            for (int i = 0; i < n; ++i) {
+                const double zr = z[i].re;
+                z[i] = mk(zr * ph.re, zr * ph.im);
+                if (i + 1 < n) {
+                    const double a = sqrt(norm2(alph[i]));
+                    if (a > 0.0) ph = ph * mk(alph[i].re / a, alph[i].im / a);
+                }
+            }
+        }
+        __syncwarp();
+        for (int k = n - 3; k >= 0; --k) {
+            const int L = n - k - 1;
+            const c64* v = T + (k + 1) + kLd * k;
+            c64 acc = mk(0.0, 0.0);
+            for (int i = lane; i < L; i += 32) cmac_conj(acc, v[i], z[k + 1 + i]);
+            acc = warp_csum(acc);
+            for (int i = lane; i < L; i += 32) z[k + 1 + i] = z[k + 1 + i] - 2.0 * (v[i] * acc);
+            __syncwarp();
+        }
     }
     __syncthreads();
 }
@@ -552,6 +687,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lanczos_batch(Args a) {
         }
         __syncthreads();
         const int kk0 = min(K, ncols);
+        if (tid == 0) ctl[11] = ncols;  // size of the h the Ritz values below belong to
         LZ_MARK(2);  // extend + copy
         tridiagonalize(V, ncols, td, te, tv, tp, dctl + 4);
         LZ_MARK(3);  // tridiagonalise
@@ -658,43 +794,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_lanczos_batch(Args a) {
     LZ_MARK(8);  // exit
     // ---- outputs (the estimate of the last Ritz problem); the iteration cap without convergence -> NOCONV
     const bool capped = !ctl[3];
-    const int ncols = ctl[1];
-    const int kk = min(K, ncols);
-    // Ritz vectors: one cyclic Jacobi on the final h (in A) with V = I; top-K of its diagonal
-    for (int e = tid; e < ncols * ncols; e += kThreads) {
-        const int x = e % ncols, c = e / ncols;
-        V[x + kLd * c] = mk(x == c ? 1.0 : 0.0, 0.0);
+    const int hn = ctl[11];  // the h of the last Ritz values (the basis may hold one more block after the cap)
+    const int kk = min(K, hn);
+    // Ritz vectors of h for those values: tridiagonalise a copy keeping the reflectors, inverse iteration, back-
+    // transformation (ritz_vectors); Z and the solver scratch live in A's space once h is copied out
+    for (int e = tid; e < hn * hn; e += kThreads) {
+        const int x = e % hn, c = e / hn;
+        V[x + kLd * c] = A[x + kLd * c];
     }
     __syncthreads();
-    const int sweeps = jacobi_sweeps(A, V, ncols, rot, &ctl[0], &dctl[3]);
-    LZ_MARK(7);  // final Jacobi
-    if (tid == 0) {
-        ctl[10] = sweeps;
-        if (sweeps > kMaxSweeps) ctl[6] |= kFrameNoConv;
-        for (int j = 0; j < kk; ++j) {
-            int best = -1;
-            double bv = 0.0;
-            for (int x = 0; x < ncols; ++x) {
-                bool used = false;
-                for (int u = 0; u < j; ++u) used |= (top[u] == x);
-                if (used) continue;
-                const double v = A[x + kLd * x].re;
-                if (best < 0 || v > bv) {
-                    best = x;
-                    bv = v;
-                }
-            }
-            top[j] = best;
-            vals[j] = bv;
-        }
-    }
-    __syncthreads();
+    c64* Zs = A;                                                  // kLd x kk
+    double* scr = reinterpret_cast<double*>(A + kLd * kBMax);     // kBMax x 5 x kNBMax
+    c64* alph = reinterpret_cast<c64*>(scr + kBMax * 5 * kNBMax);  // kNBMax
+    tridiagonalize(V, hn, td, te, tv, tp, dctl + 4, alph);
+    ritz_vectors(V, td, te, alph, hn, kk, vals, Zs, scr);
+    LZ_MARK(7);  // Ritz vectors
     double* ob = a.out_basis + static_cast<size_t>(f) * K * M * 2;
     for (int e = tid; e < M * K; e += kThreads) {
         const int j = e / M, i = e - j * M;
         c64 u = mk(0.0, 0.0);
         if (j < kk)
-            for (int r = 0; r < ncols; ++r) u = u + B[static_cast<size_t>(r) * M + i] * V[r + kLd * top[j]];
+            for (int r = 0; r < hn; ++r) u = u + B[static_cast<size_t>(r) * M + i] * Zs[r + kLd * j];
         ob[2 * e] = u.re;
         ob[2 * e + 1] = u.im;
     }
@@ -707,7 +827,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lanczos_batch(Args a) {
         int flags = ctl[6] | (capped ? kFrameNoConv : 0) | ((ctl[6] & kFrameCap) ? kFrameNoConv : 0);
         if (flags) atomicOr(&a.status[f], flags);
         if (a.last_change) a.last_change[f] = dctl[0];
-        if (a.iters) a.iters[f] = ctl[9] * 10000 + ctl[10];  // iterations, Jacobi sweeps of the final Ritz solve
+        if (a.iters) a.iters[f] = ctl[9] * 10000;  // Krylov iterations
     }
 }
 
