@@ -43,7 +43,6 @@ constexpr int kNBMax = 72;  // basis columns: A, V complex128 72 x 72 each in sh
 constexpr int kLd = kNBMax + 1;
 static_assert(16 * kLd * 16 + 8 * 16 * 5 * kNBMax + 16 * kNBMax <= 16 * kLd * kNBMax,
               "exit-time Ritz-vector scratch (Z, solver rows, phases) fits in A");  // their leading dimension: 1168 B, so rows walked across columns are bank-conflict free
-constexpr int kMaxSweeps = 60;
 constexpr double kTol = 1e-10;  // R/src/estimators.cpp:160
 
 #ifdef FM_LZ_TIMELINE  // experiment only: clock64 per phase of block 0 (tools/lz_timeline.py)
@@ -96,159 +95,6 @@ __device__ __forceinline__ c64 warp_csum(c64 v) {
     v.re = warp_sum(v.re);
     v.im = warp_sum(v.im);
     return v;
-}
-
-// Round-robin pairing (circle method) over n2 (even) slots: step r in [0, n2 - 1), pair t in [0, n2 / 2).
-__device__ __forceinline__ void rr_pair(int r, int t, int n2, int& p, int& q) {
-    const int L = n2 - 1;
-    int a, b;
-    if (t == 0) {
-        a = r;
-        b = L;
-    } else {
-        a = (r + t) % L;
-        b = (r - t + L) % L;
-    }
-    p = min(a, b);
-    q = max(a, b);
-}
-
-struct Rot {
-    int p, q;
-    double c, s;
-    c64 e;  // phase of A(p, q)
-    double t_g;  // t |A(p, q)| (diagonal update)
-};
-
-// Two-sided cyclic Jacobi on the Hermitian n x n leading block of A (column-major, leading dim kLd),
-// accumulating the rotations into V's n x n block. Returns the number of sweeps (kMaxSweeps + 1: no convergence).
-// Rotation threshold: |A(p, q)| <= 2^-52 max_i |A(i, i)| is at the rounding level of the matrix (a purely relative
-// test, |A(p, q)| <= eps sqrt|A(p, p) A(q, q)|, keeps re-rotating the rounding noise that rotations of large entries
-// leave between pairs of small ones, and never ends); the top-K Ritz values it decides are then exact to that level.
-__device__ int jacobi_sweeps(c64* A, c64* V, int n, Rot* rot, int* s_any, double* s_amax) {
-    const int n2 = n + (n & 1);
-    const int np = n2 / 2;
-    const int tid = threadIdx.x;
-    for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
-        if (tid == 0) {
-            *s_any = 0;
-            double am = 0.0;
-            for (int x = 0; x < n; ++x) am = fmax(am, fabs(A[x + kLd * x].re));
-            *s_amax = am;
-        }
-        __syncthreads();
-        const double thr = 2.220446049250313e-16 * *s_amax;
-        for (int r = 0; r < n2 - 1; ++r) {
-            if (tid < np) {
-                int p, q;
-                rr_pair(r, tid, n2, p, q);
-                Rot o;
-                o.p = p;
-                o.q = q;
-                o.c = 1.0;
-                o.s = 0.0;
-                o.e = mk(1.0, 0.0);
-                o.t_g = 0.0;
-                if (q < n) {
-                    const c64 apq = A[p + kLd * q];
-                    const double g = sqrt(norm2(apq));
-                    const double app = A[p + kLd * p].re, aqq = A[q + kLd * q].re;
-                    // skip rotations below the relative accuracy of the pair (and denormal-size entries)
-                    if (g > 1e-290 && g > thr) {
-                        const double tau = (aqq - app) / (2.0 * g);
-                        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                        o.c = 1.0 / sqrt(1.0 + t * t);
-                        o.s = t * o.c;
-                        o.e = mk(apq.re / g, apq.im / g);
-                        o.t_g = t * g;
-                        *s_any = 1;
-                    } else {
-                        o.q = -1;  // inactive
-                    }
-                } else {
-                    o.q = -1;
-                }
-                rot[tid] = o;
-            }
-            __syncthreads();
-            // columns: A <- A J, V <- V J with J = [[c, s e], [-s conj(e), c]] on (p, q); tpp threads per pair,
-            // the rotation in registers, two rows per pass (independent loads in flight)
-            const int tpp = kThreads / np;
-            const int pt = tid / tpp, sub = tid - pt * tpp;
-            if (pt < np) {
-                const Rot o = rot[pt];
-                if (o.q >= 0) {
-                    const c64 ep = mk(o.s * o.e.re, o.s * o.e.im);  // s e
-                    const c64 epc = conj(ep);
-                    c64* Ap = A + kLd * o.p;
-                    c64* Aq = A + kLd * o.q;
-                    c64* Vp = V + kLd * o.p;
-                    c64* Vq = V + kLd * o.q;
-                    for (int row = sub; row < n; row += 2 * tpp) {
-                        const int r2 = row + tpp;
-                        const bool two = r2 < n;
-                        const c64 ap = Ap[row], aq = Aq[row], vp = Vp[row], vq = Vq[row];
-                        c64 ap2 = mk(0.0, 0.0), aq2 = ap2, vp2 = ap2, vq2 = ap2;
-                        if (two) {
-                            ap2 = Ap[r2];
-                            aq2 = Aq[r2];
-                            vp2 = Vp[r2];
-                            vq2 = Vq[r2];
-                        }
-                        Ap[row] = o.c * ap - epc * aq;
-                        Aq[row] = ep * ap + o.c * aq;
-                        Vp[row] = o.c * vp - epc * vq;
-                        Vq[row] = ep * vp + o.c * vq;
-                        if (two) {
-                            Ap[r2] = o.c * ap2 - epc * aq2;
-                            Aq[r2] = ep * ap2 + o.c * aq2;
-                            Vp[r2] = o.c * vp2 - epc * vq2;
-                            Vq[r2] = ep * vp2 + o.c * vq2;
-                        }
-                    }
-                }
-            }
-            __syncthreads();
-            // rows: A <- J^H A (J^H = [[c, -s e], [s conj(e), c]])
-            if (pt < np) {
-                const Rot o = rot[pt];
-                if (o.q >= 0) {
-                    const c64 ep = mk(o.s * o.e.re, o.s * o.e.im);
-                    const c64 epc = conj(ep);
-                    for (int col = sub; col < n; col += 2 * tpp) {
-                        const int c2 = col + tpp;
-                        const bool two = c2 < n;
-                        const c64 ap = A[o.p + kLd * col], aq = A[o.q + kLd * col];
-                        c64 ap2 = mk(0.0, 0.0), aq2 = ap2;
-                        if (two) {
-                            ap2 = A[o.p + kLd * c2];
-                            aq2 = A[o.q + kLd * c2];
-                        }
-                        A[o.p + kLd * col] = o.c * ap - ep * aq;
-                        A[o.q + kLd * col] = epc * ap + o.c * aq;
-                        if (two) {
-                            A[o.p + kLd * c2] = o.c * ap2 - ep * aq2;
-                            A[o.q + kLd * c2] = epc * ap2 + o.c * aq2;
-                        }
-                    }
-                }
-            }
-            __syncthreads();
-            if (tid < np) {  // the pair's closed form: zero off-diagonal, real diagonal
-                const Rot o = rot[tid];
-                if (o.q >= 0) {
-                    A[o.p + kLd * o.q] = mk(0.0, 0.0);
-                    A[o.q + kLd * o.p] = mk(0.0, 0.0);
-                    A[o.p + kLd * o.p].im = 0.0;
-                    A[o.q + kLd * o.q].im = 0.0;
-                }
-            }
-            __syncthreads();
-        }
-        if (*s_any == 0) return sweep + 1;
-        __syncthreads();
-    }
-    return kMaxSweeps + 1;
 }
 
 // strip(r, c) = sum_i conj(B(i, r)) X(i, c) for r < ncols, c < bq: warp per basis column r, lanes over rows, all bq
@@ -591,8 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lanczos_batch(Args a) {
     c64* A = reinterpret_cast<c64*>(smem_raw);
     c64* V = A + kLd * kNBMax;
     c64* strip = V + kLd * kNBMax;                // kNBMax x kBMax, row-major [r][c]
-    Rot* rot = reinterpret_cast<Rot*>(strip + kNBMax * kBMax);
-    double* vals = reinterpret_cast<double*>(rot + kNBMax / 2);  // [kBMax]
+    double* vals = reinterpret_cast<double*>(strip + kNBMax * kBMax);  // [kBMax]
     double* prev = vals + kBMax;                                   // [kBMax]
     double* nrm = prev + kBMax;                                    // [kBMax] column norms^2 (orthonormal_range)
     int* top = reinterpret_cast<int*>(nrm + kBMax);                // [kBMax]
@@ -861,7 +706,7 @@ std::vector<double> fm_lanczos_start_block(int64_t m, int b) {
 
 size_t fm_lanczos_batch_smem() {
     using namespace fmk::lzb;
-    return sizeof(fmk::c64) * (2 * kLd * kNBMax + kNBMax * kBMax) + sizeof(Rot) * (kNBMax / 2) +
+    return sizeof(fmk::c64) * (2 * kLd * kNBMax + kNBMax * kBMax) +
            sizeof(double) * 3 * kBMax + sizeof(int) * (kBMax + 16) + sizeof(double) * (16 + 2 * kNBMax) +
            sizeof(fmk::c64) * 2 * kNBMax + 64;
 }
