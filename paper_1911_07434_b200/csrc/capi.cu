@@ -83,10 +83,10 @@ cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K,
                                  double* heights, double* baseline, int32_t* count, void* gws, cudaStream_t s,
                                  const int32_t* only = nullptr);
 cudaError_t fm_launch_orthocheck(const void* basis, int frames, int m, int k, double* dev, cudaStream_t s);
-int fm_spectrum_tc_pairs_pad(int L);
+int fm_spectrum_tc_pairs_pad(int L, int half);
 int fm_spectrum_tc_canon_off(int row, int k);
 cudaError_t fm_launch_spectrum_tc(const void* t, const int8_t* zk, int8_t* tk, double* tscale, int frames, int m, int L,
-                                  float* spec32, double* spec64, cudaStream_t s);
+                                  float* spec32, double* spec64, cudaStream_t s, int half);
 cudaError_t fm_launch_spectrum_multi(const void* t, const void* zgrid, int frames, int m, int L, float* spec32,
                                      double* spec64, cudaStream_t s);
 template <typename T>
@@ -273,9 +273,10 @@ std::vector<double> zgrid_host(int64_t L, double theta0, double theta1, double d
 // z = (cos, sin)(delta phi_q) (angle in fp64, glibc) as 5 signed base-128 digits of z / 2, in the zK layout
 // [pair tile of 48][K block of 32][plane = s * 2 + cs][canonical 48 x 32 tile] (zero padding past nq and m).
 std::vector<int8_t> zdig_host_k(int64_t L, double theta0, double theta1, double d, double lambda, int64_t m,
-                                bool beat) {
+                                bool beat, bool half) {
     constexpr int kS = 5;
-    const int64_t nq = (L + 1) / 2, nqp = fm_spectrum_tc_pairs_pad(static_cast<int>(L)), mk = (m + 31) / 32 * 32;
+    const int64_t nq = half ? L : (L + 1) / 2, nqp = fm_spectrum_tc_pairs_pad(static_cast<int>(L), half ? 1 : 0),
+                  mk = (m + 31) / 32 * 32;
     std::vector<int8_t> z(static_cast<size_t>(kS * 2 * nqp * mk), 0);
     const double span = theta1 - theta0;
     for (int64_t q = 0; q < nq; ++q) {
@@ -505,7 +506,8 @@ struct fm_plan_s {
     double* spec64 = nullptr; // frames x L (fp64 spectrum for peak picking)
     double* zgrid = nullptr;  // L complex128
     uint8_t* peak_ws = nullptr;  // peak-picking workspace when a frame's does not fit in shared memory (long grids)
-    int8_t* zk = nullptr;     // mirror-symmetric grids: int8 digits of the cos / sin table (zdig_host_k)
+    int8_t* zk = nullptr;     // int8 digits of the grid's cos / sin table (zdig_host_k)
+    bool zk_half = false;     // grid not mirror-symmetric: every point evaluated as its own pair
     int8_t* tdig = nullptr;   // per batch: int8 digits of t (frames padded per sub-batch)
     double* tscale = nullptr; // per batch: power-of-two scale of each frame's t
     size_t tdig_rows = 0;     // frame rows of tdig / tscale (sub-batch i uses rows f0 + 64 i ..)
@@ -761,10 +763,11 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
         delete pl;
         return fm_fail_cuda(e, "fm_plan_create zgrid", __FILE__, __LINE__);
     }
-    if (desc->theta0 == -desc->theta1) {
+    {  // the tensor-core spectrum for every grid: mirror pairs when symmetric, single points otherwise
+        pl->zk_half = !(desc->theta0 == -desc->theta1);
         const size_t mk = (static_cast<size_t>(desc->m) + 31) / 32 * 32;
-        const auto zkh =
-            zdig_host_k(desc->grid_size, desc->theta0, desc->theta1, desc->d, desc->lambda, desc->m, pl->temporal);
+        const auto zkh = zdig_host_k(desc->grid_size, desc->theta0, desc->theta1, desc->d, desc->lambda, desc->m,
+                                     pl->temporal, pl->zk_half);
         e = pl->get(&pl->zk, zkh.size());
         if (e == cudaSuccess) e = cudaMemcpy(pl->zk, zkh.data(), zkh.size(), cudaMemcpyHostToDevice);
         pl->tdig_rows = B + 128 * 16;
@@ -1097,14 +1100,15 @@ static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io,
     if (prof) mark(pl, 2, s);
     FM_LAUNCH(fm_launch_autocorr(basis, w.t, F, M, K, s));
     if (prof) mark(pl, 3, s);
-    // mirror-symmetric grid (theta0 = -theta1): pairs (theta, -theta) share one evaluation on the INT8 tensor cores
-    // (tcgen05 kind::i8) with fp64-exact digit splitting (spectrum_tc.cu); other grids: the fp64 power recurrence
-    const bool sym = d.theta0 == -d.theta1;
+    // the spectrum on the INT8 tensor cores (tcgen05 kind::i8) with fp64-exact digit splitting (spectrum_tc.cu):
+    // mirror-symmetric grids (theta0 = -theta1) as pairs (theta, -theta) sharing one evaluation, other grids point
+    // by point; the fp64 power recurrence only when the digit workspace does not cover the batch
     const bool dig_fits = w.dslot + (static_cast<size_t>(F) + 127) / 128 * 128 <= pl->tdig_rows;
-    if (sym && pl->zk && dig_fits) {
+    if (pl->zk && dig_fits) {
         const size_t mk = (static_cast<size_t>(M) + 31) / 32 * 32;
         FM_LAUNCH(fm_launch_spectrum_tc(w.t, pl->zk, pl->tdig + w.dslot * 5 * 2 * mk, pl->tscale + w.dslot, F, M,
-                                        static_cast<int>(d.grid_size), io->spectrum, w.spec64, s));
+                                        static_cast<int>(d.grid_size), io->spectrum, w.spec64, s,
+                                        pl->zk_half ? 1 : 0));
     } else {
         FM_LAUNCH(fm_launch_spectrum_multi(w.t, pl->zgrid, F, M, static_cast<int>(d.grid_size), io->spectrum, w.spec64,
                                            s));

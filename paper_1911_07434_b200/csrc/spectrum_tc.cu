@@ -1,4 +1,6 @@
-// MUSIC pseudo-spectrum on mirror-symmetric grids (theta_0 = -theta_{L-1}) on the 5th-gen INT8 tensor cores:
+// MUSIC pseudo-spectrum on the 5th-gen INT8 tensor cores, mirror-symmetric grids (theta_0 = -theta_{L-1}) as
+// pairs (theta, -theta) sharing one evaluation, any other grid (half mode: the ToA beat grid, asymmetric spans) with
+// every point a pair of its own and the mirror values dropped:
 // tcgen05.mma kind::i8 with TMEM int32 accumulators, operands streamed by bulk async copies
 // (R/src/spectrum.cpp:37-68 music_spectrum; steering R/src/scene.cpp:72-82).
 //
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(256) k_slice_tk(const c64* __restrict__ t, int
 
 __global__ void __launch_bounds__(kThreads, 1)
     k_spectrum_tc(const int8_t* __restrict__ tk, const int8_t* __restrict__ zk, const double* __restrict__ tscale, const c64* __restrict__ t, int frames, int m, int nkb, int L,
-                  float* __restrict__ spec32, double* __restrict__ spec64) {
+                  float* __restrict__ spec32, double* __restrict__ spec64, int half) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             named_bar_sync(1 + quarter, 32 * kSplit);
         else
             __syncwarp();
-        const int nq = (L + 1) / 2;
+        const int nq = half ? L : (L + 1) / 2;  // half: every grid point is a "pair" of its own, mirrors dropped
         const int fw = f0 + 32 * quarter;
         constexpr int kRows = (32 + kSplit - 1) / kSplit;
 #pragma unroll 1
@@ -273,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = lane; i < 2 * kN; i += 32) {
                 const int q = i < kN ? q0 + i : q0 + (2 * kN - 1 - i);  // pair of this slot
-                if (q >= nq) continue;
+                if (q >= nq || (half && i >= kN)) continue;
                 const int cell = i < kN ? q : L - 1 - q;
                 if (i >= kN && cell == q) continue;  // centre cell of an odd grid: written once
                 const double P = stg[r * kRow + i];
@@ -295,17 +297,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace fmk
 
 // Plan-side geometry of the tensor-core spectrum: pairs padded to kN, delta to 32.
-int fm_spectrum_tc_pairs_pad(int L) { return ((L + 1) / 2 + fmk::spectc::kN - 1) / fmk::spectc::kN * fmk::spectc::kN; }
+// half = 0: mirror-symmetric grid, (L + 1) / 2 pairs (theta_q, -theta_q); half = 1: any grid, all L points as pairs whose
+// mirror half is discarded (twice the symmetric work per point, still on the tensor cores)
+int fm_spectrum_tc_pairs_pad(int L, int half) {
+    return ((half ? L : (L + 1) / 2) + fmk::spectc::kN - 1) / fmk::spectc::kN * fmk::spectc::kN;
+}
 int fm_spectrum_tc_canon_off(int row, int k) { return fmk::spectc::canon_off(row, k); }
 int fm_spectrum_tc_frames_pad(int frames) { return (frames + fmk::spectc::kM - 1) / fmk::spectc::kM * fmk::spectc::kM; }
 
 // zk: the plan's zK table (capi.cu zdig_host_k); tk / tscale: workspace of fm_spectrum_tc_frames_pad(frames) rows
 // (x 10 planes x mk bytes, mk = M rounded up to 32) and doubles.
 cudaError_t fm_launch_spectrum_tc(const void* t, const int8_t* zk, int8_t* tk, double* tscale, int frames, int m, int L,
-                                  float* spec32, double* spec64, cudaStream_t s) {
+                                  float* spec32, double* spec64, cudaStream_t s, int half) {
     using namespace fmk::spectc;
     const int nkb = (m + kK - 1) / kK;
-    const int fpad = fm_spectrum_tc_frames_pad(frames), nqp = fm_spectrum_tc_pairs_pad(L);
+    const int fpad = fm_spectrum_tc_frames_pad(frames), nqp = fm_spectrum_tc_pairs_pad(L, half);
     k_slice_tk<<<fpad, 256, 0, s>>>(static_cast<const fmk::c64*>(t), tk, tscale, frames, m, nkb);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -313,6 +319,6 @@ cudaError_t fm_launch_spectrum_tc(const void* t, const int8_t* zk, int8_t* tk, d
     if (e != cudaSuccess) return e;
     const dim3 grid(nqp / kN, fpad / kM);
     k_spectrum_tc<<<grid, kThreads, kSmem, s>>>(tk, zk, tscale, static_cast<const fmk::c64*>(t), frames, m, nkb, L,
-                                                spec32, spec64);
+                                                spec32, spec64, half);
     return cudaGetLastError();
 }
