@@ -392,8 +392,8 @@ __device__ __forceinline__ bool better_w(double h1, int c1, double h2, int c2) {
     return h1 > h2 || (h1 == h2 && c1 < c2);
 }
 
-template <bool kInSmem>
-__global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict__ values, int L, int K, int min_sep,
+template <bool kInSmem, int NT = kPRT>
+__global__ void __launch_bounds__(NT) k_peaks_rounds(const double* __restrict__ values, int L, int K, int min_sep,
                                                       PeakOut out, uint8_t* __restrict__ gws,
                                                       const int32_t* __restrict__ only) {
     extern __shared__ __align__(16) uint8_t prs[];
@@ -411,26 +411,26 @@ __global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict_
     int* s_sel = reinterpret_cast<int*>(base + lay.o_sel);
     uint8_t* ex = base + lay.o_ex;
     const int nmask = lay.nmask;
-    __shared__ int s_cnt[kPRT / 32];
+    __shared__ int s_cnt[NT / 32];
     __shared__ int s_nsel;
-    __shared__ double s_wmax[kPRT / 32];
+    __shared__ double s_wmax[NT / 32];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (kInSmem) {
-        for (int l0 = tid; l0 < L; l0 += 8 * kPRT) {
+        for (int l0 = tid; l0 < L; l0 += 8 * NT) {
             double tmp[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const int l = l0 + u * kPRT;
+                const int l = l0 + u * NT;
                 tmp[u] = l < L ? __ldcs(v + l) : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const int l = l0 + u * kPRT;
+                const int l = l0 + u * NT;
                 if (l < L) svw[l] = tmp[u];
             }
         }
     }
-    for (int w = tid; w < nmask; w += kPRT) near[w] = 0u;
+    for (int w = tid; w < nmask; w += NT) near[w] = 0u;
     __syncthreads();
     auto is_max = [&](int l) -> bool {
         if (l < 1 || l >= L - 1) return false;
@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict_
         return (r + 1 < L) && sv[r + 1] < x;
     };
     const int ngroups = lay.ngroups;
-    const int gpw = (ngroups + kPRT / 32 - 1) / (kPRT / 32);
+    const int gpw = (ngroups + NT / 32 - 1) / (NT / 32);
     const int g0 = warp * gpw, g1 = min(ngroups, g0 + gpw);
     int cnt = 0;
     for (int gb = g0; gb < g1; gb += 4) {  // four groups' loads in flight
@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict_
     __syncthreads();
     int off = 0, nc = 0;
 #pragma unroll
-    for (int w = 0; w < kPRT / 32; ++w) {
+    for (int w = 0; w < NT / 32; ++w) {
         off += w < warp ? s_cnt[w] : 0;
         nc += s_cnt[w];
     }
@@ -585,14 +585,14 @@ __global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict_
     }
     __syncthreads();
     double p0 = 0.0;
-    for (int l = tid; l < L; l += kPRT)
+    for (int l = tid; l < L; l += NT)
         if (!((near[l >> 5] >> (l & 31)) & 1u)) p0 = fmax(p0, sv[l]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) p0 = fmax(p0, __shfl_xor_sync(0xffffffffu, p0, o));
     if (lane == 0) s_wmax[warp] = p0;
     __syncthreads();
     const int nsel = s_nsel;
-    for (int xk = tid; xk < K; xk += kPRT) {
+    for (int xk = tid; xk < K; xk += NT) {
         if (xk < nsel) {
             const int c = s_sel[xk];
             int rank = 0;
@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(kPRT) k_peaks_rounds(const double* __restrict_
     }
     if (tid == 0) {
         double b = 0.0;
-        for (int w = 0; w < kPRT / 32; ++w) b = fmax(b, s_wmax[w]);
+        for (int w = 0; w < NT / 32; ++w) b = fmax(b, s_wmax[w]);
         out.baseline[f] = b;
         out.count[f] = nsel;
     }
@@ -724,6 +724,17 @@ cudaError_t fm_launch_peaks_only(const double* values, int frames, int L, int K,
     spec::PeakOut out{cells, heights, baseline, count};
     const spec::PeakLayout lay = spec::peak_layout(L, K, true);
     if (lay.bytes <= spec::kPeakSmemMax) {
+#ifndef FM_PEAKS_LONG_NT
+#define FM_PEAKS_LONG_NT 512
+#endif
+        if (L > 8192) {  // long grids (c4's 18001 cells): one frame per SM by shared memory -> more warps per frame
+            constexpr int NT = FM_PEAKS_LONG_NT;
+            cudaError_t e = cudaFuncSetAttribute(spec::k_peaks_rounds<true, NT>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lay.bytes));
+            if (e != cudaSuccess) return e;
+            spec::k_peaks_rounds<true, NT><<<frames, NT, lay.bytes, s>>>(values, L, K, min_sep, out, nullptr, only);
+            return cudaGetLastError();
+        }
         cudaError_t e = cudaFuncSetAttribute(spec::k_peaks_rounds<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(lay.bytes));
         if (e != cudaSuccess) return e;
