@@ -3,6 +3,9 @@
 // behind the reference-named C++ facade, host random draws and the synthetic frame
 // generator. No CPU compute fallback: every numeric stage below launches a kernel.
 
+#ifndef FM_COV_F16
+#define FM_COV_F16 1  // multi-tile covariance from fp16 planes converted once per batch
+#endif
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -25,7 +28,7 @@
 cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, int64_t frames, int64_t m, int64_t n,
                              cudaStream_t stream, void* planes_hi = nullptr, void* planes_lo = nullptr,
                              float* scale = nullptr, int64_t n_true = 0, const FmCovRescue* rescue = nullptr,
-                             int64_t t_rows = 0);
+                             int64_t t_rows = 0, void* xplanes = nullptr);
 size_t fm_final_fallback_scratch_bytes(int ctas);
 template <typename TS>
 cudaError_t fm_launch_lanczos_batch(const void* S, const double* q0, double* basis_ws, double* w_ws, double* z_ws,
@@ -517,6 +520,9 @@ struct fm_plan_s {
     // X itself is xrows x xlen per frame (M x N). Spatial plans: xrows = d.m, xlen = d.n.
     bool temporal = false;
     int64_t xrows = 0, xlen = 0;
+    // multi-tile spatial frames (M > 256): X as fp16 Re / Im planes, converted once per batch (cov_tc.cu kF16)
+    uint16_t* xplanes = nullptr;
+    int64_t xplane_len = 0;  // halves per plane row (X row length rounded up to 64)
     float* rscale = nullptr;            // frames: s_f of the fp16 hi/lo R planes (plane mode)
     // covariance rescue pass (cov_tc.cu): per-frame max |x|, out-of-range list, counts (one per sub-batch), prescale
     uint32_t* amax = nullptr;
@@ -723,6 +729,10 @@ extern "C" fm_status fm_plan_create(const fm_plan_desc* desc, int32_t device, fm
         pl->fb_scratch = fb;
     }
     if (pl->xlen & 1) chk(pl->get(&pl->x_pad, B * static_cast<size_t>(pl->xrows) * (static_cast<size_t>(pl->xlen) + 1) * 2));
+    if (FM_COV_F16 && !pl->temporal && desc->m > 256 && desc->m % 2 == 0) {
+        pl->xplane_len = ((pl->xlen + (pl->xlen & 1)) + 63) / 64 * 64;
+        chk(pl->get(&pl->xplanes, B * static_cast<size_t>(pl->xrows) * pl->xplane_len * 2));
+    }
     if (desc->method == FM_METHOD_FAST1_NORM2) chk(pl->get(&pl->omega_e, B * M * P));  // selection Omega = E_I
     if ((desc->method == FM_METHOD_FAST2 || desc->method == FM_METHOD_FAST1_NORM2) && M <= 256 && P <= 16) {
         chk(pl->get(&pl->gpart, B * 2 * P * P * 2));  // Gram halves from the product epilogue (plane path)
@@ -1163,6 +1173,9 @@ static fm_status run_batch_at(fm_plan pl, int64_t ws0, int64_t frames, const fm_
     pl->last_planes = planes;
     const int64_t nx = pl->x_pad ? pl->xlen + 1 : pl->xlen;  // X row length fed to the covariance kernel
     const int64_t trows = pl->temporal ? pl->xrows : 0;     // temporal mode: contraction over X's rows
+    auto xpl = [&](int64_t f0) -> void* {  // this frame range's region of the plane workspace (both planes)
+        return pl->xplanes ? static_cast<void*>(pl->xplanes + f0 * pl->xrows * pl->xplane_len * 2) : nullptr;
+    };
     const size_t MM2 = static_cast<size_t>(pl->d.m) * pl->d.m * 2;
     auto xin = [&](const float* x, int64_t f0, int64_t nf, cudaStream_t q) -> const float* {
         if (!pl->x_pad) return x;
@@ -1178,7 +1191,7 @@ static fm_status run_batch_at(fm_plan pl, int64_t ws0, int64_t frames, const fm_
         const WorkView w = work_view(pl, ws0);
         mark(pl, 0, s);
         FM_LAUNCH(fm_launch_cov_tc(xin(io->x, ws0, frames, s), R, io->status, frames, pl->d.m, nx, s, pv.hi, pv.lo,
-                                   pv.scale, pl->d.n, &w.resc, trows));
+                                   pv.scale, pl->d.n, &w.resc, trows, xpl(ws0)));
         mark(pl, 1, s);
         return run_post_cov(pl, frames, io, R, s, w, true, pv);
     }
@@ -1208,7 +1221,7 @@ static fm_status run_batch_at(fm_plan pl, int64_t ws0, int64_t frames, const fm_
         {
             cudaStream_t s = q;  // FM_LAUNCH synchronises `s` in debug mode
             FM_LAUNCH(fm_launch_cov_tc(xin(o.x, ws0 + f0, nf, q), R, o.status, nf, pl->d.m, nx, q, pv.hi, pv.lo,
-                                       pv.scale, pl->d.n, &w.resc, trows));
+                                       pv.scale, pl->d.n, &w.resc, trows, xpl(ws0 + f0)));
         }
         if (i == 0) mark(pl, 1, q);
         fm_status st = run_post_cov(pl, nf, &o, R, q, w, i == 0, pv);

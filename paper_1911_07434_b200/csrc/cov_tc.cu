@@ -82,12 +82,94 @@ __host__ __device__ constexpr int ring_region_bytes(int ring, bool diag_only) {
 // PTX wrappers: tc_common.cuh
 using namespace fmk::tc;
 
+__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
+    __half2 h = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
 // UMMA shared-memory descriptor, K-major, SWIZZLE_NONE: core matrices of 8 rows x 16 B,
 // LBO = 128 B (next 8 K-elements), SBO = 256 B (next 8 rows), version bit 46 (sm_100).
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
     return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(128 >> 4) << 16) |
            (static_cast<uint64_t>(256 >> 4) << 32) | (1ull << 46);
 }
+// UMMA smem descriptor, K-major, SWIZZLE_128B (TMA-written fp16 plane tiles: rows of 64 halves = 128 B, 8-row
+// atoms 1024 B apart); a K step of 16 advances the start address by 32 B inside the atom.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (static_cast<uint64_t>(1024 >> 4) << 32) |
+           (1ull << 46) | (2ull << 61);
+}
+// Multi-tile frames (M > 256: every 256-row block of X feeds nb tiles, so the fused fp32 -> fp16 conversion would
+// run nb times per block and the converters, not the tensor cores, would set the pace): X is converted ONCE into
+// Re / Im fp16 planes (frames x M x n_pad halves, zero-padded to a multiple of 64 snapshots) with each frame's
+// max |x| (the rescue list's input) and non-finite flag, and the covariance kernel (kF16) TMA-loads the planes
+// straight into 128B-swizzled UMMA operand tiles.
+#ifndef FM_F16_KC
+#define FM_F16_KC 32
+#endif
+constexpr int kF16Kc = FM_F16_KC;                  // snapshots per fp16 stage (one 64-B / 128-B swizzle row)
+constexpr int kF16Plane = kRows * kF16Kc * 2;      // 128 rows x kF16Kc halves
+constexpr int kF16Stage = 4 * kF16Plane;           // A re, A im, B re, B im
+constexpr int kF16Stages = kF16Kc == 64 ? 2 : 4;   // 128 KB of ring either way
+// K-major swizzled descriptor of the plane tiles: rows of 2 kF16Kc bytes, 8-row atoms (SBO) 16 kF16Kc bytes apart
+__device__ __forceinline__ uint64_t umma_desc_plane(uint32_t saddr) {
+    constexpr uint64_t layout = kF16Kc == 64 ? 2ull : 4ull;  // SWIZZLE_128B / SWIZZLE_64B
+    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (1ull << 16) |
+           (static_cast<uint64_t>((16 * kF16Kc) >> 4) << 32) | (1ull << 46) | (layout << 61);
+}
+constexpr int kXpRows = 4;  // rows per warp (one max |x| atomic per warp and frame run of rows)
+__global__ void __launch_bounds__(256) k_x_planes(const float4* __restrict__ x, uint2* __restrict__ pre,
+                                                  uint2* __restrict__ pim, uint32_t* __restrict__ amax,
+                                                  int32_t* __restrict__ status, int64_t rows, int m, int n,
+                                                  int n_pad) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5)) * kXpRows;
+    float mx = 0.f;
+    bool bad = false;
+    int fcur = -1;
+    for (int64_t row = r0; row < r0 + kXpRows && row < rows; ++row) {
+        const int f = static_cast<int>(row / m);
+        if (f != fcur) {  // the warp's rows crossed into another frame: flush the previous frame's max
+            if (fcur >= 0) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                if (lane == 0 && amax) atomicMax(&amax[fcur], __float_as_uint(mx));
+                if (__any_sync(0xffffffffu, bad) && lane == 0 && status) atomicOr(&status[fcur], kFrameNonFinite);
+                mx = 0.f;
+                bad = false;
+            }
+            fcur = f;
+        }
+        const float4* xr = x + row * (n / 2);
+        uint2* rr = pre + row * (n_pad / 4);
+        uint2* ri = pim + row * (n_pad / 4);
+        for (int q = lane; q < n_pad / 4; q += 32) {  // four snapshots per lane and step
+            float re[4] = {0.f, 0.f, 0.f, 0.f}, im[4] = {0.f, 0.f, 0.f, 0.f};
+            if (4 * q < n) {
+                const float4 a = __ldcs(xr + 2 * q);
+                re[0] = a.x; im[0] = a.y; re[1] = a.z; im[1] = a.w;
+                if (4 * q + 2 < n) {
+                    const float4 c = __ldcs(xr + 2 * q + 1);
+                    re[2] = c.x; im[2] = c.y; re[3] = c.z; im[3] = c.w;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                mx = fmaxf(mx, fmaxf(fabsf(re[u]), fabsf(im[u])));
+                bad |= !(isfinite(re[u]) && isfinite(im[u]));
+            }
+            rr[q] = make_uint2(pack_half2(re[0], re[1]), pack_half2(re[2], re[3]));
+            ri[q] = make_uint2(pack_half2(im[0], im[1]), pack_half2(im[2], im[3]));
+        }
+    }
+    if (fcur >= 0) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0 && amax) atomicMax(&amax[fcur], __float_as_uint(mx));
+        if (__any_sync(0xffffffffu, bad) && lane == 0 && status) atomicOr(&status[fcur], kFrameNonFinite);
+    }
+}
+
 // Instruction descriptor: kind::f16, A=B=F16, D=F32, K-major both, M=256, N=256.
 __host__ __device__ constexpr uint32_t umma_idesc(bool neg_a) {
     return (1u << 4) | (0u << 7) | (0u << 10) | ((neg_a ? 1u : 0u) << 13) | ((256u >> 3) << 17) | ((256u >> 4) << 24);
@@ -99,10 +181,6 @@ __device__ __forceinline__ void umma_f16_2sm(uint32_t d_tmem, uint64_t a, uint64
         "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
-}
-__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
-    __half2 h = __floats2half2_rn(lo, hi);
-    return *reinterpret_cast<uint32_t*>(&h);
 }
 
 #ifdef FM_COV_TIMELINE  // experiment only: clock64 stamps of CTA 0's first 16 tiles (tools/experiments)
@@ -233,7 +311,7 @@ __device__ __forceinline__ void convert_tile_t(const uint8_t* stage, uint8_t* op
 // kSplit (with kConv8): the eight converter warps form two groups of four that take alternate pipeline stages
 // (each group converts whole stages, 32 rows per warp), so one stage's fixed costs -- the proxy fence, the group
 // barrier and the cross-CTA operand-ready arrive -- overlap the other group's conversion.
-template <int kEpi, bool kConv8, bool kSplit = false>
+template <int kEpi, bool kConv8, bool kSplit = false, bool kF16 = false>
 #ifdef FM_COV_MAXNREG  // experiment: register cap so fp64 kernels of another sub-batch can co-reside
 #define FM_COV_BOUNDS(t) __maxnreg__(FM_COV_MAXNREG)
 #else
@@ -245,7 +323,8 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
                   int m, int n, int tiles_per_frame, int total_tiles, float* __restrict__ rscale,
                   float inv_n_true, int dbg, int ring, const int32_t* __restrict__ flist,
                   const int32_t* __restrict__ fcount, const float* __restrict__ xscale,
-                  uint32_t* __restrict__ amax_out, int temporal) {
+                  uint32_t* __restrict__ amax_out, int temporal, const __grid_constant__ CUtensorMap pre_map,
+                  const __grid_constant__ CUtensorMap pim_map) {
     constexpr bool kTmaStore = kEpi >= 1;
     // rescue pass: only the listed frames (the count is device-resident; every CTA of the grid reads the same
     // value, so an empty list ends all of them before any barrier or TMEM allocation)
@@ -268,7 +347,7 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
     const int gS = ring & 0xff, gO = (ring >> 8) & 0xff, dS = (ring >> 16) & 0xff, dO = (ring >> 24) & 0xff;
     uint8_t* operand = smem + (tiles_per_frame == 1 ? dS * kStageBytes : gS * 2 * kStageBytes);
     // epilogue region right after the rings (1024-aligned for the 128B-swizzled TMA store boxes)
-    uint8_t* epi_bytes = smem + ring_region_bytes(ring, tiles_per_frame == 1);
+    uint8_t* epi_bytes = smem + (kF16 ? kF16Stages * kF16Stage : ring_region_bytes(ring, tiles_per_frame == 1));
     uint64_t* bars = reinterpret_cast<uint64_t*>(epi_bytes + kSmemEpilogue);
     uint64_t* stage_full = bars;
     uint64_t* stage_empty = bars + kMaxStages;
@@ -288,7 +367,7 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
     const uint32_t rank = __shfl_sync(0xffffffffu, cluster_rank(), 0);  // warp-uniform for the compiler
     const int pair = blockIdx.x >> 1;
     const int npairs = gridDim.x >> 1;
-    const int nk = (n + kChunk - 1) / kChunk;
+    const int nk = kF16 ? (n + kF16Kc - 1) / kF16Kc : (n + kChunk - 1) / kChunk;  // K stages per tile
     // ring geometry: diagonal-only launches (one tile per frame) use half-size stages, twice as many
     const bool diag_only = tiles_per_frame == 1;
     const int nS = diag_only ? dS : gS, nO = diag_only ? dO : gO;
@@ -343,6 +422,21 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
                 const int ta = 2 * (256 * bi + 128 * static_cast<int>(rank));
                 const int tb = 2 * (256 * bj + 128 * static_cast<int>(rank));
                 for (int kc = 0; kc < nk; ++kc, ++g) {
+                    if constexpr (kF16) {  // fp16 planes straight into the operand slots (freed by the MMA)
+                        const int s = g % kF16Stages;
+                        mbar_wait(smem_u32(&op_empty[s]), ((g / kF16Stages) & 1) ^ 1);
+                        const uint32_t full = smem_u32(&stage_full[s]);
+                        mbar_arrive_expect_tx(full, (diag ? 2 : 4) * kF16Plane);
+                        uint8_t* st = smem + s * kF16Stage;
+                        const int x = kF16Kc * kc;
+                        tma_load_2d(smem_u32(st), &pre_map, full, x, ya);
+                        tma_load_2d(smem_u32(st + kF16Plane), &pim_map, full, x, ya);
+                        if (!diag) {
+                            tma_load_2d(smem_u32(st + 2 * kF16Plane), &pre_map, full, x, yb);
+                            tma_load_2d(smem_u32(st + 3 * kF16Plane), &pim_map, full, x, yb);
+                        }
+                        continue;
+                    }
                     const int s = g % nS;
                     mbar_wait(smem_u32(&stage_empty[s]), ((g / nS) & 1) ^ 1);
                     const uint32_t full = smem_u32(&stage_full[s]);
@@ -373,6 +467,29 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
                 tc_fence_after();
                 COV_STAMP(t, 0);
                 for (int kc = 0; kc < nk; ++kc, ++g) {
+                    if constexpr (kF16) {  // four K steps of 16 inside each 128B-swizzled 64-snapshot stage
+                        const int o = g % kF16Stages;
+                        mbar_wait_cluster(smem_u32(&op_full[o]), (g / kF16Stages) & 1);
+                        tc_fence_after();
+                        const uint32_t a = smem_u32(smem + o * kF16Stage);
+                        const uint32_t b = diag ? a : a + 2 * kF16Plane;
+                        if (elect_one()) {
+#pragma unroll
+                            for (int ks = 0; ks < kF16Kc / kChunk; ++ks) {
+                                const uint32_t off = 32u * ks;
+                                const uint64_t ar = umma_desc_plane(a + off), ai = umma_desc_plane(a + kF16Plane + off);
+                                const uint64_t br = umma_desc_plane(b + off), bim = umma_desc_plane(b + kF16Plane + off);
+                                const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
+                                umma_f16_2sm(tmem + 0, ar, br, id_pos, acc);
+                                umma_f16_2sm(tmem + 0, ai, bim, id_pos, 1u);
+                                umma_f16_2sm(tmem + 256, ai, br, id_pos, acc);
+                                umma_f16_2sm(tmem + 256, ar, bim, id_neg, 1u);
+                            }
+                            umma_commit_mc(smem_u32(&op_empty[o]));
+                        }
+                        __syncwarp();
+                        continue;
+                    }
                     const int o = g % nO;
                     const long long c0 = COV_CLK();
                     mbar_wait_cluster(smem_u32(&op_full[o]), (g / nO) & 1);
@@ -408,6 +525,18 @@ __global__ void __cluster_dims__(2, 1, 1) FM_COV_BOUNDS((kEpi == 2 ? kThreadsP :
         const int cw = kSplit ? (cwid & 3) : cwid;
         const bool lead = kSplit ? (cwid & 3) == 0 : warp == 2;          // arrives for the group's stages
         int g = 0, tt = 0;
+        if constexpr (kF16) {  // no conversion: warp 2 tells the leader CTA each stage's planes have landed
+            if (warp == 2 && lane == 0) {
+                for (int tile = pair; tile < total_tiles; tile += npairs) {
+                    for (int kc = 0; kc < nk; ++kc, ++g) {
+                        const int s = g % kF16Stages;
+                        mbar_wait(smem_u32(&stage_full[s]), (g / kF16Stages) & 1);
+                        if (rank == 0) mbar_arrive_local(smem_u32(&op_full[s]));
+                        else mbar_arrive_cluster(smem_u32(&op_full[s]), 0);
+                    }
+                }
+            }
+        } else
         for (int tile = pair; tile < total_tiles; tile += npairs, ++tt) {
             const int frame = frame_of(tile);
             int bi, bj;
@@ -749,7 +878,7 @@ extern "C" int fm_debug_cov_timeline(long long* host, int zero) {
 // rescue list / count and the prescale; with it the call enqueues pass 1, k_rescue_list and the rescue pass.
 cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, int64_t frames, int64_t m, int64_t n,
                              cudaStream_t stream, void* planes_hi, void* planes_lo, float* scale, int64_t n_true,
-                             const FmCovRescue* rescue, int64_t t_rows) {
+                             const FmCovRescue* rescue, int64_t t_rows, void* xplanes) {
     if (n_true <= 0) n_true = n;  // n: row length of d_x (even); n_true: snapshots for the 1/N scaling
     using namespace fmk::cov;
     const bool temporal = t_rows > 0;  // d_x: frames x t_rows x n; output m x m (m <= n), contraction over t_rows
@@ -824,7 +953,7 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
     if (!attr_set) {
         cudaError_t e = cudaSuccess;
         for (cudaError_t x : {set_attr(cov_tc_kernel<0, true, true>), set_attr(cov_tc_kernel<1, true, true>),
-                              set_attr(cov_tc_kernel<2, true, true>)})
+                              set_attr(cov_tc_kernel<2, true, true>), set_attr(cov_tc_kernel<1, true, true, true>)})
             if (e == cudaSuccess) e = x;
         if (e != cudaSuccess) return e;
         attr_set = true;
@@ -841,23 +970,51 @@ cudaError_t fm_launch_cov_tc(const float* d_x, float* d_r, int32_t* d_status, in
     }
     const int64_t pairs = std::min<int64_t>(tiles, std::max(1, sm_count / 2));
     const dim3 grid(static_cast<unsigned>(2 * pairs));
-    auto go = [&](auto kern, bool conv8, bool pass2) {
+    // multi-tile spatial frames with a plane workspace: X converted once (k_x_planes), kF16 pass 1
+    const bool f16 = xplanes != nullptr && tiles_per_frame > 1 && !temporal && epi == 1;
+    const int64_t n_pad = (n + kF16Kc - 1) / kF16Kc * kF16Kc;
+    CUtensorMap pre_map = map, pim_map = map;
+    if (f16) {
+        __half* pre = static_cast<__half*>(xplanes);
+        __half* pim = pre + static_cast<size_t>(frames) * m * n_pad;
+        cuuint64_t fdims[2] = {static_cast<cuuint64_t>(n_pad), static_cast<cuuint64_t>(frames * m)};
+        cuuint64_t fstr[1] = {static_cast<cuuint64_t>(2 * n_pad)};
+        cuuint32_t fbox[2] = {static_cast<cuuint32_t>(kF16Kc), static_cast<cuuint32_t>(kRows)};
+        const CUtensorMapSwizzle sw = kF16Kc == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+        cr = enc(&pre_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, pre, fdims, fstr, fbox, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+        cr = enc(&pim_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, pim, fdims, fstr, fbox, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+        const int64_t xrows = frames * m;
+        k_x_planes<<<static_cast<unsigned>((xrows + 8 * kXpRows - 1) / (8 * kXpRows)), 256, 0, stream>>>(
+            reinterpret_cast<const float4*>(d_x), reinterpret_cast<uint2*>(pre), reinterpret_cast<uint2*>(pim),
+            rescue ? rescue->amax : nullptr, d_status, xrows, static_cast<int>(m), static_cast<int>(n),
+            static_cast<int>(n_pad));
+    }
+    auto go = [&](auto kern, bool conv8, bool pass2, bool kf16) {
         const int threads = (epi == 2 ? kThreadsP : kThreads) + (conv8 ? 128 : 0);
-        const int smem = 1024 + ring_region_bytes(ring, tiles_per_frame == 1) + kSmemEpilogue + kSmemBarriers;
+        const int smem = 1024 + (kf16 ? kF16Stages * kF16Stage : ring_region_bytes(ring, tiles_per_frame == 1)) +
+                         kSmemEpilogue + kSmemBarriers;
         const bool r = rescue != nullptr;
         kern<<<grid, threads, smem, stream>>>(map, rmap, mmap, d_r, d_status, static_cast<int>(m),
                                               static_cast<int>(nk_len), tiles_per_frame, static_cast<int>(tiles),
                                               scale, static_cast<float>(1.0 / static_cast<double>(n_true)), 0, ring,
                                               pass2 ? rescue->list : nullptr, pass2 ? rescue->count : nullptr,
-                                              pass2 ? rescue->xscale : nullptr, (r && !pass2) ? rescue->amax : nullptr,
-                                              temporal ? 1 : 0);
+                                              pass2 ? rescue->xscale : nullptr,
+                                              (r && !pass2 && !kf16) ? rescue->amax : nullptr, temporal ? 1 : 0,
+                                              pre_map, pim_map);
     };
     auto launch = [&](bool pass2) {
         // eight converter warps in two groups taking alternate stages (tools/ab_build.sh, tools/ab_cov_general.sh:
         // c2 covariance 0.347 -> 0.324 ms, c4 3.25 -> 3.04 ms, the ToA path's T 0.746 -> 0.714 ms)
-        if (epi == 2) go(cov_tc_kernel<2, true, true>, true, pass2);
-        else if (epi == 1) go(cov_tc_kernel<1, true, true>, true, pass2);
-        else go(cov_tc_kernel<0, true, true>, true, pass2);
+        if (f16 && !pass2) go(cov_tc_kernel<1, true, true, true>, true, false, true);
+        else if (epi == 2) go(cov_tc_kernel<2, true, true>, true, pass2, false);
+        else if (epi == 1) go(cov_tc_kernel<1, true, true>, true, pass2, false);
+        else go(cov_tc_kernel<0, true, true>, true, pass2, false);
     };
     launch(false);
     if (rescue) {
