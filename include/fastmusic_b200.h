@@ -236,7 +236,7 @@ fm_status fm_z_fast_music_2(int64_t m, const double* s, int64_t k, int64_t p, in
                             double* basis, double* eigenvalues, double* cost_seconds, int64_t* deficient_column);
 /* block_lanczos_subspace, R/src/estimators.cpp:154-222 (block Krylov, full reorthogonalisation, top-K Ritz
  * values stable to 1e-10 relative on two consecutive checks); fp64 on the GPU: the device Krylov loop of
- * lanczos_batch.cu for block <= 16 and bases up to 72 columns, else the host-driven loop (M <= 384, block <= 64).
+ * lanczos_batch.cu for block <= 16 and bases up to 72 columns, else the host-driven loop (any M and block).
  * FM_ENOCONV at the iteration cap with the last relative change in *last_change (may be NULL). */
 fm_status fm_z_block_lanczos_subspace(int64_t m, const double* s, int64_t k, int64_t block, int32_t max_iterations,
                                       double* basis, double* eigenvalues, double* cost_seconds, double* last_change);

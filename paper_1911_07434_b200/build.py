@@ -19,7 +19,7 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build", "fastmusic_b200")
 LIB = os.path.join(PKG, "libfastmusic_b200.so")
 CU_SOURCES = ["cov_tc.cu", "rmul_tc.cu", "subspace.cu", "smallmat.cu", "final_fallback.cu", "spectrum.cu", "spectrum_tc.cu", "exact.cu", "jacobi.cu",
-              "lanczos.cu", "lanczos_batch.cu", "capi.cu"]
+              "lanczos.cu", "lanczos_batch.cu", "general.cu", "capi.cu"]
 CXX_SOURCES = ["facade.cpp", "io.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -1653,7 +1653,6 @@ extern "C" fm_status fm_z_fast_music_2(int64_t m, const double* s, int64_t k, in
     if (k < 1 || k >= m) return fail(FM_EINVAL, "fast_music_2: need 1 <= K < M");
     if (p < k || p > m) return fail(FM_EINVAL, "fast_music_2: need K <= p <= M");
     if (t < 1 || t > 20) return fail(FM_EINVAL, "fast_music_2: need 1 <= t <= 20");
-    if (p > 64) return fail(FM_ENOTSUP, "fast_music_2: p <= 64 supported");
     if (!basis || !eigenvalues) return fail(FM_EINVAL, "fast_music_2: null output");
     return z_nystrom_common(m, s, k, p, t, seed, true, basis, eigenvalues, cost_seconds, deficient_column);
 }
@@ -1664,7 +1663,6 @@ extern "C" fm_status fm_z_fast_music_1(int64_t m, const double* s, int64_t k, in
     if (st != FM_OK) return st;
     if (k < 1 || k >= m) return fail(FM_EINVAL, "fast_music_1: need 1 <= K < M");
     if (p < k || p > m) return fail(FM_EINVAL, "fast_music_1: need K <= p <= M");
-    if (p > 64) return fail(FM_ENOTSUP, "fast_music_1: p <= 64 supported");
     if (!basis || !eigenvalues) return fail(FM_EINVAL, "fast_music_1: null output");
     return z_nystrom_common(m, s, k, p, 1, seed, false, basis, eigenvalues, cost_seconds, nullptr);
 }
@@ -1675,7 +1673,6 @@ extern "C" fm_status fm_z_exact_signal_subspace(int64_t m, const double* s, int6
     if (st != FM_OK) return st;
     if (k < 1 || k >= m) return fail(FM_EINVAL, "exact_signal_subspace: need 1 <= K < M");
     if (!basis || !eigenvalues) return fail(FM_EINVAL, "exact_signal_subspace: null output");
-    if (m > 384) return fail(FM_ENOTSUP, "exact_signal_subspace: M <= 384 supported (fp64 Jacobi block staging)");
     const int64_t mp = (m + 15) / 16 * 16;
     ZCtx c;
     const auto rrow = to_rowmajor_hermitian(s, m);

@@ -233,6 +233,9 @@ __global__ void __launch_bounds__(kNT) k_jacobi_eig(const void* __restrict__ Rv,
 
 using namespace fmk;
 
+cudaError_t fm_gen_hermitian_eig(const void* R, void* work, void* basis, double* eig, int32_t* status, int m, int k,
+                                 cudaStream_t s);
+
 template <typename T>
 static cudaError_t launch_jac(const void* R, const void* a0, void* wk, void* basis, double* eig, int32_t* status,
                               int frames, int m, int k, int mode, cudaStream_t s) {
@@ -253,7 +256,21 @@ template <typename T>
 cudaError_t fm_launch_jacobi_eig(const void* R, void* work, void* basis, double* eig, int32_t* status, int frames,
                                  int m, int k, cudaStream_t s, int only_flagged, void* work32) {
     const int of = only_flagged ? jac::kModeOnlyFlagged : 0;
-    if (sizeof(T) == 8) return launch_jac<double>(R, nullptr, work, basis, eig, status, frames, m, k, of, s);
+    if (sizeof(T) == 8) {
+        const int mp = (m + jac::kB - 1) / jac::kB * jac::kB;
+        if (mp > 384 || k > 64) {  // beyond the shared-memory block staging: global-memory Jacobi (general.cu)
+            if (only_flagged) return cudaErrorInvalidValue;
+            for (int f = 0; f < frames; ++f) {
+                cudaError_t e = fm_gen_hermitian_eig(static_cast<const c64*>(R) + static_cast<size_t>(f) * m * m,
+                                                     static_cast<c64*>(work) + static_cast<size_t>(f) * mp * mp,
+                                                     static_cast<c64*>(basis) + static_cast<size_t>(f) * m * k,
+                                                     eig + static_cast<size_t>(f) * k, status + f, m, k, s);
+                if (e != cudaSuccess) return e;
+            }
+            return cudaSuccess;
+        }
+        return launch_jac<double>(R, nullptr, work, basis, eig, status, frames, m, k, of, s);
+    }
     if (!work32) return cudaErrorInvalidValue;
     cudaError_t e = launch_jac<float>(R, nullptr, work32, basis, eig, status, frames, m, k, of | jac::kModeNoStatus, s);
     if (e != cudaSuccess) return e;

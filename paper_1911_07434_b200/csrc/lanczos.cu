@@ -132,11 +132,9 @@ extern "C" fm_status fm_z_block_lanczos_subspace(int64_t m, const double* s, int
     if (block < k) return fm_set_error(FM_EINVAL, "block_lanczos_subspace: need block >= K");
     if (max_iterations < 1) return fm_set_error(FM_EINVAL, "block_lanczos_subspace: iters >= 1");
     if (!basis || !eigenvalues) return fm_set_error(FM_EINVAL, "block_lanczos_subspace: null output");
-    if (m > 384 || k > 64)
-        return fm_set_error(FM_ENOTSUP, "block_lanczos_subspace: M <= 384, K <= 64 supported (fp64 Jacobi staging)");
     const int M = static_cast<int>(m), K = static_cast<int>(k);
     const int b0 = static_cast<int>(std::min<int64_t>(block, m));
-    if (b0 > 64) return fm_set_error(FM_ENOTSUP, "block_lanczos_subspace: block <= 64 supported (QR staging)");
+    const int64_t bc = std::max<int64_t>(64, b0);  // block-column capacity of the work buffers
     constexpr double kTol = 1e-10;
     constexpr uint64_t kStartSeed = 0x6C616E637A6FULL;  // R/src/estimators.cpp:162
 
@@ -160,12 +158,12 @@ extern "C" fm_status fm_z_block_lanczos_subspace(int64_t m, const double* s, int
     const int64_t mpad = (m + 15) / 16 * 16;
     LZ_CUDA(dS.alloc(2 * mm));
     LZ_CUDA(dBasis.alloc(2 * mm));
-    LZ_CUDA(dQ.alloc(2 * m * 64));
-    LZ_CUDA(dW.alloc(2 * m * 64));
-    LZ_CUDA(dZ.alloc(2 * m * 64));
-    LZ_CUDA(dStrip.alloc(2 * m * 64));
-    LZ_CUDA(dStrip2.alloc(2 * m * 64));
-    LZ_CUDA(dQrWork.alloc(4 * m * 64));
+    LZ_CUDA(dQ.alloc(2 * m * bc));
+    LZ_CUDA(dW.alloc(2 * m * bc));
+    LZ_CUDA(dZ.alloc(2 * m * bc));
+    LZ_CUDA(dStrip.alloc(2 * m * bc));
+    LZ_CUDA(dStrip2.alloc(2 * m * bc));
+    LZ_CUDA(dQrWork.alloc(4 * m * bc));
     LZ_CUDA(dH.alloc(2 * mm));
     LZ_CUDA(dJW.alloc(2 * mpad * mpad));
     LZ_CUDA(dVec.alloc(2 * m * K));

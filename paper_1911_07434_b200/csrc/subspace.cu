@@ -139,10 +139,11 @@ __global__ void __launch_bounds__(kNT) k_qr(const cplx<T>* __restrict__ Cin, c64
                                              int32_t* __restrict__ status, int32_t* __restrict__ defcol,
                                              const int32_t* __restrict__ fmap, int m, int p,
                                              int32_t* __restrict__ rank_out = nullptr) {
-    __shared__ double nrm2[64];
-    __shared__ c64 rdiag[64];
-    __shared__ double tau[64];
-    __shared__ int perm[64];
+    extern __shared__ uint8_t qsm[];  // p entries each (any p: 36 p bytes of dynamic shared memory)
+    c64* rdiag = reinterpret_cast<c64*>(qsm);
+    double* nrm2 = reinterpret_cast<double*>(rdiag + p);
+    double* tau = nrm2 + p;
+    int* perm = reinterpret_cast<int*>(tau + p);
     __shared__ int s_pivot;
     __shared__ double s_maxcol;
     const int f = frame_of_x(fmap);
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(kNT) k_qr(const cplx<T>* __restrict__ Cin, c64
         s = warp_sum(s);
         if (lane == 0) nrm2[j] = s;
     }
-    if (threadIdx.x < p) perm[threadIdx.x] = threadIdx.x;
+    for (int j = threadIdx.x; j < p; j += kNT) perm[j] = j;
     __syncthreads();
     if (threadIdx.x == 0) {
         double mx = 0.0;
@@ -476,7 +477,7 @@ __global__ void __launch_bounds__(kNT) k_cholqr(const c32* __restrict__ Cin, c64
     __shared__ double d[64];
     const int f = frame_of_x(fmap);
     const c32* Cf = Cin + static_cast<size_t>(f) * m * p;
-    if (threadIdx.x < p) perm[threadIdx.x] = threadIdx.x;
+    for (int j = threadIdx.x; j < p; j += kNT) perm[j] = j;
     block_gram<true>(Cf, Cf, m, p, chunk, G);
     warp_cholesky_inv(G, p, true, perm, d);
     __syncthreads();
@@ -920,6 +921,9 @@ __global__ void __launch_bounds__(kNT) k_nystrom(const cplx<T>* __restrict__ V, 
 // ------------------------------------------------------------------ launchers (host)
 using namespace fmk;
 
+cudaError_t fm_gen_nystrom(const void* V, const void* C, const void* H, const void* work, const void* Rt, void* basis,
+                           double* eig, int32_t* status, int m, int p, int k, bool fast2, cudaStream_t s);
+
 template <typename T>
 cudaError_t fm_launch_rmul(const void* R, const void* omega, const void* V, void* C, const int32_t* fmap, int frames,
                            int m, int p, bool real_rhs, cudaStream_t s) {
@@ -952,16 +956,29 @@ cudaError_t fm_launch_gather(const void* R, const int32_t* idx, void* C, void* H
     return cudaGetLastError();
 }
 
+// pivoted Householder QR: dynamic shared memory of the per-column arrays (rdiag, nrm2, tau, perm)
+static size_t qr_smem(int p) { return static_cast<size_t>(p) * (sizeof(c64) + 2 * sizeof(double) + sizeof(int)); }
+template <typename K>
+static cudaError_t qr_attr(K kern, size_t smem) {
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    if (smem <= 48 * 1024) return cudaSuccess;
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+}
+
 template <typename T>
 cudaError_t fm_launch_qr(const void* C, void* work, void* Vout, void* Rt, int32_t* status, int32_t* defcol,
                          const int32_t* fmap, int frames, int m, int p, bool final_mode, cudaStream_t s) {
-    if (p > 64 || p < 1 || m < p) return cudaErrorInvalidValue;
+    if (p < 1 || m < p) return cudaErrorInvalidValue;
+    const size_t smem = qr_smem(p);
+    auto kern = final_mode ? sub::k_qr<T, 1> : sub::k_qr<T, 0>;
+    cudaError_t e = qr_attr(kern, smem);
+    if (e != cudaSuccess) return e;
     if (final_mode)
-        sub::k_qr<T, 1><<<frames, sub::kNT, 0, s>>>(static_cast<const cplx<T>*>(C), static_cast<c64*>(work), nullptr,
-                                                    static_cast<c64*>(Rt), status, defcol, fmap, m, p);
+        kern<<<frames, sub::kNT, smem, s>>>(static_cast<const cplx<T>*>(C), static_cast<c64*>(work), nullptr,
+                                            static_cast<c64*>(Rt), status, defcol, fmap, m, p, nullptr);
     else
-        sub::k_qr<T, 0><<<frames, sub::kNT, 0, s>>>(static_cast<const cplx<T>*>(C), static_cast<c64*>(work),
-                                                    static_cast<cplx<T>*>(Vout), nullptr, status, defcol, fmap, m, p);
+        kern<<<frames, sub::kNT, smem, s>>>(static_cast<const cplx<T>*>(C), static_cast<c64*>(work),
+                                            static_cast<cplx<T>*>(Vout), nullptr, status, defcol, fmap, m, p, nullptr);
     return cudaGetLastError();
 }
 
@@ -970,8 +987,11 @@ cudaError_t fm_launch_qr(const void* C, void* work, void* Vout, void* Rt, int32_
 template <typename T>
 cudaError_t fm_launch_qr_rank(const void* C, void* work, void* Vout, int32_t* status, int32_t* rank_out, int m, int p,
                               cudaStream_t s) {
-    if (p > 64 || p < 1 || m < p) return cudaErrorInvalidValue;
-    sub::k_qr<T, 0><<<1, sub::kNT, 0, s>>>(static_cast<const cplx<T>*>(C), static_cast<c64*>(work),
+    if (p < 1 || m < p) return cudaErrorInvalidValue;
+    const size_t smem = qr_smem(p);
+    cudaError_t e = qr_attr(sub::k_qr<T, 0>, smem);
+    if (e != cudaSuccess) return e;
+    sub::k_qr<T, 0><<<1, sub::kNT, smem, s>>>(static_cast<const cplx<T>*>(C), static_cast<c64*>(work),
                                            static_cast<cplx<T>*>(Vout), nullptr, status, nullptr, nullptr, m, p,
                                            rank_out);
     return cudaGetLastError();
@@ -999,6 +1019,21 @@ cudaError_t fm_launch_nystrom(const void* V, const void* C, const void* H, const
                               void* basis, double* eig, int32_t* status, const int32_t* fmap, int frames, int m,
                               int p, int k, bool fast2, cudaStream_t s) {
     const size_t smem = 3 * sizeof(c64) * p * p + sizeof(double) * p + sizeof(int) * p;
+    if (smem > 200 * 1024) {  // p > 64: the same algebra on global memory (general.cu), fp64 facade only
+        if (sizeof(T) != 8 || fmap) return cudaErrorInvalidValue;
+        for (int f = 0; f < frames; ++f) {
+            const size_t mp_ = static_cast<size_t>(m) * p, pp = static_cast<size_t>(p) * p;
+            cudaError_t e = fm_gen_nystrom(V ? static_cast<const c64*>(V) + f * mp_ : nullptr,
+                                           C ? static_cast<const c64*>(C) + f * mp_ : nullptr,
+                                           H ? static_cast<const c64*>(H) + f * pp : nullptr,
+                                           static_cast<const c64*>(work) + f * 2 * mp_,
+                                           static_cast<const c64*>(Rt) + f * pp,
+                                           static_cast<c64*>(basis) + static_cast<size_t>(f) * m * k, eig + f * k,
+                                           status + f, m, p, k, fast2, s);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
     auto kern = fast2 ? sub::k_nystrom<T, true> : sub::k_nystrom<T, false>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
