@@ -568,7 +568,7 @@ def run_ours(args):
         "stages_alone_ms": alone_ms,
         "stages_alone_note": f"all {n} frames in one launch per kernel (concurrency 1), {args.roof_steps} runs",
         "batches_in_flight": depth,
-        "gpu_launches": args.steps * plan0.launches_per_batch(),
+        "gpu_launches": args.steps * (plan0.launches_per_batch() + 1),  # + the peak-record pack
         "clocks": clk.summary(),
         "e2e": e2e,
         "frames_ok": int((status == 0).sum()), "frames_full_peaks": int((counts == K).sum()),

@@ -164,6 +164,10 @@ fm_status fm_plan_set_concurrency(fm_plan plan, int32_t subbatches);
  * into a graph and every later identical call replays it with one launch (small batches are otherwise bound by
  * the host's launch rate). Not used while profiling. Captured graphs are dropped by fm_plan_set_concurrency. */
 fm_status fm_plan_set_graphs(fm_plan plan, int32_t on);
+/* Per-frame peak records for the cross-GPU gather: rec[f] = {cells[f][0..k), count[f], status[f]}
+ * (int32, row stride k + 2), one kernel on `stream`; device pointers. */
+fm_status fm_pack_peak_records(const int32_t* cells, const int32_t* count, const int32_t* status, int64_t frames,
+                               int64_t k, int32_t* rec, void* stream);
 /* Number of kernel launches one fm_run_batch enqueues (per sub-batch). */
 int32_t fm_plan_launches_per_batch(fm_plan plan);
 

@@ -19,7 +19,7 @@ METHOD = {"exact": 0, "fast1": 1, "fast2": 2, "lanczos": 3, "fast1_norm2": 16}
 
 # Every symbol declared in include/fastmusic_b200.h (checked by tests/test_capi_symbols.py).
 EXPORTED = [
-    "fm_abi_version", "fm_status_string", "fm_last_error", "fm_device_info",
+    "fm_abi_version", "fm_status_string", "fm_last_error", "fm_device_info", "fm_pack_peak_records",
     "fm_rng_derive", "fm_rng_normals", "fm_sample_without_replacement", "fm_gaussian_matrix_real",
     "fm_draw_omega_batch", "fm_draw_indices_batch", "fm_draw_uniforms_batch", "fm_generate_frames",
     "fm_plan_create", "fm_plan_destroy", "fm_plan_workspace_bytes", "fm_run_batch", "fm_rerun_frames",
@@ -92,6 +92,7 @@ def _load():
         "fm_plan_set_concurrency": (i32, [vp, i32]),
         "fm_plan_set_graphs": (i32, [vp, i32]),
         "fm_estimate_batch_host": (i32, [vp, i64, vp, vp, vp, vp]),
+        "fm_pack_peak_records": (i32, [vp, vp, vp, i64, i64, vp, vp]),
         "fm_z_spatial_covariance": (i32, [i64, i64, vp, vp]),
         "fm_z_exact_signal_subspace": (i32, [i64, vp, i64, vp, vp, vp]),
         "fm_z_fast_music_1": (i32, [i64, vp, i64, i64, u64, vp, vp, vp]),

@@ -127,6 +127,16 @@ __global__ void k_clear_bits(int32_t* status, int frames, int32_t bits) {
     if (f < frames) status[f] &= ~bits;
 }
 
+// rec[f] = {cells[f][0..k), count[f], status[f]} (the gather record of shard.py), thread per record entry
+__global__ void k_pack_records(const int32_t* __restrict__ cells, const int32_t* __restrict__ count,
+                               const int32_t* __restrict__ status, int64_t frames, int k, int32_t* __restrict__ rec) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= frames * (k + 2)) return;
+    const int64_t f = e / (k + 2);
+    const int c = static_cast<int>(e % (k + 2));
+    rec[e] = c < k ? cells[f * k + c] : (c == k ? count[f] : status[f]);
+}
+
 // Odd N: rows of X (N complex) -> rows of N + 1 complex with a zero last snapshot (the TMA row pitch of
 // the covariance kernel must be a multiple of 16 bytes; a zero snapshot adds nothing to X X^H).
 __global__ void k_pad_rows(const float2* __restrict__ x, float2* __restrict__ xp, int64_t rows, int n) {
@@ -872,8 +882,8 @@ extern "C" int32_t fm_plan_launches_per_batch(fm_plan plan) {
     if (!plan) return 0;
     const auto& d = plan->d;
     const int t = d.t;
-    // covariance + rescue list + rescue covariance + status clear + autocorr + spectrum + peaks (+ odd-N pad)
-    int n = 1 + 2 + 1 + 3 + (plan->x_pad ? 1 : 0);
+    // covariance + rescue list + rescue covariance + autocorr + spectrum + peaks (+ odd-N pad)
+    int n = 1 + 2 + 3 + (plan->x_pad ? 1 : 0);
     if (plan->zk) n += 1;  // int8 spectrum: + the digit split of t (k_slice_tk)
     const bool tiled = d.p <= 32 && (d.p % 4) == 0;
     const int gepi = gram_epilogue(plan) ? 1 : 0;
@@ -993,14 +1003,16 @@ static fm_batch_io io_view(fm_plan pl, const fm_batch_io* io, int64_t f0) {
 }
 
 static fm_status run_post_cov(fm_plan pl, int64_t frames, const fm_batch_io* io, const float* R, cudaStream_t s,
-                              const WorkView& w, bool prof, const Planes& pv) {
+                              const WorkView& w, bool prof, const Planes& pv, bool fresh = true) {
     const auto& d = pl->d;
     const int F = static_cast<int>(frames), M = static_cast<int>(d.m), P = static_cast<int>(d.p),
               K = static_cast<int>(d.k);
     double* basis = io->basis ? io->basis : w.basis;
     double* eig = io->eigenvalues ? io->eigenvalues : w.eig;
-    k_clear_bits<<<(F + 255) / 256, 256, 0, s>>>(io->status, F, FM_FRAME_RANK | FM_FRAME_NOCONV);
-    FM_CUDA_OK(cudaGetLastError());
+    if (!fresh) {  // a rerun keeps the batch's status words: drop the stage flags of the previous pass
+        k_clear_bits<<<(F + 255) / 256, 256, 0, s>>>(io->status, F, FM_FRAME_RANK | FM_FRAME_NOCONV);
+        FM_CUDA_OK(cudaGetLastError());
+    }
     const bool warp_path = P <= 32;              // block-per-frame small-matrix kernels (smallmat.cu)
     const bool tiled = P <= 32 && (P % 4) == 0;  // register-tiled Gram + split final stage
     // Gram epilogue (plane path, p <= 16): the products also form G = C^H C (and H = V^H C on the last one),
@@ -1291,10 +1303,22 @@ static fm_status rerun_list(fm_plan pl, const int32_t* list, int64_t count, cons
         const fm_batch_io o = io_view(pl, io, f0);
         const float* R = io->covariance ? o.covariance : pl->R + f0 * MM2;
         const Planes pv = pl->last_planes && !io->covariance ? planes_view(pl, f0) : Planes{};
-        fm_status st = run_post_cov(pl, nf, &o, R, s, work_view(pl, f0), false, pv);
+        fm_status st = run_post_cov(pl, nf, &o, R, s, work_view(pl, f0), false, pv, false);
         if (st != FM_OK) return st;
         i = j;
     }
+    return FM_OK;
+}
+
+extern "C" fm_status fm_pack_peak_records(const int32_t* cells, const int32_t* count, const int32_t* status,
+                                          int64_t frames, int64_t k, int32_t* rec, void* stream) {
+    if (frames < 0 || k < 1 || k > (1 << 20) || (frames > 0 && (!cells || !count || !status || !rec)))
+        return fail(FM_EINVAL, "fm_pack_peak_records: bad arguments");
+    if (frames == 0) return FM_OK;
+    const int64_t n = frames * (k + 2);
+    k_pack_records<<<static_cast<unsigned>((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        cells, count, status, frames, static_cast<int>(k), rec);
+    FM_CUDA_OK(cudaGetLastError());
     return FM_OK;
 }
 

@@ -151,6 +151,10 @@ __global__ void __launch_bounds__(kT) k_final_fallback(const c32* __restrict__ C
     c64* X = Vm + pp;  // V_c, later T
     c64* Y = X + pp;   // W
     const double eps = static_cast<double>(p) * eps_of<float>::value;
+    // one parallel pass over this CTA's status words first: a CTA without flagged frames exits after one load
+    int any = 0;
+    for (int f = blockIdx.x + tid * gridDim.x; f < frames; f += kT * gridDim.x) any |= status[f] & kFrameNoConv;
+    if (!__syncthreads_or(any)) return;
     for (int f = blockIdx.x; f < frames; f += gridDim.x) {
         if (!(status[f] & kFrameNoConv)) continue;  // block-uniform
         const c32* Cf = C + static_cast<size_t>(f) * m * p;

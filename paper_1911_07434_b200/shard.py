@@ -32,6 +32,13 @@ def pack_records(peak_cells, peak_count, status, out=None):
     import torch
     b, k = peak_cells.shape
     rec = out if out is not None else torch.empty((b, k + 2), dtype=torch.int32, device=peak_cells.device)
+    if rec.is_cuda and rec.is_contiguous() and all(t.is_contiguous() for t in (peak_cells, peak_count, status)):
+        from . import _capi  # one kernel (fm_pack_peak_records) on the current stream
+        st = _capi.LIB.fm_pack_peak_records(_capi.ptr(peak_cells), _capi.ptr(peak_count), _capi.ptr(status), b, k,
+                                            _capi.ptr(rec), torch.cuda.current_stream(rec.device).cuda_stream)
+        if st != 0:
+            raise RuntimeError(_capi.last_error())
+        return rec
     rec[:, :k].copy_(peak_cells)
     rec[:, k].copy_(peak_count)
     rec[:, k + 1].copy_(status)
