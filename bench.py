@@ -311,7 +311,7 @@ def run_reference(args):
     return 0
 
 
-def config_dict(name, cfgd, world, mode="strong", per_gpu=None, depth=1):
+def config_dict(name, cfgd, world, mode="strong", per_gpu=None, depth=1, coalesce=1):
     per_gpu = cfgd["frames"] if per_gpu is None else per_gpu
     gfr = cfgd["frames"] if mode == "strong" else cfgd["frames"] * world
     xb = per_gpu * cfgd["m"] * cfgd["n"] * 8
@@ -324,7 +324,10 @@ def config_dict(name, cfgd, world, mode="strong", per_gpu=None, depth=1):
             else "[-90, 90] deg", "l2": l2,
             "parallelism": (f"{mode} scaling: frames of each {gfr}-frame batch sharded over {world} GPU(s) "
                             f"[g B/G, (g+1) B/G), NCCL all-gather of peak records" if mode == "strong" else
-                            f"weak scaling: {per_gpu} frames per GPU, NCCL all-gather of peak records")}
+                            f"weak scaling: {per_gpu} frames per GPU, NCCL all-gather of peak records"),
+            "coalesce": coalesce,
+            "coalesce_note": "each launch runs this GPU's shards of `coalesce` consecutive global batches together"
+                             " (frames are independent; the timed region still covers exactly `steps` global batches)"}
 
 
 # ----------------------------------------------------------------------------- ours
@@ -374,14 +377,19 @@ def run_ours(args):
     # batches in flight: small shards leave too little work per kernel to hide ramps and tails
     # (measured at N = 1, c2, tools/bench_sweep.sh: 1024 frames 0.954 / 1.075 / 1.105 M frames/s at depth 1 / 2 / 3;
     # 128-frame shards 0.37 / 0.54 / 0.65 / 0.71 M at depth 1 .. 4)
-    depth = args.depth if args.depth > 0 else (3 if n >= 512 else 4 if n >= 256 else 6)
+    # Shard coalescing (SURVEY H6, strong scaling): a GPU's shard of one global batch shrinks to 1024 / G frames
+    # (128 at G = 8), too few to fill 148 SMs; one launch therefore carries its shards of `co` consecutive global
+    # batches (>= 512 frames). Frames are independent, so only the launch granularity changes.
+    co = args.coalesce if args.coalesce > 0 else (max(1, -(-512 // n)) if mode == "strong" else 1)
+    nl = co * n  # frames per launch
+    depth = args.depth if args.depth > 0 else (3 if nl >= 512 else 4 if nl >= 256 else 6)
 
     # CUDA-graph replay of whole batches: small shards are otherwise bound by the host's launch rate
     graphs = args.graphs == "on" or (args.graphs == "auto" and depth <= 2)
 
     def make_plan(i):
         grid = dict(theta0=cfgd["w0"], theta1=cfgd["w1"], temporal=True) if cfgd.get("temporal") else {}
-        p = fm.BatchPlan(M, N, K, cfgd["method"], p=P, t=cfgd["t"], grid_size=L, max_frames=n, device=local,
+        p = fm.BatchPlan(M, N, K, cfgd["method"], p=P, t=cfgd["t"], grid_size=L, max_frames=nl, device=local,
                          exact_jacobi=args.exact_jacobi, **grid)
         if args.subbatches > 0:
             p.set_concurrency(args.subbatches)
@@ -389,23 +397,28 @@ def run_ours(args):
         return p
 
     streams = [torch.cuda.Stream(device=dev) for _ in range(depth)]
-    fs = FrameStream(make_plan, n, nmax, K, world, depth, streams, dev, spectrum=True)
+    fs = FrameStream(make_plan, nl, co * nmax, K, world, depth, streams, dev, spectrum=True)
     plan0 = fs.plans[0]
     main_s = torch.cuda.current_stream(dev)
 
     # L2 hygiene: steps cycle through enough copies of X that every step reads its input from HBM (> 3x L2 in all)
-    nbuf = max(depth, -(-3 * 126 * 2**20 // (n * M * N * 8)))
-    xs = [xd] + [xd.clone() for _ in range(nbuf - 1)]
+    nbuf = max(depth, -(-3 * 126 * 2**20 // (nl * M * N * 8)))
+    xl = xd if co == 1 else xd.repeat(co, 1, 1, 1)
+    xs = [xl] + [xl.clone() for _ in range(nbuf - 1)]
+    om_l = omega if (omega is None or co == 1) else omega.repeat(co, *([1] * (omega.dim() - 1)))
+    ix_l = idx if (idx is None or co == 1) else idx.repeat(co, *([1] * (idx.dim() - 1)))
     ctr = [0]
 
-    def run_steps(count):
+    def run_steps(count):  # `count` global batches: count // co full launches, then one partial launch
         gathered = None
-        for _ in range(count):
-            _, gathered = fs.step(xs[ctr[0] % nbuf], omega, idx)
+        full, rem = divmod(count, co)
+        for i in range(full + (1 if rem else 0)):
+            fr = nl if i < full else rem * n
+            _, gathered = fs.step(xs[ctr[0] % nbuf], om_l, ix_l, frames=fr)
             ctr[0] += 1
         return gathered
 
-    run_steps(max(3, args.warmup) + depth)
+    run_steps((max(3, args.warmup) + depth) * co)
     torch.cuda.synchronize()
     out0 = fs.output(0)
     status = out0["status"].cpu().numpy()
@@ -440,7 +453,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     value = gfr * args.steps / (ms_max / 1e3)
-    recs = unshard_records(gathered, world, B, mode) if world > 1 else None
+    recs = unshard_records(gathered[:, :nmax], world, B, mode) if world > 1 else None  # first batch of the launch
 
     # ---------------- weak-scaling companion (N > 1, strong default): B frames per rank, same timing rules
     weak = None
@@ -498,7 +511,7 @@ def run_ours(args):
         e2e = {"value": gfr * e2e_steps / float(te.item()), "unit": "frames/s", "h2d_bytes_per_step": h2d * world,
                "d2h_bytes_per_step": d2h * world, "steps": e2e_steps,
                "path": "fm_estimate_batch_host (pinned host X, host draws of Omega, redraw check, D2H peaks)"}
-        same = np.array_equal(res["peak_cells"], out0["peak_cells"].cpu().numpy())
+        same = np.array_equal(res["peak_cells"], out0["peak_cells"][:n].cpu().numpy())
         e2e["peaks_match_device_run"] = bool(same)
 
     if rank != 0:
@@ -548,7 +561,7 @@ def run_ours(args):
         "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": mode, "vs_baseline": None, "dtype": "c64",
         "data": "synthetic (seeded BASELINE frame model, DESIGN.md §3)",
-        "config": config_dict(args.config, cfgd, world, mode, n, depth),
+        "config": config_dict(args.config, cfgd, world, mode, n, depth, co),
         "roofline": roof,
         "roofline_path": {"t_roof_ms_per_step": t_roof_ms, "t_meas_ms_per_step": ms_max / args.steps,
                           "frac": t_roof_ms / (ms_max / args.steps),
@@ -568,7 +581,7 @@ def run_ours(args):
         "stages_alone_ms": alone_ms,
         "stages_alone_note": f"all {n} frames in one launch per kernel (concurrency 1), {args.roof_steps} runs",
         "batches_in_flight": depth,
-        "gpu_launches": args.steps * (plan0.launches_per_batch() + 1),  # + the peak-record pack
+        "gpu_launches": -(-args.steps // co) * (plan0.launches_per_batch() + 1),  # launches x (+ the record pack)
         "clocks": clk.summary(),
         "e2e": e2e,
         "frames_ok": int((status == 0).sum()), "frames_full_peaks": int((counts == K).sum()),
@@ -673,6 +686,8 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: each global batch's frames split over the GPUs (SURVEY §8e); weak: a batch per GPU")
     ap.add_argument("--depth", type=int, default=0, help="batches in flight per GPU (0 = auto)")
+    ap.add_argument("--coalesce", type=int, default=0,
+                    help="global batches per launch on each GPU (0 = auto: shards of >= 512 frames per launch)")
     ap.add_argument("--exact-jacobi", action="store_true",
                     help="exact method (c5): the full Jacobi eigensolver on every frame (no certified iteration)")
     ap.add_argument("--graphs", default="auto", choices=["auto", "on", "off"],

@@ -67,6 +67,20 @@ def unshard_records(gathered, world: int, total: int, mode: str = "strong"):
     return torch.cat(rows, 0)
 
 
+def unshard_coalesced(gathered, world: int, total: int, co: int, mode: str = "strong"):
+    """Records of a coalesced launch (each rank ran its shards of `co` consecutive global batches back to back:
+    rank g's rows [i n_g, (i + 1) n_g) belong to batch i) -> list of `co` [global frames, K+2] arrays."""
+    import torch
+    out = []
+    for i in range(co):
+        rows = []
+        for g in range(world):
+            _, n = shard_range(g, world, total, mode)
+            rows.append(gathered[g, i * n:(i + 1) * n])
+        out.append(torch.cat(rows, 0))
+    return out
+
+
 class FrameStream:
     """One rank's part of a stream of global batches: `depth` plans / streams used round-robin, so up to `depth`
     batches are in flight; step() enqueues the batch (plan.run), packs its peak records and all-gathers them on
@@ -89,17 +103,22 @@ class FrameStream:
                      for _ in range(self.depth)] if world > 1 else [None] * self.depth
         self.i = 0
 
-    def step(self, x, omega=None, indices=None):
+    def step(self, x, omega=None, indices=None, frames=None):
+        """frames (<= the stream's frames): a shorter launch over the first `frames` frames (records beyond them
+        keep the previous contents)."""
         import contextlib
 
         import torch
+        nf = self.frames if frames is None else frames
+        if not 0 < nf <= self.frames:
+            raise ValueError("FrameStream.step: 0 < frames <= stream frames")
         d = self.i % self.depth
         self.i += 1
         plan, out, s = self.plans[d], self.outs[d], self.streams[d]
-        plan.run(self.frames, x, omega, indices, out, stream=s)
+        plan.run(nf, x, omega, indices, out, stream=s)
         ctx = torch.cuda.stream(s) if s is not None else contextlib.nullcontext()
         with ctx:
-            pack_records(out["peak_cells"], out["peak_count"], out["status"], out=self.recs[d][: self.frames])
+            pack_records(out["peak_cells"][:nf], out["peak_count"][:nf], out["status"][:nf], out=self.recs[d][:nf])
             g = gather_records(self.recs[d], self.world, out=self.gath[d])
         return d, g
 

@@ -33,9 +33,9 @@ class StubPlan:
 
     def run(self, frames, x, omega, indices, out, stream=None):
         gid = x[:frames, 0].to(torch.int32)
-        out["peak_cells"].copy_(gid[:, None] * 10 + torch.arange(self.k, dtype=torch.int32)[None, :])
-        out["peak_count"].fill_(self.k)
-        out["status"].copy_(gid % 3)
+        out["peak_cells"][:frames].copy_(gid[:, None] * 10 + torch.arange(self.k, dtype=torch.int32)[None, :])
+        out["peak_count"][:frames].fill_(self.k)
+        out["status"][:frames].copy_(gid % 3)
 
 
 def _worker(rank, world, port, total, k, mode, depth, q):
@@ -58,6 +58,52 @@ def _worker(rank, world, port, total, k, mode, depth, q):
         q.put((rank, got, seeds, f0, n))
     finally:
         dist.destroy_process_group()
+
+
+def _worker_coalesced(rank, world, port, total, k, co, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1911_07434_b200.shard import FrameStream, shard_range, unshard_coalesced
+        f0, n = shard_range(rank, world, total)
+        nmax = max(shard_range(g, world, total)[1] for g in range(world))
+        fs = FrameStream(lambda i: StubPlan(k), co * n, co * nmax, k, world, 2)
+        got = []
+        for launch, nb in enumerate((co, 1)):  # one full launch of `co` global batches, then a partial one
+            b0 = launch * co
+            x = torch.tensor([[1000 * (b0 + i) + f0 + f] for i in range(co) for f in range(n)], dtype=torch.float64)
+            _, g = fs.step(x, frames=nb * n)
+            got.append([r.numpy().copy() for r in unshard_coalesced(g, world, total, nb)])
+        q.put((rank, got))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total,co", [(5, 2), (8, 3)])
+def test_frame_stream_coalesced_world2(total, co):
+    """Shard coalescing (bench.py --coalesce): each rank runs its shards of `co` consecutive global batches in one
+    launch; the gathered records unshard per batch into global frame order (uneven strong splits included)."""
+    world, k = 2, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_coalesced, args=(r, world, port, total, k, co, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, got in out:
+        batches = [b for launch in got for b in launch]
+        ids = list(range(co)) + [co]
+        assert len(batches) == co + 1
+        for b, recs in zip(ids, batches):
+            gid = np.arange(total) + 1000 * b
+            expect = np.concatenate([gid[:, None] * 10 + np.arange(k)[None, :], np.full((total, 1), k),
+                                     (gid % 3)[:, None]], 1).astype(np.int32)
+            assert np.array_equal(recs, expect), (rank, b)
 
 
 @pytest.mark.parametrize("mode,total,depth", [("strong", 5, 2), ("strong", 8, 1), ("weak", 3, 2)])
