@@ -95,3 +95,33 @@ def test_host_path_from_frame_files(fm, tmp_path):
     assert np.all(host["status"] == 0)
     assert np.array_equal(host["peak_cells"], dev["peak_cells"])
     assert np.array_equal(host["spectrum"], dev["spectrum"])
+
+
+def test_coalesced_frame_stream_matches_per_batch_runs(fm):
+    """bench.py's shard coalescing on real plans: one FrameStream launch over the shards of three consecutive
+    batches (then a partial launch of one) packs the same per-frame records (fm_pack_peak_records) as three
+    separate device runs."""
+    import torch
+
+    from paper_1911_07434_b200.shard import FrameStream, unshard_coalesced
+    n, co = 40, 3
+    x, _, _ = fm.generate_frames(M, N, K, 11, 0, co * n)
+    seeds = np.array([fm.derive(fm.derive(11, f), 4) for f in range(co * n)], np.uint64)
+    ref = _device_run(fm, "fast2", x, seeds, 721)
+    xd = torch.from_numpy(np.ascontiguousarray(x).view(np.float32)).cuda()
+    om = torch.from_numpy(fm.draw_omega_batch(seeds, M, P)).cuda()
+    s = torch.cuda.Stream()
+    fs = FrameStream(lambda i: fm.BatchPlan(M, N, K, "fast2", p=P, t=1, grid_size=721, max_frames=co * n),
+                     co * n, co * n, K, 1, 2, [s, s], torch.device("cuda"))
+    _, g = fs.step(xd, om)
+    torch.cuda.synchronize()
+    recs = [r.cpu().numpy() for r in unshard_coalesced(g, 1, n, co)]
+    for i in range(co):
+        sl = slice(i * n, (i + 1) * n)
+        assert np.array_equal(recs[i][:, :K], ref["peak_cells"][sl])
+        assert np.array_equal(recs[i][:, K], ref["peak_count"][sl])
+        assert np.array_equal(recs[i][:, K + 1], ref["status"][sl])
+    _, g = fs.step(xd, om, frames=n)  # partial launch: the first shard only
+    torch.cuda.synchronize()
+    assert np.array_equal(unshard_coalesced(g, 1, n, 1)[0].cpu().numpy()[:, :K], ref["peak_cells"][:n])
+    fs.close()
