@@ -41,7 +41,26 @@ def run_gpu(fm, oracle, cfg, x, frames, basis=True, covariance=False):
     return res
 
 
+def tie_margins(oracle, p, cells, k):
+    """how close the oracle spectrum is to a tie. Returns (min over the selected peaks of
+    (P_peak - P_neighbour) / P_peak, (h_K - h_{K+1}) / h_K between the last selected and the best rejected
+    local maximum). A mismatch with a margin below ~1e-5 is a tie the fp32 spectrum may legitimately flip."""
+    p = np.asarray(p, dtype=np.float64)
+    nb = 1.0
+    for c in cells:
+        for d in (-1, 1):
+            if 0 <= c + d < p.size and p[c] > 0:
+                nb = min(nb, float((p[c] - p[c + d]) / p[c]))
+    cands = sorted((float(h) for _, h in oracle.local_maxima(p)), reverse=True)
+    rank = 1.0
+    if len(cands) > k and cands[k - 1] > 0:
+        rank = (cands[k - 1] - cands[k]) / cands[k - 1]
+    return nb, rank
+
+
 def compare_frames(oracle, cfg, x, frames, res, grid=None, a_mat=None, db_tol=0.05):
+    """(worst spectrum error in dB, mismatches). Each mismatch is (frame, gpu cells, oracle cells,
+    {"nb_margin", "rank_margin", "near_tie"}): near-ties are reported, never silently dropped."""
     grid = grid or oracle.baseline_grid(cfg.grid_size)
     worst = 0.0
     mismatched = []
@@ -52,7 +71,9 @@ def compare_frames(oracle, cfg, x, frames, res, grid=None, a_mat=None, db_tol=0.
         n = int(res["peak_count"][i])
         cells = [int(c) for c in res["peak_cells"][i][:n]]
         if cells != pk.cells:
-            mismatched.append((f, cells, pk.cells))
+            nb, rank = tie_margins(oracle, p_ref, pk.cells, cfg.spec.k)
+            mismatched.append((f, cells, pk.cells,
+                               {"nb_margin": nb, "rank_margin": rank, "near_tie": min(nb, rank) < 1e-5}))
     return worst, mismatched
 
 
@@ -61,7 +82,12 @@ def _oracle_job(args):
     cfg, xf, f, p_gpu, cells = args
     est, p_ref, pk = O.run_frame(cfg, xf, f)
     db = O.spectrum_db_error(p_gpu, p_ref)
-    return f, db, cells == pk.cells, pk.cells
+    same = cells == pk.cells
+    tie = None
+    if not same:
+        nb, rank = tie_margins(O, p_ref, pk.cells, cfg.spec.k)
+        tie = {"nb_margin": nb, "rank_margin": rank, "near_tie": min(nb, rank) < 1e-5}
+    return f, db, same, pk.cells, tie
 
 
 def compare_frames_parallel(cfg, x, frames, res, procs=None):
@@ -77,9 +103,9 @@ def compare_frames_parallel(cfg, x, frames, res, procs=None):
     procs = procs or min(32, os.cpu_count() or 1)
     worst, mism, dbs = 0.0, [], []
     with cf.ProcessPoolExecutor(procs, mp_context=mp.get_context("fork")) as ex:
-        for (f, db, same, ref_cells), job in zip(ex.map(_oracle_job, jobs, chunksize=4), jobs):
+        for (f, db, same, ref_cells, tie), job in zip(ex.map(_oracle_job, jobs, chunksize=4), jobs):
             worst = max(worst, db)
             dbs.append(db)
             if not same:
-                mism.append((f, job[4], ref_cells))
+                mism.append((f, job[4], ref_cells, tie))
     return worst, mism, dbs
