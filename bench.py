@@ -556,6 +556,20 @@ def run_ours(args):
     step_prof = prof.get("step", {})
     p_tf32 = bf16 / 2.0
     t_roof_ms = max(gfr * alg["q_frame"] / world / (hbm * 1e9), gfr * alg["w_frame"] / world / (p_tf32 * 1e12)) * 1e3
+    # "the builder should measure TF32 ... peaks": cuBLAS TF32 8192^3 on this pool's B200s
+    # (tools/measure_peaks_extra.py -> profiles/measured_peaks_extra.json), reported beside the strict figure
+    extra = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "measured_peaks_extra.json")) as f:
+            extra = json.load(f)
+    except Exception:
+        pass
+
+    def path_frac(p_tf):
+        if not p_tf:
+            return None
+        t = max(gfr * alg["q_frame"] / world / (hbm * 1e9), gfr * alg["w_frame"] / world / (p_tf * 1e12)) * 1e3
+        return t / (ms_max / args.steps)
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -567,6 +581,11 @@ def run_ours(args):
                           "frac": t_roof_ms / (ms_max / args.steps),
                           "def": "SURVEY.md §8d: max(B*Q/HBM, B*W/P_TF32) per GPU, P_TF32 = measured bf16/2, "
                                  "1xTF32 strict",
+                          "frac_measured_tf32": path_frac(extra.get("tf32_tflops")),
+                          "frac_measured_tf32_sustained": path_frac(extra.get("tf32_tflops_sustained")),
+                          "measured_tf32_tflops": [extra.get("tf32_tflops"), extra.get("tf32_tflops_sustained")],
+                          "measured_tf32_source": "profiles/measured_peaks_extra.json (cuBLAS TF32 8192^3, burst / "
+                                                  "sustained)" if extra else None,
                           "dram_bytes_per_frame_ncu": step_prof.get("dram_bytes_per_frame"),
                           "algorithmic_bytes_per_frame": alg["q_frame"],
                           "dram_over_algorithmic": (step_prof["dram_bytes_per_frame"] / alg["q_frame"])
