@@ -342,10 +342,18 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # FM_BENCH_DRYRUN_GLOO=1: rehearse the N > 1 control flow on a box with fewer GPUs than ranks (every rank on a
+    # visible device, gloo instead of NCCL). Its line is marked "dryrun" and is not a measurement.
+    dry = world > 1 and os.environ.get("FM_BENCH_DRYRUN_GLOO") == "1"
+    if dry:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if dry:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     cfgd = CONFIGS[args.config]
     if args.frames:
@@ -605,6 +613,8 @@ def run_ours(args):
         "e2e": e2e,
         "frames_ok": int((status == 0).sum()), "frames_full_peaks": int((counts == K).sum()),
     }
+    if dry:
+        line["dryrun"] = "gloo, ranks share GPUs: control-flow rehearsal, not a measurement"
     if weak is not None:
         line["weak_scaling"] = weak
     if recs is not None:
@@ -676,7 +686,7 @@ def spawn_ranks(args) -> int:
 
     import torch
     have = torch.cuda.device_count()
-    if have < args.gpus:
+    if have < args.gpus and os.environ.get("FM_BENCH_DRYRUN_GLOO") != "1":
         print(json.dumps({"error": f"--gpus {args.gpus} but only {have} CUDA device(s) visible"}), flush=True)
         return 2
     s = socket.socket()

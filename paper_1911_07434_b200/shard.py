@@ -53,6 +53,13 @@ def gather_records(rec, world: int, out=None, group=None):
     if world == 1:
         return rec.unsqueeze(0)
     g = out if out is not None else torch.empty((world,) + tuple(rec.shape), dtype=rec.dtype, device=rec.device)
+    if rec.is_cuda and dist.get_backend(group) == "gloo":
+        # dry runs of the N > 1 flow on a one-GPU box (bench.py FM_BENCH_DRYRUN_GLOO): gloo has no CUDA all-gather,
+        # so the 40 KB of records take a host round trip; never the measured path (NCCL gathers in place)
+        h = torch.empty((world,) + tuple(rec.shape), dtype=rec.dtype)
+        dist.all_gather_into_tensor(h.view(-1, rec.shape[1]), rec.cpu().contiguous(), group=group)
+        g.copy_(h)
+        return g
     dist.all_gather_into_tensor(g.view(-1, rec.shape[1]), rec.contiguous(), group=group)
     return g
 
