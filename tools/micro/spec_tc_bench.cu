@@ -12,7 +12,7 @@
 
 int main(int argc, char** argv) {
     const int frames = argc > 1 ? atoi(argv[1]) : 1024, m = argc > 2 ? atoi(argv[2]) : 256, L = argc > 3 ? atoi(argv[3]) : 3601;
-    const int mk = (m + 31) / 32 * 32, nqp = fm_spectrum_tc_pairs_pad(L), fpad = fm_spectrum_tc_frames_pad(frames);
+    const int mk = (m + 31) / 32 * 32, nqp = fm_spectrum_tc_pairs_pad(L, 0), fpad = fm_spectrum_tc_frames_pad(frames);
     std::vector<double> th(2 * static_cast<size_t>(frames) * m);
     for (size_t i = 0; i < th.size(); ++i) th[i] = std::sin(0.37 * i) * 0.3;
     std::vector<int8_t> zh(static_cast<size_t>(10) * nqp * mk);
@@ -29,10 +29,10 @@ int main(int argc, char** argv) {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    for (int i = 0; i < 5; ++i) fm_launch_spectrum_tc(t, zk, tk, ts, frames, m, L, s32, s64, 0);
+    for (int i = 0; i < 5; ++i) fm_launch_spectrum_tc(t, zk, tk, ts, frames, m, L, s32, s64, 0, 0);
     cudaEventRecord(a);
     const int reps = 50;
-    for (int i = 0; i < reps; ++i) fm_launch_spectrum_tc(t, zk, tk, ts, frames, m, L, s32, s64, 0);
+    for (int i = 0; i < reps; ++i) fm_launch_spectrum_tc(t, zk, tk, ts, frames, m, L, s32, s64, 0, 0);
     cudaEventRecord(b);
     cudaError_t e = cudaEventSynchronize(b);
     float ms = 0;
