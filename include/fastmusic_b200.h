@@ -229,6 +229,11 @@ fm_status fm_write_spectrum_csv(const char* path, int64_t grid_size, double thet
 fm_status fm_z_spatial_covariance(int64_t m, int64_t n, const double* y, double* s_out);
 /* temporal_covariance, R/src/scene.cpp:140-153,161-163: T = Y^H Y / M (N x N), fp64 on the GPU */
 fm_status fm_z_temporal_covariance(int64_t m, int64_t n, const double* y, double* t_out);
+/* hermitian_eig, R/src/linalg.cpp:77-89: full spectral decomposition of the Hermitian S (column-major complex128,
+ * symmetrised like HermitianMatrix), eigenvalues[m] descending (signed), eigenvectors m x m column-major complex128,
+ * column i pairing with eigenvalue i. One-sided Jacobi on the GPU (the exact estimator's solver with K = M);
+ * FM_ENOCONV at the sweep cap. */
+fm_status fm_z_hermitian_eig(int64_t m, const double* s, double* eigenvalues, double* eigenvectors);
 /* exact_signal_subspace, R/src/estimators.cpp:73-85 */
 fm_status fm_z_exact_signal_subspace(int64_t m, const double* s, int64_t k, double* basis, double* eigenvalues,
                                      double* cost_seconds);

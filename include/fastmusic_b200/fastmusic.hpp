@@ -107,6 +107,11 @@ public:
 
 enum class Method { Exact, Fast1, Fast2, Lanczos, MatrixInverse, Propagator, Fft };
 const char* method_name(Method m);
+Method method_from_name(const std::string& name);  // std::invalid_argument("unknown method name: ...")
+
+// R/include/fastmusic/types.hpp:59-62, R/src/linalg.cpp:36-44
+bool is_finite(const CxMat& a);
+void ensure_finite(const CxMat& a, const char* what);  // std::invalid_argument("<what>: non-finite entries")
 
 // Square complex matrix kept Hermitian by symmetrising on construction (R/src/linalg.cpp:46-52).
 class HermitianMatrix {
@@ -118,6 +123,20 @@ public:
 private:
     CxMat m_;
 };
+
+// R/include/fastmusic/types.hpp:78-90. Eigenvalues descending, column i of `eigenvectors` pairs with eigenvalue i;
+// thin SVD with singular values descending.
+struct EigResult {
+    RealVec eigenvalues;
+    CxMat eigenvectors;
+};
+struct SvdResult {
+    CxMat u;
+    RealVec sigma;
+    CxMat v;
+};
+// R/include/fastmusic/linalg.hpp:13 (R/src/linalg.cpp:77-89): one-sided Jacobi on the GPU, fp64.
+EigResult hermitian_eig(const HermitianMatrix& s);
 
 struct SubspaceEstimate {
     CxMat basis;

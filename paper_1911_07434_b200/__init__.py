@@ -4,8 +4,9 @@ The compute lives in ``libfastmusic_b200.so`` (hand-written CUDA kernels behind 
 C ABI in ``include/fastmusic_b200.h``); this package is the Python mirror of the
 reference estimator API over that ABI. Importing fails loudly if the library is absent.
 """
-from .api import (AngleGrid, BatchPlan, CudaError, Fast1Params, Fast2Params, NonConvergenceError, PeakSet,  # noqa: F401
-                  PseudoSpectrum, RankDeficiencyError, SingularMatrixError, SubspaceEstimate, baseline_grid,
+from .api import (AngleGrid, BatchPlan, CudaError, EigResult, Fast1Params, Fast2Params, NonConvergenceError, PeakSet,  # noqa: F401
+                  PseudoSpectrum, RankDeficiencyError, SingularMatrixError, SubspaceEstimate, SvdResult, baseline_grid,
+                  ensure_finite, hermitian_eig, is_finite, method_from_name, method_name,
                   block_lanczos_batch, block_lanczos_subspace, derive,
                   draw_indices_batch, draw_omega_batch, draw_uniforms_batch, exact_signal_subspace, extract_peaks, fast_music_1,
                   fast_music_2, gaussian_matrix_real, generate_frames, hermitian, music_spectrum, normals,

@@ -24,7 +24,7 @@ EXPORTED = [
     "fm_draw_omega_batch", "fm_draw_indices_batch", "fm_draw_uniforms_batch", "fm_generate_frames",
     "fm_plan_create", "fm_plan_destroy", "fm_plan_workspace_bytes", "fm_run_batch", "fm_rerun_frames",
     "fm_plan_launches_per_batch", "fm_plan_set_profiling", "fm_plan_stage_times", "fm_plan_set_concurrency", "fm_plan_set_graphs", "fm_estimate_batch_host",
-    "fm_z_spatial_covariance", "fm_z_exact_signal_subspace", "fm_z_fast_music_1", "fm_z_fast_music_2",
+    "fm_z_spatial_covariance", "fm_z_hermitian_eig", "fm_z_exact_signal_subspace", "fm_z_fast_music_1", "fm_z_fast_music_2",
     "fm_z_music_spectrum", "fm_z_extract_peaks",
     "fm_z_temporal_covariance", "fm_temporal_covariance_batch", "fm_z_block_lanczos_subspace",
     "fm_block_lanczos_batch",
@@ -94,6 +94,7 @@ def _load():
         "fm_estimate_batch_host": (i32, [vp, i64, vp, vp, vp, vp]),
         "fm_pack_peak_records": (i32, [vp, vp, vp, i64, i64, vp, vp]),
         "fm_z_spatial_covariance": (i32, [i64, i64, vp, vp]),
+        "fm_z_hermitian_eig": (i32, [i64, vp, vp, vp]),
         "fm_z_exact_signal_subspace": (i32, [i64, vp, i64, vp, vp, vp]),
         "fm_z_fast_music_1": (i32, [i64, vp, i64, i64, u64, vp, vp, vp]),
         "fm_z_fast_music_2": (i32, [i64, vp, i64, i64, i32, u64, vp, vp, vp, vp]),

@@ -76,6 +76,49 @@ class Fast2Params:
     seed: int = 0
 
 
+METHOD_NAMES = ("exact", "fast1", "fast2", "lanczos", "matrix_inverse", "propagator", "fft")
+
+
+def method_name(method) -> str:
+    """R/src/linalg.cpp:14-26 — the reference's names, by enum value or name."""
+    if isinstance(method, str):
+        return method if method in METHOD_NAMES else "unknown"
+    return METHOD_NAMES[method] if 0 <= int(method) < len(METHOD_NAMES) else "unknown"
+
+
+def method_from_name(name: str) -> int:
+    """R/src/linalg.cpp:28-34 — Method enum value (types.hpp:45-53); ValueError('unknown method name: ...')."""
+    if name not in METHOD_NAMES:
+        raise ValueError("unknown method name: " + str(name))
+    return METHOD_NAMES.index(name)
+
+
+def is_finite(a) -> bool:
+    """R/src/linalg.cpp:36-38."""
+    return bool(np.all(np.isfinite(np.asarray(a))))
+
+
+def ensure_finite(a, what: str) -> None:
+    """R/src/linalg.cpp:40-44 — ValueError('<what>: non-finite entries')."""
+    if not is_finite(a):
+        raise ValueError(f"{what}: non-finite entries")
+
+
+@dataclass
+class EigResult:
+    """R/include/fastmusic/types.hpp:78-83 — eigenvalues descending, column i pairs with eigenvalue i."""
+    eigenvalues: np.ndarray
+    eigenvectors: np.ndarray
+
+
+@dataclass
+class SvdResult:
+    """R/include/fastmusic/types.hpp:85-90 — thin SVD, singular values descending."""
+    u: np.ndarray
+    sigma: np.ndarray
+    v: np.ndarray
+
+
 @dataclass
 class SubspaceEstimate:
     """R/include/fastmusic/estimators.hpp:13-18."""
@@ -279,6 +322,16 @@ def block_lanczos_batch(s, k: int, block: int, max_iterations: int, stream=None)
 
 def _est_out(m, k):
     return np.empty((m, k), np.complex128, order="F"), np.empty(k, np.float64), C.c_double(0.0)
+
+
+def hermitian_eig(s) -> EigResult:
+    """R/src/linalg.cpp:77-89 — full decomposition of a Hermitian matrix by one-sided Jacobi on the GPU (fp64)."""
+    s = hermitian(s)
+    m = s.shape[0]
+    v = np.empty((m, m), np.complex128, order="F")
+    e = np.empty(m, np.float64)
+    _check(LIB.fm_z_hermitian_eig(m, ptr(s), ptr(e), ptr(v)))
+    return EigResult(e, v)
 
 
 def exact_signal_subspace(s, k: int) -> SubspaceEstimate:

@@ -1691,12 +1691,10 @@ extern "C" fm_status fm_z_fast_music_1(int64_t m, const double* s, int64_t k, in
     return z_nystrom_common(m, s, k, p, 1, seed, false, basis, eigenvalues, cost_seconds, nullptr);
 }
 
-extern "C" fm_status fm_z_exact_signal_subspace(int64_t m, const double* s, int64_t k, double* basis,
-                                                double* eigenvalues, double* cost_seconds) {
-    fm_status st = check_hermitian_input(s, m, "exact_signal_subspace");
-    if (st != FM_OK) return st;
-    if (k < 1 || k >= m) return fail(FM_EINVAL, "exact_signal_subspace: need 1 <= K < M");
-    if (!basis || !eigenvalues) return fail(FM_EINVAL, "exact_signal_subspace: null output");
+// The K leading (signed-descending) eigenpairs of the Hermitian S by the Jacobi eigensolver; K = M gives the full
+// decomposition (hermitian_eig).
+static fm_status z_leading_eigenpairs(int64_t m, const double* s, int64_t k, double* basis, double* eigenvalues,
+                                      double* cost_seconds) {
     const int64_t mp = (m + 15) / 16 * 16;
     ZCtx c;
     const auto rrow = to_rowmajor_hermitian(s, m);
@@ -1723,6 +1721,28 @@ extern "C" fm_status fm_z_exact_signal_subspace(int64_t m, const double* s, int6
     if (cost_seconds) *cost_seconds = ms * 1e-3;
     if (st_host & FM_FRAME_NOCONV) return fail(FM_ENOCONV, "hermitian_eig: eigensolver did not converge");
     return FM_OK;
+}
+
+extern "C" fm_status fm_z_exact_signal_subspace(int64_t m, const double* s, int64_t k, double* basis,
+                                                double* eigenvalues, double* cost_seconds) {
+    fm_status st = check_hermitian_input(s, m, "exact_signal_subspace");
+    if (st != FM_OK) return st;
+    if (k < 1 || k >= m) return fail(FM_EINVAL, "exact_signal_subspace: need 1 <= K < M");
+    if (!basis || !eigenvalues) return fail(FM_EINVAL, "exact_signal_subspace: null output");
+    return z_leading_eigenpairs(m, s, k, basis, eigenvalues, cost_seconds);
+}
+
+extern "C" fm_status fm_z_hermitian_eig(int64_t m, const double* s, double* eigenvalues, double* eigenvectors) {
+    fm_status st = check_hermitian_input(s, m, "hermitian_eig");
+    if (st != FM_OK) return st;
+    if (!eigenvalues || !eigenvectors) return fail(FM_EINVAL, "hermitian_eig: null output");
+    if (m == 1) {  // nothing to rotate: the entry itself
+        eigenvalues[0] = s[0];
+        eigenvectors[0] = 1.0;
+        eigenvectors[1] = 0.0;
+        return FM_OK;
+    }
+    return z_leading_eigenpairs(m, s, m, eigenvectors, eigenvalues, nullptr);
 }
 
 extern "C" fm_status fm_z_music_spectrum(int64_t m, int64_t kb, const double* basis, int64_t L, double theta0,

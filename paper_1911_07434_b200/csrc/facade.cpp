@@ -69,6 +69,19 @@ const char* method_name(Method m) {
     return "unknown";
 }
 
+Method method_from_name(const std::string& name) {
+    for (Method m : {Method::Exact, Method::Fast1, Method::Fast2, Method::Lanczos, Method::MatrixInverse,
+                     Method::Propagator, Method::Fft})
+        if (name == method_name(m)) return m;
+    throw std::invalid_argument("unknown method name: " + name);
+}
+
+bool is_finite(const CxMat& a) { return finite(a); }
+
+void ensure_finite(const CxMat& a, const char* what) {
+    if (!finite(a)) throw std::invalid_argument(std::string(what) + ": non-finite entries");
+}
+
 HermitianMatrix::HermitianMatrix(const CxMat& a) {
     if (a.rows() != a.cols() || a.rows() < 1)
         throw std::invalid_argument("HermitianMatrix: input must be square and non-empty");
@@ -116,6 +129,14 @@ static SubspaceEstimate make_estimate(Index m, Index k, Method method) {
     out.basis = CxMat(m, k);
     out.eigenvalues = RealVec(k, 1);
     out.method = method;
+    return out;
+}
+
+EigResult hermitian_eig(const HermitianMatrix& s) {
+    EigResult out;
+    out.eigenvalues = RealVec(s.dim(), 1);
+    out.eigenvectors = CxMat(s.dim(), s.dim());
+    check(fm_z_hermitian_eig(s.dim(), raw(s.mat()), out.eigenvalues.data(), raw(out.eigenvectors)));
     return out;
 }
 

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
+#include <limits>
 #include <string>
 
 #include "fastmusic_b200/fastmusic.hpp"
@@ -90,6 +91,27 @@ int main(int argc, char** argv) {
         std::printf(" eig %.9g %.9g\n", e->eigenvalues(0), e->eigenvalues(1));
     }
     std::printf("true_cells %ld %ld\n", static_cast<long>(grid.nearest(th[0])), static_cast<long>(grid.nearest(th[1])));
+    // types.hpp:56-62 / linalg.hpp:13: the full decomposition pairs with the exact estimator's leading part
+    const EigResult full = hermitian_eig(s);
+    std::printf("heig %.9g %.9g n %ld name %s\n", full.eigenvalues(0), full.eigenvalues(1),
+                static_cast<long>(full.eigenvectors.cols()), method_name(method_from_name("fast2")));
+    try {
+        method_from_name("nope");
+        std::printf("bad_name no-throw\n");
+    } catch (const std::invalid_argument& e) {
+        std::printf("bad_name %s\n", std::string(e.what()) == "unknown method name: nope" ? "invalid_argument" : e.what());
+    }
+    {
+        CxMat bad(2, 2);
+        bad(1, 0) = Complex(std::numeric_limits<double>::infinity(), 0.0);
+        try {
+            ensure_finite(bad, "thin_svd");
+            std::printf("nonfinite no-throw\n");
+        } catch (const std::invalid_argument& e) {
+            std::printf("nonfinite %s\n", std::string(e.what()) == "thin_svd: non-finite entries" && !is_finite(bad)
+                                               ? "invalid_argument" : e.what());
+        }
+    }
     try {
         fast_music_2(s, m, Fast2Params{m, 1, 1});
         std::printf("invalid_k no-throw\n");

@@ -96,3 +96,24 @@ def test_library_has_no_unresolved_internal_symbols():
     out = subprocess.run(["nm", "-D", "--undefined-only", _capi.LIB_PATH], capture_output=True, text=True).stdout
     bad = [ln for ln in out.splitlines() if "fm_" in ln or "fmk" in ln]
     assert not bad, bad
+
+
+def test_api_type_helpers(fm):
+    """R/include/fastmusic/types.hpp:45-62 (R/src/linalg.cpp:14-44): method names round-trip through the enum
+    order, unknown names and non-finite matrices raise with the reference's messages."""
+    names = ["exact", "fast1", "fast2", "lanczos", "matrix_inverse", "propagator", "fft"]
+    for i, n in enumerate(names):
+        assert fm.method_from_name(n) == i and fm.method_name(i) == n
+    assert fm.method_name(99) == "unknown"
+    with pytest.raises(ValueError, match="unknown method name: nope"):
+        fm.method_from_name("nope")
+    good = np.ones((2, 2), complex)
+    bad = good.copy()
+    bad[1, 0] = np.inf
+    assert fm.is_finite(good) and not fm.is_finite(bad)
+    fm.ensure_finite(good, "thin_svd")
+    with pytest.raises(ValueError, match="thin_svd: non-finite entries"):
+        fm.ensure_finite(bad, "thin_svd")
+    e = fm.EigResult(np.zeros(2), np.eye(2, dtype=complex))
+    s = fm.SvdResult(np.eye(2, dtype=complex), np.ones(2), np.eye(2, dtype=complex))
+    assert e.eigenvectors.shape == (2, 2) and s.sigma.shape == (2,)

@@ -71,3 +71,9 @@ def test_facade_driver_runs(tmp_path):
             assert abs(a - b) <= tol * abs(b), (meth, eig)
     assert lines["invalid_k"] == ["invalid_argument"]
     assert lines["invalid_t"] == ["invalid_argument"]
+    heig = lines["heig"]
+    for a, b in zip((float(heig[0]), float(heig[1])), eig["exact"]):
+        assert abs(a - b) <= 1e-9 * abs(b), (heig, eig)
+    assert heig[2:] == ["n", "16", "name", "fast2"], heig
+    assert lines["bad_name"] == ["invalid_argument"]
+    assert lines["nonfinite"] == ["invalid_argument"]

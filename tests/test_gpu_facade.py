@@ -53,6 +53,37 @@ def test_exact_diagonal_and_validation(fm):
         fm.exact_signal_subspace(d, 3)
 
 
+@pytest.mark.parametrize("m", [1, 2, 7, 64, 65, 130, 300])
+def test_hermitian_eig_full_decomposition(fm, m):
+    """R/src/linalg.cpp:77-89: eigenvalues descending (signed), column i pairs with eigenvalue i, orthonormal
+    eigenvectors; against numpy's eigh on an indefinite Hermitian matrix (shared-memory Jacobi for M <= 64, the
+    global-memory Jacobi beyond)."""
+    rng = np.random.default_rng(100 + m)
+    a = rng.standard_normal((m, m)) + 1j * rng.standard_normal((m, m))
+    s = 0.5 * (a + a.conj().T)
+    r = fm.hermitian_eig(s)
+    w = np.linalg.eigvalsh(s)[::-1]
+    scale = max(1.0, np.abs(w).max())
+    assert r.eigenvalues.shape == (m,) and r.eigenvectors.shape == (m, m)
+    assert np.all(np.diff(r.eigenvalues) <= 1e-12 * scale)
+    assert np.abs(r.eigenvalues - w).max() < 1e-10 * scale
+    v = r.eigenvectors
+    assert np.abs(v.conj().T @ v - np.eye(m)).max() < 1e-10
+    assert np.abs(s @ v - v * r.eigenvalues[None, :]).max() < 1e-9 * scale
+
+
+def test_hermitian_eig_matches_exact_signal_subspace(fm):
+    s = psd_with_spectrum(fm, gapped_spectrum(12, 4, 0.4), 5)
+    full = fm.hermitian_eig(s)
+    est = fm.exact_signal_subspace(s, 4)
+    assert np.allclose(full.eigenvalues[:4], est.eigenvalues, rtol=1e-12)
+    assert proj_err(full.eigenvectors[:, :4], est.basis) < 1e-10
+    with pytest.raises(ValueError):
+        fm.hermitian_eig(np.full((3, 3), np.nan, complex))
+    with pytest.raises(ValueError):
+        fm.hermitian_eig(np.zeros((2, 3), complex))
+
+
 def test_exact_projector_vs_full_decomposition(fm):
     s = psd_with_spectrum(fm, gapped_spectrum(10, 3, 0.4), 3)
     est = fm.exact_signal_subspace(s, 3)
